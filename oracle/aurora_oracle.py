@@ -1,0 +1,271 @@
+"""CPU oracle for the Aurora speculator-training hot path — TEST INFRASTRUCTURE ONLY.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline /
+`--impl reference` legs may import this module.  The product path (the CUDA
+library `libaurora.so` and its Python binding) never imports, links or calls
+anything under `oracle/`, and this module imports nothing from the product.
+
+It is the plain, slow, float64 definition of what the path computes, written
+step by step in the paper's order (PAPER.md = P, SPEC.md = S, line numbers):
+
+  O1 target_scan   y = argmax of the verifier logits (lowest index wins ties),
+                   and the top-K list ordered by (value desc, index asc).
+                   P:120 §2.1 "accepting the longest matching prefix" (greedy,
+                   P:526 Table 3 "Top-k Sampling 1"); ties S:84.
+  O2 verify        acc(n) = acc(parent(n)) AND [x_n == y at the parent's row];
+                   accept_len = (#accepted) + 1 (bonus counts);
+                   bonus = y at the deepest accepted row.  P:120.
+  O3 row_targets   ACCEPT rows (root + accepted nodes) use the target's top-k_acc
+                   support, DISCARD rows (context contains a rejected token)
+                   the top-k_disc support (k=10); p~ = target
+                   softmax renormalised on the support; weight 1/N_A or
+                   lambda/N_D (lambda=1.0; per-term means).
+  O4 loss_fwd      L = sum_m w_m KL(p~_m || softmax(z_m)),  z_m = W h_m
+                   (Eq. 3; full-vocab log-softmax per north_star).
+  O5 loss_bwd      dL/dz = w (q - p~) (gradient of KL(p~||q) wrt logits);
+                   dW = dZ^T H, dH = dZ W (fp32 gradients; here fp64).
+
+Readings where the paper is silent/ambiguous are listed in DESIGN.md
+("Readings Q1-Q15"); each function names the ones it relies on.
+
+Pins (tests/test_oracle_pins.py, `-m "not gpu"`): brute-force top-k on tiny
+vocabularies and hand-written tie rows (tests/golden), SPEC worked examples
+S:182-184 / S:325 / S:345, exhaustive chain and tree verification
+enumeration, Eq. 1 Monte Carlo, torch f64 cross_entropy / kl_div /
+autograd, central finite differences, row-sum-zero and shift invariance.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+ACCEPT, DISCARD, PAD = 0, 1, 2
+
+
+def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:
+    """Exact upcast of bf16 bit patterns: bf16 -> f32 by a 16-bit shift -> f64."""
+    b = np.asarray(bits, dtype=np.uint16)
+    return (b.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+# --------------------------------------------------------------------------- O1
+def target_scan(T_rows: np.ndarray, k_max: int):
+    """O1 (reading Q8).
+
+    T_rows: f64 [m, V].  Returns (argmax int64 [m], topk int64 [m, k_max],
+    nonfinite bool).  Order is (value desc, index asc) with numeric compare, so
+    -0 == +0; a stable argsort of -t gives exactly that order.
+    """
+    T_rows = np.asarray(T_rows, dtype=np.float64)
+    nonfinite = not bool(np.all(np.isfinite(T_rows)))
+    order = np.argsort(-T_rows, axis=1, kind="stable")
+    topk = order[:, :k_max]
+    return topk[:, 0].copy(), topk.copy(), nonfinite
+
+
+# --------------------------------------------------------------------------- O2
+def verify(draft_tokens: np.ndarray, parents, num_nodes, argmax: np.ndarray,
+           discard_scope: int = 0):
+    """O2 greedy verification over chains or trees.
+
+    Row of node n in request r is r*(N+1) + n + 1; the root row is r*(N+1).
+    Node n is *matched* iff draft_tokens[r,n] == argmax[row(parent(n))]; it is
+    *accepted* iff matched and its parent is accepted (root always is).  If two
+    siblings both match, the lowest node index wins (reading Q12; "the
+    accepted path is a path, never a branch").
+    accept_len = #accepted + 1 ("accepted_path length + 1").
+    bonus = argmax at the row of the deepest accepted node (root row if none).
+    Row classes (readings Q1-Q3): root and accepted-node rows ACCEPT; other
+    valid node rows DISCARD ("all rejected nodes"); with discard_scope=1
+    only first-divergence rows (rejected node whose parent is accepted) stay
+    DISCARD and deeper ones become PAD; nodes >= num_nodes[r] are PAD.
+    """
+    draft_tokens = np.asarray(draft_tokens)
+    R, N = draft_tokens.shape
+    accepted = np.zeros((R, N), dtype=np.uint8)
+    accept_len = np.zeros(R, dtype=np.int32)
+    bonus = np.zeros(R, dtype=np.int32)
+    row_class = np.full(R * (N + 1), PAD, dtype=np.uint8)
+    for r in range(R):
+        nn = N if num_nodes is None else int(num_nodes[r])
+        base = r * (N + 1)
+        acc = [False] * N
+        depth = [0] * N
+        won_parent = set()            # parents that already have an accepted child
+        for n in range(nn):
+            p = (n - 1) if parents is None else int(parents[r, n])
+            if not (-1 <= p < n):
+                raise ValueError("malformed parents: parent must satisfy -1 <= p < n")
+            parent_acc = True if p < 0 else acc[p]
+            depth[n] = 1 if p < 0 else depth[p] + 1
+            match = int(draft_tokens[r, n]) == int(argmax[base + p + 1])
+            if parent_acc and match and p not in won_parent:
+                acc[n] = True
+                won_parent.add(p)
+        row_class[base] = ACCEPT
+        deepest_row, deepest_depth, a = 0, 0, 0
+        for n in range(nn):
+            p = (n - 1) if parents is None else int(parents[r, n])
+            if acc[n]:
+                accepted[r, n] = 1
+                row_class[base + n + 1] = ACCEPT
+                a += 1
+                if depth[n] > deepest_depth:
+                    deepest_row, deepest_depth = n + 1, depth[n]
+            else:
+                first_div = (p < 0) or acc[p]
+                if discard_scope == 0 or first_div:
+                    row_class[base + n + 1] = DISCARD
+        accept_len[r] = a + 1
+        bonus[r] = int(argmax[base + deepest_row])
+    return dict(accepted=accepted, accept_len=accept_len, bonus=bonus, row_class=row_class)
+
+
+# --------------------------------------------------------------------------- O3
+def row_targets(row_class: np.ndarray, T_rows_by_m, topk: np.ndarray, k_accept: int = 1,
+                k_discard: int = 10, lambda_discard: float = 1.0, normalize: int = 0,
+                rows=None):
+    """O3 row supports, renormalised target distributions and weights.
+
+    P:185 (accepted term: CE on the verified token = support {y} when
+    k_accept=1, reading Q5), P:191-195 (discard term, top-k filtered target,
+    k=10 P:520, lambda=1.0 P:521), reading Q6 (support = target top-k by
+    (logit desc, index asc), target renormalised on it), reading Q7 (per-term
+    means over the global counts N_A, N_D; normalize=1: mean over all rows).
+
+    T_rows_by_m(m) -> f64 [V] gives the verifier logits of row m; topk[m] is O1's
+    ordered list.  Returns dict with per-row lists sup_idx (index-sorted),
+    sup_p (aligned), H (sum p log p), w, and counts (N_A, N_D).
+    """
+    M = row_class.shape[0]
+    n_acc = int(np.sum(row_class == ACCEPT))
+    n_dis = int(np.sum(row_class == DISCARD))
+    rows = range(M) if rows is None else rows
+    sup_idx, sup_p, Hs, ws = {}, {}, {}, {}
+    for m in rows:
+        c = int(row_class[m])
+        if c == PAD:
+            sup_idx[m] = np.zeros(0, dtype=np.int64)
+            sup_p[m] = np.zeros(0)
+            Hs[m] = 0.0
+            ws[m] = 0.0
+            continue
+        k = k_accept if c == ACCEPT else k_discard
+        S = np.asarray(topk[m][:k], dtype=np.int64)
+        t = np.asarray(T_rows_by_m(m), dtype=np.float64)[S]
+        e = np.exp(t - t.max())
+        p = e / e.sum()
+        order = np.argsort(S, kind="stable")
+        sup_idx[m] = S[order]
+        sup_p[m] = p[order]
+        Hs[m] = float(np.sum(p * np.log(p)))
+        if normalize == 0:
+            ws[m] = (1.0 / n_acc) if c == ACCEPT else (lambda_discard / n_dis if n_dis else 0.0)
+        else:
+            ws[m] = (1.0 if c == ACCEPT else lambda_discard) / (n_acc + n_dis)
+    return dict(sup_idx=sup_idx, sup_p=sup_p, H=Hs, w=ws, counts=(n_acc, n_dis))
+
+
+# --------------------------------------------------------------------------- O4
+def logits(H64: np.ndarray, W_bits_or_64, v0: int, v1: int) -> np.ndarray:
+    W = W_bits_or_64[v0:v1]
+    if W.dtype == np.uint16:
+        W = bf16_bits_to_f64(W)
+    return H64 @ W.T
+
+
+def loss_fwd(H64: np.ndarray, W, targets: dict, rows=None, chunk: int = 8192):
+    """O4: per-row lse (exact f64 log-sum-exp over the full vocabulary),
+    u_m = sum_{j in S_m} p~_j z_mj computed from direct dot products
+    H_m . W_j, row loss l_m = lse_m - u_m + H~_m = KL(p~_m || q_m), and
+    L = sum_m w_m l_m (Eq. 3)."""
+    M = H64.shape[0]
+    rows = np.arange(M) if rows is None else np.asarray(rows)
+    Hr = H64[rows]
+    V = W.shape[0]
+    mx = np.full(len(rows), -np.inf)
+    s = np.zeros(len(rows))
+    for v0 in range(0, V, chunk):
+        z = logits(Hr, W, v0, min(V, v0 + chunk))
+        cm = z.max(axis=1)
+        nm = np.maximum(mx, cm)
+        s = s * np.exp(mx - nm) + np.exp(z - nm[:, None]).sum(axis=1)
+        mx = nm
+    lse = mx + np.log(s)
+    row_loss = np.zeros(len(rows))
+    for i, m in enumerate(rows):
+        S = targets["sup_idx"][int(m)]
+        if len(S) == 0:
+            continue
+        Ws = W[S]
+        if Ws.dtype == np.uint16:
+            Ws = bf16_bits_to_f64(Ws)
+        zS = Ws @ H64[m]
+        u = float(np.dot(targets["sup_p"][int(m)], zS))
+        row_loss[i] = lse[i] - u + targets["H"][int(m)]
+    w = np.array([targets["w"][int(m)] for m in rows])
+    return dict(rows=rows, lse=lse, row_loss=row_loss, loss=float(np.dot(w, row_loss)))
+
+
+# --------------------------------------------------------------------------- O5
+def loss_bwd(H64: np.ndarray, W, targets: dict, lse: np.ndarray, g: float = 1.0,
+             chunk: int = 8192, want_dW: bool = True):
+    """O5: dZ = g w (softmax(z) - p~) on the support (S:321 FKL grad q - p),
+    dW = dZ^T H, dH = dZ W.  Chunked over the vocabulary only to bound RAM
+    (no recompute trick, no reordering of the sums beyond the chunking)."""
+    M, d = H64.shape
+    V = W.shape[0]
+    w = np.array([targets["w"][m] for m in range(M)])
+    dH = np.zeros((M, d))
+    dW = np.zeros((V, d)) if want_dW else None
+    for v0 in range(0, V, chunk):
+        v1 = min(V, v0 + chunk)
+        Wc = W[v0:v1]
+        if Wc.dtype == np.uint16:
+            Wc = bf16_bits_to_f64(Wc)
+        z = H64 @ Wc.T
+        dZ = np.exp(z - lse[:, None]) * (g * w)[:, None]
+        for m in range(M):
+            S = targets["sup_idx"][m]
+            if len(S) == 0:
+                continue
+            sel = (S >= v0) & (S < v1)
+            dZ[m, S[sel] - v0] -= g * w[m] * targets["sup_p"][m][sel]
+        dH += dZ @ Wc
+        if want_dW:
+            dW[v0:v1] = dZ.T @ H64
+    return dict(dH=dH, dW=dW)
+
+
+def dlogits_rows(H64, W, targets, lse_rows, rows, g: float = 1.0):
+    """Full dZ rows for a handful of rows (test hook counterpart)."""
+    Wf = bf16_bits_to_f64(W) if W.dtype == np.uint16 else W
+    out = []
+    for i, m in enumerate(rows):
+        z = Wf @ H64[m]
+        dz = np.exp(z - lse_rows[i]) * g * targets["w"][m]
+        S = targets["sup_idx"][m]
+        dz[S] -= g * targets["w"][m] * targets["sup_p"][m]
+        out.append(dz)
+    return np.array(out)
+
+
+# ------------------------------------------------------------------ whole step
+def step(trace: dict, k_accept: int = 1, k_discard: int = 10, lambda_discard: float = 1.0,
+         normalize: int = 0, discard_scope: int = 0, g: float = 1.0, want_grads: bool = True,
+         want_dW: bool = True):
+    """verify -> targets -> fwd -> bwd for one trace batch (everything f64)."""
+    T = bf16_bits_to_f64(trace["T_bits"])
+    H64 = bf16_bits_to_f64(trace["H_bits"])
+    Wb = trace["W_bits"]
+    k_max = max(k_accept, k_discard)
+    amax, topk, nonfinite = target_scan(T, k_max)
+    if nonfinite:
+        raise ValueError("non-finite target logits")
+    lab = verify(trace["draft_tokens"], trace["parents"], trace["num_nodes"], amax, discard_scope)
+    tg = row_targets(lab["row_class"], lambda m: T[m], topk, k_accept, k_discard, lambda_discard, normalize)
+    fw = loss_fwd(H64, Wb, tg)
+    out = dict(argmax=amax, topk=topk, **lab, targets=tg, lse=fw["lse"], row_loss=fw["row_loss"],
+               loss=fw["loss"])
+    if want_grads:
+        out.update(loss_bwd(H64, Wb, tg, fw["lse"], g=g, want_dW=want_dW))
+    return out

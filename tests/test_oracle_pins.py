@@ -1,0 +1,454 @@
+"""Pins for the CPU oracle against things other than itself (-m "not gpu").
+
+Each test names what pins it: a value printed in SPEC.md/PAPER.md (golden
+fixtures), a closed form, a library routine (torch f64 on CPU), brute force on
+tiny inputs, finite differences, or an invariant of the mathematics.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import oracle
+from oracle import ACCEPT, DISCARD, PAD
+import tracegen
+
+torch.set_default_dtype(torch.float64)
+
+
+def _parse(v):
+    return -0.0 if v == "-0.0" else float(v)
+
+
+# ----------------------------------------------------------------------- O1 scan
+def _bruteforce_topk(row, k):
+    """Pure-Python selection: repeatedly take the largest remaining value,
+    lowest index on equality (numeric compare: -0 == +0)."""
+    remaining = list(range(len(row)))
+    out = []
+    for _ in range(k):
+        best = remaining[0]
+        for j in remaining[1:]:
+            if row[j] > row[best]:
+                best = j
+        out.append(best)
+        remaining.remove(best)
+    return out
+
+
+def test_bf16_upcast_exact():
+    bits = np.array([0x3F80, 0xC000, 0x8000, 0x0000, 0x7F80, 0x3E80, 0x0001], dtype=np.uint16)
+    v = oracle.bf16_bits_to_f64(bits)
+    assert v[0] == 1.0 and v[1] == -2.0 and v[3] == 0.0 and v[5] == 0.25
+    assert math.copysign(1.0, v[2]) == -1.0 and v[2] == 0.0
+    assert math.isinf(v[4])
+    assert v[6] == 2.0 ** -133          # smallest bf16 subnormal, exact
+    # cross-check against torch's own bf16 -> f64 conversion (library routine)
+    t = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).to(torch.float64).numpy()
+    np.testing.assert_array_equal(t, v)
+
+
+def test_tracegen_bf16_rounding_matches_torch():
+    rng = np.random.default_rng(0)
+    x = (rng.standard_normal(100000) * 10).astype(np.float32)
+    ours = tracegen.f32_to_bf16_bits(x)
+    ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    np.testing.assert_array_equal(ours, ref)
+
+
+def test_scan_golden_ties(golden_dir):
+    cases = json.load(open(os.path.join(golden_dir, "tie_rows.json")))["cases"]
+    for c in cases:
+        row = np.array([_parse(v) for v in c["row"]])
+        am, topk, nf = oracle.target_scan(row[None, :], c["k"])
+        assert not nf
+        assert int(am[0]) == c["argmax"], c
+        assert topk[0].tolist() == c["topk"], c
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_scan_bruteforce_small_vocab(seed):
+    rng = np.random.default_rng(seed)
+    V = int(rng.integers(1, 17))
+    k = int(rng.integers(1, V + 1))
+    # few distinct values -> many ties; include signed zeros
+    vals = np.array([-1.0, -0.0, 0.0, 0.5, 2.0])
+    T = vals[rng.integers(0, len(vals), size=(6, V))]
+    am, topk, nf = oracle.target_scan(T, k)
+    for i in range(T.shape[0]):
+        ref = _bruteforce_topk(T[i].tolist(), k)
+        assert topk[i].tolist() == ref
+        assert int(am[i]) == int(np.argmax(T[i]))          # numpy: first occurrence of the max
+
+
+def test_scan_nonfinite_flag():
+    _, _, nf = oracle.target_scan(np.array([[1.0, np.nan, 0.0]]), 1)
+    assert nf
+    _, _, nf = oracle.target_scan(np.array([[1.0, np.inf, 0.0]]), 1)
+    assert nf
+
+
+# --------------------------------------------------------------------- O2 verify
+def test_verify_spec_examples(golden_dir):
+    cases = json.load(open(os.path.join(golden_dir, "spec_verify_examples.json")))["cases"]
+    for c in cases:
+        draft = np.array([c["draft_tokens"]], dtype=np.int32)
+        parents = None if c["parents"] is None else np.array([c["parents"]], dtype=np.int32)
+        lab = oracle.verify(draft, parents, None, np.array(c["row_argmax"]))
+        e = c["expect"]
+        assert int(lab["accept_len"][0]) == e["accept_len"], c["name"]
+        assert lab["accepted"][0].tolist() == e["accepted"], c["name"]
+        assert int(lab["bonus"][0]) == e["bonus"], c["name"]
+        assert int((lab["accepted"][0] == 0).sum()) == e["n_rejected"], c["name"]
+        assert lab["row_class"].tolist() == e["row_class"], c["name"]
+
+
+def test_verify_chain_exhaustive():
+    """V=4, depth 3: all 4^3 draft sequences x 4^4 argmax patterns.
+    accept_len = 1 + longest matching prefix."""
+    drafts = np.array(list(itertools.product(range(4), repeat=3)), dtype=np.int32)
+    ams = np.array(list(itertools.product(range(4), repeat=4)), dtype=np.int64)
+    R = len(drafts) * len(ams)
+    draft_all = np.repeat(drafts, len(ams), axis=0)
+    am_all = np.tile(ams, (len(drafts), 1)).reshape(-1)
+    lab = oracle.verify(draft_all, None, None, am_all)
+    am2 = am_all.reshape(R, 4)
+    for r in range(R):
+        L = 0
+        while L < 3 and draft_all[r, L] == am2[r, L]:
+            L += 1
+        assert lab["accept_len"][r] == L + 1
+        assert lab["bonus"][r] == am2[r, L]
+        cls = lab["row_class"][r * 4:(r + 1) * 4]
+        assert cls.tolist() == [ACCEPT] * (L + 1) + [DISCARD] * (3 - L)
+
+
+def _random_tree(rng, N, max_children=3):
+    parents = np.full(N, -1, dtype=np.int32)
+    for n in range(1, N):
+        parents[n] = int(rng.integers(-1, n))
+    return parents
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_verify_tree_bruteforce(seed):
+    """Tree: accept_len = 1 + max over root-to-node paths of the number of
+    leading matches along the path (enumerated explicitly, brute force)."""
+    rng = np.random.default_rng(100 + seed)
+    R, N, V = 40, int(rng.integers(1, 14)), 3
+    parents = np.stack([_random_tree(rng, N) for _ in range(R)])
+    draft = np.empty((R, N), dtype=np.int32)
+    for r in range(R):       # distinct sibling tokens (generator contract; reading Q12)
+        for n in range(N):
+            used = {int(draft[r, s]) for s in range(n) if parents[r, s] == parents[r, n]}
+            choices = [t for t in range(V + 3) if t not in used]
+            draft[r, n] = choices[int(rng.integers(0, len(choices)))]
+    am = rng.integers(0, V, size=R * (N + 1))
+    lab = oracle.verify(draft, parents, None, am)
+    for r in range(R):
+        base = r * (N + 1)
+        best, best_node = 0, -1
+        for n in range(N):
+            path = []
+            x = n
+            while x >= 0:
+                path.append(x)
+                x = int(parents[r, x])
+            path.reverse()            # root child first
+            ok = all(draft[r, q] == am[base + int(parents[r, q]) + 1] for q in path)
+            if ok and len(path) > best:
+                best, best_node = len(path), n
+        assert lab["accept_len"][r] == best + 1
+        assert lab["bonus"][r] == am[base + best_node + 1]
+        acc_nodes = np.nonzero(lab["accepted"][r])[0].tolist()
+        assert len(acc_nodes) == best
+        # accepted nodes form one root path
+        for q in acc_nodes:
+            p = int(parents[r, q])
+            assert p < 0 or lab["accepted"][r, p]
+
+
+def test_verify_chain_encoded_as_tree_identical():
+    rng = np.random.default_rng(7)
+    R, N = 200, 6
+    draft = rng.integers(0, 3, size=(R, N)).astype(np.int32)
+    am = rng.integers(0, 3, size=R * (N + 1))
+    chain_parents = np.tile(np.arange(-1, N - 1, dtype=np.int32), (R, 1))
+    a = oracle.verify(draft, None, None, am)
+    b = oracle.verify(draft, chain_parents, None, am)
+    for key in a:
+        np.testing.assert_array_equal(a[key], b[key])
+
+
+def test_verify_ragged_and_scope():
+    draft = np.array([[1, 2, 3], [1, 9, 9]], dtype=np.int32)
+    am = np.array([1, 2, 0, 5, 1, 0, 0, 0])   # r0: node0,1 match, node2 no; r1: node0 match
+    lab = oracle.verify(draft, None, np.array([3, 2]), am, discard_scope=0)
+    assert lab["accept_len"].tolist() == [3, 2]
+    assert lab["row_class"].tolist() == [0, 0, 0, 1, 0, 0, 1, PAD]
+    lab1 = oracle.verify(draft, None, np.array([3, 1]), am, discard_scope=1)
+    assert lab1["row_class"].tolist() == [0, 0, 0, 1, 0, 0, PAD, PAD]
+    # scope 1: only the first divergence on a branch stays DISCARD
+    lab2 = oracle.verify(np.array([[7, 8, 9]], dtype=np.int32), None, None, np.array([0, 0, 0, 0]),
+                         discard_scope=1)
+    assert lab2["row_class"].tolist() == [0, 1, PAD, PAD]
+    with pytest.raises(ValueError):
+        oracle.verify(draft, np.array([[-1, 1, 0], [-1, 0, 1]], dtype=np.int32), None, am)
+
+
+def test_eq1_monte_carlo_generator():
+    """Generator pin: iid acceptance alpha=0.7, gamma=5 => E[L] = (1-a^6)/(1-a)
+    = 2.9412 (PAPER Eq. 1; SPEC S:660 'within 2%' over >= 50k steps)."""
+    cfg = tracegen.TraceConfig("mc", d=8, V=64, R=50000, N=5, seed=4242, alpha=(0.7,))
+    tr = tracegen.gen_trace(cfg)
+    T = oracle.bf16_bits_to_f64(tr["T_bits"])
+    am = np.argmax(T, axis=1)
+    lab = oracle.verify(tr["draft_tokens"], None, None, am)
+    EL = (1 - 0.7 ** 6) / (1 - 0.7)
+    assert abs(EL - 2.9412) < 1e-4
+    assert abs(lab["accept_len"].mean() - EL) / EL < 0.02
+
+
+# -------------------------------------------------------------------- O3 targets
+def test_targets_closed_forms():
+    tr = tracegen.gen_trace("small")
+    out = oracle.step(tr, want_grads=False)
+    tg = out["targets"]
+    M, R = tr["M"], tr["R"]
+    cls = out["row_class"]
+    n_acc, n_dis = tg["counts"]
+    assert n_acc + n_dis + int((cls == PAD).sum()) == M
+    assert n_acc >= R                                   # every root row is ACCEPT
+    for m in range(M):
+        if cls[m] == ACCEPT:                            # k_accept=1: p~ = 1, H~ = 0
+            assert len(tg["sup_idx"][m]) == 1 and tg["sup_p"][m][0] == 1.0 and tg["H"][m] == 0.0
+            assert tg["sup_idx"][m][0] == out["argmax"][m]
+            assert tg["w"][m] == 1.0 / n_acc
+        elif cls[m] == DISCARD:
+            assert len(tg["sup_idx"][m]) == 10
+            assert abs(tg["sup_p"][m].sum() - 1) < 1e-12
+            assert tg["H"][m] <= 0.0
+            assert tg["w"][m] == 1.0 / n_dis
+        else:
+            assert tg["w"][m] == 0.0
+
+
+# ------------------------------------------------------------------ O4/O5 loss
+def _dense_problem(seed, d=6, V=40, R=3, N=3, k_disc=10):
+    cfg = tracegen.TraceConfig("fd", d=d, V=V, R=R, N=N, seed=seed, alpha=(0.5,))
+    tr = tracegen.gen_trace(cfg)
+    return tr
+
+
+def _oracle_all(tr, W64, H64, **kw):
+    T = oracle.bf16_bits_to_f64(tr["T_bits"])
+    k_max = max(kw.get("k_accept", 1), kw.get("k_discard", 10))
+    am, topk, _ = oracle.target_scan(T, k_max)
+    lab = oracle.verify(tr["draft_tokens"], tr["parents"], tr["num_nodes"], am, kw.get("discard_scope", 0))
+    tg = oracle.row_targets(lab["row_class"], lambda m: T[m], topk, kw.get("k_accept", 1),
+                            kw.get("k_discard", 10), kw.get("lambda_discard", 1.0), kw.get("normalize", 0))
+    fw = oracle.loss_fwd(H64, W64, tg)
+    bw = oracle.loss_bwd(H64, W64, tg, fw["lse"], g=kw.get("g", 1.0))
+    return lab, tg, fw, bw, T
+
+
+def test_loss_no_rejections_equals_torch_cross_entropy():
+    """North-star invariant: no rejections + k_acc=1 => plain CE (library routine)."""
+    cfg = tracegen.TraceConfig("ce", d=32, V=300, R=6, N=4, seed=77, alpha=(0.5,))
+    tr = tracegen.gen_trace(cfg)
+    T = torch.from_numpy(oracle.bf16_bits_to_f64(tr["T_bits"]))
+    y = torch.argmax(T, dim=1)                       # first maximal index (torch docs)
+    R, N = cfg.R, cfg.N
+    tr["draft_tokens"] = np.stack([y.numpy()[r * (N + 1):r * (N + 1) + N] for r in range(R)]).astype(np.int32)
+    out = oracle.step(tr, want_grads=False)
+    assert (out["row_class"] == ACCEPT).all()
+    H = torch.from_numpy(oracle.bf16_bits_to_f64(tr["H_bits"]))
+    W = torch.from_numpy(oracle.bf16_bits_to_f64(tr["W_bits"]))
+    ref = F.cross_entropy(H @ W.T, y).item()
+    assert abs(out["loss"] - ref) <= 1e-12 * abs(ref)
+
+
+def test_loss_k_equals_V_matches_torch_kl_div():
+    """k = V on both terms, lambda=1: each term is the row-mean of
+    F.kl_div(log_softmax(Z), log_softmax(T), log_target=True) on its subset."""
+    cfg = tracegen.TraceConfig("kl", d=16, V=50, R=5, N=4, seed=78, alpha=(0.5,))
+    tr = tracegen.gen_trace(cfg)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    lab, tg, fw, _, T = _oracle_all(tr, W64, H64, k_accept=50, k_discard=50)
+    Z = torch.from_numpy(H64 @ W64.T)
+    kl = F.kl_div(F.log_softmax(Z, 1), F.log_softmax(torch.from_numpy(T), 1), log_target=True,
+                  reduction="none").sum(1).numpy()
+    cls = lab["row_class"]
+    ref = kl[cls == ACCEPT].mean() + (kl[cls == DISCARD].mean() if (cls == DISCARD).any() else 0.0)
+    assert abs(fw["loss"] - ref) <= 1e-10 * abs(ref)
+
+
+def test_spec_loss_examples(golden_dir):
+    cases = json.load(open(os.path.join(golden_dir, "loss_examples.json")))["cases"]
+    for c in cases:
+        V = c["V"]
+        if "target_row" in c:
+            t = np.array(c["target_row"])
+        else:
+            t = np.zeros(V)
+            t[c["target_row_argmax"]] = 1.0
+        am, topk, _ = oracle.target_scan(t[None], 1)
+        tg = oracle.row_targets(np.array([ACCEPT], dtype=np.uint8), lambda m: t, topk, 1, 1)
+        H64 = np.ones((1, 4))
+        W64 = np.zeros((V, 4))                  # logits identically 0
+        fw = oracle.loss_fwd(H64, W64, tg)
+        assert abs(fw["loss"] - c["expect_loss"]) < 1e-12, c["name"]
+        if "expect_dlogits" in c:
+            dz = oracle.dlogits_rows(H64, W64, tg, fw["lse"], [0])[0]
+            np.testing.assert_allclose(dz, c["expect_dlogits"], atol=1e-15)
+
+
+def test_decomposition_and_lambda_zero():
+    """S:370 L = L_A + lambda L_D (linear in lambda); S:372 lambda=0 => accept-only."""
+    tr = _dense_problem(11, d=8, V=60, R=4, N=4)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    L = {}
+    for lam in (0.0, 1.0, 2.5):
+        lab, tg, fw, _, _ = _oracle_all(tr, W64, H64, lambda_discard=lam)
+        L[lam] = fw["loss"]
+        cls = lab["row_class"]
+    assert (cls == DISCARD).any()
+    LA, LD = L[0.0], L[1.0] - L[0.0]
+    assert abs(L[2.5] - (LA + 2.5 * LD)) < 1e-12 * max(1.0, abs(L[2.5]))
+    # lambda = 0 equals the accept-only loss computed on the ACCEPT rows alone
+    lab, tg, fw, _, _ = _oracle_all(tr, W64, H64, lambda_discard=0.0)
+    accept_rows = np.nonzero(cls == ACCEPT)[0]
+    acc_only = fw["row_loss"][accept_rows].mean()
+    assert abs(LA - acc_only) < 1e-12
+
+
+def test_shift_invariance():
+    """Adding the same vector c to every vocab row of W shifts all logits of a row
+    equally: L, dH and dW are unchanged (softmax shift invariance, S:? toy-lm
+    invariant 'invariant to uniform logit shifts')."""
+    tr = _dense_problem(12, d=8, V=60, R=4, N=4)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    c = np.random.default_rng(3).standard_normal(8)
+    _, _, fw0, bw0, _ = _oracle_all(tr, W64, H64)
+    _, _, fw1, bw1, _ = _oracle_all(tr, W64 + c[None, :], H64)
+    assert abs(fw0["loss"] - fw1["loss"]) < 1e-10
+    np.testing.assert_allclose(bw1["dW"], bw0["dW"], atol=1e-12)
+    np.testing.assert_allclose(bw1["dH"], bw0["dH"], atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_finite_differences(seed):
+    """Central differences in f64, h=1e-6, on random entries of W and H
+    (labels depend only on T and tokens, so L is smooth in (H, W))."""
+    tr = _dense_problem(20 + seed, d=6, V=40, R=3, N=3)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    lab, tg, fw, bw, T = _oracle_all(tr, W64, H64)
+    rng = np.random.default_rng(seed)
+    h = 1e-6
+
+    def L_of(Wx, Hx):
+        return oracle.loss_fwd(Hx, Wx, tg)["loss"]
+
+    for _ in range(12):
+        i, j = int(rng.integers(0, W64.shape[0])), int(rng.integers(0, W64.shape[1]))
+        Wp, Wm = W64.copy(), W64.copy()
+        Wp[i, j] += h
+        Wm[i, j] -= h
+        fd = (L_of(Wp, H64) - L_of(Wm, H64)) / (2 * h)
+        assert abs(fd - bw["dW"][i, j]) <= 1e-6 * max(1e-3, abs(bw["dW"][i, j])) + 1e-9
+        i, j = int(rng.integers(0, H64.shape[0])), int(rng.integers(0, H64.shape[1]))
+        Hp, Hm = H64.copy(), H64.copy()
+        Hp[i, j] += h
+        Hm[i, j] -= h
+        fd = (L_of(W64, Hp) - L_of(W64, Hm)) / (2 * h)
+        assert abs(fd - bw["dH"][i, j]) <= 1e-6 * max(1e-3, abs(bw["dH"][i, j])) + 1e-9
+
+
+@pytest.mark.parametrize("name,kw", [("small", {}), ("small_tree", {}), ("small", {"normalize": 1}),
+                                     ("small", {"discard_scope": 1, "lambda_discard": 0.5}),
+                                     ("small_tree", {"k_accept": 3, "k_discard": 16})])
+def test_torch_autograd(name, kw):
+    """Library route: torch f64 autograd of sum_m w_m F.kl_div(log_softmax(z_m), p~_m)
+    with p~ scattered into a dense target (0 log 0 = 0 by xlogy), vs the
+    oracle's closed-form gradients."""
+    tr = tracegen.gen_trace(name)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    lab, tg, fw, bw, T = _oracle_all(tr, W64, H64, **kw)
+    M, V = T.shape
+    P = torch.zeros(M, V)
+    wv = torch.zeros(M)
+    for m in range(M):
+        P[m, torch.from_numpy(tg["sup_idx"][m])] = torch.from_numpy(tg["sup_p"][m])
+        wv[m] = tg["w"][m]
+    Ht = torch.from_numpy(H64).requires_grad_(True)
+    Wt = torch.from_numpy(W64).requires_grad_(True)
+    Z = Ht @ Wt.T
+    row = F.kl_div(F.log_softmax(Z, 1), P, reduction="none").sum(1)
+    L = (wv * row).sum()
+    L.backward()
+    assert abs(L.item() - fw["loss"]) <= 1e-11 * abs(fw["loss"])
+    np.testing.assert_allclose(fw["row_loss"], row.detach().numpy(), rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(bw["dW"], Wt.grad.numpy(), rtol=1e-9, atol=1e-14)
+    np.testing.assert_allclose(bw["dH"], Ht.grad.numpy(), rtol=1e-9, atol=1e-14)
+
+
+def test_row_sum_zero():
+    """sum_j dz_mj = w (sum q - sum p~) = 0 for every row => dW column sums vanish."""
+    tr = tracegen.gen_trace("small")
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    lab, tg, fw, bw, T = _oracle_all(tr, W64, H64)
+    rows = list(range(0, tr["M"], 7))
+    dz = oracle.dlogits_rows(H64, W64, tg, fw["lse"][rows], rows)
+    assert np.abs(dz.sum(1)).max() < 1e-15
+    colsum = bw["dW"].sum(0)
+    assert np.abs(colsum).max() < 1e-12 * max(1.0, np.abs(bw["dW"]).max() * tr["V"])
+
+
+def test_upstream_gradient_scaling():
+    tr = _dense_problem(31, d=6, V=40, R=3, N=3)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    _, _, _, b1, _ = _oracle_all(tr, W64, H64, g=1.0)
+    _, _, _, b3, _ = _oracle_all(tr, W64, H64, g=-3.0)
+    np.testing.assert_allclose(b3["dW"], -3.0 * b1["dW"], rtol=1e-12, atol=1e-15)
+
+
+def test_discard_direction():
+    """Adapted from SPEC S:664 / learner example: one SGD step on a record whose
+    first proposal was rejected lowers the draft's probability of the rejected
+    token at the context where it was proposed (the implicit negative, reading Q2)."""
+    # The draft proposed its own greedy token x0 at the root context; the
+    # verifier's argmax differs, so x0 is rejected.  h1 is made orthogonal to
+    # h0 so the discard row's W-update does not move the root-row logits; the
+    # first-order change of log q0(x0) under a W step is then
+    # -lr |h0|^2 (q_x0 + q_y - sum q^2) < 0 because q_x0 = max q >= sum q^2.
+    cfg = tracegen.TraceConfig("dd", d=16, V=30, R=1, N=1, seed=5, alpha=(0.0,))
+    tr = tracegen.gen_trace(cfg)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    H64[1] -= (H64[1] @ H64[0]) / (H64[0] @ H64[0]) * H64[0]
+    x0 = int(np.argmax(W64 @ H64[0]))
+    tr["draft_tokens"] = np.array([[x0]], dtype=np.int32)
+    lab, tg, fw, bw, T = _oracle_all(tr, W64, H64)
+    assert lab["accept_len"][0] == 1 and lab["row_class"].tolist() == [ACCEPT, DISCARD]
+
+    def q_rej(Wx, Hx):
+        z = Wx @ Hx[0]
+        z = z - z.max()
+        return np.exp(z[x0]) / np.exp(z).sum()
+
+    lr = 1e-3
+    before = q_rej(W64, H64)
+    after = q_rej(W64 - lr * bw["dW"], H64)
+    assert after < before
