@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Bench: speculator-training tokens/s of the Aurora hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama] [--impl ours|reference]
+
+A step = one pass of the whole hot path over one synthetic
+trace batch: greedy verification + labels, lm_head fwd with vocab-wide
+log-softmax + Eq. 3 loss, and the bwd (dLogits tiles -> dW, dH).  Inputs are
+resident in HBM when the timed region starts; every step is bracketed by its own
+CUDA events on the launching stream, L2 is flushed between steps (a 256 MiB write,
+outside the events).  `value` = rows (training tokens) processed by all ranks /
+max-over-ranks time.  `e2e` repeats the measurement through the public API with the
+trace batch (T, H, draft tokens) copied from pinned host memory every step and the
+loss + accept lengths read back.
+
+N > 1 (torchrun): data-parallel over trace batches (weak scaling): each rank owns a
+different seeded batch, the loss normalisation counts and dW are allreduced by the
+library's NCCL communicator (C2, C5).
+
+--impl reference: the f64 CPU oracle (the reference arm for this tier) timed on the
+host cores on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import tracegen  # noqa: E402
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("bf16_tflops", 1624.6), d.get("bf16_tflops_sustained", 1394.5), d.get("hbm_gbs", 6551.0), "measured"
+    return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 8:
+                for n, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _bf16(t_bits, torch, device):
+    return torch.from_numpy(np.ascontiguousarray(t_bits).view(np.int16)).view(torch.bfloat16).to(device)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_06932_b200 import aurora as A
+    from paper_2602_06932_b200.build import build
+
+    ws, rank, local = _dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        build()
+    if ws > 1:
+        dist.barrier()
+    A.lib()
+
+    cfg = tracegen.CONFIGS[args.config]
+    tr = tracegen.gen_trace(cfg, seed=cfg.seed + 1000 * rank)
+    R, N, d, V, M = cfg.R, cfg.N, cfg.d, cfg.V, cfg.M
+
+    comm = None
+    if ws > 1:
+        uid = A.aurora_comm_get_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        comm = A.aurora_comm_create(obj[0], ws, rank, 1, ws)
+
+    T = _bf16(tr["T_bits"], torch, dev)
+    H = _bf16(tr["H_bits"], torch, dev)
+    W = _bf16(tr["W_bits"], torch, dev)
+    draft = torch.from_numpy(tr["draft_tokens"]).to(dev)
+    parents = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).to(dev)
+    num_nodes = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).to(dev)
+    st = A.SpecTrainStep(R, N, d, V, comm=comm, device=dev)
+    dH = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dW = torch.empty(V, d, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        st.step(draft, T, H, W, dH, dW, parents, num_nodes)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert int(st.status.item()) == 0, "device status word set"
+
+    # ---------------- timed region (device-resident inputs)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    A.aurora_profile_read()  # clear
+    A.aurora_profile_enable(True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = A.aurora_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    n_launch = A.aurora_launch_count() - n0
+    A.aurora_profile_enable(False)
+    phases = A.aurora_profile_read()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    tokens_per_s = (M * ws) / (ms_step / 1e3)
+
+    # ---------------- e2e: public API with pinned host inputs, result read back
+    e2e = _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush)
+
+    if rank != 0:
+        if comm is not None:
+            A.aurora_comm_destroy(comm)
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    peak_burst, peak_sus, hbm, peak_src = _peaks()
+    roof = _roofline(phases, cfg, args.steps, peak_sus, peak_src)
+    out = {
+        "metric": "speculator-training tokens/s (verify + lm_head fwd/bwd + Eq.3 loss), % bf16 tensor peak",
+        "value": round(tokens_per_s, 1),
+        "unit": "tokens/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (tracegen seeded traces; random-init lm_head)",
+        "config": {"workload": cfg.name, "R": R, "N": N, "M_rows_per_gpu": M, "d": d, "V": V,
+                   "tree": cfg.tree, "parallelism": f"dp{ws}" if ws > 1 else "single",
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)"},
+        "gpu_launches": int(n_launch),
+        "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
+        "roofline": roof,
+        "e2e": e2e,
+        "clocks": clk.summary(),
+    }
+    out["tensor_frac_step"] = round((8.0 * M * V * d / (ms_step / 1e3)) / (peak_sus * 1e12), 4)
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = _cpu_baseline(cfg, args)
+    print(json.dumps(out), flush=True)
+    if comm is not None:
+        A.aurora_comm_destroy(comm)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush):
+    """Same step through the public API, inputs copied H2D from pinned memory each
+    step and the per-step result (loss, accept lengths) read back D2H."""
+    hT = torch.from_numpy(np.ascontiguousarray(tr["T_bits"]).view(np.int16)).pin_memory()
+    hH = torch.from_numpy(np.ascontiguousarray(tr["H_bits"]).view(np.int16)).pin_memory()
+    hX = torch.from_numpy(tr["draft_tokens"]).pin_memory()
+    hP = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).pin_memory()
+    hN = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).pin_memory()
+    dT = torch.empty(hT.shape, dtype=torch.bfloat16, device=dev)
+    dHh = torch.empty(hH.shape, dtype=torch.bfloat16, device=dev)
+    dX = torch.empty(hX.shape, dtype=torch.int32, device=dev)
+    dP = None if hP is None else torch.empty(hP.shape, dtype=torch.int32, device=dev)
+    dN = None if hN is None else torch.empty(hN.shape, dtype=torch.int32, device=dev)
+    out_loss = torch.empty(1, dtype=torch.float32).pin_memory()
+    out_al = torch.empty(st.R, dtype=torch.int32).pin_memory()
+    h2d = hT.numel() * 2 + hH.numel() * 2 + hX.numel() * 4 + (0 if hP is None else hP.numel() * 4) + \
+        (0 if hN is None else hN.numel() * 4)
+    d2h = 4 + st.R * 4
+    stream = torch.cuda.current_stream(dev)
+
+    def e2e_step():
+        dT.view(torch.int16).copy_(hT, non_blocking=True)
+        dHh.view(torch.int16).copy_(hH, non_blocking=True)
+        dX.copy_(hX, non_blocking=True)
+        if dP is not None:
+            dP.copy_(hP, non_blocking=True)
+        if dN is not None:
+            dN.copy_(hN, non_blocking=True)
+        st.step(dX, dT, dHh, W, dH, dW, dP, dN)
+        out_loss.copy_(st.loss, non_blocking=True)
+        out_al.copy_(st.accept_len, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        evs[i][0].record(stream)
+        e2e_step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    return {"value": round(st.M * ws / (ms_step / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(ms_step, 4),
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+
+def _roofline(phases, cfg, steps, peak, peak_src):
+    """Dominant lm_head kernel: algorithmic flops per launch / mean launch time."""
+    M, V, d = cfg.M, cfg.V, cfg.d
+    flops_total = {"fwd_gemm": 2.0 * M * V * d, "bwd_dz_gemm": 2.0 * M * V * d, "bwd_dw_gemm": 2.0 * M * V * d,
+                   "bwd_dh_gemm": 2.0 * M * V * d}
+    best = None
+    per = []
+    for k, f in flops_total.items():
+        if k not in phases or phases[k][1] == 0:
+            continue
+        tot_ms, n = phases[k]
+        launches_per_step = n / steps
+        ach = (f / launches_per_step) / ((tot_ms / n) / 1e3) / 1e12
+        per.append({"kernel": k, "ms_per_step": round(tot_ms / steps, 4), "launches_per_step": launches_per_step,
+                    "achieved_tflops": round(ach, 1), "frac": round(ach / peak, 4)})
+        if best is None or tot_ms > best[1]:
+            best = (k, tot_ms, ach, n)
+    if best is None:
+        return None
+    k, tot_ms, ach, n = best
+    traffic = _traffic_for(k)
+    return {"bound": "tensor", "kernel": k, "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(ach / peak, 4), "traffic": traffic,
+            "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)",
+            "work_per_launch": "2*M*V_chunk*d flops (2d per row per vocab column, SURVEY 8(d))",
+            "phases": per}
+
+
+def _traffic_for(kernel):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get(kernel)
+        except Exception:
+            return None
+    return None
+
+
+def _cpu_baseline(cfg, args, reqs=None):
+    """The oracle as it stands, on a bounded sample (first `reqs` requests of the
+    same workload, full vocabulary and hidden size), on this host's cores."""
+    import oracle
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        cores = len(os.sched_getaffinity(0))
+    reqs = reqs or args.cpu_reqs
+    tr = tracegen.gen_trace(cfg)
+    sub = _subsample(tr, reqs)
+    t0 = time.perf_counter()
+    oracle.step(sub)
+    dt = time.perf_counter() - t0
+    return {"value": round(sub["M"] / dt, 2), "unit": "tokens/s", "cores": int(cores), "kind": "oracle",
+            "sample": f"first {reqs} of {cfg.R} requests ({sub['M']} rows) of '{cfg.name}', full V={cfg.V}, "
+                      f"d={cfg.d}; verify+fwd+bwd f64; {dt:.2f} s"}
+
+
+def _subsample(tr, reqs):
+    cfg = tr["cfg"]
+    rows = reqs * (cfg.N + 1)
+    sub = dict(tr)
+    sub["draft_tokens"] = tr["draft_tokens"][:reqs]
+    sub["parents"] = None if tr["parents"] is None else tr["parents"][:reqs]
+    sub["num_nodes"] = None if tr["num_nodes"] is None else tr["num_nodes"][:reqs]
+    sub["T_bits"] = tr["T_bits"][:rows]
+    sub["H_bits"] = tr["H_bits"][:rows]
+    sub["M"] = rows
+    sub["R"] = reqs
+    return sub
+
+
+def run_reference(args):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    cfg = tracegen.CONFIGS[args.config]
+    tr = tracegen.gen_trace(cfg)
+    sub = _subsample(tr, args.ref_reqs)
+    import oracle
+    for _ in range(args.warmup if args.warmup_ref else 0):
+        oracle.step(sub)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.step(sub)
+    dt = (time.perf_counter() - t0) / args.steps
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        cores = len(os.sched_getaffinity(0))
+    val = round(sub["M"] / dt, 2)
+    out = {"impl": "reference", "metric": "speculator-training tokens/s (verify + lm_head fwd/bwd + Eq.3 loss), "
+           "% bf16 tensor peak", "value": val, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (tracegen seeded traces)",
+           "config": {"workload": cfg.name, "R": cfg.R, "N": cfg.N, "d": cfg.d, "V": cfg.V,
+                      "parallelism": "cpu oracle (rank 0 only)"},
+           "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": int(cores), "kind": "oracle",
+                            "sample": f"first {args.ref_reqs} of {cfg.R} requests ({sub['M']} rows) per step, "
+                                      f"full V and d"},
+           "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="llama", choices=sorted(tracegen.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-reqs", type=int, default=8)
+    ap.add_argument("--ref-reqs", type=int, default=2)
+    ap.add_argument("--warmup-ref", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

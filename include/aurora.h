@@ -1,0 +1,202 @@
+/*
+ * aurora.h — C-ABI boundary of the B200-native Aurora speculator-training hot path.
+ *
+ * Paper: "When RL Meets Adaptive Speculative Training: A Unified Training–Serving
+ * System" (arXiv 2602.06932).  Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.
+ *
+ * One trace batch (R requests x N draft nodes, M = R*(N+1) rows) goes through
+ *   aurora_verify_labels  greedy verification + per-row targets
+ *   aurora_spec_loss_fwd  lm_head GEMM + vocab-wide log-softmax + Eq. 3 loss
+ *   aurora_spec_loss_bwd  dLogits (tiles only) -> dW_lmhead, dHidden
+ * The [M x V] logits are never stored; dLogits exist only as a bounded per-vocab-chunk
+ * workspace (at most 1/4 of the local M x V_local, see aurora_workspace_size).
+ *
+ * Conventions (all entry points):
+ *  - Pointers marked (dev) are CUDA device pointers, (host) are host pointers.  The
+ *    caller owns every buffer; the library never allocates device memory on the hot
+ *    path (scratch comes from `ws`, sized by aurora_workspace_size).
+ *  - `stream` is a cudaStream_t passed as void*.  All work (kernels, NCCL) is
+ *    enqueued on it; no call synchronises the host.  Host structs are read during
+ *    the call and not retained.
+ *  - Host-detectable errors (NULL pointers, bad sizes, k > 16, N > 32, workspace too
+ *    small) return a non-OK status with NOTHING enqueued.  Data-dependent errors
+ *    (token id >= V, parents[n] >= n or < -1, non-finite target logits) set bits in
+ *    the device status word labels->status and the kernels still complete without
+ *    undefined behaviour; the caller reads the word at its own sync point.
+ *  - Row m = r*(N+1) + s: s = 0 is the root context (verifier logits after the
+ *    prompt), s = n+1 the context after draft node n (the D_RPC l_t).
+ *  - bf16 means IEEE bfloat16 bit patterns, row-major, densely packed unless an
+ *    explicit leading dimension is given.
+ *  - Nothing aborts; nothing prints.
+ */
+#ifndef AURORA_H_
+#define AURORA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AURORA_ABI_VERSION 1
+#define AURORA_MAX_NODES 32   /* N <= 32: one warp lane per draft node      */
+#define AURORA_MAX_K 16       /* k_accept, k_discard <= 16 on the hot path  */
+
+typedef enum {
+  AURORA_OK = 0,
+  AURORA_ERR_INVALID_ARG = 1,   /* NULL pointer, bad size or stride              */
+  AURORA_ERR_STRUCTURE = 2,     /* reserved: malformed parents (device word bit)  */
+  AURORA_ERR_RANGE = 3,         /* reserved: token id >= V (device word bit)      */
+  AURORA_ERR_NONFINITE = 4,     /* reserved: non-finite logits (device word bit)  */
+  AURORA_ERR_UNSUPPORTED = 5,   /* valid request this build does not implement    */
+  AURORA_ERR_WORKSPACE = 6,     /* ws NULL or ws_bytes < aurora_workspace_size()  */
+  AURORA_ERR_CUDA = 7,          /* kernel launch / driver failure                 */
+  AURORA_ERR_NCCL = 8           /* NCCL failure or NCCL unavailable               */
+} aurora_status_t;
+
+/* Bits of the device status word (labels->status[0]); OR-accumulated. */
+#define AURORA_STATUS_NONFINITE 1u   /* a target logit is NaN or +-Inf           */
+#define AURORA_STATUS_RANGE     2u   /* a draft token is < 0 or >= V             */
+#define AURORA_STATUS_STRUCTURE 4u   /* parents[n] >= n or < -1                  */
+
+/* Row classes (readings Q1-Q3 in DESIGN.md). */
+#define AURORA_ROW_ACCEPT  0   /* root, or context of an accepted node       */
+#define AURORA_ROW_DISCARD 1   /* context contains a rejected token  */
+#define AURORA_ROW_PAD     2   /* ragged padding / out-of-scope discard: weight 0    */
+
+/* Communicator for vocab-parallel (VP) / data-parallel (DP) runs.  NULL = 1 GPU. */
+typedef struct aurora_comm_s* aurora_comm_t;
+
+/* One local trace batch (P:372-376 D_RPC; S:397-410 TraceRecord). */
+typedef struct {
+  int32_t R;                     /* requests in this (local) batch, >= 1               */
+  int32_t N;                     /* draft nodes per request, 1..32 (chain: gamma)      */
+  const int32_t* draft_tokens;   /* (dev) int32 [R,N] proposed tokens, global vocab ids */
+  const int32_t* parents;        /* (dev) int32 [R,N]; -1 = root, parents[n] < n
+                                    (topological); NULL => chain, parent = n-1   */
+  const int32_t* num_nodes;      /* (dev) int32 [R] valid nodes per request (ragged);
+                                    NULL => all N.  Rows of nodes >= num_nodes are PAD. */
+  const void* target_logits;     /* (dev) bf16 [M, ld_target] verifier logits over this
+                                    rank's vocab slice [vocab_offset, vocab_offset+V_local) */
+  int64_t ld_target;             /* row stride of target_logits in elements (>= V_local) */
+  int64_t V;                     /* global vocabulary size                              */
+  int64_t V_local;               /* vocab columns held by this rank                     */
+  int64_t vocab_offset;          /* global id of local column 0                         */
+} aurora_trace_t;
+
+/* Loss configuration (Eq. 3; Table 3). */
+typedef struct {
+  int32_t k_accept;       /* support size on ACCEPT rows; default 1 = CE on the verified
+                             token (reading Q5); 1..16                           */
+  int32_t k_discard;      /* support size on DISCARD rows; default 10; 1..16.
+                             0 (= paper's unfiltered "top-k 0") -> UNSUPPORTED   */
+  float lambda_discard;   /* default 1.0; 0 disables the discard term          */
+  int32_t normalize;      /* 0: per-term means over GLOBAL counts N_A, N_D (default,
+                             S:378, reading Q7); 1: mean over N_A + N_D rows            */
+  int32_t discard_scope;  /* 0: all rejected nodes (default); 1: only the first
+                             rejected node on each branch (others become PAD)           */
+} aurora_loss_cfg_t;
+
+/* Caller-allocated outputs of verify; inputs of fwd/bwd.  All (dev). */
+typedef struct {
+  int32_t k_max;          /* (in) row stride of sup_idx/sup_p; >= max(k_accept,k_discard), <= 16 */
+  int32_t* target_argmax; /* [M]  y_m, global id; lowest index wins ties  */
+  uint8_t* accepted;      /* [R,N] 1 = node on the accepted path                         */
+  int32_t* accept_len;    /* [R]  #accepted + 1 (bonus counts)                    */
+  int32_t* bonus;         /* [R]  y at the deepest accepted row                          */
+  uint8_t* row_class;     /* [M]  AURORA_ROW_*                                           */
+  int32_t* sup_idx;       /* [M,k_max] target top-k support, GLOBAL ids sorted ascending;
+                             unused slots = INT32_MAX                                    */
+  float* sup_p;           /* [M,k_max] renormalised target probs p~ aligned with sup_idx */
+  float* row_H;           /* [M]  sum_j p~ log p~ (0 when k = 1)                          */
+  float* row_w;           /* [M]  loss weight: 1/N_A, lambda/N_D or 0                     */
+  int32_t* counts;        /* [2]  N_A, N_D (global over DP ranks)                        */
+  uint32_t* status;       /* [1]  device status word, AURORA_STATUS_* bits                */
+} aurora_labels_t;
+
+/* Workspace sizing.  op: 0 = verify, 1 = fwd, 2 = bwd, 3 = max over all three.
+ * Depends only on the arguments; a buffer of the returned size (256-byte aligned
+ * base) may be reused for every call with the same sizes.  Returns 0 on bad args. */
+#define AURORA_OP_VERIFY 0
+#define AURORA_OP_FWD 1
+#define AURORA_OP_BWD 2
+#define AURORA_OP_ALL 3
+size_t aurora_workspace_size(int op, int64_t M, int64_t d, int64_t V_local,
+                             const aurora_loss_cfg_t* cfg);
+
+/* Greedy verification + labels.
+ * Scans every target row once (argmax + top-k_max, exact bf16 compares), verifies
+ * chains/trees (acc(n) = acc(parent) AND x_n == y_row(parent); lowest-index sibling
+ * wins, reading Q12), classifies rows, builds supports p~ and weights w.
+ * VP: candidates are merged across ranks (global order), DP: counts are summed. */
+aurora_status_t aurora_verify_labels(const aurora_trace_t* trace, const aurora_loss_cfg_t* cfg,
+                                     aurora_labels_t* out, void* ws, size_t ws_bytes,
+                                     aurora_comm_t comm, void* stream);
+
+/* Forward (Eq. 3).
+ * H (dev) bf16 [M,d] draft-head hidden states; W (dev) bf16 [V_local,d] lm_head rows
+ * for global ids [vocab_offset, vocab_offset+V_local).  d % 64 == 0.
+ * Outputs: row_lse (dev) f32 [M] = log sum_j exp(z_mj) over the GLOBAL vocabulary;
+ * row_loss (dev, nullable) f32 [M] = KL(p~_m || softmax(z_m)); loss (dev) f32 [1] =
+ * sum_m w_m row_loss_m.  Z = H W^T is consumed tile by tile in TMEM. */
+aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, int64_t d,
+                                     int64_t V_local, int64_t vocab_offset,
+                                     const aurora_labels_t* labels, float* row_lse,
+                                     float* row_loss, float* loss, void* ws, size_t ws_bytes,
+                                     aurora_comm_t comm, void* stream);
+
+/* Backward.  dz_mj = g w_m (exp(z_mj - lse_m) - p~_mj) is
+ * recomputed per tile, rounded to bf16 into a per-vocab-chunk workspace, then
+ * dW[chunk] = dZ^T H and dH += dZ W[chunk].
+ * dloss (dev, nullable => g = 1) f32 [1] upstream gradient.
+ * dH (dev) f32 [M,d] (overwritten; VP: summed over ranks).
+ * dW (dev) [V_local,d]: f32 (dW_is_bf16 = 0) — bf16 output -> UNSUPPORTED in
+ * this build; accumulate_dW = 1 adds into dW (micro-batch accumulation). */
+aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, int64_t d,
+                                     int64_t V_local, int64_t vocab_offset,
+                                     const aurora_labels_t* labels, const float* row_lse,
+                                     const float* dloss, float* dH, void* dW, int dW_is_bf16,
+                                     int accumulate_dW, void* ws, size_t ws_bytes,
+                                     aurora_comm_t comm, void* stream);
+
+/* Communicator (vocab-parallel x data-parallel, one process per GPU).
+ * nccl_unique_id (host) points to the 128-byte ncclUniqueId that rank 0 created with
+ * aurora_comm_get_unique_id and the caller broadcast (e.g. torch.distributed).
+ * Ranks are laid out dp-major: rank = dp_rank * vp_size + vp_rank. */
+aurora_status_t aurora_comm_get_unique_id(void* nccl_unique_id_out /* 128 bytes */);
+aurora_status_t aurora_comm_create(const void* nccl_unique_id, int nranks, int rank,
+                                   int vp_size, int dp_size, aurora_comm_t* out);
+aurora_status_t aurora_comm_destroy(aurora_comm_t comm);
+
+const char* aurora_status_string(aurora_status_t s);
+/* Static build information ("sm_100a, tcgen05 ..."). */
+const char* aurora_build_info(void);
+/* Number of kernels this library has launched since load (for bench accounting). */
+uint64_t aurora_launch_count(void);
+
+/* Per-phase device timing (CUDA events recorded on the caller's stream around each
+ * phase while enabled).  aurora_profile_read must be called after the stream was
+ * synchronised; it fills up to `max` (name, total ms, launches) triples and returns
+ * the number of phases, then clears the accumulators. */
+void aurora_profile_enable(int enable);
+int aurora_profile_read(const char** names, float* total_ms, int32_t* count, int max);
+
+/* ---- Test hooks (not on the hot path) ------------------------------------ */
+/* D[M,N] (dev f32, ld ldd) = sum_k A(m,k) B(n,k) on the tcgen05 GEMM engine.
+ * a_mn_major = 0: A is bf16 [M,K] (ld lda); 1: A is stored as bf16 [K,M] (ld lda).
+ * b_mn_major = 0: B is bf16 [N,K] (ld ldb); 1: B is stored as bf16 [K,N] (ld ldb). */
+aurora_status_t aurora_debug_gemm(int a_mn_major, int b_mn_major, const void* A, const void* B,
+                                  float* D, int64_t M, int64_t N, int64_t K, int64_t lda,
+                                  int64_t ldb, int64_t ldd, void* stream);
+/* out (dev f32 [n_rows, V_local]) = full dLogits rows dz for the listed rows (dev int32). */
+aurora_status_t aurora_debug_dlogits_rows(const void* H, const void* W, int64_t M, int64_t d,
+                                          int64_t V_local, int64_t vocab_offset,
+                                          const aurora_labels_t* labels, const float* row_lse,
+                                          const float* dloss, const int32_t* rows, int32_t n_rows,
+                                          float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AURORA_H_ */

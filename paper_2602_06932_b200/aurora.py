@@ -1,0 +1,259 @@
+"""ctypes binding of libaurora.so (include/aurora.h) — argument marshalling only.
+
+Every step of the hot path runs inside the CUDA library; this module only turns
+torch tensors (device memory, streams) into pointers and raises on non-OK status.
+If libaurora.so is missing the import of the library fails loudly: there is no
+CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libaurora.so")
+
+AURORA_OK = 0
+STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "structure", 3: "range", 4: "nonfinite", 5: "unsupported",
+                6: "workspace", 7: "cuda", 8: "nccl"}
+STATUS_NONFINITE, STATUS_RANGE, STATUS_STRUCTURE = 1, 2, 4
+ROW_ACCEPT, ROW_DISCARD, ROW_PAD = 0, 1, 2
+OP_VERIFY, OP_FWD, OP_BWD, OP_ALL = 0, 1, 2, 3
+MAX_K, MAX_NODES = 16, 32
+
+# Symbols declared in include/aurora.h (checked by tests/test_abi.py).
+EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fwd", "aurora_spec_loss_bwd",
+           "aurora_comm_get_unique_id", "aurora_comm_create", "aurora_comm_destroy", "aurora_status_string",
+           "aurora_build_info", "aurora_launch_count", "aurora_profile_enable", "aurora_profile_read",
+           "aurora_debug_gemm", "aurora_debug_dlogits_rows"]
+
+
+class AuroraError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        self.status = status
+        super().__init__(f"{fn} failed: {status} ({STATUS_NAMES.get(status, '?')})")
+
+
+class aurora_trace_t(C.Structure):
+    _fields_ = [("R", C.c_int32), ("N", C.c_int32), ("draft_tokens", C.c_void_p), ("parents", C.c_void_p),
+                ("num_nodes", C.c_void_p), ("target_logits", C.c_void_p), ("ld_target", C.c_int64),
+                ("V", C.c_int64), ("V_local", C.c_int64), ("vocab_offset", C.c_int64)]
+
+
+class aurora_loss_cfg_t(C.Structure):
+    _fields_ = [("k_accept", C.c_int32), ("k_discard", C.c_int32), ("lambda_discard", C.c_float),
+                ("normalize", C.c_int32), ("discard_scope", C.c_int32)]
+
+
+class aurora_labels_t(C.Structure):
+    _fields_ = [("k_max", C.c_int32), ("target_argmax", C.c_void_p), ("accepted", C.c_void_p),
+                ("accept_len", C.c_void_p), ("bonus", C.c_void_p), ("row_class", C.c_void_p),
+                ("sup_idx", C.c_void_p), ("sup_p", C.c_void_p), ("row_H", C.c_void_p), ("row_w", C.c_void_p),
+                ("counts", C.c_void_p), ("status", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libaurora.so (in-tree).  Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} not found: build it with `python -m paper_2602_06932_b200.build` "
+                           "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    vp, i64, i32, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_size_t
+    L.aurora_workspace_size.argtypes = [C.c_int, i64, i64, i64, C.POINTER(aurora_loss_cfg_t)]
+    L.aurora_workspace_size.restype = sz
+    L.aurora_verify_labels.argtypes = [C.POINTER(aurora_trace_t), C.POINTER(aurora_loss_cfg_t),
+                                       C.POINTER(aurora_labels_t), vp, sz, vp, vp]
+    L.aurora_verify_labels.restype = C.c_int
+    L.aurora_spec_loss_fwd.argtypes = [vp, vp, i64, i64, i64, i64, C.POINTER(aurora_labels_t), vp, vp, vp, vp, sz,
+                                       vp, vp]
+    L.aurora_spec_loss_fwd.restype = C.c_int
+    L.aurora_spec_loss_bwd.argtypes = [vp, vp, i64, i64, i64, i64, C.POINTER(aurora_labels_t), vp, vp, vp, vp,
+                                       C.c_int, C.c_int, vp, sz, vp, vp]
+    L.aurora_spec_loss_bwd.restype = C.c_int
+    L.aurora_comm_get_unique_id.argtypes = [vp]
+    L.aurora_comm_get_unique_id.restype = C.c_int
+    L.aurora_comm_create.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    L.aurora_comm_create.restype = C.c_int
+    L.aurora_comm_destroy.argtypes = [vp]
+    L.aurora_comm_destroy.restype = C.c_int
+    L.aurora_status_string.argtypes = [C.c_int]
+    L.aurora_status_string.restype = C.c_char_p
+    L.aurora_build_info.argtypes = []
+    L.aurora_build_info.restype = C.c_char_p
+    L.aurora_launch_count.argtypes = []
+    L.aurora_launch_count.restype = C.c_uint64
+    L.aurora_profile_enable.argtypes = [C.c_int]
+    L.aurora_profile_enable.restype = None
+    L.aurora_profile_read.argtypes = [C.POINTER(C.c_char_p), C.POINTER(C.c_float), C.POINTER(C.c_int32), C.c_int]
+    L.aurora_profile_read.restype = C.c_int
+    L.aurora_debug_gemm.argtypes = [C.c_int, C.c_int, vp, vp, vp, i64, i64, i64, i64, i64, i64, vp]
+    L.aurora_debug_gemm.restype = C.c_int
+    L.aurora_debug_dlogits_rows.argtypes = [vp, vp, i64, i64, i64, i64, C.POINTER(aurora_labels_t), vp, vp, vp,
+                                            i32, vp, vp]
+    L.aurora_debug_dlogits_rows.restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(fn: str, st: int):
+    if st != AURORA_OK:
+        raise AuroraError(fn, st)
+
+
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# ----------------------------------------------------------- thin C-name wrappers
+def aurora_workspace_size(op: int, M: int, d: int, V_local: int, cfg: aurora_loss_cfg_t) -> int:
+    return int(lib().aurora_workspace_size(op, M, d, V_local, C.byref(cfg)))
+
+
+def aurora_verify_labels(trace: aurora_trace_t, cfg: aurora_loss_cfg_t, labels: aurora_labels_t, ws, ws_bytes: int,
+                         comm=None, stream=None) -> None:
+    _check("aurora_verify_labels", lib().aurora_verify_labels(C.byref(trace), C.byref(cfg), C.byref(labels),
+                                                              ws, ws_bytes, comm, _stream(stream)))
+
+
+def aurora_spec_loss_fwd(H, W, M, d, V_local, vocab_offset, labels, row_lse, row_loss, loss, ws, ws_bytes,
+                         comm=None, stream=None) -> None:
+    _check("aurora_spec_loss_fwd", lib().aurora_spec_loss_fwd(
+        _ptr(H), _ptr(W), M, d, V_local, vocab_offset, C.byref(labels), _ptr(row_lse), _ptr(row_loss), _ptr(loss),
+        ws, ws_bytes, comm, _stream(stream)))
+
+
+def aurora_spec_loss_bwd(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dW, dW_is_bf16,
+                         accumulate_dW, ws, ws_bytes, comm=None, stream=None) -> None:
+    _check("aurora_spec_loss_bwd", lib().aurora_spec_loss_bwd(
+        _ptr(H), _ptr(W), M, d, V_local, vocab_offset, C.byref(labels), _ptr(row_lse), _ptr(dloss), _ptr(dH),
+        _ptr(dW), int(dW_is_bf16), int(accumulate_dW), ws, ws_bytes, comm, _stream(stream)))
+
+
+def aurora_debug_gemm(a_mn: bool, b_mn: bool, A, B, D, M, N, K, lda, ldb, ldd, stream=None) -> None:
+    _check("aurora_debug_gemm", lib().aurora_debug_gemm(int(a_mn), int(b_mn), _ptr(A), _ptr(B), _ptr(D), M, N, K,
+                                                        lda, ldb, ldd, _stream(stream)))
+
+
+def aurora_launch_count() -> int:
+    return int(lib().aurora_launch_count())
+
+
+def aurora_build_info() -> str:
+    return lib().aurora_build_info().decode()
+
+
+def aurora_profile_enable(on: bool) -> None:
+    lib().aurora_profile_enable(1 if on else 0)
+
+
+def aurora_profile_read() -> dict:
+    n = 16
+    names = (C.c_char_p * n)()
+    ms = (C.c_float * n)()
+    cnt = (C.c_int32 * n)()
+    k = lib().aurora_profile_read(names, ms, cnt, n)
+    return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(k)}
+
+
+def aurora_comm_get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check("aurora_comm_get_unique_id", lib().aurora_comm_get_unique_id(buf))
+    return buf.raw
+
+
+def aurora_comm_create(uid: bytes, nranks: int, rank: int, vp_size: int, dp_size: int):
+    h = C.c_void_p()
+    buf = C.create_string_buffer(uid, 128)
+    _check("aurora_comm_create", lib().aurora_comm_create(buf, nranks, rank, vp_size, dp_size, C.byref(h)))
+    return h
+
+
+def aurora_comm_destroy(h) -> None:
+    _check("aurora_comm_destroy", lib().aurora_comm_destroy(h))
+
+
+# ----------------------------------------------------------- public step API
+class SpecTrainStep:
+    """Owns the label buffers and workspace for one trace-batch shape and runs
+    verify -> fwd -> bwd through the C-ABI on the current CUDA stream.
+
+    Shapes: R requests x N nodes (M = R(N+1) rows), hidden d, global vocab V, this
+    rank's vocab slice [vocab_offset, vocab_offset + V_local).
+    """
+
+    def __init__(self, R: int, N: int, d: int, V: int, V_local: Optional[int] = None, vocab_offset: int = 0,
+                 k_accept: int = 1, k_discard: int = 10, lambda_discard: float = 1.0, normalize: int = 0,
+                 discard_scope: int = 0, device="cuda", comm=None):
+        import torch
+        self.R, self.N, self.d, self.V = R, N, d, V
+        self.V_local = V if V_local is None else V_local
+        self.vocab_offset = vocab_offset
+        self.M = R * (N + 1)
+        self.comm = comm
+        self.cfg = aurora_loss_cfg_t(k_accept, k_discard, lambda_discard, normalize, discard_scope)
+        self.k_max = max(k_accept, k_discard)
+        dev = torch.device(device)
+        M, km = self.M, self.k_max
+        i32, u8, f32 = torch.int32, torch.uint8, torch.float32
+        self.target_argmax = torch.empty(M, dtype=i32, device=dev)
+        self.accepted = torch.empty(R, N, dtype=u8, device=dev)
+        self.accept_len = torch.empty(R, dtype=i32, device=dev)
+        self.bonus = torch.empty(R, dtype=i32, device=dev)
+        self.row_class = torch.empty(M, dtype=u8, device=dev)
+        self.sup_idx = torch.empty(M, km, dtype=i32, device=dev)
+        self.sup_p = torch.empty(M, km, dtype=f32, device=dev)
+        self.row_H = torch.empty(M, dtype=f32, device=dev)
+        self.row_w = torch.empty(M, dtype=f32, device=dev)
+        self.counts = torch.empty(2, dtype=i32, device=dev)
+        self.status = torch.zeros(1, dtype=i32, device=dev)
+        self.row_lse = torch.empty(M, dtype=f32, device=dev)
+        self.row_loss = torch.empty(M, dtype=f32, device=dev)
+        self.loss = torch.empty(1, dtype=f32, device=dev)
+        self.labels = aurora_labels_t(km, *(t.data_ptr() for t in (
+            self.target_argmax, self.accepted, self.accept_len, self.bonus, self.row_class, self.sup_idx,
+            self.sup_p, self.row_H, self.row_w, self.counts, self.status)))
+        self.ws_bytes = aurora_workspace_size(OP_ALL, M, d, self.V_local, self.cfg)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+
+    def verify(self, draft_tokens, target_logits, parents=None, num_nodes=None, stream=None):
+        t = aurora_trace_t(self.R, self.N, _ptr(draft_tokens), _ptr(parents), _ptr(num_nodes), _ptr(target_logits),
+                           target_logits.stride(0), self.V, self.V_local, self.vocab_offset)
+        aurora_verify_labels(t, self.cfg, self.labels, self.ws.data_ptr(), self.ws_bytes, self.comm, stream)
+
+    def forward(self, H, W, stream=None):
+        aurora_spec_loss_fwd(H, W, self.M, self.d, self.V_local, self.vocab_offset, self.labels, self.row_lse,
+                             self.row_loss, self.loss, self.ws.data_ptr(), self.ws_bytes, self.comm, stream)
+        return self.loss
+
+    def backward(self, H, W, dH, dW, dloss=None, accumulate_dW=False, stream=None):
+        aurora_spec_loss_bwd(H, W, self.M, self.d, self.V_local, self.vocab_offset, self.labels, self.row_lse,
+                             dloss, dH, dW, False, accumulate_dW, self.ws.data_ptr(), self.ws_bytes, self.comm,
+                             stream)
+
+    def step(self, draft_tokens, target_logits, H, W, dH, dW, parents=None, num_nodes=None, stream=None):
+        self.verify(draft_tokens, target_logits, parents, num_nodes, stream)
+        self.forward(H, W, stream)
+        self.backward(H, W, dH, dW, stream=stream)
+        return self.loss
+
+    def debug_dlogits_rows(self, H, W, rows, dloss=None, stream=None):
+        import torch
+        out = torch.empty(len(rows), self.V_local, dtype=torch.float32, device=H.device)
+        r = torch.as_tensor(rows, dtype=torch.int32, device=H.device)
+        _check("aurora_debug_dlogits_rows", lib().aurora_debug_dlogits_rows(
+            _ptr(H), _ptr(W), self.M, self.d, self.V_local, self.vocab_offset, C.byref(self.labels),
+            _ptr(self.row_lse), _ptr(dloss), _ptr(r), len(rows), _ptr(out), _stream(stream)))
+        return out

@@ -1,0 +1,628 @@
+// api.cu — the extern "C" boundary (include/aurora.h): validation, workspace carving,
+// tensor maps, kernel sequencing and the NCCL collectives of the VP/DP modes.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "internal.h"
+
+namespace aur {
+
+std::atomic<uint64_t> g_launches{0};
+
+// ------------------------------------------------------------------ profiling
+namespace {
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+struct ProfRec { int phase; cudaEvent_t a, b; };
+std::vector<ProfRec> g_prof_open, g_prof_done;
+std::vector<cudaEvent_t> g_ev_pool;
+cudaEvent_t ev_get() {
+  if (!g_ev_pool.empty()) { cudaEvent_t e = g_ev_pool.back(); g_ev_pool.pop_back(); return e; }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+const char* kPhaseNames[PH_COUNT] = {"target_scan", "verify", "fwd_gemm", "fwd_combine", "bwd_dz_gemm",
+                                     "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm"};
+}  // namespace
+
+void prof_begin(int phase, cudaStream_t s) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ProfRec r{phase, ev_get(), ev_get()};
+  cudaEventRecord(r.a, s);
+  g_prof_open.push_back(r);
+}
+void prof_end(int phase, cudaStream_t s) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (size_t i = g_prof_open.size(); i-- > 0;) {
+    if (g_prof_open[i].phase == phase) {
+      cudaEventRecord(g_prof_open[i].b, s);
+      g_prof_done.push_back(g_prof_open[i]);
+      g_prof_open.erase(g_prof_open.begin() + static_cast<long>(i));
+      return;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace nccl {
+typedef int Result;
+typedef void* Comm;
+struct UniqueId { char internal[128]; };
+enum { ncclInt32 = 2, ncclFloat32 = 7 };
+enum { ncclSum = 0 };
+struct Api {
+  bool ok = false;
+  Result (*GetUniqueId)(UniqueId*) = nullptr;
+  Result (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
+  Result (*CommDestroy)(Comm) = nullptr;
+  Result (*CommSplit)(Comm, int, int, Comm*, void*) = nullptr;
+  Result (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  Result (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
+};
+Api& api() {
+  static Api a;
+  static bool tried = false;
+  if (tried) return a;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return a;
+  a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+  a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+  a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+  a.CommSplit = reinterpret_cast<decltype(a.CommSplit)>(dlsym(h, "ncclCommSplit"));
+  a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+  a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+  a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.CommSplit && a.AllReduce && a.AllGather;
+  return a;
+}
+}  // namespace nccl
+
+}  // namespace aur
+
+struct aurora_comm_s {
+  int nranks, rank, vp_size, dp_size, vp_rank, dp_rank;
+  aur::nccl::Comm world = nullptr, vp = nullptr, dp = nullptr;
+  void* scratch = nullptr;  // comm-owned device scratch for gathered candidates / stats
+  size_t scratch_bytes = 0;
+};
+
+namespace aur {
+namespace {
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+aurora_status_t cuda_status(cudaError_t e) { return e == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA; }
+
+// ---- workspace layout: one carve routine used by both sizing and the calls
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(int64_t n) {
+    off = rup(static_cast<int64_t>(off), 256);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += static_cast<size_t>(n) * sizeof(T);
+    return p;
+  }
+};
+
+int scan_nseg(int64_t M, int64_t V_local) {
+  int64_t nseg = cdiv(8 * kNumSMs, std::max<int64_t>(M, 1));
+  nseg = std::min<int64_t>(nseg, 32);
+  nseg = std::min<int64_t>(nseg, cdiv(V_local, 2048));
+  return static_cast<int>(std::max<int64_t>(nseg, 1));
+}
+int64_t chunk_cols(int64_t V_local) {
+  if (V_local <= 4 * BN) return rup(V_local, BN);
+  return rup(cdiv(V_local, 4), BN);  // <= 1/4 of the local dLogits at any time
+}
+int dh_splits(int64_t M, int64_t d, int64_t kb_total) {
+  const int64_t tiles = cdiv(M, BM) * cdiv(d, BN);
+  int64_t s = cdiv(kNumSMs, tiles);
+  s = std::min<int64_t>(std::max<int64_t>(s, 1), 8);
+  s = std::min<int64_t>(s, kb_total);
+  if (s > 1) s = cdiv(kb_total, cdiv(kb_total, s));  // every split gets >= 1 k-block
+  return static_cast<int>(std::max<int64_t>(s, 1));
+}
+
+struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; };
+VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
+  const int nseg = scan_nseg(M, V_local);
+  VerifyWs w;
+  w.cand_val = c.take<float>(M * nseg * k_max);
+  w.cand_idx = c.take<int32_t>(M * nseg * k_max);
+  w.top_val = c.take<float>(M * k_max);
+  w.top_idx = c.take<int32_t>(M * k_max);
+  return w;
+}
+struct FwdWs { float *pm, *ps, *pu, *msu, *bp; int n_tiles; };
+FwdWs carve_fwd(Carver& c, int64_t M, int64_t V_local) {
+  FwdWs w;
+  w.n_tiles = static_cast<int>(cdiv(V_local, BN));
+  w.pm = c.take<float>(M * w.n_tiles);
+  w.ps = c.take<float>(M * w.n_tiles);
+  w.pu = c.take<float>(M * w.n_tiles);
+  w.msu = c.take<float>(M * 3);
+  w.bp = c.take<float>(cdiv(M, 256) + 1);
+  return w;
+}
+struct BwdWs { __nv_bfloat16* dzT; float* dh_part; int64_t vc, m_pad; int splits; };
+BwdWs carve_bwd(Carver& c, int64_t M, int64_t d, int64_t V_local) {
+  BwdWs w;
+  w.vc = chunk_cols(V_local);
+  w.m_pad = rup(M, 8);
+  w.dzT = c.take<__nv_bfloat16>(w.vc * w.m_pad);
+  w.splits = dh_splits(M, d, cdiv(w.vc, BK));
+  w.dh_part = w.splits > 1 ? c.take<float>(static_cast<int64_t>(w.splits) * M * d) : nullptr;
+  return w;
+}
+
+aurora_status_t check_cfg(const aurora_loss_cfg_t* cfg) {
+  if (!cfg) return AURORA_ERR_INVALID_ARG;
+  if (cfg->k_discard == 0) return AURORA_ERR_UNSUPPORTED;  // dense discard KL (NEXT F2)
+  if (cfg->k_accept < 1 || cfg->k_accept > AURORA_MAX_K || cfg->k_discard < 1 || cfg->k_discard > AURORA_MAX_K)
+    return AURORA_ERR_INVALID_ARG;
+  if (!(cfg->lambda_discard >= 0.f) || !std::isfinite(cfg->lambda_discard)) return AURORA_ERR_INVALID_ARG;
+  if (cfg->normalize != 0 && cfg->normalize != 1) return AURORA_ERR_INVALID_ARG;
+  if (cfg->discard_scope != 0 && cfg->discard_scope != 1) return AURORA_ERR_INVALID_ARG;
+  return AURORA_OK;
+}
+bool labels_ok(const aurora_labels_t* l, bool verify_outputs) {
+  if (!l) return false;
+  if (l->k_max < 1 || l->k_max > AURORA_MAX_K) return false;
+  if (!l->sup_idx || !l->sup_p || !l->row_H || !l->row_w || !l->row_class) return false;
+  if (verify_outputs && (!l->target_argmax || !l->accepted || !l->accept_len || !l->bonus || !l->counts ||
+                         !l->status))
+    return false;
+  return true;
+}
+// The comm owns a device scratch for gathered per-row data; it grows on first use
+// (one cudaMalloc per size increase, never in steady state).
+bool ensure_scratch(aurora_comm_t c, size_t bytes) {
+  if (c->scratch_bytes >= bytes) return true;
+  if (c->scratch) cudaFree(c->scratch);
+  c->scratch = nullptr;
+  c->scratch_bytes = 0;
+  if (cudaMalloc(&c->scratch, bytes) != cudaSuccess) return false;
+  c->scratch_bytes = bytes;
+  return true;
+}
+bool gemm_shape_ok(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local) {
+  return H && W && M >= 1 && d >= 64 && d % 64 == 0 && V_local >= 1 && al16(H) && al16(W) &&
+         M <= (int64_t(1) << 31) / 2 && V_local <= (int64_t(1) << 31) / 2;
+}
+
+}  // namespace
+}  // namespace aur
+
+using namespace aur;
+
+extern "C" {
+
+const char* aurora_status_string(aurora_status_t s) {
+  switch (s) {
+    case AURORA_OK: return "ok";
+    case AURORA_ERR_INVALID_ARG: return "invalid argument";
+    case AURORA_ERR_STRUCTURE: return "malformed draft tree (parents)";
+    case AURORA_ERR_RANGE: return "token id out of range";
+    case AURORA_ERR_NONFINITE: return "non-finite target logits";
+    case AURORA_ERR_UNSUPPORTED: return "unsupported configuration";
+    case AURORA_ERR_WORKSPACE: return "workspace missing or too small";
+    case AURORA_ERR_CUDA: return "CUDA error";
+    case AURORA_ERR_NCCL: return "NCCL error";
+  }
+  return "unknown status";
+}
+
+const char* aurora_build_info(void) {
+  return "libaurora abi=1 target=sm_100a engine=tcgen05.mma.cta_group::1.kind::f16 M128xN256xK16, TMA SW128 "
+         "4-stage ring, TMEM 2x256 cols; scan=16B ld.global.nc 8-deep";
+}
+
+uint64_t aurora_launch_count(void) { return g_launches.load(); }
+
+void aurora_profile_enable(int enable) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = enable != 0;
+}
+
+int aurora_profile_read(const char** names, float* total_ms, int32_t* count, int max) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  float tot[PH_COUNT] = {0};
+  int cnt[PH_COUNT] = {0};
+  for (auto& r : g_prof_done) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      tot[r.phase] += ms;
+      cnt[r.phase] += 1;
+    }
+    g_ev_pool.push_back(r.a);
+    g_ev_pool.push_back(r.b);
+  }
+  g_prof_done.clear();
+  int n = 0;
+  for (int p = 0; p < PH_COUNT && n < max; ++p) {
+    if (names) names[n] = kPhaseNames[p];
+    if (total_ms) total_ms[n] = tot[p];
+    if (count) count[n] = cnt[p];
+    ++n;
+  }
+  return n;
+}
+
+size_t aurora_workspace_size(int op, int64_t M, int64_t d, int64_t V_local, const aurora_loss_cfg_t* cfg) {
+  if (M < 1 || V_local < 1 || d < 1 || !cfg || op < 0 || op > 3) return 0;
+  const int k_max = std::max(cfg->k_accept, cfg->k_discard);
+  if (k_max < 1 || k_max > AURORA_MAX_K) return 0;
+  size_t best = 0;
+  if (op == AURORA_OP_VERIFY || op == AURORA_OP_ALL) {
+    Carver c(nullptr);
+    carve_verify(c, M, V_local, AURORA_MAX_K);
+    best = std::max(best, c.off);
+  }
+  if (op == AURORA_OP_FWD || op == AURORA_OP_ALL) {
+    Carver c(nullptr);
+    carve_fwd(c, M, V_local);
+    best = std::max(best, c.off);
+  }
+  if (op == AURORA_OP_BWD || op == AURORA_OP_ALL) {
+    Carver c(nullptr);
+    carve_bwd(c, M, d, V_local);
+    best = std::max(best, c.off);
+  }
+  return rup(static_cast<int64_t>(best), 256) + 256;
+}
+
+aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_cfg_t* cfg, aurora_labels_t* out,
+                                     void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream) {
+  if (!t || !out) return AURORA_ERR_INVALID_ARG;
+  aurora_status_t st = check_cfg(cfg);
+  if (st != AURORA_OK) return st;
+  if (t->R < 1 || t->N < 1 || t->N > AURORA_MAX_NODES || !t->draft_tokens || !t->target_logits) return AURORA_ERR_INVALID_ARG;
+  if (t->V < 1 || t->V_local < 1 || t->vocab_offset < 0 || t->vocab_offset + t->V_local > t->V ||
+      t->ld_target < t->V_local || t->V > INT32_MAX)
+    return AURORA_ERR_INVALID_ARG;
+  if (!labels_ok(out, true)) return AURORA_ERR_INVALID_ARG;
+  const int k_max = out->k_max;
+  if (k_max < std::max(cfg->k_accept, cfg->k_discard)) return AURORA_ERR_INVALID_ARG;
+  if (std::max(cfg->k_accept, cfg->k_discard) > t->V) return AURORA_ERR_INVALID_ARG;
+  const int64_t M = static_cast<int64_t>(t->R) * (t->N + 1);
+  if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->V_local, cfg)) return AURORA_ERR_WORKSPACE;
+  if (comm && comm->vp_size > 1 && t->V_local == t->V) return AURORA_ERR_INVALID_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  Carver c(ws);
+  VerifyWs w = carve_verify(c, M, t->V_local, k_max);
+  VerifyLaunch p{};
+  p.T = static_cast<const uint16_t*>(t->target_logits);
+  p.ldT = t->ld_target;
+  p.V_local = t->V_local;
+  p.vocab_offset = t->vocab_offset;
+  p.V = t->V;
+  p.M = static_cast<int32_t>(M);
+  p.R = t->R;
+  p.N = t->N;
+  p.k_max = k_max;
+  p.nseg = scan_nseg(M, t->V_local);
+  p.seg_len = rup(cdiv(t->V_local, p.nseg), 8);
+  p.draft = t->draft_tokens;
+  p.parents = t->parents;
+  p.num_nodes = t->num_nodes;
+  p.cand_val = w.cand_val;
+  p.cand_idx = w.cand_idx;
+  p.top_val = w.top_val;
+  p.top_idx = w.top_idx;
+  p.lab = *out;
+  p.cfg = *cfg;
+
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(out->counts, 0, 2 * sizeof(int32_t), s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  if ((e = cudaMemsetAsync(out->status, 0, sizeof(uint32_t), s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  prof_begin(PH_SCAN, s);
+  if ((e = launch_target_scan(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  if ((e = launch_topk_merge(p, w.cand_val, w.cand_idx, p.nseg, static_cast<int64_t>(p.nseg) * k_max, k_max, s)) !=
+      cudaSuccess)
+    return AURORA_ERR_CUDA;
+  prof_end(PH_SCAN, s);
+  if (comm && comm->vp_size > 1) {
+    // C1: gather every VP rank's (value-ordered) top list and merge in global order.
+    auto& A = nccl::api();
+    const size_t per = static_cast<size_t>(M) * k_max;
+    const size_t need = 2 * per * comm->vp_size * sizeof(float);
+    if (!ensure_scratch(comm, need)) return AURORA_ERR_CUDA;
+    float* gv = static_cast<float*>(comm->scratch);
+    int32_t* gi = reinterpret_cast<int32_t*>(gv + per * comm->vp_size);
+    prof_begin(PH_COMM, s);
+    if (A.AllGather(w.top_val, gv, per, nccl::ncclFloat32, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+    if (A.AllGather(w.top_idx, gi, per, nccl::ncclInt32, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+    prof_end(PH_COMM, s);
+    // gathered layout [rank][M][k]: list l of row m at l*M*k + m*k (global ids already)
+    if ((e = launch_topk_merge(p, gv, gi, comm->vp_size, k_max, static_cast<int64_t>(M) * k_max, s)) != cudaSuccess)
+      return AURORA_ERR_CUDA;
+  }
+  prof_begin(PH_VERIFY, s);
+  if ((e = launch_verify(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (comm && comm->dp_size > 1) {
+    auto& A = nccl::api();
+    if (A.AllReduce(out->counts, out->counts, 2, nccl::ncclInt32, nccl::ncclSum, comm->dp, s) != 0)
+      return AURORA_ERR_NCCL;
+  }
+  if ((e = launch_finalize(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  prof_end(PH_VERIFY, s);
+  return AURORA_OK;
+}
+
+aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
+                                     int64_t vocab_offset, const aurora_labels_t* labels, float* row_lse,
+                                     float* row_loss, float* loss, void* ws, size_t ws_bytes, aurora_comm_t comm,
+                                     void* stream) {
+  if (!gemm_shape_ok(H, W, M, d, V_local) || vocab_offset < 0) return AURORA_ERR_INVALID_ARG;
+  if (!labels_ok(labels, false) || !row_lse || !loss) return AURORA_ERR_INVALID_ARG;
+  aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
+  if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_FWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  FwdWs w = carve_fwd(c, M, V_local);
+
+  CUtensorMap tmH, tmW;
+  if (!make_tmap_bf16(&tmH, H, d, M, d, 64, BM)) return AURORA_ERR_CUDA;
+  if (!make_tmap_bf16(&tmW, W, d, V_local, d, 64, BN)) return AURORA_ERR_CUDA;
+  GemmArgs a{};
+  a.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+  a.n_tiles = w.n_tiles;
+  a.splits = 1;
+  a.kb_total = static_cast<int32_t>(d / BK);
+  a.kb_per_split = a.kb_total;
+  a.M = M;
+  a.N = V_local;
+  a.sup_idx = labels->sup_idx;
+  a.sup_p = labels->sup_p;
+  a.k_max = labels->k_max;
+  a.col_gid0 = vocab_offset;
+  a.p_max = w.pm;
+  a.p_sum = w.ps;
+  a.p_u = w.pu;
+  prof_begin(PH_FWD_GEMM, s);
+  cudaError_t e = launch_umma_gemm(EPI_FWD_STATS, false, false, tmH, tmW, a, s);
+  prof_end(PH_FWD_GEMM, s);
+  if (e != cudaSuccess) return AURORA_ERR_CUDA;
+  prof_begin(PH_FWD_COMBINE, s);
+  if ((e = launch_reduce_partials(w.pm, w.ps, w.pu, M, w.n_tiles, w.msu, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  const float* msu_all = w.msu;
+  int P = 1;
+  if (comm && comm->vp_size > 1) {
+    auto& A = nccl::api();
+    const size_t need = static_cast<size_t>(M) * 3 * comm->vp_size * sizeof(float);
+    if (!ensure_scratch(comm, need)) return AURORA_ERR_CUDA;
+    if (A.AllGather(w.msu, comm->scratch, static_cast<size_t>(M) * 3, nccl::ncclFloat32, comm->vp, s) != 0)
+      return AURORA_ERR_NCCL;
+    msu_all = static_cast<const float*>(comm->scratch);
+    P = comm->vp_size;
+  }
+  int nb = 0;
+  if ((e = launch_row_combine(msu_all, P, M, labels->row_H, labels->row_w, labels->row_class, row_lse, row_loss,
+                              w.bp, &nb, s)) != cudaSuccess)
+    return AURORA_ERR_CUDA;
+  if ((e = launch_loss_sum(w.bp, nb, loss, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (comm && comm->dp_size > 1) {
+    auto& A = nccl::api();
+    if (A.AllReduce(loss, loss, 1, nccl::ncclFloat32, nccl::ncclSum, comm->dp, s) != 0) return AURORA_ERR_NCCL;
+  }
+  prof_end(PH_FWD_COMBINE, s);
+  return AURORA_OK;
+}
+
+aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
+                                     int64_t vocab_offset, const aurora_labels_t* labels, const float* row_lse,
+                                     const float* dloss, float* dH, void* dW, int dW_is_bf16, int accumulate_dW,
+                                     void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream) {
+  if (!gemm_shape_ok(H, W, M, d, V_local) || vocab_offset < 0) return AURORA_ERR_INVALID_ARG;
+  if (!labels_ok(labels, false) || !row_lse || !dH || !dW || !al16(dH) || !al16(dW)) return AURORA_ERR_INVALID_ARG;
+  if (dW_is_bf16) return AURORA_ERR_UNSUPPORTED;
+  aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
+  if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  BwdWs w = carve_bwd(c, M, d, V_local);
+  float* dWf = static_cast<float*>(dW);
+
+  CUtensorMap tmH_k, tmH_mn;
+  if (!make_tmap_bf16(&tmH_k, H, d, M, d, 64, BM)) return AURORA_ERR_CUDA;
+  if (!make_tmap_bf16(&tmH_mn, H, d, M, d, 64, 64)) return AURORA_ERR_CUDA;
+  const int64_t nchunks = cdiv(V_local, w.vc);
+  const __nv_bfloat16* Wb = static_cast<const __nv_bfloat16*>(W);
+  for (int64_t ch = 0; ch < nchunks; ++ch) {
+    const int64_t c0 = ch * w.vc;
+    const int64_t vc = std::min(w.vc, V_local - c0);
+    CUtensorMap tmW_k, tmW_mn, tmZ_k, tmZ_mn;
+    if (!make_tmap_bf16(&tmW_k, Wb + c0 * d, d, vc, d, 64, BN)) return AURORA_ERR_CUDA;
+    if (!make_tmap_bf16(&tmW_mn, Wb + c0 * d, d, vc, d, 64, 64)) return AURORA_ERR_CUDA;
+    if (!make_tmap_bf16(&tmZ_k, w.dzT, M, vc, w.m_pad, 64, BM)) return AURORA_ERR_CUDA;
+    if (!make_tmap_bf16(&tmZ_mn, w.dzT, M, vc, w.m_pad, 64, 64)) return AURORA_ERR_CUDA;
+
+    // A7: recompute Z tiles, dz -> dZ^T chunk (bf16)
+    GemmArgs a{};
+    a.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+    a.n_tiles = static_cast<int32_t>(cdiv(vc, BN));
+    a.splits = 1;
+    a.kb_total = static_cast<int32_t>(d / BK);
+    a.kb_per_split = a.kb_total;
+    a.M = M;
+    a.N = vc;
+    a.sup_idx = labels->sup_idx;
+    a.sup_p = labels->sup_p;
+    a.k_max = labels->k_max;
+    a.col_gid0 = vocab_offset + c0;
+    a.row_lse = row_lse;
+    a.row_w = labels->row_w;
+    a.dloss = dloss;
+    a.dzT = w.dzT;
+    a.ld_dzT = w.m_pad;
+    prof_begin(PH_BWD_DZ, s);
+    cudaError_t e = launch_umma_gemm(EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s);
+    prof_end(PH_BWD_DZ, s);
+    if (e != cudaSuccess) return AURORA_ERR_CUDA;
+
+    // A8: dW[chunk] = dZ^T H   (A = dZ^T K-major, B = H MN-major, K = M)
+    GemmArgs b{};
+    b.m_tiles = static_cast<int32_t>(cdiv(vc, BM));
+    b.n_tiles = static_cast<int32_t>(cdiv(d, BN));
+    b.splits = 1;
+    b.kb_total = static_cast<int32_t>(cdiv(M, BK));
+    b.kb_per_split = b.kb_total;
+    b.M = vc;
+    b.N = d;
+    b.out = dWf + c0 * d;
+    b.ld_out = d;
+    b.accumulate = accumulate_dW ? 1 : 0;
+    prof_begin(PH_BWD_DW, s);
+    e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, s);
+    prof_end(PH_BWD_DW, s);
+    if (e != cudaSuccess) return AURORA_ERR_CUDA;
+
+    // A9: dH += dZ W[chunk]   (A = dZ^T as MN-major, B = W MN-major, K = vc)
+    GemmArgs h{};
+    h.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+    h.n_tiles = static_cast<int32_t>(cdiv(d, BN));
+    h.kb_total = static_cast<int32_t>(cdiv(vc, BK));
+    h.splits = w.splits > 1 ? std::min<int>(w.splits, h.kb_total) : 1;
+    h.kb_per_split = static_cast<int32_t>(cdiv(h.kb_total, h.splits));
+    h.splits = static_cast<int32_t>(cdiv(h.kb_total, h.kb_per_split));
+    h.M = M;
+    h.N = d;
+    h.ld_out = d;
+    if (h.splits > 1) {
+      h.out = w.dh_part;
+      h.split_stride = M * d;
+      h.accumulate = 0;
+    } else {
+      h.out = dH;
+      h.accumulate = ch > 0 ? 1 : 0;
+    }
+    prof_begin(PH_BWD_DH, s);
+    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, s);
+    prof_end(PH_BWD_DH, s);
+    if (e != cudaSuccess) return AURORA_ERR_CUDA;
+    if (h.splits > 1) {
+      prof_begin(PH_BWD_REDUCE, s);
+      e = launch_splitk_reduce(w.dh_part, h.splits, M * d, dH, ch > 0 ? 1 : 0, s);
+      prof_end(PH_BWD_REDUCE, s);
+      if (e != cudaSuccess) return AURORA_ERR_CUDA;
+    }
+    if (comm && comm->dp_size > 1) {  // C5: DP gradient allreduce of this dW chunk
+      auto& A = nccl::api();
+      prof_begin(PH_COMM, s);
+      if (A.AllReduce(dWf + c0 * d, dWf + c0 * d, static_cast<size_t>(vc * d), nccl::ncclFloat32, nccl::ncclSum,
+                      comm->dp, s) != 0)
+        return AURORA_ERR_NCCL;
+      prof_end(PH_COMM, s);
+    }
+  }
+  if (comm && comm->vp_size > 1) {  // C4: VP dH allreduce
+    auto& A = nccl::api();
+    prof_begin(PH_COMM, s);
+    if (A.AllReduce(dH, dH, static_cast<size_t>(M * d), nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0)
+      return AURORA_ERR_NCCL;
+    prof_end(PH_COMM, s);
+  }
+  return AURORA_OK;
+}
+
+aurora_status_t aurora_comm_get_unique_id(void* id_out) {
+  if (!id_out) return AURORA_ERR_INVALID_ARG;
+  auto& A = nccl::api();
+  if (!A.ok) return AURORA_ERR_NCCL;
+  nccl::UniqueId id;
+  if (A.GetUniqueId(&id) != 0) return AURORA_ERR_NCCL;
+  std::memcpy(id_out, &id, sizeof(id));
+  return AURORA_OK;
+}
+
+aurora_status_t aurora_comm_create(const void* id_in, int nranks, int rank, int vp_size, int dp_size,
+                                   aurora_comm_t* out) {
+  if (!id_in || !out || nranks < 1 || rank < 0 || rank >= nranks || vp_size < 1 || dp_size < 1 ||
+      vp_size * dp_size != nranks)
+    return AURORA_ERR_INVALID_ARG;
+  auto& A = nccl::api();
+  if (!A.ok) return AURORA_ERR_NCCL;
+  auto* c = new aurora_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->vp_size = vp_size;
+  c->dp_size = dp_size;
+  c->vp_rank = rank % vp_size;
+  c->dp_rank = rank / vp_size;
+  nccl::UniqueId id;
+  std::memcpy(&id, id_in, sizeof(id));
+  if (A.CommInitRank(&c->world, nranks, id, rank) != 0) { delete c; return AURORA_ERR_NCCL; }
+  if (A.CommSplit(c->world, c->dp_rank, c->vp_rank, &c->vp, nullptr) != 0 ||
+      A.CommSplit(c->world, c->vp_rank, c->dp_rank, &c->dp, nullptr) != 0) {
+    A.CommDestroy(c->world);
+    delete c;
+    return AURORA_ERR_NCCL;
+  }
+  *out = c;
+  return AURORA_OK;
+}
+
+aurora_status_t aurora_comm_destroy(aurora_comm_t c) {
+  if (!c) return AURORA_ERR_INVALID_ARG;
+  auto& A = nccl::api();
+  if (c->vp) A.CommDestroy(c->vp);
+  if (c->dp) A.CommDestroy(c->dp);
+  if (c->world) A.CommDestroy(c->world);
+  if (c->scratch) cudaFree(c->scratch);
+  delete c;
+  return AURORA_OK;
+}
+
+aurora_status_t aurora_debug_gemm(int a_mn, int b_mn, const void* A, const void* B, float* D, int64_t M, int64_t N,
+                                  int64_t K, int64_t lda, int64_t ldb, int64_t ldd, void* stream) {
+  if (!A || !B || !D || M < 1 || N < 1 || K < 1 || !al16(A) || !al16(B) || (lda * 2) % 16 || (ldb * 2) % 16)
+    return AURORA_ERR_INVALID_ARG;
+  if (ldd < N || lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return AURORA_ERR_INVALID_ARG;
+  CUtensorMap ta, tb;
+  bool ok = a_mn ? make_tmap_bf16(&ta, A, M, K, lda, 64, 64) : make_tmap_bf16(&ta, A, K, M, lda, 64, BM);
+  ok = ok && (b_mn ? make_tmap_bf16(&tb, B, N, K, ldb, 64, 64) : make_tmap_bf16(&tb, B, K, N, ldb, 64, BN));
+  if (!ok) return AURORA_ERR_CUDA;
+  GemmArgs g{};
+  g.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+  g.n_tiles = static_cast<int32_t>(cdiv(N, BN));
+  g.splits = 1;
+  g.kb_total = static_cast<int32_t>(cdiv(K, BK));
+  g.kb_per_split = g.kb_total;
+  g.M = M;
+  g.N = N;
+  g.out = D;
+  g.ld_out = ldd;
+  return cuda_status(launch_umma_gemm(EPI_STORE_F32, a_mn != 0, b_mn != 0, ta, tb, g,
+                                      static_cast<cudaStream_t>(stream)));
+}
+
+aurora_status_t aurora_debug_dlogits_rows(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
+                                          int64_t vocab_offset, const aurora_labels_t* labels, const float* row_lse,
+                                          const float* dloss, const int32_t* rows, int32_t n_rows, float* out,
+                                          void* stream) {
+  if (!H || !W || !labels || !row_lse || !rows || !out || n_rows < 1 || n_rows > 65535 || M < 1 || d < 1 ||
+      V_local < 1)
+    return AURORA_ERR_INVALID_ARG;
+  return cuda_status(launch_debug_dlogits(static_cast<const __nv_bfloat16*>(H), static_cast<const __nv_bfloat16*>(W),
+                                          M, d, V_local, vocab_offset, labels, row_lse, dloss, rows, n_rows, out,
+                                          static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

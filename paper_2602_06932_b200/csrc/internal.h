@@ -1,0 +1,107 @@
+// internal.h — host-side declarations shared by the library's translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "../../include/aurora.h"
+
+namespace aur {
+
+constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------- GEMM engine
+constexpr int BM = 128;  // tile rows (TMEM lanes)
+constexpr int BN = 256;  // tile cols (TMEM columns per accumulator)
+constexpr int BK = 64;   // K per pipeline stage (128 B of bf16 = one SW128 atom row)
+constexpr int kStages = 4;
+constexpr int kGemmThreads = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int kSmemA = BM * BK * 2;
+constexpr int kSmemB = BN * BK * 2;
+constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 256 /*barriers*/;
+
+enum EpiKind : int { EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2 };
+
+struct GemmArgs {
+  int32_t m_tiles, n_tiles, splits;
+  int32_t kb_total, kb_per_split;
+  int64_t M, N;  // valid extent of the GEMM output
+  // ---- EPI_STORE_F32
+  float* out;
+  int64_t ld_out;
+  int64_t split_stride;  // elements between split partial buffers
+  int32_t accumulate;
+  // ---- row-stat epilogues (fwd stats / bwd dz)
+  const int32_t* sup_idx;  // [M, k_max] global ids, ascending, INT32_MAX padded
+  const float* sup_p;
+  int32_t k_max;
+  int64_t col_gid0;  // global vocab id of GEMM column 0
+  float* p_max;      // [M, n_tiles] partial stats (fwd)
+  float* p_sum;
+  float* p_u;
+  const float* row_lse;  // bwd
+  const float* row_w;
+  const float* dloss;    // nullable => 1
+  __nv_bfloat16* dzT;    // [N_chunk, ld_dzT] transposed dLogits chunk (bwd)
+  int64_t ld_dzT;
+};
+
+// Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.
+cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                             const GemmArgs& args, cudaStream_t stream);
+
+// 2D bf16 tensor map (SWIZZLE_128B) over a row-major [outer, inner] matrix with row
+// stride `ld` elements; box = {box_inner, box_outer}.
+bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                    uint32_t box_inner, uint32_t box_outer);
+
+// ---------------------------------------------------------------- verify kernels
+struct VerifyLaunch {
+  const uint16_t* T;
+  int64_t ldT, V_local, vocab_offset, V;
+  int32_t M, R, N, k_max, nseg;
+  int64_t seg_len;
+  const int32_t* draft;
+  const int32_t* parents;
+  const int32_t* num_nodes;
+  float* cand_val;      // [M, nseg, k_max]
+  int32_t* cand_idx;
+  float* top_val;       // [M, k_max] merged (value order)
+  int32_t* top_idx;
+  aurora_labels_t lab;
+  aurora_loss_cfg_t cfg;
+};
+cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s);
+cudaError_t launch_topk_merge(const VerifyLaunch& p, const float* in_val, const int32_t* in_idx, int nlists,
+                              int64_t row_stride, int64_t list_stride, cudaStream_t s);
+cudaError_t launch_verify(const VerifyLaunch& p, cudaStream_t s);
+cudaError_t launch_finalize(const VerifyLaunch& p, cudaStream_t s);
+
+// ---------------------------------------------------------------- row kernels
+cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, int64_t M, int n_tiles,
+                                   float* msu /*[M,3]*/, cudaStream_t s);
+cudaError_t launch_row_combine(const float* msu_all /*[P,M,3]*/, int P, int64_t M, const float* row_H,
+                               const float* row_w, const uint8_t* row_class, float* row_lse, float* row_loss,
+                               float* block_partials, int* nblocks_out, cudaStream_t s);
+cudaError_t launch_loss_sum(const float* block_partials, int nblocks, float* loss, cudaStream_t s);
+cudaError_t launch_splitk_reduce(const float* partials, int splits, int64_t n_elems, float* out, int accumulate,
+                                 cudaStream_t s);
+cudaError_t launch_debug_dlogits(const __nv_bfloat16* H, const __nv_bfloat16* W, int64_t M, int64_t d,
+                                 int64_t V_local, int64_t vocab_offset, const aurora_labels_t* lab,
+                                 const float* row_lse, const float* dloss, const int32_t* rows, int n_rows,
+                                 float* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- accounting
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Phase profiling (CUDA events on the caller's stream).
+enum Phase : int { PH_SCAN = 0, PH_VERIFY, PH_FWD_GEMM, PH_FWD_COMBINE, PH_BWD_DZ, PH_BWD_DW, PH_BWD_DH,
+                   PH_BWD_REDUCE, PH_COMM, PH_COUNT };
+void prof_begin(int phase, cudaStream_t s);
+void prof_end(int phase, cudaStream_t s);
+
+}  // namespace aur

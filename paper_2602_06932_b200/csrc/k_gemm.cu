@@ -1,0 +1,404 @@
+// k_gemm.cu — persistent warp-specialised tcgen05 GEMM engine for the lm_head phases.
+//
+// One CTA per SM (192 threads):
+//   warp 0      TMA producer: 4-stage ring of {A 128x64, B 256x64} bf16 tiles, SW128
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes 32*(w%4)..)
+// Two 128x256 fp32 accumulators (512 TMEM columns) let the epilogue of tile i overlap
+// the MMAs of tile i+1.  Tiles are visited m-fastest, so all row tiles of one vocab
+// tile run back to back and W (the large operand) is streamed from HBM once per phase.
+//
+// Epilogues (the fused hot ops of SURVEY §8(a)):
+//   EPI_FWD_STATS  A5: per (row, vocab tile) running max m, sum exp(z-m) and the
+//                  support dot u = sum_{j in S} p~_j z_j  (Eq. 3).
+//                  Z never leaves TMEM.
+//   EPI_BWD_DZ     A7: dz = g w (exp(z - lse) - p~) (gradient of KL(p~||q)),
+//                  rounded to bf16 and stored TRANSPOSED into the chunk workspace
+//                  dZ^T[v, m] (coalesced: a warp store covers 32 consecutive rows).
+//   EPI_STORE_F32  A8/A9: fp32 tile store (overwrite / accumulate / split-K slot).
+#include <cfloat>
+#include <climits>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace aur {
+
+namespace {
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t tile_base, int k) {
+  // K-major SW128: rows of 128 B (64 bf16 of K), 8-row atoms 1024 B apart (SBO);
+  //   advancing K by 16 elements moves the start address by 32 B inside the atom.
+  // MN-major SW128: 64-element MN slices of [BK rows x 128 B] (8 KB, LBO) ;
+  //   8-row K groups 1024 B apart (SBO); advancing K by 16 rows = 2048 B.
+  if constexpr (MN) {
+    return umma_desc_sw128(tile_base + static_cast<uint32_t>(k) * 2048u, BK * 128u, 1024u);
+  } else {
+    return umma_desc_sw128(tile_base + static_cast<uint32_t>(k) * 32u, 16u, 1024u);
+  }
+}
+
+__device__ __forceinline__ float select32(const float (&z)[32], int j) {
+  float v = 0.f;
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) v = (jj == j) ? z[jj] : v;
+  return v;
+}
+
+struct SupCursor {
+  const int32_t* idx;
+  const float* p;
+  int k;
+  int pos;
+  int64_t nxt;  // local GEMM column of the next support entry (INT64_MAX = none)
+  float nxt_p;
+  int64_t limit;  // valid columns (entries at/after limit are ignored)
+  int64_t gid0;
+  __device__ __forceinline__ void load() {
+    nxt = INT64_MAX;
+    nxt_p = 0.f;
+    while (pos < k) {
+      const int32_t g = idx[pos];
+      if (g == INT32_MAX) { pos = k; break; }
+      const int64_t loc = static_cast<int64_t>(g) - gid0;
+      if (loc >= limit) { pos = k; break; }
+      nxt = loc;
+      nxt_p = p[pos];
+      return;
+    }
+  }
+  // position on the first entry with local column >= col0
+  __device__ __forceinline__ void seek(int64_t col0) {
+    pos = 0;
+    while (pos < k) {
+      const int32_t g = idx[pos];
+      if (g == INT32_MAX) { pos = k; break; }
+      if (static_cast<int64_t>(g) - gid0 >= col0) break;
+      ++pos;
+    }
+    load();
+  }
+  __device__ __forceinline__ void advance() {
+    ++pos;
+    load();
+  }
+};
+}  // namespace
+
+template <int EPI, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GemmArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kSmemA;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sB + kStages * kSmemB);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int units = args.m_tiles * args.n_tiles * args.splits;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int mt = u % args.m_tiles;
+        const int rest = u / args.m_tiles;
+        const int nt = rest % args.n_tiles;
+        const int sp = rest / args.n_tiles;
+        const int kb0 = sp * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full_bar[stage], kSmemA + kSmemB);
+          uint8_t* a = sA + stage * kSmemA;
+          uint8_t* b = sB + stage * kSmemB;
+          if constexpr (!A_MN) {
+            tma_load_2d(&tmA, &full_bar[stage], a, kb * BK, mt * BM);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BM / 64; ++i)
+              tma_load_2d(&tmA, &full_bar[stage], a + i * (BK * 128), mt * BM + i * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(&tmB, &full_bar[stage], b, kb * BK, nt * BN);
+          } else {
+#pragma unroll
+            for (int i = 0; i < BN / 64; ++i)
+              tma_load_2d(&tmB, &full_bar[stage], b + i * (BK * 128), nt * BN + i * 64, kb * BK);
+          }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int rest = u / args.m_tiles;
+        const int sp = rest / args.n_tiles;
+        const int kb0 = sp * args.kb_per_split;
+        const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * kSmemA);
+          const uint32_t b_base = smem_u32(sB + stage * kSmemB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            umma_bf16(d_tmem, operand_desc<A_MN>(a_base, k), operand_desc<B_MN>(b_base, k), idesc,
+                      (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull_bar[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    uint32_t acc = 0, acc_phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int mt = u % args.m_tiles;
+      const int rest = u / args.m_tiles;
+      const int nt = rest % args.n_tiles;
+      const int sp = rest / args.n_tiles;
+      const int64_t row = static_cast<int64_t>(mt) * BM + q * 32 + lane;
+      const bool row_ok = row < args.M;
+      const int64_t col0 = static_cast<int64_t>(nt) * BN;
+      const int64_t rem = args.N - col0;
+      const int ncols = rem < BN ? static_cast<int>(rem) : BN;
+
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+
+      if constexpr (EPI == EPI_FWD_STATS || EPI == EPI_BWD_DZ) {
+        SupCursor cur;
+        cur.idx = args.sup_idx + (row_ok ? row : 0) * args.k_max;
+        cur.p = args.sup_p + (row_ok ? row : 0) * args.k_max;
+        cur.k = row_ok ? args.k_max : 0;
+        cur.limit = args.N;
+        cur.gid0 = args.col_gid0;
+        cur.seek(col0);
+        float mrun = -INFINITY, srun = 0.f, usum = 0.f;
+        float coef = 0.f, lse2 = 0.f;
+        if constexpr (EPI == EPI_BWD_DZ) {
+          if (row_ok) {
+            const float g = args.dloss ? __ldg(args.dloss) : 1.f;
+            coef = g * __ldg(args.row_w + row);
+            lse2 = __ldg(args.row_lse + row) * kLog2e;
+          }
+        }
+        for (int c = 0; c < BN / 32; ++c) {
+          const int cb = c * 32;
+          if (cb >= ncols) break;  // warp-uniform
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + cb, r);
+          tmem_ld_wait();
+          float z[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(r[j]);
+          const bool full = (cb + 32 <= ncols);
+          if constexpr (EPI == EPI_FWD_STATS) {
+            if (!full) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) z[j] = (cb + j < ncols) ? z[j] : -INFINITY;
+            }
+            float cmax = z[0];
+#pragma unroll
+            for (int j = 1; j < 32; ++j) cmax = fmaxf(cmax, z[j]);
+            const float mnew = fmaxf(mrun, cmax);
+            const float mb = mnew * kLog2e;
+            srun *= ex2_approx(mrun * kLog2e - mb);
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              s0 += ex2_approx(fmaf(z[j], kLog2e, -mb));
+              s1 += ex2_approx(fmaf(z[j + 1], kLog2e, -mb));
+            }
+            srun += s0 + s1;
+            mrun = mnew;
+            while (cur.nxt < col0 + cb + 32) {
+              usum = fmaf(cur.nxt_p, select32(z, static_cast<int>(cur.nxt - col0 - cb)), usum);
+              cur.advance();
+            }
+          } else {
+            float dz[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) dz[j] = coef * ex2_approx(fmaf(z[j], kLog2e, -lse2));
+            while (cur.nxt < col0 + cb + 32) {
+              const int jj = static_cast<int>(cur.nxt - col0 - cb);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) dz[j] = (j == jj) ? dz[j] - coef * cur.nxt_p : dz[j];
+              cur.advance();
+            }
+            if (row_ok) {
+              __nv_bfloat16* dst = args.dzT + (col0 + cb) * args.ld_dzT + row;
+              if (full) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) dst[j * args.ld_dzT] = __float2bfloat16_rn(dz[j]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (cb + j < ncols) dst[j * args.ld_dzT] = __float2bfloat16_rn(dz[j]);
+              }
+            }
+          }
+        }
+        if constexpr (EPI == EPI_FWD_STATS) {
+          if (row_ok) {
+            const int64_t o = row * args.n_tiles + nt;
+            args.p_max[o] = mrun;
+            args.p_sum[o] = srun;
+            args.p_u[o] = usum;
+          }
+        }
+      } else {  // EPI_STORE_F32
+        float* base = args.out + static_cast<int64_t>(sp) * args.split_stride + row * args.ld_out + col0;
+        const bool vec_ok = ((args.ld_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
+        for (int c = 0; c < BN / 32; ++c) {
+          const int cb = c * 32;
+          if (cb >= ncols) break;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + cb, r);
+          tmem_ld_wait();
+          if (!row_ok) continue;
+          float* dst = base + cb;
+          if (cb + 32 <= ncols && vec_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                     __uint_as_float(r[j + 3]));
+              if (args.accumulate) {
+                const float4 o = *reinterpret_cast<const float4*>(dst + j);
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              }
+              *reinterpret_cast<float4*>(dst + j) = v;
+            }
+          } else {
+            for (int j = 0; j < 32 && cb + j < ncols; ++j) {
+              const float v = __uint_as_float(r[j]);
+              dst[j] = args.accumulate ? dst[j] + v : v;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+namespace {
+template <int EPI, bool A_MN, bool B_MN>
+cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, cudaStream_t s) {
+  static bool attr_set = false;
+  auto kern = k_umma_gemm<EPI, A_MN, B_MN>;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int units = args.m_tiles * args.n_tiles * args.splits;
+  if (units <= 0) return cudaSuccess;
+  const int grid = units < kNumSMs ? units : kNumSMs;
+  kern<<<grid, kGemmThreads, kGemmSmem, s>>>(tmA, tmB, args);
+  count_launch();
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                             const GemmArgs& args, cudaStream_t s) {
+  if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false>(tmA, tmB, args, s);
+  if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false>(tmA, tmB, args, s);
+  if (epi == EPI_STORE_F32) {
+    if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false>(tmA, tmB, args, s);
+    if (!a_mn && b_mn) return launch_impl<EPI_STORE_F32, false, true>(tmA, tmB, args, s);
+    if (a_mn && !b_mn) return launch_impl<EPI_STORE_F32, true, false>(tmA, tmB, args, s);
+    return launch_impl<EPI_STORE_F32, true, true>(tmA, tmB, args, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------ tensor maps
+namespace {
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                    uint32_t box_inner, uint32_t box_outer) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace aur

@@ -1,0 +1,176 @@
+// k_rows.cu — per-row statistic reductions and small helpers.
+//
+//   k_reduce_partials  warp per row: merge the (m, s, u) partials of all vocab tiles of
+//                      a row (coalesced: partials are [M, n_tiles] row-major) with the
+//                      online rule s = s e^{m-m'} + s_t e^{m_t-m'}; fixed shuffle order
+//                      => deterministic.
+//   k_row_combine      thread per row: merge the per-rank (m, s, u) in rank order (VP),
+//                      lse = m + log s, l = lse - u + H~ = KL(p~ || q) (Eq. 3), w l,
+//                      block-ordered partial sums.
+//   k_loss_sum         one block: ordered sum of the block partials -> loss.
+//   k_splitk_reduce    dH = (acc ? dH : 0) + sum_s partial[s], ordered (deterministic).
+#include <cfloat>
+#include <climits>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace aur {
+
+namespace {
+__device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2) {
+  const float mn = fmaxf(m, m2);
+  if (mn == -INFINITY) return;
+  s = s * __expf(m - mn) + s2 * __expf(m2 - mn);
+  m = mn;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict__ pm, const float* __restrict__ ps,
+                                                         const float* __restrict__ pu, int64_t M, int n_tiles,
+                                                         float* __restrict__ msu) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  float m = -INFINITY, s = 0.f, u = 0.f;
+  const int64_t o = row * n_tiles;
+  for (int t = lane; t < n_tiles; t += 32) {
+    ms_merge(m, s, __ldg(pm + o + t), __ldg(ps + o + t));
+    u += __ldg(pu + o + t);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    const float u2 = __shfl_xor_sync(0xffffffffu, u, off);
+    ms_merge(m, s, m2, s2);
+    u += u2;
+  }
+  if (lane == 0) {
+    msu[row * 3 + 0] = m;
+    msu[row * 3 + 1] = s;
+    msu[row * 3 + 2] = u;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_row_combine(const float* __restrict__ msu_all, int P, int64_t M,
+                                                     const float* __restrict__ row_H, const float* __restrict__ row_w,
+                                                     const uint8_t* __restrict__ row_class, float* __restrict__ row_lse,
+                                                     float* __restrict__ row_loss, float* __restrict__ block_partials) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  float wl = 0.f;
+  if (row < M) {
+    float m = -INFINITY, s = 0.f, u = 0.f;
+    for (int r = 0; r < P; ++r) {
+      const float* q = msu_all + (static_cast<int64_t>(r) * M + row) * 3;
+      ms_merge(m, s, q[0], q[1]);
+      u += q[2];
+    }
+    const float lse = m + logf(s);
+    const bool pad = row_class[row] == AURORA_ROW_PAD;
+    const float l = pad ? 0.f : (lse - u + row_H[row]);
+    row_lse[row] = lse;
+    if (row_loss) row_loss[row] = l;
+    wl = row_w[row] * l;
+  }
+  // deterministic block tree reduction
+  __shared__ float red[256];
+  red[threadIdx.x] = wl;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_partials[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(256) k_loss_sum(const float* __restrict__ bp, int nb, float* __restrict__ loss) {
+  __shared__ float red[256];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < nb; i += 256) acc += bp[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss[0] = red[0];
+}
+
+__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ part, int splits, int64_t n4,
+                                                       float* __restrict__ out, int accumulate) {
+  const int64_t stride = n4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * 256) {
+    float4 a = accumulate ? reinterpret_cast<const float4*>(out)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < splits; ++s) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(part) + s * stride + i);
+      a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    }
+    reinterpret_cast<float4*>(out)[i] = a;
+  }
+}
+
+// Test hook: full dz rows (SIMT, fp32 dot products from bf16).
+__global__ void k_debug_dlogits(const __nv_bfloat16* __restrict__ H, const __nv_bfloat16* __restrict__ W, int64_t d,
+                                int64_t V_local, int64_t vocab_offset, aurora_labels_t lab, const float* row_lse,
+                                const float* dloss, const int32_t* rows, float* out) {
+  const int r = blockIdx.y;
+  const int64_t m = rows[r];
+  const float g = dloss ? dloss[0] : 1.f;
+  const float coef = g * lab.row_w[m];
+  const float lse = row_lse[m];
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < V_local;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float z = 0.f;
+    for (int64_t k = 0; k < d; ++k)
+      z += __bfloat162float(H[m * d + k]) * __bfloat162float(W[v * d + k]);
+    float dz = coef * expf(z - lse);
+    for (int j = 0; j < lab.k_max; ++j)
+      if (static_cast<int64_t>(lab.sup_idx[m * lab.k_max + j]) == v + vocab_offset)
+        dz -= coef * lab.sup_p[m * lab.k_max + j];
+    out[r * V_local + v] = dz;
+  }
+}
+
+cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, int64_t M, int n_tiles,
+                                   float* msu, cudaStream_t s) {
+  k_reduce_partials<<<static_cast<unsigned>((M + 7) / 8), 256, 0, s>>>(pm, ps, pu, M, n_tiles, msu);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_row_combine(const float* msu_all, int P, int64_t M, const float* row_H, const float* row_w,
+                               const uint8_t* row_class, float* row_lse, float* row_loss, float* block_partials,
+                               int* nblocks_out, cudaStream_t s) {
+  const int nb = static_cast<int>((M + 255) / 256);
+  k_row_combine<<<nb, 256, 0, s>>>(msu_all, P, M, row_H, row_w, row_class, row_lse, row_loss, block_partials);
+  count_launch();
+  *nblocks_out = nb;
+  return cudaGetLastError();
+}
+cudaError_t launch_loss_sum(const float* bp, int nb, float* loss, cudaStream_t s) {
+  k_loss_sum<<<1, 256, 0, s>>>(bp, nb, loss);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_splitk_reduce(const float* partials, int splits, int64_t n_elems, float* out, int accumulate,
+                                 cudaStream_t s) {
+  const int64_t n4 = n_elems / 4;
+  int64_t blocks = (n4 + 255) / 256;
+  if (blocks > 4 * kNumSMs) blocks = 4 * kNumSMs;
+  k_splitk_reduce<<<static_cast<unsigned>(blocks), 256, 0, s>>>(partials, splits, n4, out, accumulate);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_debug_dlogits(const __nv_bfloat16* H, const __nv_bfloat16* W, int64_t M, int64_t d,
+                                 int64_t V_local, int64_t vocab_offset, const aurora_labels_t* lab,
+                                 const float* row_lse, const float* dloss, const int32_t* rows, int n_rows,
+                                 float* out, cudaStream_t s) {
+  (void)M;
+  dim3 grid(64, n_rows);
+  k_debug_dlogits<<<grid, 256, 0, s>>>(H, W, d, V_local, vocab_offset, *lab, row_lse, dloss, rows, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace aur

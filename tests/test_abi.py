@@ -1,0 +1,85 @@
+"""C-ABI library loads and exports every symbol include/aurora.h declares; host-side
+validation returns the documented status without touching a GPU (-m "not gpu")."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2602_06932_b200 import aurora as A
+from paper_2602_06932_b200.build import build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    build()
+    return A.lib()
+
+
+def _declared_symbols():
+    hdr = open(os.path.join(ROOT, "include", "aurora.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(aurora_[a-z_]+)\s*\(", hdr)))
+
+
+def test_exports_every_declared_symbol(L):
+    declared = _declared_symbols()
+    assert len(declared) >= 12
+    assert sorted(A.EXPORTS) == declared
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_status_strings_and_build_info(L):
+    for s in range(9):
+        assert L.aurora_status_string(s)
+    assert b"sm_100a" in L.aurora_build_info()
+
+
+def test_workspace_size_monotone(L):
+    cfg = A.aurora_loss_cfg_t(1, 10, 1.0, 0, 0)
+    small = A.aurora_workspace_size(A.OP_ALL, 20, 64, 1000, cfg)
+    big = A.aurora_workspace_size(A.OP_ALL, 384, 4096, 128256, cfg)
+    assert 0 < small < big
+    assert A.aurora_workspace_size(A.OP_ALL, 0, 64, 1000, cfg) == 0
+    # bwd dLogits chunk never exceeds a quarter of the local [M x V] (+ alignment)
+    bwd = A.aurora_workspace_size(A.OP_BWD, 384, 4096, 128256, cfg)
+    assert bwd < 384 * 128256 * 2 / 4 + 8 * 384 * 4096 * 4 + (1 << 20)
+
+
+def test_host_validation_without_gpu(L):
+    cfg = A.aurora_loss_cfg_t(1, 10, 1.0, 0, 0)
+    lab = A.aurora_labels_t()
+    # NULL trace -> invalid arg, nothing enqueued (no CUDA call happens)
+    assert L.aurora_verify_labels(None, C.byref(cfg), C.byref(lab), None, 0, None, None) == 1
+    # k_discard = 0 (paper's unfiltered top-k 0) -> unsupported in this build
+    cfg0 = A.aurora_loss_cfg_t(1, 0, 1.0, 0, 0)
+    t = A.aurora_trace_t(4, 4, 16, 0, 0, 16, 1000, 1000, 1000, 0)
+    assert L.aurora_verify_labels(C.byref(t), C.byref(cfg0), C.byref(lab), None, 0, None, None) == 5
+    # N > 32
+    t2 = A.aurora_trace_t(4, 33, 16, 0, 0, 16, 1000, 1000, 1000, 0)
+    assert L.aurora_verify_labels(C.byref(t2), C.byref(cfg), C.byref(lab), None, 0, None, None) == 1
+    # fwd with d not a multiple of 64
+    assert L.aurora_spec_loss_fwd(16, 16, 20, 100, 1000, 0, C.byref(lab), 16, None, 16, None, 0, None, None) == 1
+    # bf16 dW output is declared but unsupported in this build
+    lab2 = A.aurora_labels_t(10, 16, 16, 16, 16, 16, 16, 16, 16, 16, 16, 16)
+    assert L.aurora_spec_loss_bwd(16, 16, 20, 64, 1000, 0, C.byref(lab2), 16, None, 16, 16, 1, 0, 16, 1 << 30,
+                                  None, None) == 5
+    # missing workspace
+    assert L.aurora_spec_loss_fwd(16, 16, 20, 64, 1000, 0, C.byref(lab2), 16, None, 16, None, 0, None, None) == 6
+    # comm argument validation
+    h = C.c_void_p()
+    assert L.aurora_comm_create(None, 2, 0, 1, 2, C.byref(h)) == 1
+    assert L.aurora_comm_create(C.create_string_buffer(128), 2, 0, 3, 1, C.byref(h)) == 1
+
+
+def test_no_cpu_fallback_in_product():
+    """The product package never imports the oracle."""
+    pkg = os.path.join(ROOT, "paper_2602_06932_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith(".py"):
+                src = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f

@@ -1,0 +1,276 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the f64 oracle on identical
+seeded traces (-m gpu).  Tolerances (BASELINE.json north_star): labels and
+accept lengths bit-exact; loss within 1e-3 relative; dW and dH within 2e-2
+relative Frobenius error.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import tracegen
+from paper_2602_06932_b200 import aurora as A
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-3
+GRAD_RFRO = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    A.lib()
+
+
+def _bf16(bits: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def _to_gpu(tr):
+    g = dict(T=_bf16(tr["T_bits"]), H=_bf16(tr["H_bits"]), W=_bf16(tr["W_bits"]),
+             draft=torch.from_numpy(tr["draft_tokens"]).cuda())
+    g["parents"] = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).cuda()
+    g["num_nodes"] = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).cuda()
+    return g
+
+
+def _run_gpu(tr, want_grads=True, **kw):
+    c = tr["cfg"]
+    g = _to_gpu(tr)
+    st = A.SpecTrainStep(c.R, c.N, c.d, c.V, **kw)
+    st.verify(g["draft"], g["T"], g["parents"], g["num_nodes"])
+    st.forward(g["H"], g["W"])
+    out = dict(st=st, g=g)
+    if want_grads:
+        dH = torch.empty(c.M, c.d, dtype=torch.float32, device="cuda")
+        dW = torch.empty(c.V, c.d, dtype=torch.float32, device="cuda")
+        st.backward(g["H"], g["W"], dH, dW)
+        out["dH"], out["dW"] = dH, dW
+    torch.cuda.synchronize()
+    return out
+
+
+def _rfro(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _check_labels(st, ref, tr, k_accept=1, k_discard=10):
+    assert int(st.status.item()) == 0
+    np.testing.assert_array_equal(st.target_argmax.cpu().numpy(), ref["argmax"])
+    np.testing.assert_array_equal(st.accepted.cpu().numpy(), ref["accepted"])
+    np.testing.assert_array_equal(st.accept_len.cpu().numpy(), ref["accept_len"])
+    np.testing.assert_array_equal(st.bonus.cpu().numpy(), ref["bonus"])
+    np.testing.assert_array_equal(st.row_class.cpu().numpy(), ref["row_class"])
+    tg = ref["targets"]
+    assert tuple(st.counts.cpu().tolist()) == tuple(tg["counts"])
+    sup = st.sup_idx.cpu().numpy()
+    sp = st.sup_p.cpu().numpy()
+    w = st.row_w.cpu().numpy()
+    Hh = st.row_H.cpu().numpy()
+    for m in range(tr["M"]):
+        k = len(tg["sup_idx"][m])
+        np.testing.assert_array_equal(sup[m, :k], tg["sup_idx"][m])
+        assert (sup[m, k:] == np.iinfo(np.int32).max).all()
+        np.testing.assert_allclose(sp[m, :k], tg["sup_p"][m], rtol=2e-6, atol=1e-7)
+        assert abs(w[m] - tg["w"][m]) <= 1e-6 * abs(tg["w"][m]) + 1e-12
+        assert abs(Hh[m] - tg["H"][m]) <= 1e-5
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 520, 192), (37, 70, 200), (512, 1024, 1024)])
+def test_gemm_engine_vs_torch_fp32(a_mn, b_mn, M, N, K):
+    """Test hook: the tcgen05 engine on a plain GEMM vs a PyTorch fp32 reference."""
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    Am = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    Bm = torch.randn(N, K, device="cuda", generator=g).to(torch.bfloat16)
+    ref = Am.float() @ Bm.float().T
+    Ast = Am.T.contiguous() if a_mn else Am
+    Bst = Bm.T.contiguous() if b_mn else Bm
+    # pad leading dims to 16 B multiples
+    def pad(x):
+        c = x.shape[1]
+        cp = (c + 7) // 8 * 8
+        y = torch.zeros(x.shape[0], cp, dtype=x.dtype, device=x.device)
+        y[:, :c] = x
+        return y
+    Ast, Bst = pad(Ast), pad(Bst)
+    D = torch.full((M, N), float("nan"), device="cuda")
+    A.aurora_debug_gemm(bool(a_mn), bool(b_mn), Ast, Bst, D, M, N, K, Ast.stride(0), Bst.stride(0), D.stride(0))
+    torch.cuda.synchronize()
+    err = (D - ref).abs().max().item()
+    assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "small_tree", "mid"])
+def test_full_parity_small(name):
+    tr = tracegen.gen_trace(name)
+    ref = oracle.step(tr)
+    out = _run_gpu(tr)
+    st = out["st"]
+    _check_labels(st, ref, tr)
+    loss = float(st.loss.item())
+    assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"]), (loss, ref["loss"])
+    np.testing.assert_allclose(st.row_lse.cpu().numpy(), ref["lse"], rtol=2e-5, atol=1e-5)
+    assert _rfro(out["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert _rfro(out["dH"].cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+@pytest.mark.parametrize("kw", [dict(k_accept=3, k_discard=16), dict(lambda_discard=0.0), dict(normalize=1),
+                                dict(discard_scope=1, lambda_discard=2.5), dict(k_accept=1, k_discard=1)])
+def test_loss_config_variants(kw):
+    tr = tracegen.gen_trace("small_tree")
+    ref = oracle.step(tr, **kw)
+    out = _run_gpu(tr, **kw)
+    _check_labels(out["st"], ref, tr)
+    loss = float(out["st"].loss.item())
+    assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"]) + 1e-9
+    assert _rfro(out["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert _rfro(out["dH"].cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+def test_edge_shapes():
+    """R=1, N=1, V < one tile, d = 64: single partial tile in every GEMM."""
+    for cfg in [tracegen.TraceConfig("e1", d=64, V=100, R=1, N=1, seed=9, alpha=(0.5,)),
+                tracegen.TraceConfig("e2", d=128, V=257, R=3, N=32, seed=10, alpha=(0.9,)),
+                tracegen.TraceConfig("e3", d=64, V=20, R=70, N=2, seed=11, alpha=(0.5,), ragged=True)]:
+        tr = tracegen.gen_trace(cfg)
+        ref = oracle.step(tr)
+        out = _run_gpu(tr)
+        _check_labels(out["st"], ref, tr)
+        loss = float(out["st"].loss.item())
+        assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"])
+        assert _rfro(out["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+        assert _rfro(out["dH"].cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+def test_all_rejected_and_all_accepted():
+    tr = tracegen.gen_trace(tracegen.TraceConfig("rej", d=64, V=500, R=6, N=5, seed=12, alpha=(0.0,)))
+    ref = oracle.step(tr)
+    out = _run_gpu(tr)
+    _check_labels(out["st"], ref, tr)
+    assert (ref["accept_len"] == 1).all()
+    tr = tracegen.gen_trace(tracegen.TraceConfig("acc", d=64, V=500, R=6, N=5, seed=13, alpha=(1.0,)))
+    ref = oracle.step(tr)
+    out = _run_gpu(tr)
+    _check_labels(out["st"], ref, tr)
+    assert (ref["accept_len"] == 6).all() and ref["targets"]["counts"][1] == 0
+    assert abs(float(out["st"].loss.item()) - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"])
+
+
+def test_status_word_errors():
+    tr = tracegen.gen_trace("small")
+    c = tr["cfg"]
+    # non-finite logit
+    T = tr["T_bits"].copy()
+    T[3, 17] = 0x7FC0  # NaN
+    g = _to_gpu(tr)
+    st = A.SpecTrainStep(c.R, c.N, c.d, c.V)
+    st.verify(g["draft"], _bf16(T), g["parents"], g["num_nodes"])
+    torch.cuda.synchronize()
+    assert int(st.status.item()) & A.STATUS_NONFINITE
+    # out-of-range token
+    d2 = g["draft"].clone()
+    d2[0, 0] = c.V
+    st.verify(d2, g["T"], g["parents"], g["num_nodes"])
+    torch.cuda.synchronize()
+    assert int(st.status.item()) & A.STATUS_RANGE
+    # malformed parents
+    p = torch.full((c.R, c.N), -1, dtype=torch.int32, device="cuda")
+    p[0, 2] = 2
+    st.verify(g["draft"], g["T"], p, g["num_nodes"])
+    torch.cuda.synchronize()
+    assert int(st.status.item()) & A.STATUS_STRUCTURE
+    # clean again
+    st.verify(g["draft"], g["T"], g["parents"], g["num_nodes"])
+    torch.cuda.synchronize()
+    assert int(st.status.item()) == 0
+
+
+def test_dlogits_rows_hook_and_row_sum_zero():
+    tr = tracegen.gen_trace("small")
+    ref = oracle.step(tr)
+    out = _run_gpu(tr)
+    rows = [0, 5, 11, tr["M"] - 1]
+    dz = out["st"].debug_dlogits_rows(out["g"]["H"], out["g"]["W"], rows).cpu().numpy().astype(np.float64)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    dz_ref = oracle.dlogits_rows(H64, tr["W_bits"], ref["targets"], ref["lse"][rows], rows)
+    for i in range(len(rows)):
+        assert _rfro(dz[i], dz_ref[i]) <= 1e-3 or np.abs(dz_ref[i]).max() == 0
+    assert np.abs(dz.sum(1)).max() <= 1e-5 * max(1e-30, np.abs(dz).max()) * tr["V"] ** 0.5 + 1e-7
+    # dW column sums vanish (row-sum-zero of dZ)
+    dW = out["dW"].cpu().numpy().astype(np.float64)
+    assert np.abs(dW.sum(0)).max() <= 2e-2 * np.abs(dW).sum(0).max()
+
+
+def test_accumulate_and_upstream_grad():
+    tr = tracegen.gen_trace("small")
+    out = _run_gpu(tr)
+    st, g = out["st"], out["g"]
+    c = tr["cfg"]
+    dH2 = torch.empty_like(out["dH"])
+    dW2 = out["dW"].clone()
+    dl = torch.tensor([-2.0], device="cuda")
+    st.backward(g["H"], g["W"], dH2, dW2, dloss=dl, accumulate_dW=True)
+    torch.cuda.synchronize()
+    # dW2 = dW + (-2) dW = -dW ; dH2 = -2 dH
+    assert _rfro(dW2.cpu().numpy(), -out["dW"].cpu().numpy()) < 1e-5
+    assert _rfro(dH2.cpu().numpy(), -2 * out["dH"].cpu().numpy()) < 1e-5
+
+
+def test_determinism():
+    tr = tracegen.gen_trace("mid")
+    a = _run_gpu(tr)
+    b = _run_gpu(tr)
+    assert a["st"].loss.item() == b["st"].loss.item()
+    assert torch.equal(a["dW"], b["dW"]) and torch.equal(a["dH"], b["dH"])
+
+
+def test_llama_full_size_parity():
+    """configs[1] at full size, in the launch configuration bench.py times:
+    labels bit-exact on all rows, loss / dW / dH against the full f64 oracle."""
+    tr = tracegen.gen_trace("llama")
+    out = _run_gpu(tr)
+    ref = oracle.step(tr)
+    _check_labels(out["st"], ref, tr)
+    loss = float(out["st"].loss.item())
+    assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"])
+    assert _rfro(out["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert _rfro(out["dH"].cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+@pytest.mark.parametrize("name", ["qwen3", "minimax"])
+def test_large_config_sampled_parity(name):
+    """Full-size configs: labels bit-exact on every row (oracle scan row by row),
+    per-row lse / loss on sampled rows, dW column-sum property at full size."""
+    tr = tracegen.gen_trace(name)
+    out = _run_gpu(tr, want_grads=True)
+    st = out["st"]
+    M, V = tr["M"], tr["V"]
+    T = tr["T_bits"]
+    am = np.empty(M, dtype=np.int64)
+    topk = np.empty((M, 10), dtype=np.int64)
+    for m0 in range(0, M, 256):
+        a, t, nf = oracle.target_scan(oracle.bf16_bits_to_f64(T[m0:m0 + 256]), 10)
+        assert not nf
+        am[m0:m0 + 256], topk[m0:m0 + 256] = a, t
+    lab = oracle.verify(tr["draft_tokens"], tr["parents"], tr["num_nodes"], am)
+    np.testing.assert_array_equal(st.target_argmax.cpu().numpy(), am)
+    np.testing.assert_array_equal(st.accept_len.cpu().numpy(), lab["accept_len"])
+    np.testing.assert_array_equal(st.row_class.cpu().numpy(), lab["row_class"])
+    np.testing.assert_array_equal(st.bonus.cpu().numpy(), lab["bonus"])
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(M, size=24, replace=False))
+    tg = oracle.row_targets(lab["row_class"], lambda m: oracle.bf16_bits_to_f64(T[m]), topk, rows=rows)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    fw = oracle.loss_fwd(H64, tr["W_bits"], tg, rows=rows)
+    np.testing.assert_allclose(st.row_lse.cpu().numpy()[rows], fw["lse"], rtol=2e-5)
+    np.testing.assert_allclose(st.row_loss.cpu().numpy()[rows], fw["row_loss"], rtol=1e-3, atol=1e-3)
+    dW = out["dW"].double()
+    colsum = dW.sum(0).abs().max().item()
+    assert colsum <= 2e-2 * dW.abs().sum(0).max().item()
