@@ -130,13 +130,20 @@ int64_t chunk_cols(int64_t V_local) {
   if (V_local <= 4 * BN) return rup(V_local, BN);
   return rup(cdiv(V_local, 4), BN);  // <= 1/4 of the local dLogits at any time
 }
+// split-K factor for dH: the (m, n) tile count is small (M x d output) so pick the
+// split that fills whole waves of 148 SMs best (fewest splits within 3% of the best).
 int dh_splits(int64_t M, int64_t d, int64_t kb_total) {
   const int64_t tiles = cdiv(M, BM) * cdiv(d, BN);
-  int64_t s = cdiv(kNumSMs, tiles);
-  s = std::min<int64_t>(std::max<int64_t>(s, 1), 8);
-  s = std::min<int64_t>(s, kb_total);
-  if (s > 1) s = cdiv(kb_total, cdiv(kb_total, s));  // every split gets >= 1 k-block
-  return static_cast<int>(std::max<int64_t>(s, 1));
+  double best_eff = 0.0;
+  double eff[17] = {0};
+  for (int64_t s = 1; s <= 16 && s <= kb_total; ++s) {
+    const int64_t units = tiles * s;
+    eff[s] = static_cast<double>(units) / static_cast<double>(cdiv(units, kNumSMs) * kNumSMs);
+    best_eff = std::max(best_eff, eff[s]);
+  }
+  for (int64_t s = 1; s <= 16 && s <= kb_total; ++s)
+    if (eff[s] >= best_eff - 0.03) return static_cast<int>(cdiv(kb_total, cdiv(kb_total, s)));
+  return 1;
 }
 
 struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; };
@@ -499,7 +506,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     h.m_tiles = static_cast<int32_t>(cdiv(M, BM));
     h.n_tiles = static_cast<int32_t>(cdiv(d, BN));
     h.kb_total = static_cast<int32_t>(cdiv(vc, BK));
-    h.splits = w.splits > 1 ? std::min<int>(w.splits, h.kb_total) : 1;
+    h.splits = std::min<int>(dh_splits(M, d, h.kb_total), w.splits);
     h.kb_per_split = static_cast<int32_t>(cdiv(h.kb_total, h.splits));
     h.splits = static_cast<int32_t>(cdiv(h.kb_total, h.kb_per_split));
     h.M = M;

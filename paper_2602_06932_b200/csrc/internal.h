@@ -21,7 +21,8 @@ constexpr int kStages = 4;
 constexpr int kGemmThreads = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
 constexpr int kSmemA = BM * BK * 2;
 constexpr int kSmemB = BN * BK * 2;
-constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kStgLd = 36;  // fp32 staging row stride (floats): 16 B aligned, conflict-free float4
+constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 256 /*barriers*/ + 4 * 32 * kStgLd * 4;
 
 enum EpiKind : int { EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2 };
 

@@ -100,6 +100,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  float* stage_f32 = reinterpret_cast<float*>(smem + kStages * (kSmemA + kSmemB) + 256);  // 4 x 32 x kStgLd
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               cur.advance();
             }
           } else {
-            float dz[32];
+            float(&dz)[32] = z;  // in place: dz overwrites z
 #pragma unroll
             for (int j = 0; j < 32; ++j) dz[j] = coef * ex2_approx(fmaf(z[j], kLog2e, -lse2));
             while (cur.nxt < col0 + cb + 32) {
@@ -291,33 +292,48 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       } else {  // EPI_STORE_F32
-        float* base = args.out + static_cast<int64_t>(sp) * args.split_stride + row * args.ld_out + col0;
-        const bool vec_ok = ((args.ld_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 15) == 0);
+        // TMEM gives thread = row; transpose each 32x32 fp32 block through this warp's
+        // smem slice so every store instruction writes four full 128 B row segments.
+        float* stg = stage_f32 + (warp - 2) * (32 * kStgLd);
+        float* obase = args.out + static_cast<int64_t>(sp) * args.split_stride;
+        const bool vec_ok = ((args.ld_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0);
+        const int64_t row_base = static_cast<int64_t>(mt) * BM + q * 32;
         for (int c = 0; c < BN / 32; ++c) {
           const int cb = c * 32;
           if (cb >= ncols) break;
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + cb, r);
           tmem_ld_wait();
-          if (!row_ok) continue;
-          float* dst = base + cb;
-          if (cb + 32 <= ncols && vec_ok) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                     __uint_as_float(r[j + 3]));
-              if (args.accumulate) {
-                const float4 o = *reinterpret_cast<const float4*>(dst + j);
-                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(stg + lane * kStgLd + j) =
+                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                            __uint_as_float(r[j + 3]));
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rl = it * 4 + (lane >> 3);
+            const int cc = (lane & 7) * 4;
+            const int64_t grow = row_base + rl;
+            const int64_t gcol = col0 + cb + cc;
+            if (grow < args.M && cb + cc < ncols) {
+              float4 v = *reinterpret_cast<const float4*>(stg + rl * kStgLd + cc);
+              float* dst = obase + grow * args.ld_out + gcol;
+              if (vec_ok && cb + cc + 4 <= ncols) {
+                if (args.accumulate) {
+                  const float4 o = *reinterpret_cast<const float4*>(dst);
+                  v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                }
+                *reinterpret_cast<float4*>(dst) = v;
+              } else {
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (cb + cc + e < ncols) dst[e] = args.accumulate ? dst[e] + vv[e] : vv[e];
               }
-              *reinterpret_cast<float4*>(dst + j) = v;
-            }
-          } else {
-            for (int j = 0; j < 32 && cb + j < ncols; ++j) {
-              const float v = __uint_as_float(r[j]);
-              dst[j] = args.accumulate ? dst[j] + v : v;
             }
           }
+          __syncwarp();
         }
       }
       tc_fence_before();

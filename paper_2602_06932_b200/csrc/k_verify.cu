@@ -18,183 +18,173 @@
 namespace aur {
 
 namespace {
-constexpr int KM = AURORA_MAX_K;  // register list length (runtime k <= KM)
+constexpr int KM = AURORA_MAX_K;  // maximum list length (runtime k <= KM <= 32 lanes)
 
-// (v, i) ranks before (w, j)?  value desc, index asc.
+// (v, i) ranks before (w, j)?  value desc, index asc (numeric compare: -0 == +0).
 __device__ __forceinline__ bool better(float v, int32_t i, float w, int32_t j) {
   return v > w || (v == w && i < j);
 }
 
-struct TopList {
-  float v[KM];
-  int32_t i[KM];
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int j = 0; j < KM; ++j) { v[j] = -INFINITY; i[j] = INT32_MAX; }
+// A sorted top-k list distributed over the lanes of a warp: lane j holds entry j
+// ((value desc, index asc)); lanes >= k hold spilled / sentinel entries.  All lanes
+// call every member with warp-uniform arguments.
+struct WarpList {
+  float v;
+  int32_t i;
+  float thr_v;    // entry k-1 (the admission threshold)
+  int32_t thr_i;
+  int k;
+  __device__ __forceinline__ void init(int k_) {
+    v = -INFINITY; i = INT32_MAX; thr_v = -INFINITY; thr_i = INT32_MAX; k = k_;
   }
-  // bubble insertion keeping (value desc, index asc)
+  __device__ __forceinline__ bool admits(float cv, int32_t ci) const { return better(cv, ci, thr_v, thr_i); }
+  // insert a warp-uniform candidate that admits() accepted
   __device__ __forceinline__ void insert(float cv, int32_t ci) {
-#pragma unroll
-    for (int j = 0; j < KM; ++j) {
-      const bool sw = better(cv, ci, v[j], i[j]);
-      const float tv = v[j];
-      const int32_t ti = i[j];
-      v[j] = sw ? cv : tv;
-      i[j] = sw ? ci : ti;
-      cv = sw ? tv : cv;
-      ci = sw ? ti : ci;
-    }
+    const int lane = threadIdx.x & 31;
+    const uint32_t b = __ballot_sync(0xffffffffu, better(cv, ci, v, i));
+    const int pos = __ffs(b) - 1;  // >= 0 because the candidate beats entry k-1
+    const float uv = __shfl_up_sync(0xffffffffu, v, 1);
+    const int32_t ui = __shfl_up_sync(0xffffffffu, i, 1);
+    if (lane > pos) { v = uv; i = ui; }
+    if (lane == pos) { v = cv; i = ci; }
+    thr_v = __shfl_sync(0xffffffffu, v, k - 1);
+    thr_i = __shfl_sync(0xffffffffu, i, k - 1);
   }
-  __device__ __forceinline__ float kth(int k) const {
-    float t = v[0];
-#pragma unroll
-    for (int j = 0; j < KM; ++j) t = (j == k - 1) ? v[j] : t;
-    return t;
-  }
-  __device__ __forceinline__ int32_t kth_idx(int k) const {
-    int32_t t = i[0];
-#pragma unroll
-    for (int j = 0; j < KM; ++j) t = (j == k - 1) ? i[j] : t;
-    return t;
-  }
-  __device__ __forceinline__ void pop_front() {
-#pragma unroll
-    for (int j = 0; j < KM - 1; ++j) { v[j] = v[j + 1]; i[j] = i[j + 1]; }
-    v[KM - 1] = -INFINITY;
-    i[KM - 1] = INT32_MAX;
+  // offer one value held by lane `src` (warp-uniform src)
+  __device__ __forceinline__ void offer(float myv, int32_t myi, int src) {
+    const float cv = __shfl_sync(0xffffffffu, myv, src);
+    const int32_t ci = __shfl_sync(0xffffffffu, myi, src);
+    if (admits(cv, ci)) insert(cv, ci);
   }
 };
 
-// Warp-wide k-way merge of per-lane sorted lists; after the call every lane holds
-// the merged top-k in (ov, oi)[0..k).
-__device__ __forceinline__ void warp_merge(TopList& L, int k, float* ov, int32_t* oi) {
-  for (int r = 0; r < k; ++r) {
-    float bv = L.v[0];
-    int32_t bi = L.i[0];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov2 = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int32_t oi2 = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (better(ov2, oi2, bv, bi)) { bv = ov2; bi = oi2; }
-    }
-    ov[r] = bv;
-    oi[r] = bi;
-    if (L.i[0] == bi && L.v[0] == bv && bi != INT32_MAX) L.pop_front();
-  }
-}
-
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t pick4(const uint4& w, int e) {
+  return e == 0 ? w.x : (e == 1 ? w.y : (e == 2 ? w.z : w.w));
+}
+__device__ __forceinline__ uint32_t nonfinite8(const uint4& w) {
+  const uint32_t ax = __vmaxu2(__vmaxu2(w.x & 0x7FFF7FFFu, w.y & 0x7FFF7FFFu),
+                               __vmaxu2(w.z & 0x7FFF7FFFu, w.w & 0x7FFF7FFFu));
+  return static_cast<uint32_t>((ax & 0xFFFFu) >= 0x7F80u) | static_cast<uint32_t>((ax >> 16) >= 0x7F80u);
+}
+__device__ __forceinline__ float max8(const uint4& w) {
+  const __nv_bfloat162 m2 = __hmax2(__hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w.x),
+                                            *reinterpret_cast<const __nv_bfloat162*>(&w.y)),
+                                    __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w.z),
+                                            *reinterpret_cast<const __nv_bfloat162*>(&w.w)));
+  return fmaxf(__low2float(m2), __high2float(m2));
+}
+// Offer the 8 bf16 of lanes in `mask` (each lane's vector starts at column col_of_lane).
+__device__ __forceinline__ void offer_vectors(WarpList& L, uint32_t mask, const uint4& w, int64_t col) {
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int64_t c0 = __shfl_sync(0xffffffffu, col, src);
+#pragma unroll 1
+    for (int e = 0; e < 8; ++e) {
+      const uint32_t word = pick4(w, e >> 1);
+      const float myv = (e & 1) ? bf16_hi(word) : bf16_lo(word);
+      L.offer(myv, static_cast<int32_t>(c0 + e), src);
+    }
+  }
+}
+__device__ __forceinline__ uint4 ld_nc_v4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
 }  // namespace
 
 // --------------------------------------------------------------------------- A2 scan
-// grid (M * nseg), 256 threads.  Segment [seg*seg_len, min(V_local, +seg_len)).
+// grid (M * nseg), 256 threads = 8 warps.  Segment [seg*seg_len, min(V_local, +seg_len)).
+// Each warp keeps a lane-distributed top-k; a lane's 8 bf16 (one 16 B load) are only
+// offered when their bf16x2 max reaches the warp's k-th value, so after warm-up almost
+// every 16 B costs a handful of instructions (HBM-bound).
 __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
   const int row = blockIdx.x / p.nseg;
   const int seg = blockIdx.x % p.nseg;
   const int k = p.k_max;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t c0 = static_cast<int64_t>(seg) * p.seg_len;
   const int64_t c1 = min(p.V_local, c0 + p.seg_len);
   const uint16_t* T = p.T + static_cast<int64_t>(row) * p.ldT;
-  TopList L;
-  L.init();
-  float thr = -INFINITY;
+  WarpList L;
+  L.init(k);
   uint32_t bad = 0;
 
-  auto consider = [&](float v, int64_t col) {
-    if (v > thr) {  // later columns of this thread can only lose ties (index asc)
-      L.insert(v, static_cast<int32_t>(col));
-      thr = L.kth(k);
-    }
-  };
-
   const bool aligned = ((reinterpret_cast<uintptr_t>(T + c0) & 15) == 0);
-  if (aligned) {
-    const int64_t nvec = (c1 - c0) >> 3;
-    const uint4* src = reinterpret_cast<const uint4*>(T + c0);
-    constexpr int U = 8;
-    int64_t it = threadIdx.x;
-    for (; it + (U - 1) * 256 < nvec; it += U * 256) {
-      uint4 w[U];
+  const int64_t nvec = aligned ? (c1 - c0) >> 3 : 0;
+  const uint4* src = reinterpret_cast<const uint4*>(T + c0);
+  constexpr int U = 4;
+  // vector v of this segment is handled by warp (v / 32) % 8 ... interleaved by 256
+  int64_t base = static_cast<int64_t>(warp) * 32;
+  for (; base + (U - 1) * 256 + 31 < nvec; base += U * 256) {
+    uint4 w[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint4* a = src + it + u * 256;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(w[u].x), "=r"(w[u].y), "=r"(w[u].z), "=r"(w[u].w)
-                     : "l"(a));
-      }
+    for (int u = 0; u < U; ++u) w[u] = ld_nc_v4(src + base + u * 256 + lane);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        // non-finite: any |x| exponent all-ones
-        const uint32_t ax = __vmaxu2(__vmaxu2(w[u].x & 0x7FFF7FFFu, w[u].y & 0x7FFF7FFFu),
-                                     __vmaxu2(w[u].z & 0x7FFF7FFFu, w[u].w & 0x7FFF7FFFu));
-        bad |= ((ax & 0xFFFFu) >= 0x7F80u) | ((ax >> 16) >= 0x7F80u);
-        const __nv_bfloat162 m2 = __hmax2(__hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w[u].x),
-                                                  *reinterpret_cast<const __nv_bfloat162*>(&w[u].y)),
-                                          __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w[u].z),
-                                                  *reinterpret_cast<const __nv_bfloat162*>(&w[u].w)));
-        const float gm = fmaxf(__low2float(m2), __high2float(m2));
-        if (gm > thr) {
-          const int64_t col = c0 + (it + u * 256) * 8;
-          const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            consider(bf16_lo(ws[e]), col + 2 * e);
-            consider(bf16_hi(ws[e]), col + 2 * e + 1);
-          }
-        }
-      }
-    }
-    for (; it < nvec; it += 256) {
-      const uint4 w = src[it];
-      const int64_t col = c0 + it * 8;
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t a = ws[e] & 0x7FFF7FFFu;
-        bad |= ((a & 0xFFFFu) >= 0x7F80u) | ((a >> 16) >= 0x7F80u);
-        consider(bf16_lo(ws[e]), col + 2 * e);
-        consider(bf16_hi(ws[e]), col + 2 * e + 1);
-      }
-    }
-    for (int64_t col = c0 + nvec * 8 + threadIdx.x; col < c1; col += 256) {
-      const uint32_t b = T[col];
-      bad |= ((b & 0x7FFFu) >= 0x7F80u);
-      consider(__uint_as_float(b << 16), col);
-    }
-  } else {
-    for (int64_t col = c0 + threadIdx.x; col < c1; col += 256) {
-      const uint32_t b = T[col];
-      bad |= ((b & 0x7FFFu) >= 0x7F80u);
-      consider(__uint_as_float(b << 16), col);
+    for (int u = 0; u < U; ++u) {
+      bad |= nonfinite8(w[u]);
+      const float gm = max8(w[u]);
+      const uint32_t hit = __ballot_sync(0xffffffffu, gm >= L.thr_v);
+      if (hit) offer_vectors(L, hit, w[u], c0 + (base + u * 256 + lane) * 8);
     }
   }
-  if (bad) atomicOr(p.lab.status, AURORA_STATUS_NONFINITE);
+  for (; base < nvec; base += 256) {
+    const int64_t vi = base + lane;
+    uint4 w = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // -inf padding
+    if (vi < nvec) {
+      w = ld_nc_v4(src + vi);
+      bad |= nonfinite8(w);
+    }
+    const float gm = max8(w);
+    const uint32_t hit = __ballot_sync(0xffffffffu, vi < nvec && gm >= L.thr_v);
+    if (hit) offer_vectors(L, hit, w, c0 + vi * 8);
+  }
+  // scalar tail (or whole segment when the row start is not 16 B aligned)
+  for (int64_t cb = c0 + nvec * 8 + static_cast<int64_t>(warp) * 32; cb < c1; cb += 256) {
+    const int64_t col = cb + lane;
+    float v = -INFINITY;
+    if (col < c1) {
+      const uint32_t b = T[col];
+      bad |= static_cast<uint32_t>((b & 0x7FFFu) >= 0x7F80u);
+      v = __uint_as_float(b << 16);
+    }
+    uint32_t hit = __ballot_sync(0xffffffffu, col < c1 && L.admits(v, static_cast<int32_t>(col)));
+    while (hit) {
+      const int s = __ffs(hit) - 1;
+      hit &= hit - 1;
+      L.offer(v, static_cast<int32_t>(col), s);
+    }
+  }
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if (bad && lane == 0) atomicOr(p.lab.status, AURORA_STATUS_NONFINITE);
 
-  // ---- block merge: per warp, then across the 8 warps
+  // ---- block merge: warp lists -> smem -> warp 0
   __shared__ float s_v[8][KM];
   __shared__ int32_t s_i[8][KM];
-  float ov[KM];
-  int32_t oi[KM];
-  warp_merge(L, k, ov, oi);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    for (int j = 0; j < k; ++j) { s_v[warp][j] = ov[j]; s_i[warp][j] = oi[j]; }
-  }
+  if (lane < k) { s_v[warp][lane] = L.v; s_i[warp][lane] = L.i; }
   __syncthreads();
   if (warp == 0) {
-    TopList L2;
-    L2.init();
-    if (lane < 8) {
-      for (int j = 0; j < k; ++j) { L2.v[j] = s_v[lane][j]; L2.i[j] = s_i[lane][j]; }
-    }
-    warp_merge(L2, k, ov, oi);
-    if (lane == 0) {
-      const int64_t o = (static_cast<int64_t>(row) * p.nseg + seg) * k;
-      for (int j = 0; j < k; ++j) {
-        p.cand_val[o + j] = ov[j];
-        p.cand_idx[o + j] = (oi[j] == INT32_MAX) ? INT32_MAX : static_cast<int32_t>(oi[j] + p.vocab_offset);
+    WarpList F;
+    F.init(k);
+    for (int w8 = 0; w8 < 8; ++w8) {
+      const float cv = lane < k ? s_v[w8][lane] : -INFINITY;
+      const int32_t ci = lane < k ? s_i[w8][lane] : INT32_MAX;
+      uint32_t hit = __ballot_sync(0xffffffffu, lane < k && F.admits(cv, ci));
+      while (hit) {
+        const int s = __ffs(hit) - 1;
+        hit &= hit - 1;
+        F.offer(cv, ci, s);
       }
+    }
+    if (lane < k) {
+      const int64_t o = (static_cast<int64_t>(row) * p.nseg + seg) * k;
+      p.cand_val[o + lane] = F.v;
+      p.cand_idx[o + lane] = (F.i == INT32_MAX) ? INT32_MAX : static_cast<int32_t>(F.i + p.vocab_offset);
     }
   }
 }
@@ -207,22 +197,25 @@ __global__ void __launch_bounds__(256) k_topk_merge(VerifyLaunch p, const float*
   const int lane = threadIdx.x & 31;
   if (row >= p.M) return;
   const int k = p.k_max;
-  TopList L;
-  L.init();
-  if (lane < nlists) {
-    const int64_t o = static_cast<int64_t>(row) * row_stride + lane * list_stride;
-    for (int j = 0; j < k; ++j) { L.v[j] = in_val[o + j]; L.i[j] = in_idx[o + j]; }
-  }
-  float ov[KM];
-  int32_t oi[KM];
-  warp_merge(L, k, ov, oi);
-  if (lane == 0) {
-    for (int j = 0; j < k; ++j) {
-      p.top_val[static_cast<int64_t>(row) * k + j] = ov[j];
-      p.top_idx[static_cast<int64_t>(row) * k + j] = oi[j];
+  WarpList F;
+  F.init(k);
+  for (int l = 0; l < nlists; ++l) {
+    const int64_t o = static_cast<int64_t>(row) * row_stride + l * list_stride;
+    const float cv = lane < k ? in_val[o + lane] : -INFINITY;
+    const int32_t ci = lane < k ? in_idx[o + lane] : INT32_MAX;
+    uint32_t hit = __ballot_sync(0xffffffffu, lane < k && F.admits(cv, ci));
+    while (hit) {
+      const int s = __ffs(hit) - 1;
+      hit &= hit - 1;
+      F.offer(cv, ci, s);
     }
-    p.lab.target_argmax[row] = oi[0];
   }
+  if (lane < k) {
+    p.top_val[static_cast<int64_t>(row) * k + lane] = F.v;
+    p.top_idx[static_cast<int64_t>(row) * k + lane] = F.i;
+  }
+  const int32_t am = __shfl_sync(0xffffffffu, F.i, 0);
+  if (lane == 0) p.lab.target_argmax[row] = am;
 }
 
 // --------------------------------------------------------------------------- A3 verify
