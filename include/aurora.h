@@ -163,7 +163,10 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
 /* Communicator (vocab-parallel x data-parallel, one process per GPU).
  * nccl_unique_id (host) points to the 128-byte ncclUniqueId that rank 0 created with
  * aurora_comm_get_unique_id and the caller broadcast (e.g. torch.distributed).
- * Ranks are laid out dp-major: rank = dp_rank * vp_size + vp_rank. */
+ * Ranks are laid out dp-major: rank = dp_rank * vp_size + vp_rank.  A group exchanges
+ * (C1-C5) iff its size > 1; a communicator with nranks == 1 runs every exchange as an
+ * identity collective (used to test the NCCL plumbing on one GPU).  The comm owns a
+ * small device scratch for gathered per-row data that grows on first use. */
 aurora_status_t aurora_comm_get_unique_id(void* nccl_unique_id_out /* 128 bytes */);
 aurora_status_t aurora_comm_create(const void* nccl_unique_id, int nranks, int rank,
                                    int vp_size, int dp_size, aurora_comm_t* out);

@@ -92,6 +92,10 @@ Api& api() {
 
 struct aurora_comm_s {
   int nranks, rank, vp_size, dp_size, vp_rank, dp_rank;
+  // A 1-rank communicator runs every exchange (identity collectives); it exists to
+  // exercise the NCCL plumbing on one GPU.  Otherwise a group exchanges iff size > 1.
+  bool vp_x() const { return nranks == 1 || vp_size > 1; }
+  bool dp_x() const { return nranks == 1 || dp_size > 1; }
   aur::nccl::Comm world = nullptr, vp = nullptr, dp = nullptr;
   void* scratch = nullptr;  // comm-owned device scratch for gathered candidates / stats
   size_t scratch_bytes = 0;
@@ -126,9 +130,11 @@ int scan_nseg(int64_t M, int64_t V_local) {
   nseg = std::min<int64_t>(nseg, cdiv(V_local, 2048));
   return static_cast<int>(std::max<int64_t>(nseg, 1));
 }
+// dLogits chunk width: 1/8 of the local vocab, double-buffered => at most 1/4 of the
+// local [M x V_local] dLogits is live at any time.
 int64_t chunk_cols(int64_t V_local) {
-  if (V_local <= 4 * BN) return rup(V_local, BN);
-  return rup(cdiv(V_local, 4), BN);  // <= 1/4 of the local dLogits at any time
+  if (V_local <= 8 * BN) return rup(cdiv(V_local, 2), BN);
+  return rup(cdiv(V_local, 8), BN);
 }
 // split-K factor for dH: the (m, n) tile count is small (M x d output) so pick the
 // split that fills whole waves of 148 SMs best (fewest splits within 3% of the best).
@@ -160,19 +166,22 @@ struct FwdWs { float *pm, *ps, *pu, *msu, *bp; int n_tiles; };
 FwdWs carve_fwd(Carver& c, int64_t M, int64_t V_local) {
   FwdWs w;
   w.n_tiles = static_cast<int>(cdiv(V_local, BN));
-  w.pm = c.take<float>(M * w.n_tiles);
-  w.ps = c.take<float>(M * w.n_tiles);
-  w.pu = c.take<float>(M * w.n_tiles);
+  w.pm = c.take<float>(M * 2 * w.n_tiles);  // one partial per (vocab tile, column half)
+  w.ps = c.take<float>(M * 2 * w.n_tiles);
+  w.pu = c.take<float>(M * 2 * w.n_tiles);
   w.msu = c.take<float>(M * 3);
   w.bp = c.take<float>(cdiv(M, 256) + 1);
   return w;
 }
-struct BwdWs { __nv_bfloat16* dzT; float* dh_part; int64_t vc, m_pad; int splits; };
+constexpr int kCounters = 64;  // dynamic-scheduler tile counters (one per launch in a call)
+struct BwdWs { int32_t* counters; __nv_bfloat16* dzT[2]; float* dh_part; int64_t vc, m_pad; int splits; };
 BwdWs carve_bwd(Carver& c, int64_t M, int64_t d, int64_t V_local) {
   BwdWs w;
+  w.counters = c.take<int32_t>(kCounters);
   w.vc = chunk_cols(V_local);
   w.m_pad = rup(M, 8);
-  w.dzT = c.take<__nv_bfloat16>(w.vc * w.m_pad);
+  w.dzT[0] = c.take<__nv_bfloat16>(w.vc * w.m_pad);
+  w.dzT[1] = c.take<__nv_bfloat16>(w.vc * w.m_pad);
   w.splits = dh_splits(M, d, cdiv(w.vc, BK));
   w.dh_part = w.splits > 1 ? c.take<float>(static_cast<int64_t>(w.splits) * M * d) : nullptr;
   return w;
@@ -197,6 +206,38 @@ bool labels_ok(const aurora_labels_t* l, bool verify_outputs) {
     return false;
   return true;
 }
+// Library-owned side streams and events (per device, created once) for the
+// concurrent bwd: dW(c) and dH(c) overlap dz(c+1) on the caller's stream.
+struct SideStreams {
+  cudaStream_t s[2] = {nullptr, nullptr};
+  cudaEvent_t ev[160];
+  bool ok = false;
+};
+SideStreams* side_streams() {
+  static std::mutex mu;
+  static SideStreams per_dev[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  SideStreams& S = per_dev[dev];
+  if (!S.ok) {
+    for (auto& st : S.s)
+      if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    for (auto& e : S.ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    S.ok = true;
+  }
+  return &S;
+}
+bool serial_bwd() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AURORA_SERIAL_BWD");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // The comm owns a device scratch for gathered per-row data; it grows on first use
 // (one cudaMalloc per size increase, never in steady state).
 bool ensure_scratch(aurora_comm_t c, size_t bytes) {
@@ -309,7 +350,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   if (std::max(cfg->k_accept, cfg->k_discard) > t->V) return AURORA_ERR_INVALID_ARG;
   const int64_t M = static_cast<int64_t>(t->R) * (t->N + 1);
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->V_local, cfg)) return AURORA_ERR_WORKSPACE;
-  if (comm && comm->vp_size > 1 && t->V_local == t->V) return AURORA_ERR_INVALID_ARG;
+  if (comm && comm->vp_size > 1 && t->V_local == t->V) return AURORA_ERR_INVALID_ARG;  // VP needs shards
   cudaStream_t s = static_cast<cudaStream_t>(stream);
 
   Carver c(ws);
@@ -345,7 +386,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
       cudaSuccess)
     return AURORA_ERR_CUDA;
   prof_end(PH_SCAN, s);
-  if (comm && comm->vp_size > 1) {
+  if (comm && comm->vp_x()) {
     // C1: gather every VP rank's (value-ordered) top list and merge in global order.
     auto& A = nccl::api();
     const size_t per = static_cast<size_t>(M) * k_max;
@@ -363,7 +404,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   }
   prof_begin(PH_VERIFY, s);
   if ((e = launch_verify(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
-  if (comm && comm->dp_size > 1) {
+  if (comm && comm->dp_x()) {
     auto& A = nccl::api();
     if (A.AllReduce(out->counts, out->counts, 2, nccl::ncclInt32, nccl::ncclSum, comm->dp, s) != 0)
       return AURORA_ERR_NCCL;
@@ -408,10 +449,10 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   prof_end(PH_FWD_GEMM, s);
   if (e != cudaSuccess) return AURORA_ERR_CUDA;
   prof_begin(PH_FWD_COMBINE, s);
-  if ((e = launch_reduce_partials(w.pm, w.ps, w.pu, M, w.n_tiles, w.msu, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  if ((e = launch_reduce_partials(w.pm, w.ps, w.pu, M, 2 * w.n_tiles, w.msu, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   const float* msu_all = w.msu;
   int P = 1;
-  if (comm && comm->vp_size > 1) {
+  if (comm && comm->vp_x()) {
     auto& A = nccl::api();
     const size_t need = static_cast<size_t>(M) * 3 * comm->vp_size * sizeof(float);
     if (!ensure_scratch(comm, need)) return AURORA_ERR_CUDA;
@@ -425,7 +466,7 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
                               w.bp, &nb, s)) != cudaSuccess)
     return AURORA_ERR_CUDA;
   if ((e = launch_loss_sum(w.bp, nb, loss, s)) != cudaSuccess) return AURORA_ERR_CUDA;
-  if (comm && comm->dp_size > 1) {
+  if (comm && comm->dp_x()) {
     auto& A = nccl::api();
     if (A.AllReduce(loss, loss, 1, nccl::ncclFloat32, nccl::ncclSum, comm->dp, s) != 0) return AURORA_ERR_NCCL;
   }
@@ -451,15 +492,31 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
   if (!make_tmap_bf16(&tmH_k, H, d, M, d, 64, BM)) return AURORA_ERR_CUDA;
   if (!make_tmap_bf16(&tmH_mn, H, d, M, d, 64, 64)) return AURORA_ERR_CUDA;
   const int64_t nchunks = cdiv(V_local, w.vc);
+  if (3 * nchunks + 1 > kCounters) return AURORA_ERR_UNSUPPORTED;
   const __nv_bfloat16* Wb = static_cast<const __nv_bfloat16*>(W);
+  // Streams: dz on the caller's stream; dW and dH on two side streams (or all serial).
+  SideStreams* S = serial_bwd() ? nullptr : side_streams();
+  cudaStream_t sW = S ? S->s[0] : s, sH = S ? S->s[1] : s;
+  cudaEvent_t* ev = S ? S->ev : nullptr;  // [0] start, [1+3c] dz(c), [2+3c] dW(c), [3+3c] dH(c)
+  if (cudaMemsetAsync(w.counters, 0, kCounters * sizeof(int32_t), s) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (S) {
+    if (cudaEventRecord(ev[0], s) != cudaSuccess) return AURORA_ERR_CUDA;
+    cudaStreamWaitEvent(sW, ev[0], 0);
+    cudaStreamWaitEvent(sH, ev[0], 0);
+  }
   for (int64_t ch = 0; ch < nchunks; ++ch) {
     const int64_t c0 = ch * w.vc;
     const int64_t vc = std::min(w.vc, V_local - c0);
+    __nv_bfloat16* dzT = w.dzT[ch & 1];
     CUtensorMap tmW_k, tmW_mn, tmZ_k, tmZ_mn;
     if (!make_tmap_bf16(&tmW_k, Wb + c0 * d, d, vc, d, 64, BN)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmW_mn, Wb + c0 * d, d, vc, d, 64, 64)) return AURORA_ERR_CUDA;
-    if (!make_tmap_bf16(&tmZ_k, w.dzT, M, vc, w.m_pad, 64, BM)) return AURORA_ERR_CUDA;
-    if (!make_tmap_bf16(&tmZ_mn, w.dzT, M, vc, w.m_pad, 64, 64)) return AURORA_ERR_CUDA;
+    if (!make_tmap_bf16(&tmZ_k, dzT, M, vc, w.m_pad, 64, BM)) return AURORA_ERR_CUDA;
+    if (!make_tmap_bf16(&tmZ_mn, dzT, M, vc, w.m_pad, 64, 64)) return AURORA_ERR_CUDA;
+    if (S && ch >= 2) {  // the buffer dz(ch) overwrites was read by dW(ch-2), dH(ch-2)
+      cudaStreamWaitEvent(s, ev[2 + 3 * (ch - 2)], 0);
+      cudaStreamWaitEvent(s, ev[3 + 3 * (ch - 2)], 0);
+    }
 
     // A7: recompute Z tiles, dz -> dZ^T chunk (bf16)
     GemmArgs a{};
@@ -477,12 +534,18 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     a.row_lse = row_lse;
     a.row_w = labels->row_w;
     a.dloss = dloss;
-    a.dzT = w.dzT;
+    a.dzT = dzT;
     a.ld_dzT = w.m_pad;
+    a.tile_counter = w.counters + 3 * ch;
     prof_begin(PH_BWD_DZ, s);
     cudaError_t e = launch_umma_gemm(EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s);
     prof_end(PH_BWD_DZ, s);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
+    if (S) {
+      cudaEventRecord(ev[1 + 3 * ch], s);
+      cudaStreamWaitEvent(sW, ev[1 + 3 * ch], 0);
+      cudaStreamWaitEvent(sH, ev[1 + 3 * ch], 0);
+    }
 
     // A8: dW[chunk] = dZ^T H   (A = dZ^T K-major, B = H MN-major, K = M)
     GemmArgs b{};
@@ -496,10 +559,20 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     b.out = dWf + c0 * d;
     b.ld_out = d;
     b.accumulate = accumulate_dW ? 1 : 0;
-    prof_begin(PH_BWD_DW, s);
-    e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, s);
-    prof_end(PH_BWD_DW, s);
+    b.tile_counter = w.counters + 3 * ch + 1;
+    prof_begin(PH_BWD_DW, sW);
+    e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW);
+    prof_end(PH_BWD_DW, sW);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
+    if (comm && comm->dp_x()) {  // C5: DP gradient allreduce of this dW chunk
+      auto& A = nccl::api();
+      prof_begin(PH_COMM, sW);
+      if (A.AllReduce(dWf + c0 * d, dWf + c0 * d, static_cast<size_t>(vc * d), nccl::ncclFloat32, nccl::ncclSum,
+                      comm->dp, sW) != 0)
+        return AURORA_ERR_NCCL;
+      prof_end(PH_COMM, sW);
+    }
+    if (S) cudaEventRecord(ev[2 + 3 * ch], sW);
 
     // A9: dH += dZ W[chunk]   (A = dZ^T as MN-major, B = W MN-major, K = vc)
     GemmArgs h{};
@@ -512,6 +585,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     h.M = M;
     h.N = d;
     h.ld_out = d;
+    h.tile_counter = w.counters + 3 * ch + 2;
     if (h.splits > 1) {
       h.out = w.dh_part;
       h.split_stride = M * d;
@@ -520,26 +594,23 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
       h.out = dH;
       h.accumulate = ch > 0 ? 1 : 0;
     }
-    prof_begin(PH_BWD_DH, s);
-    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, s);
-    prof_end(PH_BWD_DH, s);
+    prof_begin(PH_BWD_DH, sH);
+    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, sH);
+    prof_end(PH_BWD_DH, sH);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (h.splits > 1) {
-      prof_begin(PH_BWD_REDUCE, s);
-      e = launch_splitk_reduce(w.dh_part, h.splits, M * d, dH, ch > 0 ? 1 : 0, s);
-      prof_end(PH_BWD_REDUCE, s);
+      prof_begin(PH_BWD_REDUCE, sH);
+      e = launch_splitk_reduce(w.dh_part, h.splits, M * d, dH, ch > 0 ? 1 : 0, sH);
+      prof_end(PH_BWD_REDUCE, sH);
       if (e != cudaSuccess) return AURORA_ERR_CUDA;
     }
-    if (comm && comm->dp_size > 1) {  // C5: DP gradient allreduce of this dW chunk
-      auto& A = nccl::api();
-      prof_begin(PH_COMM, s);
-      if (A.AllReduce(dWf + c0 * d, dWf + c0 * d, static_cast<size_t>(vc * d), nccl::ncclFloat32, nccl::ncclSum,
-                      comm->dp, s) != 0)
-        return AURORA_ERR_NCCL;
-      prof_end(PH_COMM, s);
-    }
+    if (S) cudaEventRecord(ev[3 + 3 * ch], sH);
   }
-  if (comm && comm->vp_size > 1) {  // C4: VP dH allreduce
+  if (S) {  // join
+    cudaStreamWaitEvent(s, ev[2 + 3 * (nchunks - 1)], 0);
+    cudaStreamWaitEvent(s, ev[3 + 3 * (nchunks - 1)], 0);
+  }
+  if (comm && comm->vp_x()) {  // C4: VP dH allreduce
     auto& A = nccl::api();
     prof_begin(PH_COMM, s);
     if (A.AllReduce(dH, dH, static_cast<size_t>(M * d), nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0)

@@ -18,11 +18,13 @@ constexpr int BM = 128;  // tile rows (TMEM lanes)
 constexpr int BN = 256;  // tile cols (TMEM columns per accumulator)
 constexpr int BK = 64;   // K per pipeline stage (128 B of bf16 = one SW128 atom row)
 constexpr int kStages = 4;
-constexpr int kGemmThreads = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int kSmemA = BM * BK * 2;
 constexpr int kSmemB = BN * BK * 2;
-constexpr int kStgLd = 36;  // fp32 staging row stride (floats): 16 B aligned, conflict-free float4
-constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 256 /*barriers*/ + 4 * 32 * kStgLd * 4;
+constexpr int kSchedDepth = 4;  // tile-index ring depth (dynamic scheduler)
+constexpr int kStgLd = 20;  // fp32 staging row stride (floats) for 32x16 blocks: 16 B aligned
+constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 256 /*barriers*/ + kEpiWarps * 32 * kStgLd * 4;
 
 enum EpiKind : int { EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2 };
 
@@ -40,7 +42,7 @@ struct GemmArgs {
   const float* sup_p;
   int32_t k_max;
   int64_t col_gid0;  // global vocab id of GEMM column 0
-  float* p_max;      // [M, n_tiles] partial stats (fwd)
+  float* p_max;      // [M, 2*n_tiles] partial stats (fwd): one per (vocab tile, column half)
   float* p_sum;
   float* p_u;
   const float* row_lse;  // bwd
@@ -48,6 +50,7 @@ struct GemmArgs {
   const float* dloss;    // nullable => 1
   __nv_bfloat16* dzT;    // [N_chunk, ld_dzT] transposed dLogits chunk (bwd)
   int64_t ld_dzT;
+  int32_t* tile_counter;  // nullable: dynamic tile scheduler counter (zero before first use)
 };
 
 // Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.

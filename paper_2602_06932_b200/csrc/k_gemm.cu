@@ -1,9 +1,10 @@
 // k_gemm.cu — persistent warp-specialised tcgen05 GEMM engine for the lm_head phases.
 //
-// One CTA per SM (192 threads):
+// One CTA per SM (320 threads):
 //   warp 0      TMA producer: 4-stage ring of {A 128x64, B 256x64} bf16 tiles, SW128
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16)
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (warp w reads TMEM lanes 32*(w%4)..)
+//   warps 2..9  epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32*(w%4)..; two warps
+//               per lane quadrant split the 256 columns)
 // Two 128x256 fp32 accumulators (512 TMEM columns) let the epilogue of tile i overlap
 // the MMAs of tile i+1.  Tiles are visited m-fastest, so all row tiles of one vocab
 // tile run back to back and W (the large operand) is streamed from HBM once per phase.
@@ -99,8 +100,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  float* stage_f32 = reinterpret_cast<float*>(smem + kStages * (kSmemA + kSmemB) + 256);  // 4 x 32 x kStgLd
+  uint64_t* sfull_bar = tempty_bar + 2;        // tile-index ring (dynamic scheduler)
+  uint64_t* sempty_bar = sfull_bar + kSchedDepth;
+  int32_t* s_sched = reinterpret_cast<int32_t*>(sempty_bar + kSchedDepth);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_sched + kSchedDepth);
+  float* stage_f32 = reinterpret_cast<float*>(smem + kStages * (kSmemA + kSmemB) + 256);  // 8 x 32 x kStgLd
+  static_assert((2 * kStages + 4 + 2 * kSchedDepth) * 8 + 4 * kSchedDepth + 4 <= 256, "barrier area");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -114,7 +119,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], kEpiWarps);
+    }
+    for (int d = 0; d < kSchedDepth; ++d) {
+      mbar_init(&sfull_bar[d], 1);
+      mbar_init(&sempty_bar[d], 1 + kEpiWarps);  // MMA lane + epilogue warps
     }
     fence_barrier_init();
   }
@@ -125,12 +134,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   const int units = args.m_tiles * args.n_tiles * args.splits;
+  // Tile scheduler.  Static: u = blockIdx.x + i*gridDim.x.  Dynamic (args.tile_counter):
+  // the producer claims tiles with atomicAdd and hands them to the MMA / epilogue warps
+  // through a small smem ring, so a kernel sharing the GPU with another stream's kernel
+  // balances itself; the globally last claim resets the counter for the next launch.
+  const bool dyn = args.tile_counter != nullptr;
+  auto consumer_next = [&](uint32_t& slot, uint32_t& ph, int& u, bool first, bool is_mma) {
+    if (!dyn) {
+      u = first ? static_cast<int>(blockIdx.x) : u + static_cast<int>(gridDim.x);
+      return;
+    }
+    mbar_wait(&sfull_bar[slot], ph);
+    u = *reinterpret_cast<volatile int32_t*>(&s_sched[slot]);
+    if (is_mma) {
+      mbar_arrive(&sempty_bar[slot]);
+    } else {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&sempty_bar[slot]);
+    }
+    if (++slot == kSchedDepth) { slot = 0; ph ^= 1; }
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      uint32_t stage = 0, phase = 0, sslot = 0, sph = 0;
+      for (int u = blockIdx.x;; u += gridDim.x) {
+        if (dyn) {
+          u = atomicAdd(args.tile_counter, 1);
+          if (u == units + static_cast<int>(gridDim.x) - 1) atomicExch(args.tile_counter, 0);
+          mbar_wait(&sempty_bar[sslot], sph ^ 1);
+          s_sched[sslot] = u;
+          mbar_arrive(&sfull_bar[sslot]);
+          if (++sslot == kSchedDepth) { sslot = 0; sph ^= 1; }
+        }
+        if (u >= units) break;
         const int mt = u % args.m_tiles;
         const int rest = u / args.m_tiles;
         const int nt = rest % args.n_tiles;
@@ -164,8 +202,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
-      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, sslot = 0, sph = 0;
+      int u = 0;
+      for (bool first = true;; first = false) {
+        consumer_next(sslot, sph, u, first, true);
+        if (u >= units) break;
         const int rest = u / args.m_tiles;
         const int sp = rest / args.n_tiles;
         const int kb0 = sp * args.kb_per_split;
@@ -193,9 +234,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    uint32_t acc = 0, acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    // 8 warps: warp w may only touch TMEM lanes 32*(w%4).. (its quadrant q); the two
+    // warps of a quadrant split the tile's 256 columns into halves.
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int cbeg = half * (BN / 2);
+    uint32_t acc = 0, acc_phase = 0, sslot = 0, sph = 0;
+    int u = 0;
+    for (bool first = true;; first = false) {
+      consumer_next(sslot, sph, u, first, false);
+      if (u >= units) break;
       const int mt = u % args.m_tiles;
       const int rest = u / args.m_tiles;
       const int nt = rest % args.n_tiles;
@@ -205,6 +253,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int64_t col0 = static_cast<int64_t>(nt) * BN;
       const int64_t rem = args.N - col0;
       const int ncols = rem < BN ? static_cast<int>(rem) : BN;
+      const int cend = ncols < cbeg + BN / 2 ? ncols : cbeg + BN / 2;  // this warp: [cbeg, cend)
 
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -217,7 +266,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         cur.k = row_ok ? args.k_max : 0;
         cur.limit = args.N;
         cur.gid0 = args.col_gid0;
-        cur.seek(col0);
+        cur.seek(col0 + cbeg);
         float mrun = -INFINITY, srun = 0.f, usum = 0.f;
         float coef = 0.f, lse2 = 0.f;
         if constexpr (EPI == EPI_BWD_DZ) {
@@ -227,9 +276,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             lse2 = __ldg(args.row_lse + row) * kLog2e;
           }
         }
-        for (int c = 0; c < BN / 32; ++c) {
-          const int cb = c * 32;
-          if (cb >= ncols) break;  // warp-uniform
+        for (int cb = cbeg; cb < cend; cb += 32) {  // warp-uniform bounds
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + cb, r);
           tmem_ld_wait();
@@ -261,64 +308,57 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               cur.advance();
             }
           } else {
-            float(&dz)[32] = z;  // in place: dz overwrites z
 #pragma unroll
-            for (int j = 0; j < 32; ++j) dz[j] = coef * ex2_approx(fmaf(z[j], kLog2e, -lse2));
+            for (int j = 0; j < 32; ++j) z[j] = coef * ex2_approx(fmaf(z[j], kLog2e, -lse2));
             while (cur.nxt < col0 + cb + 32) {
               const int jj = static_cast<int>(cur.nxt - col0 - cb);
+              const float sub = coef * cur.nxt_p;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) dz[j] = (j == jj) ? dz[j] - coef * cur.nxt_p : dz[j];
+              for (int j = 0; j < 32; ++j) z[j] = (j == jj) ? z[j] - sub : z[j];
               cur.advance();
             }
             if (row_ok) {
               __nv_bfloat16* dst = args.dzT + (col0 + cb) * args.ld_dzT + row;
-              if (full) {
+              const int nj = full ? 32 : ncols - cb;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) dst[j * args.ld_dzT] = __float2bfloat16_rn(dz[j]);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (cb + j < ncols) dst[j * args.ld_dzT] = __float2bfloat16_rn(dz[j]);
-              }
+              for (int j = 0; j < 32; ++j)
+                if (j < nj) dst[j * args.ld_dzT] = __float2bfloat16_rn(z[j]);
             }
           }
         }
         if constexpr (EPI == EPI_FWD_STATS) {
-          if (row_ok) {
-            const int64_t o = row * args.n_tiles + nt;
+          if (row_ok) {  // partial slot (vocab tile, column half); empty halves are neutral
+            const int64_t o = row * (2 * args.n_tiles) + 2 * nt + half;
             args.p_max[o] = mrun;
             args.p_sum[o] = srun;
             args.p_u[o] = usum;
           }
         }
       } else {  // EPI_STORE_F32
-        // TMEM gives thread = row; transpose each 32x32 fp32 block through this warp's
-        // smem slice so every store instruction writes four full 128 B row segments.
+        // TMEM gives thread = row; transpose each 32x16 fp32 block through this warp's
+        // smem slice so a store instruction writes eight full 64 B row segments.
         float* stg = stage_f32 + (warp - 2) * (32 * kStgLd);
         float* obase = args.out + static_cast<int64_t>(sp) * args.split_stride;
         const bool vec_ok = ((args.ld_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0);
         const int64_t row_base = static_cast<int64_t>(mt) * BM + q * 32;
-        for (int c = 0; c < BN / 32; ++c) {
-          const int cb = c * 32;
-          if (cb >= ncols) break;
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + cb, r);
+        for (int cb = cbeg; cb < cend; cb += 16) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(taddr + cb, r);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
+          for (int j = 0; j < 16; j += 4)
             *reinterpret_cast<float4*>(stg + lane * kStgLd + j) =
                 make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
                             __uint_as_float(r[j + 3]));
           __syncwarp();
 #pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int rl = it * 4 + (lane >> 3);
-            const int cc = (lane & 7) * 4;
+          for (int it = 0; it < 4; ++it) {
+            const int rl = it * 8 + (lane >> 2);
+            const int cc = (lane & 3) * 4;
             const int64_t grow = row_base + rl;
-            const int64_t gcol = col0 + cb + cc;
             if (grow < args.M && cb + cc < ncols) {
               float4 v = *reinterpret_cast<const float4*>(stg + rl * kStgLd + cc);
-              float* dst = obase + grow * args.ld_out + gcol;
+              float* dst = obase + grow * args.ld_out + col0 + cb + cc;
               if (vec_ok && cb + cc + 4 <= ncols) {
                 if (args.accumulate) {
                   const float4 o = *reinterpret_cast<const float4*>(dst);

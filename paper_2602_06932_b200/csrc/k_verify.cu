@@ -75,19 +75,46 @@ __device__ __forceinline__ float max8(const uint4& w) {
                                             *reinterpret_cast<const __nv_bfloat162*>(&w.w)));
   return fmaxf(__low2float(m2), __high2float(m2));
 }
-// Offer the 8 bf16 of lanes in `mask` (each lane's vector starts at column col_of_lane).
-__device__ __forceinline__ void offer_vectors(WarpList& L, uint32_t mask, const uint4& w, int64_t col) {
-  while (mask) {
-    const int src = __ffs(mask) - 1;
-    mask &= mask - 1;
-    const int64_t c0 = __shfl_sync(0xffffffffu, col, src);
-#pragma unroll 1
-    for (int e = 0; e < 8; ++e) {
-      const uint32_t word = pick4(w, e >> 1);
-      const float myv = (e & 1) ? bf16_hi(word) : bf16_lo(word);
-      L.offer(myv, static_cast<int32_t>(c0 + e), src);
-    }
+// Order-preserving float <-> int map (signed-int order == float order) for smem atomicMax.
+__device__ __forceinline__ int f2ord(float f) { const int i = __float_as_int(f); return i >= 0 ? i : i ^ 0x7FFFFFFF; }
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+__device__ __forceinline__ float elem8(const uint4& w, int e) {
+  const uint32_t word = pick4(w, e >> 1);
+  return (e & 1) ? bf16_hi(word) : bf16_lo(word);
+}
+// Each lane holds one 8-element vector starting at column `col`.  Elements >= floor
+// are offered one by one (warp-uniform order); the exact (value, index) admission test
+// against the list's k-th entry happens at insertion.
+__device__ __forceinline__ void offer_vectors(WarpList& L, bool lane_hit, const uint4& w, int64_t col, float floor) {
+  uint32_t my = 0;
+  if (lane_hit) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) my |= (elem8(w, e) >= fmaxf(floor, L.thr_v) ? 1u : 0u) << e;
   }
+  uint32_t lanes = __ballot_sync(0xffffffffu, my != 0);
+  while (lanes) {
+    const int src = __ffs(lanes) - 1;
+    const int e = __shfl_sync(0xffffffffu, __ffs(my) - 1, src);
+    const float cv = __shfl_sync(0xffffffffu, elem8(w, e), src);
+    const int32_t ci = static_cast<int32_t>(__shfl_sync(0xffffffffu, col, src) + e);
+    if (threadIdx.x % 32 == static_cast<unsigned>(src)) my &= my - 1;
+    if (cv >= floor && L.admits(cv, ci)) L.insert(cv, ci);
+    lanes = __ballot_sync(0xffffffffu, my != 0);
+  }
+}
+// k-th largest of the 32 lane values (k <= 32): a valid lower bound for the k-th best
+// element when every lane value is itself an element.
+__device__ __forceinline__ float warp_kth_largest(float x, int k) {
+  float kth = -INFINITY;
+  for (int r = 0; r < k; ++r) {
+    float m = x;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    kth = m;
+    const uint32_t eq = __ballot_sync(0xffffffffu, x == m);
+    if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(eq) - 1)) x = -INFINITY;
+  }
+  return kth;
 }
 __device__ __forceinline__ uint4 ld_nc_v4(const uint4* p) {
   uint4 r;
@@ -114,24 +141,43 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
   WarpList L;
   L.init(k);
   uint32_t bad = 0;
+  __shared__ int s_floor;  // max over warps of their k-th value: a CTA-wide admission floor
+  if (threadIdx.x == 0) s_floor = f2ord(-INFINITY);
+  __syncthreads();
+  float floor = -INFINITY;
 
   const bool aligned = ((reinterpret_cast<uintptr_t>(T + c0) & 15) == 0);
   const int64_t nvec = aligned ? (c1 - c0) >> 3 : 0;
   const uint4* src = reinterpret_cast<const uint4*>(T + c0);
   constexpr int U = 4;
-  // vector v of this segment is handled by warp (v / 32) % 8 ... interleaved by 256
+  // vectors are interleaved: warp w handles [w*32 + i*256, +32) for i = 0, 1, ...
   int64_t base = static_cast<int64_t>(warp) * 32;
+  bool first = true;
   for (; base + (U - 1) * 256 + 31 < nvec; base += U * 256) {
     uint4 w[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) w[u] = ld_nc_v4(src + base + u * 256 + lane);
+    float gm[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       bad |= nonfinite8(w[u]);
-      const float gm = max8(w[u]);
-      const uint32_t hit = __ballot_sync(0xffffffffu, gm >= L.thr_v);
-      if (hit) offer_vectors(L, hit, w[u], c0 + (base + u * 256 + lane) * 8);
+      gm[u] = max8(w[u]);
     }
+    if (first) {  // warm start: k-th largest lane maximum is <= the k-th best element
+      first = false;
+      float lm = gm[0];
+#pragma unroll
+      for (int u = 1; u < U; ++u) lm = fmaxf(lm, gm[u]);
+      floor = fmaxf(floor, warp_kth_largest(lm, k));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool h = gm[u] >= fmaxf(floor, L.thr_v);
+      if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, w[u], c0 + (base + u * 256 + lane) * 8, floor);
+    }
+    // share this warp's k-th value with the CTA; pick up the others'
+    if (lane == 0 && L.thr_v > floor) atomicMax(&s_floor, f2ord(L.thr_v));
+    floor = fmaxf(floor, ord2f(*reinterpret_cast<volatile int*>(&s_floor)));
   }
   for (; base < nvec; base += 256) {
     const int64_t vi = base + lane;
@@ -141,8 +187,8 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
       bad |= nonfinite8(w);
     }
     const float gm = max8(w);
-    const uint32_t hit = __ballot_sync(0xffffffffu, vi < nvec && gm >= L.thr_v);
-    if (hit) offer_vectors(L, hit, w, c0 + vi * 8);
+    const bool h = vi < nvec && gm >= fmaxf(floor, L.thr_v);
+    if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, w, c0 + vi * 8, floor);
   }
   // scalar tail (or whole segment when the row start is not 16 B aligned)
   for (int64_t cb = c0 + nvec * 8 + static_cast<int64_t>(warp) * 32; cb < c1; cb += 256) {
@@ -153,7 +199,7 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
       bad |= static_cast<uint32_t>((b & 0x7FFFu) >= 0x7F80u);
       v = __uint_as_float(b << 16);
     }
-    uint32_t hit = __ballot_sync(0xffffffffu, col < c1 && L.admits(v, static_cast<int32_t>(col)));
+    uint32_t hit = __ballot_sync(0xffffffffu, col < c1 && v >= floor && L.admits(v, static_cast<int32_t>(col)));
     while (hit) {
       const int s = __ffs(hit) - 1;
       hit &= hit - 1;

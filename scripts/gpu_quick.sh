@@ -15,3 +15,7 @@ fi
 if [ -n "$NCU_FULL" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$NCU_FULL" -s ${NCU_SKIP:-0} -c ${NCU_COUNT:-3} -o gpurun_out/prof_full python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo ncu2_rc=$?
 fi
+if [ -n "$MICRO" ]; then
+  timeout 300 python scripts/gemm_microbench.py > gpurun_out/micro.jsonl 2>&1; echo micro_rc=$?
+  cat gpurun_out/micro.jsonl
+fi

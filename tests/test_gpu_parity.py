@@ -274,3 +274,68 @@ def test_large_config_sampled_parity(name):
     dW = out["dW"].double()
     colsum = dW.sum(0).abs().max().item()
     assert colsum <= 2e-2 * dW.abs().sum(0).max().item()
+
+
+def test_single_rank_comm_runs_every_exchange_identically():
+    """A 1-rank NCCL communicator runs C1-C5 as identity collectives: results must be
+    bit-identical to the comm-less path (exercises dlopen'd NCCL, CommSplit, AllGather,
+    AllReduce on the caller's stream)."""
+    tr = tracegen.gen_trace("small_tree")
+    base = _run_gpu(tr)
+    uid = A.aurora_comm_get_unique_id()
+    comm = A.aurora_comm_create(uid, 1, 0, 1, 1)
+    try:
+        out = _run_gpu(tr, comm=comm)
+        for k in ("target_argmax", "accept_len", "row_class", "sup_idx", "sup_p", "row_w", "row_lse", "loss"):
+            assert torch.equal(getattr(out["st"], k), getattr(base["st"], k)), k
+        assert torch.equal(out["dW"], base["dW"]) and torch.equal(out["dH"], base["dH"])
+    finally:
+        A.aurora_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("cuts", [(2600,), (1000, 2049, 4100)])
+def test_emulated_vocab_parallel_shards(cuts):
+    """VP shard maths on one GPU through the C-ABI: global labels, then per-shard fwd
+    with vocab_offset (support entries outside the shard, shard sizes not multiples of
+    256), host combine of the per-shard (lse, u) exactly as C3 does, per-shard bwd with
+    the global lse, dW shards concatenated and dH summed (C4)."""
+    tr = tracegen.gen_trace("small")
+    ref = oracle.step(tr)
+    c = tr["cfg"]
+    full = _run_gpu(tr, want_grads=False)
+    st, g = full["st"], full["g"]
+    bounds = [0, *cuts, c.V]
+    lses, us = [], []
+    M = c.M
+    for v0, v1 in zip(bounds[:-1], bounds[1:]):
+        Ws = g["W"][v0:v1].contiguous()
+        row_lse = torch.empty(M, device="cuda")
+        row_loss = torch.empty(M, device="cuda")
+        loss = torch.empty(1, device="cuda")
+        A.aurora_spec_loss_fwd(g["H"], Ws, M, c.d, v1 - v0, v0, st.labels, row_lse, row_loss, loss,
+                               st.ws.data_ptr(), st.ws_bytes)
+        torch.cuda.synchronize()
+        lses.append(row_lse.double())
+        us.append(row_lse.double() + st.row_H.double() - row_loss.double())   # u_p = lse_p + H~ - l_p
+    L = torch.stack(lses)
+    lse = torch.logsumexp(L, 0)
+    pad = st.row_class == A.ROW_PAD
+    row_loss = torch.where(pad, torch.zeros_like(lse), lse - torch.stack(us).sum(0) + st.row_H.double())
+    loss = float((st.row_w.double() * row_loss).sum())
+    assert abs(loss - ref["loss"]) <= 1e-3 * abs(ref["loss"])
+    np.testing.assert_allclose(lse.cpu().numpy(), ref["lse"], rtol=2e-5)
+    glse = lse.float().contiguous()
+    dH = torch.zeros(M, c.d, device="cuda", dtype=torch.float64)
+    dWs = []
+    for v0, v1 in zip(bounds[:-1], bounds[1:]):
+        Ws = g["W"][v0:v1].contiguous()
+        dHp = torch.empty(M, c.d, device="cuda")
+        dWp = torch.empty(v1 - v0, c.d, device="cuda")
+        A.aurora_spec_loss_bwd(g["H"], Ws, M, c.d, v1 - v0, v0, st.labels, glse, None, dHp, dWp, False, False,
+                               st.ws.data_ptr(), st.ws_bytes)
+        torch.cuda.synchronize()
+        dH += dHp.double()
+        dWs.append(dWp)
+    dW = torch.cat(dWs, 0)
+    assert _rfro(dW.cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert _rfro(dH.cpu().numpy(), ref["dH"]) <= GRAD_RFRO

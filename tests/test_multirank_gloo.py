@@ -1,0 +1,180 @@
+"""World-size-2 gloo tests of the multi-GPU exchange plan (-m "not gpu").
+
+The CUDA library exchanges exactly these quantities over NCCL:
+  VP (vocab-parallel): C1 allgather of each rank's top-k (value, global id) list,
+      merged in global (value desc, index asc) order; C3 allgather of per-row
+      (m, s, u); C4 allreduce of dH.  dW stays sharded.
+  DP (data-parallel over requests): C2 allreduce of (N_A, N_D); C5 allreduce of dW;
+      loss allreduce.
+Here two CPU processes run the per-shard maths in f64 and the real torch.distributed
+collectives (gloo), and must reproduce the single-process oracle on the whole batch.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import tracegen
+
+WS = 2
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _vp_worker(rank, port, name, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WS)
+    try:
+        tr = tracegen.gen_trace(name)
+        V, M = tr["V"], tr["M"]
+        # shard on a non-tile boundary on purpose
+        cut = V // 2 + 37
+        v0, v1 = (0, cut) if rank == 0 else (cut, V)
+        T = oracle.bf16_bits_to_f64(tr["T_bits"])
+        k = 10
+        # C1: local top-k (global ids) -> allgather -> global merge
+        _, tk, _ = oracle.target_scan(T[:, v0:v1], k)
+        vals = np.take_along_axis(T[:, v0:v1], tk, axis=1)
+        ids = tk + v0
+        gv = [torch.zeros(M, k, dtype=torch.float64) for _ in range(WS)]
+        gi = [torch.zeros(M, k, dtype=torch.int64) for _ in range(WS)]
+        dist.all_gather(gv, torch.from_numpy(vals))
+        dist.all_gather(gi, torch.from_numpy(ids))
+        allv = torch.cat(gv, 1).numpy()
+        alli = torch.cat(gi, 1).numpy()
+        order = np.lexsort((alli, -allv), axis=1)
+        top = np.take_along_axis(alli, order, 1)[:, :k]
+        am = top[:, 0]
+        lab = oracle.verify(tr["draft_tokens"], tr["parents"], tr["num_nodes"], am)
+        tg = oracle.row_targets(lab["row_class"], lambda m: T[m], top)
+        # C3: per-row (m, s, u) over this shard -> allgather -> combine in rank order
+        H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+        W = tr["W_bits"]
+        Z = H64 @ oracle.bf16_bits_to_f64(W[v0:v1]).T
+        mx = Z.max(1)
+        s = np.exp(Z - mx[:, None]).sum(1)
+        u = np.zeros(M)
+        for m in range(M):
+            S = tg["sup_idx"][m]
+            sel = (S >= v0) & (S < v1)
+            u[m] = float(np.dot(tg["sup_p"][m][sel], Z[m, S[sel] - v0]))
+        msu = torch.from_numpy(np.stack([mx, s, u], 1))
+        g = [torch.zeros_like(msu) for _ in range(WS)]
+        dist.all_gather(g, msu)
+        m_all = np.stack([x.numpy()[:, 0] for x in g])
+        s_all = np.stack([x.numpy()[:, 1] for x in g])
+        u_all = np.stack([x.numpy()[:, 2] for x in g])
+        mm = m_all.max(0)
+        lse = mm + np.log((s_all * np.exp(m_all - mm)).sum(0))
+        Hs = np.array([tg["H"][m] for m in range(M)])
+        w = np.array([tg["w"][m] for m in range(M)])
+        row_loss = np.where(lab["row_class"] == oracle.PAD, 0.0, lse - u_all.sum(0) + Hs)
+        loss = float(np.dot(w, row_loss))
+        # bwd on the shard with the global lse; C4 allreduce dH
+        dZ = np.exp(Z - lse[:, None]) * w[:, None]
+        for m in range(M):
+            S = tg["sup_idx"][m]
+            sel = (S >= v0) & (S < v1)
+            dZ[m, S[sel] - v0] -= w[m] * tg["sup_p"][m][sel]
+        dW_shard = dZ.T @ H64
+        dH = torch.from_numpy(dZ @ oracle.bf16_bits_to_f64(W[v0:v1]))
+        dist.all_reduce(dH)
+        if rank == 0:
+            q.put(dict(am=am, accept_len=lab["accept_len"], loss=loss, lse=lse, dH=dH.numpy(),
+                       dW0=dW_shard, sup=[tg["sup_idx"][m] for m in range(M)]))
+        else:
+            q.put(dict(dW1=dW_shard))
+    finally:
+        dist.destroy_process_group()
+
+
+def _dp_worker(rank, port, name, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WS)
+    try:
+        tr = tracegen.gen_trace(name)
+        R, N = tr["R"], tr["N"]
+        r0, r1 = (0, R // 2) if rank == 0 else (R // 2, R)
+        rows = slice(r0 * (N + 1), r1 * (N + 1))
+        sub = dict(tr)
+        sub["draft_tokens"] = tr["draft_tokens"][r0:r1]
+        sub["parents"] = None if tr["parents"] is None else tr["parents"][r0:r1]
+        sub["num_nodes"] = None if tr["num_nodes"] is None else tr["num_nodes"][r0:r1]
+        T = oracle.bf16_bits_to_f64(tr["T_bits"][rows])
+        am, tk, _ = oracle.target_scan(T, 10)
+        lab = oracle.verify(sub["draft_tokens"], sub["parents"], sub["num_nodes"], am)
+        # C2: global counts -> weights
+        cnt = torch.tensor([int((lab["row_class"] == 0).sum()), int((lab["row_class"] == 1).sum())])
+        dist.all_reduce(cnt)
+        tg = oracle.row_targets(lab["row_class"], lambda m: T[m], tk)
+        na, nd = int(cnt[0]), int(cnt[1])
+        for m in tg["w"]:
+            c = lab["row_class"][m]
+            tg["w"][m] = 1.0 / na if c == 0 else (1.0 / nd if c == 1 else 0.0)
+        H64 = oracle.bf16_bits_to_f64(tr["H_bits"][rows])
+        fw = oracle.loss_fwd(H64, tr["W_bits"], tg)
+        bw = oracle.loss_bwd(H64, tr["W_bits"], tg, fw["lse"])
+        loss = torch.tensor([fw["loss"]], dtype=torch.float64)
+        dist.all_reduce(loss)
+        dW = torch.from_numpy(bw["dW"])
+        dist.all_reduce(dW)            # C5
+        if rank == 0:
+            q.put(dict(loss=float(loss.item()), dW=dW.numpy(), dH0=bw["dH"]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(fn, name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=fn, args=(r, port, name, q)) for r in range(WS)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=300) for _ in range(1 if fn is _dp_worker else WS)]
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    merged = {}
+    for o in outs:
+        merged.update(o)
+    return merged
+
+
+@pytest.mark.parametrize("name", ["small", "small_tree"])
+def test_vp2_exchange_reproduces_single_rank(name):
+    out = _spawn(_vp_worker, name)
+    tr = tracegen.gen_trace(name)
+    ref = oracle.step(tr)
+    np.testing.assert_array_equal(out["am"], ref["argmax"])               # C1: bit-exact global labels
+    np.testing.assert_array_equal(out["accept_len"], ref["accept_len"])
+    for m in range(tr["M"]):
+        np.testing.assert_array_equal(out["sup"][m], ref["targets"]["sup_idx"][m])
+    np.testing.assert_allclose(out["lse"], ref["lse"], rtol=1e-12)        # C3
+    assert abs(out["loss"] - ref["loss"]) <= 1e-11 * abs(ref["loss"])
+    np.testing.assert_allclose(out["dH"], ref["dH"], rtol=1e-10, atol=1e-14)   # C4
+    dW = np.concatenate([out["dW0"], out["dW1"]], 0)
+    np.testing.assert_allclose(dW, ref["dW"], rtol=1e-10, atol=1e-14)
+
+
+def test_dp2_exchange_reproduces_single_rank():
+    out = _spawn(_dp_worker, "small")
+    tr = tracegen.gen_trace("small")
+    ref = oracle.step(tr)
+    assert abs(out["loss"] - ref["loss"]) <= 1e-11 * abs(ref["loss"])      # C2 + loss allreduce
+    np.testing.assert_allclose(out["dW"], ref["dW"], rtol=1e-10, atol=1e-14)   # C5
+    half = (tr["R"] // 2) * (tr["N"] + 1)
+    np.testing.assert_allclose(out["dH0"], ref["dH"][:half], rtol=1e-10, atol=1e-14)
