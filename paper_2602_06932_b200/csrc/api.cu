@@ -130,11 +130,11 @@ int scan_nseg(int64_t M, int64_t V_local) {
   nseg = std::min<int64_t>(nseg, cdiv(V_local, 2048));
   return static_cast<int>(std::max<int64_t>(nseg, 1));
 }
-// dLogits chunk width: 1/8 of the local vocab, double-buffered => at most 1/4 of the
-// local [M x V_local] dLogits is live at any time.
+// dLogits chunk width: 1/4 of the local vocab (one buffer) => at most 1/4 of the local
+// [M x V_local] dLogits is live at any time.
 int64_t chunk_cols(int64_t V_local) {
-  if (V_local <= 8 * BN) return rup(cdiv(V_local, 2), BN);
-  return rup(cdiv(V_local, 8), BN);
+  if (V_local <= 4 * BN) return rup(V_local, BN);
+  return rup(cdiv(V_local, 4), BN);
 }
 // split-K factor for dH: the (m, n) tile count is small (M x d output) so pick the
 // split that fills whole waves of 148 SMs best (fewest splits within 3% of the best).
@@ -174,14 +174,13 @@ FwdWs carve_fwd(Carver& c, int64_t M, int64_t V_local) {
   return w;
 }
 constexpr int kCounters = 64;  // dynamic-scheduler tile counters (one per launch in a call)
-struct BwdWs { int32_t* counters; __nv_bfloat16* dzT[2]; float* dh_part; int64_t vc, m_pad; int splits; };
+struct BwdWs { int32_t* counters; __nv_bfloat16* dzT; float* dh_part; int64_t vc, m_pad; int splits; };
 BwdWs carve_bwd(Carver& c, int64_t M, int64_t d, int64_t V_local) {
   BwdWs w;
   w.counters = c.take<int32_t>(kCounters);
   w.vc = chunk_cols(V_local);
   w.m_pad = rup(M, 8);
-  w.dzT[0] = c.take<__nv_bfloat16>(w.vc * w.m_pad);
-  w.dzT[1] = c.take<__nv_bfloat16>(w.vc * w.m_pad);
+  w.dzT = c.take<__nv_bfloat16>(w.vc * w.m_pad);
   w.splits = dh_splits(M, d, cdiv(w.vc, BK));
   w.dh_part = w.splits > 1 ? c.take<float>(static_cast<int64_t>(w.splits) * M * d) : nullptr;
   return w;
@@ -206,8 +205,9 @@ bool labels_ok(const aurora_labels_t* l, bool verify_outputs) {
     return false;
   return true;
 }
-// Library-owned side streams and events (per device, created once) for the
-// concurrent bwd: dW(c) and dH(c) overlap dz(c+1) on the caller's stream.
+// Library-owned side streams and events (per device, created once) for the bwd:
+// dW(c) (HBM-store-bound) and dH(c) (tensor-bound) run concurrently on two side
+// streams; dz(c+1) on the caller's stream waits for both (single chunk buffer).
 struct SideStreams {
   cudaStream_t s[2] = {nullptr, nullptr};
   cudaEvent_t ev[160];
@@ -507,15 +507,15 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
   for (int64_t ch = 0; ch < nchunks; ++ch) {
     const int64_t c0 = ch * w.vc;
     const int64_t vc = std::min(w.vc, V_local - c0);
-    __nv_bfloat16* dzT = w.dzT[ch & 1];
+    __nv_bfloat16* dzT = w.dzT;
     CUtensorMap tmW_k, tmW_mn, tmZ_k, tmZ_mn;
     if (!make_tmap_bf16(&tmW_k, Wb + c0 * d, d, vc, d, 64, BN)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmW_mn, Wb + c0 * d, d, vc, d, 64, 64)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmZ_k, dzT, M, vc, w.m_pad, 64, BM)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmZ_mn, dzT, M, vc, w.m_pad, 64, 64)) return AURORA_ERR_CUDA;
-    if (S && ch >= 2) {  // the buffer dz(ch) overwrites was read by dW(ch-2), dH(ch-2)
-      cudaStreamWaitEvent(s, ev[2 + 3 * (ch - 2)], 0);
-      cudaStreamWaitEvent(s, ev[3 + 3 * (ch - 2)], 0);
+    if (S && ch >= 1) {  // dz(ch) overwrites the chunk buffer read by dW(ch-1), dH(ch-1)
+      cudaStreamWaitEvent(s, ev[2 + 3 * (ch - 1)], 0);
+      cudaStreamWaitEvent(s, ev[3 + 3 * (ch - 1)], 0);
     }
 
     // A7: recompute Z tiles, dz -> dZ^T chunk (bf16)
@@ -560,6 +560,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     b.ld_out = d;
     b.accumulate = accumulate_dW ? 1 : 0;
     b.tile_counter = w.counters + 3 * ch + 1;
+    b.n_fastest = 1;  // A = dZ^T chunk (M x vc, may exceed L2) streams once; H (B) stays in L2
     prof_begin(PH_BWD_DW, sW);
     e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW);
     prof_end(PH_BWD_DW, sW);

@@ -51,6 +51,7 @@ struct GemmArgs {
   __nv_bfloat16* dzT;    // [N_chunk, ld_dzT] transposed dLogits chunk (bwd)
   int64_t ld_dzT;
   int32_t* tile_counter;  // nullable: dynamic tile scheduler counter (zero before first use)
+  int32_t n_fastest;      // tile raster: 0 = m-fastest (B streams once), 1 = n-fastest (A streams once)
 };
 
 // Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.

@@ -48,6 +48,22 @@ __device__ __forceinline__ float select32(const float (&z)[32], int j) {
   return v;
 }
 
+// Tile raster: m-fastest (default: consecutive units share the B tile, so the large B
+// operand streams once) or n-fastest (the large operand is A, e.g. dZ^T in the dW GEMM).
+__device__ __forceinline__ void decode_unit(const GemmArgs& a, int u, int& mt, int& nt, int& sp) {
+  if (a.n_fastest) {
+    nt = u % a.n_tiles;
+    const int rest = u / a.n_tiles;
+    mt = rest % a.m_tiles;
+    sp = rest / a.m_tiles;
+  } else {
+    mt = u % a.m_tiles;
+    const int rest = u / a.m_tiles;
+    nt = rest % a.n_tiles;
+    sp = rest / a.n_tiles;
+  }
+}
+
 struct SupCursor {
   const int32_t* idx;
   const float* p;
@@ -169,10 +185,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (++sslot == kSchedDepth) { sslot = 0; sph ^= 1; }
         }
         if (u >= units) break;
-        const int mt = u % args.m_tiles;
-        const int rest = u / args.m_tiles;
-        const int nt = rest % args.n_tiles;
-        const int sp = rest / args.n_tiles;
+        int mt, nt, sp;
+        decode_unit(args, u, mt, nt, sp);
         const int kb0 = sp * args.kb_per_split;
         const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -207,8 +221,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (bool first = true;; first = false) {
         consumer_next(sslot, sph, u, first, true);
         if (u >= units) break;
-        const int rest = u / args.m_tiles;
-        const int sp = rest / args.n_tiles;
+        int mt, nt, sp;
+        decode_unit(args, u, mt, nt, sp);
         const int kb0 = sp * args.kb_per_split;
         const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -244,10 +258,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (bool first = true;; first = false) {
       consumer_next(sslot, sph, u, first, false);
       if (u >= units) break;
-      const int mt = u % args.m_tiles;
-      const int rest = u / args.m_tiles;
-      const int nt = rest % args.n_tiles;
-      const int sp = rest / args.n_tiles;
+      int mt, nt, sp;
+      decode_unit(args, u, mt, nt, sp);
       const int64_t row = static_cast<int64_t>(mt) * BM + q * 32 + lane;
       const bool row_ok = row < args.M;
       const int64_t col0 = static_cast<int64_t>(nt) * BN;
@@ -337,7 +349,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       } else {  // EPI_STORE_F32
         // TMEM gives thread = row; transpose each 32x16 fp32 block through this warp's
         // smem slice so a store instruction writes eight full 64 B row segments.
-        float* stg = stage_f32 + (warp - 2) * (32 * kStgLd);
+        const uint32_t stg = smem_u32(stage_f32 + (warp - 2) * (32 * kStgLd));  // explicit .shared
         float* obase = args.out + static_cast<int64_t>(sp) * args.split_stride;
         const bool vec_ok = ((args.ld_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0);
         const int64_t row_base = static_cast<int64_t>(mt) * BM + q * 32;
@@ -347,9 +359,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(stg + lane * kStgLd + j) =
-                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                            __uint_as_float(r[j + 3]));
+            sts128(stg + (lane * kStgLd + j) * 4, __uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                   __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
           __syncwarp();
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int cc = (lane & 3) * 4;
             const int64_t grow = row_base + rl;
             if (grow < args.M && cb + cc < ncols) {
-              float4 v = *reinterpret_cast<const float4*>(stg + rl * kStgLd + cc);
+              float4 v = lds128(stg + (rl * kStgLd + cc) * 4);
               float* dst = obase + grow * args.ld_out + col0 + cb + cc;
               if (vec_ok && cb + cc + 4 <= ncols) {
                 if (args.accumulate) {
