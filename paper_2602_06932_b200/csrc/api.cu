@@ -29,7 +29,7 @@ cudaEvent_t ev_get() {
   return e;
 }
 const char* kPhaseNames[PH_COUNT] = {"target_scan", "verify", "fwd_gemm", "fwd_combine", "bwd_dz_gemm",
-                                     "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm"};
+                                     "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm", "bwd_fused"};
 }  // namespace
 
 void prof_begin(int phase, cudaStream_t s) {
@@ -186,6 +186,45 @@ BwdWs carve_bwd(Carver& c, int64_t M, int64_t d, int64_t V_local) {
   return w;
 }
 
+// ---- fused bwd layout: counters, two 1/8-vocab dZ^T buffers, dH split partials
+int64_t fused_chunk_cols(int64_t V_local) {
+  if (V_local <= 8 * BN) return rup(cdiv(V_local, 2), BN);
+  return rup(cdiv(V_local, 8), BN);
+}
+int fused_dh_splits(int64_t M, int64_t d, int64_t kb_total) {
+  const int64_t tiles = cdiv(M, BM) * cdiv(d, BN);
+  int64_t s = std::min<int64_t>(std::max<int64_t>(cdiv(kNumSMs, tiles), 1), 8);
+  return static_cast<int>(std::max<int64_t>(std::min<int64_t>(s, kb_total), 1));
+}
+struct FusedWs {
+  int32_t* counters;  // [0] tile counter, [1..16] dz_done, [17..32] rd_done, [33..] dh flags
+  int n_counters;
+  __nv_bfloat16* dzT[2];
+  float* dh_part;
+  int64_t vc, m_pad;
+  int splits;
+};
+FusedWs carve_fused(Carver& c, int64_t M, int64_t d, int64_t V_local) {
+  FusedWs w;
+  w.vc = fused_chunk_cols(V_local);
+  w.m_pad = rup(M, 8);
+  w.splits = fused_dh_splits(M, d, cdiv(w.vc, BK));
+  w.n_counters = 1 + 2 * kMaxChunks + static_cast<int>(cdiv(M, BM) * cdiv(d, BN)) * w.splits;
+  w.counters = c.take<int32_t>(w.n_counters);
+  w.dzT[0] = c.take<__nv_bfloat16>(w.vc * w.m_pad);
+  w.dzT[1] = c.take<__nv_bfloat16>(w.vc * w.m_pad);
+  w.dh_part = w.splits > 1 ? c.take<float>(static_cast<int64_t>(w.splits) * M * d) : nullptr;
+  return w;
+}
+bool classic_bwd() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AURORA_BWD");
+    v = (e && std::strcmp(e, "classic") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 aurora_status_t check_cfg(const aurora_loss_cfg_t* cfg) {
   if (!cfg) return AURORA_ERR_INVALID_ARG;
   if (cfg->k_discard == 0) return AURORA_ERR_UNSUPPORTED;  // dense discard KL (NEXT F2)
@@ -252,6 +291,119 @@ bool ensure_scratch(aurora_comm_t c, size_t bytes) {
 bool gemm_shape_ok(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local) {
   return H && W && M >= 1 && d >= 64 && d % 64 == 0 && V_local >= 1 && al16(H) && al16(W) &&
          M <= (int64_t(1) << 31) / 2 && V_local <= (int64_t(1) << 31) / 2;
+}
+
+// The whole backward as one persistent launch (k_bwd.cu), then the dH split reduce and
+// the VP / DP collectives.
+aurora_status_t bwd_fused(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local, int64_t vocab_offset,
+                          const aurora_labels_t* labels, const float* row_lse, const float* dloss, float* dH,
+                          float* dWf, int accumulate_dW, void* ws, aurora_comm_t comm, cudaStream_t s) {
+  Carver c(ws);
+  FusedWs w = carve_fused(c, M, d, V_local);
+  const int64_t nchunks = cdiv(V_local, w.vc);
+  if (nchunks > kMaxChunks) return AURORA_ERR_UNSUPPORTED;
+  BwdMaps maps;
+  bool ok = make_tmap_bf16(&maps.H_k, H, d, M, d, 64, BM) && make_tmap_bf16(&maps.H_mn, H, d, M, d, 64, 64) &&
+            make_tmap_bf16(&maps.W_k, W, d, V_local, d, 64, BN) && make_tmap_bf16(&maps.W_mn, W, d, V_local, d, 64, 64);
+  for (int b = 0; b < 2; ++b)
+    ok = ok && make_tmap_bf16(&maps.Z_k[b], w.dzT[b], M, w.vc, w.m_pad, 64, BM) &&
+         make_tmap_bf16(&maps.Z_mn[b], w.dzT[b], M, w.vc, w.m_pad, 64, 64);
+  ok = ok && make_tmap_f32_out(&maps.O_W, dWf, d, V_local, d, 1, 0);
+  ok = ok && (w.splits > 1 ? make_tmap_f32_out(&maps.O_H, w.dh_part, d, M, d, w.splits, M * d)
+                           : make_tmap_f32_out(&maps.O_H, dH, d, M, d, 1, 0));
+  if (!ok) return AURORA_ERR_CUDA;
+
+  BwdArgs a{};
+  a.M = M;
+  a.d = d;
+  a.vocab_offset = vocab_offset;
+  a.sup_idx = labels->sup_idx;
+  a.sup_p = labels->sup_p;
+  a.k_max = labels->k_max;
+  a.row_lse = row_lse;
+  a.row_w = labels->row_w;
+  a.dloss = dloss;
+  a.dzT[0] = w.dzT[0];
+  a.dzT[1] = w.dzT[1];
+  a.ld_dzT = w.m_pad;
+  a.accumulate_dW = accumulate_dW ? 1 : 0;
+  a.dh_m_tiles = static_cast<int32_t>(cdiv(M, BM));
+  a.dh_n_tiles = static_cast<int32_t>(cdiv(d, BN));
+  a.tile_counter = w.counters;
+  a.dz_done = w.counters + 1;
+  a.rd_done = w.counters + 1 + kMaxChunks;
+  a.dh_flag = w.counters + 1 + 2 * kMaxChunks;
+  int base = 0;
+  auto add_seg = [&](int type, int ch) {
+    BwdSeg g{};
+    g.type = type;
+    g.chunk = ch;
+    const int64_t vc = a.vc[ch];
+    if (type == BT_DZ) {
+      g.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+      g.n_tiles = static_cast<int32_t>(cdiv(vc, BN));
+      g.kb_total = static_cast<int32_t>(d / BK);
+      g.kb_per_split = g.kb_total;
+    } else if (type == BT_DW) {
+      g.m_tiles = static_cast<int32_t>(cdiv(vc, BM));
+      g.n_tiles = static_cast<int32_t>(cdiv(d, BN));
+      g.kb_total = static_cast<int32_t>(cdiv(M, BK));
+      g.kb_per_split = g.kb_total;
+    } else {
+      g.m_tiles = a.dh_m_tiles;
+      g.n_tiles = a.dh_n_tiles;
+      g.kb_total = static_cast<int32_t>(cdiv(vc, BK));
+      g.kb_per_split = static_cast<int32_t>(cdiv(g.kb_total, w.splits));
+    }
+    const int count = g.m_tiles * g.n_tiles * (type == BT_DH ? w.splits : 1);
+    g.base = base;
+    base += count;
+    if (type == BT_DZ) a.n_dz[ch] = count;
+    else a.n_rd[ch] += count;
+    a.seg[a.nseg++] = g;
+  };
+  for (int64_t ch = 0; ch < nchunks; ++ch) {
+    a.c0[ch] = ch * w.vc;
+    a.vc[ch] = std::min(w.vc, V_local - ch * w.vc);
+  }
+  for (int64_t ch = 0; ch < nchunks; ++ch) {
+    add_seg(BT_DZ, static_cast<int>(ch));
+    if (ch >= 1) {
+      add_seg(BT_DH, static_cast<int>(ch - 1));
+      add_seg(BT_DW, static_cast<int>(ch - 1));
+    }
+  }
+  add_seg(BT_DH, static_cast<int>(nchunks - 1));
+  add_seg(BT_DW, static_cast<int>(nchunks - 1));
+  a.total_units = base;
+  a.nchunks = static_cast<int32_t>(nchunks);
+
+  if (cudaMemsetAsync(w.counters, 0, static_cast<size_t>(w.n_counters) * sizeof(int32_t), s) != cudaSuccess)
+    return AURORA_ERR_CUDA;
+  prof_begin(PH_BWD_FUSED, s);
+  cudaError_t e = launch_bwd_fused(maps, a, s);
+  prof_end(PH_BWD_FUSED, s);
+  if (e != cudaSuccess) return AURORA_ERR_CUDA;
+  if (w.splits > 1) {
+    prof_begin(PH_BWD_REDUCE, s);
+    e = launch_splitk_reduce(w.dh_part, w.splits, M * d, dH, 0, s);
+    prof_end(PH_BWD_REDUCE, s);
+    if (e != cudaSuccess) return AURORA_ERR_CUDA;
+  }
+  auto& A = nccl::api();
+  if (comm && comm->dp_x()) {  // C5: DP gradient allreduce
+    prof_begin(PH_COMM, s);
+    if (A.AllReduce(dWf, dWf, static_cast<size_t>(V_local * d), nccl::ncclFloat32, nccl::ncclSum, comm->dp, s) != 0)
+      return AURORA_ERR_NCCL;
+    prof_end(PH_COMM, s);
+  }
+  if (comm && comm->vp_x()) {  // C4: VP dH allreduce
+    prof_begin(PH_COMM, s);
+    if (A.AllReduce(dH, dH, static_cast<size_t>(M * d), nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0)
+      return AURORA_ERR_NCCL;
+    prof_end(PH_COMM, s);
+  }
+  return AURORA_OK;
 }
 
 }  // namespace
@@ -331,6 +483,9 @@ size_t aurora_workspace_size(int op, int64_t M, int64_t d, int64_t V_local, cons
     Carver c(nullptr);
     carve_bwd(c, M, d, V_local);
     best = std::max(best, c.off);
+    Carver f(nullptr);
+    carve_fused(f, M, d, V_local);
+    best = std::max(best, f.off);
   }
   return rup(static_cast<int64_t>(best), 256) + 256;
 }
@@ -484,9 +639,11 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
   aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float* dWf = static_cast<float*>(dW);
+  if (!classic_bwd()) return bwd_fused(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf,
+                                       accumulate_dW, ws, comm, s);
   Carver c(ws);
   BwdWs w = carve_bwd(c, M, d, V_local);
-  float* dWf = static_cast<float*>(dW);
 
   CUtensorMap tmH_k, tmH_mn;
   if (!make_tmap_bf16(&tmH_k, H, d, M, d, 64, BM)) return AURORA_ERR_CUDA;
@@ -561,8 +718,10 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     b.accumulate = accumulate_dW ? 1 : 0;
     b.tile_counter = w.counters + 3 * ch + 1;
     b.n_fastest = 1;  // A = dZ^T chunk (M x vc, may exceed L2) streams once; H (B) stays in L2
+    CUtensorMap tmOW;
+    const bool ow = make_tmap_f32_out(&tmOW, dWf + c0 * d, d, vc, d, 1, 0);
     prof_begin(PH_BWD_DW, sW);
-    e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW);
+    e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr);
     prof_end(PH_BWD_DW, sW);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (comm && comm->dp_x()) {  // C5: DP gradient allreduce of this dW chunk
@@ -595,8 +754,11 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
       h.out = dH;
       h.accumulate = ch > 0 ? 1 : 0;
     }
+    CUtensorMap tmOH;
+    const bool oh = h.splits > 1 ? make_tmap_f32_out(&tmOH, w.dh_part, d, M, d, h.splits, M * d)
+                                 : make_tmap_f32_out(&tmOH, dH, d, M, d, 1, 0);
     prof_begin(PH_BWD_DH, sH);
-    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, sH);
+    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, sH, oh ? &tmOH : nullptr);
     prof_end(PH_BWD_DH, sH);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (h.splits > 1) {
@@ -688,8 +850,10 @@ aurora_status_t aurora_debug_gemm(int a_mn, int b_mn, const void* A, const void*
   g.N = N;
   g.out = D;
   g.ld_out = ldd;
+  CUtensorMap tc;
+  const bool oc = make_tmap_f32_out(&tc, D, N, M, ldd, 1, 0);
   return cuda_status(launch_umma_gemm(EPI_STORE_F32, a_mn != 0, b_mn != 0, ta, tb, g,
-                                      static_cast<cudaStream_t>(stream)));
+                                      static_cast<cudaStream_t>(stream), oc ? &tc : nullptr));
 }
 
 aurora_status_t aurora_debug_dlogits_rows(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,

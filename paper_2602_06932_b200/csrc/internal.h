@@ -23,8 +23,8 @@ constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA, warp
 constexpr int kSmemA = BM * BK * 2;
 constexpr int kSmemB = BN * BK * 2;
 constexpr int kSchedDepth = 4;  // tile-index ring depth (dynamic scheduler)
-constexpr int kStgLd = 20;  // fp32 staging row stride (floats) for 32x16 blocks: 16 B aligned
-constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 256 /*barriers*/ + kEpiWarps * 32 * kStgLd * 4;
+constexpr int kStgLd = 20;  // fp32 staging row stride (floats) for 32x16 blocks (LSU path)
+constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 1024 /*barriers*/ + kEpiWarps * 2 * 2048;  // epilogue staging: 2 x (32x16 fp32) slots per warp
 
 enum EpiKind : int { EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2 };
 
@@ -52,16 +52,53 @@ struct GemmArgs {
   int64_t ld_dzT;
   int32_t* tile_counter;  // nullable: dynamic tile scheduler counter (zero before first use)
   int32_t n_fastest;      // tile raster: 0 = m-fastest (B streams once), 1 = n-fastest (A streams once)
+  int32_t tma_store;      // set by launch_umma_gemm when an output tensor map is given
 };
 
 // Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.
+// tmC (optional, EPI_STORE_F32 only): fp32 output map from make_tmap_f32_out -> TMA-store
+// epilogue (bulk stores / reduce-add); nullptr -> LSU store path.
 cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                             const GemmArgs& args, cudaStream_t stream);
+                             const GemmArgs& args, cudaStream_t stream, const CUtensorMap* tmC = nullptr);
+bool make_tmap_f32_out(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                       uint64_t depth, uint64_t dstride);
 
 // 2D bf16 tensor map (SWIZZLE_128B) over a row-major [outer, inner] matrix with row
 // stride `ld` elements; box = {box_inner, box_outer}.
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_inner, uint32_t box_outer);
+
+// ---------------------------------------------------------------- fused persistent bwd
+enum BwdType : int { BT_DZ = 0, BT_DH = 1, BT_DW = 2 };
+constexpr int kMaxChunks = 16;
+struct BwdSeg {
+  int32_t type, chunk, m_tiles, n_tiles, kb_total, kb_per_split, base, pad;
+};
+struct BwdMaps {
+  CUtensorMap H_k, H_mn, W_k, W_mn, Z_k[2], Z_mn[2], O_W, O_H;
+};
+struct BwdArgs {
+  int32_t nseg, total_units, nchunks;
+  BwdSeg seg[3 * kMaxChunks];
+  int64_t M, d, vocab_offset;
+  int64_t c0[kMaxChunks], vc[kMaxChunks];
+  int32_t n_dz[kMaxChunks], n_rd[kMaxChunks];
+  const int32_t* sup_idx;
+  const float* sup_p;
+  int32_t k_max;
+  const float* row_lse;
+  const float* row_w;
+  const float* dloss;
+  __nv_bfloat16* dzT[2];
+  int64_t ld_dzT;
+  int32_t accumulate_dW;
+  int32_t dh_m_tiles, dh_n_tiles;
+  int32_t* tile_counter;
+  int32_t* dz_done;
+  int32_t* rd_done;
+  int32_t* dh_flag;
+};
+cudaError_t launch_bwd_fused(const BwdMaps& maps, const BwdArgs& args, cudaStream_t s);
 
 // ---------------------------------------------------------------- verify kernels
 struct VerifyLaunch {
@@ -105,7 +142,7 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 
 // Phase profiling (CUDA events on the caller's stream).
 enum Phase : int { PH_SCAN = 0, PH_VERIFY, PH_FWD_GEMM, PH_FWD_COMBINE, PH_BWD_DZ, PH_BWD_DW, PH_BWD_DH,
-                   PH_BWD_REDUCE, PH_COMM, PH_COUNT };
+                   PH_BWD_REDUCE, PH_COMM, PH_BWD_FUSED, PH_COUNT };
 void prof_begin(int phase, cudaStream_t s);
 void prof_end(int phase, cudaStream_t s);
 

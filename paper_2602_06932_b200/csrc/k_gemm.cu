@@ -20,94 +20,17 @@
 #include <cfloat>
 #include <climits>
 
+#include "gemm_dev.cuh"
 #include "internal.h"
 #include "ptx.cuh"
 
 namespace aur {
 
-namespace {
-constexpr float kLog2e = 1.4426950408889634f;
-
-template <bool MN>
-__device__ __forceinline__ uint64_t operand_desc(uint32_t tile_base, int k) {
-  // K-major SW128: rows of 128 B (64 bf16 of K), 8-row atoms 1024 B apart (SBO);
-  //   advancing K by 16 elements moves the start address by 32 B inside the atom.
-  // MN-major SW128: 64-element MN slices of [BK rows x 128 B] (8 KB, LBO) ;
-  //   8-row K groups 1024 B apart (SBO); advancing K by 16 rows = 2048 B.
-  if constexpr (MN) {
-    return umma_desc_sw128(tile_base + static_cast<uint32_t>(k) * 2048u, BK * 128u, 1024u);
-  } else {
-    return umma_desc_sw128(tile_base + static_cast<uint32_t>(k) * 32u, 16u, 1024u);
-  }
-}
-
-__device__ __forceinline__ float select32(const float (&z)[32], int j) {
-  float v = 0.f;
-#pragma unroll
-  for (int jj = 0; jj < 32; ++jj) v = (jj == j) ? z[jj] : v;
-  return v;
-}
-
-// Tile raster: m-fastest (default: consecutive units share the B tile, so the large B
-// operand streams once) or n-fastest (the large operand is A, e.g. dZ^T in the dW GEMM).
-__device__ __forceinline__ void decode_unit(const GemmArgs& a, int u, int& mt, int& nt, int& sp) {
-  if (a.n_fastest) {
-    nt = u % a.n_tiles;
-    const int rest = u / a.n_tiles;
-    mt = rest % a.m_tiles;
-    sp = rest / a.m_tiles;
-  } else {
-    mt = u % a.m_tiles;
-    const int rest = u / a.m_tiles;
-    nt = rest % a.n_tiles;
-    sp = rest / a.n_tiles;
-  }
-}
-
-struct SupCursor {
-  const int32_t* idx;
-  const float* p;
-  int k;
-  int pos;
-  int64_t nxt;  // local GEMM column of the next support entry (INT64_MAX = none)
-  float nxt_p;
-  int64_t limit;  // valid columns (entries at/after limit are ignored)
-  int64_t gid0;
-  __device__ __forceinline__ void load() {
-    nxt = INT64_MAX;
-    nxt_p = 0.f;
-    while (pos < k) {
-      const int32_t g = idx[pos];
-      if (g == INT32_MAX) { pos = k; break; }
-      const int64_t loc = static_cast<int64_t>(g) - gid0;
-      if (loc >= limit) { pos = k; break; }
-      nxt = loc;
-      nxt_p = p[pos];
-      return;
-    }
-  }
-  // position on the first entry with local column >= col0
-  __device__ __forceinline__ void seek(int64_t col0) {
-    pos = 0;
-    while (pos < k) {
-      const int32_t g = idx[pos];
-      if (g == INT32_MAX) { pos = k; break; }
-      if (static_cast<int64_t>(g) - gid0 >= col0) break;
-      ++pos;
-    }
-    load();
-  }
-  __device__ __forceinline__ void advance() {
-    ++pos;
-    load();
-  }
-};
-}  // namespace
 
 template <int EPI, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const GemmArgs args) {
+                const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -120,7 +43,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* sempty_bar = sfull_bar + kSchedDepth;
   int32_t* s_sched = reinterpret_cast<int32_t*>(sempty_bar + kSchedDepth);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_sched + kSchedDepth);
-  float* stage_f32 = reinterpret_cast<float*>(smem + kStages * (kSmemA + kSmemB) + 256);  // 8 x 32 x kStgLd
+  // epilogue staging, 1024-B aligned (the 64B-swizzle pattern repeats every 512 B)
+  float* stage_f32 = reinterpret_cast<float*>(smem + kStages * (kSmemA + kSmemB) + 1024);
   static_assert((2 * kStages + 4 + 2 * kSchedDepth) * 8 + 4 * kSchedDepth + 4 <= 256, "barrier area");
 
   const int warp = threadIdx.x >> 5;
@@ -129,6 +53,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (EPI == EPI_STORE_F32 && args.tma_store) tma_prefetch_desc(&tmC);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -253,6 +178,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int cbeg = half * (BN / 2);
+    uint32_t epi_chunk = 0;  // running count of bulk-store chunks (slot parity)
     uint32_t acc = 0, acc_phase = 0, sslot = 0, sph = 0;
     int u = 0;
     for (bool first = true;; first = false) {
@@ -346,7 +272,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             args.p_u[o] = usum;
           }
         }
-      } else {  // EPI_STORE_F32
+      } else if (args.tma_store) {  // EPI_STORE_F32 via TMA bulk stores
+        // thread = row; each 32x16 fp32 block goes to a 64B-swizzled smem slot (rows of
+        // 64 B, 16 B chunk c of row r at chunk c ^ ((r >> 1) & 3): conflict-free 16 B
+        // stores), then one lane issues a bulk tensor store (or reduce-add when
+        // accumulating).  Two slots per warp; a slot is rewritten only after the bulk
+        // engine has finished reading it (wait_group.read 1).
+        uint8_t* slots = reinterpret_cast<uint8_t*>(stage_f32) + (warp - 2) * (2 * 2048);
+        const int row0 = mt * BM + q * 32;
+        for (int cb = cbeg; cb < cend; cb += 16) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(taddr + cb, r);
+          uint8_t* slot = slots + (epi_chunk & 1) * 2048;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          tmem_ld_wait();
+          const uint32_t sbase = smem_u32(slot) + lane * 64;
+          const uint32_t sw = (lane >> 1) & 3;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            sts128(sbase + ((c ^ sw) << 4), __uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
+                   __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int32_t x = static_cast<int32_t>(col0 + cb);
+            if (args.accumulate) tma_reduce_add_3d(&tmC, slot, x, row0, sp);
+            else tma_store_3d(&tmC, slot, x, row0, sp);
+            bulk_commit();
+          }
+          ++epi_chunk;
+        }
+      } else {  // EPI_STORE_F32 through the LSU (fallback: unaligned output strides)
         // TMEM gives thread = row; transpose each 32x16 fp32 block through this warp's
         // smem slice so a store instruction writes eight full 64 B row segments.
         const uint32_t stg = smem_u32(stage_f32 + (warp - 2) * (32 * kStgLd));  // explicit .shared
@@ -393,6 +350,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (EPI == EPI_STORE_F32 && args.tma_store && lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -406,7 +364,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // ------------------------------------------------------------------ host side
 namespace {
 template <int EPI, bool A_MN, bool B_MN>
-cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, cudaStream_t s) {
+cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& args,
+                        cudaStream_t s) {
   static bool attr_set = false;
   auto kern = k_umma_gemm<EPI, A_MN, B_MN>;
   if (!attr_set) {
@@ -417,21 +376,25 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
   const int units = args.m_tiles * args.n_tiles * args.splits;
   if (units <= 0) return cudaSuccess;
   const int grid = units < kNumSMs ? units : kNumSMs;
-  kern<<<grid, kGemmThreads, kGemmSmem, s>>>(tmA, tmB, args);
+  kern<<<grid, kGemmThreads, kGemmSmem, s>>>(tmA, tmB, tmC, args);
   count_launch();
   return cudaGetLastError();
 }
 }  // namespace
 
 cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                             const GemmArgs& args, cudaStream_t s) {
-  if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false>(tmA, tmB, args, s);
-  if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false>(tmA, tmB, args, s);
+                             const GemmArgs& args, cudaStream_t s, const CUtensorMap* tmC) {
+  static const CUtensorMap dummy{};
+  const CUtensorMap& C = tmC ? *tmC : dummy;
+  GemmArgs g = args;
+  g.tma_store = (epi == EPI_STORE_F32 && tmC) ? 1 : 0;
+  if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false>(tmA, tmB, C, g, s);
+  if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false>(tmA, tmB, C, g, s);
   if (epi == EPI_STORE_F32) {
-    if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false>(tmA, tmB, args, s);
-    if (!a_mn && b_mn) return launch_impl<EPI_STORE_F32, false, true>(tmA, tmB, args, s);
-    if (a_mn && !b_mn) return launch_impl<EPI_STORE_F32, true, false>(tmA, tmB, args, s);
-    return launch_impl<EPI_STORE_F32, true, true>(tmA, tmB, args, s);
+    if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false>(tmA, tmB, C, g, s);
+    if (!a_mn && b_mn) return launch_impl<EPI_STORE_F32, false, true>(tmA, tmB, C, g, s);
+    if (a_mn && !b_mn) return launch_impl<EPI_STORE_F32, true, false>(tmA, tmB, C, g, s);
+    return launch_impl<EPI_STORE_F32, true, true>(tmA, tmB, C, g, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -464,6 +427,23 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// 3D fp32 output map [depth][outer][inner] (row stride ld floats, depth stride dstride
+// floats), box {16, 32, 1}, SWIZZLE_64B.  Used by the TMA-store epilogue.
+bool make_tmap_f32_out(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                       uint64_t depth, uint64_t dstride) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 4) % 16 || (dstride * 4) % 16) return false;
+  cuuint64_t dims[3] = {inner, outer, depth};
+  cuuint64_t strides[2] = {ld * 4, (depth > 1 ? dstride : ld * outer) * 4};
+  cuuint32_t box[3] = {16, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

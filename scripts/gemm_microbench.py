@@ -56,5 +56,26 @@ def main():
                 torch.cuda.empty_cache()
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def mma_bound():
+    """L2-resident, MMA-bound shape: does operand major-ness cost throughput?"""
+    A.lib()
+    M, N, K = 1792, 4096, 8192
+    for a_mn in (0, 1):
+        for b_mn in (0, 1):
+            Am = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+            Bm = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+            Ast = Am.T.contiguous() if a_mn else Am
+            Bst = Bm.T.contiguous() if b_mn else Bm
+            D = torch.empty(M, N, device="cuda")
+            ms = t_ms(lambda: A.aurora_debug_gemm(bool(a_mn), bool(b_mn), Ast, Bst, D, M, N, K, Ast.stride(0),
+                                                  Bst.stride(0), D.stride(0)))
+            print(json.dumps(dict(shape="mma_bound", M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, ms=round(ms, 4),
+                                  tflops=round(2.0 * M * N * K / (ms / 1e3) / 1e12, 1))), flush=True)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "mma":
+    mma_bound()
