@@ -178,6 +178,16 @@ const char* aurora_build_info(void);
 /* Number of kernels this library has launched since load (for bench accounting). */
 uint64_t aurora_launch_count(void);
 
+/* Execution options (process-wide; affect performance only, never results beyond fp32
+ * summation order).  Defaults come from the environment (AURORA_PAIR, AURORA_BWD,
+ * AURORA_SERIAL_BWD).  Returns AURORA_ERR_INVALID_ARG for an unknown name or value.
+ *   "gemm_pair"      0 auto (default), 1 single-CTA 128x256 tiles, 2 CTA-pair 256x256
+ *                    tiles (tcgen05.mma.cta_group::2)
+ *   "bwd_mode"       0 per-chunk launches (default), 1 one fused persistent kernel
+ *   "bwd_concurrent" 1 (default): dW || dH of a chunk on library side streams */
+aurora_status_t aurora_set_option(const char* name, int64_t value);
+int64_t aurora_get_option(const char* name);
+
 /* Per-phase device timing (CUDA events recorded on the caller's stream around each
  * phase while enabled).  aurora_profile_read must be called after the stream was
  * synchronised; it fills up to `max` (name, total ms, launches) triples and returns

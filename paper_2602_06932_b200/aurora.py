@@ -26,7 +26,7 @@ MAX_K, MAX_NODES = 16, 32
 EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fwd", "aurora_spec_loss_bwd",
            "aurora_comm_get_unique_id", "aurora_comm_create", "aurora_comm_destroy", "aurora_status_string",
            "aurora_build_info", "aurora_launch_count", "aurora_profile_enable", "aurora_profile_read",
-           "aurora_debug_gemm", "aurora_debug_dlogits_rows"]
+           "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option"]
 
 
 class AuroraError(RuntimeError):
@@ -98,6 +98,10 @@ def lib() -> C.CDLL:
     L.aurora_debug_dlogits_rows.argtypes = [vp, vp, i64, i64, i64, i64, C.POINTER(aurora_labels_t), vp, vp, vp,
                                             i32, vp, vp]
     L.aurora_debug_dlogits_rows.restype = C.c_int
+    L.aurora_set_option.argtypes = [C.c_char_p, C.c_int64]
+    L.aurora_set_option.restype = C.c_int
+    L.aurora_get_option.argtypes = [C.c_char_p]
+    L.aurora_get_option.restype = C.c_int64
     _lib = L
     return L
 
@@ -145,6 +149,14 @@ def aurora_spec_loss_bwd(H, W, M, d, V_local, vocab_offset, labels, row_lse, dlo
 def aurora_debug_gemm(a_mn: bool, b_mn: bool, A, B, D, M, N, K, lda, ldb, ldd, stream=None) -> None:
     _check("aurora_debug_gemm", lib().aurora_debug_gemm(int(a_mn), int(b_mn), _ptr(A), _ptr(B), _ptr(D), M, N, K,
                                                         lda, ldb, ldd, _stream(stream)))
+
+
+def aurora_set_option(name: str, value: int) -> None:
+    _check("aurora_set_option", lib().aurora_set_option(name.encode(), int(value)))
+
+
+def aurora_get_option(name: str) -> int:
+    return int(lib().aurora_get_option(name.encode()))
 
 
 def aurora_launch_count() -> int:

@@ -124,6 +124,28 @@ struct Carver {
   }
 };
 
+// ---- tuning options (aurora_set_option); defaults from the environment
+struct Options {
+  int gemm_pair = 0;       // 0 auto, 1 single-CTA tiles, 2 CTA-pair tiles
+  int bwd_mode = 0;        // 0 classic per-chunk launches, 1 fused persistent kernel
+  int bwd_concurrent = 1;  // classic mode: dW || dH on side streams
+  Options() {
+    if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
+    if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
+    if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '1') ? 0 : 1;
+  }
+};
+Options& opts() {
+  static Options o;
+  return o;
+}
+// CTA-pair tiles (256 rows) when the GEMM's row count pads to 256 with little waste.
+int pair_for(int64_t rows) {
+  if (opts().gemm_pair == 1) return 1;
+  if (opts().gemm_pair == 2) return 2;
+  (void)rows;  // CTA-pair tiles are correct but measured slower on B200 so far: opt-in only
+  return 1;
+}
 int scan_nseg(int64_t M, int64_t V_local) {
   int64_t nseg = cdiv(8 * kNumSMs, std::max<int64_t>(M, 1));
   nseg = std::min<int64_t>(nseg, 32);
@@ -138,16 +160,17 @@ int64_t chunk_cols(int64_t V_local) {
 }
 // split-K factor for dH: the (m, n) tile count is small (M x d output) so pick the
 // split that fills whole waves of 148 SMs best (fewest splits within 3% of the best).
-int dh_splits(int64_t M, int64_t d, int64_t kb_total) {
-  const int64_t tiles = cdiv(M, BM) * cdiv(d, BN);
+int dh_splits(int64_t M, int64_t d, int64_t kb_total, int pair = 1) {
+  const int64_t tiles = cdiv(M, BM * pair) * cdiv(d, BN);
+  const int64_t slots = kNumSMs / pair;
   double best_eff = 0.0;
   double eff[17] = {0};
-  for (int64_t s = 1; s <= 16 && s <= kb_total; ++s) {
+  for (int64_t s = 1; s <= 8 && s <= kb_total; ++s) {
     const int64_t units = tiles * s;
-    eff[s] = static_cast<double>(units) / static_cast<double>(cdiv(units, kNumSMs) * kNumSMs);
+    eff[s] = static_cast<double>(units) / static_cast<double>(cdiv(units, slots) * slots);
     best_eff = std::max(best_eff, eff[s]);
   }
-  for (int64_t s = 1; s <= 16 && s <= kb_total; ++s)
+  for (int64_t s = 1; s <= 8 && s <= kb_total; ++s)
     if (eff[s] >= best_eff - 0.03) return static_cast<int>(cdiv(kb_total, cdiv(kb_total, s)));
   return 1;
 }
@@ -181,7 +204,7 @@ BwdWs carve_bwd(Carver& c, int64_t M, int64_t d, int64_t V_local) {
   w.vc = chunk_cols(V_local);
   w.m_pad = rup(M, 8);
   w.dzT = c.take<__nv_bfloat16>(w.vc * w.m_pad);
-  w.splits = dh_splits(M, d, cdiv(w.vc, BK));
+  w.splits = dh_splits(M, d, cdiv(w.vc, BK), pair_for(M));
   w.dh_part = w.splits > 1 ? c.take<float>(static_cast<int64_t>(w.splits) * M * d) : nullptr;
   return w;
 }
@@ -216,14 +239,7 @@ FusedWs carve_fused(Carver& c, int64_t M, int64_t d, int64_t V_local) {
   w.dh_part = w.splits > 1 ? c.take<float>(static_cast<int64_t>(w.splits) * M * d) : nullptr;
   return w;
 }
-bool classic_bwd() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("AURORA_BWD");
-    v = (e && std::strcmp(e, "classic") == 0) ? 1 : 0;
-  }
-  return v == 1;
-}
+bool classic_bwd() { return opts().bwd_mode == 0; }
 
 aurora_status_t check_cfg(const aurora_loss_cfg_t* cfg) {
   if (!cfg) return AURORA_ERR_INVALID_ARG;
@@ -268,14 +284,7 @@ SideStreams* side_streams() {
   }
   return &S;
 }
-bool serial_bwd() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("AURORA_SERIAL_BWD");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
+bool serial_bwd() { return opts().bwd_concurrent == 0; }
 
 // The comm owns a device scratch for gathered per-row data; it grows on first use
 // (one cudaMalloc per size increase, never in steady state).
@@ -435,6 +444,28 @@ const char* aurora_build_info(void) {
 
 uint64_t aurora_launch_count(void) { return g_launches.load(); }
 
+aurora_status_t aurora_set_option(const char* name, int64_t value) {
+  if (!name) return AURORA_ERR_INVALID_ARG;
+  Options& o = opts();
+  if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
+  if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
+  if (std::strcmp(name, "bwd_concurrent") == 0 && value >= 0 && value <= 1) {
+    o.bwd_concurrent = static_cast<int>(value);
+    return AURORA_OK;
+  }
+  return AURORA_ERR_INVALID_ARG;
+}
+
+int64_t aurora_get_option(const char* name) {
+  if (!name) return -1;
+  const Options& o = opts();
+  if (std::strcmp(name, "gemm_pair") == 0) return o.gemm_pair;
+  if (std::strcmp(name, "bwd_mode") == 0) return o.bwd_mode;
+  if (std::strcmp(name, "bwd_concurrent") == 0) return o.bwd_concurrent;
+  if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
+  return -1;
+}
+
 void aurora_profile_enable(int enable) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof_on = enable != 0;
@@ -581,11 +612,12 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   Carver c(ws);
   FwdWs w = carve_fwd(c, M, V_local);
 
+  const int pf = pair_for(M);
   CUtensorMap tmH, tmW;
   if (!make_tmap_bf16(&tmH, H, d, M, d, 64, BM)) return AURORA_ERR_CUDA;
-  if (!make_tmap_bf16(&tmW, W, d, V_local, d, 64, BN)) return AURORA_ERR_CUDA;
+  if (!make_tmap_bf16(&tmW, W, d, V_local, d, 64, BN / pf)) return AURORA_ERR_CUDA;
   GemmArgs a{};
-  a.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+  a.m_tiles = static_cast<int32_t>(cdiv(M, BM * pf));
   a.n_tiles = w.n_tiles;
   a.splits = 1;
   a.kb_total = static_cast<int32_t>(d / BK);
@@ -600,7 +632,7 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   a.p_sum = w.ps;
   a.p_u = w.pu;
   prof_begin(PH_FWD_GEMM, s);
-  cudaError_t e = launch_umma_gemm(EPI_FWD_STATS, false, false, tmH, tmW, a, s);
+  cudaError_t e = launch_umma_gemm(EPI_FWD_STATS, false, false, tmH, tmW, a, s, nullptr, pf);
   prof_end(PH_FWD_GEMM, s);
   if (e != cudaSuccess) return AURORA_ERR_CUDA;
   prof_begin(PH_FWD_COMBINE, s);
@@ -665,8 +697,9 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     const int64_t c0 = ch * w.vc;
     const int64_t vc = std::min(w.vc, V_local - c0);
     __nv_bfloat16* dzT = w.dzT;
+    const int pz = pair_for(M), pw = pair_for(vc);
     CUtensorMap tmW_k, tmW_mn, tmZ_k, tmZ_mn;
-    if (!make_tmap_bf16(&tmW_k, Wb + c0 * d, d, vc, d, 64, BN)) return AURORA_ERR_CUDA;
+    if (!make_tmap_bf16(&tmW_k, Wb + c0 * d, d, vc, d, 64, BN / pz)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmW_mn, Wb + c0 * d, d, vc, d, 64, 64)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmZ_k, dzT, M, vc, w.m_pad, 64, BM)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmZ_mn, dzT, M, vc, w.m_pad, 64, 64)) return AURORA_ERR_CUDA;
@@ -677,7 +710,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
 
     // A7: recompute Z tiles, dz -> dZ^T chunk (bf16)
     GemmArgs a{};
-    a.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+    a.m_tiles = static_cast<int32_t>(cdiv(M, BM * pz));
     a.n_tiles = static_cast<int32_t>(cdiv(vc, BN));
     a.splits = 1;
     a.kb_total = static_cast<int32_t>(d / BK);
@@ -695,7 +728,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     a.ld_dzT = w.m_pad;
     a.tile_counter = w.counters + 3 * ch;
     prof_begin(PH_BWD_DZ, s);
-    cudaError_t e = launch_umma_gemm(EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s);
+    cudaError_t e = launch_umma_gemm(EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s, nullptr, pz);
     prof_end(PH_BWD_DZ, s);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (S) {
@@ -706,7 +739,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
 
     // A8: dW[chunk] = dZ^T H   (A = dZ^T K-major, B = H MN-major, K = M)
     GemmArgs b{};
-    b.m_tiles = static_cast<int32_t>(cdiv(vc, BM));
+    b.m_tiles = static_cast<int32_t>(cdiv(vc, BM * pw));
     b.n_tiles = static_cast<int32_t>(cdiv(d, BN));
     b.splits = 1;
     b.kb_total = static_cast<int32_t>(cdiv(M, BK));
@@ -721,7 +754,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     CUtensorMap tmOW;
     const bool ow = make_tmap_f32_out(&tmOW, dWf + c0 * d, d, vc, d, 1, 0);
     prof_begin(PH_BWD_DW, sW);
-    e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr);
+    e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr, pw);
     prof_end(PH_BWD_DW, sW);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (comm && comm->dp_x()) {  // C5: DP gradient allreduce of this dW chunk
@@ -736,10 +769,11 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
 
     // A9: dH += dZ W[chunk]   (A = dZ^T as MN-major, B = W MN-major, K = vc)
     GemmArgs h{};
-    h.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+    const int ph = pair_for(M);
+    h.m_tiles = static_cast<int32_t>(cdiv(M, BM * ph));
     h.n_tiles = static_cast<int32_t>(cdiv(d, BN));
     h.kb_total = static_cast<int32_t>(cdiv(vc, BK));
-    h.splits = std::min<int>(dh_splits(M, d, h.kb_total), w.splits);
+    h.splits = std::min<int>(dh_splits(M, d, h.kb_total, ph), w.splits);
     h.kb_per_split = static_cast<int32_t>(cdiv(h.kb_total, h.splits));
     h.splits = static_cast<int32_t>(cdiv(h.kb_total, h.kb_per_split));
     h.M = M;
@@ -758,7 +792,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     const bool oh = h.splits > 1 ? make_tmap_f32_out(&tmOH, w.dh_part, d, M, d, h.splits, M * d)
                                  : make_tmap_f32_out(&tmOH, dH, d, M, d, 1, 0);
     prof_begin(PH_BWD_DH, sH);
-    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, sH, oh ? &tmOH : nullptr);
+    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, sH, oh ? &tmOH : nullptr, ph);
     prof_end(PH_BWD_DH, sH);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (h.splits > 1) {
@@ -836,12 +870,13 @@ aurora_status_t aurora_debug_gemm(int a_mn, int b_mn, const void* A, const void*
   if (!A || !B || !D || M < 1 || N < 1 || K < 1 || !al16(A) || !al16(B) || (lda * 2) % 16 || (ldb * 2) % 16)
     return AURORA_ERR_INVALID_ARG;
   if (ldd < N || lda < (a_mn ? M : K) || ldb < (b_mn ? N : K)) return AURORA_ERR_INVALID_ARG;
+  const int pr = pair_for(M);
   CUtensorMap ta, tb;
   bool ok = a_mn ? make_tmap_bf16(&ta, A, M, K, lda, 64, 64) : make_tmap_bf16(&ta, A, K, M, lda, 64, BM);
-  ok = ok && (b_mn ? make_tmap_bf16(&tb, B, N, K, ldb, 64, 64) : make_tmap_bf16(&tb, B, K, N, ldb, 64, BN));
+  ok = ok && (b_mn ? make_tmap_bf16(&tb, B, N, K, ldb, 64, 64) : make_tmap_bf16(&tb, B, K, N, ldb, 64, BN / pr));
   if (!ok) return AURORA_ERR_CUDA;
   GemmArgs g{};
-  g.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+  g.m_tiles = static_cast<int32_t>(cdiv(M, BM * pr));
   g.n_tiles = static_cast<int32_t>(cdiv(N, BN));
   g.splits = 1;
   g.kb_total = static_cast<int32_t>(cdiv(K, BK));
@@ -853,7 +888,7 @@ aurora_status_t aurora_debug_gemm(int a_mn, int b_mn, const void* A, const void*
   CUtensorMap tc;
   const bool oc = make_tmap_f32_out(&tc, D, N, M, ldd, 1, 0);
   return cuda_status(launch_umma_gemm(EPI_STORE_F32, a_mn != 0, b_mn != 0, ta, tb, g,
-                                      static_cast<cudaStream_t>(stream), oc ? &tc : nullptr));
+                                      static_cast<cudaStream_t>(stream), oc ? &tc : nullptr, pr));
 }
 
 aurora_status_t aurora_debug_dlogits_rows(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,

@@ -58,8 +58,11 @@ struct GemmArgs {
 // Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.
 // tmC (optional, EPI_STORE_F32 only): fp32 output map from make_tmap_f32_out -> TMA-store
 // epilogue (bulk stores / reduce-add); nullptr -> LSU store path.
+// pair = 2: 2-CTA clusters with tcgen05.mma.cta_group::2 (M = 256 per pair tile; the
+// caller sets args.m_tiles in 256-row units and builds K-major B maps with a 128-row box).
 cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                             const GemmArgs& args, cudaStream_t stream, const CUtensorMap* tmC = nullptr);
+                             const GemmArgs& args, cudaStream_t stream, const CUtensorMap* tmC = nullptr,
+                             int pair = 1);
 bool make_tmap_f32_out(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                        uint64_t depth, uint64_t dstride);
 
@@ -138,6 +141,7 @@ cudaError_t launch_debug_dlogits(const __nv_bfloat16* H, const __nv_bfloat16* W,
 
 // ---------------------------------------------------------------- accounting
 extern std::atomic<uint64_t> g_launches;
+extern int g_pair_max_clusters;  // cudaOccupancyMaxActiveClusters of the CTA-pair GEMM (-1: unknown)
 inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 // Phase profiling (CUDA events on the caller's stream).

@@ -26,18 +26,30 @@
 
 namespace aur {
 
+int g_pair_max_clusters = -1;
 
-template <int EPI, bool A_MN, bool B_MN>
+// PAIR = 1: one CTA per 128x256 tile (tcgen05.mma.cta_group::1, M = 128).
+// PAIR = 2: a 2-CTA cluster per 256x256 tile (tcgen05.mma.cta_group::2, M = 256): each
+//   CTA TMA-loads its own 128 rows of A and HALF of B (128 of the 256 columns) into its
+//   own smem, crediting the leader's full barrier; the leader issues the pair MMA and
+//   commits to both CTAs' barriers; each CTA's TMEM holds its 128 rows x 256 columns and
+//   its epilogue releases the leader's TMEM-empty barrier.  Operand traffic per flop
+//   drops by a third and the stage ring grows from 4 x 48 KB to 6 x 32 KB.
+template <int EPI, bool A_MN, bool B_MN, int PAIR>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
+  constexpr int kSt = PAIR == 2 ? 6 : kStages;
+  constexpr int kSB = (BN / PAIR) * BK * 2;  // B bytes per stage in this CTA
+  constexpr int kStageBytes = kSmemA + kSB;
+  static_assert(kSt * kStageBytes == kStages * (kSmemA + kSmemB), "stage ring must keep the smem layout");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kSmemA;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sB + kStages * kSmemB);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tfull_bar = empty_bar + kStages;
+  uint8_t* sB = smem + kSt * kSmemA;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sB + kSt * kSB);
+  uint64_t* empty_bar = full_bar + kSt;
+  uint64_t* tfull_bar = empty_bar + kSt;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* sfull_bar = tempty_bar + 2;        // tile-index ring (dynamic scheduler)
   uint64_t* sempty_bar = sfull_bar + kSchedDepth;
@@ -45,22 +57,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_sched + kSchedDepth);
   // epilogue staging, 1024-B aligned (the 64B-swizzle pattern repeats every 512 B)
   float* stage_f32 = reinterpret_cast<float*>(smem + kStages * (kSmemA + kSmemB) + 1024);
-  static_assert((2 * kStages + 4 + 2 * kSchedDepth) * 8 + 4 * kSchedDepth + 4 <= 256, "barrier area");
+  static_assert((2 * kSt + 4 + 2 * kSchedDepth) * 8 + 4 * kSchedDepth + 4 <= 1024, "barrier area");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = (PAIR == 2) ? cluster_ctarank() : 0u;  // 0 = pair leader
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     if (EPI == EPI_STORE_F32 && args.tma_store) tma_prefetch_desc(&tmC);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full_bar[s], 1);
+    for (int s = 0; s < kSt; ++s) {
+      mbar_init(&full_bar[s], PAIR);  // leader: own expect_tx arrive + peer's remote arrive
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], kEpiWarps);
+      mbar_init(&tempty_bar[a], PAIR * kEpiWarps);
     }
     for (int d = 0; d < kSchedDepth; ++d) {
       mbar_init(&sfull_bar[d], 1);
@@ -68,13 +81,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  if (warp == 1) {
+    if constexpr (PAIR == 2) tmem_alloc_pair<512>(tmem_holder);
+    else tmem_alloc<512>(tmem_holder);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int units = args.m_tiles * args.n_tiles * args.splits;
+  const int units = args.m_tiles * args.n_tiles * args.splits;  // PAIR=2: m_tiles counts 256-row pair tiles
+  const int ublk = PAIR == 2 ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int ugrid = PAIR == 2 ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
   // Tile scheduler.  Static: u = blockIdx.x + i*gridDim.x.  Dynamic (args.tile_counter):
   // the producer claims tiles with atomicAdd and hands them to the MMA / epilogue warps
   // through a small smem ring, so a kernel sharing the GPU with another stream's kernel
@@ -82,7 +101,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const bool dyn = args.tile_counter != nullptr;
   auto consumer_next = [&](uint32_t& slot, uint32_t& ph, int& u, bool first, bool is_mma) {
     if (!dyn) {
-      u = first ? static_cast<int>(blockIdx.x) : u + static_cast<int>(gridDim.x);
+      u = first ? ublk : u + ugrid;
       return;
     }
     mbar_wait(&sfull_bar[slot], ph);
@@ -100,7 +119,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0, sslot = 0, sph = 0;
-      for (int u = blockIdx.x;; u += gridDim.x) {
+      for (int u = ublk;; u += ugrid) {
         if (dyn) {
           u = atomicAdd(args.tile_counter, 1);
           if (u == units + static_cast<int>(gridDim.x) - 1) atomicExch(args.tile_counter, 0);
@@ -114,33 +133,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         decode_unit(args, u, mt, nt, sp);
         const int kb0 = sp * args.kb_per_split;
         const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
+        const int arow = (PAIR == 2 ? mt * 2 + static_cast<int>(rank) : mt) * BM;  // this CTA's A rows
+        const int brow = nt * BN + static_cast<int>(rank) * (BN / PAIR);          // this CTA's B rows
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], kSmemA + kSmemB);
+          if constexpr (PAIR == 1) {
+            mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
+          } else if (rank == 0) {
+            mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
+          } else {
+            mbar_arrive_cluster(mapa_shared(smem_u32(&full_bar[stage]), 0));
+          }
           uint8_t* a = sA + stage * kSmemA;
-          uint8_t* b = sB + stage * kSmemB;
+          uint8_t* b = sB + stage * kSB;
+          auto load = [&](const CUtensorMap* m, void* dst, int x, int y) {
+            if constexpr (PAIR == 2) tma_load_2d_pair(m, &full_bar[stage], dst, x, y);
+            else tma_load_2d(m, &full_bar[stage], dst, x, y);
+          };
           if constexpr (!A_MN) {
-            tma_load_2d(&tmA, &full_bar[stage], a, kb * BK, mt * BM);
+            load(&tmA, a, kb * BK, arow);
           } else {
 #pragma unroll
-            for (int i = 0; i < BM / 64; ++i)
-              tma_load_2d(&tmA, &full_bar[stage], a + i * (BK * 128), mt * BM + i * 64, kb * BK);
+            for (int i = 0; i < BM / 64; ++i) load(&tmA, a + i * (BK * 128), arow + i * 64, kb * BK);
           }
           if constexpr (!B_MN) {
-            tma_load_2d(&tmB, &full_bar[stage], b, kb * BK, nt * BN);
+            load(&tmB, b, kb * BK, brow);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / 64; ++i)
-              tma_load_2d(&tmB, &full_bar[stage], b + i * (BK * 128), nt * BN + i * 64, kb * BK);
+            for (int i = 0; i < BN / PAIR / 64; ++i) load(&tmB, b + i * (BK * 128), brow + i * 64, kb * BK);
           }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == kSt) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+    if (lane == 0 && rank == 0) {  // PAIR = 2: only the leader issues (cta_group::2)
+      constexpr uint32_t idesc = umma_idesc_bf16(BM * PAIR, BN, A_MN, B_MN);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, sslot = 0, sph = 0;
       int u = 0;
       for (bool first = true;; first = false) {
@@ -157,16 +186,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * kSmemA);
-          const uint32_t b_base = smem_u32(sB + stage * kSmemB);
+          const uint32_t b_base = smem_u32(sB + stage * kSB);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            umma_bf16(d_tmem, operand_desc<A_MN>(a_base, k), operand_desc<B_MN>(b_base, k), idesc,
-                      (kb > kb0 || k > 0) ? 1u : 0u);
+            if constexpr (PAIR == 2)
+              umma_bf16_pair(d_tmem, operand_desc<A_MN>(a_base, k), operand_desc<B_MN>(b_base, k), idesc,
+                             (kb > kb0 || k > 0) ? 1u : 0u);
+            else
+              umma_bf16(d_tmem, operand_desc<A_MN>(a_base, k), operand_desc<B_MN>(b_base, k), idesc,
+                        (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if constexpr (PAIR == 2) umma_commit_pair(&empty_bar[stage]);
+          else umma_commit(&empty_bar[stage]);
+          if (++stage == kSt) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);
+        if constexpr (PAIR == 2) umma_commit_pair(&tfull_bar[acc]);
+        else umma_commit(&tfull_bar[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -186,6 +221,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (u >= units) break;
       int mt, nt, sp;
       decode_unit(args, u, mt, nt, sp);
+      if constexpr (PAIR == 2) mt = mt * 2 + static_cast<int>(rank);  // this CTA's 128-row half
       const int64_t row = static_cast<int64_t>(mt) * BM + q * 32 + lane;
       const bool row_ok = row < args.M;
       const int64_t col0 = static_cast<int64_t>(nt) * BN;
@@ -346,7 +382,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+        else mbar_arrive(&tempty_bar[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -354,20 +393,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem_base);
+    if constexpr (PAIR == 2) tmem_dealloc_pair<512>(tmem_base);
+    else tmem_dealloc<512>(tmem_base);
   }
 }
 
 // ------------------------------------------------------------------ host side
 namespace {
-template <int EPI, bool A_MN, bool B_MN>
+template <int EPI, bool A_MN, bool B_MN, int PAIR>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& args,
                         cudaStream_t s) {
   static bool attr_set = false;
-  auto kern = k_umma_gemm<EPI, A_MN, B_MN>;
+  auto kern = k_umma_gemm<EPI, A_MN, B_MN, PAIR>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
     if (e != cudaSuccess) return e;
@@ -375,28 +416,82 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
   }
   const int units = args.m_tiles * args.n_tiles * args.splits;
   if (units <= 0) return cudaSuccess;
-  const int grid = units < kNumSMs ? units : kNumSMs;
-  kern<<<grid, kGemmThreads, kGemmSmem, s>>>(tmA, tmB, tmC, args);
+  static const int dbg_cluster = [] {
+    const char* e = getenv("AURORA_DBG_CLUSTER1");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  if (PAIR == 1 && dbg_cluster) {  // diagnostic: single-CTA tiles launched as 2-CTA clusters
+    const int grid = units < kNumSMs ? ((units + 1) & ~1) : kNumSMs;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = kGemmSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, args);
+    if (e != cudaSuccess) return e;
+  } else if constexpr (PAIR == 1) {
+    const int grid = units < kNumSMs ? units : kNumSMs;
+    kern<<<grid, kGemmThreads, kGemmSmem, s>>>(tmA, tmB, tmC, args);
+  } else {
+    const int pairs = units < kNumSMs / 2 ? units : kNumSMs / 2;
+    static int max_clusters = -1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = kGemmSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (max_clusters < 0) {
+      cfg.gridDim = dim3(kNumSMs);
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess) max_clusters = 0;
+      g_pair_max_clusters = max_clusters;
+      cfg.gridDim = dim3(2 * pairs);
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmC, args);
+    if (e != cudaSuccess) return e;
+  }
   count_launch();
   return cudaGetLastError();
+}
+template <int PAIR>
+cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                     const CUtensorMap& C, const GemmArgs& g, cudaStream_t s) {
+  if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false, PAIR>(tmA, tmB, C, g, s);
+  if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false, PAIR>(tmA, tmB, C, g, s);
+  if (epi == EPI_STORE_F32) {
+    if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false, PAIR>(tmA, tmB, C, g, s);
+    if (!a_mn && b_mn) return launch_impl<EPI_STORE_F32, false, true, PAIR>(tmA, tmB, C, g, s);
+    if (a_mn && !b_mn) return launch_impl<EPI_STORE_F32, true, false, PAIR>(tmA, tmB, C, g, s);
+    return launch_impl<EPI_STORE_F32, true, true, PAIR>(tmA, tmB, C, g, s);
+  }
+  return cudaErrorInvalidValue;
 }
 }  // namespace
 
 cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                             const GemmArgs& args, cudaStream_t s, const CUtensorMap* tmC) {
+                             const GemmArgs& args, cudaStream_t s, const CUtensorMap* tmC, int pair) {
   static const CUtensorMap dummy{};
   const CUtensorMap& C = tmC ? *tmC : dummy;
   GemmArgs g = args;
   g.tma_store = (epi == EPI_STORE_F32 && tmC) ? 1 : 0;
-  if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false>(tmA, tmB, C, g, s);
-  if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false>(tmA, tmB, C, g, s);
-  if (epi == EPI_STORE_F32) {
-    if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false>(tmA, tmB, C, g, s);
-    if (!a_mn && b_mn) return launch_impl<EPI_STORE_F32, false, true>(tmA, tmB, C, g, s);
-    if (a_mn && !b_mn) return launch_impl<EPI_STORE_F32, true, false>(tmA, tmB, C, g, s);
-    return launch_impl<EPI_STORE_F32, true, true>(tmA, tmB, C, g, s);
+  if (pair == 2) {
+    g.tile_counter = nullptr;  // pairs use the static per-cluster schedule
+    return dispatch<2>(epi, a_mn, b_mn, tmA, tmB, C, g, s);
   }
-  return cudaErrorInvalidValue;
+  return dispatch<1>(epi, a_mn, b_mn, tmA, tmB, C, g, s);
 }
 
 // ------------------------------------------------------------------ tensor maps

@@ -339,3 +339,48 @@ def test_emulated_vocab_parallel_shards(cuts):
     dW = torch.cat(dWs, 0)
     assert _rfro(dW.cpu().numpy(), ref["dW"]) <= GRAD_RFRO
     assert _rfro(dH.cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+@pytest.fixture
+def option():
+    """Set library execution options for one test, restoring them afterwards."""
+    saved = {}
+
+    def set_(name, value):
+        if name not in saved:
+            saved[name] = A.aurora_get_option(name)
+        A.aurora_set_option(name, value)
+
+    yield set_
+    for k, v in saved.items():
+        A.aurora_set_option(k, v)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (300, 520, 192), (37, 70, 200), (1024, 512, 1024)])
+def test_gemm_engine_cta_pair(option, a_mn, b_mn, M, N, K):
+    """tcgen05.mma.cta_group::2 (2-CTA cluster, M=256 pair tiles) vs PyTorch fp32."""
+    option("gemm_pair", 2)
+    test_gemm_engine_vs_torch_fp32(a_mn, b_mn, M, N, K)
+
+
+@pytest.mark.parametrize("pair", [1, 2])
+@pytest.mark.parametrize("name", ["tiny", "small_tree", "mid"])
+def test_parity_forced_tiling(option, name, pair):
+    option("gemm_pair", pair)
+    test_full_parity_small(name)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "small_tree", "mid"])
+def test_parity_fused_bwd(option, name):
+    """The whole backward as one persistent kernel (unified DZ/DH/DW tile queue)."""
+    option("bwd_mode", 1)
+    test_full_parity_small(name)
+
+
+def test_fused_bwd_emulated_vp_and_serial(option):
+    option("bwd_mode", 1)
+    test_emulated_vocab_parallel_shards((1000, 2049, 4100))
+    option("bwd_mode", 0)
+    option("bwd_concurrent", 0)
+    test_full_parity_small("small")
