@@ -143,8 +143,7 @@ Options& opts() {
 int pair_for(int64_t rows) {
   if (opts().gemm_pair == 1) return 1;
   if (opts().gemm_pair == 2) return 2;
-  (void)rows;  // CTA-pair tiles are correct but measured slower on B200 so far: opt-in only
-  return 1;
+  return (rows % 256 == 0 || rows >= 4096) ? 2 : 1;
 }
 int scan_nseg(int64_t M, int64_t V_local) {
   int64_t nseg = cdiv(8 * kNumSMs, std::max<int64_t>(M, 1));

@@ -152,7 +152,57 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
   constexpr int U = 4;
   // vectors are interleaved: warp w handles [w*32 + i*256, +32) for i = 0, 1, ...
   int64_t base = static_cast<int64_t>(warp) * 32;
-  bool first = true;
+  {
+    // ---- CTA-wide warm start: every warp loads its first batch, the 256 lane maxima
+    // (distinct elements) go to smem, and the k-th largest of them is a valid lower
+    // bound for the k-th best element of the segment.
+    __shared__ float s_lm[256];
+    uint4 w[U];
+    float gm[U];
+    float lm = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vi = base + u * 256 + lane;
+      w[u] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+      if (vi < nvec) {
+        w[u] = ld_nc_v4(src + vi);
+        bad |= nonfinite8(w[u]);
+      }
+      gm[u] = max8(w[u]);
+      lm = fmaxf(lm, gm[u]);
+    }
+    s_lm[threadIdx.x] = lm;
+    __syncthreads();
+    float v8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v8[j] = s_lm[lane * 8 + j];
+    for (int r = 0; r < k; ++r) {
+      float m = v8[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) m = fmaxf(m, v8[j]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+      if (r == k - 1) floor = fmaxf(floor, m);
+      const uint32_t has = __ballot_sync(0xffffffffu, v8[0] == m || v8[1] == m || v8[2] == m || v8[3] == m ||
+                                                          v8[4] == m || v8[5] == m || v8[6] == m || v8[7] == m);
+      if (lane == __ffs(has) - 1) {
+        bool done = false;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool hit = !done && v8[j] == m;
+          v8[j] = hit ? -INFINITY : v8[j];
+          done = done || hit;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vi = base + u * 256 + lane;
+      const bool h = vi < nvec && gm[u] >= fmaxf(floor, L.thr_v);
+      if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, w[u], c0 + vi * 8, floor);
+    }
+    base += U * 256;
+  }
   for (; base + (U - 1) * 256 + 31 < nvec; base += U * 256) {
     uint4 w[U];
 #pragma unroll
@@ -162,13 +212,6 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
     for (int u = 0; u < U; ++u) {
       bad |= nonfinite8(w[u]);
       gm[u] = max8(w[u]);
-    }
-    if (first) {  // warm start: k-th largest lane maximum is <= the k-th best element
-      first = false;
-      float lm = gm[0];
-#pragma unroll
-      for (int u = 1; u < U; ++u) lm = fmaxf(lm, gm[u]);
-      floor = fmaxf(floor, warp_kth_largest(lm, k));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {

@@ -181,8 +181,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// Remote arrive (default .release.cta semantics).  NOT .release.cluster: that form
+// compiles to MEMBAR.ALL.GPU + ERRBAR per call, which serialised the CTA-pair pipeline
+// (the arrivals carry no data: operand bytes are credited by TMA complete_tx).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // 2-SM TMA load: data lands in THIS CTA's smem, transaction bytes are credited to the
 // mbarrier of the pair leader (peer bit of the mbarrier address cleared).
