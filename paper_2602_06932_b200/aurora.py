@@ -115,6 +115,19 @@ def _ptr(t) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
+def _expect(t, dtype_name: str, what: str):
+    """Marshalling-level check: the C-ABI cannot see dtypes, so a wrong one would be
+    silently reinterpreted.  Raises before anything is enqueued."""
+    if t is None:
+        return
+    import torch
+    want = {"bf16": torch.bfloat16, "f32": torch.float32, "i32": torch.int32, "u8": torch.uint8}[dtype_name]
+    if t.dtype != want:
+        raise TypeError(f"{what}: expected {want}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: must be contiguous")
+
+
 def _stream(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -134,6 +147,8 @@ def aurora_verify_labels(trace: aurora_trace_t, cfg: aurora_loss_cfg_t, labels: 
 
 def aurora_spec_loss_fwd(H, W, M, d, V_local, vocab_offset, labels, row_lse, row_loss, loss, ws, ws_bytes,
                          comm=None, stream=None) -> None:
+    _expect(H, "bf16", "H"); _expect(W, "bf16", "W")
+    _expect(row_lse, "f32", "row_lse"); _expect(row_loss, "f32", "row_loss"); _expect(loss, "f32", "loss")
     _check("aurora_spec_loss_fwd", lib().aurora_spec_loss_fwd(
         _ptr(H), _ptr(W), M, d, V_local, vocab_offset, C.byref(labels), _ptr(row_lse), _ptr(row_loss), _ptr(loss),
         ws, ws_bytes, comm, _stream(stream)))
@@ -141,12 +156,15 @@ def aurora_spec_loss_fwd(H, W, M, d, V_local, vocab_offset, labels, row_lse, row
 
 def aurora_spec_loss_bwd(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dW, dW_is_bf16,
                          accumulate_dW, ws, ws_bytes, comm=None, stream=None) -> None:
+    _expect(H, "bf16", "H"); _expect(W, "bf16", "W"); _expect(row_lse, "f32", "row_lse")
+    _expect(dloss, "f32", "dloss"); _expect(dH, "f32", "dH"); _expect(dW, "bf16" if dW_is_bf16 else "f32", "dW")
     _check("aurora_spec_loss_bwd", lib().aurora_spec_loss_bwd(
         _ptr(H), _ptr(W), M, d, V_local, vocab_offset, C.byref(labels), _ptr(row_lse), _ptr(dloss), _ptr(dH),
         _ptr(dW), int(dW_is_bf16), int(accumulate_dW), ws, ws_bytes, comm, _stream(stream)))
 
 
 def aurora_debug_gemm(a_mn: bool, b_mn: bool, A, B, D, M, N, K, lda, ldb, ldd, stream=None) -> None:
+    _expect(A, "bf16", "A"); _expect(B, "bf16", "B"); _expect(D, "f32", "D")
     _check("aurora_debug_gemm", lib().aurora_debug_gemm(int(a_mn), int(b_mn), _ptr(A), _ptr(B), _ptr(D), M, N, K,
                                                         lda, ldb, ldd, _stream(stream)))
 
@@ -241,6 +259,8 @@ class SpecTrainStep:
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
 
     def verify(self, draft_tokens, target_logits, parents=None, num_nodes=None, stream=None):
+        _expect(draft_tokens, "i32", "draft_tokens"); _expect(parents, "i32", "parents")
+        _expect(num_nodes, "i32", "num_nodes"); _expect(target_logits, "bf16", "target_logits")
         t = aurora_trace_t(self.R, self.N, _ptr(draft_tokens), _ptr(parents), _ptr(num_nodes), _ptr(target_logits),
                            target_logits.stride(0), self.V, self.V_local, self.vocab_offset)
         aurora_verify_labels(t, self.cfg, self.labels, self.ws.data_ptr(), self.ws_bytes, self.comm, stream)

@@ -9,6 +9,10 @@ import numpy as np
 import pytest
 import torch
 
+# every buffer handed to the C-ABI is created with an explicit dtype; guard against a
+# process-wide default dtype change by another test module
+assert torch.get_default_dtype() == torch.float32
+
 import oracle
 import tracegen
 from paper_2602_06932_b200 import aurora as A
@@ -100,7 +104,7 @@ def test_gemm_engine_vs_torch_fp32(a_mn, b_mn, M, N, K):
         y[:, :c] = x
         return y
     Ast, Bst = pad(Ast), pad(Bst)
-    D = torch.full((M, N), float("nan"), device="cuda")
+    D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.float32)
     A.aurora_debug_gemm(bool(a_mn), bool(b_mn), Ast, Bst, D, M, N, K, Ast.stride(0), Bst.stride(0), D.stride(0))
     torch.cuda.synchronize()
     err = (D - ref).abs().max().item()
@@ -215,7 +219,7 @@ def test_accumulate_and_upstream_grad():
     c = tr["cfg"]
     dH2 = torch.empty_like(out["dH"])
     dW2 = out["dW"].clone()
-    dl = torch.tensor([-2.0], device="cuda")
+    dl = torch.tensor([-2.0], device="cuda", dtype=torch.float32)
     st.backward(g["H"], g["W"], dH2, dW2, dloss=dl, accumulate_dW=True)
     torch.cuda.synchronize()
     # dW2 = dW + (-2) dW = -dW ; dH2 = -2 dH
@@ -309,9 +313,9 @@ def test_emulated_vocab_parallel_shards(cuts):
     M = c.M
     for v0, v1 in zip(bounds[:-1], bounds[1:]):
         Ws = g["W"][v0:v1].contiguous()
-        row_lse = torch.empty(M, device="cuda")
-        row_loss = torch.empty(M, device="cuda")
-        loss = torch.empty(1, device="cuda")
+        row_lse = torch.empty(M, device="cuda", dtype=torch.float32)
+        row_loss = torch.empty(M, device="cuda", dtype=torch.float32)
+        loss = torch.empty(1, device="cuda", dtype=torch.float32)
         A.aurora_spec_loss_fwd(g["H"], Ws, M, c.d, v1 - v0, v0, st.labels, row_lse, row_loss, loss,
                                st.ws.data_ptr(), st.ws_bytes)
         torch.cuda.synchronize()
@@ -325,12 +329,12 @@ def test_emulated_vocab_parallel_shards(cuts):
     assert abs(loss - ref["loss"]) <= 1e-3 * abs(ref["loss"])
     np.testing.assert_allclose(lse.cpu().numpy(), ref["lse"], rtol=2e-5)
     glse = lse.float().contiguous()
-    dH = torch.zeros(M, c.d, device="cuda", dtype=torch.float64)
+    dH = torch.zeros(M, c.d, device="cuda", dtype=torch.float64)  # host-side accumulation only
     dWs = []
     for v0, v1 in zip(bounds[:-1], bounds[1:]):
         Ws = g["W"][v0:v1].contiguous()
-        dHp = torch.empty(M, c.d, device="cuda")
-        dWp = torch.empty(v1 - v0, c.d, device="cuda")
+        dHp = torch.empty(M, c.d, device="cuda", dtype=torch.float32)
+        dWp = torch.empty(v1 - v0, c.d, device="cuda", dtype=torch.float32)
         A.aurora_spec_loss_bwd(g["H"], Ws, M, c.d, v1 - v0, v0, st.labels, glse, None, dHp, dWp, False, False,
                                st.ws.data_ptr(), st.ws_bytes)
         torch.cuda.synchronize()

@@ -18,7 +18,6 @@ import oracle
 from oracle import ACCEPT, DISCARD, PAD
 import tracegen
 
-torch.set_default_dtype(torch.float64)
 
 
 def _parse(v):
@@ -385,8 +384,8 @@ def test_torch_autograd(name, kw):
     W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
     lab, tg, fw, bw, T = _oracle_all(tr, W64, H64, **kw)
     M, V = T.shape
-    P = torch.zeros(M, V)
-    wv = torch.zeros(M)
+    P = torch.zeros(M, V, dtype=torch.float64)
+    wv = torch.zeros(M, dtype=torch.float64)
     for m in range(M):
         P[m, torch.from_numpy(tg["sup_idx"][m])] = torch.from_numpy(tg["sup_p"][m])
         wv[m] = tg["w"][m]
