@@ -196,7 +196,7 @@ def run_ours(args):
         return
 
     peak_burst, peak_sus, hbm, peak_src = _peaks()
-    roof = _roofline(phases, cfg, args.steps, peak_sus, peak_src)
+    roof = _roofline(phases, cfg, args.steps, peak_sus, peak_src, hbm)
     out = {
         "metric": "speculator-training tokens/s (verify + lm_head fwd/bwd + Eq.3 loss), % bf16 tensor peak",
         "value": round(tokens_per_s, 1),
@@ -290,39 +290,71 @@ def _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush):
                     "no L2 flush (each step streams its trace from host)"}
 
 
-def _roofline(phases, cfg, steps, peak, peak_src):
-    """Dominant lm_head kernel: algorithmic flops per launch / mean launch time."""
+def _phase_work(cfg, k, launches_per_step):
+    """Algorithmic work of one launch of GEMM phase k (SURVEY 8(d) per-unit figures):
+    flops = 2 d per (row, vocab column); bytes = the phase's compulsory DRAM traffic."""
     M, V, d = cfg.M, cfg.V, cfg.d
-    flops_total = {"fwd_gemm": 2.0 * M * V * d, "bwd_dz_gemm": 2.0 * M * V * d, "bwd_dw_gemm": 2.0 * M * V * d,
-                   "bwd_dh_gemm": 2.0 * M * V * d}
-    best = None
+    vc = V / launches_per_step               # vocab columns per launch (chunked phases)
+    flops = 2.0 * M * vc * d
+    if k == "fwd_gemm":                      # W once, H, (m, s, u) partials
+        byts = 2.0 * V * d + 2.0 * M * d + 12.0 * M * 2 * (V / 256.0)
+    elif k == "bwd_dz_gemm":                 # W chunk once, H, bf16 dZ^T chunk write
+        byts = 2.0 * vc * d + 2.0 * M * d + 2.0 * vc * M
+    elif k == "bwd_dw_gemm":                 # fp32 dW chunk write, dZ^T chunk + H reads
+        byts = 4.0 * vc * d + 2.0 * vc * M + 2.0 * M * d
+    else:                                    # dH: W chunk + dZ^T chunk reads, fp32 dH write
+        byts = 2.0 * vc * d + 2.0 * vc * M + 4.0 * M * d
+    return flops, byts
+
+
+def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0):
+    """Dominant lm_head kernel (largest share of the step): achieved algorithmic work per
+    launch / mean launch time, against whichever roofline bounds it (tensor or HBM)."""
     per = []
-    for k, f in flops_total.items():
+    best = None
+    for k in ("fwd_gemm", "bwd_dz_gemm", "bwd_dw_gemm", "bwd_dh_gemm", "bwd_fused"):
         if k not in phases or phases[k][1] == 0:
             continue
         tot_ms, n = phases[k]
-        launches_per_step = n / steps
-        ach = (f / launches_per_step) / ((tot_ms / n) / 1e3) / 1e12
-        per.append({"kernel": k, "ms_per_step": round(tot_ms / steps, 4), "launches_per_step": launches_per_step,
-                    "achieved_tflops": round(ach, 1), "frac": round(ach / peak, 4)})
+        lps = n / steps
+        t = (tot_ms / n) / 1e3
+        if k == "bwd_fused":
+            flops, byts = 3 * 2.0 * cfg.M * cfg.V * cfg.d, 4.0 * cfg.V * cfg.d + 4.0 * cfg.V * cfg.d
+        else:
+            flops, byts = _phase_work(cfg, k, lps)
+        t_tensor, t_hbm = flops / (peak * 1e12), byts / (hbm_peak_gbs * 1e9)
+        bound = "tensor" if t_tensor >= t_hbm else "hbm"
+        rec = {"kernel": k, "ms_per_step": round(tot_ms / steps, 4), "launches_per_step": lps,
+               "achieved_tflops": round(flops / t / 1e12, 1), "achieved_gbs": round(byts / t / 1e9, 1),
+               "bound": bound, "frac": round(max(t_tensor, t_hbm) / t, 4)}
+        per.append(rec)
         if best is None or tot_ms > best[1]:
-            best = (k, tot_ms, ach, n)
+            best = (k, tot_ms, rec)
     if best is None:
         return None
-    k, tot_ms, ach, n = best
-    traffic = _traffic_for(k)
-    return {"bound": "tensor", "kernel": k, "achieved": round(ach, 1), "peak": peak, "unit": "TFLOP/s",
-            "frac": round(ach / peak, 4), "traffic": traffic,
-            "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)",
-            "work_per_launch": "2*M*V_chunk*d flops (2d per row per vocab column, SURVEY 8(d))",
-            "phases": per}
+    k, _, rec = best
+    if rec["bound"] == "tensor":
+        out = {"bound": "tensor", "kernel": k, "achieved": rec["achieved_tflops"], "peak": peak, "unit": "TFLOP/s",
+               "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)",
+               "work_per_launch": "2*M*V_chunk*d flops (2 d per row per vocab column, SURVEY 8(d))"}
+    else:
+        out = {"bound": "hbm", "kernel": k, "achieved": rec["achieved_gbs"], "peak": hbm_peak_gbs, "unit": "GB/s",
+               "peak_source": f"{peak_src} hbm_gbs (copy)",
+               "work_per_launch": "compulsory DRAM bytes per launch (fp32 dW chunk write + dZ^T/H reads, DESIGN.md 6)"}
+    out["frac"] = round(out["achieved"] / out["peak"], 4)
+    out["traffic"] = _traffic_for(k)
+    out["phases"] = per
+    return out
 
 
 def _traffic_for(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel from the
+    committed ncu --set full capture (profiles/traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get(kernel)
+            v = json.load(open(p)).get(kernel)
+            return int(v) if v is not None else None
         except Exception:
             return None
     return None
