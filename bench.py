@@ -128,7 +128,10 @@ def run_ours(args):
     A.lib()
 
     cfg = tracegen.CONFIGS[args.config]
-    tr = tracegen.gen_trace(cfg, seed=cfg.seed + 1000 * rank)
+    if args.target_topk:
+        tr = tracegen.gen_trace_topk(cfg, K_t=args.target_topk, seed=cfg.seed + 1000 * rank)
+    else:
+        tr = tracegen.gen_trace(cfg, seed=cfg.seed + 1000 * rank)
     R, N, d, V, M = cfg.R, cfg.N, cfg.d, cfg.V, cfg.M
 
     comm = None
@@ -138,20 +141,32 @@ def run_ours(args):
         dist.broadcast_object_list(obj, src=0)
         comm = A.aurora_comm_create(obj[0], ws, rank, 1, ws)
 
-    T = _bf16(tr["T_bits"], torch, dev)
+    sparse = bool(args.target_topk)
+    if sparse:
+        Tk_idx = torch.from_numpy(tr["Tk_idx"]).to(dev)
+        Tk_val = _bf16(tr["Tk_bits"], torch, dev)
+    else:
+        T = _bf16(tr["T_bits"], torch, dev)
     H = _bf16(tr["H_bits"], torch, dev)
     W = _bf16(tr["W_bits"], torch, dev)
     draft = torch.from_numpy(tr["draft_tokens"]).to(dev)
     parents = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).to(dev)
     num_nodes = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).to(dev)
     st = A.SpecTrainStep(R, N, d, V, comm=comm, device=dev)
+    if sparse and A.aurora_workspace_size(A.OP_VERIFY, M, d, args.target_topk, st.cfg) > st.ws_bytes:
+        raise SystemExit("workspace too small for --target-topk")
     dH = torch.empty(M, d, dtype=torch.float32, device=dev)
     dW = torch.empty(V, d, dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        st.step(draft, T, H, W, dH, dW, parents, num_nodes)
+        if sparse:
+            st.verify_topk(draft, Tk_idx, Tk_val, parents, num_nodes)
+            st.forward(H, W)
+            st.backward(H, W, dH, dW)
+        else:
+            st.step(draft, T, H, W, dH, dW, parents, num_nodes)
 
     for _ in range(args.warmup):
         step()
@@ -186,7 +201,7 @@ def run_ours(args):
     tokens_per_s = (M * ws) / (ms_step / 1e3)
 
     # ---------------- e2e: public API with pinned host inputs, result read back
-    e2e = _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush)
+    e2e = None if sparse else _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush)
 
     if rank != 0:
         if comm is not None:
@@ -210,7 +225,9 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (tracegen seeded traces; random-init lm_head)",
-        "config": {"workload": cfg.name, "R": R, "N": N, "M_rows_per_gpu": M, "d": d, "V": V,
+        "config": {"workload": cfg.name + (f"+topk{args.target_topk}" if sparse else ""), "R": R, "N": N,
+                   "M_rows_per_gpu": M, "d": d, "V": V,
+                   "target": f"top-{args.target_topk} (id, logit) pairs per row (F1)" if sparse else "dense bf16 logits",
                    "tree": cfg.tree, "parallelism": f"dp{ws}" if ws > 1 else "single",
                    "l2": "flushed between timed steps (256 MiB write outside the step events)"},
         "gpu_launches": int(n_launch),
@@ -438,6 +455,8 @@ def main():
     ap.add_argument("--ref-reqs", type=int, default=2)
     ap.add_argument("--warmup-ref", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--target-topk", type=int, default=0,
+                    help="NEXT F1: feed the verifier logits as the transmitted top-K payload (e.g. 1024)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

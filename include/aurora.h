@@ -134,6 +134,29 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* trace, const aurora_l
                                      aurora_labels_t* out, void* ws, size_t ws_bytes,
                                      aurora_comm_t comm, void* stream);
 
+/* NEXT F1 — sparse target ingest: the verifier's logits arrive as the paper's transmitted
+ * top-K payload ("top-K logits filtering (e.g., K=1024)").
+ * Same verification and targets as aurora_verify_labels, computed from the pairs. */
+typedef struct {
+  int32_t R, N;                  /* as aurora_trace_t                                      */
+  const int32_t* draft_tokens;   /* (dev) int32 [R,N]                                      */
+  const int32_t* parents;        /* (dev) int32 [R,N] or NULL (chain)                      */
+  const int32_t* num_nodes;      /* (dev) int32 [R] or NULL                                */
+  const int32_t* target_ids;     /* (dev) int32 [M, K_t] global vocab ids, distinct per row,
+                                    any order                                              */
+  const void* target_vals;       /* (dev) bf16 [M, K_t] verifier logits of those ids       */
+  int32_t K_t;                   /* transmitted pairs per row, >= max(k_accept, k_discard) */
+  int64_t V;                     /* global vocabulary size                                 */
+} aurora_trace_topk_t;
+
+/* argmax / top-k_max are taken over the K_t transmitted pairs by (value desc, id asc);
+ * status bits: non-finite logit, id outside [0, V) (pair skipped), an id seen twice in the
+ * top list (STRUCTURE).  Workspace: aurora_workspace_size(AURORA_OP_VERIFY, M, d, K_t, cfg).
+ * VP ranks each hold the full payload (no candidate exchange); DP sums the counts. */
+aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* trace, const aurora_loss_cfg_t* cfg,
+                                          aurora_labels_t* out, void* ws, size_t ws_bytes,
+                                          aurora_comm_t comm, void* stream);
+
 /* Forward (Eq. 3).
  * H (dev) bf16 [M,d] draft-head hidden states; W (dev) bf16 [V_local,d] lm_head rows
  * for global ids [vocab_offset, vocab_offset+V_local).  d % 64 == 0.

@@ -10,6 +10,7 @@ step by step in the paper's order (PAPER.md = P, SPEC.md = S, line numbers):
 
   O1 target_scan   y = argmax of the verifier logits (lowest index wins ties),
                    and the top-K list ordered by (value desc, index asc).
+                   target_scan_topk: the same over the transmitted top-K payload (F1).
                    P:120 §2.1 "accepting the longest matching prefix" (greedy,
                    P:526 Table 3 "Top-k Sampling 1"); ties S:84.
   O2 verify        acc(n) = acc(parent(n)) AND [x_n == y at the parent's row];
@@ -60,6 +61,28 @@ def target_scan(T_rows: np.ndarray, k_max: int):
     order = np.argsort(-T_rows, axis=1, kind="stable")
     topk = order[:, :k_max]
     return topk[:, 0].copy(), topk.copy(), nonfinite
+
+
+def target_scan_topk(idx: np.ndarray, val: np.ndarray, k_max: int, V: int):
+    """O1' (NEXT F1): the same scan over the paper's transmitted sparse payload — the
+    target's top-K logits per position as (global id, logit) pairs ("top-K
+    logits filtering (e.g., K=1024)"; SPEC S:420-428 compressed payload).  The order is
+    again (value desc, index asc) over the transmitted pairs.
+
+    idx int [m, K_t], val f64 [m, K_t].  Returns (argmax [m], topk ids [m, k_max],
+    nonfinite, out_of_range, duplicate) — the last three are the conditions the kernel
+    reports in the status word.
+    """
+    idx = np.asarray(idx, dtype=np.int64)
+    val = np.asarray(val, dtype=np.float64)
+    nonfinite = not bool(np.all(np.isfinite(val)))
+    out_of_range = bool(np.any((idx < 0) | (idx >= V)))
+    dup = any(len(np.unique(r)) != len(r) for r in idx)
+    topk = np.empty((idx.shape[0], k_max), dtype=np.int64)
+    for m in range(idx.shape[0]):
+        order = np.lexsort((idx[m], -val[m]))       # primary: value desc, secondary: id asc
+        topk[m] = idx[m][order[:k_max]]
+    return topk[:, 0].copy(), topk, nonfinite, out_of_range, dup
 
 
 # --------------------------------------------------------------------------- O2
@@ -268,4 +291,30 @@ def step(trace: dict, k_accept: int = 1, k_discard: int = 10, lambda_discard: fl
                loss=fw["loss"])
     if want_grads:
         out.update(loss_bwd(H64, Wb, tg, fw["lse"], g=g, want_dW=want_dW))
+    return out
+
+
+def step_topk(trace: dict, k_accept: int = 1, k_discard: int = 10, lambda_discard: float = 1.0,
+              normalize: int = 0, discard_scope: int = 0, g: float = 1.0, want_grads: bool = True):
+    """verify -> targets -> fwd -> bwd with the sparse target payload (F1): trace holds
+    Tk_idx int32 [M, K_t] and Tk_bits bf16 [M, K_t] instead of T_bits."""
+    vals = bf16_bits_to_f64(trace["Tk_bits"])
+    idx = np.asarray(trace["Tk_idx"], dtype=np.int64)
+    H64 = bf16_bits_to_f64(trace["H_bits"])
+    k_max = max(k_accept, k_discard)
+    amax, topk, nonfinite, oor, dup = target_scan_topk(idx, vals, k_max, trace["V"])
+    if nonfinite or oor or dup:
+        raise ValueError("invalid sparse target payload")
+    lab = verify(trace["draft_tokens"], trace["parents"], trace["num_nodes"], amax, discard_scope)
+
+    def row_logits(m):  # the support values come from the transmitted pairs
+        full = np.full(trace["V"], -np.inf)
+        full[idx[m]] = vals[m]
+        return full
+
+    tg = row_targets(lab["row_class"], row_logits, topk, k_accept, k_discard, lambda_discard, normalize)
+    fw = loss_fwd(H64, trace["W_bits"], tg)
+    out = dict(argmax=amax, topk=topk, **lab, targets=tg, lse=fw["lse"], row_loss=fw["row_loss"], loss=fw["loss"])
+    if want_grads:
+        out.update(loss_bwd(H64, trace["W_bits"], tg, fw["lse"], g=g))
     return out

@@ -26,7 +26,8 @@ MAX_K, MAX_NODES = 16, 32
 EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fwd", "aurora_spec_loss_bwd",
            "aurora_comm_get_unique_id", "aurora_comm_create", "aurora_comm_destroy", "aurora_status_string",
            "aurora_build_info", "aurora_launch_count", "aurora_profile_enable", "aurora_profile_read",
-           "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option"]
+           "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option",
+           "aurora_verify_labels_topk"]
 
 
 class AuroraError(RuntimeError):
@@ -39,6 +40,12 @@ class aurora_trace_t(C.Structure):
     _fields_ = [("R", C.c_int32), ("N", C.c_int32), ("draft_tokens", C.c_void_p), ("parents", C.c_void_p),
                 ("num_nodes", C.c_void_p), ("target_logits", C.c_void_p), ("ld_target", C.c_int64),
                 ("V", C.c_int64), ("V_local", C.c_int64), ("vocab_offset", C.c_int64)]
+
+
+class aurora_trace_topk_t(C.Structure):
+    _fields_ = [("R", C.c_int32), ("N", C.c_int32), ("draft_tokens", C.c_void_p), ("parents", C.c_void_p),
+                ("num_nodes", C.c_void_p), ("target_ids", C.c_void_p), ("target_vals", C.c_void_p),
+                ("K_t", C.c_int32), ("V", C.c_int64)]
 
 
 class aurora_loss_cfg_t(C.Structure):
@@ -98,6 +105,9 @@ def lib() -> C.CDLL:
     L.aurora_debug_dlogits_rows.argtypes = [vp, vp, i64, i64, i64, i64, C.POINTER(aurora_labels_t), vp, vp, vp,
                                             i32, vp, vp]
     L.aurora_debug_dlogits_rows.restype = C.c_int
+    L.aurora_verify_labels_topk.argtypes = [C.POINTER(aurora_trace_topk_t), C.POINTER(aurora_loss_cfg_t),
+                                            C.POINTER(aurora_labels_t), vp, sz, vp, vp]
+    L.aurora_verify_labels_topk.restype = C.c_int
     L.aurora_set_option.argtypes = [C.c_char_p, C.c_int64]
     L.aurora_set_option.restype = C.c_int
     L.aurora_get_option.argtypes = [C.c_char_p]
@@ -264,6 +274,22 @@ class SpecTrainStep:
         t = aurora_trace_t(self.R, self.N, _ptr(draft_tokens), _ptr(parents), _ptr(num_nodes), _ptr(target_logits),
                            target_logits.stride(0), self.V, self.V_local, self.vocab_offset)
         aurora_verify_labels(t, self.cfg, self.labels, self.ws.data_ptr(), self.ws_bytes, self.comm, stream)
+
+    def verify_topk(self, draft_tokens, target_ids, target_vals, parents=None, num_nodes=None, stream=None):
+        """NEXT F1: labels from the transmitted top-K target payload (ids int32 [M, K_t],
+        bf16 logits [M, K_t]) instead of dense logits."""
+        _expect(draft_tokens, "i32", "draft_tokens"); _expect(parents, "i32", "parents")
+        _expect(num_nodes, "i32", "num_nodes"); _expect(target_ids, "i32", "target_ids")
+        _expect(target_vals, "bf16", "target_vals")
+        K_t = target_ids.shape[1]
+        need = aurora_workspace_size(OP_VERIFY, self.M, self.d, K_t, self.cfg)
+        if need > self.ws_bytes:
+            raise ValueError("workspace too small for this K_t")
+        t = aurora_trace_topk_t(self.R, self.N, _ptr(draft_tokens), _ptr(parents), _ptr(num_nodes), _ptr(target_ids),
+                                _ptr(target_vals), K_t, self.V)
+        _check("aurora_verify_labels_topk", lib().aurora_verify_labels_topk(
+            C.byref(t), C.byref(self.cfg), C.byref(self.labels), self.ws.data_ptr(), self.ws_bytes, self.comm,
+            _stream(stream)))
 
     def forward(self, H, W, stream=None):
         aurora_spec_loss_fwd(H, W, self.M, self.d, self.V_local, self.vocab_offset, self.labels, self.row_lse,

@@ -599,6 +599,58 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   return AURORA_OK;
 }
 
+aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const aurora_loss_cfg_t* cfg,
+                                          aurora_labels_t* out, void* ws, size_t ws_bytes, aurora_comm_t comm,
+                                          void* stream) {
+  if (!t || !out) return AURORA_ERR_INVALID_ARG;
+  aurora_status_t st = check_cfg(cfg);
+  if (st != AURORA_OK) return st;
+  if (t->R < 1 || t->N < 1 || t->N > AURORA_MAX_NODES || !t->draft_tokens || !t->target_ids || !t->target_vals)
+    return AURORA_ERR_INVALID_ARG;
+  if (t->V < 1 || t->V > INT32_MAX || t->K_t < 1) return AURORA_ERR_INVALID_ARG;
+  if (!labels_ok(out, true)) return AURORA_ERR_INVALID_ARG;
+  const int k_max = out->k_max;
+  if (k_max < std::max(cfg->k_accept, cfg->k_discard) || std::max(cfg->k_accept, cfg->k_discard) > t->K_t)
+    return AURORA_ERR_INVALID_ARG;
+  const int64_t M = static_cast<int64_t>(t->R) * (t->N + 1);
+  if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->K_t, cfg)) return AURORA_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  VerifyWs w = carve_verify(c, M, t->K_t, k_max);
+  VerifyLaunch p{};
+  p.V = t->V;
+  p.V_local = t->V;
+  p.M = static_cast<int32_t>(M);
+  p.R = t->R;
+  p.N = t->N;
+  p.k_max = k_max;
+  p.nseg = 1;
+  p.draft = t->draft_tokens;
+  p.parents = t->parents;
+  p.num_nodes = t->num_nodes;
+  p.top_val = w.top_val;
+  p.top_idx = w.top_idx;
+  p.lab = *out;
+  p.cfg = *cfg;
+  if (cudaMemsetAsync(out->counts, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (cudaMemsetAsync(out->status, 0, sizeof(uint32_t), s) != cudaSuccess) return AURORA_ERR_CUDA;
+  prof_begin(PH_SCAN, s);
+  if (launch_target_scan_topk(p, t->target_ids, static_cast<const uint16_t*>(t->target_vals), t->K_t, s) !=
+      cudaSuccess)
+    return AURORA_ERR_CUDA;
+  prof_end(PH_SCAN, s);
+  prof_begin(PH_VERIFY, s);
+  if (launch_verify(p, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (comm && comm->dp_x()) {
+    auto& A = nccl::api();
+    if (A.AllReduce(out->counts, out->counts, 2, nccl::ncclInt32, nccl::ncclSum, comm->dp, s) != 0)
+      return AURORA_ERR_NCCL;
+  }
+  if (launch_finalize(p, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  prof_end(PH_VERIFY, s);
+  return AURORA_OK;
+}
+
 aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
                                      int64_t vocab_offset, const aurora_labels_t* labels, float* row_lse,
                                      float* row_loss, float* loss, void* ws, size_t ws_bytes, aurora_comm_t comm,

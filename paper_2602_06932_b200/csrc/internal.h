@@ -122,6 +122,8 @@ struct VerifyLaunch {
 cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s);
 cudaError_t launch_topk_merge(const VerifyLaunch& p, const float* in_val, const int32_t* in_idx, int nlists,
                               int64_t row_stride, int64_t list_stride, cudaStream_t s);
+cudaError_t launch_target_scan_topk(const VerifyLaunch& p, const int32_t* tk_idx, const uint16_t* tk_val, int32_t K_t,
+                                    cudaStream_t s);
 cudaError_t launch_verify(const VerifyLaunch& p, cudaStream_t s);
 cudaError_t launch_finalize(const VerifyLaunch& p, cudaStream_t s);
 

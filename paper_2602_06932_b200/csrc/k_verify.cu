@@ -307,6 +307,57 @@ __global__ void __launch_bounds__(256) k_topk_merge(VerifyLaunch p, const float*
   if (lane == 0) p.lab.target_argmax[row] = am;
 }
 
+// --------------------------------------------------------------------------- A2' sparse
+// NEXT F1: the target arrives as its top-K_t logits per row, (global id, bf16 logit)
+// pairs in any order ("top-K logits filtering (e.g., K=1024)").  Warp per row:
+// lanes stride over the pairs, the warp list keeps the top-k_max by (value desc, id asc).
+// Status bits: non-finite logit, id outside [0, V), an id appearing twice in the top list.
+__global__ void __launch_bounds__(256) k_target_scan_topk(VerifyLaunch p, const int32_t* __restrict__ tk_idx,
+                                                          const uint16_t* __restrict__ tk_val, int32_t K_t) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= p.M) return;
+  const int k = p.k_max;
+  WarpList L;
+  L.init(k);
+  uint32_t err = 0;
+  const int64_t o = static_cast<int64_t>(row) * K_t;
+  for (int j0 = 0; j0 < K_t; j0 += 32) {
+    const int j = j0 + lane;
+    float v = -INFINITY;
+    int32_t id = INT32_MAX;
+    bool ok = false;
+    if (j < K_t) {
+      const uint32_t b = tk_val[o + j];
+      id = tk_idx[o + j];
+      if ((b & 0x7FFFu) >= 0x7F80u) err |= AURORA_STATUS_NONFINITE;
+      else if (id < 0 || static_cast<int64_t>(id) >= p.V) err |= AURORA_STATUS_RANGE;
+      else { v = __uint_as_float(b << 16); ok = true; }
+    }
+    uint32_t hit = __ballot_sync(0xffffffffu, ok && L.admits(v, id));
+    while (hit) {
+      const int src = __ffs(hit) - 1;
+      hit &= hit - 1;
+      const float cv = __shfl_sync(0xffffffffu, v, src);
+      const int32_t ci = __shfl_sync(0xffffffffu, id, src);
+      if (L.admits(cv, ci)) {
+        if (__any_sync(0xffffffffu, lane < k && L.i == ci)) err |= AURORA_STATUS_STRUCTURE;  // duplicate id
+        else L.insert(cv, ci);
+      }
+    }
+  }
+  err = __reduce_or_sync(0xffffffffu, err);
+  if (lane < k) {
+    p.top_val[static_cast<int64_t>(row) * k + lane] = L.v;
+    p.top_idx[static_cast<int64_t>(row) * k + lane] = L.i;
+  }
+  const int32_t am = __shfl_sync(0xffffffffu, L.i, 0);
+  if (lane == 0) {
+    p.lab.target_argmax[row] = am;
+    if (err) atomicOr(p.lab.status, err);
+  }
+}
+
 // --------------------------------------------------------------------------- A3 verify
 // warp per request; lane n = draft node n.
 __global__ void __launch_bounds__(256) k_verify(VerifyLaunch p) {
@@ -443,6 +494,12 @@ cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s) {
 cudaError_t launch_topk_merge(const VerifyLaunch& p, const float* in_val, const int32_t* in_idx, int nlists,
                               int64_t row_stride, int64_t list_stride, cudaStream_t s) {
   k_topk_merge<<<(p.M + 7) / 8, 256, 0, s>>>(p, in_val, in_idx, nlists, row_stride, list_stride);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_target_scan_topk(const VerifyLaunch& p, const int32_t* tk_idx, const uint16_t* tk_val, int32_t K_t,
+                                    cudaStream_t s) {
+  k_target_scan_topk<<<(p.M + 7) / 8, 256, 0, s>>>(p, tk_idx, tk_val, K_t);
   count_launch();
   return cudaGetLastError();
 }

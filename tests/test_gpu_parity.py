@@ -248,7 +248,7 @@ def test_llama_full_size_parity():
     assert _rfro(out["dH"].cpu().numpy(), ref["dH"]) <= GRAD_RFRO
 
 
-@pytest.mark.parametrize("name", ["qwen3", "minimax"])
+@pytest.mark.parametrize("name", ["qwen3", "minimax", "tree"])
 def test_large_config_sampled_parity(name):
     """Full-size configs: labels bit-exact on every row (oracle scan row by row),
     per-row lse / loss on sampled rows, dW column-sum property at full size."""
@@ -388,3 +388,75 @@ def test_fused_bwd_emulated_vp_and_serial(option):
     option("bwd_mode", 0)
     option("bwd_concurrent", 0)
     test_full_parity_small("small")
+
+
+def _run_gpu_topk(tr, **kw):
+    c = tr["cfg"]
+    g = _to_gpu_base(tr)
+    ids = torch.from_numpy(tr["Tk_idx"]).cuda()
+    vals = torch.from_numpy(np.ascontiguousarray(tr["Tk_bits"]).view(np.int16)).view(torch.bfloat16).cuda()
+    st = A.SpecTrainStep(c.R, c.N, c.d, c.V, **kw)
+    st.verify_topk(g["draft"], ids, vals, g["parents"], g["num_nodes"])
+    st.forward(g["H"], g["W"])
+    dH = torch.empty(c.M, c.d, dtype=torch.float32, device="cuda")
+    dW = torch.empty(c.V, c.d, dtype=torch.float32, device="cuda")
+    st.backward(g["H"], g["W"], dH, dW)
+    torch.cuda.synchronize()
+    return st, dH, dW
+
+
+def _to_gpu_base(tr):
+    g = dict(H=_bf16(tr["H_bits"]), W=_bf16(tr["W_bits"]), draft=torch.from_numpy(tr["draft_tokens"]).cuda())
+    g["parents"] = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).cuda()
+    g["num_nodes"] = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).cuda()
+    return g
+
+
+@pytest.mark.parametrize("name,K_t", [("tiny", 64), ("small", 1024), ("small_tree", 100), ("mid", 1024)])
+def test_topk_ingest_parity(name, K_t):
+    """NEXT F1: labels from the transmitted top-K payload bit-exact vs the oracle's sparse
+    scan; loss / dW / dH within the north-star tolerances."""
+    tr = tracegen.gen_trace_topk(name, K_t=K_t)
+    ref = oracle.step_topk(tr)
+    st, dH, dW = _run_gpu_topk(tr)
+    _check_labels(st, ref, tr)
+    loss = float(st.loss.item())
+    assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"])
+    assert _rfro(dW.cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert _rfro(dH.cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+def test_topk_ingest_matches_dense_path():
+    """The dense path and the sparse path give identical labels when the payload holds
+    every column of the dense rows (a shuffled full row)."""
+    tr = tracegen.gen_trace("small")
+    c = tr["cfg"]
+    rng = np.random.default_rng(3)
+    perm = np.stack([rng.permutation(c.V) for _ in range(c.M)]).astype(np.int32)
+    tr["Tk_idx"] = perm
+    tr["Tk_bits"] = np.take_along_axis(tr["T_bits"], perm, 1)
+    dense = _run_gpu(tr)
+    st, dH, dW = _run_gpu_topk(tr)
+    for k in ("target_argmax", "accepted", "accept_len", "bonus", "row_class", "sup_idx", "counts"):
+        assert torch.equal(getattr(st, k), getattr(dense["st"], k)), k
+    assert torch.allclose(st.sup_p, dense["st"].sup_p)
+    assert torch.equal(dW, dense["dW"]) and torch.equal(dH, dense["dH"])
+
+
+def test_topk_ingest_status_bits():
+    tr = tracegen.gen_trace_topk("small", K_t=64)
+    c = tr["cfg"]
+    g = _to_gpu_base(tr)
+    ids = torch.from_numpy(tr["Tk_idx"]).cuda()
+    vals = torch.from_numpy(np.ascontiguousarray(tr["Tk_bits"]).view(np.int16)).view(torch.bfloat16).cuda()
+    st = A.SpecTrainStep(c.R, c.N, c.d, c.V)
+    bad = ids.clone()
+    bad[2, 5] = c.V + 3
+    st.verify_topk(g["draft"], bad, vals, g["parents"], g["num_nodes"])
+    torch.cuda.synchronize()
+    assert int(st.status.item()) & A.STATUS_RANGE
+    v2 = vals.clone()
+    v2[4, 0] = float("inf")
+    st.verify_topk(g["draft"], ids, v2, g["parents"], g["num_nodes"])
+    torch.cuda.synchronize()
+    assert int(st.status.item()) & A.STATUS_NONFINITE

@@ -85,6 +85,57 @@ def test_scan_bruteforce_small_vocab(seed):
         assert int(am[i]) == int(np.argmax(T[i]))          # numpy: first occurrence of the max
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_scan_topk_payload_equals_dense_scan(seed):
+    """F1 pin: when the transmitted pairs are a superset of a row's top-k (here: every
+    column, shuffled, or the k_max best plus random others), the sparse scan returns
+    exactly the dense O1 result; brute force on the pairs as a second route."""
+    rng = np.random.default_rng(500 + seed)
+    V, k = int(rng.integers(12, 60)), int(rng.integers(1, 11))
+    vals = np.array([-1.0, -0.0, 0.0, 0.5, 2.0, 3.0])
+    T = vals[rng.integers(0, len(vals), size=(5, V))]
+    am, topk, _ = oracle.target_scan(T, k)
+    perm = np.stack([rng.permutation(V) for _ in range(5)])
+    am2, topk2, nf, oor, dup = oracle.target_scan_topk(perm, np.take_along_axis(T, perm, 1), k, V)
+    assert not (nf or oor or dup)
+    np.testing.assert_array_equal(am2, am)
+    np.testing.assert_array_equal(topk2, topk)
+    # superset = true top-k plus random extras, shuffled
+    for i in range(5):
+        extra = rng.choice(np.setdiff1d(np.arange(V), topk[i]), size=min(3, V - k), replace=False)
+        ids = rng.permutation(np.concatenate([topk[i], extra]))
+        _, tk, _, _, _ = oracle.target_scan_topk(ids[None], T[i][ids][None], k, V)
+        assert tk[0].tolist() == topk[i].tolist()
+        # brute force over the pairs: largest value first, smallest id on ties
+        pairs = [(float(T[i][j]), int(j)) for j in ids]
+        bf = []
+        for _ in range(k):
+            best = pairs[0]
+            for pv in pairs[1:]:
+                if pv[0] > best[0] or (pv[0] == best[0] and pv[1] < best[1]):
+                    best = pv
+            bf.append(best[1])
+            pairs.remove(best)
+        assert tk[0].tolist() == bf
+
+
+def test_scan_topk_flags():
+    _, _, nf, oor, dup = oracle.target_scan_topk(np.array([[1, 5, 5]]), np.array([[0.0, 1.0, 2.0]]), 1, 10)
+    assert dup and not nf and not oor
+    _, _, nf, oor, dup = oracle.target_scan_topk(np.array([[1, 12]]), np.array([[0.0, np.nan]]), 1, 10)
+    assert nf and oor
+
+
+def test_topk_trace_generator_contract():
+    tr = tracegen.gen_trace_topk("small", K_t=64)
+    assert tr["Tk_idx"].shape == (tr["M"], 64)
+    for m in range(tr["M"]):
+        assert len(set(tr["Tk_idx"][m].tolist())) == 64
+        assert tr["designated"][m] in tr["Tk_idx"][m]
+    out = oracle.step_topk(tr, want_grads=False)
+    np.testing.assert_array_equal(out["argmax"], tr["designated"])   # planted strict maximum
+
+
 def test_scan_nonfinite_flag():
     _, _, nf = oracle.target_scan(np.array([[1.0, np.nan, 0.0]]), 1)
     assert nf

@@ -38,7 +38,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["TraceConfig", "CONFIGS", "gen_trace", "f32_to_bf16_bits", "bf16_bits_to_f32"]
+__all__ = ["TraceConfig", "CONFIGS", "gen_trace", "gen_trace_topk", "f32_to_bf16_bits", "bf16_bits_to_f32"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -229,3 +229,34 @@ def _inject_ties(rng: np.random.Generator, T_bits: np.ndarray) -> None:
     T_bits[m, :] = f32_to_bf16_bits(-np.abs(vals[m]) - 1.0)   # everything negative
     T_bits[m, 7] = 0x8000                                        # -0.0
     T_bits[m, 3] = 0x0000                                        # +0.0 (equal; lower index)
+
+
+def gen_trace_topk(cfg: TraceConfig | str, K_t: int = 1024, seed: Optional[int] = None) -> dict:
+    """NEXT F1 workload: the same trace (W, H, tokens, parents, planted designated tokens)
+    with the verifier's logits delivered as the paper's transmitted payload — K_t
+    (id, bf16 logit) pairs per row ("top-K = 1024").  Each row draws K_t
+    distinct ids (the designated token always among them, at a random slot), logits
+    ~ N(0, 2^2), and the designated token gets max + 1.0.  Drawn directly; nothing is
+    selected from a dense row, so no method arithmetic lives here."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    tr = gen_trace(cfg, seed=seed, gen_T=False)
+    rng = np.random.Generator(np.random.PCG64((cfg.seed if seed is None else seed) + 7919))
+    M, V = tr["M"], tr["V"]
+    K_t = min(K_t, V)
+    ids = np.empty((M, K_t), dtype=np.int32)
+    vals = np.empty((M, K_t), dtype=np.uint16)
+    for m in range(M):
+        row = rng.choice(V, size=K_t, replace=False)
+        des = int(tr["designated"][m])
+        hit = np.nonzero(row == des)[0]
+        slot = int(hit[0]) if len(hit) else int(rng.integers(0, K_t))
+        row[slot] = des
+        v = rng.standard_normal(K_t, dtype=np.float32) * np.float32(2.0)
+        v[slot] = v.max() + np.float32(1.0)
+        ids[m] = row
+        vals[m] = f32_to_bf16_bits(v)
+    tr["Tk_idx"] = ids
+    tr["Tk_bits"] = vals
+    tr["K_t"] = K_t
+    return tr
