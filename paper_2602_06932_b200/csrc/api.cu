@@ -128,11 +128,12 @@ struct Carver {
 struct Options {
   int gemm_pair = 0;       // 0 auto, 1 single-CTA tiles, 2 CTA-pair tiles
   int bwd_mode = 0;        // 0 classic per-chunk launches, 1 fused persistent kernel
-  int bwd_concurrent = 1;  // classic mode: dW || dH on side streams
+  int bwd_concurrent = 0;  // classic mode: dW || dH on side streams (measured equal to serial; off
+                           // by default so per-kernel event timings stay clean)
   Options() {
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
-    if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '1') ? 0 : 1;
+    if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
   }
 };
 Options& opts() {

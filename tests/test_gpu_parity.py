@@ -386,8 +386,9 @@ def test_fused_bwd_emulated_vp_and_serial(option):
     option("bwd_mode", 1)
     test_emulated_vocab_parallel_shards((1000, 2049, 4100))
     option("bwd_mode", 0)
-    option("bwd_concurrent", 0)
+    option("bwd_concurrent", 1)   # dW || dH on the library's side streams
     test_full_parity_small("small")
+    test_determinism()
 
 
 def _run_gpu_topk(tr, **kw):
