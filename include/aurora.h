@@ -207,7 +207,10 @@ uint64_t aurora_launch_count(void);
  *   "gemm_pair"      0 auto (default), 1 single-CTA 128x256 tiles, 2 CTA-pair 256x256
  *                    tiles (tcgen05.mma.cta_group::2)
  *   "bwd_mode"       0 per-chunk launches (default), 1 one fused persistent kernel
- *   "bwd_concurrent" 0 (default): serial; 1: dW || dH of a chunk on library side streams */
+ *   "bwd_concurrent" 0 (default): serial; 1: dW || dH of a chunk on library side streams
+ *   "tile_n"         fwd / dz vocab tile width with single-CTA tiles: 0 auto (default:
+ *                    the width among 256/224/192 with the least per-SM work for the
+ *                    tile count), or force 256, 224 or 192.  Other values: INVALID_ARG. */
 aurora_status_t aurora_set_option(const char* name, int64_t value);
 int64_t aurora_get_option(const char* name);
 

@@ -130,7 +130,9 @@ struct Options {
   int bwd_mode = 0;        // 0 classic per-chunk launches, 1 fused persistent kernel
   int bwd_concurrent = 0;  // classic mode: dW || dH on side streams (measured equal to serial; off
                            // by default so per-kernel event timings stay clean)
+  int tile_n = 0;          // fwd / dz tile width: 0 auto, else 256 / 224 / 192
   Options() {
+    if (const char* e = getenv("AURORA_TILE_N")) tile_n = atoi(e);
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
     if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
@@ -145,6 +147,22 @@ int pair_for(int64_t rows) {
   if (opts().gemm_pair == 1) return 1;
   if (opts().gemm_pair == 2) return 2;
   return (rows % 256 == 0 || rows >= 4096) ? 2 : 1;
+}
+// Tile width for the K-major fwd / dz GEMMs (single-CTA tiles only).  A persistent CTA
+// does ceil(tiles / 148) tiles, each costing ~width: pick the width with the least
+// per-SM work, 256 unless a narrower one is >= 2% better.
+constexpr int kTileWidths[3] = {256, 224, 192};
+constexpr int kMinBN = 192;
+int kmajor_bn(int64_t m_tiles, int64_t N, int pair) {
+  if (pair != 1) return BN;
+  if (opts().tile_n) return opts().tile_n;
+  int best = BN;
+  double best_cost = static_cast<double>(cdiv(m_tiles * cdiv(N, BN), kNumSMs)) * BN;
+  for (int bn : kTileWidths) {
+    const double cost = static_cast<double>(cdiv(m_tiles * cdiv(N, bn), kNumSMs)) * bn;
+    if (cost < 0.98 * best_cost) { best = bn; best_cost = cost; }
+  }
+  return best;
 }
 int scan_nseg(int64_t M, int64_t V_local) {
   int64_t nseg = cdiv(8 * kNumSMs, std::max<int64_t>(M, 1));
@@ -185,13 +203,13 @@ VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
   w.top_idx = c.take<int32_t>(M * k_max);
   return w;
 }
-struct FwdWs { float *pm, *ps, *pu, *msu, *bp; int n_tiles; };
+struct FwdWs { float *pm, *ps, *pu, *msu, *bp; };
 FwdWs carve_fwd(Carver& c, int64_t M, int64_t V_local) {
   FwdWs w;
-  w.n_tiles = static_cast<int>(cdiv(V_local, BN));
-  w.pm = c.take<float>(M * 2 * w.n_tiles);  // one partial per (vocab tile, column half)
-  w.ps = c.take<float>(M * 2 * w.n_tiles);
-  w.pu = c.take<float>(M * 2 * w.n_tiles);
+  const int64_t max_tiles = cdiv(V_local, kMinBN);  // sized for the narrowest tile width
+  w.pm = c.take<float>(M * 2 * max_tiles);  // one partial per (vocab tile, column half)
+  w.ps = c.take<float>(M * 2 * max_tiles);
+  w.pu = c.take<float>(M * 2 * max_tiles);
   w.msu = c.take<float>(M * 3);
   w.bp = c.take<float>(cdiv(M, 256) + 1);
   return w;
@@ -449,6 +467,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
+  if (std::strcmp(name, "tile_n") == 0 && (value == 0 || value == 256 || value == 224 || value == 192)) {
+    o.tile_n = static_cast<int>(value);
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "bwd_concurrent") == 0 && value >= 0 && value <= 1) {
     o.bwd_concurrent = static_cast<int>(value);
     return AURORA_OK;
@@ -462,6 +484,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "gemm_pair") == 0) return o.gemm_pair;
   if (std::strcmp(name, "bwd_mode") == 0) return o.bwd_mode;
   if (std::strcmp(name, "bwd_concurrent") == 0) return o.bwd_concurrent;
+  if (std::strcmp(name, "tile_n") == 0) return o.tile_n;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
   return -1;
 }
@@ -665,12 +688,13 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   FwdWs w = carve_fwd(c, M, V_local);
 
   const int pf = pair_for(M);
+  const int bn = kmajor_bn(cdiv(M, BM * pf), V_local, pf);
   CUtensorMap tmH, tmW;
   if (!make_tmap_bf16(&tmH, H, d, M, d, 64, BM)) return AURORA_ERR_CUDA;
-  if (!make_tmap_bf16(&tmW, W, d, V_local, d, 64, BN / pf)) return AURORA_ERR_CUDA;
+  if (!make_tmap_bf16(&tmW, W, d, V_local, d, 64, bn / pf)) return AURORA_ERR_CUDA;
   GemmArgs a{};
   a.m_tiles = static_cast<int32_t>(cdiv(M, BM * pf));
-  a.n_tiles = w.n_tiles;
+  a.n_tiles = static_cast<int32_t>(cdiv(V_local, bn));
   a.splits = 1;
   a.kb_total = static_cast<int32_t>(d / BK);
   a.kb_per_split = a.kb_total;
@@ -684,11 +708,11 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   a.p_sum = w.ps;
   a.p_u = w.pu;
   prof_begin(PH_FWD_GEMM, s);
-  cudaError_t e = launch_umma_gemm(EPI_FWD_STATS, false, false, tmH, tmW, a, s, nullptr, pf);
+  cudaError_t e = launch_umma_gemm(EPI_FWD_STATS, false, false, tmH, tmW, a, s, nullptr, pf, bn);
   prof_end(PH_FWD_GEMM, s);
   if (e != cudaSuccess) return AURORA_ERR_CUDA;
   prof_begin(PH_FWD_COMBINE, s);
-  if ((e = launch_reduce_partials(w.pm, w.ps, w.pu, M, 2 * w.n_tiles, w.msu, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  if ((e = launch_reduce_partials(w.pm, w.ps, w.pu, M, 2 * a.n_tiles, w.msu, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   const float* msu_all = w.msu;
   int P = 1;
   if (comm && comm->vp_x()) {
@@ -750,8 +774,9 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     const int64_t vc = std::min(w.vc, V_local - c0);
     __nv_bfloat16* dzT = w.dzT;
     const int pz = pair_for(M), pw = pair_for(vc);
+    const int bz = kmajor_bn(cdiv(M, BM * pz), vc, pz);
     CUtensorMap tmW_k, tmW_mn, tmZ_k, tmZ_mn;
-    if (!make_tmap_bf16(&tmW_k, Wb + c0 * d, d, vc, d, 64, BN / pz)) return AURORA_ERR_CUDA;
+    if (!make_tmap_bf16(&tmW_k, Wb + c0 * d, d, vc, d, 64, bz / pz)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmW_mn, Wb + c0 * d, d, vc, d, 64, 64)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmZ_k, dzT, M, vc, w.m_pad, 64, BM)) return AURORA_ERR_CUDA;
     if (!make_tmap_bf16(&tmZ_mn, dzT, M, vc, w.m_pad, 64, 64)) return AURORA_ERR_CUDA;
@@ -763,7 +788,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     // A7: recompute Z tiles, dz -> dZ^T chunk (bf16)
     GemmArgs a{};
     a.m_tiles = static_cast<int32_t>(cdiv(M, BM * pz));
-    a.n_tiles = static_cast<int32_t>(cdiv(vc, BN));
+    a.n_tiles = static_cast<int32_t>(cdiv(vc, bz));
     a.splits = 1;
     a.kb_total = static_cast<int32_t>(d / BK);
     a.kb_per_split = a.kb_total;
@@ -780,7 +805,7 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     a.ld_dzT = w.m_pad;
     a.tile_counter = w.counters + 3 * ch;
     prof_begin(PH_BWD_DZ, s);
-    cudaError_t e = launch_umma_gemm(EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s, nullptr, pz);
+    cudaError_t e = launch_umma_gemm(EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s, nullptr, pz, bz);
     prof_end(PH_BWD_DZ, s);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (S) {

@@ -60,9 +60,11 @@ struct GemmArgs {
 // epilogue (bulk stores / reduce-add); nullptr -> LSU store path.
 // pair = 2: 2-CTA clusters with tcgen05.mma.cta_group::2 (M = 256 per pair tile; the
 // caller sets args.m_tiles in 256-row units and builds K-major B maps with a 128-row box).
+// bn: tile width, BN or (pair 1, K-major operands, EPI_FWD_STATS / EPI_BWD_DZ) 224 / 192;
+// the caller sets args.n_tiles = cdiv(N, bn) and builds the B map with a bn-row box.
 cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
                              const GemmArgs& args, cudaStream_t stream, const CUtensorMap* tmC = nullptr,
-                             int pair = 1);
+                             int pair = 1, int bn = BN);
 bool make_tmap_f32_out(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                        uint64_t depth, uint64_t dstride);
 

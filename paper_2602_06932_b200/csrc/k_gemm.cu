@@ -35,14 +35,21 @@ int g_pair_max_clusters = -1;
 //   commits to both CTAs' barriers; each CTA's TMEM holds its 128 rows x 256 columns and
 //   its epilogue releases the leader's TMEM-empty barrier.  Operand traffic per flop
 //   drops by a third and the stage ring grows from 4 x 48 KB to 6 x 32 KB.
-template <int EPI, bool A_MN, bool B_MN, int PAIR>
+//
+// TBN: tile width (vocab columns per tile).  256 by default; 224 / 192 for K-major B with
+// single-CTA tiles, chosen by the host when the narrower tile fills the 148 SMs' waves
+// better (e.g. M = 384 rows x a 32K-column dz chunk: 378 tiles = 2.55 waves at 256 wide,
+// 432 tiles = 2.92 waves at 224).  Accumulators stay at TMEM columns 0 / 256.
+template <int EPI, bool A_MN, bool B_MN, int PAIR, int TBN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
   constexpr int kSt = PAIR == 2 ? 6 : kStages;
-  constexpr int kSB = (BN / PAIR) * BK * 2;  // B bytes per stage in this CTA
+  static_assert(TBN == BN || (PAIR == 1 && !B_MN), "narrow tiles: single-CTA, K-major B only");
+  static_assert(TBN % 32 == 0 && TBN > BN / 2 && TBN <= BN, "tile width");
+  constexpr int kSB = (TBN / PAIR) * BK * 2;  // B bytes per stage in this CTA
   constexpr int kStageBytes = kSmemA + kSB;
-  static_assert(kSt * kStageBytes == kStages * (kSmemA + kSmemB), "stage ring must keep the smem layout");
+  static_assert(kSt * kStageBytes <= kStages * (kSmemA + kSmemB), "stage ring must fit the smem layout");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -134,7 +141,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int kb0 = sp * args.kb_per_split;
         const int kb1 = min(args.kb_total, kb0 + args.kb_per_split);
         const int arow = (PAIR == 2 ? mt * 2 + static_cast<int>(rank) : mt) * BM;  // this CTA's A rows
-        const int brow = nt * BN + static_cast<int>(rank) * (BN / PAIR);          // this CTA's B rows
+        const int brow = nt * TBN + static_cast<int>(rank) * (TBN / PAIR);          // this CTA's B rows
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           if constexpr (PAIR == 1) {
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             load(&tmB, b, kb * BK, brow);
           } else {
 #pragma unroll
-            for (int i = 0; i < BN / PAIR / 64; ++i) load(&tmB, b + i * (BK * 128), brow + i * 64, kb * BK);
+            for (int i = 0; i < TBN / PAIR / 64; ++i) load(&tmB, b + i * (BK * 128), brow + i * 64, kb * BK);
           }
           if (++stage == kSt) { stage = 0; phase ^= 1; }
         }
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && rank == 0) {  // PAIR = 2: only the leader issues (cta_group::2)
-      constexpr uint32_t idesc = umma_idesc_bf16(BM * PAIR, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = umma_idesc_bf16(BM * PAIR, TBN, A_MN, B_MN);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, sslot = 0, sph = 0;
       int u = 0;
       for (bool first = true;; first = false) {
@@ -209,10 +216,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     // 8 warps: warp w may only touch TMEM lanes 32*(w%4).. (its quadrant q); the two
-    // warps of a quadrant split the tile's 256 columns into halves.
+    // warps of a quadrant split the tile's columns into [0, 128) and [128, TBN).
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int cbeg = half * (BN / 2);
+    const int chalf_end = half ? TBN : BN / 2;
     uint32_t epi_chunk = 0;  // running count of bulk-store chunks (slot parity)
     uint32_t acc = 0, acc_phase = 0, sslot = 0, sph = 0;
     int u = 0;
@@ -224,10 +232,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if constexpr (PAIR == 2) mt = mt * 2 + static_cast<int>(rank);  // this CTA's 128-row half
       const int64_t row = static_cast<int64_t>(mt) * BM + q * 32 + lane;
       const bool row_ok = row < args.M;
-      const int64_t col0 = static_cast<int64_t>(nt) * BN;
+      const int64_t col0 = static_cast<int64_t>(nt) * TBN;
       const int64_t rem = args.N - col0;
-      const int ncols = rem < BN ? static_cast<int>(rem) : BN;
-      const int cend = ncols < cbeg + BN / 2 ? ncols : cbeg + BN / 2;  // this warp: [cbeg, cend)
+      const int ncols = rem < TBN ? static_cast<int>(rem) : TBN;
+      const int cend = ncols < chalf_end ? ncols : chalf_end;  // this warp: [cbeg, cend)
 
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -404,11 +412,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 // ------------------------------------------------------------------ host side
 namespace {
-template <int EPI, bool A_MN, bool B_MN, int PAIR>
+template <int EPI, bool A_MN, bool B_MN, int PAIR, int TBN = BN>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& args,
                         cudaStream_t s) {
   static bool attr_set = false;
-  auto kern = k_umma_gemm<EPI, A_MN, B_MN, PAIR>;
+  auto kern = k_umma_gemm<EPI, A_MN, B_MN, PAIR, TBN>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
     if (e != cudaSuccess) return e;
@@ -468,7 +476,19 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
 }
 template <int PAIR>
 cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                     const CUtensorMap& C, const GemmArgs& g, cudaStream_t s) {
+                     const CUtensorMap& C, const GemmArgs& g, cudaStream_t s, int bn) {
+  if constexpr (PAIR == 1) {
+    if (bn != BN && (a_mn || b_mn || (epi != EPI_FWD_STATS && epi != EPI_BWD_DZ))) return cudaErrorInvalidValue;
+    if (bn == 224) {
+      if (epi == EPI_FWD_STATS) return launch_impl<EPI_FWD_STATS, false, false, 1, 224>(tmA, tmB, C, g, s);
+      return launch_impl<EPI_BWD_DZ, false, false, 1, 224>(tmA, tmB, C, g, s);
+    }
+    if (bn == 192) {
+      if (epi == EPI_FWD_STATS) return launch_impl<EPI_FWD_STATS, false, false, 1, 192>(tmA, tmB, C, g, s);
+      return launch_impl<EPI_BWD_DZ, false, false, 1, 192>(tmA, tmB, C, g, s);
+    }
+  }
+  if (bn != BN) return cudaErrorInvalidValue;
   if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_STORE_F32) {
@@ -482,16 +502,16 @@ cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, cons
 }  // namespace
 
 cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
-                             const GemmArgs& args, cudaStream_t s, const CUtensorMap* tmC, int pair) {
+                             const GemmArgs& args, cudaStream_t s, const CUtensorMap* tmC, int pair, int bn) {
   static const CUtensorMap dummy{};
   const CUtensorMap& C = tmC ? *tmC : dummy;
   GemmArgs g = args;
   g.tma_store = (epi == EPI_STORE_F32 && tmC) ? 1 : 0;
   if (pair == 2) {
     g.tile_counter = nullptr;  // pairs use the static per-cluster schedule
-    return dispatch<2>(epi, a_mn, b_mn, tmA, tmB, C, g, s);
+    return dispatch<2>(epi, a_mn, b_mn, tmA, tmB, C, g, s, bn);
   }
-  return dispatch<1>(epi, a_mn, b_mn, tmA, tmB, C, g, s);
+  return dispatch<1>(epi, a_mn, b_mn, tmA, tmB, C, g, s, bn);
 }
 
 // ------------------------------------------------------------------ tensor maps

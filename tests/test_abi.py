@@ -83,3 +83,21 @@ def test_no_cpu_fallback_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_options_validate_host_side(L):
+    """Execution options are host state: valid values round-trip, invalid ones are rejected."""
+    for name, good, bad in [("gemm_pair", (0, 1, 2), (3, -1)), ("bwd_mode", (0, 1), (2,)),
+                            ("bwd_concurrent", (0, 1), (2,)), ("tile_n", (0, 256, 224, 192), (128, 200, 512))]:
+        saved = A.aurora_get_option(name)
+        try:
+            for v in good:
+                A.aurora_set_option(name, v)
+                assert A.aurora_get_option(name) == v
+            for v in bad:
+                with pytest.raises(Exception):
+                    A.aurora_set_option(name, v)
+                assert A.aurora_get_option(name) == good[-1]
+        finally:
+            A.aurora_set_option(name, saved)
+    assert A.aurora_get_option("no_such_option") == -1

@@ -375,6 +375,23 @@ def test_parity_forced_tiling(option, name, pair):
     test_full_parity_small(name)
 
 
+@pytest.mark.parametrize("tile_n", [224, 192])
+@pytest.mark.parametrize("name", ["tiny", "small_tree", "mid"])
+def test_parity_narrow_tiles(option, name, tile_n):
+    """fwd / dz GEMMs with 224- and 192-column vocab tiles (single-CTA tiles)."""
+    option("gemm_pair", 1)
+    option("tile_n", tile_n)
+    test_full_parity_small(name)
+
+
+def test_narrow_tiles_emulated_vp(option):
+    """Ragged vocab shards (tails not multiples of 224 / 192) with narrow tiles."""
+    option("gemm_pair", 1)
+    for t in (224, 192):
+        option("tile_n", t)
+        test_emulated_vocab_parallel_shards((1000, 2049, 4100))
+
+
 @pytest.mark.parametrize("name", ["tiny", "small", "small_tree", "mid"])
 def test_parity_fused_bwd(option, name):
     """The whole backward as one persistent kernel (unified DZ/DH/DW tile queue)."""
