@@ -152,7 +152,7 @@ def run_ours(args):
     draft = torch.from_numpy(tr["draft_tokens"]).to(dev)
     parents = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).to(dev)
     num_nodes = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).to(dev)
-    st = A.SpecTrainStep(R, N, d, V, comm=comm, device=dev)
+    st = A.SpecTrainStep(R, N, d, V, comm=comm, device=dev, k_accept=args.k_accept, k_discard=args.k_discard)
     if sparse and A.aurora_workspace_size(A.OP_VERIFY, M, d, args.target_topk, st.cfg) > st.ws_bytes:
         raise SystemExit("workspace too small for --target-topk")
     dH = torch.empty(M, d, dtype=torch.float32, device=dev)
@@ -228,6 +228,7 @@ def run_ours(args):
         "config": {"workload": cfg.name + (f"+topk{args.target_topk}" if sparse else ""), "R": R, "N": N,
                    "M_rows_per_gpu": M, "d": d, "V": V,
                    "target": f"top-{args.target_topk} (id, logit) pairs per row (F1)" if sparse else "dense bf16 logits",
+                   "k_accept": args.k_accept, "k_discard": args.k_discard,
                    "tree": cfg.tree, "parallelism": f"dp{ws}" if ws > 1 else "single",
                    "l2": "flushed between timed steps (256 MiB write outside the step events)"},
         "gpu_launches": int(n_launch),
@@ -457,6 +458,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--target-topk", type=int, default=0,
                     help="NEXT F1: feed the verifier logits as the transmitted top-K payload (e.g. 1024)")
+    ap.add_argument("--k-accept", type=int, default=1, help="support size on ACCEPT rows (1 = CE; up to 1024 "
+                                                            "with --target-topk: soft distillation)")
+    ap.add_argument("--k-discard", type=int, default=10, help="support size on DISCARD rows (P:520)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -41,7 +41,9 @@ extern "C" {
 
 #define AURORA_ABI_VERSION 1
 #define AURORA_MAX_NODES 32   /* N <= 32: one warp lane per draft node      */
-#define AURORA_MAX_K 16       /* k_accept, k_discard <= 16 on the hot path  */
+#define AURORA_MAX_K 16       /* k_accept, k_discard <= 16 on the dense path */
+#define AURORA_MAX_K_SPARSE 1024  /* k <= 1024 with the sparse top-K ingest (F1) */
+#define AURORA_MAX_KT_SPARSE 16384 /* K_t limit when k > AURORA_MAX_K            */
 
 typedef enum {
   AURORA_OK = 0,
@@ -88,8 +90,9 @@ typedef struct {
 /* Loss configuration (Eq. 3; Table 3). */
 typedef struct {
   int32_t k_accept;       /* support size on ACCEPT rows; default 1 = CE on the verified
-                             token (reading Q5); 1..16                           */
-  int32_t k_discard;      /* support size on DISCARD rows; default 10; 1..16.
+                             token (reading Q5); 1..16 (dense verify), 1..1024
+                             and <= K_t (sparse verify: soft distillation, F1)          */
+  int32_t k_discard;      /* support size on DISCARD rows; default 10; same range.
                              0 (= paper's unfiltered "top-k 0") -> UNSUPPORTED   */
   float lambda_discard;   /* default 1.0; 0 disables the discard term          */
   int32_t normalize;      /* 0: per-term means over GLOBAL counts N_A, N_D (default,
@@ -100,7 +103,8 @@ typedef struct {
 
 /* Caller-allocated outputs of verify; inputs of fwd/bwd.  All (dev). */
 typedef struct {
-  int32_t k_max;          /* (in) row stride of sup_idx/sup_p; >= max(k_accept,k_discard), <= 16 */
+  int32_t k_max;          /* (in) row stride of sup_idx/sup_p; >= max(k_accept,k_discard);
+                             <= 16 for aurora_verify_labels, <= 1024 otherwise           */
   int32_t* target_argmax; /* [M]  y_m, global id; lowest index wins ties  */
   uint8_t* accepted;      /* [R,N] 1 = node on the accepted path                         */
   int32_t* accept_len;    /* [R]  #accepted + 1 (bonus counts)                    */
@@ -149,9 +153,11 @@ typedef struct {
   int64_t V;                     /* global vocabulary size                                 */
 } aurora_trace_topk_t;
 
-/* argmax / top-k_max are taken over the K_t transmitted pairs by (value desc, id asc);
+/* argmax / top-k are taken over the K_t transmitted pairs by (value desc, id asc);
  * status bits: non-finite logit, id outside [0, V) (pair skipped), an id seen twice in the
  * top list (STRUCTURE).  Workspace: aurora_workspace_size(AURORA_OP_VERIFY, M, d, K_t, cfg).
+ * k = max(k_accept, k_discard) <= 16: warp-list scan; 16 < k <= 1024 (soft distillation
+ * over up to the whole payload): CTA-per-row bitonic sort, K_t <= 16384.
  * VP ranks each hold the full payload (no candidate exchange); DP sums the counts. */
 aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* trace, const aurora_loss_cfg_t* cfg,
                                           aurora_labels_t* out, void* ws, size_t ws_bytes,

@@ -203,6 +203,12 @@ VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
   w.top_idx = c.take<int32_t>(M * k_max);
   return w;
 }
+VerifyWs carve_verify_long(Carver& c, int64_t M, int k_top) {  // F1 long supports: top lists only
+  VerifyWs w{};
+  w.top_val = c.take<float>(M * k_top);
+  w.top_idx = c.take<int32_t>(M * k_top);
+  return w;
+}
 struct FwdWs { float *pm, *ps, *pu, *msu, *bp; };
 FwdWs carve_fwd(Carver& c, int64_t M, int64_t V_local) {
   FwdWs w;
@@ -259,19 +265,19 @@ FusedWs carve_fused(Carver& c, int64_t M, int64_t d, int64_t V_local) {
 }
 bool classic_bwd() { return opts().bwd_mode == 0; }
 
-aurora_status_t check_cfg(const aurora_loss_cfg_t* cfg) {
+aurora_status_t check_cfg(const aurora_loss_cfg_t* cfg, int max_k = AURORA_MAX_K) {
   if (!cfg) return AURORA_ERR_INVALID_ARG;
   if (cfg->k_discard == 0) return AURORA_ERR_UNSUPPORTED;  // dense discard KL (NEXT F2)
-  if (cfg->k_accept < 1 || cfg->k_accept > AURORA_MAX_K || cfg->k_discard < 1 || cfg->k_discard > AURORA_MAX_K)
+  if (cfg->k_accept < 1 || cfg->k_accept > max_k || cfg->k_discard < 1 || cfg->k_discard > max_k)
     return AURORA_ERR_INVALID_ARG;
   if (!(cfg->lambda_discard >= 0.f) || !std::isfinite(cfg->lambda_discard)) return AURORA_ERR_INVALID_ARG;
   if (cfg->normalize != 0 && cfg->normalize != 1) return AURORA_ERR_INVALID_ARG;
   if (cfg->discard_scope != 0 && cfg->discard_scope != 1) return AURORA_ERR_INVALID_ARG;
   return AURORA_OK;
 }
-bool labels_ok(const aurora_labels_t* l, bool verify_outputs) {
+bool labels_ok(const aurora_labels_t* l, bool verify_outputs, int max_k = AURORA_MAX_K_SPARSE) {
   if (!l) return false;
-  if (l->k_max < 1 || l->k_max > AURORA_MAX_K) return false;
+  if (l->k_max < 1 || l->k_max > max_k) return false;
   if (!l->sup_idx || !l->sup_p || !l->row_H || !l->row_w || !l->row_class) return false;
   if (verify_outputs && (!l->target_argmax || !l->accepted || !l->accept_len || !l->bonus || !l->counts ||
                          !l->status))
@@ -521,11 +527,12 @@ int aurora_profile_read(const char** names, float* total_ms, int32_t* count, int
 size_t aurora_workspace_size(int op, int64_t M, int64_t d, int64_t V_local, const aurora_loss_cfg_t* cfg) {
   if (M < 1 || V_local < 1 || d < 1 || !cfg || op < 0 || op > 3) return 0;
   const int k_max = std::max(cfg->k_accept, cfg->k_discard);
-  if (k_max < 1 || k_max > AURORA_MAX_K) return 0;
+  if (k_max < 1 || k_max > AURORA_MAX_K_SPARSE) return 0;
   size_t best = 0;
   if (op == AURORA_OP_VERIFY || op == AURORA_OP_ALL) {
     Carver c(nullptr);
-    carve_verify(c, M, V_local, AURORA_MAX_K);
+    if (k_max <= AURORA_MAX_K) carve_verify(c, M, V_local, AURORA_MAX_K);
+    else carve_verify_long(c, M, k_max);
     best = std::max(best, c.off);
   }
   if (op == AURORA_OP_FWD || op == AURORA_OP_ALL) {
@@ -553,7 +560,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   if (t->V < 1 || t->V_local < 1 || t->vocab_offset < 0 || t->vocab_offset + t->V_local > t->V ||
       t->ld_target < t->V_local || t->V > INT32_MAX)
     return AURORA_ERR_INVALID_ARG;
-  if (!labels_ok(out, true)) return AURORA_ERR_INVALID_ARG;
+  if (!labels_ok(out, true, AURORA_MAX_K)) return AURORA_ERR_INVALID_ARG;
   const int k_max = out->k_max;
   if (k_max < std::max(cfg->k_accept, cfg->k_discard)) return AURORA_ERR_INVALID_ARG;
   if (std::max(cfg->k_accept, cfg->k_discard) > t->V) return AURORA_ERR_INVALID_ARG;
@@ -627,20 +634,23 @@ aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const au
                                           aurora_labels_t* out, void* ws, size_t ws_bytes, aurora_comm_t comm,
                                           void* stream) {
   if (!t || !out) return AURORA_ERR_INVALID_ARG;
-  aurora_status_t st = check_cfg(cfg);
+  aurora_status_t st = check_cfg(cfg, AURORA_MAX_K_SPARSE);
   if (st != AURORA_OK) return st;
   if (t->R < 1 || t->N < 1 || t->N > AURORA_MAX_NODES || !t->draft_tokens || !t->target_ids || !t->target_vals)
     return AURORA_ERR_INVALID_ARG;
   if (t->V < 1 || t->V > INT32_MAX || t->K_t < 1) return AURORA_ERR_INVALID_ARG;
   if (!labels_ok(out, true)) return AURORA_ERR_INVALID_ARG;
   const int k_max = out->k_max;
-  if (k_max < std::max(cfg->k_accept, cfg->k_discard) || std::max(cfg->k_accept, cfg->k_discard) > t->K_t)
-    return AURORA_ERR_INVALID_ARG;
+  const int kk = std::max(cfg->k_accept, cfg->k_discard);
+  if (k_max < kk || kk > t->K_t) return AURORA_ERR_INVALID_ARG;
+  const bool long_path = kk > AURORA_MAX_K;
+  if (long_path && t->K_t > AURORA_MAX_KT_SPARSE) return AURORA_ERR_UNSUPPORTED;
+  if (!long_path && k_max > AURORA_MAX_K) return AURORA_ERR_INVALID_ARG;  // warp lists hold <= 16
   const int64_t M = static_cast<int64_t>(t->R) * (t->N + 1);
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->K_t, cfg)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Carver c(ws);
-  VerifyWs w = carve_verify(c, M, t->K_t, k_max);
+  VerifyWs w = long_path ? carve_verify_long(c, M, kk) : carve_verify(c, M, t->K_t, k_max);
   VerifyLaunch p{};
   p.V = t->V;
   p.V_local = t->V;
@@ -648,6 +658,7 @@ aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const au
   p.R = t->R;
   p.N = t->N;
   p.k_max = k_max;
+  p.k_top = kk;
   p.nseg = 1;
   p.draft = t->draft_tokens;
   p.parents = t->parents;
@@ -658,10 +669,11 @@ aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const au
   p.cfg = *cfg;
   if (cudaMemsetAsync(out->counts, 0, 2 * sizeof(int32_t), s) != cudaSuccess) return AURORA_ERR_CUDA;
   if (cudaMemsetAsync(out->status, 0, sizeof(uint32_t), s) != cudaSuccess) return AURORA_ERR_CUDA;
+  const uint16_t* vals = static_cast<const uint16_t*>(t->target_vals);
   prof_begin(PH_SCAN, s);
-  if (launch_target_scan_topk(p, t->target_ids, static_cast<const uint16_t*>(t->target_vals), t->K_t, s) !=
-      cudaSuccess)
-    return AURORA_ERR_CUDA;
+  cudaError_t e = long_path ? launch_sort_pairs(p, t->target_ids, vals, t->K_t, s)
+                            : launch_target_scan_topk(p, t->target_ids, vals, t->K_t, s);
+  if (e != cudaSuccess) return AURORA_ERR_CUDA;
   prof_end(PH_SCAN, s);
   prof_begin(PH_VERIFY, s);
   if (launch_verify(p, s) != cudaSuccess) return AURORA_ERR_CUDA;
@@ -670,7 +682,7 @@ aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const au
     if (A.AllReduce(out->counts, out->counts, 2, nccl::ncclInt32, nccl::ncclSum, comm->dp, s) != 0)
       return AURORA_ERR_NCCL;
   }
-  if (launch_finalize(p, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  if ((long_path ? launch_finalize_long(p, s) : launch_finalize(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   prof_end(PH_VERIFY, s);
   return AURORA_OK;
 }

@@ -68,15 +68,17 @@ struct SupCursor {
       return;
     }
   }
-  // position on the first entry with local column >= col0
+  // position on the first entry with local column >= col0: lower_bound over the
+  // index-sorted support (INT32_MAX padding sorts last); O(log k) for supports up to 1024
   __device__ __forceinline__ void seek(int64_t col0) {
-    pos = 0;
-    while (pos < k) {
-      const int32_t g = idx[pos];
-      if (g == INT32_MAX) { pos = k; break; }
-      if (static_cast<int64_t>(g) - gid0 >= col0) break;
-      ++pos;
+    const int64_t target = gid0 + col0;
+    int lo = 0, hi = k;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (static_cast<int64_t>(idx[mid]) < target) lo = mid + 1;
+      else hi = mid;
     }
+    pos = lo;
     load();
   }
   __device__ __forceinline__ void advance() {

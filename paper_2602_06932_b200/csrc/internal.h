@@ -53,6 +53,7 @@ struct GemmArgs {
   int32_t* tile_counter;  // nullable: dynamic tile scheduler counter (zero before first use)
   int32_t n_fastest;      // tile raster: 0 = m-fastest (B streams once), 1 = n-fastest (A streams once)
   int32_t tma_store;      // set by launch_umma_gemm when an output tensor map is given
+  int32_t dbg_epi;        // diagnostics only (AURORA_DBG_EPI): 1 skip tcgen05.ld, 2 skip fence + bulk store
 };
 
 // Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.
@@ -116,8 +117,9 @@ struct VerifyLaunch {
   const int32_t* num_nodes;
   float* cand_val;      // [M, nseg, k_max]
   int32_t* cand_idx;
-  float* top_val;       // [M, k_max] merged (value order)
+  float* top_val;       // [M, k_max] merged (value order); long path: [M, k_top]
   int32_t* top_idx;
+  int32_t k_top;        // long-support path (k > AURORA_MAX_K): top-list length per row
   aurora_labels_t lab;
   aurora_loss_cfg_t cfg;
 };
@@ -128,6 +130,10 @@ cudaError_t launch_target_scan_topk(const VerifyLaunch& p, const int32_t* tk_idx
                                     cudaStream_t s);
 cudaError_t launch_verify(const VerifyLaunch& p, cudaStream_t s);
 cudaError_t launch_finalize(const VerifyLaunch& p, cudaStream_t s);
+// Long supports (F1 soft distillation, k up to AURORA_MAX_K_SPARSE): CTA per row.
+cudaError_t launch_sort_pairs(const VerifyLaunch& p, const int32_t* tk_idx, const uint16_t* tk_val, int32_t K_t,
+                              cudaStream_t s);
+cudaError_t launch_finalize_long(const VerifyLaunch& p, cudaStream_t s);
 
 // ---------------------------------------------------------------- row kernels
 cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, int64_t M, int n_tiles,

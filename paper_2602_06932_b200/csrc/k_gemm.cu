@@ -40,21 +40,40 @@ int g_pair_max_clusters = -1;
 // single-CTA tiles, chosen by the host when the narrower tile fills the 148 SMs' waves
 // better (e.g. M = 384 rows x a 32K-column dz chunk: 378 tiles = 2.55 waves at 256 wide,
 // 432 tiles = 2.92 waves at 224).  Accumulators stay at TMEM columns 0 / 256.
+// Shared-memory plan of one instantiation.  A store-bound fp32 epilogue is limited by
+// the bytes its bulk stores keep in flight (measured: 2 x 2 KB slots per warp cap a CTA
+// near 30 GB/s), so the CTA-pair STORE_F32 kernel trades two of its six ring stages (K per
+// tile is small where it is store-bound) for 6 staging slots per epilogue warp.
+template <int EPI, bool A_MN, int PAIR, int TBN>
+struct SmemPlan {
+  static constexpr int kSB = (TBN / PAIR) * BK * 2;  // B bytes per stage in this CTA
+  static constexpr int kStageBytes = kSmemA + kSB;
+  static constexpr bool kStore = EPI == EPI_STORE_F32;
+  static constexpr int kSt = PAIR == 2 ? (kStore ? 4 : 6) : kStages;
+  static constexpr int kRing = kSt * kStageBytes;
+  static constexpr int kSlots = kStore ? (PAIR == 2 ? 6 : 2) : 0;  // 2 KB bulk-store slots per warp
+  static constexpr int kStaging = kEpiWarps * kSlots * 2048;
+  static constexpr int kBytes = kRing + 1024 /*barriers*/ + 1024 /*base alignment*/ + kStaging;
+  static_assert(kBytes <= 232448, "dynamic smem per CTA");
+  static_assert(kSt * kStageBytes <= kStages * (kSmemA + kSmemB), "ring");
+  static_assert(!kStore || kSlots * 2048 >= 32 * kStgLd * 4, "LSU staging fits a warp's slots");
+};
+
 template <int EPI, bool A_MN, bool B_MN, int PAIR, int TBN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
-  constexpr int kSt = PAIR == 2 ? 6 : kStages;
+  using Plan = SmemPlan<EPI, A_MN, PAIR, TBN>;
   static_assert(TBN == BN || (PAIR == 1 && !B_MN), "narrow tiles: single-CTA, K-major B only");
   static_assert(TBN % 32 == 0 && TBN > BN / 2 && TBN <= BN, "tile width");
-  constexpr int kSB = (TBN / PAIR) * BK * 2;  // B bytes per stage in this CTA
-  constexpr int kStageBytes = kSmemA + kSB;
-  static_assert(kSt * kStageBytes <= kStages * (kSmemA + kSmemB), "stage ring must fit the smem layout");
+  constexpr int kSt = Plan::kSt;
+  constexpr int kSB = Plan::kSB;
+  constexpr int kStageBytes = Plan::kStageBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kSt * kSmemA;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sB + kSt * kSB);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Plan::kRing);
   uint64_t* empty_bar = full_bar + kSt;
   uint64_t* tfull_bar = empty_bar + kSt;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -62,8 +81,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* sempty_bar = sfull_bar + kSchedDepth;
   int32_t* s_sched = reinterpret_cast<int32_t*>(sempty_bar + kSchedDepth);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_sched + kSchedDepth);
-  // epilogue staging, 1024-B aligned (the 64B-swizzle pattern repeats every 512 B)
-  float* stage_f32 = reinterpret_cast<float*>(smem + kStages * (kSmemA + kSmemB) + 1024);
+  // epilogue staging, 1024-B aligned (the 64B / 128B swizzle patterns repeat every 512 / 1024 B)
+  float* stage_f32 = reinterpret_cast<float*>(smem + Plan::kRing + 1024);
   static_assert((2 * kSt + 4 + 2 * kSchedDepth) * 8 + 4 * kSchedDepth + 4 <= 1024, "barrier area");
 
   const int warp = threadIdx.x >> 5;
@@ -316,27 +335,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             args.p_u[o] = usum;
           }
         }
-      } else if (args.tma_store) {  // EPI_STORE_F32 via TMA bulk stores
+      } else if (args.tma_store && !((args.dbg_epi & 4) && half == 1)) {  // EPI_STORE_F32, TMA bulk stores
         // thread = row; each 32x16 fp32 block goes to a 64B-swizzled smem slot (rows of
         // 64 B, 16 B chunk c of row r at chunk c ^ ((r >> 1) & 3): conflict-free 16 B
         // stores), then one lane issues a bulk tensor store (or reduce-add when
-        // accumulating).  Two slots per warp; a slot is rewritten only after the bulk
-        // engine has finished reading it (wait_group.read 1).
-        uint8_t* slots = reinterpret_cast<uint8_t*>(stage_f32) + (warp - 2) * (2 * 2048);
+        // accumulating).  kSlots slots per warp in a ring; a slot is rewritten only after
+        // the bulk engine has finished reading it (wait_group.read kSlots-1).
+        constexpr int kSlots = Plan::kSlots > 0 ? Plan::kSlots : 1;
+        uint8_t* slots = reinterpret_cast<uint8_t*>(stage_f32) + (warp - 2) * (kSlots * 2048);
         const int row0 = mt * BM + q * 32;
+        const int dbg = args.dbg_epi;
         for (int cb = cbeg; cb < cend; cb += 16) {
           uint32_t r[16];
-          tmem_ld_32x32b_x16(taddr + cb, r);
-          uint8_t* slot = slots + (epi_chunk & 1) * 2048;
-          if (lane == 0) bulk_wait_read<1>();
+          if (!(dbg & 1)) tmem_ld_32x32b_x16(taddr + cb, r);
+          else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = static_cast<uint32_t>(cb + j);
+          }
+          uint8_t* slot = slots + (epi_chunk % kSlots) * 2048;
+          if (lane == 0) bulk_wait_read<kSlots - 1>();
           __syncwarp();
-          tmem_ld_wait();
+          if (!(dbg & 1)) tmem_ld_wait();
           const uint32_t sbase = smem_u32(slot) + lane * 64;
           const uint32_t sw = (lane >> 1) & 3;
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             sts128(sbase + ((c ^ sw) << 4), __uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
                    __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
+          if (dbg & 2) { __syncwarp(); ++epi_chunk; continue; }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -350,7 +376,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       } else {  // EPI_STORE_F32 through the LSU (fallback: unaligned output strides)
         // TMEM gives thread = row; transpose each 32x16 fp32 block through this warp's
         // smem slice so a store instruction writes eight full 64 B row segments.
-        const uint32_t stg = smem_u32(stage_f32 + (warp - 2) * (32 * kStgLd));  // explicit .shared
+        const uint32_t stg = smem_u32(reinterpret_cast<uint8_t*>(stage_f32) + (warp - 2) * (Plan::kSlots * 2048));
         float* obase = args.out + static_cast<int64_t>(sp) * args.split_stride;
         const bool vec_ok = ((args.ld_out & 3) == 0) && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0);
         const int64_t row_base = static_cast<int64_t>(mt) * BM + q * 32;
@@ -417,8 +443,9 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
                         cudaStream_t s) {
   static bool attr_set = false;
   auto kern = k_umma_gemm<EPI, A_MN, B_MN, PAIR, TBN>;
+  constexpr int kSmem = SmemPlan<EPI, A_MN, PAIR, TBN>::kBytes;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -433,7 +460,7 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = kGemmSmem;
+    cfg.dynamicSmemBytes = kSmem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -446,14 +473,14 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
     if (e != cudaSuccess) return e;
   } else if constexpr (PAIR == 1) {
     const int grid = units < kNumSMs ? units : kNumSMs;
-    kern<<<grid, kGemmThreads, kGemmSmem, s>>>(tmA, tmB, tmC, args);
+    kern<<<grid, kGemmThreads, kSmem, s>>>(tmA, tmB, tmC, args);
   } else {
     const int pairs = units < kNumSMs / 2 ? units : kNumSMs / 2;
     static int max_clusters = -1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = kGemmSmem;
+    cfg.dynamicSmemBytes = kSmem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -506,7 +533,16 @@ cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& t
   static const CUtensorMap dummy{};
   const CUtensorMap& C = tmC ? *tmC : dummy;
   GemmArgs g = args;
-  g.tma_store = (epi == EPI_STORE_F32 && tmC) ? 1 : 0;
+  static const bool no_tma_store = [] {  // diagnostic: force the LSU store epilogue
+    const char* e = getenv("AURORA_DBG_LSU_STORE");
+    return e && e[0] == '1';
+  }();
+  g.tma_store = (epi == EPI_STORE_F32 && tmC && !no_tma_store) ? 1 : 0;
+  static const int dbg_epi = [] {
+    const char* e = getenv("AURORA_DBG_EPI");
+    return e ? atoi(e) : 0;
+  }();
+  g.dbg_epi = dbg_epi;
   if (pair == 2) {
     g.tile_counter = nullptr;  // pairs use the static per-cluster schedule
     return dispatch<2>(epi, a_mn, b_mn, tmA, tmB, C, g, s, bn);
@@ -558,7 +594,8 @@ bool make_tmap_f32_out(CUtensorMap* map, const void* base, uint64_t inner, uint6
   cuuint32_t box[3] = {16, 32, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -485,6 +485,152 @@ __global__ void __launch_bounds__(256) k_finalize(VerifyLaunch p) {
   p.lab.row_w[m] = w;
 }
 
+// --------------------------------------------------------------------------- F1 long supports
+// Soft distillation over the transmitted top-K (k up to AURORA_MAX_K_SPARSE):
+// the support of a row can hold every transmitted pair, too long for a warp list.  CTA
+// per row: a block-wide bitonic sort of 64-bit keys in shared memory.
+namespace {
+// monotone float -> uint32 (numeric order, -0 == +0); finite inputs only
+__device__ __forceinline__ uint32_t f2key(float v) {
+  const uint32_t u = __float_as_uint(v == 0.f ? 0.f : v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+__device__ __forceinline__ int pow2_ceil(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+// ascending bitonic sort of n (power of two) keys in smem; all threads of the block call it
+__device__ void block_bitonic_sort(uint64_t* a, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+        const int lo = 2 * stride * (t / stride) + (t % stride);
+        const int hi = lo + stride;
+        const uint64_t x = a[lo], y = a[hi];
+        if ((x > y) == ((lo & size) == 0)) { a[lo] = y; a[hi] = x; }
+      }
+    }
+  }
+  __syncthreads();
+}
+// deterministic block sum (fixed strided partials, fixed shuffle tree, warps in order)
+__device__ float block_sum(float v, float* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[i];
+  return t;
+}
+}  // namespace
+
+// A2' (long): sort the K_t pairs of a row by (value desc, id asc) -> top list [k_top],
+// argmax; status bits as k_target_scan_topk (duplicate ids among the top k_top).
+__global__ void __launch_bounds__(256) k_sort_pairs(VerifyLaunch p, const int32_t* __restrict__ tk_idx,
+                                                    const uint16_t* __restrict__ tk_val, int32_t K_t) {
+  extern __shared__ uint64_t keys[];
+  __shared__ uint32_t s_err;
+  const int64_t row = blockIdx.x;
+  const int n = pow2_ceil(K_t);
+  const int kt = p.k_top;
+  if (threadIdx.x == 0) s_err = 0;
+  uint32_t err = 0;
+  const int64_t o = row * K_t;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    uint64_t key = ~0ull;
+    if (j < K_t) {
+      const uint32_t b = tk_val[o + j];
+      const int32_t id = tk_idx[o + j];
+      if ((b & 0x7FFFu) >= 0x7F80u) err |= AURORA_STATUS_NONFINITE;
+      else if (id < 0 || static_cast<int64_t>(id) >= p.V) err |= AURORA_STATUS_RANGE;
+      else key = (static_cast<uint64_t>(~f2key(__uint_as_float(b << 16))) << 32) | static_cast<uint32_t>(id);
+    }
+    keys[j] = key;
+  }
+  block_bitonic_sort(keys, n);
+  for (int j = threadIdx.x; j < kt; j += blockDim.x) {
+    const uint64_t key = keys[j];
+    const bool valid = key != ~0ull;
+    p.top_val[row * kt + j] = valid ? key2f(~static_cast<uint32_t>(key >> 32)) : -INFINITY;
+    p.top_idx[row * kt + j] = valid ? static_cast<int32_t>(static_cast<uint32_t>(key)) : INT32_MAX;
+  }
+  if (threadIdx.x == 0)
+    p.lab.target_argmax[row] = keys[0] != ~0ull ? static_cast<int32_t>(static_cast<uint32_t>(keys[0])) : INT32_MAX;
+  // duplicate ids among the top kt: sort their ids, compare neighbours
+  const int n2 = pow2_ceil(kt);
+  __syncthreads();
+  for (int j = threadIdx.x; j < n2; j += blockDim.x) {
+    const uint64_t key = keys[j];
+    keys[j] = (j < kt && key != ~0ull) ? static_cast<uint64_t>(static_cast<uint32_t>(key)) : ~0ull;
+  }
+  block_bitonic_sort(keys, n2);
+  for (int j = threadIdx.x; j + 1 < kt; j += blockDim.x)
+    if (keys[j] != ~0ull && keys[j] == keys[j + 1]) err |= AURORA_STATUS_STRUCTURE;
+  if (err) atomicOr(&s_err, err);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_err) atomicOr(p.lab.status, s_err);
+}
+
+// A4 (long): support = first k entries of the row's value-sorted top list, p~ =
+// softmax of their logits (Eq. 3 target renormalised on S), H~ = sum p~ log p~, sorted by
+// global id for the GEMM epilogues' merge-join.
+__global__ void __launch_bounds__(256) k_finalize_long(VerifyLaunch p) {
+  extern __shared__ uint64_t keys[];
+  __shared__ float red[8];
+  const int64_t m = blockIdx.x;
+  const int km = p.k_max, kt = p.k_top;
+  const uint8_t cls = p.lab.row_class[m];
+  const int na = p.lab.counts[0], nd = p.lab.counts[1];
+  int k = 0;
+  float w = 0.f;
+  if (cls == AURORA_ROW_ACCEPT) {
+    k = p.cfg.k_accept;
+    w = p.cfg.normalize ? 1.f / static_cast<float>(na + nd) : 1.f / static_cast<float>(na);
+  } else if (cls == AURORA_ROW_DISCARD) {
+    k = p.cfg.k_discard;
+    w = p.cfg.normalize ? p.cfg.lambda_discard / static_cast<float>(na + nd)
+                        : (nd > 0 ? p.cfg.lambda_discard / static_cast<float>(nd) : 0.f);
+  }
+  const float* tv = p.top_val + m * kt;
+  const int32_t* ti = p.top_idx + m * kt;
+  const float t0 = k > 0 ? tv[0] : 0.f;
+  float e = 0.f;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) e += expf(tv[j] - t0);
+  const float lz = logf(block_sum(e, red));
+  const int n2 = pow2_ceil(k);
+  float h = 0.f;
+  for (int j = threadIdx.x; j < n2; j += blockDim.x) {
+    uint64_t key = ~0ull;
+    if (j < k) {
+      const float lp = tv[j] - t0 - lz;
+      const float pj = expf(lp);
+      h += pj * lp;
+      key = (static_cast<uint64_t>(static_cast<uint32_t>(ti[j])) << 32) | __float_as_uint(pj);
+    }
+    keys[j] = key;
+  }
+  float H = block_sum(h, red);
+  if (k <= 1) H = 0.f;
+  block_bitonic_sort(keys, n2);
+  for (int j = threadIdx.x; j < km; j += blockDim.x) {
+    const bool in = j < k;
+    const uint64_t key = in ? keys[j] : 0ull;
+    p.lab.sup_idx[m * km + j] = in ? static_cast<int32_t>(key >> 32) : INT32_MAX;
+    p.lab.sup_p[m * km + j] = in ? __uint_as_float(static_cast<uint32_t>(key)) : 0.f;
+  }
+  if (threadIdx.x == 0) {
+    p.lab.row_H[m] = H;
+    p.lab.row_w[m] = w;
+  }
+}
+
 // --------------------------------------------------------------------------- launchers
 cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s) {
   k_target_scan<<<static_cast<unsigned>(p.M) * p.nseg, 256, 0, s>>>(p);
@@ -500,6 +646,27 @@ cudaError_t launch_topk_merge(const VerifyLaunch& p, const float* in_val, const 
 cudaError_t launch_target_scan_topk(const VerifyLaunch& p, const int32_t* tk_idx, const uint16_t* tk_val, int32_t K_t,
                                     cudaStream_t s) {
   k_target_scan_topk<<<(p.M + 7) / 8, 256, 0, s>>>(p, tk_idx, tk_val, K_t);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_sort_pairs(const VerifyLaunch& p, const int32_t* tk_idx, const uint16_t* tk_val, int32_t K_t,
+                              cudaStream_t s) {
+  int n = 1;
+  while (n < K_t) n <<= 1;
+  const size_t smem = static_cast<size_t>(n) * sizeof(uint64_t);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_sort_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  k_sort_pairs<<<p.M, 256, smem, s>>>(p, tk_idx, tk_val, K_t);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_finalize_long(const VerifyLaunch& p, cudaStream_t s) {
+  int n = 1;
+  while (n < p.k_top) n <<= 1;
+  k_finalize_long<<<p.M, 256, static_cast<size_t>(n) * sizeof(uint64_t), s>>>(p);
   count_launch();
   return cudaGetLastError();
 }

@@ -64,7 +64,7 @@ def _rfro(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def _check_labels(st, ref, tr, k_accept=1, k_discard=10):
+def _check_labels(st, ref, tr, k_accept=1, k_discard=10, h_rtol=0.0):
     assert int(st.status.item()) == 0
     np.testing.assert_array_equal(st.target_argmax.cpu().numpy(), ref["argmax"])
     np.testing.assert_array_equal(st.accepted.cpu().numpy(), ref["accepted"])
@@ -83,7 +83,7 @@ def _check_labels(st, ref, tr, k_accept=1, k_discard=10):
         assert (sup[m, k:] == np.iinfo(np.int32).max).all()
         np.testing.assert_allclose(sp[m, :k], tg["sup_p"][m], rtol=2e-6, atol=1e-7)
         assert abs(w[m] - tg["w"][m]) <= 1e-6 * abs(tg["w"][m]) + 1e-12
-        assert abs(Hh[m] - tg["H"][m]) <= 1e-5
+        assert abs(Hh[m] - tg["H"][m]) <= 1e-5 + h_rtol * abs(tg["H"][m])
 
 
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
@@ -478,3 +478,47 @@ def test_topk_ingest_status_bits():
     st.verify_topk(g["draft"], ids, v2, g["parents"], g["num_nodes"])
     torch.cuda.synchronize()
     assert int(st.status.item()) & A.STATUS_NONFINITE
+
+
+@pytest.mark.parametrize("name,K_t,ka,kd", [("tiny", 64, 64, 64), ("small", 256, 200, 17), ("small_tree", 100, 32, 100),
+                                           ("mid", 1024, 1024, 1024)])
+def test_topk_long_support_parity(name, K_t, ka, kd):
+    """F1 soft distillation: supports of up to 1024 transmitted pairs per row (CTA-per-row
+    bitonic sort + long finalize; binary-search seek in the GEMM epilogues).  H~ sums
+    up to 1024 fp32 terms, hence a relative allowance on it."""
+    tr = tracegen.gen_trace_topk(name, K_t=K_t)
+    ref = oracle.step_topk(tr, k_accept=ka, k_discard=kd)
+    st, dH, dW = _run_gpu_topk(tr, k_accept=ka, k_discard=kd)
+    _check_labels(st, ref, tr, h_rtol=2e-6)
+    loss = float(st.loss.item())
+    assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"])
+    assert _rfro(dW.cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert _rfro(dH.cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+def test_topk_long_support_status_and_limits():
+    tr = tracegen.gen_trace_topk("small", K_t=64)
+    c = tr["cfg"]
+    g = _to_gpu_base(tr)
+    ids = torch.from_numpy(tr["Tk_idx"]).cuda()
+    vals = torch.from_numpy(np.ascontiguousarray(tr["Tk_bits"]).view(np.int16)).view(torch.bfloat16).cuda()
+    st = A.SpecTrainStep(c.R, c.N, c.d, c.V, k_accept=40, k_discard=40)
+    dup = ids.clone()
+    dup[3, :2] = dup[3, 0]             # the same id twice among the row's pairs, both in the top
+    vd = vals.clone()
+    vd[3, :2] = 60.0
+    st.verify_topk(g["draft"], dup, vd, g["parents"], g["num_nodes"])
+    torch.cuda.synchronize()
+    assert int(st.status.item()) & A.STATUS_STRUCTURE
+    bad = ids.clone()
+    bad[2, 5] = -1
+    st.verify_topk(g["draft"], bad, vals, g["parents"], g["num_nodes"])
+    torch.cuda.synchronize()
+    assert int(st.status.item()) & A.STATUS_RANGE
+    with pytest.raises(Exception):     # k above the transmitted K_t
+        A.SpecTrainStep(c.R, c.N, c.d, c.V, k_accept=65).verify_topk(g["draft"], ids, vals, g["parents"],
+                                                                      g["num_nodes"])
+    with pytest.raises(Exception):     # dense verify keeps k <= 16
+        big = A.SpecTrainStep(c.R, c.N, c.d, c.V, k_accept=17)
+        T = torch.zeros(c.M, c.V, dtype=torch.bfloat16, device="cuda")
+        big.verify(g["draft"], T, g["parents"], g["num_nodes"])

@@ -339,6 +339,30 @@ def test_loss_k_equals_V_matches_torch_kl_div():
     assert abs(fw["loss"] - ref) <= 1e-10 * abs(ref)
 
 
+def test_soft_distillation_full_payload_matches_torch_kl_div():
+    """F1 soft distillation through the sparse path: a payload holding EVERY column of
+    each row (shuffled) with k = K_t = V must give, per row, the full
+    F.kl_div(log_softmax(Z), log_softmax(T)) — the paper's dense target distribution."""
+    cfg = tracegen.TraceConfig("kl_sparse", d=16, V=64, R=4, N=3, seed=91, alpha=(0.6,))
+    tr = tracegen.gen_trace(cfg)
+    rng = np.random.default_rng(5)
+    perm = np.stack([rng.permutation(cfg.V) for _ in range(tr["M"])]).astype(np.int32)
+    tr["Tk_idx"] = perm
+    tr["Tk_bits"] = np.take_along_axis(tr["T_bits"], perm, 1)
+    out = oracle.step_topk(tr, k_accept=cfg.V, k_discard=cfg.V, want_grads=False)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    T = oracle.bf16_bits_to_f64(tr["T_bits"])
+    Z = torch.from_numpy(H64 @ W64.T)
+    kl = F.kl_div(F.log_softmax(Z, 1), F.log_softmax(torch.from_numpy(T), 1), log_target=True,
+                  reduction="none").sum(1).numpy()
+    cls = out["row_class"]
+    valid = cls != PAD
+    np.testing.assert_allclose(np.asarray(out["row_loss"])[valid], kl[valid], rtol=1e-10, atol=1e-12)
+    # the argmax from the shuffled payload is the dense row's first-occurrence argmax
+    np.testing.assert_array_equal(out["argmax"], np.argmax(T, 1))
+
+
 def test_spec_loss_examples(golden_dir):
     cases = json.load(open(os.path.join(golden_dir, "loss_examples.json")))["cases"]
     for c in cases:

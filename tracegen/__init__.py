@@ -72,6 +72,9 @@ CONFIGS = {
     "minimax": TraceConfig("minimax", d=3072, V=200064, R=512, N=8, seed=1004, alpha=(0.65,)),
     # configs[4]: tree drafts, beam 4 x depth 6 = 24 nodes, Qwen3 vocab
     "tree": TraceConfig("tree", d=4096, V=151936, R=1024, N=24, seed=1005, tree=True, beam=4, alpha=(0.7,)),
+    # NEXT F1 shipping format: the Llama-3 draft's 32K draft vocabulary ("32K vs
+    # 128K for Llama3"); used with gen_trace_topk (top-1024 pairs over the draft vocab)
+    "llama_d32k": TraceConfig("llama_d32k", d=4096, V=32000, R=64, N=5, seed=1006, alpha=(0.79,)),
     # parity-only shapes: several tiles plus ragged vocab/row tails, oracle finishes in seconds
     "small": TraceConfig("small", d=256, V=5003, R=13, N=5, seed=2001, alpha=(0.7,), ragged=True),
     "small_tree": TraceConfig("small_tree", d=192, V=3001, R=9, N=12, seed=2002, tree=True, beam=3, alpha=(0.7,)),
