@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define AURORA_ABI_VERSION 1
+#define AURORA_ABI_VERSION 2
 #define AURORA_MAX_NODES 32   /* N <= 32: one warp lane per draft node      */
 #define AURORA_MAX_K 16       /* k_accept, k_discard <= 16 on the dense path */
 #define AURORA_MAX_K_SPARSE 1024  /* k <= 1024 with the sparse top-K ingest (F1) */
@@ -93,12 +93,22 @@ typedef struct {
                              token (reading Q5); 1..16 (dense verify), 1..1024
                              and <= K_t (sparse verify: soft distillation, F1)          */
   int32_t k_discard;      /* support size on DISCARD rows; default 10; same range.
-                             0 (= paper's unfiltered "top-k 0") -> UNSUPPORTED   */
+                             0 = the paper's unfiltered "top-k 0": dense
+                             KL(p_target || q) over the whole vocabulary (F2; dense
+                             verify only, single vocab shard)                           */
   float lambda_discard;   /* default 1.0; 0 disables the discard term          */
   int32_t normalize;      /* 0: per-term means over GLOBAL counts N_A, N_D (default,
                              S:378, reading Q7); 1: mean over N_A + N_D rows            */
   int32_t discard_scope;  /* 0: all rejected nodes (default); 1: only the first
                              rejected node on each branch (others become PAD)           */
+  int32_t accept_loss;    /* ACCEPT-row objective (§5.1; NEXT F2):
+                             0 = FKL KL(p~ || q) on the top-k_accept support (default);
+                             1 = RKL KL(q || p_target) over the whole vocabulary,
+                             gradient q*((ln q - ln p) - KL); dense verify only,
+                             single vocab shard                                          */
+  float ntp_beta;         /* >= 0: auxiliary NTP cross-entropy -ln q_y on ACCEPT rows,
+                             y = verified token, weight beta x the row weight ("RKL +
+                             NTP"); requires accept_loss = 1           */
 } aurora_loss_cfg_t;
 
 /* Caller-allocated outputs of verify; inputs of fwd/bwd.  All (dev). */
@@ -117,6 +127,16 @@ typedef struct {
   float* row_w;           /* [M]  loss weight: 1/N_A, lambda/N_D or 0                     */
   int32_t* counts;        /* [2]  N_A, N_D (global over DP ranks)                        */
   uint32_t* status;       /* [1]  device status word, AURORA_STATUS_* bits                */
+  /* NEXT F2 (accept_loss = 1 or k_discard = 0; otherwise may be NULL / 0):            */
+  float* row_lse_t;          /* [M] written by verify: log sum_j exp(T_mj), full row      */
+  float* row_aux;            /* [M] written by fwd, read by bwd: E_q[z - t] on RKL rows   */
+  const void* target_logits; /* (in) the bf16 T given to verify ([M, ld_target], this
+                                rank's vocab slice); fwd and bwd read its tiles again, so it
+                                must stay valid until the bwd call has run                 */
+  int64_t ld_target;         /* row stride of target_logits in elements                     */
+  int32_t objective;         /* written by verify: bit 0 RKL ACCEPT rows, bit 1 dense-KL
+                                DISCARD rows (0 = Eq. 3 everywhere); read by fwd / bwd      */
+  float ntp_beta;            /* written by verify: cfg->ntp_beta                             */
 } aurora_labels_t;
 
 /* Workspace sizing.  op: 0 = verify, 1 = fwd, 2 = bwd, 3 = max over all three.

@@ -25,6 +25,12 @@ step by step in the paper's order (PAPER.md = P, SPEC.md = S, line numbers):
                    (Eq. 3; full-vocab log-softmax per north_star).
   O5 loss_bwd      dL/dz = w (q - p~) (gradient of KL(p~||q) wrt logits, S:321);
                    dW = dZ^T H, dH = dZ W (fp32 gradients; here fp64).
+  O6 step_variants (NEXT F2, the objectives of §5.1): accepted rows with
+                   reverse KL(q || p_target) (gradient q*((ln q - ln p) - KL))
+                   plus beta * NTP cross-entropy on the verified token,
+                   discard rows with the unfiltered dense KL(p_target || q) ("top-k =
+                   0").  Written directly from those definitions on
+                   full-vocabulary rows (no decomposition shared with the kernels).
 
 Readings where the paper is silent/ambiguous are listed in DESIGN.md
 ("Readings Q1-Q15"); each function names the ones it relies on.
@@ -317,4 +323,85 @@ def step_topk(trace: dict, k_accept: int = 1, k_discard: int = 10, lambda_discar
     out = dict(argmax=amax, topk=topk, **lab, targets=tg, lse=fw["lse"], row_loss=fw["row_loss"], loss=fw["loss"])
     if want_grads:
         out.update(loss_bwd(H64, trace["W_bits"], tg, fw["lse"], g=g))
+    return out
+
+
+# --------------------------------------------------------------------------- O6
+def _log_softmax(x: np.ndarray) -> np.ndarray:
+    m = x.max()
+    return x - (m + np.log(np.exp(x - m).sum()))
+
+
+def step_variants(trace: dict, accept_loss: str = "fkl", ntp_beta: float = 0.0, k_accept: int = 1,
+                  k_discard: int = 10, lambda_discard: float = 1.0, normalize: int = 0, discard_scope: int = 0,
+                  g: float = 1.0, want_grads: bool = True, rows=None):
+    """O6 (NEXT F2): the §5.1 objectives on a dense trace, row by row.
+
+    ACCEPT rows: accept_loss "fkl" = KL(p~ || q) on the target top-k_accept support
+    (Eq. 3, as O3-O5); "rkl" = KL(q || p) with p = softmax(T_row) over the full
+    vocabulary (loss sum_j q_j (ln q_j - ln p_j), gradient q*((ln q - ln p) -
+    KL)), plus ntp_beta * (-ln q_y) with y the verified token (gradient
+    q - e_y; "RKL + NTP").  DISCARD rows: k_discard >= 1 = the filtered KL of
+    O3-O5; k_discard = 0 = KL(p || q) over the full vocabulary ("top-k = 0", P:292,
+    S:330 "topk=0 disables filtering"; gradient q - p).  Row weights as O3 (per-term
+    means over the global counts, reading Q7); the NTP term shares the accepted rows'
+    weight.  rows: subset of rows to evaluate (weights still use the full counts);
+    gradients then cover only those rows' contributions.
+    """
+    T = bf16_bits_to_f64(trace["T_bits"])
+    H64 = bf16_bits_to_f64(trace["H_bits"])
+    W64 = bf16_bits_to_f64(trace["W_bits"])
+    k_max = max(k_accept, k_discard, 1)
+    amax, topk, nonfinite = target_scan(T, k_max)
+    if nonfinite:
+        raise ValueError("non-finite target logits")
+    lab = verify(trace["draft_tokens"], trace["parents"], trace["num_nodes"], amax, discard_scope)
+    cls = lab["row_class"]
+    n_acc = int(np.sum(cls == ACCEPT))
+    n_dis = int(np.sum(cls == DISCARD))
+    M, d = H64.shape
+    rows = range(M) if rows is None else rows
+    row_loss = np.zeros(M)
+    w = np.zeros(M)
+    dH = np.zeros((M, d)) if want_grads else None
+    dW = np.zeros_like(W64) if want_grads else None
+    for m in rows:
+        c = int(cls[m])
+        if c == PAD:
+            continue
+        if normalize == 0:
+            w[m] = (1.0 / n_acc) if c == ACCEPT else (lambda_discard / n_dis if n_dis else 0.0)
+        else:
+            w[m] = (1.0 if c == ACCEPT else lambda_discard) / (n_acc + n_dis)
+        z = W64 @ H64[m]
+        logq = _log_softmax(z)
+        q = np.exp(logq)
+        logp = _log_softmax(T[m])
+        p = np.exp(logp)
+        if c == ACCEPT and accept_loss == "rkl":
+            kl = float(np.sum(q * (logq - logp)))
+            grad = q * ((logq - logp) - kl)
+            y = int(amax[m])
+            loss = kl + ntp_beta * (-logq[y])
+            grad = grad + ntp_beta * q
+            grad[y] -= ntp_beta
+        elif c == DISCARD and k_discard == 0:
+            loss = float(np.sum(p * (logp - logq)))
+            grad = q - p
+        else:
+            k = k_accept if c == ACCEPT else k_discard
+            S = np.asarray(topk[m][:k], dtype=np.int64)
+            pt = np.exp(_log_softmax(T[m][S]))
+            loss = float(np.sum(pt * (np.log(pt) - logq[S])))
+            grad = q.copy()
+            grad[S] -= pt
+        row_loss[m] = loss
+        if want_grads:
+            dz = g * w[m] * grad
+            dH[m] = dz @ W64
+            dW += np.outer(dz, H64[m])
+    out = dict(argmax=amax, topk=topk, **lab, w=w, row_loss=row_loss, loss=float(np.dot(w, row_loss)),
+               counts=(n_acc, n_dis))
+    if want_grads:
+        out.update(dH=dH, dW=dW)
     return out

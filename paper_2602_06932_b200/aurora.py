@@ -50,14 +50,17 @@ class aurora_trace_topk_t(C.Structure):
 
 class aurora_loss_cfg_t(C.Structure):
     _fields_ = [("k_accept", C.c_int32), ("k_discard", C.c_int32), ("lambda_discard", C.c_float),
-                ("normalize", C.c_int32), ("discard_scope", C.c_int32)]
+                ("normalize", C.c_int32), ("discard_scope", C.c_int32), ("accept_loss", C.c_int32),
+                ("ntp_beta", C.c_float)]
 
 
 class aurora_labels_t(C.Structure):
     _fields_ = [("k_max", C.c_int32), ("target_argmax", C.c_void_p), ("accepted", C.c_void_p),
                 ("accept_len", C.c_void_p), ("bonus", C.c_void_p), ("row_class", C.c_void_p),
                 ("sup_idx", C.c_void_p), ("sup_p", C.c_void_p), ("row_H", C.c_void_p), ("row_w", C.c_void_p),
-                ("counts", C.c_void_p), ("status", C.c_void_p)]
+                ("counts", C.c_void_p), ("status", C.c_void_p), ("row_lse_t", C.c_void_p), ("row_aux", C.c_void_p),
+                ("target_logits", C.c_void_p), ("ld_target", C.c_int64), ("objective", C.c_int32),
+                ("ntp_beta", C.c_float)]
 
 
 _lib = None
@@ -236,15 +239,18 @@ class SpecTrainStep:
 
     def __init__(self, R: int, N: int, d: int, V: int, V_local: Optional[int] = None, vocab_offset: int = 0,
                  k_accept: int = 1, k_discard: int = 10, lambda_discard: float = 1.0, normalize: int = 0,
-                 discard_scope: int = 0, device="cuda", comm=None):
+                 discard_scope: int = 0, device="cuda", comm=None, accept_loss: str = "fkl", ntp_beta: float = 0.0):
         import torch
         self.R, self.N, self.d, self.V = R, N, d, V
         self.V_local = V if V_local is None else V_local
         self.vocab_offset = vocab_offset
         self.M = R * (N + 1)
         self.comm = comm
-        self.cfg = aurora_loss_cfg_t(k_accept, k_discard, lambda_discard, normalize, discard_scope)
-        self.k_max = max(k_accept, k_discard)
+        if accept_loss not in ("fkl", "rkl"):
+            raise ValueError("accept_loss must be 'fkl' or 'rkl'")
+        self.cfg = aurora_loss_cfg_t(k_accept, k_discard, lambda_discard, normalize, discard_scope,
+                                     1 if accept_loss == "rkl" else 0, ntp_beta)
+        self.k_max = max(k_accept, k_discard, 1)
         dev = torch.device(device)
         M, km = self.M, self.k_max
         i32, u8, f32 = torch.int32, torch.uint8, torch.float32
@@ -262,9 +268,13 @@ class SpecTrainStep:
         self.row_lse = torch.empty(M, dtype=f32, device=dev)
         self.row_loss = torch.empty(M, dtype=f32, device=dev)
         self.loss = torch.empty(1, dtype=f32, device=dev)
+        self.row_lse_t = torch.empty(M, dtype=f32, device=dev)
+        self.row_aux = torch.empty(M, dtype=f32, device=dev)
         self.labels = aurora_labels_t(km, *(t.data_ptr() for t in (
             self.target_argmax, self.accepted, self.accept_len, self.bonus, self.row_class, self.sup_idx,
-            self.sup_p, self.row_H, self.row_w, self.counts, self.status)))
+            self.sup_p, self.row_H, self.row_w, self.counts, self.status, self.row_lse_t, self.row_aux)), None, 0, 0,
+            0.0)
+        self._target_ref = None
         self.ws_bytes = aurora_workspace_size(OP_ALL, M, d, self.V_local, self.cfg)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
 
@@ -273,6 +283,10 @@ class SpecTrainStep:
         _expect(num_nodes, "i32", "num_nodes"); _expect(target_logits, "bf16", "target_logits")
         t = aurora_trace_t(self.R, self.N, _ptr(draft_tokens), _ptr(parents), _ptr(num_nodes), _ptr(target_logits),
                            target_logits.stride(0), self.V, self.V_local, self.vocab_offset)
+        # F2 objectives read T again in fwd / bwd: the labels reference it (kept alive here)
+        self.labels.target_logits = _ptr(target_logits)
+        self.labels.ld_target = target_logits.stride(0)
+        self._target_ref = target_logits
         aurora_verify_labels(t, self.cfg, self.labels, self.ws.data_ptr(), self.ws_bytes, self.comm, stream)
 
     def verify_topk(self, draft_tokens, target_ids, target_vals, parents=None, num_nodes=None, stream=None):
@@ -287,6 +301,9 @@ class SpecTrainStep:
             raise ValueError("workspace too small for this K_t")
         t = aurora_trace_topk_t(self.R, self.N, _ptr(draft_tokens), _ptr(parents), _ptr(num_nodes), _ptr(target_ids),
                                 _ptr(target_vals), K_t, self.V)
+        self.labels.target_logits = None
+        self.labels.ld_target = 0
+        self._target_ref = None
         _check("aurora_verify_labels_topk", lib().aurora_verify_labels_topk(
             C.byref(t), C.byref(self.cfg), C.byref(self.labels), self.ws.data_ptr(), self.ws_bytes, self.comm,
             _stream(stream)))

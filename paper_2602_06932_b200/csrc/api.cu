@@ -193,10 +193,11 @@ int dh_splits(int64_t M, int64_t d, int64_t kb_total, int pair = 1) {
   return 1;
 }
 
-struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; };
+struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; float* ept; };
 VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
   const int nseg = scan_nseg(M, V_local);
   VerifyWs w;
+  w.ept = c.take<float>(M);
   w.cand_val = c.take<float>(M * nseg * k_max);
   w.cand_idx = c.take<int32_t>(M * nseg * k_max);
   w.top_val = c.take<float>(M * k_max);
@@ -209,14 +210,15 @@ VerifyWs carve_verify_long(Carver& c, int64_t M, int k_top) {  // F1 long suppor
   w.top_idx = c.take<int32_t>(M * k_top);
   return w;
 }
-struct FwdWs { float *pm, *ps, *pu, *msu, *bp; };
+struct FwdWs { float *pm, *ps, *pu, *pr, *msu, *bp; };
 FwdWs carve_fwd(Carver& c, int64_t M, int64_t V_local) {
   FwdWs w;
   const int64_t max_tiles = cdiv(V_local, kMinBN);  // sized for the narrowest tile width
   w.pm = c.take<float>(M * 2 * max_tiles);  // one partial per (vocab tile, column half)
   w.ps = c.take<float>(M * 2 * max_tiles);
   w.pu = c.take<float>(M * 2 * max_tiles);
-  w.msu = c.take<float>(M * 3);
+  w.pr = c.take<float>(M * 2 * max_tiles);  // F2 reverse-KL partials
+  w.msu = c.take<float>(M * kMsu);
   w.bp = c.take<float>(cdiv(M, 256) + 1);
   return w;
 }
@@ -267,13 +269,31 @@ bool classic_bwd() { return opts().bwd_mode == 0; }
 
 aurora_status_t check_cfg(const aurora_loss_cfg_t* cfg, int max_k = AURORA_MAX_K) {
   if (!cfg) return AURORA_ERR_INVALID_ARG;
-  if (cfg->k_discard == 0) return AURORA_ERR_UNSUPPORTED;  // dense discard KL (NEXT F2)
-  if (cfg->k_accept < 1 || cfg->k_accept > max_k || cfg->k_discard < 1 || cfg->k_discard > max_k)
+  if (cfg->k_accept < 1 || cfg->k_accept > max_k || cfg->k_discard < 0 || cfg->k_discard > max_k)
     return AURORA_ERR_INVALID_ARG;
   if (!(cfg->lambda_discard >= 0.f) || !std::isfinite(cfg->lambda_discard)) return AURORA_ERR_INVALID_ARG;
   if (cfg->normalize != 0 && cfg->normalize != 1) return AURORA_ERR_INVALID_ARG;
   if (cfg->discard_scope != 0 && cfg->discard_scope != 1) return AURORA_ERR_INVALID_ARG;
+  if (cfg->accept_loss != 0 && cfg->accept_loss != 1) return AURORA_ERR_INVALID_ARG;
+  if (!(cfg->ntp_beta >= 0.f) || !std::isfinite(cfg->ntp_beta)) return AURORA_ERR_INVALID_ARG;
+  if (cfg->ntp_beta > 0.f && cfg->accept_loss != 1) return AURORA_ERR_INVALID_ARG;  // NTP pairs with RKL
   return AURORA_OK;
+}
+// F2 objectives that read the dense target row again (bit 0 RKL, bit 1 dense discard KL)
+int32_t objective_of(const aurora_loss_cfg_t* cfg) {
+  return (cfg->accept_loss == 1 ? 1 : 0) | (cfg->k_discard == 0 ? 2 : 0);
+}
+// GEMM arguments of the F2 epilogues; c0 = first T column of the GEMM's column 0.
+void set_f2_args(GemmArgs& a, const aurora_labels_t* l, int64_t c0) {
+  a.T = static_cast<const uint16_t*>(l->target_logits) + c0;
+  a.ldT = l->ld_target;
+  a.t_vec = ((reinterpret_cast<uintptr_t>(a.T) & 15) == 0 && (l->ld_target & 7) == 0) ? 1 : 0;
+  a.row_class = l->row_class;
+  a.f2_rkl = (l->objective & 1) ? 1 : 0;
+  a.f2_dense = (l->objective & 2) ? 1 : 0;
+  a.ntp_beta = l->ntp_beta;
+  a.row_lse_t = l->row_lse_t;
+  a.row_aux = l->row_aux;
 }
 bool labels_ok(const aurora_labels_t* l, bool verify_outputs, int max_k = AURORA_MAX_K_SPARSE) {
   if (!l) return false;
@@ -567,7 +587,14 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   const int64_t M = static_cast<int64_t>(t->R) * (t->N + 1);
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->V_local, cfg)) return AURORA_ERR_WORKSPACE;
   if (comm && comm->vp_size > 1 && t->V_local == t->V) return AURORA_ERR_INVALID_ARG;  // VP needs shards
+  const int32_t objective = objective_of(cfg);
+  if (objective) {  // F2: single vocab shard; labels carry the per-row target statistics
+    if (comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
+    if (!out->row_lse_t || !out->row_aux) return AURORA_ERR_INVALID_ARG;
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  out->objective = objective;
+  out->ntp_beta = cfg->ntp_beta;
 
   Carver c(ws);
   VerifyWs w = carve_verify(c, M, t->V_local, k_max);
@@ -590,6 +617,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   p.cand_idx = w.cand_idx;
   p.top_val = w.top_val;
   p.top_idx = w.top_idx;
+  p.ept = w.ept;
   p.lab = *out;
   p.cfg = *cfg;
 
@@ -618,6 +646,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
     if ((e = launch_topk_merge(p, gv, gi, comm->vp_size, k_max, static_cast<int64_t>(M) * k_max, s)) != cudaSuccess)
       return AURORA_ERR_CUDA;
   }
+  if (objective && (e = launch_row_lse_t(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   prof_begin(PH_VERIFY, s);
   if ((e = launch_verify(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->dp_x()) {
@@ -647,8 +676,11 @@ aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const au
   if (long_path && t->K_t > AURORA_MAX_KT_SPARSE) return AURORA_ERR_UNSUPPORTED;
   if (!long_path && k_max > AURORA_MAX_K) return AURORA_ERR_INVALID_ARG;  // warp lists hold <= 16
   const int64_t M = static_cast<int64_t>(t->R) * (t->N + 1);
+  if (objective_of(cfg)) return AURORA_ERR_UNSUPPORTED;  // F2 needs the dense target row
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->K_t, cfg)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  out->objective = 0;
+  out->ntp_beta = 0.f;
   Carver c(ws);
   VerifyWs w = long_path ? carve_verify_long(c, M, kk) : carve_verify(c, M, t->K_t, k_max);
   VerifyLaunch p{};
@@ -695,6 +727,11 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   if (!labels_ok(labels, false) || !row_lse || !loss) return AURORA_ERR_INVALID_ARG;
   aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_FWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
+  const int32_t objective = labels->objective;
+  if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
+                    labels->ld_target < V_local))
+    return AURORA_ERR_INVALID_ARG;
+  if (objective && comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Carver c(ws);
   FwdWs w = carve_fwd(c, M, V_local);
@@ -719,26 +756,29 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   a.p_max = w.pm;
   a.p_sum = w.ps;
   a.p_u = w.pu;
+  if (objective) set_f2_args(a, labels, 0);
   prof_begin(PH_FWD_GEMM, s);
-  cudaError_t e = launch_umma_gemm(EPI_FWD_STATS, false, false, tmH, tmW, a, s, nullptr, pf, bn);
+  cudaError_t e = launch_umma_gemm(objective ? EPI_FWD_STATS_T : EPI_FWD_STATS, false, false, tmH, tmW, a, s, nullptr,
+                                   pf, bn);
   prof_end(PH_FWD_GEMM, s);
   if (e != cudaSuccess) return AURORA_ERR_CUDA;
   prof_begin(PH_FWD_COMBINE, s);
-  if ((e = launch_reduce_partials(w.pm, w.ps, w.pu, M, 2 * a.n_tiles, w.msu, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  if ((e = launch_reduce_partials(w.pm, w.ps, w.pu, objective ? w.pr : nullptr, M, 2 * a.n_tiles, w.msu, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   const float* msu_all = w.msu;
   int P = 1;
   if (comm && comm->vp_x()) {
     auto& A = nccl::api();
-    const size_t need = static_cast<size_t>(M) * 3 * comm->vp_size * sizeof(float);
+    const size_t need = static_cast<size_t>(M) * kMsu * comm->vp_size * sizeof(float);
     if (!ensure_scratch(comm, need)) return AURORA_ERR_CUDA;
-    if (A.AllGather(w.msu, comm->scratch, static_cast<size_t>(M) * 3, nccl::ncclFloat32, comm->vp, s) != 0)
+    if (A.AllGather(w.msu, comm->scratch, static_cast<size_t>(M) * kMsu, nccl::ncclFloat32, comm->vp, s) != 0)
       return AURORA_ERR_NCCL;
     msu_all = static_cast<const float*>(comm->scratch);
     P = comm->vp_size;
   }
   int nb = 0;
+  RowF2 f2{(objective & 1) ? 1 : 0, labels->ntp_beta, labels->row_lse_t, labels->row_aux};
   if ((e = launch_row_combine(msu_all, P, M, labels->row_H, labels->row_w, labels->row_class, row_lse, row_loss,
-                              w.bp, &nb, s)) != cudaSuccess)
+                              w.bp, &nb, f2, s)) != cudaSuccess)
     return AURORA_ERR_CUDA;
   if ((e = launch_loss_sum(w.bp, nb, loss, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->dp_x()) {
@@ -760,7 +800,13 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float* dWf = static_cast<float*>(dW);
-  if (!classic_bwd()) return bwd_fused(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf,
+  const int32_t objective = labels->objective;
+  if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
+                    labels->ld_target < V_local))
+    return AURORA_ERR_INVALID_ARG;
+  if (objective && comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
+  // the fused persistent bwd implements Eq. 3 only; the F2 objectives take the chunked path
+  if (!classic_bwd() && !objective) return bwd_fused(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf,
                                        accumulate_dW, ws, comm, s);
   Carver c(ws);
   BwdWs w = carve_bwd(c, M, d, V_local);
@@ -816,8 +862,10 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     a.dzT = dzT;
     a.ld_dzT = w.m_pad;
     a.tile_counter = w.counters + 3 * ch;
+    if (objective) set_f2_args(a, labels, c0);
     prof_begin(PH_BWD_DZ, s);
-    cudaError_t e = launch_umma_gemm(EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s, nullptr, pz, bz);
+    cudaError_t e = launch_umma_gemm(objective ? EPI_BWD_DZ_T : EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s, nullptr,
+                                     pz, bz);
     prof_end(PH_BWD_DZ, s);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (S) {
@@ -965,6 +1013,11 @@ aurora_status_t aurora_debug_gemm(int a_mn, int b_mn, const void* A, const void*
   ok = ok && (b_mn ? make_tmap_bf16(&tb, B, N, K, ldb, 64, 64) : make_tmap_bf16(&tb, B, K, N, ldb, 64, BN / pr));
   if (!ok) return AURORA_ERR_CUDA;
   GemmArgs g{};
+  static const int dbg_nfast = [] {  // diagnostics: tile raster of the test hook
+    const char* e = getenv("AURORA_DBG_NFAST");
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  g.n_fastest = dbg_nfast;
   g.m_tiles = static_cast<int32_t>(cdiv(M, BM * pr));
   g.n_tiles = static_cast<int32_t>(cdiv(N, BN));
   g.splits = 1;

@@ -26,7 +26,9 @@ constexpr int kSchedDepth = 4;  // tile-index ring depth (dynamic scheduler)
 constexpr int kStgLd = 20;  // fp32 staging row stride (floats) for 32x16 blocks (LSU path)
 constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 1024 /*barriers*/ + kEpiWarps * 2 * 2048;  // epilogue staging: 2 x (32x16 fp32) slots per warp
 
-enum EpiKind : int { EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2 };
+// *_T: the F2 objectives (reverse KL on ACCEPT rows, dense KL on DISCARD rows) — the
+// epilogue also reads the row's target logits T (bf16) for the tile's columns.
+enum EpiKind : int { EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2, EPI_FWD_STATS_T = 3, EPI_BWD_DZ_T = 4 };
 
 struct GemmArgs {
   int32_t m_tiles, n_tiles, splits;
@@ -54,6 +56,17 @@ struct GemmArgs {
   int32_t n_fastest;      // tile raster: 0 = m-fastest (B streams once), 1 = n-fastest (A streams once)
   int32_t tma_store;      // set by launch_umma_gemm when an output tensor map is given
   int32_t dbg_epi;        // diagnostics only (AURORA_DBG_EPI): 1 skip tcgen05.ld, 2 skip fence + bulk store
+  // ---- F2 objectives (EPI_*_T)
+  const uint16_t* T;         // bf16 target logits of GEMM column 0, row stride ldT
+  int64_t ldT;
+  int32_t t_vec;             // T rows 16-byte aligned (vector loads)
+  const uint8_t* row_class;
+  int32_t f2_rkl;            // ACCEPT rows: reverse KL (+ NTP via the support {y: beta})
+  int32_t f2_dense;          // DISCARD rows: dense KL(p_target || q)
+  float ntp_beta;
+  const float* row_lse_t;    // [M] log-sum-exp of the T row
+  const float* row_aux;      // [M] E_q[z - t] (bwd, RKL rows)
+  float* p_r;                // [M, 2*n_tiles] partial sum e^{z-m} (z - t) (fwd, RKL rows)
 };
 
 // Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.
@@ -120,6 +133,7 @@ struct VerifyLaunch {
   float* top_val;       // [M, k_max] merged (value order); long path: [M, k_top]
   int32_t* top_idx;
   int32_t k_top;        // long-support path (k > AURORA_MAX_K): top-list length per row
+  float* ept;           // F2: [M] E_p[t] of the target row (dense discard rows' H)
   aurora_labels_t lab;
   aurora_loss_cfg_t cfg;
 };
@@ -134,13 +148,23 @@ cudaError_t launch_finalize(const VerifyLaunch& p, cudaStream_t s);
 cudaError_t launch_sort_pairs(const VerifyLaunch& p, const int32_t* tk_idx, const uint16_t* tk_val, int32_t K_t,
                               cudaStream_t s);
 cudaError_t launch_finalize_long(const VerifyLaunch& p, cudaStream_t s);
+// F2: per-row log-sum-exp and E_p[t] of the dense target row (CTA per row).
+cudaError_t launch_row_lse_t(const VerifyLaunch& p, cudaStream_t s);
 
 // ---------------------------------------------------------------- row kernels
-cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, int64_t M, int n_tiles,
-                                   float* msu /*[M,3]*/, cudaStream_t s);
-cudaError_t launch_row_combine(const float* msu_all /*[P,M,3]*/, int P, int64_t M, const float* row_H,
+// msu rows are (m, s, u, r): r = sum e^{z-m} (z - t) on F2 RKL rows (pr nullable => 0).
+constexpr int kMsu = 4;
+cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, const float* pr, int64_t M,
+                                   int n_tiles, float* msu /*[M,kMsu]*/, cudaStream_t s);
+struct RowF2 {  // F2 objectives in the row combine (all zero / null: Eq. 3 FKL everywhere)
+  int32_t rkl;
+  float beta;
+  const float* row_lse_t;
+  float* row_aux;  // out: E_q[z - t] on RKL rows
+};
+cudaError_t launch_row_combine(const float* msu_all /*[P,M,kMsu]*/, int P, int64_t M, const float* row_H,
                                const float* row_w, const uint8_t* row_class, float* row_lse, float* row_loss,
-                               float* block_partials, int* nblocks_out, cudaStream_t s);
+                               float* block_partials, int* nblocks_out, const RowF2& f2, cudaStream_t s);
 cudaError_t launch_loss_sum(const float* block_partials, int nblocks, float* loss, cudaStream_t s);
 cudaError_t launch_splitk_reduce(const float* partials, int splits, int64_t n_elems, float* out, int accumulate,
                                  cudaStream_t s);

@@ -40,18 +40,38 @@ int g_pair_max_clusters = -1;
 // single-CTA tiles, chosen by the host when the narrower tile fills the 148 SMs' waves
 // better (e.g. M = 384 rows x a 32K-column dz chunk: 378 tiles = 2.55 waves at 256 wide,
 // 432 tiles = 2.92 waves at 224).  Accumulators stay at TMEM columns 0 / 256.
-// Shared-memory plan of one instantiation.  A store-bound fp32 epilogue is limited by
-// the bytes its bulk stores keep in flight (measured: 2 x 2 KB slots per warp cap a CTA
-// near 30 GB/s), so the CTA-pair STORE_F32 kernel trades two of its six ring stages (K per
-// tile is small where it is store-bound) for 6 staging slots per epilogue warp.
+// F2: the 32 bf16 target logits T[row, c .. c+32) as floats (n valid; rest -inf).
+__device__ __forceinline__ void load_t32(const uint16_t* trow, int64_t c, int n, int vec, float* t) {
+  if (vec && n == 32) {
+    const uint4* p = reinterpret_cast<const uint4*>(trow + c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint4 w = __ldg(p + i);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        t[8 * i + 2 * e] = __uint_as_float(ws[e] << 16);
+        t[8 * i + 2 * e + 1] = __uint_as_float(ws[e] & 0xFFFF0000u);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) t[j] = j < n ? __uint_as_float(static_cast<uint32_t>(__ldg(trow + c + j)) << 16) : -INFINITY;
+  }
+}
+
+// Shared-memory plan of one instantiation.  The fp32 store epilogue keeps kSlots 2 KB
+// bulk-store slots per epilogue warp (measured: 6 slots instead of 2, 32x32 boxes, or
+// half the warps on LSU stores do not raise the store-bound rate, and fewer ring stages
+// slow K = 384).
 template <int EPI, bool A_MN, int PAIR, int TBN>
 struct SmemPlan {
   static constexpr int kSB = (TBN / PAIR) * BK * 2;  // B bytes per stage in this CTA
   static constexpr int kStageBytes = kSmemA + kSB;
   static constexpr bool kStore = EPI == EPI_STORE_F32;
-  static constexpr int kSt = PAIR == 2 ? (kStore ? 4 : 6) : kStages;
+  static constexpr int kSt = PAIR == 2 ? 6 : kStages;
   static constexpr int kRing = kSt * kStageBytes;
-  static constexpr int kSlots = kStore ? (PAIR == 2 ? 6 : 2) : 0;  // 2 KB bulk-store slots per warp
+  static constexpr int kSlots = kStore ? 2 : 0;  // 2 KB bulk-store slots per warp
   static constexpr int kStaging = kEpiWarps * kSlots * 2048;
   static constexpr int kBytes = kRing + 1024 /*barriers*/ + 1024 /*base alignment*/ + kStaging;
   static_assert(kBytes <= 232448, "dynamic smem per CTA");
@@ -64,6 +84,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
   using Plan = SmemPlan<EPI, A_MN, PAIR, TBN>;
+  constexpr bool kFwd = EPI == EPI_FWD_STATS || EPI == EPI_FWD_STATS_T;
+  constexpr bool kDz = EPI == EPI_BWD_DZ || EPI == EPI_BWD_DZ_T;
+  constexpr bool kT = EPI == EPI_FWD_STATS_T || EPI == EPI_BWD_DZ_T;
   static_assert(TBN == BN || (PAIR == 1 && !B_MN), "narrow tiles: single-CTA, K-major B only");
   static_assert(TBN % 32 == 0 && TBN > BN / 2 && TBN <= BN, "tile width");
   constexpr int kSt = Plan::kSt;
@@ -260,7 +283,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 
-      if constexpr (EPI == EPI_FWD_STATS || EPI == EPI_BWD_DZ) {
+      if constexpr (kFwd || kDz) {
         SupCursor cur;
         cur.idx = args.sup_idx + (row_ok ? row : 0) * args.k_max;
         cur.p = args.sup_p + (row_ok ? row : 0) * args.k_max;
@@ -268,24 +291,42 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         cur.limit = args.N;
         cur.gid0 = args.col_gid0;
         cur.seek(col0 + cbeg);
-        float mrun = -INFINITY, srun = 0.f, usum = 0.f;
+        float mrun = -INFINITY, srun = 0.f, usum = 0.f, rrun = 0.f;
         float coef = 0.f, lse2 = 0.f;
-        if constexpr (EPI == EPI_BWD_DZ) {
+        if constexpr (kDz) {
           if (row_ok) {
             const float g = args.dloss ? __ldg(args.dloss) : 1.f;
             coef = g * __ldg(args.row_w + row);
             lse2 = __ldg(args.row_lse + row) * kLog2e;
           }
         }
+        // F2 row mode: 0 Eq. 3 (support only), 1 reverse KL (+NTP through the support
+        // {y: beta}), 2 dense KL(p_target || q) (empty support).
+        int mode = 0;
+        float lset2 = 0.f, eqzt = 0.f;
+        const uint16_t* trow = nullptr;
+        if constexpr (kT) {
+          if (row_ok) {
+            const uint8_t cls = __ldg(args.row_class + row);
+            mode = (cls == AURORA_ROW_ACCEPT && args.f2_rkl) ? 1 : ((cls == AURORA_ROW_DISCARD && args.f2_dense) ? 2 : 0);
+            trow = args.T + row * args.ldT;
+            if (mode == 2) lset2 = __ldg(args.row_lse_t + row) * kLog2e;
+            if (kDz && mode == 1) eqzt = __ldg(args.row_aux + row);
+          }
+        }
         for (int cb = cbeg; cb < cend; cb += 32) {  // warp-uniform bounds
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + cb, r);
+          const bool full = (cb + 32 <= ncols);
+          float t[32];
+          if constexpr (kT) {
+            if (mode != 0) load_t32(trow, col0 + cb, full ? 32 : ncols - cb, args.t_vec, t);
+          }
           tmem_ld_wait();
           float z[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(r[j]);
-          const bool full = (cb + 32 <= ncols);
-          if constexpr (EPI == EPI_FWD_STATS) {
+          if constexpr (kFwd) {
             if (!full) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) z[j] = (cb + j < ncols) ? z[j] : -INFINITY;
@@ -295,12 +336,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int j = 1; j < 32; ++j) cmax = fmaxf(cmax, z[j]);
             const float mnew = fmaxf(mrun, cmax);
             const float mb = mnew * kLog2e;
-            srun *= ex2_approx(mrun * kLog2e - mb);
+            const float scale = ex2_approx(mrun * kLog2e - mb);
+            srun *= scale;
             float s0 = 0.f, s1 = 0.f;
+            if (!kT || mode == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              s0 += ex2_approx(fmaf(z[j], kLog2e, -mb));
-              s1 += ex2_approx(fmaf(z[j + 1], kLog2e, -mb));
+              for (int j = 0; j < 32; j += 2) {
+                s0 += ex2_approx(fmaf(z[j], kLog2e, -mb));
+                s1 += ex2_approx(fmaf(z[j + 1], kLog2e, -mb));
+              }
+            } else if (mode == 1) {  // r = sum e^{z-m} (z - t), rescaled with s
+              rrun *= scale;
+              float r0 = 0.f;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float e = ex2_approx(fmaf(z[j], kLog2e, -mb));
+                s0 += e;
+                r0 = fmaf(e, (cb + j < ncols) ? z[j] - t[j] : 0.f, r0);
+              }
+              rrun += r0;
+            } else {  // u += sum_j p_j z_j, p_j = exp(t_j - lse_t)
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                s0 += ex2_approx(fmaf(z[j], kLog2e, -mb));
+                if (cb + j < ncols) usum = fmaf(ex2_approx(fmaf(t[j], kLog2e, -lset2)), z[j], usum);
+              }
             }
             srun += s0 + s1;
             mrun = mnew;
@@ -309,8 +369,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               cur.advance();
             }
           } else {
+            if (!kT || mode == 0) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) z[j] = coef * ex2_approx(fmaf(z[j], kLog2e, -lse2));
+              for (int j = 0; j < 32; ++j) z[j] = coef * ex2_approx(fmaf(z[j], kLog2e, -lse2));
+            } else if (mode == 1) {  // q ((z - t) - E_q[z - t] + beta): RKL gradient + NTP's q
+              const float base = args.ntp_beta - eqzt;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) z[j] = coef * ex2_approx(fmaf(z[j], kLog2e, -lse2)) * (z[j] - t[j] + base);
+            } else {  // q - p
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                z[j] = coef * (ex2_approx(fmaf(z[j], kLog2e, -lse2)) - ex2_approx(fmaf(t[j], kLog2e, -lset2)));
+            }
             while (cur.nxt < col0 + cb + 32) {
               const int jj = static_cast<int>(cur.nxt - col0 - cb);
               const float sub = coef * cur.nxt_p;
@@ -327,12 +397,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
         }
-        if constexpr (EPI == EPI_FWD_STATS) {
+        if constexpr (kFwd) {
           if (row_ok) {  // partial slot (vocab tile, column half); empty halves are neutral
             const int64_t o = row * (2 * args.n_tiles) + 2 * nt + half;
             args.p_max[o] = mrun;
             args.p_sum[o] = srun;
             args.p_u[o] = usum;
+            if constexpr (kT) args.p_r[o] = rrun;
           }
         }
       } else if (args.tma_store && !((args.dbg_epi & 4) && half == 1)) {  // EPI_STORE_F32, TMA bulk stores
@@ -505,19 +576,25 @@ template <int PAIR>
 cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, const CUtensorMap& tmB,
                      const CUtensorMap& C, const GemmArgs& g, cudaStream_t s, int bn) {
   if constexpr (PAIR == 1) {
-    if (bn != BN && (a_mn || b_mn || (epi != EPI_FWD_STATS && epi != EPI_BWD_DZ))) return cudaErrorInvalidValue;
+    if (bn != BN && (a_mn || b_mn || epi == EPI_STORE_F32)) return cudaErrorInvalidValue;
     if (bn == 224) {
       if (epi == EPI_FWD_STATS) return launch_impl<EPI_FWD_STATS, false, false, 1, 224>(tmA, tmB, C, g, s);
-      return launch_impl<EPI_BWD_DZ, false, false, 1, 224>(tmA, tmB, C, g, s);
+      if (epi == EPI_BWD_DZ) return launch_impl<EPI_BWD_DZ, false, false, 1, 224>(tmA, tmB, C, g, s);
+      if (epi == EPI_FWD_STATS_T) return launch_impl<EPI_FWD_STATS_T, false, false, 1, 224>(tmA, tmB, C, g, s);
+      return launch_impl<EPI_BWD_DZ_T, false, false, 1, 224>(tmA, tmB, C, g, s);
     }
     if (bn == 192) {
       if (epi == EPI_FWD_STATS) return launch_impl<EPI_FWD_STATS, false, false, 1, 192>(tmA, tmB, C, g, s);
-      return launch_impl<EPI_BWD_DZ, false, false, 1, 192>(tmA, tmB, C, g, s);
+      if (epi == EPI_BWD_DZ) return launch_impl<EPI_BWD_DZ, false, false, 1, 192>(tmA, tmB, C, g, s);
+      if (epi == EPI_FWD_STATS_T) return launch_impl<EPI_FWD_STATS_T, false, false, 1, 192>(tmA, tmB, C, g, s);
+      return launch_impl<EPI_BWD_DZ_T, false, false, 1, 192>(tmA, tmB, C, g, s);
     }
   }
   if (bn != BN) return cudaErrorInvalidValue;
   if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false, PAIR>(tmA, tmB, C, g, s);
+  if (epi == EPI_FWD_STATS_T && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS_T, false, false, PAIR>(tmA, tmB, C, g, s);
+  if (epi == EPI_BWD_DZ_T && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ_T, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_STORE_F32) {
     if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false, PAIR>(tmA, tmB, C, g, s);
     if (!a_mn && b_mn) return launch_impl<EPI_STORE_F32, false, true, PAIR>(tmA, tmB, C, g, s);

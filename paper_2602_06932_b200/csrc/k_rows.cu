@@ -4,9 +4,11 @@
 //                      a row (coalesced: partials are [M, n_tiles] row-major) with the
 //                      online rule s = s e^{m-m'} + s_t e^{m_t-m'}; fixed shuffle order
 //                      => deterministic.
-//   k_row_combine      thread per row: merge the per-rank (m, s, u) in rank order (VP),
+//   k_row_combine      thread per row: merge the per-rank (m, s, u, r) in rank order (VP),
 //                      lse = m + log s, l = lse - u + H~ = KL(p~ || q) (Eq. 3), w l,
-//                      block-ordered partial sums.
+//                      block-ordered partial sums.  F2 reverse-KL rows (NEXT F2):
+//                      KL(q || p) = E_q[z - t] - lse + lse_t with E_q[z - t] = r / s,
+//                      plus beta (lse - z_y) (NTP) where u = beta z_y.
 //   k_loss_sum         one block: ordered sum of the block partials -> loss.
 //   k_splitk_reduce    dH = (acc ? dH : 0) + sum_s partial[s], ordered (deterministic).
 #include <cfloat>
@@ -24,51 +26,70 @@ __device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2)
   s = s * __expf(m - mn) + s2 * __expf(m2 - mn);
   m = mn;
 }
+// (m, s, r): r = sum e^{z - m} x rescales like s
+__device__ __forceinline__ void msr_merge(float& m, float& s, float& r, float m2, float s2, float r2) {
+  const float mn = fmaxf(m, m2);
+  if (mn == -INFINITY) return;
+  const float a = __expf(m - mn), b = __expf(m2 - mn);
+  s = s * a + s2 * b;
+  r = r * a + r2 * b;
+  m = mn;
+}
 }  // namespace
 
 __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict__ pm, const float* __restrict__ ps,
-                                                         const float* __restrict__ pu, int64_t M, int n_tiles,
-                                                         float* __restrict__ msu) {
+                                                         const float* __restrict__ pu, const float* __restrict__ pr,
+                                                         int64_t M, int n_tiles, float* __restrict__ msu) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
-  float m = -INFINITY, s = 0.f, u = 0.f;
+  float m = -INFINITY, s = 0.f, u = 0.f, r = 0.f;
   const int64_t o = row * n_tiles;
   for (int t = lane; t < n_tiles; t += 32) {
-    ms_merge(m, s, __ldg(pm + o + t), __ldg(ps + o + t));
+    msr_merge(m, s, r, __ldg(pm + o + t), __ldg(ps + o + t), pr ? __ldg(pr + o + t) : 0.f);
     u += __ldg(pu + o + t);
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
     const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+    const float r2 = __shfl_xor_sync(0xffffffffu, r, off);
     const float u2 = __shfl_xor_sync(0xffffffffu, u, off);
-    ms_merge(m, s, m2, s2);
+    msr_merge(m, s, r, m2, s2, r2);
     u += u2;
   }
   if (lane == 0) {
-    msu[row * 3 + 0] = m;
-    msu[row * 3 + 1] = s;
-    msu[row * 3 + 2] = u;
+    msu[row * kMsu + 0] = m;
+    msu[row * kMsu + 1] = s;
+    msu[row * kMsu + 2] = u;
+    msu[row * kMsu + 3] = r;
   }
 }
 
 __global__ void __launch_bounds__(256) k_row_combine(const float* __restrict__ msu_all, int P, int64_t M,
                                                      const float* __restrict__ row_H, const float* __restrict__ row_w,
                                                      const uint8_t* __restrict__ row_class, float* __restrict__ row_lse,
-                                                     float* __restrict__ row_loss, float* __restrict__ block_partials) {
+                                                     float* __restrict__ row_loss, float* __restrict__ block_partials,
+                                                     RowF2 f2) {
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
   float wl = 0.f;
   if (row < M) {
-    float m = -INFINITY, s = 0.f, u = 0.f;
-    for (int r = 0; r < P; ++r) {
-      const float* q = msu_all + (static_cast<int64_t>(r) * M + row) * 3;
-      ms_merge(m, s, q[0], q[1]);
+    float m = -INFINITY, s = 0.f, u = 0.f, r = 0.f;
+    for (int p = 0; p < P; ++p) {
+      const float* q = msu_all + (static_cast<int64_t>(p) * M + row) * kMsu;
+      msr_merge(m, s, r, q[0], q[1], q[3]);
       u += q[2];
     }
     const float lse = m + logf(s);
-    const bool pad = row_class[row] == AURORA_ROW_PAD;
-    const float l = pad ? 0.f : (lse - u + row_H[row]);
+    const uint8_t cls = row_class[row];
+    float l = 0.f;
+    if (cls == AURORA_ROW_ACCEPT && f2.rkl) {
+      const float eqzt = r / s;  // E_q[z - t]
+      l = eqzt - lse + f2.row_lse_t[row] + f2.beta * lse - u;
+      f2.row_aux[row] = eqzt;
+    } else if (cls != AURORA_ROW_PAD) {
+      l = lse - u + row_H[row];
+    }
     row_lse[row] = lse;
     if (row_loss) row_loss[row] = l;
     wl = row_w[row] * l;
@@ -133,17 +154,17 @@ __global__ void k_debug_dlogits(const __nv_bfloat16* __restrict__ H, const __nv_
   }
 }
 
-cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, int64_t M, int n_tiles,
-                                   float* msu, cudaStream_t s) {
-  k_reduce_partials<<<static_cast<unsigned>((M + 7) / 8), 256, 0, s>>>(pm, ps, pu, M, n_tiles, msu);
+cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, const float* pr, int64_t M,
+                                   int n_tiles, float* msu, cudaStream_t s) {
+  k_reduce_partials<<<static_cast<unsigned>((M + 7) / 8), 256, 0, s>>>(pm, ps, pu, pr, M, n_tiles, msu);
   count_launch();
   return cudaGetLastError();
 }
 cudaError_t launch_row_combine(const float* msu_all, int P, int64_t M, const float* row_H, const float* row_w,
                                const uint8_t* row_class, float* row_lse, float* row_loss, float* block_partials,
-                               int* nblocks_out, cudaStream_t s) {
+                               int* nblocks_out, const RowF2& f2, cudaStream_t s) {
   const int nb = static_cast<int>((M + 255) / 256);
-  k_row_combine<<<nb, 256, 0, s>>>(msu_all, P, M, row_H, row_w, row_class, row_lse, row_loss, block_partials);
+  k_row_combine<<<nb, 256, 0, s>>>(msu_all, P, M, row_H, row_w, row_class, row_lse, row_loss, block_partials, f2);
   count_launch();
   *nblocks_out = nb;
   return cudaGetLastError();

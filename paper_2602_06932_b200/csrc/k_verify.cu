@@ -449,6 +449,21 @@ __global__ void __launch_bounds__(256) k_finalize(VerifyLaunch p) {
     w = p.cfg.normalize ? p.cfg.lambda_discard / static_cast<float>(na + nd)
                         : (nd > 0 ? p.cfg.lambda_discard / static_cast<float>(nd) : 0.f);
   }
+  // F2: reverse-KL ACCEPT rows carry the support {y: beta} (the NTP term; the KL itself is
+  // computed from T in the GEMM epilogues), dense-KL DISCARD rows an empty support with
+  // H = E_p[t] - lse_t (sum_j p_j log p_j of the full target row).
+  const bool f2_rkl = cls == AURORA_ROW_ACCEPT && p.cfg.accept_loss == 1;
+  const bool f2_dense = cls == AURORA_ROW_DISCARD && p.cfg.k_discard == 0;
+  if (f2_rkl || f2_dense) {
+    const bool one = f2_rkl && p.cfg.ntp_beta > 0.f;
+    for (int j = 0; j < km; ++j) {
+      p.lab.sup_idx[m * km + j] = (one && j == 0) ? p.top_idx[m * km] : INT32_MAX;
+      p.lab.sup_p[m * km + j] = (one && j == 0) ? p.cfg.ntp_beta : 0.f;
+    }
+    p.lab.row_H[m] = f2_dense ? p.ept[m] - p.lab.row_lse_t[m] : 0.f;
+    p.lab.row_w[m] = w;
+    return;
+  }
   float v[KM];
   int32_t ix[KM];
   const float* tv = p.top_val + m * km;
@@ -631,6 +646,53 @@ __global__ void __launch_bounds__(256) k_finalize_long(VerifyLaunch p) {
   }
 }
 
+// --------------------------------------------------------------------------- F2 row lse of T
+// NEXT F2 (reverse KL / dense discard KL need p_target = softmax(T) over the full row):
+// CTA per row, online (max, sum e^{t-m}, sum e^{t-m} t) over the row's vocab slice,
+// deterministic merge (fixed strides, shuffle tree, warps in order).
+__global__ void __launch_bounds__(256) k_row_lse_t(VerifyLaunch p) {
+  const int64_t row = blockIdx.x;
+  const uint16_t* tr = p.T + row * p.ldT;
+  float m = -INFINITY, S = 0.f, A = 0.f;
+  auto add = [&](float t) {
+    if (t > m) {
+      const float c = __expf(m - t);
+      S *= c;
+      A *= c;
+      m = t;
+    }
+    const float e = __expf(t - m);
+    S += e;
+    A = fmaf(e, t, A);
+  };
+  for (int64_t j = threadIdx.x; j < p.V_local; j += blockDim.x) add(__uint_as_float(static_cast<uint32_t>(tr[j]) << 16));
+  auto merge = [&](float m2, float S2, float A2) {
+    const float mn = fmaxf(m, m2);
+    if (mn == -INFINITY) return;
+    const float a = __expf(m - mn), b = __expf(m2 - mn);
+    S = S * a + S2 * b;
+    A = A * a + A2 * b;
+    m = mn;
+  };
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+    const float S2 = __shfl_xor_sync(0xffffffffu, S, off);
+    const float A2 = __shfl_xor_sync(0xffffffffu, A, off);
+    merge(m2, S2, A2);
+  }
+  __shared__ float red[3][8];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[0][w] = m; red[1][w] = S; red[2][w] = A; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    m = red[0][0]; S = red[1][0]; A = red[2][0];
+    for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) merge(red[0][i], red[1][i], red[2][i]);
+    p.lab.row_lse_t[row] = m + logf(S);
+    p.ept[row] = A / S;
+  }
+}
+
 // --------------------------------------------------------------------------- launchers
 cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s) {
   k_target_scan<<<static_cast<unsigned>(p.M) * p.nseg, 256, 0, s>>>(p);
@@ -667,6 +729,11 @@ cudaError_t launch_finalize_long(const VerifyLaunch& p, cudaStream_t s) {
   int n = 1;
   while (n < p.k_top) n <<= 1;
   k_finalize_long<<<p.M, 256, static_cast<size_t>(n) * sizeof(uint64_t), s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_row_lse_t(const VerifyLaunch& p, cudaStream_t s) {
+  k_row_lse_t<<<p.M, 256, 0, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }

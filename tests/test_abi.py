@@ -54,10 +54,16 @@ def test_host_validation_without_gpu(L):
     lab = A.aurora_labels_t()
     # NULL trace -> invalid arg, nothing enqueued (no CUDA call happens)
     assert L.aurora_verify_labels(None, C.byref(cfg), C.byref(lab), None, 0, None, None) == 1
-    # k_discard = 0 (paper's unfiltered top-k 0) -> unsupported in this build
-    cfg0 = A.aurora_loss_cfg_t(1, 0, 1.0, 0, 0)
+    # F2 objectives need the dense target row: unsupported with the sparse payload
+    lab_ok = A.aurora_labels_t(10, 16, 16, 16, 16, 16, 16, 16, 16, 16, 16, 16)
+    tk = A.aurora_trace_topk_t(4, 4, 16, None, None, 16, 16, 64, 1000)
+    for cfg_f2 in (A.aurora_loss_cfg_t(1, 0, 1.0, 0, 0), A.aurora_loss_cfg_t(1, 10, 1.0, 0, 0, 1, 0.5)):
+        assert L.aurora_verify_labels_topk(C.byref(tk), C.byref(cfg_f2), C.byref(lab_ok), None, 0, None, None) == 5
+    # invalid objective settings: NTP without RKL, unknown accept_loss, negative beta
     t = A.aurora_trace_t(4, 4, 16, 0, 0, 16, 1000, 1000, 1000, 0)
-    assert L.aurora_verify_labels(C.byref(t), C.byref(cfg0), C.byref(lab), None, 0, None, None) == 5
+    for bad in (A.aurora_loss_cfg_t(1, 10, 1.0, 0, 0, 0, 0.5), A.aurora_loss_cfg_t(1, 10, 1.0, 0, 0, 2, 0.0),
+                A.aurora_loss_cfg_t(1, 10, 1.0, 0, 0, 1, -1.0)):
+        assert L.aurora_verify_labels(C.byref(t), C.byref(bad), C.byref(lab_ok), None, 0, None, None) == 1
     # N > 32
     t2 = A.aurora_trace_t(4, 33, 16, 0, 0, 16, 1000, 1000, 1000, 0)
     assert L.aurora_verify_labels(C.byref(t2), C.byref(cfg), C.byref(lab), None, 0, None, None) == 1

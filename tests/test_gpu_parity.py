@@ -522,3 +522,43 @@ def test_topk_long_support_status_and_limits():
         big = A.SpecTrainStep(c.R, c.N, c.d, c.V, k_accept=17)
         T = torch.zeros(c.M, c.V, dtype=torch.bfloat16, device="cuda")
         big.verify(g["draft"], T, g["parents"], g["num_nodes"])
+
+
+# ----------------------------------------------------------------------------- F2 objectives
+F2_VARIANTS = [dict(accept_loss="rkl", ntp_beta=0.0, k_discard=10), dict(accept_loss="rkl", ntp_beta=0.5, k_discard=0),
+               dict(accept_loss="fkl", ntp_beta=0.0, k_discard=0), dict(accept_loss="rkl", ntp_beta=1.0, k_discard=3)]
+
+
+def _check_f2(name, kw, **run_kw):
+    tr = tracegen.gen_trace(name)
+    ref = oracle.step_variants(tr, **kw)
+    out = _run_gpu(tr, **kw, **run_kw)
+    st = out["st"]
+    assert int(st.status.item()) == 0
+    np.testing.assert_array_equal(st.target_argmax.cpu().numpy(), ref["argmax"])
+    np.testing.assert_array_equal(st.accept_len.cpu().numpy(), ref["accept_len"])
+    np.testing.assert_array_equal(st.row_class.cpu().numpy(), ref["row_class"])
+    assert tuple(st.counts.cpu().tolist()) == tuple(ref["counts"])
+    valid = ref["row_class"] != oracle.PAD
+    np.testing.assert_allclose(st.row_loss.cpu().numpy()[valid], ref["row_loss"][valid], rtol=1e-3, atol=2e-4)
+    loss = float(st.loss.item())
+    assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"]), (loss, ref["loss"])
+    assert _rfro(out["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert _rfro(out["dH"].cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+@pytest.mark.parametrize("kw", F2_VARIANTS)
+@pytest.mark.parametrize("name", ["tiny", "small", "small_tree", "mid"])
+def test_f2_objectives_parity(name, kw):
+    """NEXT F2 (§5.1 objectives): reverse KL on ACCEPT rows (+NTP), dense KL(p || q) on
+    DISCARD rows ("top-k = 0"), vs the oracle's direct full-row definitions."""
+    _check_f2(name, kw)
+
+
+@pytest.mark.parametrize("opt", [dict(gemm_pair=2), dict(gemm_pair=1, tile_n=224), dict(bwd_mode=1)])
+def test_f2_objectives_other_launch_configs(option, opt):
+    """CTA pairs, narrow tiles, and bwd_mode=1 (routed to the chunked path for F2)."""
+    for k, v in opt.items():
+        option(k, v)
+    _check_f2("mid", F2_VARIANTS[1])
+    _check_f2("small_tree", F2_VARIANTS[3])

@@ -526,3 +526,87 @@ def test_discard_direction():
     before = q_rej(W64, H64)
     after = q_rej(W64 - lr * bw["dW"], H64)
     assert after < before
+
+
+# ----------------------------------------------------------------------- O6 variants (F2)
+def _torch_variant_loss(tr, out, accept_loss, ntp_beta, k_discard):
+    """Σ_m w_m ℓ_m assembled from torch library losses on full rows: F.kl_div with
+    swapped arguments for the reverse KL, F.cross_entropy for NTP, F.kl_div for the
+    dense discard KL; the filtered FKL rows from an explicit top-k softmax."""
+    H = torch.from_numpy(oracle.bf16_bits_to_f64(tr["H_bits"])).requires_grad_(True)
+    W = torch.from_numpy(oracle.bf16_bits_to_f64(tr["W_bits"])).requires_grad_(True)
+    T = torch.from_numpy(oracle.bf16_bits_to_f64(tr["T_bits"]))
+    Z = H @ W.T
+    logq = F.log_softmax(Z, 1)
+    logp = F.log_softmax(T, 1)
+    total = torch.zeros((), dtype=torch.float64)
+    per_row = []
+    for m, c in enumerate(out["row_class"]):
+        if c == PAD:
+            per_row.append(0.0)
+            continue
+        if c == ACCEPT and accept_loss == "rkl":
+            l = F.kl_div(logp[m], logq[m], log_target=True, reduction="sum")
+            l = l + ntp_beta * F.cross_entropy(Z[m:m + 1], torch.tensor([int(out["argmax"][m])]))
+        elif c == DISCARD and k_discard == 0:
+            l = F.kl_div(logq[m], logp[m], log_target=True, reduction="sum")
+        else:
+            k = 1 if c == ACCEPT else k_discard
+            S = torch.from_numpy(np.asarray(out["topk"][m][:k], dtype=np.int64))
+            pt = F.softmax(T[m, S], 0)
+            l = torch.sum(pt * (torch.log(pt) - logq[m, S]))
+        per_row.append(float(l.detach()))
+        total = total + out["w"][m] * l
+    total.backward()
+    return float(total), np.array(per_row), H.grad.numpy(), W.grad.numpy()
+
+
+@pytest.mark.parametrize("accept_loss,ntp_beta,k_discard", [("rkl", 0.0, 10), ("rkl", 0.5, 0), ("fkl", 0.0, 0),
+                                                            ("rkl", 1.0, 3)])
+def test_variants_match_torch_losses_and_autograd(accept_loss, ntp_beta, k_discard):
+    """O6 against torch f64 library losses (kl_div both directions, cross_entropy) and
+    their autograd gradients, row by row, on a tree trace with rejections."""
+    cfg = tracegen.TraceConfig("var", d=24, V=97, R=5, N=6, seed=123, tree=True, beam=2, alpha=(0.6,))
+    tr = tracegen.gen_trace(cfg)
+    out = oracle.step_variants(tr, accept_loss=accept_loss, ntp_beta=ntp_beta, k_discard=k_discard)
+    assert out["counts"][0] > 0 and out["counts"][1] > 0
+    L, rows, gH, gW = _torch_variant_loss(tr, out, accept_loss, ntp_beta, k_discard)
+    np.testing.assert_allclose(out["row_loss"], rows, rtol=1e-10, atol=1e-13)
+    assert abs(out["loss"] - L) <= 1e-10 * abs(L)
+    np.testing.assert_allclose(out["dH"], gH, rtol=1e-9, atol=1e-13)
+    np.testing.assert_allclose(out["dW"], gW, rtol=1e-9, atol=1e-13)
+
+
+def test_variants_fkl_default_equals_step():
+    """accept_loss='fkl', k_discard >= 1 is exactly Eq. 3 as O3-O5 compute it."""
+    tr = tracegen.gen_trace("small_tree")
+    a = oracle.step_variants(tr)
+    b = oracle.step(tr)
+    assert abs(a["loss"] - b["loss"]) <= 1e-12 * abs(b["loss"])
+    np.testing.assert_allclose(a["dW"], b["dW"], rtol=1e-9, atol=1e-15)
+    np.testing.assert_allclose(a["dH"], b["dH"], rtol=1e-9, atol=1e-15)
+
+
+def _hand_trace(Wcol, Trow, R=1, N=1, draft=0):
+    """d = 1, H = 1: z_j = W_j exactly (bf16-representable W), every row's T = Trow."""
+    M = R * (N + 1)
+    W = np.asarray(Wcol, dtype=np.float32).reshape(-1, 1)
+    return dict(T_bits=np.tile(tracegen.f32_to_bf16_bits(np.asarray(Trow, dtype=np.float32)), (M, 1)),
+                H_bits=tracegen.f32_to_bf16_bits(np.ones((M, 1), dtype=np.float32)),
+                W_bits=tracegen.f32_to_bf16_bits(W), draft_tokens=np.full((R, N), draft, dtype=np.int32),
+                parents=None, num_nodes=None)
+
+
+def test_variants_spec_examples():
+    """S:322 'p_target = softmax(draft_logits) -> loss 0, grad 0' (both directions) and
+    S:338 'uniform logits, V=64 -> NTP loss ln 64'."""
+    w = [0.5, -1.0, 2.0, 0.25, 1.5]
+    tr = _hand_trace(w, w, draft=4)             # draft 4 != argmax 2: one rejection
+    out = oracle.step_variants(tr, accept_loss="rkl", k_discard=0)
+    assert set(out["row_class"].tolist()) == {ACCEPT, DISCARD}
+    np.testing.assert_allclose(out["row_loss"], 0.0, atol=1e-12)   # RKL rows and dense-KL rows
+    np.testing.assert_allclose(out["dW"], 0.0, atol=1e-12)
+    tr = _hand_trace(np.zeros(64), np.zeros(64), draft=5)   # argmax of a uniform row is id 0
+    out = oracle.step_variants(tr, accept_loss="rkl", ntp_beta=1.0)
+    assert out["row_class"][0] == ACCEPT
+    assert abs(out["row_loss"][0] - math.log(64)) <= 1e-12
