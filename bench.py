@@ -152,11 +152,15 @@ def run_ours(args):
     draft = torch.from_numpy(tr["draft_tokens"]).to(dev)
     parents = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).to(dev)
     num_nodes = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).to(dev)
-    st = A.SpecTrainStep(R, N, d, V, comm=comm, device=dev, k_accept=args.k_accept, k_discard=args.k_discard)
+    st = A.SpecTrainStep(R, N, d, V, comm=comm, device=dev, k_accept=args.k_accept, k_discard=args.k_discard,
+                         accept_loss=args.accept_loss, ntp_beta=args.ntp_beta)
     if sparse and A.aurora_workspace_size(A.OP_VERIFY, M, d, args.target_topk, st.cfg) > st.ws_bytes:
         raise SystemExit("workspace too small for --target-topk")
     dH = torch.empty(M, d, dtype=torch.float32, device=dev)
     dW = torch.empty(V, d, dtype=torch.float32, device=dev)
+    opt = None
+    if args.optimizer:  # F3: fp32 master lm_head + fused AdamW; the GEMMs read its bf16 copy
+        opt = A.AdamW(W.float().reshape(-1), lr=1e-5, warmup_steps=400)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -167,6 +171,8 @@ def run_ours(args):
             st.backward(H, W, dH, dW)
         else:
             st.step(draft, T, H, W, dH, dW, parents, num_nodes)
+        if opt is not None:
+            opt.step(dW.reshape(-1), W_bf16=W.reshape(-1))
 
     for _ in range(args.warmup):
         step()
@@ -201,7 +207,7 @@ def run_ours(args):
     tokens_per_s = (M * ws) / (ms_step / 1e3)
 
     # ---------------- e2e: public API with pinned host inputs, result read back
-    e2e = None if sparse else _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush)
+    e2e = None if (sparse or opt is not None) else _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush)
 
     if rank != 0:
         if comm is not None:
@@ -228,7 +234,8 @@ def run_ours(args):
         "config": {"workload": cfg.name + (f"+topk{args.target_topk}" if sparse else ""), "R": R, "N": N,
                    "M_rows_per_gpu": M, "d": d, "V": V,
                    "target": f"top-{args.target_topk} (id, logit) pairs per row (F1)" if sparse else "dense bf16 logits",
-                   "k_accept": args.k_accept, "k_discard": args.k_discard,
+                   "k_accept": args.k_accept, "k_discard": args.k_discard, "accept_loss": args.accept_loss,
+                   "ntp_beta": args.ntp_beta, "optimizer": "adamw (F3)" if args.optimizer else None,
                    "tree": cfg.tree, "parallelism": f"dp{ws}" if ws > 1 else "single",
                    "l2": "flushed between timed steps (256 MiB write outside the step events)"},
         "gpu_launches": int(n_launch),
@@ -330,13 +337,15 @@ def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0):
     launch / mean launch time, against whichever roofline bounds it (tensor or HBM)."""
     per = []
     best = None
-    for k in ("fwd_gemm", "bwd_dz_gemm", "bwd_dw_gemm", "bwd_dh_gemm", "bwd_fused"):
+    for k in ("fwd_gemm", "bwd_dz_gemm", "bwd_dw_gemm", "bwd_dh_gemm", "bwd_fused", "adamw"):
         if k not in phases or phases[k][1] == 0:
             continue
         tot_ms, n = phases[k]
         lps = n / steps
         t = (tot_ms / n) / 1e3
-        if k == "bwd_fused":
+        if k == "adamw":  # F3: norm pass 4 B + update 30 B per lm_head element, no flops bound
+            flops, byts = 0.0, 34.0 * cfg.V * cfg.d
+        elif k == "bwd_fused":
             flops, byts = 3 * 2.0 * cfg.M * cfg.V * cfg.d, 4.0 * cfg.V * cfg.d + 4.0 * cfg.V * cfg.d
         else:
             flops, byts = _phase_work(cfg, k, lps)
@@ -359,6 +368,8 @@ def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0):
         out = {"bound": "hbm", "kernel": k, "achieved": rec["achieved_gbs"], "peak": hbm_peak_gbs, "unit": "GB/s",
                "peak_source": f"{peak_src} hbm_gbs (copy)",
                "work_per_launch": "compulsory DRAM bytes per launch (fp32 dW chunk write + dZ^T/H reads, DESIGN.md 6)"}
+    if k == "adamw":
+        out["work_per_launch"] = "34 B per lm_head element (F3: dW norm pass + dW/m/v/W reads, m/v/W fp32 + W bf16 writes)"
     out["frac"] = round(out["achieved"] / out["peak"], 4)
     out["traffic"] = _traffic_for(k)
     out["phases"] = per
@@ -460,7 +471,10 @@ def main():
                     help="NEXT F1: feed the verifier logits as the transmitted top-K payload (e.g. 1024)")
     ap.add_argument("--k-accept", type=int, default=1, help="support size on ACCEPT rows (1 = CE; up to 1024 "
                                                             "with --target-topk: soft distillation)")
-    ap.add_argument("--k-discard", type=int, default=10, help="support size on DISCARD rows (P:520)")
+    ap.add_argument("--k-discard", type=int, default=10, help="support size on DISCARD rows (P:520; 0 = dense KL, F2)")
+    ap.add_argument("--accept-loss", default="fkl", choices=["fkl", "rkl"], help="ACCEPT-row objective (F2)")
+    ap.add_argument("--ntp-beta", type=float, default=0.0, help="NTP auxiliary weight with --accept-loss rkl (F2)")
+    ap.add_argument("--optimizer", action="store_true", help="add the fused AdamW step on the fp32 master lm_head (F3)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -8,8 +8,8 @@
  *   aurora_verify_labels  greedy verification + per-row targets
  *   aurora_spec_loss_fwd  lm_head GEMM + vocab-wide log-softmax + Eq. 3 loss
  *   aurora_spec_loss_bwd  dLogits (tiles only) -> dW_lmhead, dHidden
- * The [M x V] logits are never stored; dLogits exist only as a bounded per-vocab-chunk
- * workspace (at most 1/4 of the local M x V_local, see aurora_workspace_size).
+ * The [M x V] logits are never stored; dLogits exist only as a bf16 per-vocab-chunk
+ * workspace bounded by the "dz_chunk_bytes" option (default 2 GiB; see aurora_set_option).
  *
  * Conventions (all entry points):
  *  - Pointers marked (dev) are CUDA device pointers, (host) are host pointers.  The
@@ -234,11 +234,40 @@ uint64_t aurora_launch_count(void);
  *                    tiles (tcgen05.mma.cta_group::2)
  *   "bwd_mode"       0 per-chunk launches (default), 1 one fused persistent kernel
  *   "bwd_concurrent" 0 (default): serial; 1: dW || dH of a chunk on library side streams
+ *   "dz_chunk_bytes" budget of the bwd's bf16 dZ^T chunk (default 2 GiB: the whole local
+ *                    vocabulary at the bench shapes; smaller -> more chunks).  Options that
+ *                    change workspace sizes must be set before aurora_workspace_size.
  *   "tile_n"         fwd / dz vocab tile width with single-CTA tiles: 0 auto (default:
  *                    the width among 256/224/192 with the least per-SM work for the
  *                    tile count), or force 256, 224 or 192.  Other values: INVALID_ARG. */
 aurora_status_t aurora_set_option(const char* name, int64_t value);
 int64_t aurora_get_option(const char* name);
+
+/* NEXT F3 — the optimizer step on the (vocab-sharded) lm_head, Table 3 P:507-515:
+ * AdamW (decoupled weight decay, default 0.0), global-norm gradient clipping (max norm
+ * 0.5), linear warm-up over warmup_steps then a constant learning rate (S:379:
+ * lr(s) = lr * s / warmup for s < warmup).  "FP32 master weights and gradients cast to
+ * FP32 before optimization": W_master, m, v, dW are fp32; the bf16 copy the
+ * GEMMs read is rewritten from the updated master.
+ *   W_master, m, v (dev) f32 [n], updated in place; W_bf16 (dev, nullable) bf16 [n] out;
+ *   dW (dev) f32 [n]; step >= 1 (bias corrections 1 - beta^step);
+ *   extra_sq (dev, nullable) f32 [1]: sum of squares of the gradients of parameters
+ *   outside this call (they share the global norm); grad_norm (dev, nullable) f32 [1]
+ *   out: the global norm before clipping.  comm: norm^2 is summed over the VP group
+ *   (disjoint vocab shards); DP replicas hold the already-reduced dW (C5).
+ *   n % 4 == 0 and 16-byte aligned pointers.  Deterministic (fixed reduction order). */
+typedef struct {
+  float lr;              /* base learning rate (1e-5 finetune / 1e-4 scratch)  */
+  float beta1, beta2;    /* 0.9, 0.999 (SPEC design decision; paper silent)            */
+  float eps;             /* 1e-8                                                        */
+  float weight_decay;    /* 0.0 (Table 3)                                               */
+  float max_grad_norm;   /* 0.5 (Table 3); <= 0 disables clipping                        */
+  int32_t warmup_steps;  /* 400; 0 = constant from step 1                       */
+} aurora_adamw_cfg_t;
+size_t aurora_adamw_workspace_size(int64_t n);
+aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float* v, const float* dW, int64_t n,
+                                  int64_t step, const aurora_adamw_cfg_t* cfg, const float* extra_sq,
+                                  float* grad_norm, void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream);
 
 /* Per-phase device timing (CUDA events recorded on the caller's stream around each
  * phase while enabled).  aurora_profile_read must be called after the stream was

@@ -31,6 +31,9 @@ step by step in the paper's order (PAPER.md = P, SPEC.md = S, line numbers):
                    discard rows with the unfiltered dense KL(p_target || q) ("top-k =
                    0").  Written directly from those definitions on
                    full-vocabulary rows (no decomposition shared with the kernels).
+  O7 adamw_step    (NEXT F3) one AdamW step (Table 3): global-norm clip at
+                   0.5, linear warm-up over 400 steps then constant, decoupled
+                   weight decay, bias-corrected moments (SPEC: betas 0.9/0.999, eps 1e-8).
 
 Readings where the paper is silent/ambiguous are listed in DESIGN.md
 ("Readings Q1-Q15"); each function names the ones it relies on.
@@ -405,3 +408,33 @@ def step_variants(trace: dict, accept_loss: str = "fkl", ntp_beta: float = 0.0, 
     if want_grads:
         out.update(dH=dH, dW=dW)
     return out
+
+
+# --------------------------------------------------------------------------- O7
+def warmup_lr(lr: float, step: int, warmup_steps: int) -> float:
+    """S:379 'Learning rate at step s < 400 equals base_lr*s/400; afterwards constant' (P:489)."""
+    return lr * step / warmup_steps if (warmup_steps > 0 and step < warmup_steps) else lr
+
+
+def adamw_step(W: np.ndarray, m: np.ndarray, v: np.ndarray, dW: np.ndarray, step: int, lr: float,
+               beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0,
+               max_grad_norm: float = 0.5, warmup_steps: int = 400, extra_sq: float = 0.0):
+    """O7 (NEXT F3): AdamW (Loshchilov & Hutter: decoupled weight decay) with global-norm
+    clipping, in the paper's order (P:487-489): norm = sqrt(sum g^2 (+ other groups));
+    g <- g * min(1, max_norm / (norm + 1e-6)); m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2;
+    W <- W - lr_t (m/(1-b1^t) / (sqrt(v/(1-b2^t)) + eps) + wd W).  f64; returns new arrays
+    and the pre-clip norm."""
+    W = np.asarray(W, dtype=np.float64)
+    m = np.asarray(m, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    g = np.asarray(dW, dtype=np.float64)
+    norm = float(np.sqrt(np.sum(g * g) + extra_sq))
+    clip = min(1.0, max_grad_norm / (norm + 1e-6)) if max_grad_norm > 0 else 1.0
+    g = g * clip
+    lr_t = warmup_lr(lr, step, warmup_steps)
+    m = beta1 * m + (1.0 - beta1) * g
+    v = beta2 * v + (1.0 - beta2) * g * g
+    mhat = m / (1.0 - beta1 ** step)
+    vhat = v / (1.0 - beta2 ** step)
+    W = W - lr_t * (mhat / (np.sqrt(vhat) + eps) + weight_decay * W)
+    return W, m, v, norm

@@ -27,7 +27,7 @@ EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fw
            "aurora_comm_get_unique_id", "aurora_comm_create", "aurora_comm_destroy", "aurora_status_string",
            "aurora_build_info", "aurora_launch_count", "aurora_profile_enable", "aurora_profile_read",
            "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option",
-           "aurora_verify_labels_topk"]
+           "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step"]
 
 
 class AuroraError(RuntimeError):
@@ -61,6 +61,11 @@ class aurora_labels_t(C.Structure):
                 ("counts", C.c_void_p), ("status", C.c_void_p), ("row_lse_t", C.c_void_p), ("row_aux", C.c_void_p),
                 ("target_logits", C.c_void_p), ("ld_target", C.c_int64), ("objective", C.c_int32),
                 ("ntp_beta", C.c_float)]
+
+
+class aurora_adamw_cfg_t(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float), ("max_grad_norm", C.c_float), ("warmup_steps", C.c_int32)]
 
 
 _lib = None
@@ -112,6 +117,10 @@ def lib() -> C.CDLL:
                                             C.POINTER(aurora_labels_t), vp, sz, vp, vp]
     L.aurora_verify_labels_topk.restype = C.c_int
     L.aurora_set_option.argtypes = [C.c_char_p, C.c_int64]
+    L.aurora_adamw_workspace_size.argtypes = [i64]
+    L.aurora_adamw_workspace_size.restype = sz
+    L.aurora_adamw_step.argtypes = [vp, vp, vp, vp, vp, i64, i64, C.POINTER(aurora_adamw_cfg_t), vp, vp, vp, sz, vp,
+                                    vp]
     L.aurora_set_option.restype = C.c_int
     L.aurora_get_option.argtypes = [C.c_char_p]
     L.aurora_get_option.restype = C.c_int64
@@ -180,6 +189,41 @@ def aurora_debug_gemm(a_mn: bool, b_mn: bool, A, B, D, M, N, K, lda, ldb, ldd, s
     _expect(A, "bf16", "A"); _expect(B, "bf16", "B"); _expect(D, "f32", "D")
     _check("aurora_debug_gemm", lib().aurora_debug_gemm(int(a_mn), int(b_mn), _ptr(A), _ptr(B), _ptr(D), M, N, K,
                                                         lda, ldb, ldd, _stream(stream)))
+
+
+def aurora_adamw_step(W_master, W_bf16, m, v, dW, step: int, cfg: aurora_adamw_cfg_t, ws, extra_sq=None,
+                      grad_norm=None, comm=None, stream=None) -> None:
+    """NEXT F3: one fused AdamW step (global-norm clip, warm-up LR) on fp32 master weights."""
+    for t, n in ((W_master, "W_master"), (m, "m"), (v, "v"), (dW, "dW")):
+        _expect(t, "f32", n)
+    _expect(W_bf16, "bf16", "W_bf16")
+    _check("aurora_adamw_step", lib().aurora_adamw_step(
+        _ptr(W_master), _ptr(W_bf16), _ptr(m), _ptr(v), _ptr(dW), W_master.numel(), int(step), C.byref(cfg),
+        _ptr(extra_sq), _ptr(grad_norm), _ptr(ws), ws.numel() if ws is not None else 0, comm, _stream(stream)))
+
+
+class AdamW:
+    """Owns the fp32 moments and workspace of a fused AdamW over one fp32 master tensor
+    (defaults: P:487-489 / Table 3 — lr 1e-5, wd 0.0, clip 0.5, 400 warm-up steps;
+    betas / eps per SPEC's design decision)."""
+
+    def __init__(self, W_master, lr: float = 1e-5, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
+                 max_grad_norm: float = 0.5, warmup_steps: int = 400, comm=None):
+        import torch
+        self.W = W_master
+        self.m = torch.zeros_like(W_master)
+        self.v = torch.zeros_like(W_master)
+        self.cfg = aurora_adamw_cfg_t(lr, betas[0], betas[1], eps, weight_decay, max_grad_norm, warmup_steps)
+        n = int(lib().aurora_adamw_workspace_size(W_master.numel()))
+        self.ws = torch.empty(n, dtype=torch.uint8, device=W_master.device)
+        self.grad_norm = torch.zeros(1, dtype=torch.float32, device=W_master.device)
+        self.step_count = 0
+        self.comm = comm
+
+    def step(self, dW, W_bf16=None, extra_sq=None, stream=None):
+        self.step_count += 1
+        aurora_adamw_step(self.W, W_bf16, self.m, self.v, dW, self.step_count, self.cfg, self.ws, extra_sq,
+                          self.grad_norm, self.comm, stream)
 
 
 def aurora_set_option(name: str, value: int) -> None:

@@ -29,7 +29,7 @@ cudaEvent_t ev_get() {
   return e;
 }
 const char* kPhaseNames[PH_COUNT] = {"target_scan", "verify", "fwd_gemm", "fwd_combine", "bwd_dz_gemm",
-                                     "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm", "bwd_fused"};
+                                     "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm", "bwd_fused", "adamw"};
 }  // namespace
 
 void prof_begin(int phase, cudaStream_t s) {
@@ -131,7 +131,9 @@ struct Options {
   int bwd_concurrent = 0;  // classic mode: dW || dH on side streams (measured equal to serial; off
                            // by default so per-kernel event timings stay clean)
   int tile_n = 0;          // fwd / dz tile width: 0 auto, else 256 / 224 / 192
+  int64_t dz_chunk_bytes = int64_t(2) << 30;  // classic bwd: dZ^T chunk budget (bytes)
   Options() {
+    if (const char* e = getenv("AURORA_DZ_CHUNK_BYTES")) dz_chunk_bytes = atoll(e);
     if (const char* e = getenv("AURORA_TILE_N")) tile_n = atoi(e);
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
@@ -170,11 +172,15 @@ int scan_nseg(int64_t M, int64_t V_local) {
   nseg = std::min<int64_t>(nseg, cdiv(V_local, 2048));
   return static_cast<int>(std::max<int64_t>(nseg, 1));
 }
-// dLogits chunk width: 1/4 of the local vocab (one buffer) => at most 1/4 of the local
-// [M x V_local] dLogits is live at any time.
-int64_t chunk_cols(int64_t V_local) {
-  if (V_local <= 4 * BN) return rup(V_local, BN);
-  return rup(cdiv(V_local, 4), BN);
+// dLogits chunk width.  The bf16 dZ^T of the whole local vocabulary is M x V_local x 2 B
+// (Llama: 98 MB of the 180 GB HBM): keep it whole when it fits the chunk budget (option
+// "dz_chunk_bytes", default 2 GiB) so the bwd is one dz, one dW and one dH launch with no
+// per-chunk wave tails; otherwise the fewest equal chunks that fit (<= 20), rounded to 256.
+int64_t chunk_cols(int64_t V_local, int64_t M) {
+  const int64_t per_col = rup(M, 8) * 2;
+  int64_t n = cdiv(V_local * per_col, std::max<int64_t>(opts().dz_chunk_bytes, per_col * 256));
+  n = std::min<int64_t>(std::max<int64_t>(n, 1), 20);
+  return std::min(rup(cdiv(V_local, n), 256), rup(V_local, 256));
 }
 // split-K factor for dH: the (m, n) tile count is small (M x d output) so pick the
 // split that fills whole waves of 148 SMs best (fewest splits within 3% of the best).
@@ -227,7 +233,7 @@ struct BwdWs { int32_t* counters; __nv_bfloat16* dzT; float* dh_part; int64_t vc
 BwdWs carve_bwd(Carver& c, int64_t M, int64_t d, int64_t V_local) {
   BwdWs w;
   w.counters = c.take<int32_t>(kCounters);
-  w.vc = chunk_cols(V_local);
+  w.vc = chunk_cols(V_local, M);
   w.m_pad = rup(M, 8);
   w.dzT = c.take<__nv_bfloat16>(w.vc * w.m_pad);
   w.splits = dh_splits(M, d, cdiv(w.vc, BK), pair_for(M));
@@ -493,6 +499,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
+  if (std::strcmp(name, "dz_chunk_bytes") == 0 && value >= 1) {
+    o.dz_chunk_bytes = value;
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "tile_n") == 0 && (value == 0 || value == 256 || value == 224 || value == 192)) {
     o.tile_n = static_cast<int>(value);
     return AURORA_OK;
@@ -511,6 +521,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "bwd_mode") == 0) return o.bwd_mode;
   if (std::strcmp(name, "bwd_concurrent") == 0) return o.bwd_concurrent;
   if (std::strcmp(name, "tile_n") == 0) return o.tile_n;
+  if (std::strcmp(name, "dz_chunk_bytes") == 0) return o.dz_chunk_bytes;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
   return -1;
 }
@@ -756,7 +767,10 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   a.p_max = w.pm;
   a.p_sum = w.ps;
   a.p_u = w.pu;
-  if (objective) set_f2_args(a, labels, 0);
+  if (objective) {
+    set_f2_args(a, labels, 0);
+    a.p_r = w.pr;
+  }
   prof_begin(PH_FWD_GEMM, s);
   cudaError_t e = launch_umma_gemm(objective ? EPI_FWD_STATS_T : EPI_FWD_STATS, false, false, tmH, tmW, a, s, nullptr,
                                    pf, bn);
@@ -999,6 +1013,45 @@ aurora_status_t aurora_comm_destroy(aurora_comm_t c) {
   if (c->world) A.CommDestroy(c->world);
   if (c->scratch) cudaFree(c->scratch);
   delete c;
+  return AURORA_OK;
+}
+
+size_t aurora_adamw_workspace_size(int64_t n) {
+  if (n < 1) return 0;
+  return rup(static_cast<int64_t>(adamw_partials() + 64) * 4, 256) + 256;
+}
+
+aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float* v, const float* dW, int64_t n,
+                                  int64_t step, const aurora_adamw_cfg_t* cfg, const float* extra_sq, float* grad_norm,
+                                  void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream) {
+  if (!W_master || !m || !v || !dW || !cfg || n < 4 || n % 4 || step < 1) return AURORA_ERR_INVALID_ARG;
+  if (!al16(W_master) || !al16(m) || !al16(v) || !al16(dW) || (W_bf16 && (reinterpret_cast<uintptr_t>(W_bf16) & 7)))
+    return AURORA_ERR_INVALID_ARG;
+  if (!(cfg->lr >= 0.f) || !(cfg->beta1 >= 0.f && cfg->beta1 < 1.f) || !(cfg->beta2 >= 0.f && cfg->beta2 < 1.f) ||
+      !(cfg->eps > 0.f) || !(cfg->weight_decay >= 0.f) || !std::isfinite(cfg->max_grad_norm) || cfg->warmup_steps < 0)
+    return AURORA_ERR_INVALID_ARG;
+  if (!ws || ws_bytes < aurora_adamw_workspace_size(n)) return AURORA_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  float* norm_sq = c.take<float>(64);
+  float* partials = c.take<float>(adamw_partials());
+  // S:379 / P:489: lr(s) = lr * s / warmup for s < warmup, then constant
+  const double lr_t = (cfg->warmup_steps > 0 && step < cfg->warmup_steps)
+                          ? static_cast<double>(cfg->lr) * static_cast<double>(step) / cfg->warmup_steps
+                          : static_cast<double>(cfg->lr);
+  const double bc1 = 1.0 - std::pow(static_cast<double>(cfg->beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(cfg->beta2), static_cast<double>(step));
+  AdamwScalars sc{cfg->beta1, cfg->beta2, cfg->eps, static_cast<float>(lr_t / bc1),
+                  static_cast<float>(1.0 / std::sqrt(bc2)), static_cast<float>(1.0 - lr_t * cfg->weight_decay),
+                  cfg->max_grad_norm};
+  prof_begin(PH_OPTIM, s);
+  if (launch_sumsq(dW, n, extra_sq, partials, norm_sq, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (comm && comm->vp_x()) {  // disjoint vocab shards: the global norm^2 sums over the VP group
+    auto& A = nccl::api();
+    if (A.AllReduce(norm_sq, norm_sq, 1, nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+  }
+  if (launch_adamw(W_master, W_bf16, m, v, dW, n, norm_sq, grad_norm, sc, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  prof_end(PH_OPTIM, s);
   return AURORA_OK;
 }
 

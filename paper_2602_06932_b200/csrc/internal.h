@@ -173,6 +173,20 @@ cudaError_t launch_debug_dlogits(const __nv_bfloat16* H, const __nv_bfloat16* W,
                                  const float* row_lse, const float* dloss, const int32_t* rows, int n_rows,
                                  float* out, cudaStream_t s);
 
+// ---------------------------------------------------------------- F3 optimizer
+struct AdamwScalars {  // host-computed per step (torch.optim.AdamW formulation)
+  float beta1, beta2, eps;
+  float step_size;     // lr_t / (1 - beta1^t)
+  float inv_sqrt_bc2;  // 1 / sqrt(1 - beta2^t)
+  float decay;         // 1 - lr_t * weight_decay
+  float max_norm;      // <= 0: no clipping
+};
+int adamw_partials();
+cudaError_t launch_sumsq(const float* g, int64_t n, const float* extra_sq, float* partials, float* norm_sq,
+                         cudaStream_t s);
+cudaError_t launch_adamw(float* W, void* Wb, float* m, float* v, const float* g, int64_t n, const float* norm_sq,
+                         float* grad_norm, const AdamwScalars& c, cudaStream_t s);
+
 // ---------------------------------------------------------------- accounting
 extern std::atomic<uint64_t> g_launches;
 extern int g_pair_max_clusters;  // cudaOccupancyMaxActiveClusters of the CTA-pair GEMM (-1: unknown)
@@ -180,7 +194,7 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 
 // Phase profiling (CUDA events on the caller's stream).
 enum Phase : int { PH_SCAN = 0, PH_VERIFY, PH_FWD_GEMM, PH_FWD_COMBINE, PH_BWD_DZ, PH_BWD_DW, PH_BWD_DH,
-                   PH_BWD_REDUCE, PH_COMM, PH_BWD_FUSED, PH_COUNT };
+                   PH_BWD_REDUCE, PH_COMM, PH_BWD_FUSED, PH_OPTIM, PH_COUNT };
 void prof_begin(int phase, cudaStream_t s);
 void prof_end(int phase, cudaStream_t s);
 

@@ -1,9 +1,9 @@
 // k_rows.cu — per-row statistic reductions and small helpers.
 //
-//   k_reduce_partials  warp per row: merge the (m, s, u) partials of all vocab tiles of
+//   k_reduce_partials  CTA per row: merge the (m, s, u, r) partials of all vocab tiles of
 //                      a row (coalesced: partials are [M, n_tiles] row-major) with the
-//                      online rule s = s e^{m-m'} + s_t e^{m_t-m'}; fixed shuffle order
-//                      => deterministic.
+//                      online rule s = s e^{m-m'} + s_t e^{m_t-m'}; fixed strides, shuffle
+//                      tree and warp order => deterministic.
 //   k_row_combine      thread per row: merge the per-rank (m, s, u, r) in rank order (VP),
 //                      lse = m + log s, l = lse - u + H~ = KL(p~ || q) (Eq. 3), w l,
 //                      block-ordered partial sums.  F2 reverse-KL rows (NEXT F2):
@@ -37,15 +37,35 @@ __device__ __forceinline__ void msr_merge(float& m, float& s, float& r, float m2
 }
 }  // namespace
 
-__global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict__ pm, const float* __restrict__ ps,
-                                                         const float* __restrict__ pu, const float* __restrict__ pr,
-                                                         int64_t M, int n_tiles, float* __restrict__ msu) {
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= M) return;
+constexpr int kRedThreads = 128;
+// CTA per row: each thread merges a fixed strided subset of the row's partials with four
+// independent loads in flight (the chain is latency-bound, not bandwidth-bound), then a
+// fixed shuffle tree and the warps in order => deterministic.
+__global__ void __launch_bounds__(kRedThreads) k_reduce_partials(const float* __restrict__ pm,
+                                                                 const float* __restrict__ ps,
+                                                                 const float* __restrict__ pu,
+                                                                 const float* __restrict__ pr, int64_t M, int n_tiles,
+                                                                 float* __restrict__ msu) {
+  const int64_t row = blockIdx.x;
   float m = -INFINITY, s = 0.f, u = 0.f, r = 0.f;
   const int64_t o = row * n_tiles;
-  for (int t = lane; t < n_tiles; t += 32) {
+  int t = threadIdx.x;
+  for (; t + 3 * kRedThreads < n_tiles; t += 4 * kRedThreads) {
+    float mm[4], ss[4], uu[4], rr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      mm[i] = __ldg(pm + o + t + i * kRedThreads);
+      ss[i] = __ldg(ps + o + t + i * kRedThreads);
+      uu[i] = __ldg(pu + o + t + i * kRedThreads);
+      rr[i] = pr ? __ldg(pr + o + t + i * kRedThreads) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      msr_merge(m, s, r, mm[i], ss[i], rr[i]);
+      u += uu[i];
+    }
+  }
+  for (; t < n_tiles; t += kRedThreads) {
     msr_merge(m, s, r, __ldg(pm + o + t), __ldg(ps + o + t), pr ? __ldg(pr + o + t) : 0.f);
     u += __ldg(pu + o + t);
   }
@@ -58,7 +78,16 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const float* __restrict
     msr_merge(m, s, r, m2, s2, r2);
     u += u2;
   }
-  if (lane == 0) {
+  __shared__ float red[4][kRedThreads / 32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { red[0][w] = m; red[1][w] = s; red[2][w] = u; red[3][w] = r; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    m = red[0][0]; s = red[1][0]; u = red[2][0]; r = red[3][0];
+    for (int i = 1; i < kRedThreads / 32; ++i) {
+      msr_merge(m, s, r, red[0][i], red[1][i], red[3][i]);
+      u += red[2][i];
+    }
     msu[row * kMsu + 0] = m;
     msu[row * kMsu + 1] = s;
     msu[row * kMsu + 2] = u;
@@ -156,7 +185,7 @@ __global__ void k_debug_dlogits(const __nv_bfloat16* __restrict__ H, const __nv_
 
 cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, const float* pr, int64_t M,
                                    int n_tiles, float* msu, cudaStream_t s) {
-  k_reduce_partials<<<static_cast<unsigned>((M + 7) / 8), 256, 0, s>>>(pm, ps, pu, pr, M, n_tiles, msu);
+  k_reduce_partials<<<static_cast<unsigned>(M), kRedThreads, 0, s>>>(pm, ps, pu, pr, M, n_tiles, msu);
   count_launch();
   return cudaGetLastError();
 }

@@ -44,9 +44,15 @@ def test_workspace_size_monotone(L):
     big = A.aurora_workspace_size(A.OP_ALL, 384, 4096, 128256, cfg)
     assert 0 < small < big
     assert A.aurora_workspace_size(A.OP_ALL, 0, 64, 1000, cfg) == 0
-    # bwd dLogits chunk never exceeds a quarter of the local [M x V] (+ alignment)
-    bwd = A.aurora_workspace_size(A.OP_BWD, 384, 4096, 128256, cfg)
-    assert bwd < 384 * 128256 * 2 / 4 + 8 * 384 * 4096 * 4 + (1 << 20)
+    # bwd dLogits chunk never exceeds the dz_chunk_bytes budget (+ split-K partials, alignment)
+    saved = A.aurora_get_option("dz_chunk_bytes")
+    try:
+        for budget in (1 << 31, 16 << 20):
+            A.aurora_set_option("dz_chunk_bytes", budget)
+            bwd = A.aurora_workspace_size(A.OP_BWD, 384, 4096, 128256, cfg)
+            assert bwd < min(budget, 384 * 128256 * 2) + 256 * 384 * 2 + 8 * 384 * 4096 * 4 + (1 << 20)
+    finally:
+        A.aurora_set_option("dz_chunk_bytes", saved)
 
 
 def test_host_validation_without_gpu(L):
@@ -94,7 +100,8 @@ def test_no_cpu_fallback_in_product():
 def test_options_validate_host_side(L):
     """Execution options are host state: valid values round-trip, invalid ones are rejected."""
     for name, good, bad in [("gemm_pair", (0, 1, 2), (3, -1)), ("bwd_mode", (0, 1), (2,)),
-                            ("bwd_concurrent", (0, 1), (2,)), ("tile_n", (0, 256, 224, 192), (128, 200, 512))]:
+                            ("bwd_concurrent", (0, 1), (2,)), ("tile_n", (0, 256, 224, 192), (128, 200, 512)),
+                            ("dz_chunk_bytes", (1 << 20, 1 << 31), (0, -5))]:
         saved = A.aurora_get_option(name)
         try:
             for v in good:

@@ -1,0 +1,74 @@
+"""GPU parity of the NEXT F3 optimizer step (aurora_adamw_step) vs the f64 oracle O7.
+
+fp32 arithmetic against f64: the update of one element is a handful of fp32 operations,
+so W, m, v agree to a few fp32 ulps; the norm is an fp32 sum of n squares (relative
+error ~1e-6 at these sizes).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import tracegen
+from paper_2602_06932_b200 import aurora as A
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    A.lib()
+
+
+def _bf16_rne(x32: np.ndarray) -> np.ndarray:
+    return tracegen.f32_to_bf16_bits(x32)
+
+
+def _f32(x: float) -> float:
+    """The C-ABI takes fp32 hyperparameters (0.999f = 0.99900001...); the oracle gets the
+    value the library actually received."""
+    return float(np.float32(x))
+
+
+HP = dict(beta1=_f32(0.9), beta2=_f32(0.999), eps=_f32(1e-8))
+
+
+@pytest.mark.parametrize("n,grad_scale,wd,warmup", [(4 * 100003, 1e-3, 0.0, 400), (4096 * 257, 1e-6, 0.01, 3),
+                                                     (1 << 22, 1e-2, 0.0, 0)])
+def test_adamw_parity(n, grad_scale, wd, warmup):
+    inp = tracegen.gen_adamw_inputs(n, steps=3, grad_scale=grad_scale)
+    W = torch.from_numpy(inp["W"].copy()).cuda()
+    Wb = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    opt = A.AdamW(W, lr=1e-4, weight_decay=wd, warmup_steps=warmup)
+    Wr, mr, vr = inp["W"].astype(np.float64), np.zeros(n), np.zeros(n)
+    for step, g in enumerate(inp["G"], start=1):
+        opt.step(torch.from_numpy(g).cuda(), W_bf16=Wb)
+        Wr, mr, vr, norm = oracle.adamw_step(Wr, mr, vr, g, step, _f32(1e-4), weight_decay=_f32(wd),
+                                             max_grad_norm=0.5, warmup_steps=warmup, **HP)
+        torch.cuda.synchronize()
+        assert abs(float(opt.grad_norm.item()) - norm) <= 2e-5 * norm
+        np.testing.assert_allclose(W.cpu().numpy(), Wr, rtol=2e-6, atol=1e-9)
+        # m, v: sums of two fp32 terms that can cancel -> a few fp32 ulps of the operand scale
+        np.testing.assert_allclose(opt.m.cpu().numpy(), mr, rtol=1e-5, atol=4e-7 * np.abs(mr).max())
+        np.testing.assert_allclose(opt.v.cpu().numpy(), vr, rtol=1e-5, atol=4e-7 * np.abs(vr).max())
+    # the bf16 copy is the RNE rounding of the fp32 master
+    np.testing.assert_array_equal(Wb.view(torch.int16).cpu().numpy().view(np.uint16), _bf16_rne(W.cpu().numpy()))
+
+
+def test_adamw_extra_sq_and_validation():
+    n = 4096
+    inp = tracegen.gen_adamw_inputs(n, steps=1, grad_scale=1e-2)
+    W = torch.from_numpy(inp["W"].copy()).cuda()
+    opt = A.AdamW(W, lr=1e-3, warmup_steps=0)
+    extra = torch.tensor([3.0], device="cuda")
+    opt.step(torch.from_numpy(inp["G"][0]).cuda(), extra_sq=extra)
+    Wr, _, _, norm = oracle.adamw_step(inp["W"], np.zeros(n), np.zeros(n), inp["G"][0], 1, _f32(1e-3), warmup_steps=0,
+                                       extra_sq=3.0, **HP)
+    torch.cuda.synchronize()
+    assert abs(float(opt.grad_norm.item()) - norm) <= 1e-5 * norm
+    np.testing.assert_allclose(W.cpu().numpy(), Wr, rtol=2e-6, atol=1e-9)
+    with pytest.raises(Exception):  # n % 4 != 0
+        A.aurora_adamw_step(W[:4093], None, opt.m[:4093], opt.v[:4093], torch.zeros(4093, device="cuda"), 1, opt.cfg,
+                            opt.ws)

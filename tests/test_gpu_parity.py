@@ -562,3 +562,14 @@ def test_f2_objectives_other_launch_configs(option, opt):
         option(k, v)
     _check_f2("mid", F2_VARIANTS[1])
     _check_f2("small_tree", F2_VARIANTS[3])
+
+
+@pytest.mark.parametrize("budget", [64 << 10, 700 << 10])
+@pytest.mark.parametrize("name", ["small", "small_tree", "mid"])
+def test_parity_multi_chunk_bwd(option, name, budget):
+    """A small dz_chunk_bytes budget splits the backward into several dZ^T vocab chunks
+    (the default keeps the whole local vocabulary in one): dH accumulates over chunks,
+    each dW chunk lands at its own rows."""
+    option("dz_chunk_bytes", budget)
+    test_full_parity_small(name)
+    _check_f2(name, F2_VARIANTS[1])

@@ -610,3 +610,36 @@ def test_variants_spec_examples():
     out = oracle.step_variants(tr, accept_loss="rkl", ntp_beta=1.0)
     assert out["row_class"][0] == ACCEPT
     assert abs(out["row_loss"][0] - math.log(64)) <= 1e-12
+
+
+# ----------------------------------------------------------------------- O7 AdamW (F3)
+def test_warmup_schedule_spec_statement():
+    """lr(s) = base * s / 400 for s < 400, then constant."""
+    for s_, want in [(1, 1e-4 / 400), (200, 0.5e-4), (399, 1e-4 * 399 / 400), (400, 1e-4), (5000, 1e-4)]:
+        assert abs(oracle.warmup_lr(1e-4, s_, 400) - want) <= 1e-18
+
+
+@pytest.mark.parametrize("wd,max_norm,scale", [(0.0, 0.5, 1.0), (0.01, 0.5, 1e-4), (0.0, 0.0, 1.0)])
+def test_adamw_matches_torch_optim(wd, max_norm, scale):
+    """O7 over 6 steps against torch.optim.AdamW (f64) + clip_grad_norm_ with the same
+    per-step learning rate; clipping active (scale 1), inactive (1e-4) and disabled."""
+    rng = np.random.default_rng(17)
+    n = 1000
+    W0 = rng.standard_normal(n)
+    Wt = torch.tensor(W0.copy(), requires_grad=True)
+    opt = torch.optim.AdamW([Wt], lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=wd)
+    W, m, v = W0.copy(), np.zeros(n), np.zeros(n)
+    for step in range(1, 7):
+        g = rng.standard_normal(n) * scale
+        W, m, v, norm = oracle.adamw_step(W, m, v, g, step, 1e-3, weight_decay=wd, max_grad_norm=max_norm,
+                                          warmup_steps=4)
+        Wt.grad = torch.tensor(g)
+        if max_norm > 0:
+            tn = torch.nn.utils.clip_grad_norm_([Wt], max_norm)
+            assert abs(float(tn) - norm) <= 1e-12 * norm
+        opt.param_groups[0]["lr"] = oracle.warmup_lr(1e-3, step, 4)
+        opt.step()
+        np.testing.assert_allclose(W, Wt.detach().numpy(), rtol=1e-12, atol=1e-15)
+        st = opt.state[Wt]
+        np.testing.assert_allclose(m, st["exp_avg"].numpy(), rtol=1e-12, atol=1e-18)
+        np.testing.assert_allclose(v, st["exp_avg_sq"].numpy(), rtol=1e-12, atol=1e-20)

@@ -263,3 +263,12 @@ def gen_trace_topk(cfg: TraceConfig | str, K_t: int = 1024, seed: Optional[int] 
     tr["Tk_bits"] = vals
     tr["K_t"] = K_t
     return tr
+
+
+def gen_adamw_inputs(n: int, steps: int, seed: int = 4242, grad_scale: float = 1e-3) -> dict:
+    """NEXT F3 inputs: fp32 master weights (the lm_head init of gen_trace, N(0, (2/sqrt d)^2)
+    with d = 4096) and `steps` fp32 gradients ~ N(0, grad_scale^2).  Draws only."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    W = (rng.standard_normal(n, dtype=np.float32) * np.float32(2.0 / 64.0)).astype(np.float32)
+    G = [(rng.standard_normal(n, dtype=np.float32) * np.float32(grad_scale)).astype(np.float32) for _ in range(steps)]
+    return dict(W=W, G=G)
