@@ -275,6 +275,10 @@ aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float
  * the number of phases, then clears the accumulators. */
 void aurora_profile_enable(int enable);
 int aurora_profile_read(const char** names, float* total_ms, int32_t* count, int max);
+/* As aurora_profile_read but keeps the recorded events: phases captured into a CUDA graph
+ * (recorded there as external event nodes) are re-timed by every replay; peek after each
+ * replay returns that replay's per-phase times. */
+int aurora_profile_peek(const char** names, float* total_ms, int32_t* count, int max);
 
 /* ---- Test hooks (not on the hot path) ------------------------------------ */
 /* D[M,N] (dev f32, ld ldd) = sum_k A(m,k) B(n,k) on the tcgen05 GEMM engine.

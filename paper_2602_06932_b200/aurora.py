@@ -27,7 +27,8 @@ EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fw
            "aurora_comm_get_unique_id", "aurora_comm_create", "aurora_comm_destroy", "aurora_status_string",
            "aurora_build_info", "aurora_launch_count", "aurora_profile_enable", "aurora_profile_read",
            "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option",
-           "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step"]
+           "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step",
+           "aurora_profile_peek"]
 
 
 class AuroraError(RuntimeError):
@@ -108,6 +109,8 @@ def lib() -> C.CDLL:
     L.aurora_profile_enable.restype = None
     L.aurora_profile_read.argtypes = [C.POINTER(C.c_char_p), C.POINTER(C.c_float), C.POINTER(C.c_int32), C.c_int]
     L.aurora_profile_read.restype = C.c_int
+    L.aurora_profile_peek.argtypes = [C.POINTER(C.c_char_p), C.POINTER(C.c_float), C.POINTER(C.c_int32), C.c_int]
+    L.aurora_profile_peek.restype = C.c_int
     L.aurora_debug_gemm.argtypes = [C.c_int, C.c_int, vp, vp, vp, i64, i64, i64, i64, i64, i64, vp]
     L.aurora_debug_gemm.restype = C.c_int
     L.aurora_debug_dlogits_rows.argtypes = [vp, vp, i64, i64, i64, i64, C.POINTER(aurora_labels_t), vp, vp, vp,
@@ -246,12 +249,15 @@ def aurora_profile_enable(on: bool) -> None:
     lib().aurora_profile_enable(1 if on else 0)
 
 
-def aurora_profile_read() -> dict:
+def aurora_profile_read(peek: bool = False) -> dict:
+    """Per-phase (total ms, launches) since the last read; peek=True keeps the events (a
+    captured CUDA graph re-times them on every replay)."""
     n = 16
     names = (C.c_char_p * n)()
     ms = (C.c_float * n)()
     cnt = (C.c_int32 * n)()
-    k = lib().aurora_profile_read(names, ms, cnt, n)
+    fn = lib().aurora_profile_peek if peek else lib().aurora_profile_read
+    k = fn(names, ms, cnt, n)
     return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(k)}
 
 

@@ -32,11 +32,20 @@ const char* kPhaseNames[PH_COUNT] = {"target_scan", "verify", "fwd_gemm", "fwd_c
                                      "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm", "bwd_fused", "adamw"};
 }  // namespace
 
+// Inside a CUDA-graph capture the phase events become external event-record nodes, so
+// every replay re-records them and they stay readable (aurora_profile_peek).
+void prof_record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
 void prof_begin(int phase, cudaStream_t s) {
   if (!g_prof_on) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   ProfRec r{phase, ev_get(), ev_get()};
-  cudaEventRecord(r.a, s);
+  prof_record(r.a, s);
   g_prof_open.push_back(r);
 }
 void prof_end(int phase, cudaStream_t s) {
@@ -44,7 +53,7 @@ void prof_end(int phase, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   for (size_t i = g_prof_open.size(); i-- > 0;) {
     if (g_prof_open[i].phase == phase) {
-      cudaEventRecord(g_prof_open[i].b, s);
+      prof_record(g_prof_open[i].b, s);
       g_prof_done.push_back(g_prof_open[i]);
       g_prof_open.erase(g_prof_open.begin() + static_cast<long>(i));
       return;
@@ -132,7 +141,9 @@ struct Options {
                            // by default so per-kernel event timings stay clean)
   int tile_n = 0;          // fwd / dz tile width: 0 auto, else 256 / 224 / 192
   int64_t dz_chunk_bytes = int64_t(2) << 30;  // classic bwd: dZ^T chunk budget (bytes)
+  int scan_ctas = 2;                           // target-scan CTAs per SM (segments per row)
   Options() {
+    if (const char* e = getenv("AURORA_SCAN_CTAS")) scan_ctas = std::max(1, atoi(e));
     if (const char* e = getenv("AURORA_DZ_CHUNK_BYTES")) dz_chunk_bytes = atoll(e);
     if (const char* e = getenv("AURORA_TILE_N")) tile_n = atoi(e);
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
@@ -151,23 +162,32 @@ int pair_for(int64_t rows) {
   return (rows % 256 == 0 || rows >= 4096) ? 2 : 1;
 }
 // Tile width for the K-major fwd / dz GEMMs (single-CTA tiles only).  A persistent CTA
-// does ceil(tiles / 148) tiles, each costing ~width: pick the width with the least
-// per-SM work, 256 unless a narrower one is >= 2% better.
+// does ceil(tiles / 148) tiles, each costing ~(width + a fixed per-tile overhead, measured
+// ~160 columns' worth: operand refill of A, epilogue tail): pick the width with the least
+// per-SM cost, 256 unless a narrower one is >= 2% better.  (M = 384, one 32K-column chunk:
+// 224 wins, 2.55 -> 2.92 waves; the whole 128K vocabulary at once: 256 wins.)
 constexpr int kTileWidths[3] = {256, 224, 192};
 constexpr int kMinBN = 192;
+constexpr int kTileOverheadCols = 160;
 int kmajor_bn(int64_t m_tiles, int64_t N, int pair) {
   if (pair != 1) return BN;
   if (opts().tile_n) return opts().tile_n;
+  auto cost = [&](int bn) {
+    return static_cast<double>(cdiv(m_tiles * cdiv(N, bn), kNumSMs)) * (bn + kTileOverheadCols);
+  };
   int best = BN;
-  double best_cost = static_cast<double>(cdiv(m_tiles * cdiv(N, BN), kNumSMs)) * BN;
+  double best_cost = cost(BN);
   for (int bn : kTileWidths) {
-    const double cost = static_cast<double>(cdiv(m_tiles * cdiv(N, bn), kNumSMs)) * bn;
-    if (cost < 0.98 * best_cost) { best = bn; best_cost = cost; }
+    const double c = cost(bn);
+    if (c < 0.98 * best_cost) { best = bn; best_cost = c; }
   }
   return best;
 }
+// Scan segments per row: enough (row, segment) CTAs for `scan_ctas` per SM; long segments
+// amortise the per-CTA warm start and list merge (measured: 32K-column segments spent most
+// of their instructions there).
 int scan_nseg(int64_t M, int64_t V_local) {
-  int64_t nseg = cdiv(8 * kNumSMs, std::max<int64_t>(M, 1));
+  int64_t nseg = cdiv(static_cast<int64_t>(opts().scan_ctas) * kNumSMs, std::max<int64_t>(M, 1));
   nseg = std::min<int64_t>(nseg, 32);
   nseg = std::min<int64_t>(nseg, cdiv(V_local, 2048));
   return static_cast<int>(std::max<int64_t>(nseg, 1));
@@ -488,8 +508,9 @@ const char* aurora_status_string(aurora_status_t s) {
 }
 
 const char* aurora_build_info(void) {
-  return "libaurora abi=1 target=sm_100a engine=tcgen05.mma.cta_group::1.kind::f16 M128xN256xK16, TMA SW128 "
-         "4-stage ring, TMEM 2x256 cols; scan=16B ld.global.nc 8-deep";
+  return "libaurora abi=2 target=sm_100a engine=tcgen05.mma cta_group::1 M128xN{256,224,192}xK16 / cta_group::2 "
+         "M256xN256, TMA SW128 4/6-stage ring, TMEM 2x256 cols, TMA bulk-store epilogue; scan=16B ld.global.nc; "
+         "objectives: Eq.3 FKL, F1 sparse top-K (k<=1024), F2 RKL+NTP / dense KL; F3 fused AdamW";
 }
 
 uint64_t aurora_launch_count(void) { return g_launches.load(); }
@@ -499,6 +520,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
+  if (std::strcmp(name, "scan_ctas") == 0 && value >= 1 && value <= 16) {
+    o.scan_ctas = static_cast<int>(value);
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "dz_chunk_bytes") == 0 && value >= 1) {
     o.dz_chunk_bytes = value;
     return AURORA_OK;
@@ -522,6 +547,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "bwd_concurrent") == 0) return o.bwd_concurrent;
   if (std::strcmp(name, "tile_n") == 0) return o.tile_n;
   if (std::strcmp(name, "dz_chunk_bytes") == 0) return o.dz_chunk_bytes;
+  if (std::strcmp(name, "scan_ctas") == 0) return o.scan_ctas;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
   return -1;
 }
@@ -531,7 +557,8 @@ void aurora_profile_enable(int enable) {
   g_prof_on = enable != 0;
 }
 
-int aurora_profile_read(const char** names, float* total_ms, int32_t* count, int max) {
+namespace {
+int profile_collect(const char** names, float* total_ms, int32_t* count, int max, bool recycle) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   float tot[PH_COUNT] = {0};
   int cnt[PH_COUNT] = {0};
@@ -541,10 +568,12 @@ int aurora_profile_read(const char** names, float* total_ms, int32_t* count, int
       tot[r.phase] += ms;
       cnt[r.phase] += 1;
     }
-    g_ev_pool.push_back(r.a);
-    g_ev_pool.push_back(r.b);
+    if (recycle) {
+      g_ev_pool.push_back(r.a);
+      g_ev_pool.push_back(r.b);
+    }
   }
-  g_prof_done.clear();
+  if (recycle) g_prof_done.clear();
   int n = 0;
   for (int p = 0; p < PH_COUNT && n < max; ++p) {
     if (names) names[n] = kPhaseNames[p];
@@ -553,6 +582,15 @@ int aurora_profile_read(const char** names, float* total_ms, int32_t* count, int
     ++n;
   }
   return n;
+}
+}  // namespace
+
+int aurora_profile_read(const char** names, float* total_ms, int32_t* count, int max) {
+  return profile_collect(names, total_ms, count, max, true);
+}
+
+int aurora_profile_peek(const char** names, float* total_ms, int32_t* count, int max) {
+  return profile_collect(names, total_ms, count, max, false);
 }
 
 size_t aurora_workspace_size(int op, int64_t M, int64_t d, int64_t V_local, const aurora_loss_cfg_t* cfg) {
@@ -657,7 +695,11 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
     if ((e = launch_topk_merge(p, gv, gi, comm->vp_size, k_max, static_cast<int64_t>(M) * k_max, s)) != cudaSuccess)
       return AURORA_ERR_CUDA;
   }
-  if (objective && (e = launch_row_lse_t(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (objective) {  // F2: row statistics of T (a second read of T, so it counts as scan time)
+    prof_begin(PH_SCAN, s);
+    if ((e = launch_row_lse_t(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+    prof_end(PH_SCAN, s);
+  }
   prof_begin(PH_VERIFY, s);
   if ((e = launch_verify(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->dp_x()) {

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(T + c0) & 15) == 0);
   const int64_t nvec = aligned ? (c1 - c0) >> 3 : 0;
   const uint4* src = reinterpret_cast<const uint4*>(T + c0);
-  constexpr int U = 4;
+  constexpr int U = 8;  // 16 B loads in flight per lane
   // vectors are interleaved: warp w handles [w*32 + i*256, +32) for i = 0, 1, ...
   int64_t base = static_cast<int64_t>(warp) * 32;
   {
@@ -432,9 +432,11 @@ __global__ void __launch_bounds__(256) k_verify(VerifyLaunch p) {
 }
 
 // --------------------------------------------------------------------------- A4 finalize
-// thread per row.
+// warp per row: lane j holds support entry j (k <= 16 <= 32); sums over a fixed xor tree
+// (deterministic); the index-sorted order is each entry's rank among the row's ids.
 __global__ void __launch_bounds__(256) k_finalize(VerifyLaunch p) {
-  const int64_t m = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  const int64_t m = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (m >= p.M) return;
   const int km = p.k_max;
   const uint8_t cls = p.lab.row_class[m];
@@ -456,48 +458,43 @@ __global__ void __launch_bounds__(256) k_finalize(VerifyLaunch p) {
   const bool f2_dense = cls == AURORA_ROW_DISCARD && p.cfg.k_discard == 0;
   if (f2_rkl || f2_dense) {
     const bool one = f2_rkl && p.cfg.ntp_beta > 0.f;
-    for (int j = 0; j < km; ++j) {
+    for (int j = lane; j < km; j += 32) {
       p.lab.sup_idx[m * km + j] = (one && j == 0) ? p.top_idx[m * km] : INT32_MAX;
       p.lab.sup_p[m * km + j] = (one && j == 0) ? p.cfg.ntp_beta : 0.f;
     }
-    p.lab.row_H[m] = f2_dense ? p.ept[m] - p.lab.row_lse_t[m] : 0.f;
-    p.lab.row_w[m] = w;
+    if (lane == 0) {
+      p.lab.row_H[m] = f2_dense ? p.ept[m] - p.lab.row_lse_t[m] : 0.f;
+      p.lab.row_w[m] = w;
+    }
     return;
   }
-  float v[KM];
-  int32_t ix[KM];
-  const float* tv = p.top_val + m * km;
-  const int32_t* ti = p.top_idx + m * km;
-  float esum = 0.f;
-  const float t0 = k > 0 ? tv[0] : 0.f;
-  for (int j = 0; j < k; ++j) {
-    v[j] = tv[j] - t0;  // <= 0
-    ix[j] = ti[j];
-    esum += expf(v[j]);
+  const bool in = lane < k;
+  const float v = in ? p.top_val[m * km + lane] : -INFINITY;
+  const int32_t ix = in ? p.top_idx[m * km + lane] : INT32_MAX;
+  const float t0 = __shfl_sync(0xffffffffu, v, 0);  // the row's largest (value-ordered list)
+  float e = in ? expf(v - t0) : 0.f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  const float lz = logf(e);
+  const float lp = v - t0 - lz;
+  const float pj = in ? expf(lp) : 0.f;
+  float h = in ? pj * lp : 0.f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  int rank = 0;  // position in the index-sorted support (ids are distinct)
+  for (int i = 0; i < k; ++i) rank += (__shfl_sync(0xffffffffu, ix, i) < ix) ? 1 : 0;
+  if (in) {
+    p.lab.sup_idx[m * km + rank] = ix;
+    p.lab.sup_p[m * km + rank] = pj;
   }
-  const float lz = logf(esum);
-  float H = 0.f;
-  for (int j = 0; j < k; ++j) {
-    const float lp = v[j] - lz;
-    v[j] = expf(lp);  // p~
-    H += v[j] * lp;
+  for (int j = k + lane; j < km; j += 32) {
+    p.lab.sup_idx[m * km + j] = INT32_MAX;
+    p.lab.sup_p[m * km + j] = 0.f;
   }
-  if (k == 1) H = 0.f;
-  // sort support by global index (insertion sort, k <= 16)
-  for (int a = 1; a < k; ++a) {
-    const float pv = v[a];
-    const int32_t pi = ix[a];
-    int b = a - 1;
-    while (b >= 0 && ix[b] > pi) { v[b + 1] = v[b]; ix[b + 1] = ix[b]; --b; }
-    v[b + 1] = pv;
-    ix[b + 1] = pi;
+  if (lane == 0) {
+    p.lab.row_H[m] = k <= 1 ? 0.f : h;
+    p.lab.row_w[m] = w;
   }
-  for (int j = 0; j < km; ++j) {
-    p.lab.sup_idx[m * km + j] = j < k ? ix[j] : INT32_MAX;
-    p.lab.sup_p[m * km + j] = j < k ? v[j] : 0.f;
-  }
-  p.lab.row_H[m] = H;
-  p.lab.row_w[m] = w;
 }
 
 // --------------------------------------------------------------------------- F1 long supports
@@ -743,7 +740,7 @@ cudaError_t launch_verify(const VerifyLaunch& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 cudaError_t launch_finalize(const VerifyLaunch& p, cudaStream_t s) {
-  k_finalize<<<(p.M + 255) / 256, 256, 0, s>>>(p);
+  k_finalize<<<(p.M + 7) / 8, 256, 0, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }
