@@ -251,7 +251,7 @@ def run_ours(args):
     tokens_per_s = (M * ws) / (ms_step / 1e3)
 
     # ---------------- e2e: public API with pinned host inputs, result read back
-    e2e = None if (sparse or opt is not None) else _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush)
+    e2e = None if opt is not None else _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush, sparse)
 
     if rank != 0:
         if comm is not None:
@@ -301,14 +301,16 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush):
-    """Same step through the public API (SpecTrainStep), with the trace batch (T, H,
-    draft tokens, parents, ragged counts) copied H2D from pinned host memory every
-    step and the step's result (loss, accept lengths) read back D2H.  The copy of
-    step i+1 runs on a second stream into the other half of a double buffer while
-    step i computes — all of it inside the timed region."""
+def _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush, sparse=False):
+    """Same step through the public API (SpecTrainStep), with the trace batch (T -- or,
+    sparse, the top-K (id, logit) payload the paper transmits, P:391-392 --, H, draft
+    tokens, parents, ragged counts) copied H2D from pinned host memory every step and the
+    step's result (loss, accept lengths) read back D2H.  The copy of step i+1 runs on a
+    second stream into the other half of a double buffer while step i computes -- all of
+    it inside the timed region."""
+    keys = ("Tk_idx", "Tk_bits") if sparse else ("T_bits",)
     hostb = {k: torch.from_numpy(np.ascontiguousarray(tr[k]).view(np.int16 if k.endswith("bits") else np.int32))
-             .pin_memory() for k in ("T_bits", "H_bits", "draft_tokens", "parents", "num_nodes")
+             .pin_memory() for k in keys + ("H_bits", "draft_tokens", "parents", "num_nodes")
              if tr[k] is not None}
     bufs = [{k: torch.empty(v.shape, dtype=v.dtype, device=dev) for k, v in hostb.items()} for _ in range(2)]
     outs = [(torch.empty(1, dtype=torch.float32).pin_memory(), torch.empty(st.R, dtype=torch.int32).pin_memory())
@@ -334,8 +336,14 @@ def _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush):
                 copied[b].record(copy)
             comp.wait_event(copied[b])
             B = bufs[b]
-            st.step(B["draft_tokens"], as_bf16(B["T_bits"]), as_bf16(B["H_bits"]), W, dH, dW,
-                    B.get("parents"), B.get("num_nodes"))
+            if sparse:
+                st.verify_topk(B["draft_tokens"], B["Tk_idx"], as_bf16(B["Tk_bits"]), B.get("parents"),
+                               B.get("num_nodes"))
+                st.forward(as_bf16(B["H_bits"]), W)
+                st.backward(as_bf16(B["H_bits"]), W, dH, dW)
+            else:
+                st.step(B["draft_tokens"], as_bf16(B["T_bits"]), as_bf16(B["H_bits"]), W, dH, dW,
+                        B.get("parents"), B.get("num_nodes"))
             consumed[b].record(comp)
             outs[b][0].copy_(st.loss, non_blocking=True)
             outs[b][1].copy_(st.accept_len, non_blocking=True)

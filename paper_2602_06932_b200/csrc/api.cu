@@ -142,7 +142,9 @@ struct Options {
   int tile_n = 0;          // fwd / dz tile width: 0 auto, else 256 / 224 / 192
   int64_t dz_chunk_bytes = int64_t(2) << 30;  // classic bwd: dZ^T chunk budget (bytes)
   int scan_ctas = 2;                           // target-scan CTAs per SM (segments per row)
+  int dw_resident = 1;                         // dW with K = M <= 512: A-resident pair sweep
   Options() {
+    if (const char* e = getenv("AURORA_DW_RESIDENT")) dw_resident = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_CTAS")) scan_ctas = std::max(1, atoi(e));
     if (const char* e = getenv("AURORA_DZ_CHUNK_BYTES")) dz_chunk_bytes = atoll(e);
     if (const char* e = getenv("AURORA_TILE_N")) tile_n = atoi(e);
@@ -520,6 +522,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
+  if (std::strcmp(name, "dw_resident") == 0 && (value == 0 || value == 1)) {
+    o.dw_resident = static_cast<int>(value);
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "scan_ctas") == 0 && value >= 1 && value <= 16) {
     o.scan_ctas = static_cast<int>(value);
     return AURORA_OK;
@@ -548,6 +554,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "tile_n") == 0) return o.tile_n;
   if (std::strcmp(name, "dz_chunk_bytes") == 0) return o.dz_chunk_bytes;
   if (std::strcmp(name, "scan_ctas") == 0) return o.scan_ctas;
+  if (std::strcmp(name, "dw_resident") == 0) return o.dw_resident;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
   return -1;
 }
@@ -947,7 +954,10 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     CUtensorMap tmOW;
     const bool ow = make_tmap_f32_out(&tmOW, dWf + c0 * d, d, vc, d, 1, 0);
     prof_begin(PH_BWD_DW, sW);
-    e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr, pw);
+    if (pw == 2 && ow && opts().dw_resident && dw_resident_ok(b.kb_total))
+      e = launch_dw_resident(tmZ_k, tmH_mn, tmOW, b, sW);  // small M: dZ^T rows stay in smem
+    else
+      e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr, pw);
     prof_end(PH_BWD_DW, sW);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (comm && comm->dp_x()) {  // C5: DP gradient allreduce of this dW chunk

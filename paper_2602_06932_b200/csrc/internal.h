@@ -81,6 +81,12 @@ cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& t
                              int pair = 1, int bn = BN);
 bool make_tmap_f32_out(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                        uint64_t depth, uint64_t dstride);
+// A8 for K = M <= 512 (k_dw.cu): CTA pairs keep their 128 rows of dZ^T resident and sweep
+// every column tile.  args: m_tiles = 256-row pair blocks, n_tiles, kb_total, N, accumulate;
+// tmA = dZ^T K-major (box 64x128), tmB = H MN-major (box 64x64), tmC = fp32 output map.
+bool dw_resident_ok(int64_t kb_total);
+cudaError_t launch_dw_resident(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                               const GemmArgs& args, cudaStream_t s);
 
 // 2D bf16 tensor map (SWIZZLE_128B) over a row-major [outer, inner] matrix with row
 // stride `ld` elements; box = {box_inner, box_outer}.

@@ -573,3 +573,17 @@ def test_parity_multi_chunk_bwd(option, name, budget):
     option("dz_chunk_bytes", budget)
     test_full_parity_small(name)
     _check_f2(name, F2_VARIANTS[1])
+
+
+@pytest.mark.parametrize("name", ["small", "small_tree", "mid"])
+def test_dw_resident_matches_streamed(option, name):
+    """A8 for K = M <= 512: the A-resident CTA-pair sweep issues the same MMA sequence per
+    tile as the streamed pair kernel, so dW is bit-identical; both match the oracle."""
+    tr = tracegen.gen_trace(name)
+    option("dw_resident", 1)
+    a = _run_gpu(tr)
+    option("dw_resident", 0)
+    b = _run_gpu(tr)
+    assert torch.equal(a["dW"], b["dW"]) and torch.equal(a["dH"], b["dH"])
+    ref = oracle.step(tr)
+    assert _rfro(a["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
