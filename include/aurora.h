@@ -234,8 +234,8 @@ uint64_t aurora_launch_count(void);
  *                    tiles (tcgen05.mma.cta_group::2)
  *   "bwd_mode"       0 per-chunk launches (default), 1 one fused persistent kernel
  *   "bwd_concurrent" 0 (default): serial; 1: dW || dH of a chunk on library side streams
- *   "dw_resident"    1 (default): dW with K = M <= 512 keeps each CTA pair's dZ^T rows in
- *                    shared memory across all column tiles; 0: streamed pair tiles
+ *   "dw_resident"    0 (default): streamed pair tiles for dW; 1: with K = M <= 512 each CTA
+ *                    pair keeps its dZ^T rows in shared memory across all column tiles
  *   "scan_ctas"      target-scan CTAs per SM (row segments), default 2
  *   "dz_chunk_bytes" budget of the bwd's bf16 dZ^T chunk (default 2 GiB: the whole local
  *                    vocabulary at the bench shapes; smaller -> more chunks).  Options that

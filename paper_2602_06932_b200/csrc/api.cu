@@ -142,7 +142,8 @@ struct Options {
   int tile_n = 0;          // fwd / dz tile width: 0 auto, else 256 / 224 / 192
   int64_t dz_chunk_bytes = int64_t(2) << 30;  // classic bwd: dZ^T chunk budget (bytes)
   int scan_ctas = 2;                           // target-scan CTAs per SM (segments per row)
-  int dw_resident = 1;                         // dW with K = M <= 512: A-resident pair sweep
+  int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
+                                               // slower at M = 384: 0.507 vs 0.470 ms; opt-in)
   Options() {
     if (const char* e = getenv("AURORA_DW_RESIDENT")) dw_resident = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_CTAS")) scan_ctas = std::max(1, atoi(e));

@@ -577,8 +577,9 @@ def test_parity_multi_chunk_bwd(option, name, budget):
 
 @pytest.mark.parametrize("name", ["small", "small_tree", "mid"])
 def test_dw_resident_matches_streamed(option, name):
-    """A8 for K = M <= 512: the A-resident CTA-pair sweep issues the same MMA sequence per
-    tile as the streamed pair kernel, so dW is bit-identical; both match the oracle."""
+    """A8 for K = M <= 512: the A-resident CTA-pair sweep (opt-in) issues the same MMA
+    sequence per tile as the streamed pair kernel, so dW is bit-identical; both match the
+    oracle."""
     tr = tracegen.gen_trace(name)
     option("dw_resident", 1)
     a = _run_gpu(tr)
