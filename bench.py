@@ -166,13 +166,21 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     def step():
+        if opt is not None and args.optimizer == "fused":
+            if sparse:
+                st.verify_topk(draft, Tk_idx, Tk_val, parents, num_nodes)
+            else:
+                st.verify(draft, T, parents, num_nodes)
+            st.forward(H, W)
+            st.backward_adamw(H, W, dH, opt)
+            return
         if sparse:
             st.verify_topk(draft, Tk_idx, Tk_val, parents, num_nodes)
             st.forward(H, W)
             st.backward(H, W, dH, dW)
         else:
             st.step(draft, T, H, W, dH, dW, parents, num_nodes)
-        if opt is not None:
+        if opt is not None and args.optimizer == "unfused":
             opt.step(dW.reshape(-1), W_bf16=W.reshape(-1))
 
     for _ in range(args.warmup):
@@ -262,8 +270,10 @@ def run_ours(args):
 
     peak_burst, peak_sus, hbm, peak_src = _peaks()
     # traffic: only for the exact workload the committed ncu capture ran (default objective)
-    plain = not sparse and args.k_accept == 1 and args.k_discard == 10 and args.accept_loss == "fkl"
-    roof = _roofline(phases, cfg, args.steps, peak_sus, peak_src, hbm, workload=cfg.name if plain else None)
+    plain = (not sparse and args.k_accept == 1 and args.k_discard == 10 and args.accept_loss == "fkl"
+             and args.optimizer != "fused")
+    roof = _roofline(phases, cfg, args.steps, peak_sus, peak_src, hbm, workload=cfg.name if plain else None,
+                     optimizer=args.optimizer)
     out = {
         "metric": "speculator-training tokens/s (verify + lm_head fwd/bwd + Eq.3 loss), % bf16 tensor peak",
         "value": round(tokens_per_s, 1),
@@ -281,7 +291,8 @@ def run_ours(args):
                    "M_rows_per_gpu": M, "d": d, "V": V,
                    "target": f"top-{args.target_topk} (id, logit) pairs per row (F1)" if sparse else "dense bf16 logits",
                    "k_accept": args.k_accept, "k_discard": args.k_discard, "accept_loss": args.accept_loss,
-                   "ntp_beta": args.ntp_beta, "optimizer": "adamw (F3)" if args.optimizer else None,
+                   "ntp_beta": args.ntp_beta,
+                   "optimizer": f"adamw ({args.optimizer}, F3)" if args.optimizer else None,
                    "tree": cfg.tree, "parallelism": f"dp{ws}" if ws > 1 else "single",
                    "l2": "flushed between timed steps (256 MiB write outside the step events)",
                    "launch": launch_mode},
@@ -387,7 +398,7 @@ def _phase_work(cfg, k, launches_per_step):
     return flops, byts
 
 
-def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0, workload=None):
+def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0, workload=None, optimizer=None):
     """Dominant lm_head kernel (largest share of the step): achieved algorithmic work per
     launch / mean launch time, against whichever roofline bounds it (tensor or HBM)."""
     per = []
@@ -398,7 +409,9 @@ def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0, workload=
         tot_ms, n = phases[k]
         lps = n / steps
         t = (tot_ms / n) / 1e3
-        if k == "adamw":  # F3: norm pass 4 B + update 30 B per lm_head element, no flops bound
+        if k == "adamw" and optimizer == "fused":  # F3 in the dW epilogue: m, v, W read + written, bf16 W
+            flops, byts = 2 * 2.0 * cfg.M * cfg.V * cfg.d, 26.0 * cfg.V * cfg.d
+        elif k == "adamw":  # F3 unfused: norm pass 4 B + update 30 B per lm_head element
             flops, byts = 0.0, 34.0 * cfg.V * cfg.d
         elif k == "bwd_fused":
             flops, byts = 3 * 2.0 * cfg.M * cfg.V * cfg.d, 4.0 * cfg.V * cfg.d + 4.0 * cfg.V * cfg.d
@@ -434,7 +447,9 @@ def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0, workload=
                "peak_source": f"{peak_src} hbm_gbs (copy)",
                "work_per_launch": "compulsory DRAM bytes per launch (fp32 dW chunk write + dZ^T/H reads, DESIGN.md 6)"}
     if k == "adamw":
-        out["work_per_launch"] = "34 B per lm_head element (F3: dW norm pass + dW/m/v/W reads, m/v/W fp32 + W bf16 writes)"
+        out["work_per_launch"] = ("26 B per lm_head element (F3 fused: m/v/W fp32 read + write, W bf16 write; dW never "
+                                  "stored)" if optimizer == "fused" else
+                                  "34 B per lm_head element (F3: dW norm pass + dW/m/v/W reads, m/v/W fp32 + W bf16 writes)")
     out["frac"] = round(out["achieved"] / out["peak"], 4)
     out["traffic"] = _traffic_for(k, workload)
     out["phases"] = per
@@ -541,7 +556,9 @@ def main():
     ap.add_argument("--ntp-beta", type=float, default=0.0, help="NTP auxiliary weight with --accept-loss rkl (F2)")
     ap.add_argument("--eager", action="store_true", help="launch the timed steps directly instead of replaying "
                                                           "them as one captured CUDA graph")
-    ap.add_argument("--optimizer", action="store_true", help="add the fused AdamW step on the fp32 master lm_head (F3)")
+    ap.add_argument("--optimizer", nargs="?", const="fused", default=None, choices=["fused", "unfused"],
+                    help="add the AdamW step on the fp32 master lm_head (F3): 'fused' (default) applies it from the "
+                         "dW GEMM epilogue, 'unfused' = bwd (dW to HBM) + aurora_adamw_step")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

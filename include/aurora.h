@@ -272,6 +272,23 @@ aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float
                                   int64_t step, const aurora_adamw_cfg_t* cfg, const float* extra_sq,
                                   float* grad_norm, void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream);
 
+/* NEXT F3, fused with the backward (SURVEY F3 "applied from the dW epilogue"): runs the
+ * backward of aurora_spec_loss_bwd for dH, then the optimizer step of aurora_adamw_step on
+ * the fp32 master lm_head WITHOUT materialising dW: the dW GEMM is recomputed from the
+ * bf16 dZ^T the backward left in `ws`, once for the global gradient norm (sum of squares
+ * in the epilogue) and once with the AdamW update in the epilogue.  W (bf16 [V_local, d])
+ * is rewritten from the updated master after dz and dH have read it.  Requires the whole
+ * local vocabulary in one dZ^T chunk (option dz_chunk_bytes) and no DP group (the DP dW
+ * allreduce must precede the optimizer: use aurora_spec_loss_bwd + aurora_adamw_step);
+ * otherwise UNSUPPORTED.  opt_ws: aurora_adamw_workspace_size(V_local * d) bytes. */
+aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, int64_t d, int64_t V_local,
+                                           int64_t vocab_offset, const aurora_labels_t* labels,
+                                           const float* row_lse, const float* dloss, float* dH,
+                                           float* W_master, float* m, float* v, int64_t step,
+                                           const aurora_adamw_cfg_t* cfg, const float* extra_sq,
+                                           float* grad_norm, void* ws, size_t ws_bytes, void* opt_ws,
+                                           size_t opt_ws_bytes, aurora_comm_t comm, void* stream);
+
 /* Per-phase device timing (CUDA events recorded on the caller's stream around each
  * phase while enabled).  aurora_profile_read must be called after the stream was
  * synchronised; it fills up to `max` (name, total ms, launches) triples and returns

@@ -28,7 +28,7 @@ EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fw
            "aurora_build_info", "aurora_launch_count", "aurora_profile_enable", "aurora_profile_read",
            "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option",
            "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step",
-           "aurora_profile_peek"]
+           "aurora_profile_peek", "aurora_spec_loss_bwd_adamw"]
 
 
 class AuroraError(RuntimeError):
@@ -120,6 +120,9 @@ def lib() -> C.CDLL:
                                             C.POINTER(aurora_labels_t), vp, sz, vp, vp]
     L.aurora_verify_labels_topk.restype = C.c_int
     L.aurora_set_option.argtypes = [C.c_char_p, C.c_int64]
+    L.aurora_spec_loss_bwd_adamw.argtypes = [vp, vp, i64, i64, i64, i64, C.POINTER(aurora_labels_t), vp, vp, vp, vp,
+                                             vp, vp, i64, C.POINTER(aurora_adamw_cfg_t), vp, vp, vp, sz, vp, sz, vp,
+                                             vp]
     L.aurora_adamw_workspace_size.argtypes = [i64]
     L.aurora_adamw_workspace_size.restype = sz
     L.aurora_adamw_step.argtypes = [vp, vp, vp, vp, vp, i64, i64, C.POINTER(aurora_adamw_cfg_t), vp, vp, vp, sz, vp,
@@ -368,6 +371,17 @@ class SpecTrainStep:
                              dloss, dH, dW, False, accumulate_dW, self.ws.data_ptr(), self.ws_bytes, self.comm,
                              stream)
 
+    def backward_adamw(self, H, W, dH, opt: "AdamW", dloss=None, extra_sq=None, stream=None):
+        """NEXT F3 fused: backward (dH) + the AdamW step applied from the dW GEMM epilogue
+        (dW never materialised).  opt owns the fp32 master of W, its moments and workspace;
+        W (bf16) is rewritten from the updated master."""
+        _expect(H, "bf16", "H"); _expect(W, "bf16", "W"); _expect(dH, "f32", "dH")
+        opt.step_count += 1
+        _check("aurora_spec_loss_bwd_adamw", lib().aurora_spec_loss_bwd_adamw(
+            _ptr(H), _ptr(W), self.M, self.d, self.V_local, self.vocab_offset, C.byref(self.labels), _ptr(self.row_lse),
+            _ptr(dloss), _ptr(dH), _ptr(opt.W), _ptr(opt.m), _ptr(opt.v), opt.step_count, C.byref(opt.cfg),
+            _ptr(extra_sq), _ptr(opt.grad_norm), _ptr(self.ws), self.ws_bytes, _ptr(opt.ws), opt.ws.numel(),
+            self.comm, _stream(stream)))
     def step(self, draft_tokens, target_logits, H, W, dH, dW, parents=None, num_nodes=None, stream=None):
         self.verify(draft_tokens, target_logits, parents, num_nodes, stream)
         self.forward(H, W, stream)

@@ -853,25 +853,13 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   return AURORA_OK;
 }
 
-aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
-                                     int64_t vocab_offset, const aurora_labels_t* labels, const float* row_lse,
-                                     const float* dloss, float* dH, void* dW, int dW_is_bf16, int accumulate_dW,
-                                     void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream) {
-  if (!gemm_shape_ok(H, W, M, d, V_local) || vocab_offset < 0) return AURORA_ERR_INVALID_ARG;
-  if (!labels_ok(labels, false) || !row_lse || !dH || !dW || !al16(dH) || !al16(dW)) return AURORA_ERR_INVALID_ARG;
-  if (dW_is_bf16) return AURORA_ERR_UNSUPPORTED;
-  aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
-  if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  float* dWf = static_cast<float*>(dW);
-  const int32_t objective = labels->objective;
-  if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
-                    labels->ld_target < V_local))
-    return AURORA_ERR_INVALID_ARG;
-  if (objective && comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
-  // the fused persistent bwd implements Eq. 3 only; the F2 objectives take the chunked path
-  if (!classic_bwd() && !objective) return bwd_fused(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf,
-                                       accumulate_dW, ws, comm, s);
+// The chunked backward (dz -> dW -> dH per dZ^T chunk).  dWf == nullptr skips dW and its
+// DP allreduce (the F3 fused optimizer recomputes dW tiles from the dZ^T left in ws).
+static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
+                                        int64_t vocab_offset, const aurora_labels_t* labels,
+                                        const float* row_lse, const float* dloss, float* dH, float* dWf,
+                                        int accumulate_dW, void* ws, aurora_comm_t comm, cudaStream_t s,
+                                        int32_t objective) {
   Carver c(ws);
   BwdWs w = carve_bwd(c, M, d, V_local);
 
@@ -938,39 +926,40 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
       cudaStreamWaitEvent(sH, ev[1 + 3 * ch], 0);
     }
 
-    // A8: dW[chunk] = dZ^T H   (A = dZ^T K-major, B = H MN-major, K = M)
-    GemmArgs b{};
-    b.m_tiles = static_cast<int32_t>(cdiv(vc, BM * pw));
-    b.n_tiles = static_cast<int32_t>(cdiv(d, BN));
-    b.splits = 1;
-    b.kb_total = static_cast<int32_t>(cdiv(M, BK));
-    b.kb_per_split = b.kb_total;
-    b.M = vc;
-    b.N = d;
-    b.out = dWf + c0 * d;
-    b.ld_out = d;
-    b.accumulate = accumulate_dW ? 1 : 0;
-    b.tile_counter = w.counters + 3 * ch + 1;
-    b.n_fastest = 1;  // A = dZ^T chunk (M x vc, may exceed L2) streams once; H (B) stays in L2
-    CUtensorMap tmOW;
-    const bool ow = make_tmap_f32_out(&tmOW, dWf + c0 * d, d, vc, d, 1, 0);
-    prof_begin(PH_BWD_DW, sW);
-    if (pw == 2 && ow && opts().dw_resident && dw_resident_ok(b.kb_total))
-      e = launch_dw_resident(tmZ_k, tmH_mn, tmOW, b, sW);  // small M: dZ^T rows stay in smem
-    else
-      e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr, pw);
-    prof_end(PH_BWD_DW, sW);
-    if (e != cudaSuccess) return AURORA_ERR_CUDA;
-    if (comm && comm->dp_x()) {  // C5: DP gradient allreduce of this dW chunk
-      auto& A = nccl::api();
-      prof_begin(PH_COMM, sW);
-      if (A.AllReduce(dWf + c0 * d, dWf + c0 * d, static_cast<size_t>(vc * d), nccl::ncclFloat32, nccl::ncclSum,
-                      comm->dp, sW) != 0)
-        return AURORA_ERR_NCCL;
-      prof_end(PH_COMM, sW);
+    if (dWf) {
+      // A8: dW[chunk] = dZ^T H   (A = dZ^T K-major, B = H MN-major, K = M)
+      GemmArgs b{};
+      b.m_tiles = static_cast<int32_t>(cdiv(vc, BM * pw));
+      b.n_tiles = static_cast<int32_t>(cdiv(d, BN));
+      b.splits = 1;
+      b.kb_total = static_cast<int32_t>(cdiv(M, BK));
+      b.kb_per_split = b.kb_total;
+      b.M = vc;
+      b.N = d;
+      b.out = dWf + c0 * d;
+      b.ld_out = d;
+      b.accumulate = accumulate_dW ? 1 : 0;
+      b.tile_counter = w.counters + 3 * ch + 1;
+      b.n_fastest = 1;  // A = dZ^T chunk (M x vc, may exceed L2) streams once; H (B) stays in L2
+      CUtensorMap tmOW;
+      const bool ow = make_tmap_f32_out(&tmOW, dWf + c0 * d, d, vc, d, 1, 0);
+      prof_begin(PH_BWD_DW, sW);
+      if (pw == 2 && ow && opts().dw_resident && dw_resident_ok(b.kb_total))
+        e = launch_dw_resident(tmZ_k, tmH_mn, tmOW, b, sW);  // small M: dZ^T rows stay in smem
+      else
+        e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr, pw);
+      prof_end(PH_BWD_DW, sW);
+      if (e != cudaSuccess) return AURORA_ERR_CUDA;
+      if (comm && comm->dp_x()) {  // C5: DP gradient allreduce of this dW chunk
+        auto& A = nccl::api();
+        prof_begin(PH_COMM, sW);
+        if (A.AllReduce(dWf + c0 * d, dWf + c0 * d, static_cast<size_t>(vc * d), nccl::ncclFloat32, nccl::ncclSum,
+                        comm->dp, sW) != 0)
+          return AURORA_ERR_NCCL;
+        prof_end(PH_COMM, sW);
+      }
+      if (S) cudaEventRecord(ev[2 + 3 * ch], sW);
     }
-    if (S) cudaEventRecord(ev[2 + 3 * ch], sW);
-
     // A9: dH += dZ W[chunk]   (A = dZ^T as MN-major, B = W MN-major, K = vc)
     GemmArgs h{};
     const int ph = pair_for(M);
@@ -1019,6 +1008,29 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
     prof_end(PH_COMM, s);
   }
   return AURORA_OK;
+}
+
+aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
+                                     int64_t vocab_offset, const aurora_labels_t* labels, const float* row_lse,
+                                     const float* dloss, float* dH, void* dW, int dW_is_bf16, int accumulate_dW,
+                                     void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream) {
+  if (!gemm_shape_ok(H, W, M, d, V_local) || vocab_offset < 0) return AURORA_ERR_INVALID_ARG;
+  if (!labels_ok(labels, false) || !row_lse || !dH || !dW || !al16(dH) || !al16(dW)) return AURORA_ERR_INVALID_ARG;
+  if (dW_is_bf16) return AURORA_ERR_UNSUPPORTED;
+  aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
+  if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float* dWf = static_cast<float*>(dW);
+  const int32_t objective = labels->objective;
+  if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
+                    labels->ld_target < V_local))
+    return AURORA_ERR_INVALID_ARG;
+  if (objective && comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
+  // the fused persistent bwd implements Eq. 3 only; the F2 objectives take the chunked path
+  if (!classic_bwd() && !objective) return bwd_fused(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf,
+                                       accumulate_dW, ws, comm, s);
+  return bwd_classic_impl(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf, accumulate_dW, ws,
+                          comm, s, objective);
 }
 
 aurora_status_t aurora_comm_get_unique_id(void* id_out) {
@@ -1071,7 +1083,26 @@ aurora_status_t aurora_comm_destroy(aurora_comm_t c) {
 
 size_t aurora_adamw_workspace_size(int64_t n) {
   if (n < 1) return 0;
-  return rup(static_cast<int64_t>(adamw_partials() + 64) * 4, 256) + 256;
+  // norm-pass partials: the standalone pass (adamw_partials) or, fused into the dW GEMM,
+  // one per (tile, CTA, epilogue warp) <= n / 4096 + tails
+  const int64_t parts = std::max<int64_t>(adamw_partials(), n / 4096 + 4 * 1024);
+  return rup((parts + 64) * 4, 256) + 256;
+}
+
+static bool adamw_cfg_ok(const aurora_adamw_cfg_t* cfg) {
+  return cfg && cfg->lr >= 0.f && cfg->beta1 >= 0.f && cfg->beta1 < 1.f && cfg->beta2 >= 0.f && cfg->beta2 < 1.f &&
+         cfg->eps > 0.f && cfg->weight_decay >= 0.f && std::isfinite(cfg->max_grad_norm) && cfg->warmup_steps >= 0;
+}
+// S:379 / P:489: lr(s) = lr * s / warmup for s < warmup, then constant; torch AdamW scalars
+static AdamwScalars adamw_scalars(const aurora_adamw_cfg_t* cfg, int64_t step) {
+  const double lr_t = (cfg->warmup_steps > 0 && step < cfg->warmup_steps)
+                          ? static_cast<double>(cfg->lr) * static_cast<double>(step) / cfg->warmup_steps
+                          : static_cast<double>(cfg->lr);
+  const double bc1 = 1.0 - std::pow(static_cast<double>(cfg->beta1), static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(static_cast<double>(cfg->beta2), static_cast<double>(step));
+  return AdamwScalars{cfg->beta1, cfg->beta2, cfg->eps, static_cast<float>(lr_t / bc1),
+                      static_cast<float>(1.0 / std::sqrt(bc2)), static_cast<float>(1.0 - lr_t * cfg->weight_decay),
+                      cfg->max_grad_norm};
 }
 
 aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float* v, const float* dW, int64_t n,
@@ -1080,23 +1111,13 @@ aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float
   if (!W_master || !m || !v || !dW || !cfg || n < 4 || n % 4 || step < 1) return AURORA_ERR_INVALID_ARG;
   if (!al16(W_master) || !al16(m) || !al16(v) || !al16(dW) || (W_bf16 && (reinterpret_cast<uintptr_t>(W_bf16) & 7)))
     return AURORA_ERR_INVALID_ARG;
-  if (!(cfg->lr >= 0.f) || !(cfg->beta1 >= 0.f && cfg->beta1 < 1.f) || !(cfg->beta2 >= 0.f && cfg->beta2 < 1.f) ||
-      !(cfg->eps > 0.f) || !(cfg->weight_decay >= 0.f) || !std::isfinite(cfg->max_grad_norm) || cfg->warmup_steps < 0)
-    return AURORA_ERR_INVALID_ARG;
+  if (!adamw_cfg_ok(cfg)) return AURORA_ERR_INVALID_ARG;
   if (!ws || ws_bytes < aurora_adamw_workspace_size(n)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Carver c(ws);
   float* norm_sq = c.take<float>(64);
   float* partials = c.take<float>(adamw_partials());
-  // S:379 / P:489: lr(s) = lr * s / warmup for s < warmup, then constant
-  const double lr_t = (cfg->warmup_steps > 0 && step < cfg->warmup_steps)
-                          ? static_cast<double>(cfg->lr) * static_cast<double>(step) / cfg->warmup_steps
-                          : static_cast<double>(cfg->lr);
-  const double bc1 = 1.0 - std::pow(static_cast<double>(cfg->beta1), static_cast<double>(step));
-  const double bc2 = 1.0 - std::pow(static_cast<double>(cfg->beta2), static_cast<double>(step));
-  AdamwScalars sc{cfg->beta1, cfg->beta2, cfg->eps, static_cast<float>(lr_t / bc1),
-                  static_cast<float>(1.0 / std::sqrt(bc2)), static_cast<float>(1.0 - lr_t * cfg->weight_decay),
-                  cfg->max_grad_norm};
+  const AdamwScalars sc = adamw_scalars(cfg, step);
   prof_begin(PH_OPTIM, s);
   if (launch_sumsq(dW, n, extra_sq, partials, norm_sq, s) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->vp_x()) {  // disjoint vocab shards: the global norm^2 sums over the VP group
@@ -1104,6 +1125,76 @@ aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float
     if (A.AllReduce(norm_sq, norm_sq, 1, nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0) return AURORA_ERR_NCCL;
   }
   if (launch_adamw(W_master, W_bf16, m, v, dW, n, norm_sq, grad_norm, sc, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  prof_end(PH_OPTIM, s);
+  return AURORA_OK;
+}
+
+aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, int64_t d, int64_t V_local,
+                                           int64_t vocab_offset, const aurora_labels_t* labels, const float* row_lse,
+                                           const float* dloss, float* dH, float* W_master, float* m, float* v,
+                                           int64_t step, const aurora_adamw_cfg_t* cfg, const float* extra_sq,
+                                           float* grad_norm, void* ws, size_t ws_bytes, void* opt_ws,
+                                           size_t opt_ws_bytes, aurora_comm_t comm, void* stream) {
+  if (!gemm_shape_ok(H, W, M, d, V_local) || vocab_offset < 0) return AURORA_ERR_INVALID_ARG;
+  if (!labels_ok(labels, false) || !row_lse || !dH || !al16(dH)) return AURORA_ERR_INVALID_ARG;
+  if (!W_master || !m || !v || !al16(W_master) || !al16(m) || !al16(v) || step < 1 || !adamw_cfg_ok(cfg))
+    return AURORA_ERR_INVALID_ARG;
+  aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
+  if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
+  if (!opt_ws || opt_ws_bytes < aurora_adamw_workspace_size(V_local * d)) return AURORA_ERR_WORKSPACE;
+  const int32_t objective = labels->objective;
+  if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
+                    labels->ld_target < V_local))
+    return AURORA_ERR_INVALID_ARG;
+  if (objective && comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
+  if (comm && comm->dp_x()) return AURORA_ERR_UNSUPPORTED;        // DP: the dW allreduce must come first
+  if (chunk_cols(V_local, M) < V_local) return AURORA_ERR_UNSUPPORTED;  // dZ^T of the whole slice in ws
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // 1) dz (whole local vocabulary) and dH, no dW
+  aurora_status_t st = bwd_classic_impl(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, nullptr, 0,
+                                        ws, comm, s, objective);
+  if (st != AURORA_OK) return st;
+  // 2) dW tiles recomputed from the dZ^T left in ws: pass 1 their sum of squares (global
+  //    norm), pass 2 the AdamW update from the epilogue -- dW never reaches HBM
+  Carver c(ws);
+  BwdWs w = carve_bwd(c, M, d, V_local);
+  CUtensorMap tmZ_k, tmH_mn;
+  if (!make_tmap_bf16(&tmZ_k, w.dzT, M, V_local, w.m_pad, 64, BM)) return AURORA_ERR_CUDA;
+  if (!make_tmap_bf16(&tmH_mn, H, d, M, d, 64, 64)) return AURORA_ERR_CUDA;
+  const int pw = pair_for(w.vc);
+  GemmArgs b{};
+  b.m_tiles = static_cast<int32_t>(cdiv(V_local, BM * pw));
+  b.n_tiles = static_cast<int32_t>(cdiv(d, BN));
+  b.splits = 1;
+  b.kb_total = static_cast<int32_t>(cdiv(M, BK));
+  b.kb_per_split = b.kb_total;
+  b.M = V_local;
+  b.N = d;
+  b.ld_out = d;
+  b.n_fastest = 1;
+  const int64_t nparts = static_cast<int64_t>(b.m_tiles) * b.n_tiles * pw * kEpiWarps;
+  Carver oc(opt_ws);
+  float* norm_sq = oc.take<float>(64);
+  float* partials = oc.take<float>(nparts);
+  if (oc.off > opt_ws_bytes) return AURORA_ERR_WORKSPACE;
+  prof_begin(PH_OPTIM, s);
+  b.out = partials;
+  if (launch_umma_gemm(EPI_SUMSQ, false, true, tmZ_k, tmH_mn, b, s, nullptr, pw) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (launch_sum_partials(partials, static_cast<int>(nparts), extra_sq, norm_sq, s) != cudaSuccess)
+    return AURORA_ERR_CUDA;
+  if (comm && comm->vp_x()) {
+    auto& A = nccl::api();
+    if (A.AllReduce(norm_sq, norm_sq, 1, nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+  }
+  b.out = nullptr;
+  b.opt_norm_sq = norm_sq;
+  b.opt_grad_norm = grad_norm;
+  b.opt_w = W_master;
+  b.opt_m = m;
+  b.opt_v = v;
+  b.opt_wb = static_cast<uint16_t*>(W);
+  b.opt = adamw_scalars(cfg, step);
+  if (launch_umma_gemm(EPI_ADAMW, false, true, tmZ_k, tmH_mn, b, s, nullptr, pw) != cudaSuccess) return AURORA_ERR_CUDA;
   prof_end(PH_OPTIM, s);
   return AURORA_OK;
 }

@@ -28,7 +28,21 @@ constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 1024 /*
 
 // *_T: the F2 objectives (reverse KL on ACCEPT rows, dense KL on DISCARD rows) — the
 // epilogue also reads the row's target logits T (bf16) for the tile's columns.
-enum EpiKind : int { EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2, EPI_FWD_STATS_T = 3, EPI_BWD_DZ_T = 4 };
+// EPI_SUMSQ / EPI_ADAMW (F3 fused into the dW GEMM): sum of squares of the output tile per
+// (unit, CTA, epilogue warp) / the AdamW update applied straight from TMEM to the fp32
+// master weights, moments and bf16 copy (the output itself is never stored).
+enum EpiKind : int {
+  EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2, EPI_FWD_STATS_T = 3, EPI_BWD_DZ_T = 4,
+  EPI_SUMSQ = 5, EPI_ADAMW = 6
+};
+
+struct AdamwScalars {  // host-computed per step (torch.optim.AdamW formulation)
+  float beta1, beta2, eps;
+  float step_size;     // lr_t / (1 - beta1^t)
+  float inv_sqrt_bc2;  // 1 / sqrt(1 - beta2^t)
+  float decay;         // 1 - lr_t * weight_decay
+  float max_norm;      // <= 0: no clipping
+};
 
 struct GemmArgs {
   int32_t m_tiles, n_tiles, splits;
@@ -67,6 +81,14 @@ struct GemmArgs {
   const float* row_lse_t;    // [M] log-sum-exp of the T row
   const float* row_aux;      // [M] E_q[z - t] (bwd, RKL rows)
   float* p_r;                // [M, 2*n_tiles] partial sum e^{z-m} (z - t) (fwd, RKL rows)
+  // ---- F3 fused optimizer (EPI_SUMSQ: partials in `out`; EPI_ADAMW: the update)
+  const float* opt_norm_sq;  // device scalar: global sum of squares (clip coefficient)
+  float* opt_grad_norm;      // nullable out: sqrt(norm_sq)
+  float* opt_w;              // fp32 master [M, ld_out] (the dW GEMM's output layout)
+  float* opt_m;
+  float* opt_v;
+  uint16_t* opt_wb;          // nullable bf16 copy
+  AdamwScalars opt;
 };
 
 // Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.
@@ -180,14 +202,9 @@ cudaError_t launch_debug_dlogits(const __nv_bfloat16* H, const __nv_bfloat16* W,
                                  float* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- F3 optimizer
-struct AdamwScalars {  // host-computed per step (torch.optim.AdamW formulation)
-  float beta1, beta2, eps;
-  float step_size;     // lr_t / (1 - beta1^t)
-  float inv_sqrt_bc2;  // 1 / sqrt(1 - beta2^t)
-  float decay;         // 1 - lr_t * weight_decay
-  float max_norm;      // <= 0: no clipping
-};
 int adamw_partials();
+// ordered sum of n partials (+ extra_sq) -> out[0] (one CTA)
+cudaError_t launch_sum_partials(const float* partials, int nparts, const float* extra_sq, float* out, cudaStream_t s);
 cudaError_t launch_sumsq(const float* g, int64_t n, const float* extra_sq, float* partials, float* norm_sq,
                          cudaStream_t s);
 cudaError_t launch_adamw(float* W, void* Wb, float* m, float* v, const float* g, int64_t n, const float* norm_sq,

@@ -406,6 +406,91 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if constexpr (kT) args.p_r[o] = rrun;
           }
         }
+      } else if constexpr (EPI == EPI_SUMSQ) {
+        // F3 pass 1: sum of squares of this warp's 32 rows x (up to) 128 columns, one partial
+        // per (unit, CTA, epilogue warp) -- fixed slots and a fixed shuffle tree
+        float acc2 = 0.f;
+        for (int cb = cbeg; cb < cend; cb += 16) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(taddr + cb, r);
+          tmem_ld_wait();
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float x = (cb + j < ncols) ? __uint_as_float(r[j]) : 0.f;
+              acc2 = fmaf(x, x, acc2);
+            }
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
+        if (lane == 0) args.out[(static_cast<int64_t>(u) * PAIR + rank) * kEpiWarps + (warp - 2)] = acc2;
+      } else if constexpr (EPI == EPI_ADAMW) {
+        // F3 pass 2: the dW tile goes straight from TMEM into the AdamW update (torch.optim
+        // AdamW form, global-norm clip): fp32 master / moments read and written as 16 B
+        // vectors per row segment, bf16 copy rewritten; dW itself never reaches HBM.
+        const float nsq = __ldg(args.opt_norm_sq);
+        const float norm = sqrtf(nsq);
+        const AdamwScalars c = args.opt;
+        const float clip = (c.max_norm > 0.f) ? fminf(1.f, c.max_norm / (norm + 1e-6f)) : 1.f;
+        if (args.opt_grad_norm && blockIdx.x == 0 && warp == 2 && lane == 0) args.opt_grad_norm[0] = norm;
+        const int64_t base = row * args.ld_out + col0;
+        for (int cb = cbeg; cb < cend; cb += 16) {
+          uint32_t r[16];
+          tmem_ld_32x32b_x16(taddr + cb, r);
+          const bool vec = row_ok && (cb + 16 <= ncols);
+          float4 mm[4], vv[4], ww[4];
+          if (vec) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              mm[i] = *reinterpret_cast<const float4*>(args.opt_m + base + cb + 4 * i);
+              vv[i] = *reinterpret_cast<const float4*>(args.opt_v + base + cb + 4 * i);
+              ww[i] = *reinterpret_cast<const float4*>(args.opt_w + base + cb + 4 * i);
+            }
+          }
+          tmem_ld_wait();
+          if (vec) {
+            uint32_t wb[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float* mp = &mm[i].x;
+              float* vp = &vv[i].x;
+              float* wp = &ww[i].x;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float g = __uint_as_float(r[4 * i + e]) * clip;
+                mp[e] = fmaf(c.beta1, mp[e], (1.f - c.beta1) * g);
+                vp[e] = fmaf(c.beta2, vp[e], (1.f - c.beta2) * g * g);
+                const float denom = sqrtf(vp[e]) * c.inv_sqrt_bc2 + c.eps;
+                wp[e] = wp[e] * c.decay - c.step_size * (mp[e] / denom);
+              }
+              *reinterpret_cast<float4*>(args.opt_m + base + cb + 4 * i) = mm[i];
+              *reinterpret_cast<float4*>(args.opt_v + base + cb + 4 * i) = vv[i];
+              *reinterpret_cast<float4*>(args.opt_w + base + cb + 4 * i) = ww[i];
+              const __nv_bfloat162 lo = __floats2bfloat162_rn(ww[i].x, ww[i].y);
+              const __nv_bfloat162 hi = __floats2bfloat162_rn(ww[i].z, ww[i].w);
+              wb[2 * i] = *reinterpret_cast<const uint32_t*>(&lo);
+              wb[2 * i + 1] = *reinterpret_cast<const uint32_t*>(&hi);
+            }
+            if (args.opt_wb) {
+              uint4* dst = reinterpret_cast<uint4*>(args.opt_wb + base + cb);
+              dst[0] = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+              dst[1] = make_uint4(wb[4], wb[5], wb[6], wb[7]);
+            }
+          } else if (row_ok) {  // column tail (N not a multiple of 16)
+            for (int j = 0; j < 16 && cb + j < ncols; ++j) {
+              const int64_t o = base + cb + j;
+              const float g = __uint_as_float(r[j]) * clip;
+              const float mj = fmaf(c.beta1, args.opt_m[o], (1.f - c.beta1) * g);
+              const float vj = fmaf(c.beta2, args.opt_v[o], (1.f - c.beta2) * g * g);
+              const float wj = args.opt_w[o] * c.decay - c.step_size * (mj / (sqrtf(vj) * c.inv_sqrt_bc2 + c.eps));
+              args.opt_m[o] = mj;
+              args.opt_v[o] = vj;
+              args.opt_w[o] = wj;
+              if (args.opt_wb) args.opt_wb[o] = __bfloat16_as_ushort(__float2bfloat16_rn(wj));
+            }
+          }
+        }
       } else if (args.tma_store && !((args.dbg_epi & 4) && half == 1)) {  // EPI_STORE_F32, TMA bulk stores
         // thread = row; each 32x16 fp32 block goes to a 64B-swizzled smem slot (rows of
         // 64 B, 16 B chunk c of row r at chunk c ^ ((r >> 1) & 3): conflict-free 16 B
@@ -594,6 +679,8 @@ cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, cons
   if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_FWD_STATS_T && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS_T, false, false, PAIR>(tmA, tmB, C, g, s);
+  if (epi == EPI_SUMSQ && !a_mn && b_mn) return launch_impl<EPI_SUMSQ, false, true, PAIR>(tmA, tmB, C, g, s);
+  if (epi == EPI_ADAMW && !a_mn && b_mn) return launch_impl<EPI_ADAMW, false, true, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_BWD_DZ_T && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ_T, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_STORE_F32) {
     if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false, PAIR>(tmA, tmB, C, g, s);

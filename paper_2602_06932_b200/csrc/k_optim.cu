@@ -90,6 +90,12 @@ __global__ void __launch_bounds__(kOptThreads) k_adamw(float4* __restrict__ W, u
 
 int adamw_partials() { return kOptBlocks; }
 
+cudaError_t launch_sum_partials(const float* partials, int nparts, const float* extra_sq, float* out, cudaStream_t s) {
+  k_sumsq_final<<<1, kOptThreads, 0, s>>>(partials, nparts, extra_sq, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sumsq(const float* g, int64_t n, const float* extra_sq, float* partials, float* norm_sq,
                          cudaStream_t s) {
   k_sumsq_partial<<<kOptBlocks, kOptThreads, 0, s>>>(reinterpret_cast<const float4*>(g), n / 4, partials);

@@ -72,3 +72,71 @@ def test_adamw_extra_sq_and_validation():
     with pytest.raises(Exception):  # n % 4 != 0
         A.aurora_adamw_step(W[:4093], None, opt.m[:4093], opt.v[:4093], torch.zeros(4093, device="cuda"), 1, opt.cfg,
                             opt.ws)
+
+
+def _bf16(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).cuda()
+
+
+def _prepare(tr):
+    c = tr["cfg"]
+    H, W = _bf16(tr["H_bits"]), _bf16(tr["W_bits"])
+    draft = torch.from_numpy(tr["draft_tokens"]).cuda()
+    par = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).cuda()
+    nn = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).cuda()
+    st = A.SpecTrainStep(c.R, c.N, c.d, c.V)
+    st.verify(draft, _bf16(tr["T_bits"]), par, nn)
+    return c, H, W, st
+
+
+@pytest.mark.parametrize("name", ["small", "small_tree", "mid"])
+def test_fused_bwd_adamw_matches_unfused(name):
+    """F3 fused into the dW epilogue (dW never stored) vs bwd + aurora_adamw_step: same dH
+    bits, the same update up to the norm's summation order; and the oracle's AdamW applied
+    to the unfused dW pins the arithmetic."""
+    tr = tracegen.gen_trace(name)
+    c, H, W1, st1 = _prepare(tr)
+    st1.forward(H, W1)
+    dH1 = torch.empty(c.M, c.d, device="cuda")
+    dW1 = torch.empty(c.V, c.d, device="cuda")
+    st1.backward(H, W1, dH1, dW1)
+    W0 = W1.float().clone()
+    opt1 = A.AdamW(W1.float().reshape(-1).clone(), lr=1e-4, warmup_steps=0)
+    opt1.step(dW1.reshape(-1), W_bf16=W1.reshape(-1))
+    _, _, W2, st2 = _prepare(tr)
+    st2.forward(H, W2)
+    dH2 = torch.empty(c.M, c.d, device="cuda")
+    opt2 = A.AdamW(W2.float().reshape(-1).clone(), lr=1e-4, warmup_steps=0)
+    st2.backward_adamw(H, W2, dH2, opt2)
+    torch.cuda.synchronize()
+    assert torch.equal(dH1, dH2)
+    n1, n2 = float(opt1.grad_norm.item()), float(opt2.grad_norm.item())
+    assert abs(n1 - n2) <= 1e-5 * n1
+    np.testing.assert_allclose(opt2.W.cpu().numpy(), opt1.W.cpu().numpy(), rtol=1e-6, atol=1e-9)
+    np.testing.assert_allclose(opt2.m.cpu().numpy(), opt1.m.cpu().numpy(), rtol=1e-4,
+                               atol=1e-6 * float(opt1.m.abs().max()))
+    assert (W2.float() - opt2.W.reshape(c.V, c.d)).abs().max() <= 4e-3 * W0.abs().max()  # bf16 copy of the master
+    f32 = lambda x: float(np.float32(x))
+    Wr, mr, vr, norm = oracle.adamw_step(W0.reshape(-1).cpu().numpy(), np.zeros(W0.numel()), np.zeros(W0.numel()),
+                                         dW1.reshape(-1).cpu().numpy(), 1, f32(1e-4), warmup_steps=0,
+                                         beta1=f32(0.9), beta2=f32(0.999), eps=f32(1e-8))
+    assert abs(n2 - norm) <= 2e-5 * norm
+    np.testing.assert_allclose(opt2.W.cpu().numpy(), Wr, rtol=2e-6, atol=1e-9)
+
+
+def test_fused_bwd_adamw_needs_one_chunk():
+    tr = tracegen.gen_trace("small")
+    c, H, W, st = _prepare(tr)
+    saved = A.aurora_get_option("dz_chunk_bytes")
+    try:
+        A.aurora_set_option("dz_chunk_bytes", 64 << 10)
+        st = A.SpecTrainStep(c.R, c.N, c.d, c.V)
+        st.verify(torch.from_numpy(tr["draft_tokens"]).cuda(), _bf16(tr["T_bits"]), None,
+                  torch.from_numpy(tr["num_nodes"]).cuda() if tr["num_nodes"] is not None else None)
+        st.forward(H, W)
+        opt = A.AdamW(W.float().reshape(-1).clone())
+        with pytest.raises(A.AuroraError) as ei:
+            st.backward_adamw(H, W, torch.empty(c.M, c.d, device="cuda"), opt)
+        assert ei.value.status == 5
+    finally:
+        A.aurora_set_option("dz_chunk_bytes", saved)
