@@ -556,9 +556,9 @@ def main():
     ap.add_argument("--ntp-beta", type=float, default=0.0, help="NTP auxiliary weight with --accept-loss rkl (F2)")
     ap.add_argument("--eager", action="store_true", help="launch the timed steps directly instead of replaying "
                                                           "them as one captured CUDA graph")
-    ap.add_argument("--optimizer", nargs="?", const="fused", default=None, choices=["fused", "unfused"],
-                    help="add the AdamW step on the fp32 master lm_head (F3): 'fused' (default) applies it from the "
-                         "dW GEMM epilogue, 'unfused' = bwd (dW to HBM) + aurora_adamw_step")
+    ap.add_argument("--optimizer", nargs="?", const="unfused", default=None, choices=["fused", "unfused"],
+                    help="add the AdamW step on the fp32 master lm_head (F3): 'unfused' (default) = bwd (dW to HBM) + "
+                         "aurora_adamw_step; 'fused' applies it from the dW GEMM epilogue (measured slower, DESIGN.md)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -69,10 +69,12 @@ struct SmemPlan {
   static constexpr int kSB = (TBN / PAIR) * BK * 2;  // B bytes per stage in this CTA
   static constexpr int kStageBytes = kSmemA + kSB;
   static constexpr bool kStore = EPI == EPI_STORE_F32;
-  static constexpr int kSt = PAIR == 2 ? 6 : kStages;
+  static constexpr bool kAdamw = EPI == EPI_ADAMW;  // 32x36 fp32 transpose slice per epilogue warp
+  static constexpr int kSt = PAIR == 2 ? (kAdamw ? 5 : 6) : (kAdamw ? 3 : kStages);
   static constexpr int kRing = kSt * kStageBytes;
   static constexpr int kSlots = kStore ? 2 : 0;  // 2 KB bulk-store slots per warp
-  static constexpr int kStaging = kEpiWarps * kSlots * 2048;
+  static constexpr int kAdamwLd = 36;            // staging row stride (floats): conflict-free 16 B access
+  static constexpr int kStaging = kAdamw ? kEpiWarps * 32 * kAdamwLd * 4 : kEpiWarps * kSlots * 2048;
   static constexpr int kBytes = kRing + 1024 /*barriers*/ + 1024 /*base alignment*/ + kStaging;
   static_assert(kBytes <= 232448, "dynamic smem per CTA");
   static_assert(kSt * kStageBytes <= kStages * (kSmemA + kSmemB), "ring");
@@ -427,69 +429,71 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) args.out[(static_cast<int64_t>(u) * PAIR + rank) * kEpiWarps + (warp - 2)] = acc2;
       } else if constexpr (EPI == EPI_ADAMW) {
         // F3 pass 2: the dW tile goes straight from TMEM into the AdamW update (torch.optim
-        // AdamW form, global-norm clip): fp32 master / moments read and written as 16 B
-        // vectors per row segment, bf16 copy rewritten; dW itself never reaches HBM.
+        // AdamW form, global-norm clip); dW itself never reaches HBM.  TMEM gives thread =
+        // row, so each 32x32 block is transposed through this warp's smem slice and the
+        // fp32 master / moments are then read and written 4 rows x 128 B per instruction.
         const float nsq = __ldg(args.opt_norm_sq);
         const float norm = sqrtf(nsq);
         const AdamwScalars c = args.opt;
         const float clip = (c.max_norm > 0.f) ? fminf(1.f, c.max_norm / (norm + 1e-6f)) : 1.f;
         if (args.opt_grad_norm && blockIdx.x == 0 && warp == 2 && lane == 0) args.opt_grad_norm[0] = norm;
-        const int64_t base = row * args.ld_out + col0;
-        for (int cb = cbeg; cb < cend; cb += 16) {
-          uint32_t r[16];
-          tmem_ld_32x32b_x16(taddr + cb, r);
-          const bool vec = row_ok && (cb + 16 <= ncols);
-          float4 mm[4], vv[4], ww[4];
-          if (vec) {
+        constexpr int LD = Plan::kAdamwLd;
+        const uint32_t stg = smem_u32(reinterpret_cast<uint8_t*>(stage_f32) + (warp - 2) * (32 * LD * 4));
+        const int64_t row0 = static_cast<int64_t>(mt) * BM + q * 32;
+        const int rl0 = lane >> 3, cc = (lane & 7) * 4;  // 4 rows x 8 lanes of 16 B per pass
+        for (int cb = cbeg; cb < cend; cb += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + cb, r);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              mm[i] = *reinterpret_cast<const float4*>(args.opt_m + base + cb + 4 * i);
-              vv[i] = *reinterpret_cast<const float4*>(args.opt_v + base + cb + 4 * i);
-              ww[i] = *reinterpret_cast<const float4*>(args.opt_w + base + cb + 4 * i);
+          for (int j = 0; j < 32; j += 4)
+            sts128(stg + (lane * LD + j) * 4, __uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                   __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          __syncwarp();
+          // all 24 16-B loads of the block in flight before any arithmetic (memory-level
+          // parallelism: ~12 KB per warp); d % 64 == 0 => no column tails, rows predicated
+          float4 mm[8], vv[8], ww[8];
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int64_t grow = row0 + it * 4 + rl0;
+            const int64_t o = grow * args.ld_out + col0 + cb + cc;
+            if (grow < args.M) {
+              mm[it] = *reinterpret_cast<const float4*>(args.opt_m + o);
+              vv[it] = *reinterpret_cast<const float4*>(args.opt_v + o);
+              ww[it] = *reinterpret_cast<const float4*>(args.opt_w + o);
             }
           }
-          tmem_ld_wait();
-          if (vec) {
-            uint32_t wb[8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float* mp = &mm[i].x;
-              float* vp = &vv[i].x;
-              float* wp = &ww[i].x;
+          for (int it = 0; it < 8; ++it) {
+            const int rl = it * 4 + rl0;
+            const int64_t grow = row0 + rl;
+            if (grow < args.M) {
+              const float4 gv = lds128(stg + (rl * LD + cc) * 4);
+              const int64_t o = grow * args.ld_out + col0 + cb + cc;
+              const float gs[4] = {gv.x, gv.y, gv.z, gv.w};
+              float* mp = &mm[it].x;
+              float* vp = &vv[it].x;
+              float* wp = &ww[it].x;
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float g = __uint_as_float(r[4 * i + e]) * clip;
+                const float g = gs[e] * clip;
                 mp[e] = fmaf(c.beta1, mp[e], (1.f - c.beta1) * g);
                 vp[e] = fmaf(c.beta2, vp[e], (1.f - c.beta2) * g * g);
                 const float denom = sqrtf(vp[e]) * c.inv_sqrt_bc2 + c.eps;
                 wp[e] = wp[e] * c.decay - c.step_size * (mp[e] / denom);
               }
-              *reinterpret_cast<float4*>(args.opt_m + base + cb + 4 * i) = mm[i];
-              *reinterpret_cast<float4*>(args.opt_v + base + cb + 4 * i) = vv[i];
-              *reinterpret_cast<float4*>(args.opt_w + base + cb + 4 * i) = ww[i];
-              const __nv_bfloat162 lo = __floats2bfloat162_rn(ww[i].x, ww[i].y);
-              const __nv_bfloat162 hi = __floats2bfloat162_rn(ww[i].z, ww[i].w);
-              wb[2 * i] = *reinterpret_cast<const uint32_t*>(&lo);
-              wb[2 * i + 1] = *reinterpret_cast<const uint32_t*>(&hi);
-            }
-            if (args.opt_wb) {
-              uint4* dst = reinterpret_cast<uint4*>(args.opt_wb + base + cb);
-              dst[0] = make_uint4(wb[0], wb[1], wb[2], wb[3]);
-              dst[1] = make_uint4(wb[4], wb[5], wb[6], wb[7]);
-            }
-          } else if (row_ok) {  // column tail (N not a multiple of 16)
-            for (int j = 0; j < 16 && cb + j < ncols; ++j) {
-              const int64_t o = base + cb + j;
-              const float g = __uint_as_float(r[j]) * clip;
-              const float mj = fmaf(c.beta1, args.opt_m[o], (1.f - c.beta1) * g);
-              const float vj = fmaf(c.beta2, args.opt_v[o], (1.f - c.beta2) * g * g);
-              const float wj = args.opt_w[o] * c.decay - c.step_size * (mj / (sqrtf(vj) * c.inv_sqrt_bc2 + c.eps));
-              args.opt_m[o] = mj;
-              args.opt_v[o] = vj;
-              args.opt_w[o] = wj;
-              if (args.opt_wb) args.opt_wb[o] = __bfloat16_as_ushort(__float2bfloat16_rn(wj));
+              *reinterpret_cast<float4*>(args.opt_m + o) = mm[it];
+              *reinterpret_cast<float4*>(args.opt_v + o) = vv[it];
+              *reinterpret_cast<float4*>(args.opt_w + o) = ww[it];
+              if (args.opt_wb) {
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(ww[it].x, ww[it].y);
+                const __nv_bfloat162 hi = __floats2bfloat162_rn(ww[it].z, ww[it].w);
+                *reinterpret_cast<uint2*>(args.opt_wb + o) =
+                    make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+              }
             }
           }
+          __syncwarp();
         }
       } else if (args.tma_store && !((args.dbg_epi & 4) && half == 1)) {  // EPI_STORE_F32, TMA bulk stores
         // thread = row; each 32x16 fp32 block goes to a 64B-swizzled smem slot (rows of
