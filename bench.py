@@ -49,18 +49,43 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML polled every 2 ms
+    from a thread (a graph-replayed timed region lasts only tens of ms), else nvidia-smi
+    -lms 100.  Reasons: hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NVML_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu_index: int):
-        self.idx = gpu_index
-        self.rows = []
+        idx = gpu_index
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                idx = int(vis.split(",")[gpu_index])
+            except (ValueError, IndexError):
+                idx = gpu_index
+        self.idx = idx
+        self.rows = []      # nvidia-smi rows
+        self.sm, self.mx, self.reasons = [], [], set()
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.mx.append(float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)))
+            self._sample_nvml()  # one sample at the start of the timed region
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -71,11 +96,34 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _sample_nvml(self):
+        n = self.nvml
+        self.sm.append(float(n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)))
+        try:
+            bits = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except AttributeError:
+            bits = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        for name, bit in self.NVML_BITS.items():
+            if bits & bit:
+                self.reasons.add(name)
+
+    def _poll_nvml(self):
+        while not self.stop.wait(0.002):
+            try:
+                self._sample_nvml()
+            except Exception:
+                return
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self._sample_nvml()  # and one at the end
+            self.stop.set()
+            self.t.join(timeout=1)
+            return
         if self.proc:
             self.proc.terminate()
             try:
@@ -84,6 +132,10 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        if self.nvml is not None:
+            return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                    "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                    "samples": len(self.sm), "source": "nvml (2 ms polling during the timed region)"}
         sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
         reasons = set()
@@ -94,7 +146,7 @@ class ClockSampler:
                     if v.strip().lower() == "active":
                         reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 def _dist_env():
@@ -199,7 +251,9 @@ def run_ours(args):
     launch_mode = "eager"
     graph = None
     launches_per_step = None
-    if not args.eager:
+    # multi-rank runs stay eager: the DP exchanges are NCCL calls, and capturing them is
+    # untestable on the one-GPU development box
+    if not args.eager and ws == 1:
         try:
             A.aurora_profile_read()  # clear
             A.aurora_profile_enable(True)
