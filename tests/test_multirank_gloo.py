@@ -178,3 +178,48 @@ def test_dp2_exchange_reproduces_single_rank():
     np.testing.assert_allclose(out["dW"], ref["dW"], rtol=1e-10, atol=1e-14)   # C5
     half = (tr["R"] // 2) * (tr["N"] + 1)
     np.testing.assert_allclose(out["dH0"], ref["dH"][:half], rtol=1e-10, atol=1e-14)
+
+
+def _adamw_vp_worker(rank, port, q):
+    """F3 over VP shards: each rank holds rows [v0, v1) of the lm_head; the global-norm
+    clip needs sum(dW^2) over ALL shards = one scalar allreduce (the library's VP
+    AllReduce of norm_sq), passed in as the other shards' share (extra_sq)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WS)
+    try:
+        inp = tracegen.gen_adamw_inputs(4096, steps=2, grad_scale=1e-2)
+        W = inp["W"].astype(np.float64).reshape(64, 64)
+        v0, v1 = (0, 40) if rank == 0 else (40, 64)
+        Ws, ms, vs = W[v0:v1].reshape(-1), np.zeros((v1 - v0) * 64), np.zeros((v1 - v0) * 64)
+        for step, g in enumerate(inp["G"], start=1):
+            gs = g.astype(np.float64).reshape(64, 64)[v0:v1].reshape(-1)
+            local = torch.tensor([float(np.sum(gs * gs))], dtype=torch.float64)
+            tot = local.clone()
+            dist.all_reduce(tot)
+            Ws, ms, vs, norm = oracle.adamw_step(Ws, ms, vs, gs, step, 1e-3, warmup_steps=0,
+                                                 extra_sq=float(tot.item() - local.item()))
+        q.put((rank, v0, v1, Ws, norm))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_adamw_vp_norm_exchange_matches_single_process():
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_adamw_vp_worker, args=(r, port, q)) for r in range(WS)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(WS)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    inp = tracegen.gen_adamw_inputs(4096, steps=2, grad_scale=1e-2)
+    W, m, v = inp["W"].astype(np.float64), np.zeros(4096), np.zeros(4096)
+    for step, g in enumerate(inp["G"], start=1):
+        W, m, v, norm = oracle.adamw_step(W, m, v, g, step, 1e-3, warmup_steps=0)
+    W = W.reshape(64, 64)
+    for rank, v0, v1, Ws, n in res:
+        assert abs(n - norm) <= 1e-12 * norm
+        np.testing.assert_allclose(Ws, W[v0:v1].reshape(-1), rtol=1e-13, atol=1e-16)
