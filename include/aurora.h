@@ -95,7 +95,7 @@ typedef struct {
   int32_t k_discard;      /* support size on DISCARD rows; default 10; same range.
                              0 = the paper's unfiltered "top-k 0": dense
                              KL(p_target || q) over the whole vocabulary (F2; dense
-                             verify only, single vocab shard)                           */
+                             verify only; VP: the T row statistics are allgathered)     */
   float lambda_discard;   /* default 1.0; 0 disables the discard term          */
   int32_t normalize;      /* 0: per-term means over GLOBAL counts N_A, N_D (default,
                              S:378, reading Q7); 1: mean over N_A + N_D rows            */
@@ -104,8 +104,8 @@ typedef struct {
   int32_t accept_loss;    /* ACCEPT-row objective (§5.1; NEXT F2):
                              0 = FKL KL(p~ || q) on the top-k_accept support (default);
                              1 = RKL KL(q || p_target) over the whole vocabulary,
-                             gradient q*((ln q - ln p) - KL); dense verify only,
-                             single vocab shard                                          */
+                             gradient q*((ln q - ln p) - KL); dense verify only
+                             (VP shards allgather per-row T statistics)                  */
   float ntp_beta;         /* >= 0: auxiliary NTP cross-entropy -ln q_y on ACCEPT rows,
                              y = verified token, weight beta x the row weight ("RKL +
                              NTP"); requires accept_loss = 1           */

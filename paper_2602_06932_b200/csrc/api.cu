@@ -222,11 +222,12 @@ int dh_splits(int64_t M, int64_t d, int64_t kb_total, int pair = 1) {
   return 1;
 }
 
-struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; float* ept; };
+struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; float* ept; float* lse_part; };
 VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
   const int nseg = scan_nseg(M, V_local);
   VerifyWs w;
   w.ept = c.take<float>(M);
+  w.lse_part = c.take<float>(M * 3);
   w.cand_val = c.take<float>(M * nseg * k_max);
   w.cand_idx = c.take<int32_t>(M * nseg * k_max);
   w.top_val = c.take<float>(M * k_max);
@@ -645,10 +646,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->V_local, cfg)) return AURORA_ERR_WORKSPACE;
   if (comm && comm->vp_size > 1 && t->V_local == t->V) return AURORA_ERR_INVALID_ARG;  // VP needs shards
   const int32_t objective = objective_of(cfg);
-  if (objective) {  // F2: single vocab shard; labels carry the per-row target statistics
-    if (comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
-    if (!out->row_lse_t || !out->row_aux) return AURORA_ERR_INVALID_ARG;
-  }
+  if (objective && (!out->row_lse_t || !out->row_aux)) return AURORA_ERR_INVALID_ARG;  // F2 row statistics
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   out->objective = objective;
   out->ntp_beta = cfg->ntp_beta;
@@ -705,7 +703,20 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   }
   if (objective) {  // F2: row statistics of T (a second read of T, so it counts as scan time)
     prof_begin(PH_SCAN, s);
-    if ((e = launch_row_lse_t(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+    if (comm && comm->vp_x()) {  // VP: per-rank (max, sum, sum*t) triples -> allgather -> merge
+      p.lse_part = w.lse_part;
+      if ((e = launch_row_lse_t(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
+      auto& A = nccl::api();
+      const size_t per = static_cast<size_t>(M) * 3;
+      if (!ensure_scratch(comm, per * comm->vp_size * sizeof(float))) return AURORA_ERR_CUDA;
+      if (A.AllGather(w.lse_part, comm->scratch, per, nccl::ncclFloat32, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+      p.lse_part = nullptr;
+      if ((e = launch_row_lse_t_combine(p, static_cast<const float*>(comm->scratch), comm->vp_size, s)) !=
+          cudaSuccess)
+        return AURORA_ERR_CUDA;
+    } else if ((e = launch_row_lse_t(p, s)) != cudaSuccess) {
+      return AURORA_ERR_CUDA;
+    }
     prof_end(PH_SCAN, s);
   }
   prof_begin(PH_VERIFY, s);
@@ -792,7 +803,6 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
                     labels->ld_target < V_local))
     return AURORA_ERR_INVALID_ARG;
-  if (objective && comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Carver c(ws);
   FwdWs w = carve_fwd(c, M, V_local);
@@ -1025,7 +1035,6 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
   if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
                     labels->ld_target < V_local))
     return AURORA_ERR_INVALID_ARG;
-  if (objective && comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
   // the fused persistent bwd implements Eq. 3 only; the F2 objectives take the chunked path
   if (!classic_bwd() && !objective) return bwd_fused(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf,
                                        accumulate_dW, ws, comm, s);
@@ -1146,7 +1155,6 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
   if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
                     labels->ld_target < V_local))
     return AURORA_ERR_INVALID_ARG;
-  if (objective && comm && comm->vp_size > 1) return AURORA_ERR_UNSUPPORTED;
   if (comm && comm->dp_x()) return AURORA_ERR_UNSUPPORTED;        // DP: the dW allreduce must come first
   if (chunk_cols(V_local, M) < V_local) return AURORA_ERR_UNSUPPORTED;  // dZ^T of the whole slice in ws
   cudaStream_t s = static_cast<cudaStream_t>(stream);

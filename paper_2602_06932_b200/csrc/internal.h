@@ -162,6 +162,7 @@ struct VerifyLaunch {
   int32_t* top_idx;
   int32_t k_top;        // long-support path (k > AURORA_MAX_K): top-list length per row
   float* ept;           // F2: [M] E_p[t] of the target row (dense discard rows' H)
+  float* lse_part;      // F2 x VP: [M, 3] this rank's (max, sum e^{t-m}, sum e^{t-m} t); null = final
   aurora_labels_t lab;
   aurora_loss_cfg_t cfg;
 };
@@ -178,6 +179,7 @@ cudaError_t launch_sort_pairs(const VerifyLaunch& p, const int32_t* tk_idx, cons
 cudaError_t launch_finalize_long(const VerifyLaunch& p, cudaStream_t s);
 // F2: per-row log-sum-exp and E_p[t] of the dense target row (CTA per row).
 cudaError_t launch_row_lse_t(const VerifyLaunch& p, cudaStream_t s);
+cudaError_t launch_row_lse_t_combine(const VerifyLaunch& p, const float* parts /*[P,M,3]*/, int P, cudaStream_t s);
 
 // ---------------------------------------------------------------- row kernels
 // msu rows are (m, s, u, r): r = sum e^{z-m} (z - t) on F2 RKL rows (pr nullable => 0).

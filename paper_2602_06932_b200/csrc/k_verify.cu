@@ -685,9 +685,33 @@ __global__ void __launch_bounds__(256) k_row_lse_t(VerifyLaunch p) {
   if (threadIdx.x == 0) {
     m = red[0][0]; S = red[1][0]; A = red[2][0];
     for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) merge(red[0][i], red[1][i], red[2][i]);
-    p.lab.row_lse_t[row] = m + logf(S);
-    p.ept[row] = A / S;
+    if (p.lse_part) {  // vocab-parallel: this rank's (max, sum e^{t-m}, sum e^{t-m} t) for the allgather
+      p.lse_part[row * 3 + 0] = m;
+      p.lse_part[row * 3 + 1] = S;
+      p.lse_part[row * 3 + 2] = A;
+    } else {
+      p.lab.row_lse_t[row] = m + logf(S);
+      p.ept[row] = A / S;
+    }
   }
+}
+
+// F2 x VP: merge the ranks' (max, sum e^{t-m}, sum e^{t-m} t) triples in rank order.
+__global__ void __launch_bounds__(256) k_row_lse_t_combine(VerifyLaunch p, const float* __restrict__ parts, int P) {
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  if (row >= p.M) return;
+  float m = -INFINITY, S = 0.f, A = 0.f;
+  for (int r = 0; r < P; ++r) {
+    const float* q = parts + (static_cast<int64_t>(r) * p.M + row) * 3;
+    const float mn = fmaxf(m, q[0]);
+    if (mn == -INFINITY) continue;
+    const float a = __expf(m - mn), b = __expf(q[0] - mn);
+    S = S * a + q[1] * b;
+    A = A * a + q[2] * b;
+    m = mn;
+  }
+  p.lab.row_lse_t[row] = m + logf(S);
+  p.ept[row] = A / S;
 }
 
 // --------------------------------------------------------------------------- launchers
@@ -731,6 +755,11 @@ cudaError_t launch_finalize_long(const VerifyLaunch& p, cudaStream_t s) {
 }
 cudaError_t launch_row_lse_t(const VerifyLaunch& p, cudaStream_t s) {
   k_row_lse_t<<<p.M, 256, 0, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_row_lse_t_combine(const VerifyLaunch& p, const float* parts, int P, cudaStream_t s) {
+  k_row_lse_t_combine<<<(p.M + 255) / 256, 256, 0, s>>>(p, parts, P);
   count_launch();
   return cudaGetLastError();
 }

@@ -588,3 +588,27 @@ def test_dw_resident_matches_streamed(option, name):
     assert torch.equal(a["dW"], b["dW"]) and torch.equal(a["dH"], b["dH"])
     ref = oracle.step(tr)
     assert _rfro(a["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+
+
+def test_single_rank_comm_f2_objectives():
+    """F2 under a (1-rank) vocab-parallel communicator: the T row statistics go through the
+    VP triple allgather + ordered merge, (m, s, u, r) through C3; results match the
+    comm-less path (the merge of one triple reproduces it up to the log/exp round trip)
+    and the oracle."""
+    tr = tracegen.gen_trace("small")
+    kw = F2_VARIANTS[1]
+    base = _run_gpu(tr, **kw)
+    ref = oracle.step_variants(tr, **kw)
+    uid = A.aurora_comm_get_unique_id()
+    comm = A.aurora_comm_create(uid, 1, 0, 1, 1)
+    try:
+        out = _run_gpu(tr, comm=comm, **kw)
+        for k in ("target_argmax", "accept_len", "row_class", "sup_idx", "row_w"):
+            assert torch.equal(getattr(out["st"], k), getattr(base["st"], k)), k
+        np.testing.assert_allclose(out["st"].row_lse_t.cpu().numpy(), base["st"].row_lse_t.cpu().numpy(), rtol=1e-6)
+        loss = float(out["st"].loss.item())
+        assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"])
+        assert _rfro(out["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+        assert _rfro(out["dH"].cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+    finally:
+        A.aurora_comm_destroy(comm)

@@ -223,3 +223,107 @@ def test_adamw_vp_norm_exchange_matches_single_process():
     for rank, v0, v1, Ws, n in res:
         assert abs(n - norm) <= 1e-12 * norm
         np.testing.assert_allclose(Ws, W[v0:v1].reshape(-1), rtol=1e-13, atol=1e-16)
+
+
+def _f2_vp_worker(rank, port, q):
+    """F2 (RKL + NTP on ACCEPT rows, dense KL on DISCARD rows) over two vocab shards: the
+    exchanges the library makes -- C1 top lists (argmax), the T-row triples (max,
+    sum e^{t-m}, sum e^{t-m} t), C3 (m, s, u, r), C4 dH -- run as gloo collectives."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WS)
+    try:
+        tr = tracegen.gen_trace("small_tree")
+        V, M = tr["V"], tr["M"]
+        cut = V // 2 + 37
+        v0, v1 = (0, cut) if rank == 0 else (cut, V)
+        beta = 0.5
+        T = oracle.bf16_bits_to_f64(tr["T_bits"])[:, v0:v1]
+        # C1 (k = 1 suffices: RKL + NTP needs only the argmax; dense discard has no support)
+        loc = np.lexsort((np.arange(v1 - v0)[None, :].repeat(M, 0), -T), axis=1)[:, 0]
+        cand = torch.from_numpy(np.stack([T[np.arange(M), loc], loc + v0], 1))
+        g = [torch.zeros_like(cand) for _ in range(WS)]
+        dist.all_gather(g, cand)
+        allc = torch.stack(g).numpy()  # [rank, M, (value, id)]
+        best = np.lexsort((allc[:, :, 1], -allc[:, :, 0]), axis=0)[0]
+        am = allc[best, np.arange(M), 1].astype(np.int64)
+        lab = oracle.verify(tr["draft_tokens"], tr["parents"], tr["num_nodes"], am)
+        cls = lab["row_class"]
+        na, nd = int((cls == 0).sum()), int((cls == 1).sum())
+        w = np.where(cls == 0, 1.0 / na, np.where(cls == 1, 1.0 / nd, 0.0))
+        # T-row triples -> global lse_t, E_p[t]
+        mt = T.max(1)
+        St = np.exp(T - mt[:, None]).sum(1)
+        At = (np.exp(T - mt[:, None]) * T).sum(1)
+        g = [torch.zeros(M, 3, dtype=torch.float64) for _ in range(WS)]
+        dist.all_gather(g, torch.from_numpy(np.stack([mt, St, At], 1)))
+        trip = torch.stack(g).numpy()
+        mm = trip[:, :, 0].max(0)
+        S = (trip[:, :, 1] * np.exp(trip[:, :, 0] - mm)).sum(0)
+        Asum = (trip[:, :, 2] * np.exp(trip[:, :, 0] - mm)).sum(0)
+        lse_t = mm + np.log(S)
+        Hp = Asum / S - lse_t
+        # C3: (m, s, u, r) per shard
+        H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+        Wsh = oracle.bf16_bits_to_f64(tr["W_bits"][v0:v1])
+        Z = H64 @ Wsh.T
+        mz = Z.max(1)
+        e = np.exp(Z - mz[:, None])
+        s = e.sum(1)
+        r = (e * (Z - T)).sum(1)
+        p = np.exp(T - lse_t[:, None])
+        u = np.zeros(M)
+        for m_ in range(M):
+            if cls[m_] == 0 and v0 <= am[m_] < v1:
+                u[m_] = beta * Z[m_, am[m_] - v0]
+            elif cls[m_] == 1:
+                u[m_] = float(np.dot(p[m_], Z[m_]))
+        g = [torch.zeros(M, 4, dtype=torch.float64) for _ in range(WS)]
+        dist.all_gather(g, torch.from_numpy(np.stack([mz, s, u, r], 1)))
+        q4 = torch.stack(g).numpy()
+        MM = q4[:, :, 0].max(0)
+        sc = np.exp(q4[:, :, 0] - MM)
+        ssum = (q4[:, :, 1] * sc).sum(0)
+        R = (q4[:, :, 3] * sc).sum(0)
+        U = q4[:, :, 2].sum(0)
+        lse = MM + np.log(ssum)
+        eqzt = R / ssum
+        row_loss = np.where(cls == 0, eqzt - lse + lse_t + beta * lse - U,
+                            np.where(cls == 1, lse - U + Hp, 0.0))
+        loss = float(np.dot(w, row_loss))
+        # bwd on the shard: dz = w (q ((z - t) - E + beta) - beta e_y) / w (q - p); C4 dH
+        qz = np.exp(Z - lse[:, None])
+        dZ = np.zeros_like(Z)
+        for m_ in range(M):
+            if cls[m_] == 0:
+                dZ[m_] = qz[m_] * ((Z[m_] - T[m_]) - eqzt[m_] + beta)
+                if v0 <= am[m_] < v1:
+                    dZ[m_, am[m_] - v0] -= beta
+            elif cls[m_] == 1:
+                dZ[m_] = qz[m_] - p[m_]
+            dZ[m_] *= w[m_]
+        dW_shard = dZ.T @ H64
+        dH = torch.from_numpy(dZ @ Wsh)
+        dist.all_reduce(dH)
+        q.put((rank, v0, v1, loss, dH.numpy(), dW_shard))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_f2_objectives_vp_exchange_matches_oracle():
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_f2_vp_worker, args=(r, port, q)) for r in range(WS)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=180) for _ in range(WS)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    tr = tracegen.gen_trace("small_tree")
+    ref = oracle.step_variants(tr, accept_loss="rkl", ntp_beta=0.5, k_discard=0)
+    for rank, v0, v1, loss, dH, dWs in res:
+        assert abs(loss - ref["loss"]) <= 1e-10 * abs(ref["loss"])
+        np.testing.assert_allclose(dH, ref["dH"], rtol=1e-9, atol=1e-13)
+        np.testing.assert_allclose(dWs, ref["dW"][v0:v1], rtol=1e-9, atol=1e-13)
