@@ -21,6 +21,7 @@ KEYS = [
     ("dram__bytes_write.sum", "dram_write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%peak"),
     ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_%peak"),
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "tc_pipe_active_%"),
     ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor_mem_active_%"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm_%peak"),
     ("smsp__inst_executed.sum", "warp_inst"),
