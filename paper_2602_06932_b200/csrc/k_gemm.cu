@@ -528,6 +528,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) {
             const int32_t x = static_cast<int32_t>(col0 + cb);
             if (args.accumulate) tma_reduce_add_3d(&tmC, slot, x, row0, sp);
+            else if (dbg & 8) tma_store_3d_hint(&tmC, slot, x, row0, sp, l2_policy_evict_first());
             else tma_store_3d(&tmC, slot, x, row0, sp);
             bulk_commit();
           }
