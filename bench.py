@@ -23,6 +23,7 @@ host cores on a bounded sample of the same workload; rank 0 only.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -181,18 +182,36 @@ def run_ours(args):
     A.lib()
 
     cfg = tracegen.CONFIGS[args.config]
+    # Multi-GPU (N > 1): vocab-parallel weak scaling by default (the north star's box-level
+    # scheme): one global batch of N x R requests, rank p holds vocab slice p of the lm_head
+    # W and of the target logits T; per-GPU GEMM work M*N x V/N = M x V stays fixed, and
+    # only per-row scalars (C1, C3) and the dH partials (C4) cross NVLink.  --parallel dp:
+    # data-parallel (each rank its own batch, the full vocabulary, a dW allreduce of V*d fp32).
+    vp = ws > 1 and args.parallel == "vp"
+    if vp:
+        cfg = dataclasses.replace(cfg, R=cfg.R * ws)
+    seed = cfg.seed if vp else cfg.seed + 1000 * rank
     if args.target_topk:
-        tr = tracegen.gen_trace_topk(cfg, K_t=args.target_topk, seed=cfg.seed + 1000 * rank)
+        tr = tracegen.gen_trace_topk(cfg, K_t=args.target_topk, seed=seed)
     else:
-        tr = tracegen.gen_trace(cfg, seed=cfg.seed + 1000 * rank)
+        tr = tracegen.gen_trace(cfg, seed=seed)
     R, N, d, V, M = cfg.R, cfg.N, cfg.d, cfg.V, cfg.M
+    v0, v1 = (rank * V // ws, (rank + 1) * V // ws) if vp else (0, V)
+    V_local = v1 - v0
+    if vp:  # this rank's vocab slice (the sparse payload stays replicated: no candidate exchange)
+        tr = dict(tr)
+        tr["W_bits"] = np.ascontiguousarray(tr["W_bits"][v0:v1])
+        if not args.target_topk:
+            tr["T_bits"] = np.ascontiguousarray(tr["T_bits"][:, v0:v1])
 
     comm = None
     if ws > 1:
         uid = A.aurora_comm_get_unique_id() if rank == 0 else bytes(128)
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
-        comm = A.aurora_comm_create(obj[0], ws, rank, 1, ws)
+        comm = A.aurora_comm_create(obj[0], ws, rank, ws, 1) if vp else A.aurora_comm_create(obj[0], ws, rank, 1, ws)
+    elif args.comm1:  # 1-rank communicator: every exchange runs (as an identity) on one GPU
+        comm = A.aurora_comm_create(A.aurora_comm_get_unique_id(), 1, 0, 1, 1)
 
     sparse = bool(args.target_topk)
     if sparse:
@@ -205,15 +224,16 @@ def run_ours(args):
     draft = torch.from_numpy(tr["draft_tokens"]).to(dev)
     parents = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).to(dev)
     num_nodes = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).to(dev)
-    st = A.SpecTrainStep(R, N, d, V, comm=comm, device=dev, k_accept=args.k_accept, k_discard=args.k_discard,
-                         accept_loss=args.accept_loss, ntp_beta=args.ntp_beta)
+    st = A.SpecTrainStep(R, N, d, V, V_local=V_local, vocab_offset=v0, comm=comm, device=dev,
+                         k_accept=args.k_accept, k_discard=args.k_discard, accept_loss=args.accept_loss,
+                         ntp_beta=args.ntp_beta)
     if sparse and A.aurora_workspace_size(A.OP_VERIFY, M, d, args.target_topk, st.cfg) > st.ws_bytes:
         raise SystemExit("workspace too small for --target-topk")
     dH = torch.empty(M, d, dtype=torch.float32, device=dev)
-    dW = torch.empty(V, d, dtype=torch.float32, device=dev)
+    dW = torch.empty(V_local, d, dtype=torch.float32, device=dev)
     opt = None
     if args.optimizer:  # F3: fp32 master lm_head + fused AdamW; the GEMMs read its bf16 copy
-        opt = A.AdamW(W.float().reshape(-1), lr=1e-5, warmup_steps=400)
+        opt = A.AdamW(W.float().reshape(-1), lr=1e-5, warmup_steps=400, comm=comm)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -310,10 +330,11 @@ def run_ours(args):
         dist.barrier()
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    tokens_per_s = (M * ws) / (ms_step / 1e3)
+    tokens_per_s = (M if vp else M * ws) / (ms_step / 1e3)   # VP: one global batch of M rows
 
     # ---------------- e2e: public API with pinned host inputs, result read back
-    e2e = None if opt is not None else _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush, sparse)
+    e2e = None if opt is not None else _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush, sparse,
+                                                 rows_total=M if vp else M * ws)
 
     if rank != 0:
         if comm is not None:
@@ -326,8 +347,9 @@ def run_ours(args):
     # traffic: only for the exact workload the committed ncu capture ran (default objective)
     plain = (not sparse and args.k_accept == 1 and args.k_discard == 10 and args.accept_loss == "fkl"
              and args.optimizer != "fused")
-    roof = _roofline(phases, cfg, args.steps, peak_sus, peak_src, hbm, workload=cfg.name if plain else None,
-                     optimizer=args.optimizer)
+    cfg_dev = dataclasses.replace(cfg, V=V_local)  # the work one GPU does (VP: its vocab slice)
+    roof = _roofline(phases, cfg_dev, args.steps, peak_sus, peak_src, hbm,
+                     workload=cfg.name if (plain and not vp and ws == 1) else None, optimizer=args.optimizer)
     out = {
         "metric": "speculator-training tokens/s (verify + lm_head fwd/bwd + Eq.3 loss), % bf16 tensor peak",
         "value": round(tokens_per_s, 1),
@@ -347,7 +369,10 @@ def run_ours(args):
                    "k_accept": args.k_accept, "k_discard": args.k_discard, "accept_loss": args.accept_loss,
                    "ntp_beta": args.ntp_beta,
                    "optimizer": f"adamw ({args.optimizer}, F3)" if args.optimizer else None,
-                   "tree": cfg.tree, "parallelism": f"dp{ws}" if ws > 1 else "single",
+                   "tree": cfg.tree,
+                   "parallelism": (f"vp{ws} (vocab-parallel lm_head, global batch {R} requests)" if vp else
+                                   f"dp{ws}" if ws > 1 else ("single (1-rank comm)" if args.comm1 else "single")),
+                   "V_local": V_local,
                    "l2": "flushed between timed steps (256 MiB write outside the step events)",
                    "launch": launch_mode},
         "gpu_launches": int(n_launch),
@@ -356,7 +381,7 @@ def run_ours(args):
         "e2e": e2e,
         "clocks": clk.summary(),
     }
-    out["tensor_frac_step"] = round((8.0 * M * V * d / (ms_step / 1e3)) / (peak_sus * 1e12), 4)
+    out["tensor_frac_step"] = round((8.0 * M * V_local * d / (ms_step / 1e3)) / (peak_sus * 1e12), 4)
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = _cpu_baseline(cfg, args)
     print(json.dumps(out), flush=True)
@@ -366,7 +391,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush, sparse=False):
+def _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush, sparse=False, rows_total=None):
     """Same step through the public API (SpecTrainStep), with the trace batch (T -- or,
     sparse, the top-K (id, logit) payload the paper transmits, P:391-392 --, H, draft
     tokens, parents, ragged counts) copied H2D from pinned host memory every step and the
@@ -429,7 +454,8 @@ def _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush, sparse=False)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
-    return {"value": round(st.M * ws / (ms_step / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(ms_step, 4),
+    rows_total = st.M * ws if rows_total is None else rows_total
+    return {"value": round(rows_total / (ms_step / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(ms_step, 4),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "note": "pinned H2D of step i+1 overlapped with step i on a copy stream (double buffer); "
                     "no L2 flush (each step streams its trace from host)"}
@@ -608,6 +634,9 @@ def main():
     ap.add_argument("--k-discard", type=int, default=10, help="support size on DISCARD rows (P:520; 0 = dense KL, F2)")
     ap.add_argument("--accept-loss", default="fkl", choices=["fkl", "rkl"], help="ACCEPT-row objective (F2)")
     ap.add_argument("--ntp-beta", type=float, default=0.0, help="NTP auxiliary weight with --accept-loss rkl (F2)")
+    ap.add_argument("--parallel", default="vp", choices=["vp", "dp"],
+                    help="N > 1: vocab-parallel weak scaling (default) or data-parallel")
+    ap.add_argument("--comm1", action="store_true", help="N = 1: run every exchange through a 1-rank communicator")
     ap.add_argument("--eager", action="store_true", help="launch the timed steps directly instead of replaying "
                                                           "them as one captured CUDA graph")
     ap.add_argument("--optimizer", nargs="?", const="unfused", default=None, choices=["fused", "unfused"],
