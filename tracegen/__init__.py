@@ -38,7 +38,8 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["TraceConfig", "CONFIGS", "gen_trace", "gen_trace_topk", "f32_to_bf16_bits", "bf16_bits_to_f32"]
+__all__ = ["TraceConfig", "CONFIGS", "gen_trace", "gen_trace_topk", "f32_to_bf16_bits", "bf16_bits_to_f32",
+           "TreeAttnConfig", "TREE_ATTN_CONFIGS", "gen_tree_attn", "gen_tree_attn_meta"]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -272,3 +273,103 @@ def gen_adamw_inputs(n: int, steps: int, seed: int = 4242, grad_scale: float = 1
     W = (rng.standard_normal(n, dtype=np.float32) * np.float32(2.0 / 64.0)).astype(np.float32)
     G = [(rng.standard_normal(n, dtype=np.float32) * np.float32(grad_scale)).astype(np.float32) for _ in range(steps)]
     return dict(W=W, G=G)
+
+
+# ----------------------------------------------------------------------------- NEXT F4
+@dataclasses.dataclass(frozen=True)
+class TreeAttnConfig:
+    """Tree-attention workload of the draft layer (F4): R requests, each a ragged prefix of
+    P_r cached positions (K/V) plus the N + 1 tree rows (root + draft nodes)."""
+    name: str
+    R: int
+    N: int
+    Hq: int
+    Hkv: int
+    dh: int
+    p_min: int
+    p_max: int
+    seed: int
+    tree: bool = False
+    beam: int = 4
+    ragged_nodes: bool = False
+
+
+TREE_ATTN_CONFIGS = {
+    # oracle-pin sizes (not run on the GPU: dh != 128)
+    "ta_tiny": TreeAttnConfig("ta_tiny", R=3, N=6, Hq=4, Hkv=2, dh=8, p_min=0, p_max=5, seed=3001, tree=True, beam=2),
+    # GPU parity: several 64-key tiles, ragged tails, an empty prefix, ragged node counts
+    "ta_small": TreeAttnConfig("ta_small", R=5, N=12, Hq=8, Hkv=2, dh=128, p_min=0, p_max=300, seed=3002,
+                               tree=True, beam=3, ragged_nodes=True),
+    "ta_chain": TreeAttnConfig("ta_chain", R=6, N=5, Hq=32, Hkv=8, dh=128, p_min=1, p_max=200, seed=3003),
+    "ta_gqa8": TreeAttnConfig("ta_gqa8", R=4, N=15, Hq=16, Hkv=2, dh=128, p_min=60, p_max=130, seed=3004,
+                              tree=True, beam=5),
+    # full sizes: the Llama chain traces and the tree-draft traces (BASELINE configs[1], [4]);
+    # Llama-3.1-8B / Qwen3-8B attention shapes (32 query heads, 8 KV heads, head_dim 128);
+    # prefixes up to the paper's max sequence 2048 (P:493) minus the tree depth
+    "ta_llama": TreeAttnConfig("ta_llama", R=64, N=5, Hq=32, Hkv=8, dh=128, p_min=128, p_max=2042, seed=3011),
+    "ta_tree": TreeAttnConfig("ta_tree", R=1024, N=24, Hq=32, Hkv=8, dh=128, p_min=128, p_max=2041, seed=3012,
+                              tree=True, beam=4),
+}
+
+
+def gen_tree_attn_meta(cfg: TreeAttnConfig | str) -> dict:
+    """Structure only: prefix lengths ~ U[p_min, p_max], the parent array (chain: None;
+    tree: the same beam recipe as gen_trace) and ragged node counts."""
+    if isinstance(cfg, str):
+        cfg = TREE_ATTN_CONFIGS[cfg]
+    rng = np.random.Generator(np.random.PCG64(cfg.seed))
+    lens = rng.integers(cfg.p_min, cfg.p_max + 1, size=cfg.R).astype(np.int64)
+    if cfg.R > 1 and cfg.p_min == 0:
+        lens[1] = 0                                   # an empty prefix
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    parents = _tree_parents(rng, cfg.R, cfg.N // cfg.beam, cfg.beam) if cfg.tree else None
+    num_nodes = None
+    if cfg.ragged_nodes:
+        num_nodes = np.full(cfg.R, cfg.N, dtype=np.int32)
+        num_nodes[0] = max(1, cfg.N // 2)
+        if cfg.R > 2:
+            num_nodes[2] = 0
+    return dict(cfg=cfg, prefix_off=off, parents=parents, num_nodes=num_nodes)
+
+
+def gen_tree_attn(cfg: TreeAttnConfig | str, requests=None) -> dict:
+    """Q [R, N+1, Hq, dh], Kt/Vt [R, N+1, Hkv, dh], Kp/Vp [P_total, Hkv, dh], dO like Q, as
+    bf16 bits.  Each request draws from its own stream PCG64(seed * 100003 + 1 + r), so
+    `requests` (a subset) reproduces exactly those requests' inputs (the full-size parity
+    tests hand the oracle a sample).  Q, K ~ N(0, 1) (scaled scores ~ N(0, 1)); the query
+    heads of every fourth KV group are scaled by 3 (peaked rows); V ~ N(0, 1); dO ~
+    N(0, 0.1^2)."""
+    meta = gen_tree_attn_meta(cfg)
+    c = meta["cfg"]
+    off = meta["prefix_off"]
+    reqs = np.arange(c.R) if requests is None else np.asarray(requests)
+    N1 = c.N + 1
+    Q = np.empty((len(reqs), N1, c.Hq, c.dh), np.uint16)
+    dO = np.empty_like(Q)
+    Kt = np.empty((len(reqs), N1, c.Hkv, c.dh), np.uint16)
+    Vt = np.empty_like(Kt)
+    lens = [int(off[r + 1] - off[r]) for r in reqs]
+    Kp = np.empty((sum(lens), c.Hkv, c.dh), np.uint16)
+    Vp = np.empty_like(Kp)
+    qscale = np.ones((c.Hq, 1), np.float32)
+    G = c.Hq // c.Hkv
+    for h in range(c.Hq):
+        if (h // G) % 4 == 3:
+            qscale[h] = 3.0
+    pos = 0
+    for i, r in enumerate(reqs):
+        rng = np.random.Generator(np.random.PCG64(c.seed * 100003 + 1 + int(r)))
+        Q[i] = f32_to_bf16_bits(rng.standard_normal((N1, c.Hq, c.dh), dtype=np.float32) * qscale)
+        Kt[i] = f32_to_bf16_bits(rng.standard_normal((N1, c.Hkv, c.dh), dtype=np.float32))
+        Vt[i] = f32_to_bf16_bits(rng.standard_normal((N1, c.Hkv, c.dh), dtype=np.float32))
+        L = lens[i]
+        Kp[pos:pos + L] = f32_to_bf16_bits(rng.standard_normal((L, c.Hkv, c.dh), dtype=np.float32))
+        Vp[pos:pos + L] = f32_to_bf16_bits(rng.standard_normal((L, c.Hkv, c.dh), dtype=np.float32))
+        dO[i] = f32_to_bf16_bits(rng.standard_normal((N1, c.Hq, c.dh), dtype=np.float32) * np.float32(0.1))
+        pos += L
+    sub_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    par = meta["parents"]
+    nn = meta["num_nodes"]
+    return dict(cfg=c, requests=reqs, Q_bits=Q, Kt_bits=Kt, Vt_bits=Vt, Kp_bits=Kp, Vp_bits=Vp, dO_bits=dO,
+                prefix_off=sub_off, parents=None if par is None else par[reqs],
+                num_nodes=None if nn is None else nn[reqs])
