@@ -616,6 +616,172 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------------------- NEXT F4
+def _ta_work(meta):
+    """Algorithmic work of one tree-attention fwd+bwd over a batch (F4):
+    visible (row, key) pairs per query head -- every prefix key for each valid tree row plus
+    the row's ancestor closure -- times 4 dh flops forward and 10 dh backward (S, dP, dV, dQ,
+    dK); compulsory DRAM bytes: Q, K/V (prefix + tree) read once per kernel that needs them,
+    O/lse written, dO/O/lse read, dQ fp32 and dK/dV bf16 written."""
+    c = meta["cfg"]
+    off = meta["prefix_off"]
+    lens = np.diff(off).astype(np.int64)
+    N1 = c.N + 1
+    pairs = 0
+    for r in range(c.R):
+        nn = c.N if meta["num_nodes"] is None else int(meta["num_nodes"][r])
+        par = None if meta["parents"] is None else meta["parents"][r]
+        depth_sum = 1                                   # root sees itself
+        for n in range(nn):
+            d, p = 2, (n - 1 if par is None else int(par[n]))
+            while p >= 0:
+                d += 1
+                p = p - 1 if par is None else int(par[p])
+            depth_sum += d
+        pairs += (nn + 1) * int(lens[r]) + depth_sum
+    pairs *= c.Hq
+    rows = c.R * N1
+    q_b = rows * c.Hq * c.dh * 2
+    kv_b = (int(lens.sum()) + rows) * c.Hkv * c.dh * 2 * 2       # K and V
+    fwd_b = q_b + kv_b + q_b + rows * c.Hq * 4                    # + O + lse
+    dq_b = 3 * q_b + rows * c.Hq * 8 + kv_b + 2 * q_b             # Q, dO, O(dsum), lse+Dsum, K/V, dQ fp32
+    dkdv_b = kv_b + kv_b + 2 * q_b + rows * c.Hq * 8              # K/V read, dK/dV write, Q/dO, lse/Dsum
+    return dict(pairs=pairs, fwd_flops=4.0 * c.dh * pairs, bwd_flops=10.0 * c.dh * pairs, fwd_bytes=fwd_b,
+                dq_bytes=dq_b, dkdv_bytes=dkdv_b, rows=rows)
+
+
+def run_tree_attn(args):
+    """F4 bench: tree-attention fwd + bwd of the draft layer over a batch of speculative trees
+    with ragged cached prefixes (tracegen TREE_ATTN_CONFIGS; values drawn on the device from a
+    seeded generator with the distributions of tracegen.gen_tree_attn)."""
+    import torch
+    from paper_2602_06932_b200 import aurora as A
+    from paper_2602_06932_b200.build import build
+
+    ws, rank, local = _dist_env()
+    if rank != 0:        # F4 is measured on one GPU (replicas would repeat rank 0's work)
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    build()
+    A.lib()
+    meta = tracegen.gen_tree_attn_meta(args.ta_config)
+    c = meta["cfg"]
+    N1 = c.N + 1
+    off = meta["prefix_off"]
+    P = int(off[-1])
+    g = torch.Generator(device=dev)
+    g.manual_seed(c.seed)
+    qscale = torch.ones(c.Hq, 1, device=dev)
+    G = c.Hq // c.Hkv
+    for h in range(c.Hq):
+        if (h // G) % 4 == 3:
+            qscale[h] = 3.0
+
+    def rnd(*shape, scale=1.0):
+        return (torch.randn(*shape, generator=g, device=dev, dtype=torch.float32) * scale).to(torch.bfloat16)
+
+    Q = (torch.randn(c.R, N1, c.Hq, c.dh, generator=g, device=dev) * qscale).to(torch.bfloat16)
+    Kt, Vt = rnd(c.R, N1, c.Hkv, c.dh), rnd(c.R, N1, c.Hkv, c.dh)
+    Kp, Vp = rnd(P, c.Hkv, c.dh), rnd(P, c.Hkv, c.dh)
+    dO = rnd(c.R, N1, c.Hq, c.dh, scale=0.1)
+    poff = torch.from_numpy(off.astype(np.int32)).to(dev)
+    par = None if meta["parents"] is None else torch.from_numpy(meta["parents"].astype(np.int32)).to(dev)
+    nn = None if meta["num_nodes"] is None else torch.from_numpy(meta["num_nodes"].astype(np.int32)).to(dev)
+    max_prefix = int(np.diff(off).max())
+    ta = A.TreeAttention(c.R, c.N, c.Hq, c.Hkv, c.dh, poff, max_prefix, parents=par, num_nodes=nn)
+    O = torch.empty_like(Q)
+    lse = torch.empty(c.R, N1, c.Hq, dtype=torch.float32, device=dev)
+    dQ = torch.empty(Q.shape, dtype=torch.float32, device=dev)
+    dKt, dVt, dKp, dVp = (torch.empty_like(x) for x in (Kt, Vt, Kp, Vp))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(q=Q, kt=Kt, vt=Vt, kp=Kp, vp=Vp, do=dO):
+        ta.forward(q, kt, vt, kp, vp, O, lse)
+        ta.backward(q, kt, vt, kp, vp, O, lse, do, dQ, dKt, dVt, dKp, dVp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert int(ta.status.item()) == 0
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    A.aurora_profile_read()
+    A.aurora_profile_enable(True)
+    n0 = A.aurora_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    n_launch = A.aurora_launch_count() - n0
+    A.aurora_profile_enable(False)
+    phases = A.aurora_profile_read()
+    ms_step = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    w = _ta_work(meta)
+    rows_per_s = w["rows"] / (ms_step / 1e3)
+
+    # e2e: every step copies its inputs from pinned host memory and reads lse back
+    host = {k: v.cpu().pin_memory() for k, v in dict(Q=Q, Kt=Kt, Vt=Vt, Kp=Kp, Vp=Vp, dO=dO).items()}
+    lse_h = torch.empty(lse.shape, dtype=torch.float32).pin_memory()
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    e_steps = max(2, min(args.steps, 5))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e_steps):
+        dv = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+        step(dv["Q"], dv["Kt"], dv["Vt"], dv["Kp"], dv["Vp"], dv["dO"])
+        lse_h.copy_(lse, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e_steps
+
+    _, _, hbm, peak_src = _peaks()
+    per = []
+    for k, byts, flops in (("tree_attn_fwd", w["fwd_bytes"], w["fwd_flops"]),
+                           ("tree_attn_bwd_dq", w["dq_bytes"], 0.4 * w["bwd_flops"]),
+                           ("tree_attn_bwd_dkdv", w["dkdv_bytes"], 0.6 * w["bwd_flops"])):
+        if k in phases and phases[k][1]:
+            t = phases[k][0] / args.steps / 1e3
+            per.append({"kernel": k, "ms_per_step": round(t * 1e3, 4), "achieved_gbs": round(byts / t / 1e9, 1),
+                        "achieved_tflops": round(flops / t / 1e12, 1), "frac_hbm": round(byts / t / 1e9 / hbm, 4)})
+    dom = max(per, key=lambda x: x["ms_per_step"])
+    out = {
+        "metric": "tree-attention fwd+bwd tokens/s (F4 draft-layer attention, ancestor-closure mask)",
+        "value": round(rows_per_s, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded device generator; tracegen structure)",
+        "config": {"workload": c.name, "R": c.R, "N": c.N, "Hq": c.Hq, "Hkv": c.Hkv, "dh": c.dh,
+                   "prefix_tokens": P, "max_prefix": max_prefix, "tree": c.tree,
+                   "visible_pairs_per_head_avg": round(w["pairs"] / c.Hq / c.R, 1),
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": "eager"},
+        "gpu_launches": int(n_launch),
+        "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
+        "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved_gbs"], "peak": hbm,
+                     "unit": "GB/s", "frac": round(dom["achieved_gbs"] / hbm, 4), "traffic": None,
+                     "peak_source": f"{peak_src} hbm_gbs (copy)",
+                     "work_per_launch": "compulsory DRAM bytes (prefix+tree K/V, Q/dO/O, outputs), DESIGN.md §6 F4",
+                     "phases": per},
+        "e2e": {"value": round(w["rows"] / (e2e_ms / 1e3), 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(lse.numel() * 4)},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        from oracle import tree_attention as TA
+        reqs = list(range(min(4, c.R)))
+        sub = tracegen.gen_tree_attn(c.name, requests=reqs)
+        t0 = time.perf_counter()
+        TA.fwd_bwd(sub)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": round(len(reqs) * N1 / dt, 2), "unit": "tokens/s",
+                               "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+                               "sample": f"first {len(reqs)} of {c.R} requests of '{c.name}', fwd+bwd f64; {dt:.2f} s"}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -642,11 +808,17 @@ def main():
     ap.add_argument("--optimizer", nargs="?", const="unfused", default=None, choices=["fused", "unfused"],
                     help="add the AdamW step on the fp32 master lm_head (F3): 'unfused' (default) = bwd (dW to HBM) + "
                          "aurora_adamw_step; 'fused' applies it from the dW GEMM epilogue (measured slower, DESIGN.md)")
+    ap.add_argument("--workload", default="spec_loss", choices=["spec_loss", "tree_attn"],
+                    help="spec_loss: the north-star hot path (default); tree_attn: NEXT F4 draft-layer tree attention")
+    ap.add_argument("--ta-config", default="ta_tree", choices=sorted(tracegen.TREE_ATTN_CONFIGS),
+                    help="F4 workload (--workload tree_attn)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "tree_attn":
+        run_tree_attn(args)
     else:
         run_ours(args)
 

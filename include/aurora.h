@@ -289,6 +289,51 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
                                            float* grad_norm, void* ws, size_t ws_bytes, void* opt_ws,
                                            size_t opt_ws_bytes, aurora_comm_t comm, void* stream);
 
+/* ---- NEXT F4: tree attention of the draft layer -------------------------------------
+ * P:163-169 §3.2 "Efficient Tree Attention ... a custom attention mask that respects the
+ * causal structure of the speculative tree ... all accepted and rejected branches in a
+ * single batched forward and backward pass"; the tree is S:134-140 (parents[n] < n).
+ * Readings F4-R1..R5:
+ *  - request r has P_r prefix positions (K/V given: the draft layer's cached prefix, packed
+ *    [P_total, Hkv, dh], request r at rows prefix_off[r] .. prefix_off[r+1]-1) and N+1 tree
+ *    rows in the lm_head path's order (s = 0 root, s = n+1 draft node n);
+ *  - tree row s attends every prefix position of its request and the tree rows in its
+ *    ancestor closure anc*(s) (its ancestors, the root and itself) — never a sibling
+ *    branch; rows of padded nodes (n >= num_nodes[r]) are keys of nobody and, as queries,
+ *    produce O = 0, lse = -inf and zero gradients;
+ *  - GQA: query head h reads kv head h / (Hq / Hkv).
+ *  O = softmax(scale * Q K^T + mask) V per (row, head); lse = natural log-sum-exp of the
+ *  scaled, masked scores.  Backward: the gradients of <dO, O> (textbook softmax-attention
+ *  backward), with dK/dV of a kv head summed over its Hq/Hkv query heads.
+ * Layouts (bf16 unless stated, dense row-major):
+ *  Q, O, dO [R, N+1, Hq, dh]; Kt, Vt, dKt, dVt [R, N+1, Hkv, dh]; Kp, Vp, dKp, dVp
+ *  [P_total, Hkv, dh]; lse f32 [R, N+1, Hq]; dQ f32 [R, N+1, Hq, dh].
+ * Limits (else UNSUPPORTED, nothing enqueued): dh == 128, 1 <= N <= 32, Hq % Hkv == 0,
+ * (Hq/Hkv)*(N+1) <= 256.  Data errors OR bits into *status (if non-NULL): STRUCTURE for a
+ * malformed parent array or num_nodes outside [0, N] (that request's rows are treated as
+ * padding), RANGE for a prefix longer than max_prefix (its keys beyond max_prefix are
+ * ignored). */
+typedef struct {
+  int32_t R, N, Hq, Hkv, dh;
+  int32_t max_prefix;            /* host bound on every P_r (sizes the backward grid)    */
+  const int32_t* prefix_off;     /* (dev) int32 [R+1], prefix_off[0] = 0, non-decreasing  */
+  const int32_t* parents;        /* (dev) int32 [R,N] or NULL (chain)                    */
+  const int32_t* num_nodes;      /* (dev) int32 [R] or NULL (all N)                      */
+  float scale;                   /* softmax scale; <= 0 means 1/sqrt(dh)                 */
+  uint32_t* status;              /* (dev) optional OR-accumulated status word            */
+} aurora_tree_attn_t;
+
+aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, const void* Q, const void* Kt,
+                                     const void* Vt, const void* Kp, const void* Vp, void* O, float* lse,
+                                     void* stream);
+/* Scratch of the backward: 4 B per (row, query head) (the rowsum(dO * O) terms). */
+size_t aurora_tree_attn_workspace_size(const aurora_tree_attn_t* ta);
+/* dKp/dVp/dKt/dVt are overwritten (every element: keys nobody attends get 0). */
+aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, const void* Q, const void* Kt,
+                                     const void* Vt, const void* Kp, const void* Vp, const void* O,
+                                     const float* lse, const void* dO, float* dQ, void* dKt, void* dVt,
+                                     void* dKp, void* dVp, void* ws, size_t ws_bytes, void* stream);
+
 /* Per-phase device timing (CUDA events recorded on the caller's stream around each
  * phase while enabled).  aurora_profile_read must be called after the stream was
  * synchronised; it fills up to `max` (name, total ms, launches) triples and returns

@@ -28,7 +28,8 @@ EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fw
            "aurora_build_info", "aurora_launch_count", "aurora_profile_enable", "aurora_profile_read",
            "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option",
            "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step",
-           "aurora_profile_peek", "aurora_spec_loss_bwd_adamw"]
+           "aurora_profile_peek", "aurora_spec_loss_bwd_adamw", "aurora_tree_attn_fwd",
+           "aurora_tree_attn_workspace_size", "aurora_tree_attn_bwd"]
 
 
 class AuroraError(RuntimeError):
@@ -67,6 +68,12 @@ class aurora_labels_t(C.Structure):
 class aurora_adamw_cfg_t(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
                 ("weight_decay", C.c_float), ("max_grad_norm", C.c_float), ("warmup_steps", C.c_int32)]
+
+
+class aurora_tree_attn_t(C.Structure):
+    _fields_ = [("R", C.c_int32), ("N", C.c_int32), ("Hq", C.c_int32), ("Hkv", C.c_int32), ("dh", C.c_int32),
+                ("max_prefix", C.c_int32), ("prefix_off", C.c_void_p), ("parents", C.c_void_p),
+                ("num_nodes", C.c_void_p), ("scale", C.c_float), ("status", C.c_void_p)]
 
 
 _lib = None
@@ -128,6 +135,12 @@ def lib() -> C.CDLL:
     L.aurora_adamw_step.argtypes = [vp, vp, vp, vp, vp, i64, i64, C.POINTER(aurora_adamw_cfg_t), vp, vp, vp, sz, vp,
                                     vp]
     L.aurora_set_option.restype = C.c_int
+    L.aurora_tree_attn_fwd.argtypes = [C.POINTER(aurora_tree_attn_t), vp, vp, vp, vp, vp, vp, vp, vp]
+    L.aurora_tree_attn_fwd.restype = C.c_int
+    L.aurora_tree_attn_workspace_size.argtypes = [C.POINTER(aurora_tree_attn_t)]
+    L.aurora_tree_attn_workspace_size.restype = sz
+    L.aurora_tree_attn_bwd.argtypes = [C.POINTER(aurora_tree_attn_t)] + [vp] * 14 + [sz, vp]
+    L.aurora_tree_attn_bwd.restype = C.c_int
     L.aurora_get_option.argtypes = [C.c_char_p]
     L.aurora_get_option.restype = C.c_int64
     _lib = L
@@ -396,3 +409,47 @@ class SpecTrainStep:
             _ptr(H), _ptr(W), self.M, self.d, self.V_local, self.vocab_offset, C.byref(self.labels),
             _ptr(self.row_lse), _ptr(dloss), _ptr(r), len(rows), _ptr(out), _stream(stream)))
         return out
+
+
+# ----------------------------------------------------------------------------- NEXT F4
+class TreeAttention:
+    """Tree attention of the draft layer (include/aurora.h aurora_tree_attn_*).
+
+    Marshalling only: holds the batch structure (prefix offsets, parents, node counts, all
+    device int32) and the device status word / backward workspace, and calls the library.
+    Q/O/dO bf16 [R, N+1, Hq, dh]; Kt/Vt bf16 [R, N+1, Hkv, dh]; Kp/Vp bf16 [P_total, Hkv, dh];
+    lse f32 [R, N+1, Hq]; dQ f32 like Q; dK*/dV* bf16 like their inputs."""
+
+    def __init__(self, R: int, N: int, Hq: int, Hkv: int, dh: int, prefix_off, max_prefix: int,
+                 parents=None, num_nodes=None, scale: float = 0.0, device=None):
+        import torch
+        dev = device or prefix_off.device
+        _expect(prefix_off, "i32", "prefix_off")
+        _expect(parents, "i32", "parents")
+        _expect(num_nodes, "i32", "num_nodes")
+        self.R, self.N, self.Hq, self.Hkv, self.dh = R, N, Hq, Hkv, dh
+        self.prefix_off, self.parents, self.num_nodes = prefix_off, parents, num_nodes
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.cfg = aurora_tree_attn_t(R, N, Hq, Hkv, dh, int(max_prefix), _ptr(prefix_off), _ptr(parents),
+                                      _ptr(num_nodes), float(scale), _ptr(self.status))
+        nbytes = int(lib().aurora_tree_attn_workspace_size(C.byref(self.cfg)))
+        self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+
+    def forward(self, Q, Kt, Vt, Kp, Vp, O, lse, stream=None):
+        for t, n in [(Q, "Q"), (Kt, "Kt"), (Vt, "Vt"), (Kp, "Kp"), (Vp, "Vp"), (O, "O")]:
+            _expect(t, "bf16", n)
+        _expect(lse, "f32", "lse")
+        _check("aurora_tree_attn_fwd", lib().aurora_tree_attn_fwd(
+            C.byref(self.cfg), _ptr(Q), _ptr(Kt), _ptr(Vt), _ptr(Kp), _ptr(Vp), _ptr(O), _ptr(lse),
+            _stream(stream)))
+
+    def backward(self, Q, Kt, Vt, Kp, Vp, O, lse, dO, dQ, dKt, dVt, dKp, dVp, stream=None):
+        for t, n in [(Q, "Q"), (Kt, "Kt"), (Vt, "Vt"), (Kp, "Kp"), (Vp, "Vp"), (O, "O"), (dO, "dO"),
+                     (dKt, "dKt"), (dVt, "dVt"), (dKp, "dKp"), (dVp, "dVp")]:
+            _expect(t, "bf16", n)
+        _expect(lse, "f32", "lse")
+        _expect(dQ, "f32", "dQ")
+        _check("aurora_tree_attn_bwd", lib().aurora_tree_attn_bwd(
+            C.byref(self.cfg), _ptr(Q), _ptr(Kt), _ptr(Vt), _ptr(Kp), _ptr(Vp), _ptr(O), _ptr(lse), _ptr(dO),
+            _ptr(dQ), _ptr(dKt), _ptr(dVt), _ptr(dKp), _ptr(dVp), _ptr(self.ws), self.ws.numel(),
+            _stream(stream)))

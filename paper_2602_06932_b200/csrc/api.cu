@@ -29,7 +29,8 @@ cudaEvent_t ev_get() {
   return e;
 }
 const char* kPhaseNames[PH_COUNT] = {"target_scan", "verify", "fwd_gemm", "fwd_combine", "bwd_dz_gemm",
-                                     "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm", "bwd_fused", "adamw"};
+                                     "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm", "bwd_fused", "adamw",
+                                     "tree_attn_fwd", "tree_attn_bwd_dq", "tree_attn_bwd_dkdv"};
 }  // namespace
 
 // Inside a CUDA-graph capture the phase events become external event-record nodes, so

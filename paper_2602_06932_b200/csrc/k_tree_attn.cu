@@ -1,0 +1,726 @@
+// k_tree_attn.cu — NEXT F4: tree attention of the draft layer, forward and backward.
+//
+// P:163-169 §3.2 "Efficient Tree Attention": one batched pass over every accepted and
+// rejected branch with a mask that follows the speculative tree (parents[n] < n).
+// Row s of request r (s = 0 root, s = n+1 draft node n) attends the P_r cached prefix
+// positions of its request and the tree rows of its ancestor closure (F4-R1..R5).
+//
+// Work decomposition (one launch per phase, no atomics, deterministic):
+//   k_ta_fwd    CTA = (request, kv head, query-head chunk): the G query heads of a kv head
+//               share every K/V tile they read (GQA), so a tile of 64 keys is loaded once for
+//               up to 128 query rows = (heads x tree rows); warp = 16 query rows; online
+//               softmax (FA2-style), K/V double-buffered through cp.async; O staged through
+//               shared memory for 16-B stores; lse in natural log.
+//   k_ta_dsum   warp per (row, head): Dsum = rowsum(dO * O) (fp32).
+//   k_ta_bwd_dq the forward's decomposition: recompute S, P = exp(S - lse), dP = dO V^T,
+//               dS = P (dP - Dsum), dQ += dS K (fp32 out).
+//   k_ta_bwd_dkdv CTA = (128-key tile, kv head, request): 8 warps x 16 keys; every query
+//               row of the request that can see the tile (all G heads x N+1 rows, streamed in
+//               32-row chunks) is in the CTA, so dK/dV of a key are complete in one CTA and
+//               are written once as bf16 — the G-head GQA sum happens in registers.
+// Tensor cores: mma.sync m16n8k16 bf16 (fp32 accumulate) with ldmatrix from 128-B-XOR
+// swizzled shared tiles (conflict-free).  The tcgen05 (TMEM) version is the next step
+// (DESIGN.md §6): at these shapes the phase is close to HBM-bound on the prefix K/V.
+#include <cmath>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace aur {
+namespace {
+
+constexpr int D = 128;        // head dim
+constexpr int ROWB = 2 * D;   // bytes per K/V/Q row
+constexpr int KT = 64;        // keys per tile (row-owner kernels)
+constexpr int KT2 = 128;      // keys per CTA (dK/dV kernel)
+constexpr int QC = 32;        // query rows per streamed chunk (dK/dV kernel)
+constexpr int kMaxRowsCta = 128;
+constexpr int kMaxRowsReq = 256;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct TaParams {
+  const uint16_t *Q, *Kt, *Vt, *Kp, *Vp, *O, *dO;
+  const float* lse;
+  const float* Dsum;
+  uint16_t* Oout;
+  float* lse_out;
+  float* dQ;
+  uint16_t *dKt, *dVt, *dKp, *dVp;
+  const int32_t *prefix_off, *parents, *num_nodes;
+  uint32_t* status;
+  int R, N, N1, Hq, Hkv, G, Gc, max_prefix;
+  float scale, c2;  // c2 = scale * log2(e)
+};
+
+__device__ __forceinline__ uint32_t swz(int row, int ch) { return row * ROWB + ((ch ^ (row & 7)) << 4); }
+
+__device__ __forceinline__ void cp16(uint32_t s, const void* g, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int n>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(n) : "memory");
+}
+__device__ __forceinline__ void ldsm4(uint32_t (&r)[4], uint32_t a) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t (&r)[4], uint32_t a) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pk_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+
+// Prefix extent of request r (clamped to max_prefix; a violation is flagged by the caller).
+__device__ __forceinline__ void prefix_of(const TaParams& p, int r, int& p0, int& Pr, bool flag) {
+  p0 = p.prefix_off[r];
+  int len = p.prefix_off[r + 1] - p0;
+  if (len < 0 || len > p.max_prefix) {
+    if (flag && p.status) atomicOr(p.status, (uint32_t)AURORA_STATUS_RANGE);
+    len = len < 0 ? 0 : p.max_prefix;
+  }
+  Pr = len;
+}
+
+// anc[s] (bit t = tree row t visible from row s), threads 0..N1-1.  0 = padded/malformed row.
+__device__ void build_anc(const TaParams& p, int r, uint64_t* anc) {
+  const int s = threadIdx.x;
+  if (s >= p.N1) return;
+  const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
+  bool bad = nn < 0 || nn > p.N;
+  uint64_t m = 0;
+  if (!bad) {
+    if (s == 0) {
+      m = 1ull;
+    } else if (s - 1 < nn) {
+      int cur = s - 1;
+      m = 1ull | (1ull << s);
+      for (int it = 0; it <= p.N; ++it) {
+        const int par = p.parents ? p.parents[(size_t)r * p.N + cur] : cur - 1;
+        if (par < -1 || par >= cur) { bad = true; break; }
+        if (par < 0) break;
+        m |= 1ull << (par + 1);
+        cur = par;
+      }
+    }
+  }
+  if (bad && p.status) atomicOr(p.status, (uint32_t)AURORA_STATUS_STRUCTURE);
+  anc[s] = bad ? 0ull : m;
+}
+
+__device__ __forceinline__ bool visible(uint64_t a, int kj, int Pr, int N1) {
+  const int t = kj - Pr;
+  return a != 0ull && (kj < Pr || (t < N1 && ((a >> t) & 1ull)));
+}
+
+// cp.async one K and one V tile of `nrows` keys starting at key0 (zero-filled past nkeys).
+__device__ __forceinline__ void load_kv(const TaParams& p, uint32_t sK, uint32_t sV, int nrows, int key0, int nkeys,
+                                        int Pr, int p0, int r, int hk) {
+  for (int idx = threadIdx.x; idx < nrows * 16; idx += blockDim.x) {
+    const int row = idx >> 4, ch = idx & 15, kj = key0 + row;
+    const uint16_t *ks = p.Kt, *vs = p.Vt;
+    int bytes = 0;
+    if (kj < nkeys) {
+      bytes = 16;
+      size_t off;
+      if (kj < Pr) {
+        off = ((size_t)(p0 + kj) * p.Hkv + hk) * D + ch * 8;
+        ks = p.Kp + off;
+        vs = p.Vp + off;
+      } else {
+        off = (((size_t)r * p.N1 + (kj - Pr)) * p.Hkv + hk) * D + ch * 8;
+        ks = p.Kt + off;
+        vs = p.Vt + off;
+      }
+    }
+    cp16(sK + swz(row, ch), ks, bytes);
+    cp16(sV + swz(row, ch), vs, bytes);
+  }
+}
+
+// cp.async query-ordered rows [i0, i0+nrows) of a [R, N1, Hq, D] tensor for heads h0.. into
+// smem rows 0..nrows-1 (zero past `rows`).  Row i -> (g = i / N1, s = i % N1).
+__device__ __forceinline__ void load_rows(const TaParams& p, const uint16_t* X, uint32_t sX, int i0, int nrows,
+                                          int rows, int r, int h0) {
+  for (int idx = threadIdx.x; idx < nrows * 16; idx += blockDim.x) {
+    const int row = idx >> 4, ch = idx & 15, i = i0 + row;
+    const uint16_t* src = X;
+    int bytes = 0;
+    if (i < rows) {
+      const int g = i / p.N1, s = i - g * p.N1;
+      src = X + (((size_t)r * p.N1 + s) * p.Hq + h0 + g) * D + ch * 8;
+      bytes = 16;
+    }
+    cp16(sX + swz(row, ch), src, bytes);
+  }
+}
+
+// S[16 x 64] (+)= A[16 rows of sA from arow0] . B[64 rows of sB]^T over D (both row-major).
+__device__ __forceinline__ void mma_rows_x_keys(float (&s)[8][4], uint32_t sA, int arow0, uint32_t sB, int lane) {
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    uint32_t a[4];
+    ldsm4(a, sA + swz(arow0 + (lane & 7) + (((lane >> 3) & 1) << 3), 2 * ks + (lane >> 4)));
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+      uint32_t b[4];
+      ldsm4(b, sB + swz(np * 16 + (lane & 7) + ((lane >> 4) << 3), 2 * ks + ((lane >> 3) & 1)));
+      mma16816(s[2 * np], a, b[0], b[1]);
+      mma16816(s[2 * np + 1], a, b[2], b[3]);
+    }
+  }
+}
+
+// acc[16 x 128] += P[16 x 64] (C fragments, cast to bf16) . B[64 rows of sB, 128 cols].
+__device__ __forceinline__ void mma_p_x_rows(float (&acc)[16][4], const float (&pf)[8][4], uint32_t sB, int lane) {
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    uint32_t a[4] = {pk_bf16(pf[2 * kk][0], pf[2 * kk][1]), pk_bf16(pf[2 * kk][2], pf[2 * kk][3]),
+                     pk_bf16(pf[2 * kk + 1][0], pf[2 * kk + 1][1]), pk_bf16(pf[2 * kk + 1][2], pf[2 * kk + 1][3])};
+#pragma unroll
+    for (int np = 0; np < 8; ++np) {
+      uint32_t b[4];
+      ldsm4t(b, sB + swz(kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), 2 * np + (lane >> 4)));
+      mma16816(acc[2 * np], a, b[0], b[1]);
+      mma16816(acc[2 * np + 1], a, b[2], b[3]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ forward
+__global__ void __launch_bounds__(256) k_ta_fwd(TaParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int r = blockIdx.x, hk = blockIdx.y, hc = blockIdx.z;
+  const int h0 = hk * p.G + hc * p.Gc;
+  const int nh = min(p.Gc, p.G - hc * p.Gc);
+  const int rows = nh * p.N1;
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + nw * 16 * ROWB;
+  uint8_t* sV = sK + 2 * KT * ROWB;
+  uint64_t* anc = reinterpret_cast<uint64_t*>(sV + 2 * KT * ROWB);
+  const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
+
+  int p0, Pr;
+  prefix_of(p, r, p0, Pr, threadIdx.x == 0 && hk == 0 && hc == 0);
+  const int nkeys = Pr + p.N1, ntiles = (nkeys + KT - 1) / KT;
+  build_anc(p, r, anc);
+  load_rows(p, p.Q, aQ, 0, nw * 16, rows, r, h0);
+  load_kv(p, aK, aV, KT, 0, nkeys, Pr, p0, r, hk);
+  cp_commit();
+
+  const int i0 = warp * 16 + (lane >> 2), i1 = i0 + 8;
+  uint64_t a0 = 0, a1 = 0;
+  float o[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  for (int t = 0; t < ntiles; ++t) {
+    if (t + 1 < ntiles) {
+      load_kv(p, aK + ((t + 1) & 1) * KT * ROWB, aV + ((t + 1) & 1) * KT * ROWB, KT, (t + 1) * KT, nkeys, Pr, p0, r, hk);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    if (t == 0) {
+      if (i0 < rows) a0 = anc[i0 % p.N1];
+      if (i1 < rows) a1 = anc[i1 % p.N1];
+    }
+    const uint32_t kb = aK + (t & 1) * KT * ROWB, vb = aV + (t & 1) * KT * ROWB;
+    float s[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+    mma_rows_x_keys(s, aQ, warp * 16, kb, lane);
+
+    const int key0 = t * KT + 2 * (lane & 3);
+    float mx0 = m0, mx1 = m1;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kj = key0 + nt * 8 + (e & 1);
+        const bool ok = visible(e < 2 ? a0 : a1, kj, Pr, p.N1);
+        s[nt][e] = ok ? s[nt][e] * p.c2 : -INFINITY;
+      }
+      mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][1]));
+      mx1 = fmaxf(mx1, fmaxf(s[nt][2], s[nt][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float ms0 = mx0 == -INFINITY ? 0.f : mx0, ms1 = mx1 == -INFINITY ? 0.f : mx1;
+    const float al0 = ex2_approx(m0 - ms0), al1 = ex2_approx(m1 - ms1);  // m = -inf -> 0
+    m0 = mx0;
+    m1 = mx1;
+    float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      s[nt][0] = ex2_approx(s[nt][0] - ms0);
+      s[nt][1] = ex2_approx(s[nt][1] - ms0);
+      s[nt][2] = ex2_approx(s[nt][2] - ms1);
+      s[nt][3] = ex2_approx(s[nt][3] - ms1);
+      ls0 += s[nt][0] + s[nt][1];
+      ls1 += s[nt][2] + s[nt][3];
+    }
+    l0 = l0 * al0 + ls0;
+    l1 = l1 * al1 + ls1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      o[j][0] *= al0;
+      o[j][1] *= al0;
+      o[j][2] *= al1;
+      o[j][3] *= al1;
+    }
+    mma_p_x_rows(o, s, vb, lane);
+    __syncthreads();
+  }
+
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
+  // stage the warp's 16 output rows (bf16) in its own rows of sQ, then 16-B stores
+  const int lr0 = warp * 16 + (lane >> 2);
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    sts32(aQ + swz(lr0, nt) + (lane & 3) * 4, pk_bf16(o[nt][0] * inv0, o[nt][1] * inv0));
+    sts32(aQ + swz(lr0 + 8, nt) + (lane & 3) * 4, pk_bf16(o[nt][2] * inv1, o[nt][3] * inv1));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = lane; c < 16 * 16; c += 32) {
+    const int row = warp * 16 + (c >> 4), ch = c & 15;
+    if (row < rows) {
+      const int g = row / p.N1, s = row - g * p.N1;
+      *reinterpret_cast<uint4*>(p.Oout + (((size_t)r * p.N1 + s) * p.Hq + h0 + g) * D + ch * 8) =
+          lds_u4(aQ + swz(row, ch));
+    }
+  }
+  if ((lane & 3) == 0) {
+    if (i0 < rows) {
+      const int g = i0 / p.N1, s = i0 - g * p.N1;
+      p.lse_out[((size_t)r * p.N1 + s) * p.Hq + h0 + g] = l0 > 0.f ? (m0 + __log2f(l0)) * kLn2 : -INFINITY;
+    }
+    if (i1 < rows) {
+      const int g = i1 / p.N1, s = i1 - g * p.N1;
+      p.lse_out[((size_t)r * p.N1 + s) * p.Hq + h0 + g] = l1 > 0.f ? (m1 + __log2f(l1)) * kLn2 : -INFINITY;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ backward
+__global__ void __launch_bounds__(256) k_ta_dsum(const uint16_t* __restrict__ O, const uint16_t* __restrict__ dO,
+                                                 float* __restrict__ Dsum, int64_t n_rows) {
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= n_rows) return;
+  const uint2 o = *reinterpret_cast<const uint2*>(O + w * D + lane * 4);
+  const uint2 g = *reinterpret_cast<const uint2*>(dO + w * D + lane * 4);
+  const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&o);
+  const __nv_bfloat162* gb = reinterpret_cast<const __nv_bfloat162*>(&g);
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const float2 a = __bfloat1622float2(ob[j]), b = __bfloat1622float2(gb[j]);
+    acc += a.x * b.x + a.y * b.y;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) Dsum[w] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_ta_bwd_dq(TaParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int r = blockIdx.x, hk = blockIdx.y, hc = blockIdx.z;
+  const int h0 = hk * p.G + hc * p.Gc;
+  const int nh = min(p.Gc, p.G - hc * p.Gc);
+  const int rows = nh * p.N1;
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sQ = smem;
+  uint8_t* sdO = sQ + nw * 16 * ROWB;
+  uint8_t* sK = sdO + nw * 16 * ROWB;
+  uint8_t* sV = sK + 2 * KT * ROWB;
+  uint64_t* anc = reinterpret_cast<uint64_t*>(sV + 2 * KT * ROWB);
+  const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), aK = smem_u32(sK), aV = smem_u32(sV);
+
+  int p0, Pr;
+  prefix_of(p, r, p0, Pr, false);
+  const int nkeys = Pr + p.N1, ntiles = (nkeys + KT - 1) / KT;
+  build_anc(p, r, anc);
+  load_rows(p, p.Q, aQ, 0, nw * 16, rows, r, h0);
+  load_rows(p, p.dO, adO, 0, nw * 16, rows, r, h0);
+  load_kv(p, aK, aV, KT, 0, nkeys, Pr, p0, r, hk);
+  cp_commit();
+
+  const int i0 = warp * 16 + (lane >> 2), i1 = i0 + 8;
+  uint64_t a0 = 0, a1 = 0;
+  float lse0 = 0.f, lse1 = 0.f, d0 = 0.f, d1 = 0.f;
+  if (i0 < rows) {
+    const int g = i0 / p.N1, s = i0 - g * p.N1;
+    const size_t k = ((size_t)r * p.N1 + s) * p.Hq + h0 + g;
+    lse0 = p.lse[k] * kLog2e;
+    d0 = p.Dsum[k];
+  }
+  if (i1 < rows) {
+    const int g = i1 / p.N1, s = i1 - g * p.N1;
+    const size_t k = ((size_t)r * p.N1 + s) * p.Hq + h0 + g;
+    lse1 = p.lse[k] * kLog2e;
+    d1 = p.Dsum[k];
+  }
+  float dq[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
+
+  for (int t = 0; t < ntiles; ++t) {
+    if (t + 1 < ntiles) {
+      load_kv(p, aK + ((t + 1) & 1) * KT * ROWB, aV + ((t + 1) & 1) * KT * ROWB, KT, (t + 1) * KT, nkeys, Pr, p0, r, hk);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    if (t == 0) {
+      if (i0 < rows) a0 = anc[i0 % p.N1];
+      if (i1 < rows) a1 = anc[i1 % p.N1];
+    }
+    const uint32_t kb = aK + (t & 1) * KT * ROWB, vb = aV + (t & 1) * KT * ROWB;
+    float s[8][4], dp[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+      dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
+    }
+    mma_rows_x_keys(s, aQ, warp * 16, kb, lane);
+    mma_rows_x_keys(dp, adO, warp * 16, vb, lane);
+    const int key0 = t * KT + 2 * (lane & 3);
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kj = key0 + nt * 8 + (e & 1);
+        const bool lo = e < 2;
+        const bool ok = visible(lo ? a0 : a1, kj, Pr, p.N1);
+        const float pv = ok ? ex2_approx(s[nt][e] * p.c2 - (lo ? lse0 : lse1)) : 0.f;
+        s[nt][e] = pv * (dp[nt][e] - (lo ? d0 : d1));  // dS
+      }
+    }
+    mma_p_x_rows(dq, s, kb, lane);  // dQ += dS K
+    __syncthreads();
+  }
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int i = half ? i1 : i0;
+    if (i >= rows) continue;
+    const int g = i / p.N1, s = i - g * p.N1;
+    float* dst = p.dQ + (((size_t)r * p.N1 + s) * p.Hq + h0 + g) * D + 2 * (lane & 3);
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+      *reinterpret_cast<float2*>(dst + nt * 8) =
+          make_float2(dq[nt][2 * half] * p.scale, dq[nt][2 * half + 1] * p.scale);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tile = blockIdx.x, hk = blockIdx.y, r = blockIdx.z;
+  int p0, Pr;
+  prefix_of(p, r, p0, Pr, false);
+  const int nkeys = Pr + p.N1, key0 = tile * KT2;
+  if (key0 >= nkeys) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rows = p.G * p.N1, nchunks = (rows + QC - 1) / QC;
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + KT2 * ROWB;
+  uint8_t* sQ = sV + KT2 * ROWB;        // 2 stages x QC rows
+  uint8_t* sdO = sQ + 2 * QC * ROWB;    // 2 stages x QC rows
+  uint64_t* anc = reinterpret_cast<uint64_t*>(sdO + 2 * QC * ROWB);  // [40]
+  uint64_t* ancr = anc + 40;                                          // [kMaxRowsReq]
+  float* lse2 = reinterpret_cast<float*>(ancr + kMaxRowsReq);
+  float* dsum = lse2 + kMaxRowsReq;
+  const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
+  const int h0 = hk * p.G;
+
+  build_anc(p, r, anc);
+  load_kv(p, aK, aV, KT2, key0, nkeys, Pr, p0, r, hk);
+  load_rows(p, p.Q, aQ, 0, QC, rows, r, h0);
+  load_rows(p, p.dO, adO, 0, QC, rows, r, h0);
+  cp_commit();
+  __syncthreads();  // anc visible
+  for (int i = threadIdx.x; i < nchunks * QC; i += blockDim.x) {
+    uint64_t a = 0;
+    float l = 0.f, dd = 0.f;
+    if (i < rows) {
+      const int g = i / p.N1, s = i - g * p.N1;
+      const size_t k = ((size_t)r * p.N1 + s) * p.Hq + h0 + g;
+      a = anc[s];
+      l = p.lse[k] * kLog2e;
+      dd = p.Dsum[k];
+    }
+    ancr[i] = a;
+    lse2[i] = l;
+    dsum[i] = dd;
+  }
+
+  float dv[16][4], dk[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
+    dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = 0.f;
+  }
+  const int kw = warp * 16;                       // this warp's keys within the tile
+  const int kj0 = key0 + kw + (lane >> 2), kj1 = kj0 + 8;
+
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      const int st = (c + 1) & 1;
+      load_rows(p, p.Q, aQ + st * QC * ROWB, (c + 1) * QC, QC, rows, r, h0);
+      load_rows(p, p.dO, adO + st * QC * ROWB, (c + 1) * QC, QC, rows, r, h0);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const uint32_t qb = aQ + (c & 1) * QC * ROWB, gb = adO + (c & 1) * QC * ROWB;
+    // S^T [16 keys x 32 rows] = K_w Q^T ; dP^T = V_w dO^T
+    float s[4][4], dp[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+      dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t ak[4], av[4];
+      const int arow = kw + (lane & 7) + (((lane >> 3) & 1) << 3), ach = 2 * ks + (lane >> 4);
+      ldsm4(ak, aK + swz(arow, ach));
+      ldsm4(av, aV + swz(arow, ach));
+#pragma unroll
+      for (int np = 0; np < 2; ++np) {
+        uint32_t b[4];
+        const int brow = np * 16 + (lane & 7) + ((lane >> 4) << 3), bch = 2 * ks + ((lane >> 3) & 1);
+        ldsm4(b, qb + swz(brow, bch));
+        mma16816(s[2 * np], ak, b[0], b[1]);
+        mma16816(s[2 * np + 1], ak, b[2], b[3]);
+        ldsm4(b, gb + swz(brow, bch));
+        mma16816(dp[2 * np], av, b[0], b[1]);
+        mma16816(dp[2 * np + 1], av, b[2], b[3]);
+      }
+    }
+    // P^T, dS^T (C layout: rows = keys kj0/kj1, cols = query rows)
+    const int qcol = c * QC + 2 * (lane & 3);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = qcol + nt * 8 + (e & 1);
+        const bool ok = visible(ancr[i], e < 2 ? kj0 : kj1, Pr, p.N1);
+        const float pv = ok ? ex2_approx(s[nt][e] * p.c2 - lse2[i]) : 0.f;
+        s[nt][e] = pv;
+        dp[nt][e] = pv * (dp[nt][e] - dsum[i]);
+      }
+    }
+    // dV += P^T dO ; dK += dS^T Q   (k = the chunk's 32 query rows)
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t ap[4] = {pk_bf16(s[2 * kk][0], s[2 * kk][1]), pk_bf16(s[2 * kk][2], s[2 * kk][3]),
+                              pk_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]), pk_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+      const uint32_t ad[4] = {pk_bf16(dp[2 * kk][0], dp[2 * kk][1]), pk_bf16(dp[2 * kk][2], dp[2 * kk][3]),
+                              pk_bf16(dp[2 * kk + 1][0], dp[2 * kk + 1][1]),
+                              pk_bf16(dp[2 * kk + 1][2], dp[2 * kk + 1][3])};
+#pragma unroll
+      for (int np = 0; np < 8; ++np) {
+        uint32_t b[4];
+        const int brow = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), bch = 2 * np + (lane >> 4);
+        ldsm4t(b, gb + swz(brow, bch));
+        mma16816(dv[2 * np], ap, b[0], b[1]);
+        mma16816(dv[2 * np + 1], ap, b[2], b[3]);
+        ldsm4t(b, qb + swz(brow, bch));
+        mma16816(dk[2 * np], ad, b[0], b[1]);
+        mma16816(dk[2 * np + 1], ad, b[2], b[3]);
+      }
+    }
+    __syncthreads();
+  }
+  // stage bf16 dK (scaled) / dV rows in sK / sV (every warp is past its last read), then 16-B stores
+  const int lr = kw + (lane >> 2);
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    sts32(aK + swz(lr, nt) + (lane & 3) * 4, pk_bf16(dk[nt][0] * p.scale, dk[nt][1] * p.scale));
+    sts32(aK + swz(lr + 8, nt) + (lane & 3) * 4, pk_bf16(dk[nt][2] * p.scale, dk[nt][3] * p.scale));
+    sts32(aV + swz(lr, nt) + (lane & 3) * 4, pk_bf16(dv[nt][0], dv[nt][1]));
+    sts32(aV + swz(lr + 8, nt) + (lane & 3) * 4, pk_bf16(dv[nt][2], dv[nt][3]));
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < KT2 * 16; idx += blockDim.x) {
+    const int row = idx >> 4, ch = idx & 15, kj = key0 + row;
+    if (kj >= nkeys) continue;
+    size_t off;
+    uint16_t *dk_dst, *dv_dst;
+    if (kj < Pr) {
+      off = ((size_t)(p0 + kj) * p.Hkv + hk) * D + ch * 8;
+      dk_dst = p.dKp;
+      dv_dst = p.dVp;
+    } else {
+      off = (((size_t)r * p.N1 + (kj - Pr)) * p.Hkv + hk) * D + ch * 8;
+      dk_dst = p.dKt;
+      dv_dst = p.dVt;
+    }
+    *reinterpret_cast<uint4*>(dk_dst + off) = lds_u4(aK + swz(row, ch));
+    *reinterpret_cast<uint4*>(dv_dst + off) = lds_u4(aV + swz(row, ch));
+  }
+}
+
+// ------------------------------------------------------------------------------ host
+struct TaLaunch {
+  int Gc, nchunk, nw;
+};
+
+aurora_status_t ta_check(const aurora_tree_attn_t* ta) {
+  if (!ta || !ta->prefix_off) return AURORA_ERR_INVALID_ARG;
+  if (ta->R < 1 || ta->N < 1 || ta->Hq < 1 || ta->Hkv < 1 || ta->max_prefix < 0) return AURORA_ERR_INVALID_ARG;
+  if (ta->Hq % ta->Hkv) return AURORA_ERR_INVALID_ARG;
+  if (ta->R > 65535 || ta->Hkv > 65535) return AURORA_ERR_UNSUPPORTED;
+  if (ta->dh != D || ta->N > AURORA_MAX_NODES) return AURORA_ERR_UNSUPPORTED;
+  if ((ta->Hq / ta->Hkv) * (ta->N + 1) > kMaxRowsReq) return AURORA_ERR_UNSUPPORTED;
+  return AURORA_OK;
+}
+
+TaParams ta_params(const aurora_tree_attn_t* ta, TaLaunch& L) {
+  TaParams p{};
+  p.R = ta->R;
+  p.N = ta->N;
+  p.N1 = ta->N + 1;
+  p.Hq = ta->Hq;
+  p.Hkv = ta->Hkv;
+  p.G = ta->Hq / ta->Hkv;
+  p.max_prefix = ta->max_prefix;
+  p.scale = ta->scale > 0.f ? ta->scale : 1.f / sqrtf((float)D);
+  p.c2 = p.scale * kLog2e;
+  p.prefix_off = ta->prefix_off;
+  p.parents = ta->parents;
+  p.num_nodes = ta->num_nodes;
+  p.status = ta->status;
+  L.Gc = std::min(p.G, kMaxRowsCta / p.N1);
+  L.nchunk = (p.G + L.Gc - 1) / L.Gc;
+  L.nw = (L.Gc * p.N1 + 15) / 16;
+  p.Gc = L.Gc;
+  return p;
+}
+
+size_t smem_fwd(int nw) { return (size_t)nw * 16 * ROWB + 4 * KT * ROWB + 40 * 8; }
+size_t smem_dq(int nw) { return (size_t)2 * nw * 16 * ROWB + 4 * KT * ROWB + 40 * 8; }
+constexpr size_t kSmemDkdv = 2 * KT2 * ROWB + 4 * QC * ROWB + 40 * 8 + kMaxRowsReq * 16;
+
+}  // namespace
+}  // namespace aur
+
+using namespace aur;
+
+extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, const void* Q, const void* Kt,
+                                                const void* Vt, const void* Kp, const void* Vp, void* O, float* lse,
+                                                void* stream) {
+  aurora_status_t st = ta_check(ta);
+  if (st != AURORA_OK) return st;
+  if (!Q || !Kt || !Vt || !O || !lse) return AURORA_ERR_INVALID_ARG;
+  if (ta->max_prefix > 0 && (!Kp || !Vp)) return AURORA_ERR_INVALID_ARG;
+  TaLaunch L;
+  TaParams p = ta_params(ta, L);
+  p.Q = (const uint16_t*)Q;
+  p.Kt = (const uint16_t*)Kt;
+  p.Vt = (const uint16_t*)Vt;
+  p.Kp = (const uint16_t*)Kp;
+  p.Vp = (const uint16_t*)Vp;
+  p.Oout = (uint16_t*)O;
+  p.lse_out = lse;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm = smem_fwd(L.nw);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ta_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd(8));
+    attr = true;
+  }
+  prof_begin(PH_TREE_FWD, s);
+  k_ta_fwd<<<dim3(p.R, p.Hkv, L.nchunk), L.nw * 32, sm, s>>>(p);
+  count_launch();
+  prof_end(PH_TREE_FWD, s);
+  return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
+}
+
+extern "C" size_t aurora_tree_attn_workspace_size(const aurora_tree_attn_t* ta) {
+  if (!ta) return 0;
+  return (size_t)ta->R * (ta->N + 1) * ta->Hq * sizeof(float) + 256;
+}
+
+extern "C" aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, const void* Q, const void* Kt,
+                                                const void* Vt, const void* Kp, const void* Vp, const void* O,
+                                                const float* lse, const void* dO, float* dQ, void* dKt, void* dVt,
+                                                void* dKp, void* dVp, void* ws, size_t ws_bytes, void* stream) {
+  aurora_status_t st = ta_check(ta);
+  if (st != AURORA_OK) return st;
+  if (!Q || !Kt || !Vt || !O || !lse || !dO || !dQ || !dKt || !dVt) return AURORA_ERR_INVALID_ARG;
+  if (ta->max_prefix > 0 && (!Kp || !Vp || !dKp || !dVp)) return AURORA_ERR_INVALID_ARG;
+  if (!ws || ws_bytes < aurora_tree_attn_workspace_size(ta)) return AURORA_ERR_WORKSPACE;
+  TaLaunch L;
+  TaParams p = ta_params(ta, L);
+  p.Q = (const uint16_t*)Q;
+  p.Kt = (const uint16_t*)Kt;
+  p.Vt = (const uint16_t*)Vt;
+  p.Kp = (const uint16_t*)Kp;
+  p.Vp = (const uint16_t*)Vp;
+  p.O = (const uint16_t*)O;
+  p.dO = (const uint16_t*)dO;
+  p.lse = lse;
+  p.Dsum = (const float*)ws;
+  p.dQ = dQ;
+  p.dKt = (uint16_t*)dKt;
+  p.dVt = (uint16_t*)dVt;
+  p.dKp = (uint16_t*)dKp;
+  p.dVp = (uint16_t*)dVp;
+  cudaStream_t s = (cudaStream_t)stream;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ta_bwd_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dq(8));
+    cudaFuncSetAttribute(k_ta_bwd_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemDkdv);
+    attr = true;
+  }
+  const int64_t n_rows = (int64_t)p.R * p.N1 * p.Hq;
+  prof_begin(PH_TREE_BWD_DQ, s);
+  k_ta_dsum<<<(unsigned)((n_rows + 7) / 8), 256, 0, s>>>(p.O, p.dO, (float*)ws, n_rows);
+  k_ta_bwd_dq<<<dim3(p.R, p.Hkv, L.nchunk), L.nw * 32, smem_dq(L.nw), s>>>(p);
+  prof_end(PH_TREE_BWD_DQ, s);
+  prof_begin(PH_TREE_BWD_DKDV, s);
+  const int ktiles = (ta->max_prefix + p.N1 + KT2 - 1) / KT2;
+  k_ta_bwd_dkdv<<<dim3(ktiles, p.Hkv, p.R), 256, kSmemDkdv, s>>>(p);
+  prof_end(PH_TREE_BWD_DKDV, s);
+  count_launch(3);
+  return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
+}
