@@ -646,8 +646,9 @@ def _ta_work(meta):
     fwd_b = q_b + kv_b + q_b + rows * c.Hq * 4                    # + O + lse
     dq_b = 3 * q_b + rows * c.Hq * 8 + kv_b + 2 * q_b             # Q, dO, O(dsum), lse+Dsum, K/V, dQ fp32
     dkdv_b = kv_b + kv_b + 2 * q_b + rows * c.Hq * 8              # K/V read, dK/dV write, Q/dO, lse/Dsum
+    fused_b = 3 * q_b + rows * c.Hq * 8 + kv_b + 2 * q_b + kv_b   # Q, dO, O, lse+Dsum, K/V, dQ, dK/dV
     return dict(pairs=pairs, fwd_flops=4.0 * c.dh * pairs, bwd_flops=10.0 * c.dh * pairs, fwd_bytes=fwd_b,
-                dq_bytes=dq_b, dkdv_bytes=dkdv_b, rows=rows)
+                dq_bytes=dq_b, dkdv_bytes=dkdv_b, fused_bytes=fused_b, rows=rows)
 
 
 def run_tree_attn(args):
@@ -743,7 +744,8 @@ def run_tree_attn(args):
     per = []
     for k, byts, flops in (("tree_attn_fwd", w["fwd_bytes"], w["fwd_flops"]),
                            ("tree_attn_bwd_dq", w["dq_bytes"], 0.4 * w["bwd_flops"]),
-                           ("tree_attn_bwd_dkdv", w["dkdv_bytes"], 0.6 * w["bwd_flops"])):
+                           ("tree_attn_bwd_dkdv", w["dkdv_bytes"], 0.6 * w["bwd_flops"]),
+                           ("tree_attn_bwd_fused", w["fused_bytes"], w["bwd_flops"])):
         if k in phases and phases[k][1]:
             t = phases[k][0] / args.steps / 1e3
             per.append({"kernel": k, "ms_per_step": round(t * 1e3, 4), "achieved_gbs": round(byts / t / 1e9, 1),

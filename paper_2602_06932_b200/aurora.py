@@ -12,7 +12,7 @@ import os
 from typing import Optional
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libaurora.so")
+LIB_PATH = os.environ.get("AURORA_LIB") or os.path.join(_PKG, "libaurora.so")  # override: A/B experiments
 
 AURORA_OK = 0
 STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "structure", 3: "range", 4: "nonfinite", 5: "unsupported",

@@ -220,8 +220,9 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 // Phase profiling (CUDA events on the caller's stream).
 enum Phase : int { PH_SCAN = 0, PH_VERIFY, PH_FWD_GEMM, PH_FWD_COMBINE, PH_BWD_DZ, PH_BWD_DW, PH_BWD_DH,
                    PH_BWD_REDUCE, PH_COMM, PH_BWD_FUSED, PH_OPTIM, PH_TREE_FWD, PH_TREE_BWD_DQ,
-                   PH_TREE_BWD_DKDV, PH_COUNT };
+                   PH_TREE_BWD_DKDV, PH_TREE_BWD_FUSED, PH_COUNT };
 void prof_begin(int phase, cudaStream_t s);
+int opt_tree_bwd_split();  // aurora_set_option("tree_bwd_split")
 void prof_end(int phase, cudaStream_t s);
 
 }  // namespace aur

@@ -31,10 +31,12 @@ namespace {
 
 constexpr int D = 128;        // head dim
 constexpr int ROWB = 2 * D;   // bytes per K/V/Q row
-constexpr int KT = 64;        // keys per tile (row-owner kernels)
 constexpr int KT2 = 128;      // keys per CTA (dK/dV kernel)
-constexpr int QC = 32;        // query rows per streamed chunk (dK/dV kernel)
-constexpr int kMaxRowsCta = 128;
+#ifndef TA_QC
+#define TA_QC 32
+#endif
+constexpr int QC = TA_QC;     // query rows per streamed chunk (dK/dV kernel)
+constexpr int kMaxRowsCta = 112;  // 7 warps: two CTAs per SM fit the register file
 constexpr int kMaxRowsReq = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -177,14 +179,15 @@ __device__ __forceinline__ void load_rows(const TaParams& p, const uint16_t* X, 
   }
 }
 
-// S[16 x 64] (+)= A[16 rows of sA from arow0] . B[64 rows of sB]^T over D (both row-major).
-__device__ __forceinline__ void mma_rows_x_keys(float (&s)[8][4], uint32_t sA, int arow0, uint32_t sB, int lane) {
+// S[16 x NK] (+)= A[16 rows of sA from arow0] . B[NK rows of sB]^T over D (both row-major).
+template <int NK>
+__device__ __forceinline__ void mma_rows_x_keys(float (&s)[NK / 8][4], uint32_t sA, int arow0, uint32_t sB, int lane) {
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     uint32_t a[4];
     ldsm4(a, sA + swz(arow0 + (lane & 7) + (((lane >> 3) & 1) << 3), 2 * ks + (lane >> 4)));
 #pragma unroll
-    for (int np = 0; np < 4; ++np) {
+    for (int np = 0; np < NK / 16; ++np) {
       uint32_t b[4];
       ldsm4(b, sB + swz(np * 16 + (lane & 7) + ((lane >> 4) << 3), 2 * ks + ((lane >> 3) & 1)));
       mma16816(s[2 * np], a, b[0], b[1]);
@@ -193,10 +196,11 @@ __device__ __forceinline__ void mma_rows_x_keys(float (&s)[8][4], uint32_t sA, i
   }
 }
 
-// acc[16 x 128] += P[16 x 64] (C fragments, cast to bf16) . B[64 rows of sB, 128 cols].
-__device__ __forceinline__ void mma_p_x_rows(float (&acc)[16][4], const float (&pf)[8][4], uint32_t sB, int lane) {
+// acc[16 x 128] += P[16 x NK] (C fragments, cast to bf16) . B[NK rows of sB, 128 cols].
+template <int NK>
+__device__ __forceinline__ void mma_p_x_rows(float (&acc)[16][4], const float (&pf)[NK / 8][4], uint32_t sB, int lane) {
 #pragma unroll
-  for (int kk = 0; kk < 4; ++kk) {
+  for (int kk = 0; kk < NK / 16; ++kk) {
     uint32_t a[4] = {pk_bf16(pf[2 * kk][0], pf[2 * kk][1]), pk_bf16(pf[2 * kk][2], pf[2 * kk][3]),
                      pk_bf16(pf[2 * kk + 1][0], pf[2 * kk + 1][1]), pk_bf16(pf[2 * kk + 1][2], pf[2 * kk + 1][3])};
 #pragma unroll
@@ -210,8 +214,45 @@ __device__ __forceinline__ void mma_p_x_rows(float (&acc)[16][4], const float (&
 }
 
 // ------------------------------------------------------------------------------ forward
-__global__ void __launch_bounds__(256) k_ta_fwd(TaParams p) {
+// K/V ring of ST stages x NK keys.  Every iteration commits exactly one cp.async group (possibly
+// empty), so wait_group<ST-1> always means "tile t has landed".
+template <int NK, int ST>
+__device__ __forceinline__ void kv_prologue(const TaParams& p, uint32_t aK, uint32_t aV, int ntiles, int nkeys, int Pr,
+                                            int p0, int r, int hk) {
+#pragma unroll
+  for (int j = 0; j < ST - 1; ++j) {
+    if (j < ntiles) load_kv(p, aK + j * NK * ROWB, aV + j * NK * ROWB, NK, j * NK, nkeys, Pr, p0, r, hk);
+    cp_commit();
+  }
+}
+template <int NK, int ST>
+__device__ __forceinline__ void kv_next(const TaParams& p, uint32_t aK, uint32_t aV, int t, int ntiles, int nkeys,
+                                        int Pr, int p0, int r, int hk) {
+  const int j = t + ST - 1;
+  if (j < ntiles) load_kv(p, aK + (j % ST) * NK * ROWB, aV + (j % ST) * NK * ROWB, NK, j * NK, nkeys, Pr, p0, r, hk);
+  cp_commit();
+  cp_wait<ST - 1>();
+  __syncthreads();
+}
+
+// Raw scores of keys this warp's rows may not see -> -inf.  Skipped (warp-uniform) for tiles
+// wholly inside the prefix when every row of the warp is a valid query row.
+template <int NK>
+__device__ __forceinline__ void mask_scores(float (&s)[NK / 8][4], bool fast, int key0, uint64_t a0, uint64_t a1,
+                                            int Pr, int N1) {
+  if (fast) return;
+#pragma unroll
+  for (int nt = 0; nt < NK / 8; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (!visible(e < 2 ? a0 : a1, key0 + nt * 8 + (e & 1), Pr, N1)) s[nt][e] = -INFINITY;
+}
+
+constexpr int kFwdNK = 64, kFwdST = 2;
+
+__global__ void __launch_bounds__(224, 2) k_ta_fwd(TaParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int NK = kFwdNK, ST = kFwdST;
   const int r = blockIdx.x, hk = blockIdx.y, hc = blockIdx.z;
   const int h0 = hk * p.G + hc * p.Gc;
   const int nh = min(p.Gc, p.G - hc * p.Gc);
@@ -219,54 +260,43 @@ __global__ void __launch_bounds__(256) k_ta_fwd(TaParams p) {
   const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + nw * 16 * ROWB;
-  uint8_t* sV = sK + 2 * KT * ROWB;
-  uint64_t* anc = reinterpret_cast<uint64_t*>(sV + 2 * KT * ROWB);
+  uint8_t* sV = sK + ST * NK * ROWB;
+  uint64_t* anc = reinterpret_cast<uint64_t*>(sV + ST * NK * ROWB);
   const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
 
   int p0, Pr;
   prefix_of(p, r, p0, Pr, threadIdx.x == 0 && hk == 0 && hc == 0);
-  const int nkeys = Pr + p.N1, ntiles = (nkeys + KT - 1) / KT;
+  const int nkeys = Pr + p.N1, ntiles = (nkeys + NK - 1) / NK;
   build_anc(p, r, anc);
   load_rows(p, p.Q, aQ, 0, nw * 16, rows, r, h0);
-  load_kv(p, aK, aV, KT, 0, nkeys, Pr, p0, r, hk);
-  cp_commit();
+  kv_prologue<NK, ST>(p, aK, aV, ntiles, nkeys, Pr, p0, r, hk);  // Q rides in the first group
 
   const int i0 = warp * 16 + (lane >> 2), i1 = i0 + 8;
   uint64_t a0 = 0, a1 = 0;
+  bool rows_ok = false;
   float o[16][4];
 #pragma unroll
   for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // m in scaled log2 units
+  const float c2 = p.c2;
 
   for (int t = 0; t < ntiles; ++t) {
-    if (t + 1 < ntiles) {
-      load_kv(p, aK + ((t + 1) & 1) * KT * ROWB, aV + ((t + 1) & 1) * KT * ROWB, KT, (t + 1) * KT, nkeys, Pr, p0, r, hk);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
+    kv_next<NK, ST>(p, aK, aV, t, ntiles, nkeys, Pr, p0, r, hk);
     if (t == 0) {
       if (i0 < rows) a0 = anc[i0 % p.N1];
       if (i1 < rows) a1 = anc[i1 % p.N1];
+      rows_ok = __all_sync(0xffffffffu, a0 != 0ull && a1 != 0ull);
     }
-    const uint32_t kb = aK + (t & 1) * KT * ROWB, vb = aV + (t & 1) * KT * ROWB;
-    float s[8][4];
+    const uint32_t kb = aK + (t % ST) * NK * ROWB, vb = aV + (t % ST) * NK * ROWB;
+    float s[NK / 8][4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
-    mma_rows_x_keys(s, aQ, warp * 16, kb, lane);
+    for (int j = 0; j < NK / 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+    mma_rows_x_keys<NK>(s, aQ, warp * 16, kb, lane);
+    mask_scores<NK>(s, rows_ok && (t + 1) * NK <= Pr, t * NK + 2 * (lane & 3), a0, a1, Pr, p.N1);
 
-    const int key0 = t * KT + 2 * (lane & 3);
-    float mx0 = m0, mx1 = m1;
+    float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int kj = key0 + nt * 8 + (e & 1);
-        const bool ok = visible(e < 2 ? a0 : a1, kj, Pr, p.N1);
-        s[nt][e] = ok ? s[nt][e] * p.c2 : -INFINITY;
-      }
+    for (int nt = 0; nt < NK / 8; ++nt) {
       mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][1]));
       mx1 = fmaxf(mx1, fmaxf(s[nt][2], s[nt][3]));
     }
@@ -274,17 +304,18 @@ __global__ void __launch_bounds__(256) k_ta_fwd(TaParams p) {
     mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
     mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
     mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float ms0 = mx0 == -INFINITY ? 0.f : mx0, ms1 = mx1 == -INFINITY ? 0.f : mx1;
+    const float mn0 = fmaxf(m0, mx0 * c2), mn1 = fmaxf(m1, mx1 * c2);
+    const float ms0 = mn0 == -INFINITY ? 0.f : mn0, ms1 = mn1 == -INFINITY ? 0.f : mn1;
     const float al0 = ex2_approx(m0 - ms0), al1 = ex2_approx(m1 - ms1);  // m = -inf -> 0
-    m0 = mx0;
-    m1 = mx1;
+    m0 = mn0;
+    m1 = mn1;
     float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      s[nt][0] = ex2_approx(s[nt][0] - ms0);
-      s[nt][1] = ex2_approx(s[nt][1] - ms0);
-      s[nt][2] = ex2_approx(s[nt][2] - ms1);
-      s[nt][3] = ex2_approx(s[nt][3] - ms1);
+    for (int nt = 0; nt < NK / 8; ++nt) {
+      s[nt][0] = ex2_approx(fmaf(s[nt][0], c2, -ms0));
+      s[nt][1] = ex2_approx(fmaf(s[nt][1], c2, -ms0));
+      s[nt][2] = ex2_approx(fmaf(s[nt][2], c2, -ms1));
+      s[nt][3] = ex2_approx(fmaf(s[nt][3], c2, -ms1));
       ls0 += s[nt][0] + s[nt][1];
       ls1 += s[nt][2] + s[nt][3];
     }
@@ -297,7 +328,7 @@ __global__ void __launch_bounds__(256) k_ta_fwd(TaParams p) {
       o[j][2] *= al1;
       o[j][3] *= al1;
     }
-    mma_p_x_rows(o, s, vb, lane);
+    mma_p_x_rows<NK>(o, s, vb, lane);
     __syncthreads();
   }
 
@@ -356,8 +387,11 @@ __global__ void __launch_bounds__(256) k_ta_dsum(const uint16_t* __restrict__ O,
   if (lane == 0) Dsum[w] = acc;
 }
 
-__global__ void __launch_bounds__(256) k_ta_bwd_dq(TaParams p) {
+constexpr int kDqNK = 32, kDqST = 3;
+
+__global__ void __maxnreg__(144) k_ta_bwd_dq(TaParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int NK = kDqNK, ST = kDqST;
   const int r = blockIdx.x, hk = blockIdx.y, hc = blockIdx.z;
   const int h0 = hk * p.G + hc * p.Gc;
   const int nh = min(p.Gc, p.G - hc * p.Gc);
@@ -366,73 +400,64 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dq(TaParams p) {
   uint8_t* sQ = smem;
   uint8_t* sdO = sQ + nw * 16 * ROWB;
   uint8_t* sK = sdO + nw * 16 * ROWB;
-  uint8_t* sV = sK + 2 * KT * ROWB;
-  uint64_t* anc = reinterpret_cast<uint64_t*>(sV + 2 * KT * ROWB);
+  uint8_t* sV = sK + ST * NK * ROWB;
+  uint64_t* anc = reinterpret_cast<uint64_t*>(sV + ST * NK * ROWB);
   const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), aK = smem_u32(sK), aV = smem_u32(sV);
 
   int p0, Pr;
   prefix_of(p, r, p0, Pr, false);
-  const int nkeys = Pr + p.N1, ntiles = (nkeys + KT - 1) / KT;
+  const int nkeys = Pr + p.N1, ntiles = (nkeys + NK - 1) / NK;
   build_anc(p, r, anc);
   load_rows(p, p.Q, aQ, 0, nw * 16, rows, r, h0);
   load_rows(p, p.dO, adO, 0, nw * 16, rows, r, h0);
-  load_kv(p, aK, aV, KT, 0, nkeys, Pr, p0, r, hk);
-  cp_commit();
+  kv_prologue<NK, ST>(p, aK, aV, ntiles, nkeys, Pr, p0, r, hk);
 
   const int i0 = warp * 16 + (lane >> 2), i1 = i0 + 8;
   uint64_t a0 = 0, a1 = 0;
+  bool rows_ok = false;
   float lse0 = 0.f, lse1 = 0.f, d0 = 0.f, d1 = 0.f;
   if (i0 < rows) {
     const int g = i0 / p.N1, s = i0 - g * p.N1;
     const size_t k = ((size_t)r * p.N1 + s) * p.Hq + h0 + g;
-    lse0 = p.lse[k] * kLog2e;
+    lse0 = isinf(p.lse[k]) ? 0.f : p.lse[k] * kLog2e;  // padded rows: every key masked anyway
     d0 = p.Dsum[k];
   }
   if (i1 < rows) {
     const int g = i1 / p.N1, s = i1 - g * p.N1;
     const size_t k = ((size_t)r * p.N1 + s) * p.Hq + h0 + g;
-    lse1 = p.lse[k] * kLog2e;
+    lse1 = isinf(p.lse[k]) ? 0.f : p.lse[k] * kLog2e;
     d1 = p.Dsum[k];
   }
   float dq[16][4];
 #pragma unroll
   for (int j = 0; j < 16; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
+  const float c2 = p.c2;
 
   for (int t = 0; t < ntiles; ++t) {
-    if (t + 1 < ntiles) {
-      load_kv(p, aK + ((t + 1) & 1) * KT * ROWB, aV + ((t + 1) & 1) * KT * ROWB, KT, (t + 1) * KT, nkeys, Pr, p0, r, hk);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
+    kv_next<NK, ST>(p, aK, aV, t, ntiles, nkeys, Pr, p0, r, hk);
     if (t == 0) {
       if (i0 < rows) a0 = anc[i0 % p.N1];
       if (i1 < rows) a1 = anc[i1 % p.N1];
+      rows_ok = __all_sync(0xffffffffu, a0 != 0ull && a1 != 0ull);
     }
-    const uint32_t kb = aK + (t & 1) * KT * ROWB, vb = aV + (t & 1) * KT * ROWB;
-    float s[8][4], dp[8][4];
+    const uint32_t kb = aK + (t % ST) * NK * ROWB, vb = aV + (t % ST) * NK * ROWB;
+    float s[NK / 8][4], dp[NK / 8][4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < NK / 8; ++j) {
       s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
       dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
     }
-    mma_rows_x_keys(s, aQ, warp * 16, kb, lane);
-    mma_rows_x_keys(dp, adO, warp * 16, vb, lane);
-    const int key0 = t * KT + 2 * (lane & 3);
+    mma_rows_x_keys<NK>(s, aQ, warp * 16, kb, lane);
+    mma_rows_x_keys<NK>(dp, adO, warp * 16, vb, lane);
+    mask_scores<NK>(s, rows_ok && (t + 1) * NK <= Pr, t * NK + 2 * (lane & 3), a0, a1, Pr, p.N1);
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int kj = key0 + nt * 8 + (e & 1);
-        const bool lo = e < 2;
-        const bool ok = visible(lo ? a0 : a1, kj, Pr, p.N1);
-        const float pv = ok ? ex2_approx(s[nt][e] * p.c2 - (lo ? lse0 : lse1)) : 0.f;
-        s[nt][e] = pv * (dp[nt][e] - (lo ? d0 : d1));  // dS
-      }
+    for (int nt = 0; nt < NK / 8; ++nt) {
+      s[nt][0] = ex2_approx(fmaf(s[nt][0], c2, -lse0)) * (dp[nt][0] - d0);  // dS (masked: exp2(-inf) = 0)
+      s[nt][1] = ex2_approx(fmaf(s[nt][1], c2, -lse0)) * (dp[nt][1] - d0);
+      s[nt][2] = ex2_approx(fmaf(s[nt][2], c2, -lse1)) * (dp[nt][2] - d1);
+      s[nt][3] = ex2_approx(fmaf(s[nt][3], c2, -lse1)) * (dp[nt][3] - d1);
     }
-    mma_p_x_rows(dq, s, kb, lane);  // dQ += dS K
+    mma_p_x_rows<NK>(dq, s, kb, lane);  // dQ += dS K
     __syncthreads();
   }
 #pragma unroll
@@ -465,6 +490,7 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
   uint64_t* ancr = anc + 40;                                          // [kMaxRowsReq]
   float* lse2 = reinterpret_cast<float*>(ancr + kMaxRowsReq);
   float* dsum = lse2 + kMaxRowsReq;
+  int* chunk_ok = reinterpret_cast<int*>(dsum + kMaxRowsReq);  // [kMaxRowsReq / QC]
   const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), adO = smem_u32(sdO);
   const int h0 = hk * p.G;
 
@@ -485,8 +511,13 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
       dd = p.Dsum[k];
     }
     ancr[i] = a;
-    lse2[i] = l;
+    lse2[i] = isinf(l) ? 0.f : l;
     dsum[i] = dd;
+  }
+  for (int c = warp; c < nchunks; c += blockDim.x >> 5) {  // chunk_ok[c]: all QC rows valid
+    const int i = c * QC + lane;
+    const bool v = __all_sync(0xffffffffu, lane >= QC || (i < rows && anc[i % p.N1] != 0ull));
+    if (lane == 0) chunk_ok[c] = v ? 1 : 0;
   }
 
   float dv[16][4], dk[16][4];
@@ -511,9 +542,9 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
     __syncthreads();
     const uint32_t qb = aQ + (c & 1) * QC * ROWB, gb = adO + (c & 1) * QC * ROWB;
     // S^T [16 keys x 32 rows] = K_w Q^T ; dP^T = V_w dO^T
-    float s[4][4], dp[4][4];
+    float s[QC / 8][4], dp[QC / 8][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < QC / 8; ++j) {
       s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
       dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
     }
@@ -524,7 +555,7 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
       ldsm4(ak, aK + swz(arow, ach));
       ldsm4(av, aV + swz(arow, ach));
 #pragma unroll
-      for (int np = 0; np < 2; ++np) {
+      for (int np = 0; np < QC / 16; ++np) {
         uint32_t b[4];
         const int brow = np * 16 + (lane & 7) + ((lane >> 4) << 3), bch = 2 * ks + ((lane >> 3) & 1);
         ldsm4(b, qb + swz(brow, bch));
@@ -537,20 +568,31 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
     }
     // P^T, dS^T (C layout: rows = keys kj0/kj1, cols = query rows)
     const int qcol = c * QC + 2 * (lane & 3);
+    const bool fast = chunk_ok[c] && key0 + kw + 16 <= Pr;  // warp-uniform: no mask needed
+    if (!fast) {
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
+      for (int nt = 0; nt < QC / 8; ++nt)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = qcol + nt * 8 + (e & 1);
-        const bool ok = visible(ancr[i], e < 2 ? kj0 : kj1, Pr, p.N1);
-        const float pv = ok ? ex2_approx(s[nt][e] * p.c2 - lse2[i]) : 0.f;
-        s[nt][e] = pv;
-        dp[nt][e] = pv * (dp[nt][e] - dsum[i]);
+        for (int e = 0; e < 4; ++e)
+          if (!visible(ancr[qcol + nt * 8 + (e & 1)], e < 2 ? kj0 : kj1, Pr, p.N1)) s[nt][e] = -INFINITY;
+    }
+#pragma unroll
+    for (int nt = 0; nt < QC / 8; ++nt) {
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const int i = qcol + nt * 8 + e2;
+        const float l = lse2[i], dd = dsum[i];
+#pragma unroll
+        for (int e = e2; e < 4; e += 2) {
+          const float pv = ex2_approx(fmaf(s[nt][e], p.c2, -l));  // masked: exp2(-inf) = 0
+          s[nt][e] = pv;
+          dp[nt][e] = pv * (dp[nt][e] - dd);
+        }
       }
     }
     // dV += P^T dO ; dK += dS^T Q   (k = the chunk's 32 query rows)
 #pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
+    for (int kk = 0; kk < QC / 16; ++kk) {
       const uint32_t ap[4] = {pk_bf16(s[2 * kk][0], s[2 * kk][1]), pk_bf16(s[2 * kk][2], s[2 * kk][3]),
                               pk_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]), pk_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3])};
       const uint32_t ad[4] = {pk_bf16(dp[2 * kk][0], dp[2 * kk][1]), pk_bf16(dp[2 * kk][2], dp[2 * kk][3]),
@@ -599,6 +641,165 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
   }
 }
 
+// Fused backward for G*(N+1) <= 128 (every query row of (request, kv head) in one CTA): per
+// 32-key tile, a row phase (warp = 16 query rows: S, dP, P, dS, dQ += dS K; P and dS parked in
+// shared memory as bf16) and a key phase (warp = 16 keys x 32 head-dim columns: dV = P^T dO,
+// dK = dS^T Q over all rows) -- the five backward products each run once, K/V are read once,
+// and dK/dV of a tile are complete when the tile is done (stored once, no atomics).
+constexpr int kFbNK = 32, kFbST = 3;
+constexpr int kFbRowB = kFbNK * 2;  // bytes per row of the parked P / dS tiles
+
+__device__ __forceinline__ uint32_t swz_p(int row, int ch) { return row * kFbRowB + ((ch ^ ((row >> 1) & 3)) << 4); }
+
+__global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int NK = kFbNK, ST = kFbST;
+  const int r = blockIdx.x, hk = blockIdx.y;
+  const int h0 = hk * p.G;
+  const int rows = p.G * p.N1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* sQ = smem;                       // 128 rows
+  uint8_t* sdO = sQ + 128 * ROWB;
+  uint8_t* sK = sdO + 128 * ROWB;
+  uint8_t* sV = sK + ST * NK * ROWB;
+  uint8_t* sP = sV + ST * NK * ROWB;        // [128 rows][NK keys] bf16
+  uint8_t* sdS = sP + 128 * kFbRowB;
+  uint64_t* anc = reinterpret_cast<uint64_t*>(sdS + 128 * kFbRowB);
+  const uint32_t aQ = smem_u32(sQ), adO = smem_u32(sdO), aK = smem_u32(sK), aV = smem_u32(sV);
+  const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS);
+
+  int p0, Pr;
+  prefix_of(p, r, p0, Pr, false);
+  const int nkeys = Pr + p.N1, ntiles = (nkeys + NK - 1) / NK;
+  build_anc(p, r, anc);
+  load_rows(p, p.Q, aQ, 0, 128, rows, r, h0);
+  load_rows(p, p.dO, adO, 0, 128, rows, r, h0);
+  kv_prologue<NK, ST>(p, aK, aV, ntiles, nkeys, Pr, p0, r, hk);
+
+  const int i0 = warp * 16 + (lane >> 2), i1 = i0 + 8;
+  uint64_t a0 = 0, a1 = 0;
+  bool rows_ok = false;
+  float lse0 = 0.f, lse1 = 0.f, d0 = 0.f, d1 = 0.f;
+  if (i0 < rows) {
+    const int g = i0 / p.N1, s = i0 - g * p.N1;
+    const size_t k = ((size_t)r * p.N1 + s) * p.Hq + h0 + g;
+    lse0 = isinf(p.lse[k]) ? 0.f : p.lse[k] * kLog2e;
+    d0 = p.Dsum[k];
+  }
+  if (i1 < rows) {
+    const int g = i1 / p.N1, s = i1 - g * p.N1;
+    const size_t k = ((size_t)r * p.N1 + s) * p.Hq + h0 + g;
+    lse1 = isinf(p.lse[k]) ? 0.f : p.lse[k] * kLog2e;
+    d1 = p.Dsum[k];
+  }
+  float dq[16][4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
+  const float c2 = p.c2;
+  const int mt = warp & 1, quarter = warp >> 1;  // key phase: keys 16*mt.., head dims 32*quarter..
+  const int nks = (rows + 15) >> 4;               // 16-row steps holding valid rows
+
+  for (int t = 0; t < ntiles; ++t) {
+    kv_next<NK, ST>(p, aK, aV, t, ntiles, nkeys, Pr, p0, r, hk);
+    if (t == 0) {
+      if (i0 < rows) a0 = anc[i0 % p.N1];
+      if (i1 < rows) a1 = anc[i1 % p.N1];
+      rows_ok = __all_sync(0xffffffffu, a0 != 0ull && a1 != 0ull);
+    }
+    const uint32_t kb = aK + (t % ST) * NK * ROWB, vb = aV + (t % ST) * NK * ROWB;
+    // ---- row phase (warps past the last valid row have nothing to do)
+    if (warp < nks) {
+      float s[NK / 8][4], dp[NK / 8][4];
+#pragma unroll
+      for (int j = 0; j < NK / 8; ++j) {
+        s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+        dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
+      }
+      mma_rows_x_keys<NK>(s, aQ, warp * 16, kb, lane);
+      mma_rows_x_keys<NK>(dp, adO, warp * 16, vb, lane);
+      mask_scores<NK>(s, rows_ok && (t + 1) * NK <= Pr, t * NK + 2 * (lane & 3), a0, a1, Pr, p.N1);
+      const int lr = warp * 16 + (lane >> 2);
+#pragma unroll
+      for (int nt = 0; nt < NK / 8; ++nt) {
+        const float p0v = ex2_approx(fmaf(s[nt][0], c2, -lse0)), p1v = ex2_approx(fmaf(s[nt][1], c2, -lse0));
+        const float p2v = ex2_approx(fmaf(s[nt][2], c2, -lse1)), p3v = ex2_approx(fmaf(s[nt][3], c2, -lse1));
+        sts32(aP + swz_p(lr, nt) + (lane & 3) * 4, pk_bf16(p0v, p1v));
+        sts32(aP + swz_p(lr + 8, nt) + (lane & 3) * 4, pk_bf16(p2v, p3v));
+        s[nt][0] = p0v * (dp[nt][0] - d0);
+        s[nt][1] = p1v * (dp[nt][1] - d0);
+        s[nt][2] = p2v * (dp[nt][2] - d1);
+        s[nt][3] = p3v * (dp[nt][3] - d1);
+        sts32(adS + swz_p(lr, nt) + (lane & 3) * 4, pk_bf16(s[nt][0], s[nt][1]));
+        sts32(adS + swz_p(lr + 8, nt) + (lane & 3) * 4, pk_bf16(s[nt][2], s[nt][3]));
+      }
+      mma_p_x_rows<NK>(dq, s, kb, lane);  // dQ += dS K
+    }
+    __syncthreads();
+    // ---- key phase: dV[16 keys x 32 dims] = P^T dO, dK = dS^T Q over the 128 rows
+    {
+      float dv[4][4], dk[4][4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
+        dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = 0.f;
+      }
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {  // 16 query rows per step
+        if (ks >= nks) break;
+        uint32_t ap[4], ad[4];
+        const int prow = ks * 16 + (lane & 7) + ((lane >> 4) << 3), pch = 2 * mt + ((lane >> 3) & 1);
+        ldsm4t(ap, aP + swz_p(prow, pch));
+        ldsm4t(ad, adS + swz_p(prow, pch));
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+          uint32_t b[4];
+          const int brow = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), bch = 4 * quarter + 2 * np + (lane >> 4);
+          ldsm4t(b, adO + swz(brow, bch));
+          mma16816(dv[2 * np], ap, b[0], b[1]);
+          mma16816(dv[2 * np + 1], ap, b[2], b[3]);
+          ldsm4t(b, aQ + swz(brow, bch));
+          mma16816(dk[2 * np], ad, b[0], b[1]);
+          mma16816(dk[2 * np + 1], ad, b[2], b[3]);
+        }
+      }
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int kj = t * NK + mt * 16 + (lane >> 2) + half * 8;
+        if (kj >= nkeys) continue;
+        size_t off;
+        uint16_t *dk_dst, *dv_dst;
+        if (kj < Pr) {
+          off = ((size_t)(p0 + kj) * p.Hkv + hk) * D;
+          dk_dst = p.dKp;
+          dv_dst = p.dVp;
+        } else {
+          off = (((size_t)r * p.N1 + (kj - Pr)) * p.Hkv + hk) * D;
+          dk_dst = p.dKt;
+          dv_dst = p.dVt;
+        }
+        off += 32 * quarter + 2 * (lane & 3);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          *reinterpret_cast<uint32_t*>(dv_dst + off + nt * 8) = pk_bf16(dv[nt][2 * half], dv[nt][2 * half + 1]);
+          *reinterpret_cast<uint32_t*>(dk_dst + off + nt * 8) =
+              pk_bf16(dk[nt][2 * half] * p.scale, dk[nt][2 * half + 1] * p.scale);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int i = half ? i1 : i0;
+    if (i >= rows) continue;
+    const int g = i / p.N1, s = i - g * p.N1;
+    float* dst = p.dQ + (((size_t)r * p.N1 + s) * p.Hq + h0 + g) * D + 2 * (lane & 3);
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt)
+      *reinterpret_cast<float2*>(dst + nt * 8) =
+          make_float2(dq[nt][2 * half] * p.scale, dq[nt][2 * half + 1] * p.scale);
+  }
+}
+
 // ------------------------------------------------------------------------------ host
 struct TaLaunch {
   int Gc, nchunk, nw;
@@ -636,9 +837,10 @@ TaParams ta_params(const aurora_tree_attn_t* ta, TaLaunch& L) {
   return p;
 }
 
-size_t smem_fwd(int nw) { return (size_t)nw * 16 * ROWB + 4 * KT * ROWB + 40 * 8; }
-size_t smem_dq(int nw) { return (size_t)2 * nw * 16 * ROWB + 4 * KT * ROWB + 40 * 8; }
-constexpr size_t kSmemDkdv = 2 * KT2 * ROWB + 4 * QC * ROWB + 40 * 8 + kMaxRowsReq * 16;
+size_t smem_fwd(int nw) { return (size_t)nw * 16 * ROWB + 2 * kFwdST * kFwdNK * ROWB + 40 * 8; }
+size_t smem_dq(int nw) { return (size_t)2 * nw * 16 * ROWB + 2 * kDqST * kDqNK * ROWB + 40 * 8; }
+constexpr size_t kSmemFused = 2 * 128 * ROWB + 2 * kFbST * kFbNK * ROWB + 2 * 128 * kFbRowB + 40 * 8;
+constexpr size_t kSmemDkdv = 2 * KT2 * ROWB + 4 * QC * ROWB + 40 * 8 + kMaxRowsReq * 16 + 4 * (kMaxRowsReq / QC);
 
 }  // namespace
 }  // namespace aur
@@ -665,7 +867,8 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
   const size_t sm = smem_fwd(L.nw);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_ta_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd(8));
+    cudaFuncSetAttribute(k_ta_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd(7));
+    cudaFuncSetAttribute(k_ta_fwd, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr = true;
   }
   prof_begin(PH_TREE_FWD, s);
@@ -708,19 +911,36 @@ extern "C" aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, co
   cudaStream_t s = (cudaStream_t)stream;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_ta_bwd_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dq(8));
+    cudaFuncSetAttribute(k_ta_bwd_dq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dq(7));
     cudaFuncSetAttribute(k_ta_bwd_dkdv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemDkdv);
+    cudaFuncSetAttribute(k_ta_bwd_dq, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#ifndef TA_NO_DKDV_CARVEOUT
+    cudaFuncSetAttribute(k_ta_bwd_dkdv, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#endif
     attr = true;
   }
   const int64_t n_rows = (int64_t)p.R * p.N1 * p.Hq;
-  prof_begin(PH_TREE_BWD_DQ, s);
-  k_ta_dsum<<<(unsigned)((n_rows + 7) / 8), 256, 0, s>>>(p.O, p.dO, (float*)ws, n_rows);
-  k_ta_bwd_dq<<<dim3(p.R, p.Hkv, L.nchunk), L.nw * 32, smem_dq(L.nw), s>>>(p);
-  prof_end(PH_TREE_BWD_DQ, s);
-  prof_begin(PH_TREE_BWD_DKDV, s);
-  const int ktiles = (ta->max_prefix + p.N1 + KT2 - 1) / KT2;
-  k_ta_bwd_dkdv<<<dim3(ktiles, p.Hkv, p.R), 256, kSmemDkdv, s>>>(p);
-  prof_end(PH_TREE_BWD_DKDV, s);
-  count_launch(3);
+  if (p.G * p.N1 <= 128 && !opt_tree_bwd_split()) {
+    static bool fattr = false;
+    if (!fattr) {
+      cudaFuncSetAttribute(k_ta_bwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemFused);
+      fattr = true;
+    }
+    prof_begin(PH_TREE_BWD_FUSED, s);
+    k_ta_dsum<<<(unsigned)((n_rows + 7) / 8), 256, 0, s>>>(p.O, p.dO, (float*)ws, n_rows);
+    k_ta_bwd_fused<<<dim3(p.R, p.Hkv), 256, kSmemFused, s>>>(p);
+    prof_end(PH_TREE_BWD_FUSED, s);
+    count_launch(2);
+  } else {
+    prof_begin(PH_TREE_BWD_DQ, s);
+    k_ta_dsum<<<(unsigned)((n_rows + 7) / 8), 256, 0, s>>>(p.O, p.dO, (float*)ws, n_rows);
+    k_ta_bwd_dq<<<dim3(p.R, p.Hkv, L.nchunk), L.nw * 32, smem_dq(L.nw), s>>>(p);
+    prof_end(PH_TREE_BWD_DQ, s);
+    prof_begin(PH_TREE_BWD_DKDV, s);
+    const int ktiles = (ta->max_prefix + p.N1 + KT2 - 1) / KT2;
+    k_ta_bwd_dkdv<<<dim3(ktiles, p.Hkv, p.R), 256, kSmemDkdv, s>>>(p);
+    prof_end(PH_TREE_BWD_DKDV, s);
+    count_launch(3);
+  }
   return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
 }

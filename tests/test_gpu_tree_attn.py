@@ -81,10 +81,18 @@ def _compare(got, ref, reqs_got, off_got, reqs_ref_off=None):
             assert _rel(a, ref[name]) <= 2e-2, (name, _rel(a, ref[name]))
 
 
+@pytest.mark.parametrize("split", [0, 1], ids=["fused_bwd", "split_bwd"])
 @pytest.mark.parametrize("name", ["ta_small", "ta_chain", "ta_gqa8"])
-def test_tree_attention_parity(name):
+def test_tree_attention_parity(name, split):
+    """split=0: the one-kernel backward (all rows of a kv head in one CTA); split=1: the
+    general dQ + dK/dV kernels (used when G*(N+1) > 128), forced by the option."""
+    from paper_2602_06932_b200 import aurora as A
     inp = tracegen.gen_tree_attn(name)
-    got = _run(inp)
+    A.aurora_set_option("tree_bwd_split", split)
+    try:
+        got = _run(inp)
+    finally:
+        A.aurora_set_option("tree_bwd_split", 0)
     ref = TA.fwd_bwd(inp)
     R = len(inp["requests"])
     _compare(got, ref, np.arange(R), inp["prefix_off"])
