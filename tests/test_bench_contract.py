@@ -49,3 +49,27 @@ def test_roofline_tensor_bound_at_large_m(bench):
     phases["bwd_dw_gemm"] = (16.5, 10)
     r = bench._roofline(phases, cfg, 10, 1394.5, "measured", 6551.0)
     assert r["kernel"] == "bwd_dw_gemm" and r["bound"] == "tensor" and r["unit"] == "TFLOP/s"
+
+
+@pytest.mark.parametrize("name", ["ta_small", "ta_tiny"])
+def test_tree_attn_work_counts_visible_pairs(bench, name):
+    """bench._ta_work's algorithmic pair count equals the number of unmasked (row, key, head)
+    triples of the oracle's mask (F4-R2), including ragged node counts and empty prefixes."""
+    import numpy as np
+    import tracegen
+    from oracle import tree_attention as TA
+    meta = tracegen.gen_tree_attn_meta(name)
+    c = meta["cfg"]
+    w = bench._ta_work(meta)
+    off = meta["prefix_off"]
+    pairs = 0
+    for r in range(c.R):
+        nn = c.N if meta["num_nodes"] is None else int(meta["num_nodes"][r])
+        anc = TA.ancestor_rows(None if meta["parents"] is None else meta["parents"][r], nn, c.N)
+        A = TA._allowed(anc, int(off[r + 1] - off[r]), c.N)
+        pairs += int(A.sum())
+    assert w["pairs"] == pairs * c.Hq
+    assert w["fwd_flops"] == 4.0 * c.dh * w["pairs"] and w["bwd_flops"] == 10.0 * c.dh * w["pairs"]
+    assert w["rows"] == c.R * (c.N + 1)
+    kv = (int(np.diff(off).sum()) + c.R * (c.N + 1)) * c.Hkv * c.dh * 4
+    assert w["fused_bytes"] >= 2 * kv                        # K/V read once + dK/dV written once
