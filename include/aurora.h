@@ -316,6 +316,7 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
 typedef struct {
   int32_t R, N, Hq, Hkv, dh;
   int32_t max_prefix;            /* host bound on every P_r (sizes the backward grid)    */
+  int64_t prefix_total;          /* rows of Kp / Vp (= prefix_off[R]; bounds the TMA maps) */
   const int32_t* prefix_off;     /* (dev) int32 [R+1], prefix_off[0] = 0, non-decreasing  */
   const int32_t* parents;        /* (dev) int32 [R,N] or NULL (chain)                    */
   const int32_t* num_nodes;      /* (dev) int32 [R] or NULL (all N)                      */

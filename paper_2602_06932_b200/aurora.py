@@ -72,7 +72,7 @@ class aurora_adamw_cfg_t(C.Structure):
 
 class aurora_tree_attn_t(C.Structure):
     _fields_ = [("R", C.c_int32), ("N", C.c_int32), ("Hq", C.c_int32), ("Hkv", C.c_int32), ("dh", C.c_int32),
-                ("max_prefix", C.c_int32), ("prefix_off", C.c_void_p), ("parents", C.c_void_p),
+                ("max_prefix", C.c_int32), ("prefix_total", C.c_int64), ("prefix_off", C.c_void_p), ("parents", C.c_void_p),
                 ("num_nodes", C.c_void_p), ("scale", C.c_float), ("status", C.c_void_p)]
 
 
@@ -421,7 +421,7 @@ class TreeAttention:
     lse f32 [R, N+1, Hq]; dQ f32 like Q; dK*/dV* bf16 like their inputs."""
 
     def __init__(self, R: int, N: int, Hq: int, Hkv: int, dh: int, prefix_off, max_prefix: int,
-                 parents=None, num_nodes=None, scale: float = 0.0, device=None):
+                 parents=None, num_nodes=None, scale: float = 0.0, device=None, prefix_total: int = None):
         import torch
         dev = device or prefix_off.device
         _expect(prefix_off, "i32", "prefix_off")
@@ -430,7 +430,10 @@ class TreeAttention:
         self.R, self.N, self.Hq, self.Hkv, self.dh = R, N, Hq, Hkv, dh
         self.prefix_off, self.parents, self.num_nodes = prefix_off, parents, num_nodes
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.cfg = aurora_tree_attn_t(R, N, Hq, Hkv, dh, int(max_prefix), _ptr(prefix_off), _ptr(parents),
+        if prefix_total is None:   # one small D2H read at construction, not per call
+            prefix_total = int(prefix_off[-1].item())
+        self.cfg = aurora_tree_attn_t(R, N, Hq, Hkv, dh, int(max_prefix), int(prefix_total), _ptr(prefix_off),
+                                      _ptr(parents),
                                       _ptr(num_nodes), float(scale), _ptr(self.status))
         nbytes = int(lib().aurora_tree_attn_workspace_size(C.byref(self.cfg)))
         self.ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)

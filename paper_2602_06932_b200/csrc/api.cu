@@ -31,7 +31,7 @@ cudaEvent_t ev_get() {
 const char* kPhaseNames[PH_COUNT] = {"target_scan", "verify", "fwd_gemm", "fwd_combine", "bwd_dz_gemm",
                                      "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm", "bwd_fused", "adamw",
                                      "tree_attn_fwd", "tree_attn_bwd_dq", "tree_attn_bwd_dkdv",
-                                     "tree_attn_bwd_fused"};
+                                     "tree_attn_bwd_fused", "tree_attn_fwd_tc"};
 }  // namespace
 
 // Inside a CUDA-graph capture the phase events become external event-record nodes, so
@@ -144,6 +144,8 @@ struct Options {
   int tile_n = 0;          // fwd / dz tile width: 0 auto, else 256 / 224 / 192
   int64_t dz_chunk_bytes = int64_t(2) << 30;  // classic bwd: dZ^T chunk budget (bytes)
   int scan_ctas = 2;                           // target-scan CTAs per SM (segments per row)
+  int tree_fwd_tc = 0;                         // F4 fwd: 1 = tcgen05 kernel when G*(N+1) <= 128 (opt-in:
+                                               // measured slower than the mma.sync kernel)
   int tree_bwd_split = 0;                      // F4 bwd: 1 = separate dQ / dK-dV kernels even when the
                                                // fused one applies (A/B and coverage of the general path)
   int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
@@ -495,6 +497,7 @@ aurora_status_t bwd_fused(const void* H, const void* W, int64_t M, int64_t d, in
 
 }  // namespace
 int opt_tree_bwd_split() { return opts().tree_bwd_split; }
+int opt_tree_fwd_tc() { return opts().tree_fwd_tc; }
 }  // namespace aur
 
 using namespace aur;
@@ -529,6 +532,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
+  if (std::strcmp(name, "tree_fwd_tc") == 0 && (value == 0 || value == 1)) {
+    o.tree_fwd_tc = static_cast<int>(value);
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "tree_bwd_split") == 0 && (value == 0 || value == 1)) {
     o.tree_bwd_split = static_cast<int>(value);
     return AURORA_OK;
@@ -562,6 +569,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "gemm_pair") == 0) return o.gemm_pair;
   if (std::strcmp(name, "bwd_mode") == 0) return o.bwd_mode;
   if (std::strcmp(name, "tree_bwd_split") == 0) return o.tree_bwd_split;
+  if (std::strcmp(name, "tree_fwd_tc") == 0) return o.tree_fwd_tc;
   if (std::strcmp(name, "bwd_concurrent") == 0) return o.bwd_concurrent;
   if (std::strcmp(name, "tile_n") == 0) return o.tile_n;
   if (std::strcmp(name, "dz_chunk_bytes") == 0) return o.dz_chunk_bytes;

@@ -115,6 +115,9 @@ cudaError_t launch_dw_resident(const CUtensorMap& tmA, const CUtensorMap& tmB, c
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_inner, uint32_t box_outer);
 
+bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                       uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2);
+
 // ---------------------------------------------------------------- fused persistent bwd
 enum BwdType : int { BT_DZ = 0, BT_DH = 1, BT_DW = 2 };
 constexpr int kMaxChunks = 16;
@@ -220,9 +223,10 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 // Phase profiling (CUDA events on the caller's stream).
 enum Phase : int { PH_SCAN = 0, PH_VERIFY, PH_FWD_GEMM, PH_FWD_COMBINE, PH_BWD_DZ, PH_BWD_DW, PH_BWD_DH,
                    PH_BWD_REDUCE, PH_COMM, PH_BWD_FUSED, PH_OPTIM, PH_TREE_FWD, PH_TREE_BWD_DQ,
-                   PH_TREE_BWD_DKDV, PH_TREE_BWD_FUSED, PH_COUNT };
+                   PH_TREE_BWD_DKDV, PH_TREE_BWD_FUSED, PH_TREE_FWD_TC, PH_COUNT };
 void prof_begin(int phase, cudaStream_t s);
 int opt_tree_bwd_split();  // aurora_set_option("tree_bwd_split")
+int opt_tree_fwd_tc();     // aurora_set_option("tree_fwd_tc")
 void prof_end(int phase, cudaStream_t s);
 
 }  // namespace aur

@@ -800,6 +800,365 @@ __global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
   }
 }
 
+// ------------------------------------------------------------------------------ tcgen05 forward
+// Persistent, one CTA per SM, work item = (request, KV head) with all G*(N+1) <= 128 query rows
+// of the KV head as the M = 128 rows of the UMMA tile.  Warp roles: warp 0 = TMA producer (Q box,
+// then K / V tiles of 64 keys through a 4-stage ring: the request's prefix tiles from Kp/Vp, then
+// one tree tile from Kt/Vt), warp 1 = MMA issuer (tcgen05.mma kind::f16, fp32 accumulators in
+// TMEM), warps 2-9 = softmax (thread = TMEM lane = query row; warps w and w+4 split the 64 key
+// columns of a tile).  Two passes over the key tiles per item: pass A accumulates the row max /
+// sum-exp of S = Q K^T (S double-buffered in TMEM), pass B recomputes S, writes the normalised
+// P = exp(S - lse) as bf16 into shared memory (the A operand, K-major SW128, double-buffered)
+// and accumulates O += P V in TMEM (V as the MN-major B operand) — O is never rescaled.
+// TMEM columns: S[0] 0..63, S[1] 64..127, O 128..255.
+#ifdef TA_TC_SPIN
+#define TC_WAIT mbar_wait
+#else
+#define TC_WAIT mbar_wait_sleep
+#endif
+struct TaTcMaps {
+  CUtensorMap Q, Kp, Vp, Kt, Vt;
+};
+constexpr int kTcNK = 64;                     // keys per item
+constexpr int kTcKST = 6;                     // K ring depth (released when S completes)
+constexpr int kTcVST = 3;                     // V ring depth (released when P V completes)
+constexpr int kTcNS = 4;                      // S buffers in TMEM (columns 0 .. 4*64), O after them
+constexpr int kTcThreads = 320;               // TMA warp, MMA warp, 8 softmax warps
+constexpr int kTcOffQ = 0;                    // 2 K-major atoms [128 rows x 128 B]
+constexpr int kTcSlot = 2 * kTcNK * 128;      // 16 KB: K (2 atoms [64 x 128 B]) or V (2 MN slices)
+constexpr int kTcOffK = 32768;
+constexpr int kTcOffV = kTcOffK + kTcKST * kTcSlot;
+constexpr int kTcOffP = kTcOffV + kTcVST * kTcSlot;
+constexpr int kTcPBuf = 128 * kTcNK * 2;      // 16 KB: [128 rows x 64 keys] bf16, one K atom
+constexpr int kTcOffBar = kTcOffP + 2 * kTcPBuf;
+constexpr size_t kSmemTc = kTcOffBar + 512 + 4096 + 1024;  // barriers, anc, (m, l) exchange, align
+
+// K-major SW128 operand with `rows` rows per 64-element K atom; k-step kk = 16 elements.
+__device__ __forceinline__ uint64_t kmaj_desc(uint32_t base, int kk, int rows) {
+  return umma_desc_sw128(base + (kk >> 2) * rows * 128 + (kk & 3) * 32, 16, 1024);
+}
+// MN-major SW128 B operand [K rows x 128 MN] stored as two 64-wide MN slices of `krows` rows.
+__device__ __forceinline__ uint64_t mnmaj_desc(uint32_t base, int kk, int krows) {
+  return umma_desc_sw128(base + kk * 2048, krows * 128, 1024);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_ta_fwd_tc(const __grid_constant__ TaTcMaps maps, TaParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTcOffBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_free = bars + 1;
+  uint64_t* k_full = bars + 2;    // [6]
+  uint64_t* k_empty = bars + 8;   // [6]
+  uint64_t* v_full = bars + 14;   // [3]
+  uint64_t* v_empty = bars + 17;  // [3]
+  uint64_t* s_full = bars + 20;   // [kTcNS]
+  uint64_t* s_free = bars + 24;   // [kTcNS]
+  uint64_t* p_full = bars + 28;   // [2]
+  uint64_t* p_free = bars + 30;   // [2]
+  uint64_t* o_done = bars + 32;
+  uint64_t* o_free = bars + 33;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 34);
+  uint64_t* anc = bars + 36;      // [40]
+  const int G = p.G, N1 = p.N1;
+  const int nwork = p.R * p.Hkv;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_free, 1);
+    for (int s = 0; s < kTcKST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kTcVST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < kTcNS; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 256);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&p_full[s], 256);
+      mbar_init(&p_free[s], 1);
+    }
+    mbar_init(o_done, 1);
+    mbar_init(o_free, 256);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.Q);
+      tma_prefetch_desc(&maps.Kp);
+      tma_prefetch_desc(&maps.Vp);
+      tma_prefetch_desc(&maps.Kt);
+      tma_prefetch_desc(&maps.Vt);
+      uint32_t ki = 0, vi = 0;  // global K / V load counters
+      int wi = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++wi) {
+        const int r = w / p.Hkv, hk = w - r * p.Hkv;
+        int p0, Pr;
+        prefix_of(p, r, p0, Pr, hk == 0);
+        const int npt = (Pr + kTcNK - 1) / kTcNK, ntiles = npt + 1;
+        if (wi > 0) TC_WAIT(q_free, (wi - 1) & 1);
+        mbar_arrive_expect_tx(q_full, 2u * 128u * G * N1);
+        tma_load_3d(&maps.Q, q_full, smem + kTcOffQ, 0, hk * G, r * N1);
+        tma_load_3d(&maps.Q, q_full, smem + kTcOffQ + 16384, 64, hk * G, r * N1);
+        for (int it = 0; it < 2 * ntiles; ++it) {
+          const int j = it % ntiles;
+          const bool pass_b = it >= ntiles;
+          const CUtensorMap* mk = j < npt ? &maps.Kp : &maps.Kt;
+          const CUtensorMap* mv = j < npt ? &maps.Vp : &maps.Vt;
+          const int z = j < npt ? p0 + j * kTcNK : r * N1;
+          {
+            const int ks = ki % kTcKST;
+            if (ki >= kTcKST) TC_WAIT(&k_empty[ks], ((ki / kTcKST) & 1) ^ 1);
+            uint8_t* kd = smem + kTcOffK + ks * kTcSlot;
+#ifdef TA_TC_NOLOAD
+            mbar_arrive(&k_full[ks]);
+            (void)kd; (void)mk;
+#else
+            mbar_arrive_expect_tx(&k_full[ks], kTcSlot);
+            tma_load_3d(mk, &k_full[ks], kd, 0, hk, z);
+            tma_load_3d(mk, &k_full[ks], kd + kTcNK * 128, 64, hk, z);
+#endif
+            ++ki;
+          }
+          if (pass_b) {
+            const int vs = vi % kTcVST;
+            if (vi >= kTcVST) TC_WAIT(&v_empty[vs], ((vi / kTcVST) & 1) ^ 1);
+            uint8_t* vd = smem + kTcOffV + vs * kTcSlot;
+#ifdef TA_TC_NOLOAD
+            mbar_arrive(&v_full[vs]);
+            (void)vd; (void)mv;
+#else
+            mbar_arrive_expect_tx(&v_full[vs], kTcSlot);
+            tma_load_3d(mv, &v_full[vs], vd, 0, hk, z);
+            tma_load_3d(mv, &v_full[vs], vd + kTcNK * 128, 64, hk, z);
+#endif
+            ++vi;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, kTcNK, false, false);
+      constexpr uint32_t idPV = umma_idesc_bf16(128, 128, false, true);
+      const uint32_t aQ = smem_u32(smem + kTcOffQ), aP = smem_u32(smem + kTcOffP);
+      uint32_t gs = 0, pb = 0;  // S items issued (= K items consumed), P V items (= V items consumed)
+      int wi = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++wi) {
+        const int r = w / p.Hkv;
+        int p0, Pr;
+        prefix_of(p, r, p0, Pr, false);
+        const int ntiles = (Pr + kTcNK - 1) / kTcNK + 1, total = 2 * ntiles;
+        TC_WAIT(q_full, wi & 1);
+        auto issue_s = [&](uint32_t g) {
+          const int ks = g % kTcKST, sb = g % kTcNS;
+          TC_WAIT(&k_full[ks], (g / kTcKST) & 1);
+          if (g >= kTcNS) TC_WAIT(&s_free[sb], ((g / kTcNS) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t kb = smem_u32(smem + kTcOffK + ks * kTcSlot);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + sb * kTcNK, kmaj_desc(aQ, kk, 128), kmaj_desc(kb, kk, kTcNK), idS, kk > 0);
+          umma_commit(&s_full[sb]);
+          umma_commit(&k_empty[ks]);  // the K slot is free once this S has been computed
+        };
+        const uint32_t g0 = gs;  // S items run up to kTcNS - 1 ahead of the P V item
+        for (int k = 0; k < kTcNS - 1 && k < total; ++k) issue_s(gs++);
+        for (int it = 0; it < total; ++it) {
+          if (it + kTcNS - 1 < total) issue_s(gs++);
+          (void)g0;
+          if (it >= ntiles) {
+            const int jb = it - ntiles, pbuf = pb & 1, vs = pb % kTcVST;
+            if (jb == 0 && wi > 0) TC_WAIT(o_free, (wi - 1) & 1);  // epilogue read the previous O
+            TC_WAIT(&v_full[vs], (pb / kTcVST) & 1);
+            TC_WAIT(&p_full[pbuf], (pb >> 1) & 1);
+            tc_fence_after();
+            const uint32_t vb = smem_u32(smem + kTcOffV + vs * kTcSlot);
+#pragma unroll
+            for (int kk = 0; kk < kTcNK / 16; ++kk)
+              umma_bf16(tmem + kTcNS * kTcNK, kmaj_desc(aP + pbuf * kTcPBuf, kk, 128), mnmaj_desc(vb, kk, kTcNK), idPV,
+                        (jb > 0 || kk > 0) ? 1u : 0u);
+            umma_commit(&p_free[pbuf]);
+            umma_commit(&v_empty[vs]);
+            ++pb;
+          }
+        }
+        umma_commit(o_done);
+        umma_commit(q_free);
+      }
+    }
+  } else {
+    // ---- softmax / epilogue warps (8): thread = query row i (TMEM lane) x column half hf.
+    const int q4 = warp & 3, hf = (warp - 2) >> 2;
+    const int i = q4 * 32 + lane;
+    const int rows = G * N1;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
+    const uint32_t aProw = smem_u32(smem + kTcOffP) + i * 128;
+    float* stat = reinterpret_cast<float*>(anc + 40);  // [2 halves][2][128]: (m, l)
+    const float c2 = p.c2;
+    const int st_id = threadIdx.x - 64;                 // 0..255
+    uint32_t gs = 0, pb = 0;
+    int wi = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++wi) {
+      const int r = w / p.Hkv, hk = w - r * p.Hkv;
+      int p0, Pr;
+      prefix_of(p, r, p0, Pr, false);
+      const int npt = (Pr + kTcNK - 1) / kTcNK, ntiles = npt + 1;
+      if (st_id < N1) {  // ancestor masks of this request
+        const int s = st_id;
+        const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
+        bool bad = nn < 0 || nn > p.N;
+        uint64_t m = 0;
+        if (!bad) {
+          if (s == 0) {
+            m = 1ull;
+          } else if (s - 1 < nn) {
+            int cur = s - 1;
+            m = 1ull | (1ull << s);
+            for (int k = 0; k <= p.N; ++k) {
+              const int par = p.parents ? p.parents[(size_t)r * p.N + cur] : cur - 1;
+              if (par < -1 || par >= cur) { bad = true; break; }
+              if (par < 0) break;
+              m |= 1ull << (par + 1);
+              cur = par;
+            }
+          }
+        }
+        if (bad && p.status && hk == 0) atomicOr(p.status, (uint32_t)AURORA_STATUS_STRUCTURE);
+        anc[s] = bad ? 0ull : m;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const int s_row = i / G, g = i - s_row * G;
+      const uint64_t a = i < rows ? anc[s_row] : 0ull;
+      const uint64_t ah = hf ? (a >> 32) : a;           // tree-tile bits of this half's 32 columns
+      float m = -INFINITY, l = 0.f, mfin = 0.f;
+      for (int it = 0; it < 2 * ntiles; ++it, ++gs) {
+        const int sb = gs % kTcNS;
+        const int j = it % ntiles;
+        const bool pass_b = it >= ntiles;
+        if (pass_b && it == ntiles) {  // combine the two halves' (m, l) once per item
+          stat[(hf * 2 + 0) * 128 + i] = m;
+          stat[(hf * 2 + 1) * 128 + i] = l;
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          const float mo = stat[((1 - hf) * 2 + 0) * 128 + i], lo = stat[((1 - hf) * 2 + 1) * 128 + i];
+          const float mm = fmaxf(m, mo);
+          const float ll = (mm == -INFINITY) ? 0.f : l * ex2_approx(m - mm) + lo * ex2_approx(mo - mm);
+          mfin = ll > 0.f ? mm + __log2f(ll) : 0.f;
+          l = ll;
+        }
+        const bool tree = j >= npt;
+        const int lim = tree ? 0 : min(Pr - j * kTcNK - hf * 32, 32);  // visible prefix columns
+        mbar_wait(&s_full[sb], (gs / kTcNS) & 1);
+        tc_fence_after();
+        uint32_t v[32];
+#ifdef TA_TC_NOSOFTMAX
+        tc_fence_before();
+        mbar_arrive(&s_free[sb]);
+        if (pass_b) {
+          const int pbuf = pb & 1;
+          if (pb >= 2) mbar_wait(&p_free[pbuf], ((pb >> 1) & 1) ^ 1);
+          fence_proxy_async_smem();
+          mbar_arrive(&p_full[pbuf]);
+          ++pb;
+        }
+        continue;
+#endif
+        tmem_ld_32x32b_x32(trow + sb * kTcNK + hf * 32, v);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&s_free[sb]);
+        float x[32];
+        const bool full = a != 0ull && !tree && lim >= 32;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          bool ok;
+          if (full) ok = true;
+          else if (tree) ok = (ah >> e) & 1ull;
+          else ok = a != 0ull && e < lim;
+          x[e] = ok ? __uint_as_float(v[e]) : -INFINITY;
+        }
+        if (!pass_b) {
+          float mr = -INFINITY;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) mr = fmaxf(mr, x[e]);
+          const float mx = fmaxf(m, mr * c2);
+          if (mx != -INFINITY) {
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              s0 += ex2_approx(fmaf(x[e], c2, -mx));
+              s1 += ex2_approx(fmaf(x[e + 1], c2, -mx));
+            }
+            l = l * ex2_approx(m - mx) + (s0 + s1);
+            m = mx;
+          }
+        } else {
+          uint32_t w16[16];
+#pragma unroll
+          for (int h = 0; h < 16; ++h)
+            w16[h] = pk_bf16(ex2_approx(fmaf(x[2 * h], c2, -mfin)), ex2_approx(fmaf(x[2 * h + 1], c2, -mfin)));
+          const int pbuf = pb & 1;
+          if (pb >= 2) mbar_wait(&p_free[pbuf], ((pb >> 1) & 1) ^ 1);
+          const uint32_t rowb = aProw + pbuf * kTcPBuf;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t ch = static_cast<uint32_t>((hf * 4 + q) ^ (i & 7));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowb + ch * 16), "r"(w16[4 * q]),
+                         "r"(w16[4 * q + 1]), "r"(w16[4 * q + 2]), "r"(w16[4 * q + 3])
+                         : "memory");
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&p_full[pbuf]);
+          ++pb;
+        }
+      }
+      // epilogue: O (normalised already) -> bf16 global (this half's 64 columns), lse
+      mbar_wait(o_done, wi & 1);
+      tc_fence_after();
+      uint32_t v[2][32];
+      tmem_ld_32x32b_x32(trow + kTcNS * kTcNK + hf * 64, v[0]);
+      tmem_ld_32x32b_x32(trow + kTcNS * kTcNK + hf * 64 + 32, v[1]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(o_free);
+      if (i < rows) {
+        uint16_t* orow = p.Oout + (((size_t)r * N1 + s_row) * p.Hq + hk * G + g) * D + hf * 64;
+        const bool live = a != 0ull;
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 o4;
+            o4.x = live ? pk_bf16(__uint_as_float(v[c][8 * q + 0]), __uint_as_float(v[c][8 * q + 1])) : 0u;
+            o4.y = live ? pk_bf16(__uint_as_float(v[c][8 * q + 2]), __uint_as_float(v[c][8 * q + 3])) : 0u;
+            o4.z = live ? pk_bf16(__uint_as_float(v[c][8 * q + 4]), __uint_as_float(v[c][8 * q + 5])) : 0u;
+            o4.w = live ? pk_bf16(__uint_as_float(v[c][8 * q + 6]), __uint_as_float(v[c][8 * q + 7])) : 0u;
+            *reinterpret_cast<uint4*>(orow + c * 32 + q * 8) = o4;
+          }
+        if (hf == 0)
+          p.lse_out[((size_t)r * N1 + s_row) * p.Hq + hk * G + g] = (live && l > 0.f) ? mfin * kLn2 : -INFINITY;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // anc / stat are rewritten by the next item
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ------------------------------------------------------------------------------ host
 struct TaLaunch {
   int Gc, nchunk, nw;
@@ -864,6 +1223,30 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
   p.Oout = (uint16_t*)O;
   p.lse_out = lse;
   cudaStream_t s = (cudaStream_t)stream;
+  if (opt_tree_fwd_tc() && p.G * p.N1 <= 128) {
+    TaTcMaps maps;
+    const uint64_t rows_t = (uint64_t)p.R * p.N1;
+    const uint64_t ptot = ta->prefix_total > 0 ? (uint64_t)ta->prefix_total : 1;
+    const void* kp = ta->prefix_total > 0 ? Kp : Kt;
+    const void* vp = ta->prefix_total > 0 ? Vp : Vt;
+    bool ok = make_tmap_bf16_3d(&maps.Q, Q, D, p.Hq, rows_t, D, (uint64_t)p.Hq * D, 64, p.G, p.N1) &&
+              make_tmap_bf16_3d(&maps.Kp, kp, D, p.Hkv, ptot, D, (uint64_t)p.Hkv * D, 64, 1, kTcNK) &&
+              make_tmap_bf16_3d(&maps.Vp, vp, D, p.Hkv, ptot, D, (uint64_t)p.Hkv * D, 64, 1, kTcNK) &&
+              make_tmap_bf16_3d(&maps.Kt, Kt, D, p.Hkv, rows_t, D, (uint64_t)p.Hkv * D, 64, 1, kTcNK) &&
+              make_tmap_bf16_3d(&maps.Vt, Vt, D, p.Hkv, rows_t, D, (uint64_t)p.Hkv * D, 64, 1, kTcNK);
+    if (!ok) return AURORA_ERR_CUDA;
+    static bool tattr = false;
+    if (!tattr) {
+      cudaFuncSetAttribute(k_ta_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTc);
+      tattr = true;
+    }
+    const int work = p.R * p.Hkv;
+    prof_begin(PH_TREE_FWD_TC, s);
+    k_ta_fwd_tc<<<std::min(work, kNumSMs), kTcThreads, kSmemTc, s>>>(maps, p);
+    count_launch();
+    prof_end(PH_TREE_FWD_TC, s);
+    return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
+  }
   const size_t sm = smem_fwd(L.nw);
   static bool attr = false;
   if (!attr) {

@@ -3,7 +3,7 @@
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 python -m paper_2602_06932_b200.build > /dev/null
-timeout 900 python -m pytest tests/test_gpu_tree_attn.py -q -x > gpurun_out/f4_tests.log 2>&1; echo f4_tests_rc=$?; tail -3 gpurun_out/f4_tests.log
+timeout 600 python -m pytest tests/test_gpu_tree_attn.py -q -x > gpurun_out/f4_tests.log 2>&1; echo f4_tests_rc=$?; tail -3 gpurun_out/f4_tests.log
 for c in ta_tree ta_llama; do
   timeout 400 python bench.py --workload tree_attn --ta-config $c --no-cpu-baseline > gpurun_out/b_$c.json 2> gpurun_out/b_$c.err; echo ${c}_rc=$?
   python -c "

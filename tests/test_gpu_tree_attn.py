@@ -81,18 +81,22 @@ def _compare(got, ref, reqs_got, off_got, reqs_ref_off=None):
             assert _rel(a, ref[name]) <= 2e-2, (name, _rel(a, ref[name]))
 
 
-@pytest.mark.parametrize("split", [0, 1], ids=["fused_bwd", "split_bwd"])
+@pytest.mark.parametrize("tc,split", [(1, 0), (0, 1), (0, 0)], ids=["tc_fwd+fused_bwd", "sync_fwd+split_bwd",
+                                                                      "sync_fwd+fused_bwd"])
 @pytest.mark.parametrize("name", ["ta_small", "ta_chain", "ta_gqa8"])
-def test_tree_attention_parity(name, split):
-    """split=0: the one-kernel backward (all rows of a kv head in one CTA); split=1: the
-    general dQ + dK/dV kernels (used when G*(N+1) > 128), forced by the option."""
+def test_tree_attention_parity(name, tc, split):
+    """tc=1: the tcgen05 forward (TMEM accumulators, TMA K/V; opt-in, option tree_fwd_tc),
+    tc=0: the mma.sync forward (default); split=0: the one-kernel backward (all rows of
+    a kv head in one CTA); split=1: the general dQ + dK/dV kernels (used when G*(N+1) > 128)."""
     from paper_2602_06932_b200 import aurora as A
     inp = tracegen.gen_tree_attn(name)
     A.aurora_set_option("tree_bwd_split", split)
+    A.aurora_set_option("tree_fwd_tc", tc)
     try:
         got = _run(inp)
     finally:
         A.aurora_set_option("tree_bwd_split", 0)
+        A.aurora_set_option("tree_fwd_tc", 0)
     ref = TA.fwd_bwd(inp)
     R = len(inp["requests"])
     _compare(got, ref, np.arange(R), inp["prefix_off"])
