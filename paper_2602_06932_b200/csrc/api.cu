@@ -158,6 +158,8 @@ struct Options {
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
     if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
+    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = atoi(e) ? 1 : 0;
+    if (const char* e = getenv("AURORA_TREE_BWD_SPLIT")) tree_bwd_split = atoi(e) ? 1 : 0;
   }
 };
 Options& opts() {

@@ -646,10 +646,18 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
 // shared memory as bf16) and a key phase (warp = 16 keys x 32 head-dim columns: dV = P^T dO,
 // dK = dS^T Q over all rows) -- the five backward products each run once, K/V are read once,
 // and dK/dV of a tile are complete when the tile is done (stored once, no atomics).
-constexpr int kFbNK = 32, kFbST = 3;
+#ifndef TA_FB_NK
+#define TA_FB_NK 64
+#endif
+constexpr int kFbNK = TA_FB_NK, kFbST = 3;
 constexpr int kFbRowB = kFbNK * 2;  // bytes per row of the parked P / dS tiles
+constexpr int kFbMT = kFbNK / 16;   // key phase: 16-key m-tiles per tile
+constexpr int kFbDW = 128 * kFbMT / 8;  // key phase: head dims per warp (8 warps)
 
-__device__ __forceinline__ uint32_t swz_p(int row, int ch) { return row * kFbRowB + ((ch ^ ((row >> 1) & 3)) << 4); }
+__device__ __forceinline__ uint32_t swz_p(int row, int ch) {
+  if constexpr (kFbRowB == 128) return row * 128 + ((ch ^ (row & 7)) << 4);
+  else return row * kFbRowB + ((ch ^ ((row >> 1) & 3)) << 4);
+}
 
 __global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -696,7 +704,7 @@ __global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
   const float c2 = p.c2;
-  const int mt = warp & 1, quarter = warp >> 1;  // key phase: keys 16*mt.., head dims 32*quarter..
+  const int mt = warp % kFbMT, grp = warp / kFbMT;  // key phase: keys 16*mt.., head dims kFbDW*grp..
   const int nks = (rows + 15) >> 4;               // 16-row steps holding valid rows
 
   for (int t = 0; t < ntiles; ++t) {
@@ -735,11 +743,12 @@ __global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
       mma_p_x_rows<NK>(dq, s, kb, lane);  // dQ += dS K
     }
     __syncthreads();
-    // ---- key phase: dV[16 keys x 32 dims] = P^T dO, dK = dS^T Q over the 128 rows
+    // ---- key phase: dV[16 keys x kFbDW dims] = P^T dO, dK = dS^T Q over the valid rows
     {
-      float dv[4][4], dk[4][4];
+      constexpr int NT8 = kFbDW / 8;
+      float dv[NT8][4], dk[NT8][4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NT8; ++j) {
         dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
         dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = 0.f;
       }
@@ -751,9 +760,9 @@ __global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
         ldsm4t(ap, aP + swz_p(prow, pch));
         ldsm4t(ad, adS + swz_p(prow, pch));
 #pragma unroll
-        for (int np = 0; np < 2; ++np) {
+        for (int np = 0; np < NT8 / 2; ++np) {
           uint32_t b[4];
-          const int brow = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), bch = 4 * quarter + 2 * np + (lane >> 4);
+          const int brow = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), bch = NT8 * grp + 2 * np + (lane >> 4);
           ldsm4t(b, adO + swz(brow, bch));
           mma16816(dv[2 * np], ap, b[0], b[1]);
           mma16816(dv[2 * np + 1], ap, b[2], b[3]);
@@ -777,9 +786,9 @@ __global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
           dk_dst = p.dKt;
           dv_dst = p.dVt;
         }
-        off += 32 * quarter + 2 * (lane & 3);
+        off += kFbDW * grp + 2 * (lane & 3);
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
+        for (int nt = 0; nt < NT8; ++nt) {
           *reinterpret_cast<uint32_t*>(dv_dst + off + nt * 8) = pk_bf16(dv[nt][2 * half], dv[nt][2 * half + 1]);
           *reinterpret_cast<uint32_t*>(dk_dst + off + nt * 8) =
               pk_bf16(dk[nt][2 * half] * p.scale, dk[nt][2 * half + 1] * p.scale);
