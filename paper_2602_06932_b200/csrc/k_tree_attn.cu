@@ -248,7 +248,11 @@ __device__ __forceinline__ void mask_scores(float (&s)[NK / 8][4], bool fast, in
       if (!visible(e < 2 ? a0 : a1, key0 + nt * 8 + (e & 1), Pr, N1)) s[nt][e] = -INFINITY;
 }
 
-constexpr int kFwdNK = 64, kFwdST = 2;
+#ifndef TA_FWD_NK
+#define TA_FWD_NK 64
+#define TA_FWD_ST 2
+#endif
+constexpr int kFwdNK = TA_FWD_NK, kFwdST = TA_FWD_ST;
 
 __global__ void __launch_bounds__(224, 2) k_ta_fwd(TaParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
