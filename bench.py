@@ -763,7 +763,8 @@ def run_tree_attn(args):
         "gpu_launches": int(n_launch),
         "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
         "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved_gbs"], "peak": hbm,
-                     "unit": "GB/s", "frac": round(dom["achieved_gbs"] / hbm, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(dom["achieved_gbs"] / hbm, 4),
+                     "traffic": _traffic_for(dom["kernel"], c.name),
                      "peak_source": f"{peak_src} hbm_gbs (copy)",
                      "work_per_launch": "compulsory DRAM bytes (prefix+tree K/V, Q/dO/O, outputs), DESIGN.md §6 F4",
                      "phases": per},
