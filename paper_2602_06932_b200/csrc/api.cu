@@ -144,7 +144,6 @@ struct Options {
   int tile_n = 0;          // fwd / dz tile width: 0 auto, else 256 / 224 / 192
   int64_t dz_chunk_bytes = int64_t(2) << 30;  // classic bwd: dZ^T chunk budget (bytes)
   int scan_ctas = 2;                           // target-scan CTAs per SM (segments per row)
-  int scan_prefetch = 1;                       // A2: bulk L2 prefetch of each scan segment at CTA start
   int tree_fwd_tc = 0;                         // F4 fwd: 1 = tcgen05 kernel when G*(N+1) <= 128 (opt-in:
                                                // measured slower than the mma.sync kernel)
   int tree_bwd_split = 0;                      // F4 bwd: 1 = separate dQ / dK-dV kernels even when the
@@ -160,7 +159,6 @@ struct Options {
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
     if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
     if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = atoi(e) ? 1 : 0;
-    if (const char* e = getenv("AURORA_SCAN_PREFETCH")) scan_prefetch = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_TREE_BWD_SPLIT")) tree_bwd_split = atoi(e) ? 1 : 0;
   }
 };
@@ -536,10 +534,6 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
-  if (std::strcmp(name, "scan_prefetch") == 0 && (value == 0 || value == 1)) {
-    o.scan_prefetch = static_cast<int>(value);
-    return AURORA_OK;
-  }
   if (std::strcmp(name, "tree_fwd_tc") == 0 && (value == 0 || value == 1)) {
     o.tree_fwd_tc = static_cast<int>(value);
     return AURORA_OK;
@@ -578,7 +572,6 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "bwd_mode") == 0) return o.bwd_mode;
   if (std::strcmp(name, "tree_bwd_split") == 0) return o.tree_bwd_split;
   if (std::strcmp(name, "tree_fwd_tc") == 0) return o.tree_fwd_tc;
-  if (std::strcmp(name, "scan_prefetch") == 0) return o.scan_prefetch;
   if (std::strcmp(name, "bwd_concurrent") == 0) return o.bwd_concurrent;
   if (std::strcmp(name, "tile_n") == 0) return o.tile_n;
   if (std::strcmp(name, "dz_chunk_bytes") == 0) return o.dz_chunk_bytes;
@@ -692,7 +685,6 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   p.k_max = k_max;
   p.nseg = scan_nseg(M, t->V_local);
   p.seg_len = rup(cdiv(t->V_local, p.nseg), 8);
-  p.prefetch_l2 = opts().scan_prefetch;
   p.draft = t->draft_tokens;
   p.parents = t->parents;
   p.num_nodes = t->num_nodes;

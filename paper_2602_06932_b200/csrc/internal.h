@@ -156,7 +156,6 @@ struct VerifyLaunch {
   int64_t ldT, V_local, vocab_offset, V;
   int32_t M, R, N, k_max, nseg;
   int64_t seg_len;
-  int32_t prefetch_l2;  // A2: each CTA bulk-prefetches its segment into L2 first (option scan_prefetch)
   const int32_t* draft;
   const int32_t* parents;
   const int32_t* num_nodes;

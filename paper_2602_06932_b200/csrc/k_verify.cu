@@ -149,11 +149,6 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(T + c0) & 15) == 0);
   const int64_t nvec = aligned ? (c1 - c0) >> 3 : 0;
   const uint4* src = reinterpret_cast<const uint4*>(T + c0);
-  // Start the whole segment's DRAM stream at once (one bulk L2 prefetch per CTA): the warm
-  // start and the first loads then overlap the fetch of the rest instead of serialising on it.
-  if (p.prefetch_l2 && threadIdx.x == 0 && nvec > 0)
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(static_cast<uint32_t>(nvec * 16))
-                 : "memory");
   constexpr int U = 8;  // 16 B loads in flight per lane
   // vectors are interleaved: warp w handles [w*32 + i*256, +32) for i = 0, 1, ...
   int64_t base = static_cast<int64_t>(warp) * 32;
