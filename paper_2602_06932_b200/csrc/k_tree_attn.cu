@@ -235,6 +235,18 @@ __device__ __forceinline__ void kv_next(const TaParams& p, uint32_t aK, uint32_t
   __syncthreads();
 }
 
+// One barrier per tile: wait for tile t, sync (so every warp is also done with tile t-1), then
+// refill tile t-1's stage with tile t+ST-1.
+template <int NK, int ST>
+__device__ __forceinline__ void kv_next_1sync(const TaParams& p, uint32_t aK, uint32_t aV, int t, int ntiles,
+                                              int nkeys, int Pr, int p0, int r, int hk) {
+  cp_wait<ST - 2>();
+  __syncthreads();
+  const int j = t + ST - 1;
+  if (j < ntiles) load_kv(p, aK + (j % ST) * NK * ROWB, aV + (j % ST) * NK * ROWB, NK, j * NK, nkeys, Pr, p0, r, hk);
+  cp_commit();
+}
+
 // Raw scores of keys this warp's rows may not see -> -inf.  Skipped (warp-uniform) for tiles
 // wholly inside the prefix when every row of the warp is a valid query row.
 template <int NK>
@@ -285,7 +297,11 @@ __global__ void __launch_bounds__(224, 2) k_ta_fwd(TaParams p) {
   const float c2 = p.c2;
 
   for (int t = 0; t < ntiles; ++t) {
+#ifdef TA_FWD_2SYNC
     kv_next<NK, ST>(p, aK, aV, t, ntiles, nkeys, Pr, p0, r, hk);
+#else
+    kv_next_1sync<NK, ST>(p, aK, aV, t, ntiles, nkeys, Pr, p0, r, hk);
+#endif
     if (t == 0) {
       if (i0 < rows) a0 = anc[i0 % p.N1];
       if (i1 < rows) a1 = anc[i1 % p.N1];
@@ -333,8 +349,11 @@ __global__ void __launch_bounds__(224, 2) k_ta_fwd(TaParams p) {
       o[j][3] *= al1;
     }
     mma_p_x_rows<NK>(o, s, vb, lane);
+#ifdef TA_FWD_2SYNC
     __syncthreads();
+#endif
   }
+  __syncthreads();  // the O staging below reuses sQ rows of this warp only, but K/V stages may refill
 
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
