@@ -309,7 +309,8 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
  *  Q, O, dO [R, N+1, Hq, dh]; Kt, Vt, dKt, dVt [R, N+1, Hkv, dh]; Kp, Vp, dKp, dVp
  *  [P_total, Hkv, dh]; lse f32 [R, N+1, Hq]; dQ f32 [R, N+1, Hq, dh].
  * Limits (else UNSUPPORTED, nothing enqueued): dh == 128, 1 <= N <= 32, Hq % Hkv == 0,
- * (Hq/Hkv)*(N+1) <= 256.  Data errors OR bits into *status (if non-NULL): STRUCTURE for a
+ * (Hq/Hkv)*(N+1) <= 256, R <= 65535.  NULL or non-16-byte-aligned tensors: INVALID_ARG; a
+ * backward workspace below aurora_tree_attn_workspace_size(): WORKSPACE.  Data errors OR bits into *status (if non-NULL): STRUCTURE for a
  * malformed parent array or num_nodes outside [0, N] (that request's rows are treated as
  * padding), RANGE for a prefix longer than max_prefix (its keys beyond max_prefix are
  * ignored). */

@@ -22,6 +22,7 @@
 // swizzled shared tiles (conflict-free).  The tcgen05 (TMEM) version is the next step
 // (DESIGN.md §6): at these shapes the phase is close to HBM-bound on the prefix K/V.
 #include <cmath>
+#include <initializer_list>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -1196,6 +1197,12 @@ struct TaLaunch {
   int Gc, nchunk, nw;
 };
 
+bool misaligned16(std::initializer_list<const void*> ps) {
+  for (const void* q : ps)
+    if (reinterpret_cast<uintptr_t>(q) & 15) return true;
+  return false;
+}
+
 aurora_status_t ta_check(const aurora_tree_attn_t* ta) {
   if (!ta || !ta->prefix_off) return AURORA_ERR_INVALID_ARG;
   if (ta->R < 1 || ta->N < 1 || ta->Hq < 1 || ta->Hkv < 1 || ta->max_prefix < 0) return AURORA_ERR_INVALID_ARG;
@@ -1245,6 +1252,7 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
   if (st != AURORA_OK) return st;
   if (!Q || !Kt || !Vt || !O || !lse) return AURORA_ERR_INVALID_ARG;
   if (ta->max_prefix > 0 && (!Kp || !Vp)) return AURORA_ERR_INVALID_ARG;
+  if (misaligned16({Q, Kt, Vt, Kp, Vp, O})) return AURORA_ERR_INVALID_ARG;  // 16-B vector / TMA access
   TaLaunch L;
   TaParams p = ta_params(ta, L);
   p.Q = (const uint16_t*)Q;
@@ -1306,6 +1314,7 @@ extern "C" aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, co
   if (st != AURORA_OK) return st;
   if (!Q || !Kt || !Vt || !O || !lse || !dO || !dQ || !dKt || !dVt) return AURORA_ERR_INVALID_ARG;
   if (ta->max_prefix > 0 && (!Kp || !Vp || !dKp || !dVp)) return AURORA_ERR_INVALID_ARG;
+  if (misaligned16({Q, Kt, Vt, Kp, Vp, O, dO, dQ, dKt, dVt, dKp, dVp})) return AURORA_ERR_INVALID_ARG;
   if (!ws || ws_bytes < aurora_tree_attn_workspace_size(ta)) return AURORA_ERR_WORKSPACE;
   TaLaunch L;
   TaParams p = ta_params(ta, L);

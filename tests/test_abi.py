@@ -115,3 +115,29 @@ def test_options_validate_host_side(L):
         finally:
             A.aurora_set_option(name, saved)
     assert A.aurora_get_option("no_such_option") == -1
+
+
+def test_tree_attn_host_validation_without_gpu(L):
+    """F4 entry points reject bad configurations before any CUDA call (nothing enqueued)."""
+    ok = dict(R=4, N=5, Hq=32, Hkv=8, dh=128, max_prefix=100, prefix_total=300, prefix_off=16)
+    ta = lambda **kw: A.aurora_tree_attn_t(**{**ok, **kw})
+    P = [16] * 5                                     # Q, Kt, Vt, Kp, Vp (aligned dummies)
+    f = lambda t, ptrs=P, o=16, lse=16: L.aurora_tree_attn_fwd(C.byref(t), *ptrs, o, lse, None)
+    assert L.aurora_tree_attn_fwd(None, *P, 16, 16, None) == 1
+    assert f(ta(dh=64)) == 5                         # head dim 128 only
+    assert f(ta(N=33)) == 5                          # N <= 32
+    assert f(ta(Hq=30)) == 1                         # Hq % Hkv
+    assert f(ta(Hq=64, Hkv=1, N=5)) == 5             # G * (N + 1) = 384 > 256 rows per KV head
+    assert f(ta(R=0)) == 1
+    assert f(ta(prefix_off=None)) == 1
+    assert f(ta(), ptrs=[16, 16, 16, None, 16]) == 1  # prefix K missing while max_prefix > 0
+    assert f(ta(), ptrs=[24, 16, 16, 16, 16]) == 1    # Q not 16-B aligned
+    assert f(ta(), o=None) == 1
+    t = ta()
+    need = L.aurora_tree_attn_workspace_size(C.byref(t))
+    assert need >= 4 * 6 * 32 * 4
+    b = lambda t, ws_bytes, dq=16: L.aurora_tree_attn_bwd(C.byref(t), *P, 16, 16, 16, dq, 16, 16, 16, 16, 16,
+                                                          ws_bytes, None)
+    assert b(t, need - 1) == 6                       # workspace too small
+    assert b(t, need, dq=None) == 1
+    assert b(ta(dh=64), need) == 5
