@@ -659,12 +659,19 @@ def run_tree_attn(args):
     from paper_2602_06932_b200 import aurora as A
     from paper_2602_06932_b200.build import build
 
+    import torch.distributed as dist
+    # N > 1: requests are independent (no exchange step exists), so every rank attends its own
+    # batch of trees (weak scaling, its own seed) and no collective touches the data path; the
+    # barrier + max-over-ranks timing follows the bench contract.
     ws, rank, local = _dist_env()
-    if rank != 0:        # F4 is measured on one GPU (replicas would repeat rank 0's work)
-        return
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    build()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        build()
+    if ws > 1:
+        dist.barrier()
     A.lib()
     meta = tracegen.gen_tree_attn_meta(args.ta_config)
     c = meta["cfg"]
@@ -672,7 +679,7 @@ def run_tree_attn(args):
     off = meta["prefix_off"]
     P = int(off[-1])
     g = torch.Generator(device=dev)
-    g.manual_seed(c.seed)
+    g.manual_seed(c.seed + 7919 * rank)
     qscale = torch.ones(c.Hq, 1, device=dev)
     G = c.Hq // c.Hkv
     for h in range(c.Hq):
@@ -709,6 +716,9 @@ def run_tree_attn(args):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     A.aurora_profile_read()
     A.aurora_profile_enable(True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     n0 = A.aurora_launch_count()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
@@ -720,9 +730,13 @@ def run_tree_attn(args):
     n_launch = A.aurora_launch_count() - n0
     A.aurora_profile_enable(False)
     phases = A.aurora_profile_read()
-    ms_step = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    t_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in evs)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_step = float(t_ms.item()) / args.steps
     w = _ta_work(meta)
-    rows_per_s = w["rows"] / (ms_step / 1e3)
+    rows_per_s = w["rows"] * ws / (ms_step / 1e3)   # every rank's batch counts
 
     # e2e: every step copies its inputs from pinned host memory and reads lse back
     host = {k: v.cpu().pin_memory() for k, v in dict(Q=Q, Kt=Kt, Vt=Vt, Kp=Kp, Vp=Vp, dO=dO).items()}
@@ -738,7 +752,13 @@ def run_tree_attn(args):
         lse_h.copy_(lse, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e_steps
+    e_ms = torch.tensor([e0.elapsed_time(e1) / e_steps], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e_ms.item())
+    if rank != 0:
+        dist.destroy_process_group()
+        return
 
     _, _, hbm, peak_src = _peaks()
     per = []
@@ -753,13 +773,14 @@ def run_tree_attn(args):
     dom = max(per, key=lambda x: x["ms_per_step"])
     out = {
         "metric": "tree-attention fwd+bwd tokens/s (F4 draft-layer attention, ancestor-closure mask)",
-        "value": round(rows_per_s, 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "value": round(rows_per_s, 1), "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (seeded device generator; tracegen structure)",
         "config": {"workload": c.name, "R": c.R, "N": c.N, "Hq": c.Hq, "Hkv": c.Hkv, "dh": c.dh,
                    "prefix_tokens": P, "max_prefix": max_prefix, "tree": c.tree,
                    "visible_pairs_per_head_avg": round(w["pairs"] / c.Hq / c.R, 1),
-                   "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": "eager"},
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": "eager",
+                   "parallelism": f"dp{ws} (independent tree batches per rank, no collective)" if ws > 1 else "single"},
         "gpu_launches": int(n_launch),
         "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
         "roofline": {"bound": "hbm", "kernel": dom["kernel"], "achieved": dom["achieved_gbs"], "peak": hbm,
@@ -768,11 +789,11 @@ def run_tree_attn(args):
                      "peak_source": f"{peak_src} hbm_gbs (copy)",
                      "work_per_launch": "compulsory DRAM bytes (prefix+tree K/V, Q/dO/O, outputs), DESIGN.md §6 F4",
                      "phases": per},
-        "e2e": {"value": round(w["rows"] / (e2e_ms / 1e3), 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+        "e2e": {"value": round(w["rows"] * ws / (e2e_ms / 1e3), 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(lse.numel() * 4)},
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:
         from oracle import tree_attention as TA
         reqs = list(range(min(4, c.R)))
         sub = tracegen.gen_tree_attn(c.name, requests=reqs)
@@ -783,6 +804,8 @@ def run_tree_attn(args):
                                "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                                "sample": f"first {len(reqs)} of {c.R} requests of '{c.name}', fwd+bwd f64; {dt:.2f} s"}
     print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
 
 
 def main():

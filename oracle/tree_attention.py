@@ -27,6 +27,13 @@ What it computes (PAPER.md = P, SPEC.md = S, line numbers):
       dQ = scale * dS K,  dK = scale * dS^T Q.
   GQA: the G = Hq / Hkv query heads of a kv head share its K, V; their dK, dV add up.
 
+Tree positions and RoPE (F4-R6): node n of request r sits at position
+P_r + depth(n) (depth of the root row = 0, a child of the root = 1, ...), so siblings share a
+position; queries and tree keys are rotated there with the rotate-half convention used by the
+Llama / Qwen3 targets, x'[i] = x[i] cos(p w_i) - x[i + dh/2] sin(p w_i),
+x'[i + dh/2] = x[i + dh/2] cos(p w_i) + x[i] sin(p w_i), w_i = theta^(-2i/dh); the gradient
+w.r.t. the unrotated input is the inverse (transposed) rotation.
+
 Everything is float64 on the exact upcast of the bf16 inputs.  Pins:
 tests/test_tree_attn_oracle.py (torch f64 SDPA + autograd with a mask built by boolean
 matrix powers, causal special case, brute-force scalar loops, finite differences,
@@ -178,3 +185,42 @@ def _select(a, dO, reqs):
              parents=None if a["parents"] is None else a["parents"][reqs],
              num_nodes=None if a["num_nodes"] is None else a["num_nodes"][reqs])
     return b, dO[reqs]
+
+
+def tree_positions(parents_r, num_nodes_r: int, N: int, P_r: int) -> np.ndarray:
+    """Position of every tree row (F4-R6): P_r + depth, depth by walking parent pointers;
+    rows of padded nodes get -1 (left unrotated)."""
+    pos = np.full(N + 1, -1, dtype=np.int64)
+    pos[0] = P_r
+    for n in range(min(num_nodes_r, N)):
+        d, p = 1, (n - 1) if parents_r is None else int(parents_r[n])
+        while p >= 0:
+            d += 1
+            p = (p - 1) if parents_r is None else int(parents_r[p])
+        pos[n + 1] = P_r + d
+    return pos
+
+
+def rope(x: np.ndarray, pos: np.ndarray, theta: float, inverse: bool = False) -> np.ndarray:
+    """Rotate-half RoPE of x [..., rows, heads, dh] at integer positions pos [..., rows]
+    (pos < 0: row left unchanged); inverse=True applies the transposed rotation."""
+    dh = x.shape[-1]
+    half = dh // 2
+    w = theta ** (-2.0 * np.arange(half, dtype=np.float64) / dh)
+    ang = np.asarray(pos, dtype=np.float64)[..., None, None] * w          # [..., rows, 1, half]
+    c, s_ = np.cos(ang), np.sin(ang)
+    if inverse:
+        s_ = -s_
+    a, b = x[..., :half], x[..., half:]
+    out = np.concatenate([a * c - b * s_, b * c + a * s_], axis=-1)
+    keep = np.asarray(pos)[..., None, None] < 0
+    return np.where(keep, x, out)
+
+
+def tree_rope_positions(prefix_off, parents, num_nodes, R: int, N: int) -> np.ndarray:
+    """[R, N+1] positions of every tree row of the batch."""
+    out = np.empty((R, N + 1), dtype=np.int64)
+    for r in range(R):
+        nn = N if num_nodes is None else int(num_nodes[r])
+        out[r] = tree_positions(None if parents is None else parents[r], nn, N, int(prefix_off[r + 1] - prefix_off[r]))
+    return out

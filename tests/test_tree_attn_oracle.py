@@ -234,3 +234,44 @@ def test_sample_subset_is_exact():
     sub = TA.fwd_bwd(tracegen.gen_tree_attn("ta_tiny", requests=[2, 0]))
     np.testing.assert_array_equal(sub["O"], full["O"][[2, 0]])
     np.testing.assert_array_equal(sub["dQ"], full["dQ"][[2, 0]])
+
+
+# ---------------------------------------------------------------- F4-R6 tree positions + RoPE
+def test_tree_positions_are_prefix_plus_depth():
+    par = np.array([-1, -1, 0, 0, 1, 3], dtype=np.int32)     # depths 1 1 2 2 2 3
+    pos = TA.tree_positions(par, 6, 6, 100)
+    assert pos.tolist() == [100, 101, 101, 102, 102, 102, 103]
+    assert TA.tree_positions(None, 4, 4, 7).tolist() == [7, 8, 9, 10, 11]     # chain = causal positions
+    assert TA.tree_positions(par, 2, 6, 0).tolist() == [0, 1, 1, -1, -1, -1, -1]  # padded nodes
+
+
+def test_rope_matches_transformers_llama_rotary():
+    """Pinned to the library routine the targets use (transformers' apply_rotary_pos_emb with
+    Llama's inv_freq = theta^(-2i/dh) and cos/sin of pos * inv_freq repeated over both halves)."""
+    from transformers.models.llama.modeling_llama import apply_rotary_pos_emb
+    rng = np.random.default_rng(2)
+    rows, H, dh, theta = 9, 3, 16, 500000.0
+    q = rng.standard_normal((rows, H, dh))
+    k = rng.standard_normal((rows, 1, dh))
+    pos = np.array([5, 6, 6, 7, 7, 7, 2040, 0, 1])
+    inv = 1.0 / (theta ** (torch.arange(0, dh, 2, dtype=torch.float64) / dh))
+    fr = torch.tensor(pos, dtype=torch.float64)[:, None] * inv[None, :]
+    emb = torch.cat([fr, fr], dim=-1)
+    qt, kt = apply_rotary_pos_emb(torch.tensor(q).transpose(0, 1)[None], torch.tensor(k).transpose(0, 1)[None],
+                                  emb.cos()[None], emb.sin()[None])
+    np.testing.assert_allclose(TA.rope(q, pos, theta), qt[0].transpose(0, 1).numpy(), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(TA.rope(k, pos, theta), kt[0].transpose(0, 1).numpy(), rtol=1e-12, atol=1e-12)
+
+
+def test_rope_invariants():
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((6, 2, 32))
+    pos = np.array([0, 3, 3, 9, -1, 2047])
+    y = TA.rope(x, pos, 10000.0)
+    np.testing.assert_allclose(np.linalg.norm(y, axis=-1), np.linalg.norm(x, axis=-1), rtol=1e-13)   # rotation
+    np.testing.assert_allclose(TA.rope(y, pos, 10000.0, inverse=True), x, rtol=1e-12, atol=1e-12)    # inverse
+    assert np.array_equal(y[4], x[4])                                                                 # pos < 0
+    # relative positions: <R(m) q, R(n) k> depends only on m - n
+    q, k = rng.standard_normal((1, 1, 32)), rng.standard_normal((1, 1, 32))
+    dot = lambda m, n: float(np.sum(TA.rope(q, np.array([m]), 1e4) * TA.rope(k, np.array([n]), 1e4)))
+    assert abs(dot(10, 7) - dot(103, 100)) < 1e-10 and abs(dot(0, 0) - float(np.sum(q * k))) < 1e-12
