@@ -336,6 +336,17 @@ aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, const void* Q
                                      const float* lse, const void* dO, float* dQ, void* dKt, void* dVt,
                                      void* dKp, void* dVp, void* ws, size_t ws_bytes, void* stream);
 
+/* Tree positions + RoPE (F4-R6): tree row s of request r sits at position P_r + depth(s)
+ * (root depth 0; siblings share a position); rotates, in place, Q [R, N+1, Hq, dh] and the tree
+ * keys Kt [R, N+1, Hkv, dh] there with the rotate-half convention (pairs (i, i + dh/2), angle
+ * pos * theta^(-2i/dh)); inverse != 0 applies the transposed rotation (dQ / dKt of the rotated
+ * tensors -> gradients of the unrotated ones).  Q or Kt may be NULL (skipped); *_fp32 selects
+ * f32 instead of bf16 storage.  Padded / malformed rows are left unrotated (STRUCTURE bit for
+ * malformed parents, as the attention kernels).  The cached prefix keys are not touched (already
+ * rotated at positions 0..P_r-1).  Limits: dh even, <= 256; theta > 1. */
+aurora_status_t aurora_tree_rope(const aurora_tree_attn_t* ta, void* Q, int q_fp32, void* Kt, int kt_fp32,
+                                 float theta, int inverse, void* stream);
+
 /* Per-phase device timing (CUDA events recorded on the caller's stream around each
  * phase while enabled).  aurora_profile_read must be called after the stream was
  * synchronised; it fills up to `max` (name, total ms, launches) triples and returns

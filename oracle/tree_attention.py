@@ -37,7 +37,8 @@ w.r.t. the unrotated input is the inverse (transposed) rotation.
 Everything is float64 on the exact upcast of the bf16 inputs.  Pins:
 tests/test_tree_attn_oracle.py (torch f64 SDPA + autograd with a mask built by boolean
 matrix powers, causal special case, brute-force scalar loops, finite differences,
-branch-independence, single-key identity, GQA = repeated-KV MHA).
+branch-independence, single-key identity, GQA = repeated-KV MHA; RoPE against transformers'
+apply_rotary_pos_emb, rotation / inverse / relative-position invariants).
 """
 from __future__ import annotations
 

@@ -29,7 +29,7 @@ EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fw
            "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option",
            "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step",
            "aurora_profile_peek", "aurora_spec_loss_bwd_adamw", "aurora_tree_attn_fwd",
-           "aurora_tree_attn_workspace_size", "aurora_tree_attn_bwd"]
+           "aurora_tree_attn_workspace_size", "aurora_tree_attn_bwd", "aurora_tree_rope"]
 
 
 class AuroraError(RuntimeError):
@@ -141,6 +141,8 @@ def lib() -> C.CDLL:
     L.aurora_tree_attn_workspace_size.restype = sz
     L.aurora_tree_attn_bwd.argtypes = [C.POINTER(aurora_tree_attn_t)] + [vp] * 14 + [sz, vp]
     L.aurora_tree_attn_bwd.restype = C.c_int
+    L.aurora_tree_rope.argtypes = [C.POINTER(aurora_tree_attn_t), vp, C.c_int, vp, C.c_int, C.c_float, C.c_int, vp]
+    L.aurora_tree_rope.restype = C.c_int
     L.aurora_get_option.argtypes = [C.c_char_p]
     L.aurora_get_option.restype = C.c_int64
     _lib = L
@@ -456,3 +458,13 @@ class TreeAttention:
             C.byref(self.cfg), _ptr(Q), _ptr(Kt), _ptr(Vt), _ptr(Kp), _ptr(Vp), _ptr(O), _ptr(lse), _ptr(dO),
             _ptr(dQ), _ptr(dKt), _ptr(dVt), _ptr(dKp), _ptr(dVp), _ptr(self.ws), self.ws.numel(),
             _stream(stream)))
+
+    def rope(self, Q=None, Kt=None, theta: float = 500000.0, inverse: bool = False, stream=None):
+        """In-place tree-position RoPE of Q and/or the tree keys Kt (bf16 or f32 tensors)."""
+        for t, n in [(Q, "Q"), (Kt, "Kt")]:
+            if t is not None:
+                _expect(t, "f32" if t.dtype.is_floating_point and t.element_size() == 4 else "bf16", n)
+        q32 = int(Q is not None and Q.element_size() == 4)
+        k32 = int(Kt is not None and Kt.element_size() == 4)
+        _check("aurora_tree_rope", lib().aurora_tree_rope(C.byref(self.cfg), _ptr(Q), q32, _ptr(Kt), k32,
+                                                          float(theta), int(bool(inverse)), _stream(stream)))

@@ -23,6 +23,7 @@
 // (DESIGN.md §6): at these shapes the phase is close to HBM-bound on the prefix K/V.
 #include <cmath>
 #include <initializer_list>
+#include <type_traits>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -1192,6 +1193,68 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_ta_fwd_tc(const __grid_consta
   }
 }
 
+
+// ------------------------------------------------------------------------------ tree RoPE
+// Block per tree row (request r, row s): position P_r + depth(s) (F4-R6; siblings share it),
+// cos/sin of pos * theta^(-2i/dh) for the dh/2 frequencies computed once in double into shared
+// memory, then every query head of the row (and every KV head of its tree key) is rotated in
+// place (rotate-half pairs (i, i + dh/2)); inverse = the transposed rotation (for gradients).
+template <typename TQ, typename TK>
+__global__ void __launch_bounds__(128) k_ta_rope(TaParams p, TQ* __restrict__ Q, TK* __restrict__ Kt, int dh,
+                                                 double log2_theta, int inverse) {
+  __shared__ float s_cos[128], s_sin[128];
+  __shared__ int s_pos;
+  const int row = blockIdx.x, r = row / p.N1, s = row - r * p.N1;
+  if (threadIdx.x == 0) {
+    const int Pr = p.prefix_off[r + 1] - p.prefix_off[r];
+    const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
+    int pos = -1;
+    if (nn >= 0 && nn <= p.N) {
+      if (s == 0) {
+        pos = Pr;
+      } else if (s - 1 < nn) {
+        int cur = s - 1, d = 1;
+        for (int it = 0; it <= p.N; ++it) {
+          const int par = p.parents ? p.parents[(size_t)r * p.N + cur] : cur - 1;
+          if (par < -1 || par >= cur) { d = -1; break; }
+          if (par < 0) break;
+          ++d;
+          cur = par;
+        }
+        pos = d < 0 ? -1 : Pr + d;
+        if (d < 0 && p.status) atomicOr(p.status, (uint32_t)AURORA_STATUS_STRUCTURE);
+      }
+    } else if (p.status) {
+      atomicOr(p.status, (uint32_t)AURORA_STATUS_STRUCTURE);
+    }
+    s_pos = pos;
+  }
+  __syncthreads();
+  const int pos = s_pos;
+  if (pos < 0) return;  // padded / malformed row: left unrotated
+  const int half = dh >> 1;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const double w = exp2(-(2.0 * i / dh) * log2_theta);
+    double sn, cs;
+    sincos(static_cast<double>(pos) * w, &sn, &cs);
+    s_cos[i] = static_cast<float>(cs);
+    s_sin[i] = static_cast<float>(inverse ? -sn : sn);
+  }
+  __syncthreads();
+  auto rot = [&](auto* base, int heads) {
+    for (int e = threadIdx.x; e < heads * half; e += blockDim.x) {
+      const int h = e / half, i = e - h * half;
+      auto* x = base + ((size_t)row * heads + h) * dh;
+      const float a = static_cast<float>(x[i]), b = static_cast<float>(x[i + half]);
+      const float c = s_cos[i], sn = s_sin[i];
+      x[i] = static_cast<std::remove_reference_t<decltype(x[i])>>(a * c - b * sn);
+      x[i + half] = static_cast<std::remove_reference_t<decltype(x[i])>>(b * c + a * sn);
+    }
+  };
+  if (Q) rot(Q, p.Hq);
+  if (Kt) rot(Kt, p.Hkv);
+}
+
 // ------------------------------------------------------------------------------ host
 struct TaLaunch {
   int Gc, nchunk, nw;
@@ -1366,5 +1429,29 @@ extern "C" aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, co
     prof_end(PH_TREE_BWD_DKDV, s);
     count_launch(3);
   }
+  return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
+}
+
+extern "C" aurora_status_t aurora_tree_rope(const aurora_tree_attn_t* ta, void* Q, int q_fp32, void* Kt,
+                                            int kt_fp32, float theta, int inverse, void* stream) {
+  if (!ta || !ta->prefix_off || ta->R < 1 || ta->N < 1 || ta->Hq < 1 || ta->Hkv < 1) return AURORA_ERR_INVALID_ARG;
+  if (ta->N > AURORA_MAX_NODES || ta->dh < 2 || ta->dh > 256 || (ta->dh & 1)) return AURORA_ERR_UNSUPPORTED;
+  if (!(theta > 1.f)) return AURORA_ERR_INVALID_ARG;
+  if (!Q && !Kt) return AURORA_OK;
+  TaLaunch L;
+  TaParams p = ta_params(ta, L);
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)(ta->R * (ta->N + 1));
+  const double l2t = std::log2(static_cast<double>(theta));
+  using bf = __nv_bfloat16;
+  if (!q_fp32 && !kt_fp32)
+    k_ta_rope<bf, bf><<<grid, 128, 0, s>>>(p, (bf*)Q, (bf*)Kt, ta->dh, l2t, inverse);
+  else if (q_fp32 && kt_fp32)
+    k_ta_rope<float, float><<<grid, 128, 0, s>>>(p, (float*)Q, (float*)Kt, ta->dh, l2t, inverse);
+  else if (q_fp32)
+    k_ta_rope<float, bf><<<grid, 128, 0, s>>>(p, (float*)Q, (bf*)Kt, ta->dh, l2t, inverse);
+  else
+    k_ta_rope<bf, float><<<grid, 128, 0, s>>>(p, (bf*)Q, (float*)Kt, ta->dh, l2t, inverse);
+  count_launch();
   return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
 }

@@ -153,3 +153,40 @@ def test_tree_attention_errors():
     ta.forward(t["Q"], t["Kt"], t["Vt"], t["Kp"], t["Vp"], O, lse)
     torch.cuda.synchronize()
     assert int(ta.status.item()) & A.STATUS_RANGE
+
+
+@pytest.mark.parametrize("name,theta", [("ta_small", 500000.0), ("ta_gqa8", 1000000.0), ("ta_chain", 10000.0)])
+def test_tree_rope_parity(name, theta):
+    """F4-R6: tree positions + rotate-half RoPE against the oracle (bf16 in place: one bf16
+    rounding of the rotated value; f32 inverse on the rotated values: round trip)."""
+    from paper_2602_06932_b200 import aurora as A
+    inp = tracegen.gen_tree_attn(name)
+    c = inp["cfg"]
+    R = len(inp["requests"])
+    off = inp["prefix_off"]
+    poff = torch.from_numpy(off.astype(np.int32)).cuda()
+    par = None if inp["parents"] is None else torch.from_numpy(inp["parents"].astype(np.int32)).cuda()
+    nn = None if inp["num_nodes"] is None else torch.from_numpy(inp["num_nodes"].astype(np.int32)).cuda()
+    ta = A.TreeAttention(R, c.N, c.Hq, c.Hkv, c.dh, poff, int(np.diff(off).max()), parents=par, num_nodes=nn)
+    Q, Kt = _bf(inp["Q_bits"]), _bf(inp["Kt_bits"])
+    pos = TA.tree_rope_positions(off, inp["parents"], inp["num_nodes"], R, c.N)
+    q64, k64 = TA.bf16_bits_to_f64(inp["Q_bits"]), TA.bf16_bits_to_f64(inp["Kt_bits"])
+    ref_q, ref_k = TA.rope(q64, pos, theta), TA.rope(k64, pos, theta)
+    Qf, Ktf = Q.float().clone(), Kt.float().clone()
+    ta.rope(Q, Kt, theta=theta)
+    ta.rope(Qf, Ktf, theta=theta)
+    torch.cuda.synchronize()
+    assert int(ta.status.item()) == 0
+    for got, ref in [(Q, ref_q), (Kt, ref_k)]:
+        g = _to64(got)
+        np.testing.assert_allclose(g, ref, rtol=2 ** -8, atol=1e-5)           # one bf16 rounding
+    np.testing.assert_allclose(Qf.cpu().numpy(), ref_q, rtol=1e-5, atol=1e-5)   # f32 storage
+    np.testing.assert_allclose(Ktf.cpu().numpy(), ref_k, rtol=1e-5, atol=1e-5)
+    # padded rows untouched, inverse restores the input (f32)
+    pad = pos < 0
+    if pad.any():
+        assert np.array_equal(_to64(Q)[pad], q64[pad])
+    ta.rope(Qf, Ktf, theta=theta, inverse=True)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(Qf.cpu().numpy(), q64, rtol=1e-5, atol=2e-5)
+    np.testing.assert_allclose(Ktf.cpu().numpy(), k64, rtol=1e-5, atol=2e-5)
