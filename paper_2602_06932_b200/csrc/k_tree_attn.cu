@@ -676,8 +676,6 @@ __global__ void __launch_bounds__(256) k_ta_bwd_dkdv(TaParams p) {
 #endif
 constexpr int kFbNK = TA_FB_NK, kFbST = 3;
 constexpr int kFbRowB = kFbNK * 2;  // bytes per row of the parked P / dS tiles
-constexpr int kFbMT = kFbNK / 16;   // key phase: 16-key m-tiles per tile
-constexpr int kFbDW = 128 * kFbMT / 8;  // key phase: head dims per warp (8 warps)
 
 __device__ __forceinline__ uint32_t swz_p(int row, int ch) {
   if constexpr (kFbRowB == 128) return row * 128 + ((ch ^ (row & 7)) << 4);
@@ -729,7 +727,6 @@ __global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
   const float c2 = p.c2;
-  const int mt = warp % kFbMT, grp = warp / kFbMT;  // key phase: keys 16*mt.., head dims kFbDW*grp..
   const int nks = (rows + 15) >> 4;               // 16-row steps holding valid rows
 
   for (int t = 0; t < ntiles; ++t) {
@@ -768,58 +765,75 @@ __global__ void __launch_bounds__(256) k_ta_bwd_fused(TaParams p) {
       mma_p_x_rows<NK>(dq, s, kb, lane);  // dQ += dS K
     }
     __syncthreads();
-    // ---- key phase: dV[16 keys x kFbDW dims] = P^T dO, dK = dS^T Q over the valid rows
+    // ---- key phase: warp = 32 keys (two 16-key m-tiles) x 32 head dims; dV = P^T dO, dK = dS^T Q
+    // over the valid rows.  Each B fragment (dO, Q) now feeds two m-tiles: 8 ldmatrix per 16 MMAs.
     {
-      constexpr int NT8 = kFbDW / 8;
-      float dv[NT8][4], dk[NT8][4];
+      static_assert(kFbNK == 64, "key phase tiling assumes 64-key tiles");
+      const int kp = warp & 1, g32 = warp >> 1;
+      float dv[2][4][4], dk[2][4][4];
 #pragma unroll
-      for (int j = 0; j < NT8; ++j) {
-        dv[j][0] = dv[j][1] = dv[j][2] = dv[j][3] = 0.f;
-        dk[j][0] = dk[j][1] = dk[j][2] = dk[j][3] = 0.f;
-      }
+      for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          dv[m][j][0] = dv[m][j][1] = dv[m][j][2] = dv[m][j][3] = 0.f;
+          dk[m][j][0] = dk[m][j][1] = dk[m][j][2] = dk[m][j][3] = 0.f;
+        }
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {  // 16 query rows per step
         if (ks >= nks) break;
-        uint32_t ap[4], ad[4];
-        const int prow = ks * 16 + (lane & 7) + ((lane >> 4) << 3), pch = 2 * mt + ((lane >> 3) & 1);
-        ldsm4t(ap, aP + swz_p(prow, pch));
-        ldsm4t(ad, adS + swz_p(prow, pch));
+        uint32_t ap[2][4], ad[2][4];
+        const int prow = ks * 16 + (lane & 7) + ((lane >> 4) << 3);
 #pragma unroll
-        for (int np = 0; np < NT8 / 2; ++np) {
+        for (int m = 0; m < 2; ++m) {
+          const int pch = 2 * (2 * kp + m) + ((lane >> 3) & 1);
+          ldsm4t(ap[m], aP + swz_p(prow, pch));
+          ldsm4t(ad[m], adS + swz_p(prow, pch));
+        }
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
           uint32_t b[4];
-          const int brow = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), bch = NT8 * grp + 2 * np + (lane >> 4);
+          const int brow = ks * 16 + (lane & 7) + (((lane >> 3) & 1) << 3), bch = 4 * g32 + 2 * np + (lane >> 4);
           ldsm4t(b, adO + swz(brow, bch));
-          mma16816(dv[2 * np], ap, b[0], b[1]);
-          mma16816(dv[2 * np + 1], ap, b[2], b[3]);
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            mma16816(dv[m][2 * np], ap[m], b[0], b[1]);
+            mma16816(dv[m][2 * np + 1], ap[m], b[2], b[3]);
+          }
           ldsm4t(b, aQ + swz(brow, bch));
-          mma16816(dk[2 * np], ad, b[0], b[1]);
-          mma16816(dk[2 * np + 1], ad, b[2], b[3]);
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            mma16816(dk[m][2 * np], ad[m], b[0], b[1]);
+            mma16816(dk[m][2 * np + 1], ad[m], b[2], b[3]);
+          }
         }
       }
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int kj = t * NK + mt * 16 + (lane >> 2) + half * 8;
-        if (kj >= nkeys) continue;
-        size_t off;
-        uint16_t *dk_dst, *dv_dst;
-        if (kj < Pr) {
-          off = ((size_t)(p0 + kj) * p.Hkv + hk) * D;
-          dk_dst = p.dKp;
-          dv_dst = p.dVp;
-        } else {
-          off = (((size_t)r * p.N1 + (kj - Pr)) * p.Hkv + hk) * D;
-          dk_dst = p.dKt;
-          dv_dst = p.dVt;
-        }
-        off += kFbDW * grp + 2 * (lane & 3);
+      for (int m = 0; m < 2; ++m)
 #pragma unroll
-        for (int nt = 0; nt < NT8; ++nt) {
-          *reinterpret_cast<uint32_t*>(dv_dst + off + nt * 8) = pk_bf16(dv[nt][2 * half], dv[nt][2 * half + 1]);
-          *reinterpret_cast<uint32_t*>(dk_dst + off + nt * 8) =
-              pk_bf16(dk[nt][2 * half] * p.scale, dk[nt][2 * half + 1] * p.scale);
+        for (int half = 0; half < 2; ++half) {
+          const int kj = t * NK + (2 * kp + m) * 16 + (lane >> 2) + half * 8;
+          if (kj >= nkeys) continue;
+          size_t off;
+          uint16_t *dk_dst, *dv_dst;
+          if (kj < Pr) {
+            off = ((size_t)(p0 + kj) * p.Hkv + hk) * D;
+            dk_dst = p.dKp;
+            dv_dst = p.dVp;
+          } else {
+            off = (((size_t)r * p.N1 + (kj - Pr)) * p.Hkv + hk) * D;
+            dk_dst = p.dKt;
+            dv_dst = p.dVt;
+          }
+          off += 32 * g32 + 2 * (lane & 3);
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) {
+            *reinterpret_cast<uint32_t*>(dv_dst + off + nt * 8) = pk_bf16(dv[m][nt][2 * half], dv[m][nt][2 * half + 1]);
+            *reinterpret_cast<uint32_t*>(dk_dst + off + nt * 8) =
+                pk_bf16(dk[m][nt][2 * half] * p.scale, dk[m][nt][2 * half + 1] * p.scale);
+          }
         }
-      }
     }
+
   }
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
