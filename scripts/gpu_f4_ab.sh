@@ -3,7 +3,7 @@
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 export AURORA_TREE_FWD_TC=${AURORA_TREE_FWD_TC:-1}
-for v in "" B C D; do
+for v in "" B C; do
   lib=paper_2602_06932_b200/libaurora${v:+_$v}.so
   AURORA_LIB=$PWD/$lib timeout 400 python bench.py --workload tree_attn --ta-config ${TA_CFG:-ta_tree} --no-cpu-baseline > gpurun_out/ab_$v.json 2>/dev/null
   python -c "
