@@ -29,7 +29,8 @@ EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fw
            "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option",
            "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step",
            "aurora_profile_peek", "aurora_spec_loss_bwd_adamw", "aurora_tree_attn_fwd",
-           "aurora_tree_attn_workspace_size", "aurora_tree_attn_bwd", "aurora_tree_rope"]
+           "aurora_tree_attn_workspace_size", "aurora_tree_attn_bwd", "aurora_tree_rope",
+           "aurora_draft_layer_workspace_size", "aurora_draft_layer_fwd", "aurora_draft_layer_bwd"]
 
 
 class AuroraError(RuntimeError):
@@ -74,6 +75,22 @@ class aurora_tree_attn_t(C.Structure):
     _fields_ = [("R", C.c_int32), ("N", C.c_int32), ("Hq", C.c_int32), ("Hkv", C.c_int32), ("dh", C.c_int32),
                 ("max_prefix", C.c_int32), ("prefix_total", C.c_int64), ("prefix_off", C.c_void_p), ("parents", C.c_void_p),
                 ("num_nodes", C.c_void_p), ("scale", C.c_float), ("status", C.c_void_p)]
+
+
+class aurora_draft_layer_t(C.Structure):
+    _fields_ = [("ta", aurora_tree_attn_t), ("d", C.c_int32), ("I", C.c_int32), ("theta", C.c_float),
+                ("eps", C.c_float)]
+
+
+_DL_W = ["Wfc", "Wq", "Wk", "Wv", "Wo", "Wg", "Wu", "Wd", "we", "wh", "wpost"]
+
+
+class aurora_draft_weights_t(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in _DL_W]
+
+
+class aurora_draft_grads_t(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in _DL_W]
 
 
 _lib = None
@@ -143,6 +160,14 @@ def lib() -> C.CDLL:
     L.aurora_tree_attn_bwd.restype = C.c_int
     L.aurora_tree_rope.argtypes = [C.POINTER(aurora_tree_attn_t), vp, C.c_int, vp, C.c_int, C.c_float, C.c_int, vp]
     L.aurora_tree_rope.restype = C.c_int
+    L.aurora_draft_layer_workspace_size.argtypes = [C.POINTER(aurora_draft_layer_t)]
+    L.aurora_draft_layer_workspace_size.restype = sz
+    L.aurora_draft_layer_fwd.argtypes = [C.POINTER(aurora_draft_layer_t), C.POINTER(aurora_draft_weights_t)] + \
+        [vp] * 6 + [sz, vp]
+    L.aurora_draft_layer_fwd.restype = C.c_int
+    L.aurora_draft_layer_bwd.argtypes = [C.POINTER(aurora_draft_layer_t), C.POINTER(aurora_draft_weights_t)] + \
+        [vp] * 5 + [C.POINTER(aurora_draft_grads_t)] + [vp] * 5 + [sz, vp]
+    L.aurora_draft_layer_bwd.restype = C.c_int
     L.aurora_get_option.argtypes = [C.c_char_p]
     L.aurora_get_option.restype = C.c_int64
     _lib = L
@@ -468,3 +493,35 @@ class TreeAttention:
         k32 = int(Kt is not None and Kt.element_size() == 4)
         _check("aurora_tree_rope", lib().aurora_tree_rope(C.byref(self.cfg), _ptr(Q), q32, _ptr(Kt), k32,
                                                           float(theta), int(bool(inverse)), _stream(stream)))
+
+
+class DraftLayer:
+    """F4 draft layer (include/aurora.h aurora_draft_layer_*, reading F4-R7): marshalling only.
+    `ta` is a TreeAttention (batch structure + heads); W maps the names of aurora_draft_weights_t
+    to device tensors (bf16 matrices, f32 norm weights)."""
+
+    def __init__(self, ta: "TreeAttention", d: int, I: int, W: dict, theta: float = 500000.0, eps: float = 1e-6):
+        import torch
+        for n in _DL_W:
+            _expect(W[n], "f32" if n in ("we", "wh", "wpost") else "bf16", n)
+        self.ta, self.W = ta, W
+        self.cfg = aurora_draft_layer_t(ta.cfg, d, I, float(theta), float(eps))
+        self.w = aurora_draft_weights_t(*[_ptr(W[n]) for n in _DL_W])
+        nbytes = int(lib().aurora_draft_layer_workspace_size(C.byref(self.cfg)))
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=ta.status.device)
+
+    def forward(self, h3, e, Kp, Vp, H, stream=None):
+        for t, n in [(h3, "h3"), (e, "e"), (Kp, "Kp"), (Vp, "Vp"), (H, "H")]:
+            _expect(t, "bf16", n)
+        _check("aurora_draft_layer_fwd", lib().aurora_draft_layer_fwd(
+            C.byref(self.cfg), C.byref(self.w), _ptr(h3), _ptr(e), _ptr(Kp), _ptr(Vp), _ptr(H), _ptr(self.ws),
+            self.ws.numel(), _stream(stream)))
+
+    def backward(self, h3, e, Kp, Vp, dH, G: dict, dh3, de, dKp, dVp, stream=None):
+        _expect(dH, "f32", "dH")
+        for n in _DL_W:
+            _expect(G[n], "f32", "G." + n)
+        g = aurora_draft_grads_t(*[_ptr(G[n]) for n in _DL_W])
+        _check("aurora_draft_layer_bwd", lib().aurora_draft_layer_bwd(
+            C.byref(self.cfg), C.byref(self.w), _ptr(h3), _ptr(e), _ptr(Kp), _ptr(Vp), _ptr(dH), C.byref(g),
+            _ptr(dh3), _ptr(de), _ptr(dKp), _ptr(dVp), _ptr(self.ws), self.ws.numel(), _stream(stream)))

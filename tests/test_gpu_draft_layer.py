@@ -1,0 +1,81 @@
+"""GPU parity of the F4 draft layer (aurora_draft_layer_fwd/bwd, reading F4-R7) against the f64
+oracle (oracle/draft_layer.py, pinned to torch autograd in tests/test_draft_layer_oracle.py) on
+identical seeded bf16 inputs.  Tolerances: H at 1e-2 relative Frobenius error (bf16 activations
+between the GEMMs), every gradient at the north star's 2e-2."""
+import numpy as np
+import pytest
+import torch
+
+import tracegen
+from oracle import draft_layer as DL
+from oracle import tree_attention as TA
+
+pytestmark = pytest.mark.gpu
+
+
+def _bf_round(x):
+    return TA.bf16_bits_to_f64(tracegen.f32_to_bf16_bits(np.asarray(x, np.float32)))
+
+
+def _case(seed=7):
+    rng = np.random.default_rng(seed)
+    R, N, d, I, Hq, Hkv, dh = 3, 8, 256, 384, 4, 2, 128
+    parents = np.array([[-1, -1, 0, 0, 1, 2, 3, 4], [-1, 0, 1, 2, 3, 4, 5, 6], [-1, -1, -1, 0, 1, 2, 3, 3]],
+                       dtype=np.int32)
+    num_nodes = np.array([8, 8, 6], dtype=np.int32)
+    lens = np.array([40, 0, 75])
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    sc = lambda fan: 1.0 / np.sqrt(fan)
+    n = lambda *s, k=1.0: rng.standard_normal(s) * k
+    P = dict(Wfc=_bf_round(n(d, 3 * d, k=sc(3 * d))), we=1 + n(d, k=0.1), wh=1 + n(d, k=0.1),
+             Wq=_bf_round(n(Hq * dh, 2 * d, k=sc(2 * d))), Wk=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))),
+             Wv=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))), Wo=_bf_round(n(d, Hq * dh, k=sc(Hq * dh))),
+             wpost=1 + n(d, k=0.1), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
+             Wd=_bf_round(n(d, I, k=sc(I))))
+    for k in ("we", "wh", "wpost"):
+        P[k] = P[k].astype(np.float32).astype(np.float64)
+    X = dict(h3=_bf_round(n(R, N + 1, 3 * d)), e=_bf_round(n(R, N + 1, d)), Kp=_bf_round(n(int(lens.sum()), Hkv, dh)),
+             Vp=_bf_round(n(int(lens.sum()), Hkv, dh)), prefix_off=off, parents=parents, num_nodes=num_nodes)
+    cfg = dict(Hq=Hq, Hkv=Hkv, dh=dh, theta=500000.0, eps=1e-6, d=d, I=I, R=R, N=N)
+    dH = n(R, N + 1, d, k=0.1).astype(np.float32).astype(np.float64)
+    return P, X, cfg, dH
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def test_draft_layer_parity():
+    from paper_2602_06932_b200 import aurora as A
+    P, X, cfg, dH = _case()
+    dev = "cuda"
+    bf = lambda x: torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16).to(dev).contiguous()
+    f32 = lambda x: torch.tensor(np.asarray(x, np.float32)).to(dev).contiguous()
+    W = {k: (f32(v) if k in ("we", "wh", "wpost") else bf(v)) for k, v in P.items()}
+    R, N, d, I = cfg["R"], cfg["N"], cfg["d"], cfg["I"]
+    M = R * (N + 1)
+    poff = torch.tensor(X["prefix_off"], dtype=torch.int32, device=dev)
+    ta = A.TreeAttention(R, N, cfg["Hq"], cfg["Hkv"], cfg["dh"], poff, int(np.diff(X["prefix_off"]).max()),
+                         parents=torch.tensor(X["parents"], device=dev), num_nodes=torch.tensor(X["num_nodes"], device=dev))
+    layer = A.DraftLayer(ta, d, I, W, theta=cfg["theta"], eps=cfg["eps"])
+    h3, e = bf(X["h3"].reshape(M, 3 * d)), bf(X["e"].reshape(M, d))
+    Kp, Vp = bf(X["Kp"]), bf(X["Vp"])
+    H = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    layer.forward(h3, e, Kp, Vp, H)
+    G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in W.items()}
+    dh3 = torch.empty(M, 3 * d, dtype=torch.float32, device=dev)
+    de = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
+    layer.backward(h3, e, Kp, Vp, f32(dH.reshape(M, d)), G, dh3, de, dKp, dVp)
+    torch.cuda.synchronize()
+    assert int(ta.status.item()) == 0
+
+    Hr, S = DL.layer_fwd(P, X, cfg)
+    Gr = DL.layer_bwd(P, X, cfg, S, dH)
+    assert _rel(H.float().cpu().numpy().reshape(Hr.shape), Hr) <= 1e-2
+    got = {k: G[k].cpu().numpy() for k in G}
+    got.update(h3=dh3.cpu().numpy().reshape(Gr["h3"].shape), e=de.cpu().numpy().reshape(Gr["e"].shape),
+               Kp=dKp.float().cpu().numpy(), Vp=dVp.float().cpu().numpy())
+    errs = {k: _rel(got[k], Gr[k]) for k in Gr}
+    bad = {k: v for k, v in errs.items() if v > 2e-2}
+    assert not bad, errs
