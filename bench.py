@@ -808,6 +808,102 @@ def run_tree_attn(args):
         dist.destroy_process_group()
 
 
+def run_draft_layer(args):
+    """F4 bench: the whole EAGLE-3 draft layer (fc + decoder layer with tree RoPE and tree
+    attention), fwd + bwd, over the F4 tree workloads with the target's dense shapes (d = 4096;
+    MLP 14336 for the Llama-3.1-8B speculator, 12288 for Qwen3-8B).  Weights/inputs drawn on the
+    device from a seeded generator (N(0, 1/fan_in) weights, N(0, 1) inputs)."""
+    import torch
+    from paper_2602_06932_b200 import aurora as A
+    from paper_2602_06932_b200.build import build
+
+    ws, rank, local = _dist_env()
+    if rank != 0:        # measured on one GPU (requests are independent; see run_tree_attn for N > 1)
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    build()
+    A.lib()
+    meta = tracegen.gen_tree_attn_meta(args.ta_config)
+    c = meta["cfg"]
+    d, I = 4096, (14336 if c.name == "ta_llama" else 12288)
+    N1 = c.N + 1
+    M = c.R * N1
+    off = meta["prefix_off"]
+    P = int(off[-1])
+    g = torch.Generator(device=dev)
+    g.manual_seed(c.seed + 17)
+    rnd = lambda *s, k=1.0: (torch.randn(*s, generator=g, device=dev) * k).to(torch.bfloat16)
+    qd, kd = c.Hq * c.dh, c.Hkv * c.dh
+    W = dict(Wfc=rnd(d, 3 * d, k=(3 * d) ** -0.5), Wq=rnd(qd, 2 * d, k=(2 * d) ** -0.5),
+             Wk=rnd(kd, 2 * d, k=(2 * d) ** -0.5), Wv=rnd(kd, 2 * d, k=(2 * d) ** -0.5), Wo=rnd(d, qd, k=qd ** -0.5),
+             Wg=rnd(I, d, k=d ** -0.5), Wu=rnd(I, d, k=d ** -0.5), Wd=rnd(d, I, k=I ** -0.5),
+             we=torch.ones(d, device=dev), wh=torch.ones(d, device=dev), wpost=torch.ones(d, device=dev))
+    h3, e = rnd(M, 3 * d), rnd(M, d)
+    Kp, Vp = rnd(P, c.Hkv, c.dh), rnd(P, c.Hkv, c.dh)
+    dH = torch.randn(M, d, generator=g, device=dev) * 0.1
+    poff = torch.from_numpy(off.astype(np.int32)).to(dev)
+    par = None if meta["parents"] is None else torch.from_numpy(meta["parents"].astype(np.int32)).to(dev)
+    nn = None if meta["num_nodes"] is None else torch.from_numpy(meta["num_nodes"].astype(np.int32)).to(dev)
+    ta = A.TreeAttention(c.R, c.N, c.Hq, c.Hkv, c.dh, poff, int(np.diff(off).max()), parents=par, num_nodes=nn)
+    layer = A.DraftLayer(ta, d, I, W, theta=500000.0 if c.name == "ta_llama" else 1000000.0, eps=1e-6)
+    H = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in W.items()}
+    dh3 = torch.empty(M, 3 * d, dtype=torch.float32, device=dev)
+    de = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        layer.forward(h3, e, Kp, Vp, H)
+        layer.backward(h3, e, Kp, Vp, dH, G, dh3, de, dKp, dVp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert int(ta.status.item()) == 0
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    A.aurora_profile_read()
+    A.aurora_profile_enable(True)
+    n0 = A.aurora_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    n_launch = A.aurora_launch_count() - n0
+    A.aurora_profile_enable(False)
+    phases = A.aurora_profile_read()
+    ms_step = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    w = _ta_work(meta)
+    gemm_fwd = 2.0 * M * (3 * d * d + 2 * d * (qd + 2 * kd) + qd * d + 3 * d * I)
+    flops = 3.0 * gemm_fwd + w["fwd_flops"] + w["bwd_flops"]
+    peak_burst, peak_sus, hbm, peak_src = _peaks()
+    achieved = flops / (ms_step / 1e3) / 1e12
+    attn_ms = sum(v[0] for k, v in phases.items() if k.startswith("tree_attn")) / args.steps
+    out = {
+        "metric": "draft-layer fwd+bwd tokens/s (F4: EAGLE-3 fc + decoder layer with tree RoPE + tree attention)",
+        "value": round(M / (ms_step / 1e3), 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded device generator; tracegen structure)",
+        "config": {"workload": c.name + "+draft_layer", "R": c.R, "N": c.N, "d": d, "I": I, "Hq": c.Hq, "Hkv": c.Hkv,
+                   "dh": c.dh, "prefix_tokens": P, "gemm": "cuBLAS bf16 (library GEMMs)",
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": "eager"},
+        "gpu_launches": int(n_launch),
+        "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
+        "roofline": {"bound": "tensor", "kernel": "draft_layer_step", "achieved": round(achieved, 1),
+                     "peak": peak_sus, "unit": "TFLOP/s", "frac": round(achieved / peak_sus, 4), "traffic": None,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained",
+                     "work_per_launch": "3 x dense GEMM flops of the layer (fwd + 2 bwd) + tree attention 14 dh per pair",
+                     "attention_ms_per_step": round(attn_ms, 4)},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -834,8 +930,9 @@ def main():
     ap.add_argument("--optimizer", nargs="?", const="unfused", default=None, choices=["fused", "unfused"],
                     help="add the AdamW step on the fp32 master lm_head (F3): 'unfused' (default) = bwd (dW to HBM) + "
                          "aurora_adamw_step; 'fused' applies it from the dW GEMM epilogue (measured slower, DESIGN.md)")
-    ap.add_argument("--workload", default="spec_loss", choices=["spec_loss", "tree_attn"],
-                    help="spec_loss: the north-star hot path (default); tree_attn: NEXT F4 draft-layer tree attention")
+    ap.add_argument("--workload", default="spec_loss", choices=["spec_loss", "tree_attn", "draft_layer"],
+                    help="spec_loss: the north-star hot path (default); tree_attn: NEXT F4 tree attention; "
+                         "draft_layer: NEXT F4 whole draft layer (fc + decoder layer) fwd+bwd")
     ap.add_argument("--ta-config", default="ta_tree", choices=sorted(tracegen.TREE_ATTN_CONFIGS),
                     help="F4 workload (--workload tree_attn)")
     args = ap.parse_args()
@@ -845,6 +942,8 @@ def main():
         run_reference(args)
     elif args.workload == "tree_attn":
         run_tree_attn(args)
+    elif args.workload == "draft_layer":
+        run_draft_layer(args)
     else:
         run_ours(args)
 

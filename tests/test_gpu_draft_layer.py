@@ -77,5 +77,7 @@ def test_draft_layer_parity():
     got.update(h3=dh3.cpu().numpy().reshape(Gr["h3"].shape), e=de.cpu().numpy().reshape(Gr["e"].shape),
                Kp=dKp.float().cpu().numpy(), Vp=dVp.float().cpu().numpy())
     errs = {k: _rel(got[k], Gr[k]) for k in Gr}
+    print("draft layer rel. Frobenius errors: H %.2e, " % _rel(H.float().cpu().numpy().reshape(Hr.shape), Hr) +
+          ", ".join(f"{k} {v:.2e}" for k, v in sorted(errs.items())))
     bad = {k: v for k, v in errs.items() if v > 2e-2}
     assert not bad, errs
