@@ -141,3 +141,24 @@ def test_tree_attn_host_validation_without_gpu(L):
     assert b(t, need - 1) == 6                       # workspace too small
     assert b(t, need, dq=None) == 1
     assert b(ta(dh=64), need) == 5
+
+
+def test_draft_layer_host_validation_without_gpu(L):
+    """F4 draft layer: bad configurations and missing buffers return before any CUDA call."""
+    ta = A.aurora_tree_attn_t(R=4, N=5, Hq=32, Hkv=8, dh=128, max_prefix=100, prefix_total=300, prefix_off=16)
+    cfg = A.aurora_draft_layer_t(ta, 4096, 14336, 500000.0, 1e-6)
+    W = A.aurora_draft_weights_t(*([16] * 11))
+    need = L.aurora_draft_layer_workspace_size(C.byref(cfg))
+    assert need > 24 * 4096 * 4
+    f = lambda c, w=W, ws=need, h=16: L.aurora_draft_layer_fwd(C.byref(c), C.byref(w), h, 16, 16, 16, 16, 16, ws, None)
+    assert f(A.aurora_draft_layer_t(ta, 4100, 14336, 5e5, 1e-6)) == 1                                   # d % 8
+    assert f(A.aurora_draft_layer_t(ta, 4096, 14336, 5e5, 0.0)) == 1                                    # eps
+    assert f(A.aurora_draft_layer_t(A.aurora_tree_attn_t(R=4, N=5, Hq=32, Hkv=8, dh=64, prefix_off=16), 4096,
+                                    14336, 5e5, 1e-6)) == 5                                             # dh
+    assert f(cfg, w=A.aurora_draft_weights_t(*([16] * 10 + [None]))) == 1                              # w_post
+    assert f(cfg, h=None) == 1
+    assert f(cfg, ws=need - 1) == 6
+    G = A.aurora_draft_grads_t(*([16] * 11))
+    b = lambda g: L.aurora_draft_layer_bwd(C.byref(cfg), C.byref(W), 16, 16, 16, 16, 16, C.byref(g), 16, 16, 16, 16,
+                                           16, need, None)
+    assert b(A.aurora_draft_grads_t(*([16] * 10 + [None]))) == 1
