@@ -864,19 +864,55 @@ def run_draft_layer(args):
     torch.cuda.synchronize()
     assert int(ta.status.item()) == 0
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    A.aurora_profile_read()
-    A.aurora_profile_enable(True)
+    # one step captured into a CUDA graph (the layer is stream-ordered: cuBLAS + library kernels,
+    # no host syncs); each timed step is one replay, per-phase events re-timed by every replay
+    graph, launch_mode = None, "eager"
+    if not args.eager:
+        try:
+            A.aurora_profile_read()
+            A.aurora_profile_enable(True)
+            n0 = A.aurora_launch_count()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            per_step = A.aurora_launch_count() - n0
+            A.aurora_profile_enable(False)
+            graph.replay()
+            torch.cuda.synchronize()
+            launch_mode = "cuda_graph (one step captured once; each timed step is one replay)"
+        except Exception as ex:
+            A.aurora_profile_enable(False)
+            A.aurora_profile_read()
+            graph, launch_mode = None, f"eager (graph capture failed: {type(ex).__name__})"
+    if graph is None:
+        A.aurora_profile_read()
+        A.aurora_profile_enable(True)
     n0 = A.aurora_launch_count()
+    acc = {}
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             evs[i][0].record(stream)
-            step()
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
             evs[i][1].record(stream)
+            if graph is not None:
+                torch.cuda.synchronize()
+                for k, (t, n) in A.aurora_profile_read(peek=True).items():
+                    a_ = acc.setdefault(k, [0.0, 0])
+                    a_[0] += t
+                    a_[1] += n
         torch.cuda.synchronize()
-    n_launch = A.aurora_launch_count() - n0
-    A.aurora_profile_enable(False)
-    phases = A.aurora_profile_read()
+    if graph is None:
+        n_launch = A.aurora_launch_count() - n0
+        A.aurora_profile_enable(False)
+        phases = A.aurora_profile_read()
+    else:
+        n_launch = per_step * args.steps
+        phases = {k: (v[0], v[1]) for k, v in acc.items()}
+        A.aurora_profile_read()
     ms_step = sum(a.elapsed_time(b) for a, b in evs) / args.steps
     w = _ta_work(meta)
     gemm_fwd = 2.0 * M * (3 * d * d + 2 * d * (qd + 2 * kd) + qd * d + 3 * d * I)
@@ -891,7 +927,7 @@ def run_draft_layer(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded device generator; tracegen structure)",
         "config": {"workload": c.name + "+draft_layer", "R": c.R, "N": c.N, "d": d, "I": I, "Hq": c.Hq, "Hkv": c.Hkv,
                    "dh": c.dh, "prefix_tokens": P, "gemm": "cuBLAS bf16 (library GEMMs)",
-                   "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": "eager"},
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": launch_mode},
         "gpu_launches": int(n_launch),
         "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
         "roofline": {"bound": "tensor", "kernel": "draft_layer_step", "achieved": round(achieved, 1),
