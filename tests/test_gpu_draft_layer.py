@@ -17,13 +17,18 @@ def _bf_round(x):
     return TA.bf16_bits_to_f64(tracegen.f32_to_bf16_bits(np.asarray(x, np.float32)))
 
 
-def _case(seed=7):
+def _case(seed=7, chain=False):
+    """tree: 3 requests (a beam tree, a chain written as a tree, a ragged tree), one empty prefix;
+    chain=True: parents NULL (chain), GQA group 4, one request with no valid node."""
     rng = np.random.default_rng(seed)
     R, N, d, I, Hq, Hkv, dh = 3, 8, 256, 384, 4, 2, 128
     parents = np.array([[-1, -1, 0, 0, 1, 2, 3, 4], [-1, 0, 1, 2, 3, 4, 5, 6], [-1, -1, -1, 0, 1, 2, 3, 3]],
                        dtype=np.int32)
     num_nodes = np.array([8, 8, 6], dtype=np.int32)
     lens = np.array([40, 0, 75])
+    if chain:
+        R, N, Hq, Hkv = 4, 5, 8, 2
+        parents, num_nodes, lens = None, np.array([5, 0, 3, 5], dtype=np.int32), np.array([10, 130, 0, 64])
     off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     sc = lambda fan: 1.0 / np.sqrt(fan)
     n = lambda *s, k=1.0: rng.standard_normal(s) * k
@@ -45,9 +50,8 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def test_draft_layer_parity():
+def _run_layer(P, X, cfg, dH, reps=1):
     from paper_2602_06932_b200 import aurora as A
-    P, X, cfg, dH = _case()
     dev = "cuda"
     bf = lambda x: torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16).to(dev).contiguous()
     f32 = lambda x: torch.tensor(np.asarray(x, np.float32)).to(dev).contiguous()
@@ -55,21 +59,33 @@ def test_draft_layer_parity():
     R, N, d, I = cfg["R"], cfg["N"], cfg["d"], cfg["I"]
     M = R * (N + 1)
     poff = torch.tensor(X["prefix_off"], dtype=torch.int32, device=dev)
+    par = None if X["parents"] is None else torch.tensor(X["parents"], device=dev)
     ta = A.TreeAttention(R, N, cfg["Hq"], cfg["Hkv"], cfg["dh"], poff, int(np.diff(X["prefix_off"]).max()),
-                         parents=torch.tensor(X["parents"], device=dev), num_nodes=torch.tensor(X["num_nodes"], device=dev))
+                         parents=par, num_nodes=torch.tensor(X["num_nodes"], device=dev))
     layer = A.DraftLayer(ta, d, I, W, theta=cfg["theta"], eps=cfg["eps"])
     h3, e = bf(X["h3"].reshape(M, 3 * d)), bf(X["e"].reshape(M, d))
     Kp, Vp = bf(X["Kp"]), bf(X["Vp"])
-    H = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
-    layer.forward(h3, e, Kp, Vp, H)
-    G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in W.items()}
-    dh3 = torch.empty(M, 3 * d, dtype=torch.float32, device=dev)
-    de = torch.empty(M, d, dtype=torch.float32, device=dev)
-    dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
-    layer.backward(h3, e, Kp, Vp, f32(dH.reshape(M, d)), G, dh3, de, dKp, dVp)
-    torch.cuda.synchronize()
-    assert int(ta.status.item()) == 0
+    outs = []
+    for _ in range(reps):
+        H = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+        layer.forward(h3, e, Kp, Vp, H)
+        G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in W.items()}
+        dh3 = torch.empty(M, 3 * d, dtype=torch.float32, device=dev)
+        de = torch.empty(M, d, dtype=torch.float32, device=dev)
+        dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
+        layer.backward(h3, e, Kp, Vp, f32(dH.reshape(M, d)), G, dh3, de, dKp, dVp)
+        torch.cuda.synchronize()
+        assert int(ta.status.item()) == 0
+        outs.append(dict(H=H, dh3=dh3, de=de, dKp=dKp, dVp=dVp, **{"G" + k: v for k, v in G.items()}))
+    return outs
 
+
+@pytest.mark.parametrize("chain", [False, True], ids=["tree", "chain_ragged"])
+def test_draft_layer_parity(chain):
+    P, X, cfg, dH = _case(chain=chain)
+    o = _run_layer(P, X, cfg, dH)[0]
+    H, dh3, de, dKp, dVp = o["H"], o["dh3"], o["de"], o["dKp"], o["dVp"]
+    G = {k: o["G" + k] for k in P}
     Hr, S = DL.layer_fwd(P, X, cfg)
     Gr = DL.layer_bwd(P, X, cfg, S, dH)
     assert _rel(H.float().cpu().numpy().reshape(Hr.shape), Hr) <= 1e-2
@@ -81,3 +97,10 @@ def test_draft_layer_parity():
           ", ".join(f"{k} {v:.2e}" for k, v in sorted(errs.items())))
     bad = {k: v for k, v in errs.items() if v > 2e-2}
     assert not bad, errs
+
+
+def test_draft_layer_deterministic():
+    P, X, cfg, dH = _case(seed=11)
+    a, b = _run_layer(P, X, cfg, dH, reps=2)
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
