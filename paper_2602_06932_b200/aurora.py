@@ -525,3 +525,24 @@ class DraftLayer:
         _check("aurora_draft_layer_bwd", lib().aurora_draft_layer_bwd(
             C.byref(self.cfg), C.byref(self.w), _ptr(h3), _ptr(e), _ptr(Kp), _ptr(Vp), _ptr(dH), C.byref(g),
             _ptr(dh3), _ptr(de), _ptr(dKp), _ptr(dVp), _ptr(self.ws), self.ws.numel(), _stream(stream)))
+
+
+class SpeculatorStep:
+    """One whole speculator training step (marshalling only; every stage is a library call on
+    the current stream): greedy verification + labels (A2-A4) -> draft layer forward (F4) -> H
+    -> lm_head forward / backward with the Eq. 3 loss (A5-A9) -> dH -> draft layer backward (F4).
+    `spec` (SpecTrainStep) and `layer` (DraftLayer) must describe the same batch (R, N, tree)."""
+
+    def __init__(self, spec: "SpecTrainStep", layer: "DraftLayer"):
+        if spec.R != layer.ta.R or spec.N != layer.ta.N or spec.d != layer.cfg.d:
+            raise ValueError("SpeculatorStep: spec and layer shapes differ")
+        self.spec, self.layer = spec, layer
+
+    def step(self, draft_tokens, T, h3, e, Kp, Vp, W_lm, H, dH, dW_lm, G, dh3, de, dKp, dVp, parents=None,
+             num_nodes=None, stream=None):
+        self.spec.verify(draft_tokens, T, parents, num_nodes, stream)
+        self.layer.forward(h3, e, Kp, Vp, H, stream)
+        self.spec.forward(H, W_lm, stream)
+        self.spec.backward(H, W_lm, dH, dW_lm, stream=stream)
+        self.layer.backward(h3, e, Kp, Vp, dH, G, dh3, de, dKp, dVp, stream)
+        return self.spec.loss

@@ -104,3 +104,74 @@ def test_draft_layer_deterministic():
     a, b = _run_layer(P, X, cfg, dH, reps=2)
     for k in a:
         assert torch.equal(a[k], b[k]), k
+
+
+def test_whole_speculator_step_parity():
+    """Verification + draft layer + lm_head loss fwd/bwd + draft layer bwd in one step
+    (SpeculatorStep) against the oracle chain (draft-layer oracle -> H in f64 -> the lm_head /
+    Eq. 3 oracle -> dH -> draft-layer oracle bwd) on the small tree trace."""
+    import oracle
+    from paper_2602_06932_b200 import aurora as A
+    tr = tracegen.gen_trace("small_tree")
+    c = tr["cfg"]
+    R, N, d, V = c.R, c.N, c.d, c.V
+    M = R * (N + 1)
+    rng = np.random.default_rng(21)
+    I, Hq, Hkv, dh = 256, 2, 1, 128
+    lens = rng.integers(0, 80, size=R)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    sc = lambda fan: 1.0 / np.sqrt(fan)
+    n = lambda *s, k=1.0: rng.standard_normal(s) * k
+    P = dict(Wfc=_bf_round(n(d, 3 * d, k=sc(3 * d))), we=np.ones(d), wh=np.ones(d),
+             Wq=_bf_round(n(Hq * dh, 2 * d, k=sc(2 * d))), Wk=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))),
+             Wv=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))), Wo=_bf_round(n(d, Hq * dh, k=sc(Hq * dh))),
+             wpost=np.ones(d), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
+             Wd=_bf_round(n(d, I, k=sc(I))))
+    X = dict(h3=_bf_round(n(R, N + 1, 3 * d)), e=_bf_round(n(R, N + 1, d)), Kp=_bf_round(n(int(lens.sum()), Hkv, dh)),
+             Vp=_bf_round(n(int(lens.sum()), Hkv, dh)), prefix_off=off, parents=tr["parents"], num_nodes=tr["num_nodes"])
+    cfg = dict(Hq=Hq, Hkv=Hkv, dh=dh, theta=1000000.0, eps=1e-6)
+    # ---- oracle chain
+    Hr, S = DL.layer_fwd(P, X, cfg)
+    T64 = oracle.bf16_bits_to_f64(tr["T_bits"])
+    amax, topk, _ = oracle.target_scan(T64, 10)
+    lab = oracle.verify(tr["draft_tokens"], tr["parents"], tr["num_nodes"], amax, 0)
+    tg = oracle.row_targets(lab["row_class"], lambda m: T64[m], topk, 1, 10, 1.0, 0)
+    fw = oracle.loss_fwd(Hr.reshape(M, d), tr["W_bits"], tg)
+    bw = oracle.loss_bwd(Hr.reshape(M, d), tr["W_bits"], tg, fw["lse"])
+    Gr = DL.layer_bwd(P, X, cfg, S, bw["dH"].reshape(R, N + 1, d))
+    # ---- GPU step
+    dev = "cuda"
+    bf = lambda x: torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16).to(dev).contiguous()
+    f32 = lambda x: torch.tensor(np.asarray(x, np.float32)).to(dev).contiguous()
+    bits = lambda b: torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).view(torch.bfloat16).to(dev)
+    W = {k: (f32(v) if k in ("we", "wh", "wpost") else bf(v)) for k, v in P.items()}
+    par = torch.from_numpy(tr["parents"]).to(dev)
+    ta = A.TreeAttention(R, N, Hq, Hkv, dh, torch.tensor(off, dtype=torch.int32, device=dev), int(lens.max()),
+                         parents=par)
+    layer = A.DraftLayer(ta, d, I, W, theta=cfg["theta"], eps=cfg["eps"])
+    spec = A.SpecTrainStep(R, N, d, V)
+    step = A.SpeculatorStep(spec, layer)
+    h3, e, Kp, Vp = bf(X["h3"].reshape(M, 3 * d)), bf(X["e"].reshape(M, d)), bf(X["Kp"]), bf(X["Vp"])
+    W_lm = bits(tr["W_bits"])
+    H = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    dH = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dW_lm = torch.empty(V, d, dtype=torch.float32, device=dev)
+    G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in W.items()}
+    dh3 = torch.empty(M, 3 * d, dtype=torch.float32, device=dev)
+    de = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
+    loss = step.step(torch.from_numpy(tr["draft_tokens"]).to(dev), bits(tr["T_bits"]), h3, e, Kp, Vp, W_lm, H, dH,
+                     dW_lm, G, dh3, de, dKp, dVp, parents=par)
+    torch.cuda.synchronize()
+    assert int(spec.status.item()) == 0 and int(ta.status.item()) == 0
+    assert np.array_equal(spec.accept_len.cpu().numpy(), lab["accept_len"])
+    assert abs(float(loss.item()) - fw["loss"]) <= 5e-3 * abs(fw["loss"])
+    assert _rel(dW_lm.cpu().numpy(), bw["dW"]) <= 2e-2
+    assert _rel(dH.cpu().numpy(), bw["dH"]) <= 2e-2
+    got = {k: G[k].cpu().numpy() for k in G}
+    got.update(h3=dh3.cpu().numpy().reshape(Gr["h3"].shape), e=de.cpu().numpy().reshape(Gr["e"].shape),
+               Kp=dKp.float().cpu().numpy(), Vp=dVp.float().cpu().numpy())
+    errs = {k: _rel(got[k], Gr[k]) for k in Gr}
+    print("whole step: loss %.6f (oracle %.6f); " % (float(loss.item()), fw["loss"]) +
+          ", ".join(f"{k} {v:.2e}" for k, v in sorted(errs.items())))
+    assert not {k: v for k, v in errs.items() if v > 2e-2}, errs
