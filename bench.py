@@ -940,6 +940,116 @@ def run_draft_layer(args):
     print(json.dumps(out), flush=True)
 
 
+def run_full_step(args):
+    """Whole speculator training step on one GPU: greedy verification + labels -> F4 draft layer
+    (fc + decoder layer with tree RoPE + tree attention) -> H -> lm_head fwd/bwd with the Eq. 3
+    loss -> dH -> draft layer bwd (SpeculatorStep).  Trace (T, draft tokens, tree) from tracegen's
+    `--config` workload; cached prefixes from the matching F4 workload (ta_llama for llama, ta_tree
+    otherwise); layer weights / inputs from a seeded device generator."""
+    import torch
+    from paper_2602_06932_b200 import aurora as A
+    from paper_2602_06932_b200.build import build
+
+    ws, rank, local = _dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    build()
+    A.lib()
+    cfg = tracegen.CONFIGS[args.config]
+    tr = tracegen.gen_trace(cfg)
+    R, N, d, V, M = cfg.R, cfg.N, cfg.d, cfg.V, cfg.M
+    meta = tracegen.gen_tree_attn_meta("ta_llama" if args.config == "llama" else "ta_tree")
+    ca = meta["cfg"]
+    off = meta["prefix_off"][:R + 1]
+    P = int(off[-1])
+    I = 14336 if args.config == "llama" else 12288
+    g = torch.Generator(device=dev)
+    g.manual_seed(cfg.seed + 23)
+    rnd = lambda *s, k=1.0: (torch.randn(*s, generator=g, device=dev) * k).to(torch.bfloat16)
+    qd, kd = ca.Hq * ca.dh, ca.Hkv * ca.dh
+    W = dict(Wfc=rnd(d, 3 * d, k=(3 * d) ** -0.5), Wq=rnd(qd, 2 * d, k=(2 * d) ** -0.5),
+             Wk=rnd(kd, 2 * d, k=(2 * d) ** -0.5), Wv=rnd(kd, 2 * d, k=(2 * d) ** -0.5), Wo=rnd(d, qd, k=qd ** -0.5),
+             Wg=rnd(I, d, k=d ** -0.5), Wu=rnd(I, d, k=d ** -0.5), Wd=rnd(d, I, k=I ** -0.5),
+             we=torch.ones(d, device=dev), wh=torch.ones(d, device=dev), wpost=torch.ones(d, device=dev))
+    h3, e = rnd(M, 3 * d), rnd(M, d)
+    Kp, Vp = rnd(P, ca.Hkv, ca.dh), rnd(P, ca.Hkv, ca.dh)
+    T = _bf16(tr["T_bits"], torch, dev)
+    W_lm = _bf16(tr["W_bits"], torch, dev)
+    draft = torch.from_numpy(tr["draft_tokens"]).to(dev)
+    par = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).to(dev)
+    nn = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).to(dev)
+    ta = A.TreeAttention(R, N, ca.Hq, ca.Hkv, ca.dh, torch.from_numpy(off.astype(np.int32)).to(dev),
+                         int(np.diff(off).max()), parents=par, num_nodes=nn)
+    layer = A.DraftLayer(ta, d, I, W, theta=500000.0 if args.config == "llama" else 1000000.0, eps=1e-6)
+    spec = A.SpecTrainStep(R, N, d, V, device=dev)
+    st = A.SpeculatorStep(spec, layer)
+    H = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    dH = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dW_lm = torch.empty(V, d, dtype=torch.float32, device=dev)
+    G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in W.items()}
+    dh3 = torch.empty(M, 3 * d, dtype=torch.float32, device=dev)
+    de = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        st.step(draft, T, h3, e, Kp, Vp, W_lm, H, dH, dW_lm, G, dh3, de, dKp, dVp, parents=par, num_nodes=nn)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert int(spec.status.item()) == 0 and int(ta.status.item()) == 0
+    graph, launch_mode = None, "eager"
+    per_step = None
+    if not args.eager:
+        try:
+            c0 = A.aurora_launch_count()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                step()
+            per_step = A.aurora_launch_count() - c0
+            graph.replay()
+            torch.cuda.synchronize()
+            launch_mode = "cuda_graph (one step captured once; each timed step is one replay)"
+        except Exception as ex:
+            graph, launch_mode = None, f"eager (graph capture failed: {type(ex).__name__})"
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    n0 = A.aurora_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            graph.replay() if graph is not None else step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    ms_step = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    w = _ta_work(dict(meta, cfg=dataclasses.replace(ca, R=R), prefix_off=off, parents=tr["parents"],
+                      num_nodes=tr["num_nodes"]))
+    gemm_fwd = 2.0 * M * (3 * d * d + 2 * d * (qd + 2 * kd) + qd * d + 3 * d * I)
+    flops = 3.0 * gemm_fwd + w["fwd_flops"] + w["bwd_flops"] + 8.0 * M * V * d   # + lm_head: 4 GEMMs executed
+    _, peak_sus, _, peak_src = _peaks()
+    achieved = flops / (ms_step / 1e3) / 1e12
+    out = {
+        "metric": "whole speculator training step tokens/s (verify + F4 draft layer + lm_head Eq.3 fwd/bwd)",
+        "value": round(M / (ms_step / 1e3), 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (tracegen trace + seeded device generator)",
+        "config": {"workload": cfg.name + "+draft_layer", "R": R, "N": N, "d": d, "V": V, "I": I, "Hq": ca.Hq,
+                   "Hkv": ca.Hkv, "prefix_tokens": P, "tree": cfg.tree,
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": launch_mode},
+        "gpu_launches": int(per_step * args.steps if graph is not None else A.aurora_launch_count() - n0),
+        "roofline": {"bound": "tensor", "kernel": "speculator_step", "achieved": round(achieved, 1), "peak": peak_sus,
+                     "unit": "TFLOP/s", "frac": round(achieved / peak_sus, 4), "traffic": None,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained",
+                     "work_per_launch": "executed GEMM flops: 3 x draft-layer dense fwd + 8 M V d lm_head + tree attention"},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -966,9 +1076,10 @@ def main():
     ap.add_argument("--optimizer", nargs="?", const="unfused", default=None, choices=["fused", "unfused"],
                     help="add the AdamW step on the fp32 master lm_head (F3): 'unfused' (default) = bwd (dW to HBM) + "
                          "aurora_adamw_step; 'fused' applies it from the dW GEMM epilogue (measured slower, DESIGN.md)")
-    ap.add_argument("--workload", default="spec_loss", choices=["spec_loss", "tree_attn", "draft_layer"],
+    ap.add_argument("--workload", default="spec_loss", choices=["spec_loss", "tree_attn", "draft_layer", "full_step"],
                     help="spec_loss: the north-star hot path (default); tree_attn: NEXT F4 tree attention; "
-                         "draft_layer: NEXT F4 whole draft layer (fc + decoder layer) fwd+bwd")
+                         "draft_layer: NEXT F4 whole draft layer (fc + decoder layer) fwd+bwd; full_step: verify + "
+                         "draft layer + lm_head loss fwd/bwd (SpeculatorStep) on --config")
     ap.add_argument("--ta-config", default="ta_tree", choices=sorted(tracegen.TREE_ATTN_CONFIGS),
                     help="F4 workload (--workload tree_attn)")
     args = ap.parse_args()
@@ -980,6 +1091,8 @@ def main():
         run_tree_attn(args)
     elif args.workload == "draft_layer":
         run_draft_layer(args)
+    elif args.workload == "full_step":
+        run_full_step(args)
     else:
         run_ours(args)
 
