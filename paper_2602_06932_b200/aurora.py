@@ -11,6 +11,8 @@ import ctypes as C
 import os
 from typing import Optional
 
+import numpy as np
+
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AURORA_LIB") or os.path.join(_PKG, "libaurora.so")  # override: A/B experiments
 
@@ -546,3 +548,45 @@ class SpeculatorStep:
         self.spec.backward(H, W_lm, dH, dW_lm, stream=stream)
         self.layer.backward(h3, e, Kp, Vp, dH, G, dh3, de, dKp, dVp, stream)
         return self.spec.loss
+
+
+class SpeculatorParams:
+    """Every trainable speculator parameter (the F4 draft layer's and the lm_head W) in three flat
+    device buffers — fp32 master, the bf16 copy the GEMMs read, fp32 gradients — so that ONE
+    aurora_adamw_step (F3) updates all of them under one global gradient norm (clip 0.5
+    over the model).  `W` / `G` are views into the buffers (the norm weights' views are fp32 slices
+    of the master: the kernels read them directly); `W_lm` / `dW_lm` are the lm_head's."""
+
+    NORMS = ("we", "wh", "wpost")
+
+    def __init__(self, d: int, I: int, Hq: int, Hkv: int, dh: int, V: int, device):
+        import torch
+        qd, kd = Hq * dh, Hkv * dh
+        self.shapes = [("W_lm", (V, d)), ("Wfc", (d, 3 * d)), ("Wq", (qd, 2 * d)), ("Wk", (kd, 2 * d)),
+                       ("Wv", (kd, 2 * d)), ("Wo", (d, qd)), ("Wg", (I, d)), ("Wu", (I, d)), ("Wd", (d, I)),
+                       ("we", (d,)), ("wh", (d,)), ("wpost", (d,))]
+        sizes = [int(np.prod(s)) for _, s in self.shapes]
+        total = int(sum(sizes))
+        self.master = torch.zeros(total, dtype=torch.float32, device=device)
+        self.bf = torch.zeros(total, dtype=torch.bfloat16, device=device)
+        self.grad = torch.zeros(total, dtype=torch.float32, device=device)
+        self.W, self.G, self.M, o = {}, {}, {}, 0
+        for (name, shape), n in zip(self.shapes, sizes):
+            self.M[name] = self.master[o:o + n].view(shape)
+            self.W[name] = self.M[name] if name in self.NORMS else self.bf[o:o + n].view(shape)
+            self.G[name] = self.grad[o:o + n].view(shape)
+            o += n
+        self.W_lm, self.dW_lm = self.W.pop("W_lm"), self.G.pop("W_lm")
+
+    def load(self, values: dict):
+        """Set the fp32 master from host / device arrays by name and refresh the bf16 copy."""
+        import torch
+        for name, v in values.items():
+            self.M[name].copy_(torch.as_tensor(np.asarray(v, np.float32)))
+        self.bf.copy_(self.master.to(torch.bfloat16))
+
+    def adamw(self, **kw) -> "AdamW":
+        return AdamW(self.master, **kw)
+
+    def optimizer_step(self, opt: "AdamW", stream=None):
+        opt.step(self.grad, W_bf16=self.bf, stream=stream)

@@ -175,3 +175,76 @@ def test_whole_speculator_step_parity():
     print("whole step: loss %.6f (oracle %.6f); " % (float(loss.item()), fw["loss"]) +
           ", ".join(f"{k} {v:.2e}" for k, v in sorted(errs.items())))
     assert not {k: v for k, v in errs.items() if v > 2e-2}, errs
+
+
+def test_whole_step_with_adamw_over_all_params():
+    """F3 over the whole speculator: lm_head + draft-layer parameters in one flat master
+    (SpeculatorParams), one AdamW step with one global norm after SpeculatorStep.  Against the
+    oracle chain's gradients -> oracle.adamw_step: the global norm within 1e-2, and the first-step
+    update (= lr * sign(g) up to eps) agrees on >= 99 % of the elements outside the smallest
+    decile of |g| (tiny gradients may flip sign under bf16 rounding)."""
+    import oracle
+    from paper_2602_06932_b200 import aurora as A
+    tr = tracegen.gen_trace("small_tree")
+    c = tr["cfg"]
+    R, N, d, V = c.R, c.N, c.d, c.V
+    M = R * (N + 1)
+    rng = np.random.default_rng(31)
+    I, Hq, Hkv, dh = 256, 2, 1, 128
+    lens = rng.integers(0, 80, size=R)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    sc = lambda fan: 1.0 / np.sqrt(fan)
+    n = lambda *s, k=1.0: rng.standard_normal(s) * k
+    P = dict(Wfc=_bf_round(n(d, 3 * d, k=sc(3 * d))), we=np.ones(d), wh=np.ones(d),
+             Wq=_bf_round(n(Hq * dh, 2 * d, k=sc(2 * d))), Wk=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))),
+             Wv=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))), Wo=_bf_round(n(d, Hq * dh, k=sc(Hq * dh))),
+             wpost=np.ones(d), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
+             Wd=_bf_round(n(d, I, k=sc(I))))
+    X = dict(h3=_bf_round(n(R, N + 1, 3 * d)), e=_bf_round(n(R, N + 1, d)), Kp=_bf_round(n(int(lens.sum()), Hkv, dh)),
+             Vp=_bf_round(n(int(lens.sum()), Hkv, dh)), prefix_off=off, parents=tr["parents"], num_nodes=tr["num_nodes"])
+    cfg = dict(Hq=Hq, Hkv=Hkv, dh=dh, theta=1000000.0, eps=1e-6)
+    W_lm64 = TA.bf16_bits_to_f64(tr["W_bits"])
+    # ---- oracle chain + oracle AdamW over the flat parameter vector (same order as SpeculatorParams)
+    Hr, S = DL.layer_fwd(P, X, cfg)
+    T64 = oracle.bf16_bits_to_f64(tr["T_bits"])
+    amax, topk, _ = oracle.target_scan(T64, 10)
+    lab = oracle.verify(tr["draft_tokens"], tr["parents"], tr["num_nodes"], amax, 0)
+    tg = oracle.row_targets(lab["row_class"], lambda m: T64[m], topk, 1, 10, 1.0, 0)
+    fw = oracle.loss_fwd(Hr.reshape(M, d), tr["W_bits"], tg)
+    bw = oracle.loss_bwd(Hr.reshape(M, d), tr["W_bits"], tg, fw["lse"])
+    Gr = DL.layer_bwd(P, X, cfg, S, bw["dH"].reshape(R, N + 1, d))
+    order = ["Wfc", "Wq", "Wk", "Wv", "Wo", "Wg", "Wu", "Wd", "we", "wh", "wpost"]
+    w0 = np.concatenate([W_lm64.ravel()] + [np.asarray(P[k], np.float32).astype(np.float64).ravel() for k in order])
+    g64 = np.concatenate([bw["dW"].ravel()] + [Gr[k].ravel() for k in order])
+    lr = 1e-3
+    w1, _, _, norm = oracle.adamw_step(w0, np.zeros_like(w0), np.zeros_like(w0), g64, 1, lr, warmup_steps=0)
+    # ---- GPU: flat parameters, whole step, one AdamW step
+    dev = "cuda"
+    sp = A.SpeculatorParams(d, I, Hq, Hkv, dh, V, dev)
+    sp.load(dict(W_lm=W_lm64, **{k: P[k] for k in order}))
+    par = torch.from_numpy(tr["parents"]).to(dev)
+    ta = A.TreeAttention(R, N, Hq, Hkv, dh, torch.tensor(off, dtype=torch.int32, device=dev), int(lens.max()),
+                         parents=par)
+    layer = A.DraftLayer(ta, d, I, sp.W, theta=cfg["theta"], eps=cfg["eps"])
+    step = A.SpeculatorStep(A.SpecTrainStep(R, N, d, V), layer)
+    bf = lambda x: torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16).to(dev).contiguous()
+    bits = lambda b: torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).view(torch.bfloat16).to(dev)
+    h3, e, Kp, Vp = bf(X["h3"].reshape(M, 3 * d)), bf(X["e"].reshape(M, d)), bf(X["Kp"]), bf(X["Vp"])
+    H = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    dH = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dh3 = torch.empty(M, 3 * d, dtype=torch.float32, device=dev)
+    de = torch.empty(M, d, dtype=torch.float32, device=dev)
+    dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
+    step.step(torch.from_numpy(tr["draft_tokens"]).to(dev), bits(tr["T_bits"]), h3, e, Kp, Vp, sp.W_lm, H, dH,
+              sp.dW_lm, sp.G, dh3, de, dKp, dVp, parents=par)
+    opt = sp.adamw(lr=lr, warmup_steps=0)
+    sp.optimizer_step(opt)
+    torch.cuda.synchronize()
+    assert abs(float(opt.grad_norm.item()) - norm) <= 1e-2 * norm
+    dw_gpu = sp.master.cpu().numpy().astype(np.float64) - w0.astype(np.float32).astype(np.float64)
+    dw_ref = w1 - w0
+    big = np.abs(g64) > np.quantile(np.abs(g64), 0.1)
+    agree = np.mean(np.sign(dw_gpu[big]) == np.sign(dw_ref[big]))
+    assert agree >= 0.99, agree
+    # the bf16 copy the GEMMs read was refreshed from the updated master
+    np.testing.assert_allclose(sp.bf.float().cpu().numpy(), sp.master.cpu().numpy(), rtol=2 ** -8, atol=1e-30)
