@@ -969,14 +969,21 @@ def run_full_step(args):
     g.manual_seed(cfg.seed + 23)
     rnd = lambda *s, k=1.0: (torch.randn(*s, generator=g, device=dev) * k).to(torch.bfloat16)
     qd, kd = ca.Hq * ca.dh, ca.Hkv * ca.dh
-    W = dict(Wfc=rnd(d, 3 * d, k=(3 * d) ** -0.5), Wq=rnd(qd, 2 * d, k=(2 * d) ** -0.5),
-             Wk=rnd(kd, 2 * d, k=(2 * d) ** -0.5), Wv=rnd(kd, 2 * d, k=(2 * d) ** -0.5), Wo=rnd(d, qd, k=qd ** -0.5),
-             Wg=rnd(I, d, k=d ** -0.5), Wu=rnd(I, d, k=d ** -0.5), Wd=rnd(d, I, k=I ** -0.5),
-             we=torch.ones(d, device=dev), wh=torch.ones(d, device=dev), wpost=torch.ones(d, device=dev))
+    # every trainable parameter in flat buffers (SpeculatorParams): --optimizer adds ONE AdamW step
+    # over lm_head + draft layer per training step (F3 over the whole speculator)
+    sp = A.SpeculatorParams(d, I, ca.Hq, ca.Hkv, ca.dh, V, dev)
+    fan = dict(Wfc=3 * d, Wq=2 * d, Wk=2 * d, Wv=2 * d, Wo=qd, Wg=d, Wu=d, Wd=I)
+    for k_, f_ in fan.items():
+        sp.M[k_].copy_(torch.randn(sp.M[k_].shape, generator=g, device=dev) * f_ ** -0.5)
+    for k_ in ("we", "wh", "wpost"):
+        sp.M[k_].fill_(1.0)
+    sp.M["W_lm"].copy_(_bf16(tr["W_bits"], torch, dev).float())
+    sp.bf.copy_(sp.master.to(torch.bfloat16))
+    W, W_lm = sp.W, sp.W_lm
+    opt = sp.adamw(lr=1e-5, warmup_steps=400) if args.optimizer else None
     h3, e = rnd(M, 3 * d), rnd(M, d)
     Kp, Vp = rnd(P, ca.Hkv, ca.dh), rnd(P, ca.Hkv, ca.dh)
     T = _bf16(tr["T_bits"], torch, dev)
-    W_lm = _bf16(tr["W_bits"], torch, dev)
     draft = torch.from_numpy(tr["draft_tokens"]).to(dev)
     par = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).to(dev)
     nn = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).to(dev)
@@ -987,8 +994,7 @@ def run_full_step(args):
     st = A.SpeculatorStep(spec, layer)
     H = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
     dH = torch.empty(M, d, dtype=torch.float32, device=dev)
-    dW_lm = torch.empty(V, d, dtype=torch.float32, device=dev)
-    G = {k: torch.empty(v.shape, dtype=torch.float32, device=dev) for k, v in W.items()}
+    dW_lm, G = sp.dW_lm, sp.G
     dh3 = torch.empty(M, 3 * d, dtype=torch.float32, device=dev)
     de = torch.empty(M, d, dtype=torch.float32, device=dev)
     dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
@@ -997,6 +1003,8 @@ def run_full_step(args):
 
     def step():
         st.step(draft, T, h3, e, Kp, Vp, W_lm, H, dH, dW_lm, G, dh3, de, dKp, dVp, parents=par, num_nodes=nn)
+        if opt is not None:
+            sp.optimizer_step(opt)
 
     for _ in range(args.warmup):
         step()
@@ -1037,7 +1045,8 @@ def run_full_step(args):
         "value": round(M / (ms_step / 1e3), 1), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (tracegen trace + seeded device generator)",
-        "config": {"workload": cfg.name + "+draft_layer", "R": R, "N": N, "d": d, "V": V, "I": I, "Hq": ca.Hq,
+        "config": {"workload": cfg.name + "+draft_layer", "optimizer": "adamw over all params (F3)" if opt else None,
+                   "params": int(sp.master.numel()), "R": R, "N": N, "d": d, "V": V, "I": I, "Hq": ca.Hq,
                    "Hkv": ca.Hkv, "prefix_tokens": P, "tree": cfg.tree,
                    "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": launch_mode},
         "gpu_launches": int(per_step * args.steps if graph is not None else A.aurora_launch_count() - n0),
