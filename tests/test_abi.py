@@ -162,3 +162,28 @@ def test_draft_layer_host_validation_without_gpu(L):
     b = lambda g: L.aurora_draft_layer_bwd(C.byref(cfg), C.byref(W), 16, 16, 16, 16, 16, C.byref(g), 16, 16, 16, 16,
                                            16, need, None)
     assert b(A.aurora_draft_grads_t(*([16] * 10 + [None]))) == 1
+
+
+def test_speculator_params_layout():
+    """SpeculatorParams views tile the flat buffers exactly (no overlap, no gap); the norm weights
+    are fp32 views of the master (the kernels read them), the matrices bf16 views of the copy."""
+    import numpy as np
+    import torch
+    sp = A.SpeculatorParams(d=64, I=96, Hq=2, Hkv=1, dh=128, V=300, device="cpu")
+    names = [n for n, _ in sp.shapes]
+    total = sum(int(np.prod(s)) for _, s in sp.shapes)
+    assert sp.master.numel() == sp.bf.numel() == sp.grad.numel() == total
+    starts = sorted((sp.M[n].data_ptr() - sp.master.data_ptr()) // 4 for n in names)
+    sizes = {(sp.M[n].data_ptr() - sp.master.data_ptr()) // 4: sp.M[n].numel() for n in names}
+    pos = 0
+    for st in starts:
+        assert st == pos
+        pos += sizes[st]
+    assert pos == total
+    for n in ("we", "wh", "wpost"):
+        assert sp.W[n].dtype == torch.float32 and sp.W[n].data_ptr() == sp.M[n].data_ptr()
+    for n in ("Wfc", "Wq", "Wd"):
+        assert sp.W[n].dtype == torch.bfloat16 and sp.W[n].is_contiguous()
+    assert sp.W_lm.shape == (300, 64) and sp.dW_lm.shape == (300, 64) and "W_lm" not in sp.W
+    sp.load({"wh": np.full(64, 2.0), "Wq": np.ones((256, 128))})
+    assert float(sp.W["wh"].sum()) == 128.0 and float(sp.W["Wq"].float().sum()) == 256 * 128
