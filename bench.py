@@ -13,9 +13,13 @@ max-over-ranks time.  `e2e` repeats the measurement through the public API with 
 trace batch (T, H, draft tokens) copied from pinned host memory every step and the
 loss + accept lengths read back.
 
-N > 1 (torchrun): data-parallel over trace batches (weak scaling): each rank owns a
-different seeded batch, the loss normalisation counts and dW are allreduced by the
-library's NCCL communicator (C2, C5).
+Default workload: `qwen3` (BASELINE.json configs[2], the largest configuration that fits
+one GPU; configs[1] `llama` and the others via --config).
+
+N > 1 (torchrun): vocab-parallel lm_head by default (weak scaling: one global batch of
+N x R requests, rank p owns vocab slice p of W and T; C1/C3 per-row exchanges and the C4
+dH allreduce); `--vp A --dp B` (A x B = N) is the 2-D DP x VP layout; `--parallel dp` is
+pure data parallelism (C2 counts + C5 dW allreduce).
 
 --impl reference: the f64 CPU oracle (the reference arm for this tier) timed on the
 host cores on a bounded sample of the same workload; rank 0 only.
@@ -348,7 +352,7 @@ def run_ours(args):
     plain = (not sparse and args.k_accept == 1 and args.k_discard == 10 and args.accept_loss == "fkl"
              and args.optimizer != "fused")
     cfg_dev = dataclasses.replace(cfg, V=V_local)  # the work one GPU does (VP: its vocab slice)
-    roof = _roofline(phases, cfg_dev, args.steps, peak_sus, peak_src, hbm,
+    roof = _roofline(phases, cfg_dev, args.steps, peak_burst, peak_src, hbm,
                      workload=cfg.name if (plain and not vp and ws == 1) else None, optimizer=args.optimizer)
     out = {
         "metric": "speculator-training tokens/s (verify + lm_head fwd/bwd + Eq.3 loss), % bf16 tensor peak",
@@ -381,7 +385,10 @@ def run_ours(args):
         "e2e": e2e,
         "clocks": clk.summary(),
     }
-    out["tensor_frac_step"] = round((8.0 * M * V_local * d / (ms_step / 1e3)) / (peak_sus * 1e12), 4)
+    # executed 8MVd (fwd, dz recompute, dW, dH) over the step, against the BURST bf16 peak
+    # (MEASURED_PEAKS.json bf16_tflops); the sustained figure is the power-capped 4 s loop
+    out["tensor_frac_step"] = round((8.0 * M * V_local * d / (ms_step / 1e3)) / (peak_burst * 1e12), 4)
+    out["tensor_frac_step_vs_sustained"] = round((8.0 * M * V_local * d / (ms_step / 1e3)) / (peak_sus * 1e12), 4)
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = _cpu_baseline(cfg, args)
     print(json.dumps(out), flush=True)
@@ -520,7 +527,7 @@ def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0, workload=
     k, _, rec = best
     if rec["bound"] == "tensor":
         out = {"bound": "tensor", "kernel": k, "achieved": rec["achieved_tflops"], "peak": peak, "unit": "TFLOP/s",
-               "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)",
+               "peak_source": f"{peak_src} bf16_tflops (burst, torch.matmul 8192^3 best of 10)",
                "work_per_launch": "2*M*V_chunk*d flops (2 d per row per vocab column, SURVEY 8(d))"}
     else:
         out = {"bound": "hbm", "kernel": k, "achieved": rec["achieved_gbs"], "peak": hbm_peak_gbs, "unit": "GB/s",
@@ -931,8 +938,9 @@ def run_draft_layer(args):
         "gpu_launches": int(n_launch),
         "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
         "roofline": {"bound": "tensor", "kernel": "draft_layer_step", "achieved": round(achieved, 1),
-                     "peak": peak_sus, "unit": "TFLOP/s", "frac": round(achieved / peak_sus, 4), "traffic": None,
-                     "peak_source": f"{peak_src} bf16_tflops_sustained",
+                     "peak": peak_burst, "unit": "TFLOP/s", "frac": round(achieved / peak_burst, 4), "traffic": None,
+                     "peak_source": f"{peak_src} bf16_tflops (burst)",
+                     "frac_vs_sustained": round(achieved / peak_sus, 4),
                      "work_per_launch": "3 x dense GEMM flops of the layer (fwd + 2 bwd) + tree attention 14 dh per pair",
                      "attention_ms_per_step": round(attn_ms, 4)},
         "clocks": clk.summary(),
@@ -1038,7 +1046,7 @@ def run_full_step(args):
                       num_nodes=tr["num_nodes"]))
     gemm_fwd = 2.0 * M * (3 * d * d + 2 * d * (qd + 2 * kd) + qd * d + 3 * d * I)
     flops = 3.0 * gemm_fwd + w["fwd_flops"] + w["bwd_flops"] + 8.0 * M * V * d   # + lm_head: 4 GEMMs executed
-    _, peak_sus, _, peak_src = _peaks()
+    peak_burst, peak_sus, _, peak_src = _peaks()
     achieved = flops / (ms_step / 1e3) / 1e12
     out = {
         "metric": "whole speculator training step tokens/s (verify + F4 draft layer + lm_head Eq.3 fwd/bwd)",
@@ -1050,9 +1058,10 @@ def run_full_step(args):
                    "Hkv": ca.Hkv, "prefix_tokens": P, "tree": cfg.tree,
                    "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": launch_mode},
         "gpu_launches": int(per_step * args.steps if graph is not None else A.aurora_launch_count() - n0),
-        "roofline": {"bound": "tensor", "kernel": "speculator_step", "achieved": round(achieved, 1), "peak": peak_sus,
-                     "unit": "TFLOP/s", "frac": round(achieved / peak_sus, 4), "traffic": None,
-                     "peak_source": f"{peak_src} bf16_tflops_sustained",
+        "roofline": {"bound": "tensor", "kernel": "speculator_step", "achieved": round(achieved, 1), "peak": peak_burst,
+                     "unit": "TFLOP/s", "frac": round(achieved / peak_burst, 4), "traffic": None,
+                     "peak_source": f"{peak_src} bf16_tflops (burst)",
+                     "frac_vs_sustained": round(achieved / peak_sus, 4),
                      "work_per_launch": "executed GEMM flops: 3 x draft-layer dense fwd + 8 M V d lm_head + tree attention"},
         "clocks": clk.summary(),
     }
@@ -1064,7 +1073,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="llama", choices=sorted(tracegen.CONFIGS))
+    ap.add_argument("--config", default="qwen3", choices=sorted(tracegen.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-reqs", type=int, default=8)
     ap.add_argument("--ref-reqs", type=int, default=2)

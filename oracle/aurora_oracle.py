@@ -268,6 +268,38 @@ def loss_bwd(H64: np.ndarray, W, targets: dict, lse: np.ndarray, g: float = 1.0,
     return dict(dH=dH, dW=dW)
 
 
+def loss_bwd_sampled(H64: np.ndarray, W, targets: dict, lse: np.ndarray, dh_rows, dw_ranges, g: float = 1.0):
+    """O5 restricted to what a full-size check can afford: dH at the rows `dh_rows`
+    (dH_m = sum_j dz_mj W_j over the whole vocabulary) and dW at the vocabulary ranges
+    `dw_ranges` (dW_j = sum_m dz_mj H_m over every row), with dz = g w (softmax(z) - p~)
+    as in loss_bwd.  lse: f64 [M] for every row (O4).  Returns
+    dict(dH=[len(dh_rows), d], dW={(v0, v1): [v1 - v0, d]})."""
+    M, d = H64.shape
+    w = np.array([targets["w"][m] for m in range(M)])
+    Wf = lambda v0, v1: bf16_bits_to_f64(W[v0:v1]) if W.dtype == np.uint16 else W[v0:v1]
+
+    def dz_block(rows, v0, v1):
+        z = H64[rows] @ Wf(v0, v1).T
+        dz = np.exp(z - lse[rows][:, None]) * (g * w[rows])[:, None]
+        for i, m in enumerate(rows):
+            S = targets["sup_idx"][int(m)]
+            sel = (S >= v0) & (S < v1)
+            dz[i, S[sel] - v0] -= g * w[m] * targets["sup_p"][int(m)][sel]
+        return dz
+
+    rows = np.asarray(dh_rows, dtype=np.int64)
+    V = W.shape[0]
+    dH = np.zeros((len(rows), d))
+    for v0 in range(0, V, 8192):
+        v1 = min(V, v0 + 8192)
+        dH += dz_block(rows, v0, v1) @ Wf(v0, v1)
+    dW = {}
+    allrows = np.arange(M)
+    for v0, v1 in dw_ranges:
+        dW[(v0, v1)] = dz_block(allrows, v0, v1).T @ H64
+    return dict(dH=dH, dW=dW)
+
+
 def dlogits_rows(H64, W, targets, lse_rows, rows, g: float = 1.0):
     """Full dZ rows for a handful of rows (test hook counterpart)."""
     Wf = bf16_bits_to_f64(W) if W.dtype == np.uint16 else W

@@ -643,3 +643,27 @@ def test_adamw_matches_torch_optim(wd, max_norm, scale):
         st = opt.state[Wt]
         np.testing.assert_allclose(m, st["exp_avg"].numpy(), rtol=1e-12, atol=1e-18)
         np.testing.assert_allclose(v, st["exp_avg_sq"].numpy(), rtol=1e-12, atol=1e-20)
+
+
+def test_loss_bwd_sampled_matches_torch_autograd():
+    """O5 restricted to sampled dH rows and dW vocabulary ranges (the full-size GPU check's
+    oracle) against torch f64 autograd of sum_m w_m F.kl_div(log_softmax(z_m), p~_m)."""
+    tr = tracegen.gen_trace("small_tree")
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    lab, tg, fw, bw, T = _oracle_all(tr, W64, H64)
+    M, V = T.shape
+    P = torch.zeros(M, V, dtype=torch.float64)
+    wv = torch.zeros(M, dtype=torch.float64)
+    for m in range(M):
+        P[m, torch.from_numpy(tg["sup_idx"][m])] = torch.from_numpy(tg["sup_p"][m])
+        wv[m] = tg["w"][m]
+    Ht = torch.from_numpy(H64).requires_grad_(True)
+    Wt = torch.from_numpy(W64).requires_grad_(True)
+    (wv * F.kl_div(F.log_softmax(Ht @ Wt.T, 1), P, reduction="none").sum(1)).sum().backward()
+    rows = np.array([0, 5, 17, M - 1])
+    ranges = [(0, 100), (1500, 2100), (V - 37, V)]
+    s = oracle.loss_bwd_sampled(H64, tr["W_bits"], tg, fw["lse"], rows, ranges)
+    np.testing.assert_allclose(s["dH"], Ht.grad.numpy()[rows], rtol=1e-9, atol=1e-14)
+    for v0, v1 in ranges:
+        np.testing.assert_allclose(s["dW"][(v0, v1)], Wt.grad.numpy()[v0:v1], rtol=1e-9, atol=1e-14)
