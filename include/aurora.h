@@ -220,6 +220,16 @@ aurora_status_t aurora_comm_get_unique_id(void* nccl_unique_id_out /* 128 bytes 
 aurora_status_t aurora_comm_create(const void* nccl_unique_id, int nranks, int rank,
                                    int vp_size, int dp_size, aurora_comm_t* out);
 aurora_status_t aurora_comm_destroy(aurora_comm_t comm);
+/* Loopback communicator: `nranks` = vp_size x dp_size VIRTUAL ranks on the current device
+ * (same rank layout as above), written to out[0 .. nranks-1] (host array, caller-owned;
+ * each handle released with aurora_comm_destroy).  Each virtual rank must be driven from
+ * its own host thread on its own stream, issuing the same calls in the same order as a
+ * real rank would (SPMD); the collectives are device copies into a group-shared staging
+ * buffer, ordered by CUDA events plus a host barrier per collective, and the sums run in
+ * rank order (deterministic).  Not capturable into a CUDA graph.  Purpose: execute the
+ * library's multi-rank code (C1-C5, the F2 merge, the DP reduce-scatter) on one GPU and
+ * check it against the single-process oracle. */
+aurora_status_t aurora_comm_create_loopback(int nranks, int vp_size, int dp_size, aurora_comm_t* out);
 
 const char* aurora_status_string(aurora_status_t s);
 /* Static build information ("sm_100a, tcgen05 ..."). */

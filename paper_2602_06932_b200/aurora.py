@@ -26,7 +26,7 @@ MAX_K, MAX_NODES = 16, 32
 
 # Symbols declared in include/aurora.h (checked by tests/test_abi.py).
 EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fwd", "aurora_spec_loss_bwd",
-           "aurora_comm_get_unique_id", "aurora_comm_create", "aurora_comm_destroy", "aurora_status_string",
+           "aurora_comm_get_unique_id", "aurora_comm_create", "aurora_comm_create_loopback", "aurora_comm_destroy", "aurora_status_string",
            "aurora_build_info", "aurora_launch_count", "aurora_profile_enable", "aurora_profile_read",
            "aurora_debug_gemm", "aurora_debug_dlogits_rows", "aurora_set_option", "aurora_get_option",
            "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step",
@@ -124,6 +124,8 @@ def lib() -> C.CDLL:
     L.aurora_comm_create.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
     L.aurora_comm_create.restype = C.c_int
     L.aurora_comm_destroy.argtypes = [vp]
+    L.aurora_comm_create_loopback.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    L.aurora_comm_create_loopback.restype = C.c_int
     L.aurora_comm_destroy.restype = C.c_int
     L.aurora_status_string.argtypes = [C.c_int]
     L.aurora_status_string.restype = C.c_char_p
@@ -317,6 +319,14 @@ def aurora_comm_create(uid: bytes, nranks: int, rank: int, vp_size: int, dp_size
     buf = C.create_string_buffer(uid, 128)
     _check("aurora_comm_create", lib().aurora_comm_create(buf, nranks, rank, vp_size, dp_size, C.byref(h)))
     return h
+
+
+def aurora_comm_create_loopback(nranks: int, vp_size: int, dp_size: int) -> list:
+    """`nranks` virtual-rank communicators on the current device (one host thread + stream
+    per rank; see include/aurora.h)."""
+    hs = (C.c_void_p * nranks)()
+    _check("aurora_comm_create_loopback", lib().aurora_comm_create_loopback(nranks, vp_size, dp_size, hs))
+    return [C.c_void_p(h) for h in hs]
 
 
 def aurora_comm_destroy(h) -> None:

@@ -9,6 +9,7 @@
 #include <mutex>
 #include <vector>
 
+#include "comm.h"
 #include "internal.h"
 
 namespace aur {
@@ -63,54 +64,7 @@ void prof_end(int phase, cudaStream_t s) {
   }
 }
 
-// ------------------------------------------------------------------ NCCL (dlopen)
-namespace nccl {
-typedef int Result;
-typedef void* Comm;
-struct UniqueId { char internal[128]; };
-enum { ncclInt32 = 2, ncclFloat32 = 7 };
-enum { ncclSum = 0 };
-struct Api {
-  bool ok = false;
-  Result (*GetUniqueId)(UniqueId*) = nullptr;
-  Result (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
-  Result (*CommDestroy)(Comm) = nullptr;
-  Result (*CommSplit)(Comm, int, int, Comm*, void*) = nullptr;
-  Result (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
-  Result (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
-};
-Api& api() {
-  static Api a;
-  static bool tried = false;
-  if (tried) return a;
-  tried = true;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) return a;
-  a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
-  a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
-  a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
-  a.CommSplit = reinterpret_cast<decltype(a.CommSplit)>(dlsym(h, "ncclCommSplit"));
-  a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
-  a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
-  a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.CommSplit && a.AllReduce && a.AllGather;
-  return a;
-}
-}  // namespace nccl
-
 }  // namespace aur
-
-struct aurora_comm_s {
-  int nranks, rank, vp_size, dp_size, vp_rank, dp_rank;
-  // A 1-rank communicator runs every exchange (identity collectives); it exists to
-  // exercise the NCCL plumbing on one GPU.  Otherwise a group exchanges iff size > 1.
-  bool vp_x() const { return nranks == 1 || vp_size > 1; }
-  bool dp_x() const { return nranks == 1 || dp_size > 1; }
-  aur::nccl::Comm world = nullptr, vp = nullptr, dp = nullptr;
-  void* scratch = nullptr;  // comm-owned device scratch for gathered candidates / stats
-  size_t scratch_bytes = 0;
-};
 
 namespace aur {
 namespace {
@@ -389,6 +343,7 @@ bool gemm_shape_ok(const void* H, const void* W, int64_t M, int64_t d, int64_t V
 aurora_status_t bwd_fused(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local, int64_t vocab_offset,
                           const aurora_labels_t* labels, const float* row_lse, const float* dloss, float* dH,
                           float* dWf, int accumulate_dW, void* ws, aurora_comm_t comm, cudaStream_t s) {
+  aurora_status_t st = AURORA_OK;
   Carver c(ws);
   FusedWs w = carve_fused(c, M, d, V_local);
   const int64_t nchunks = cdiv(V_local, w.vc);
@@ -481,17 +436,16 @@ aurora_status_t bwd_fused(const void* H, const void* W, int64_t M, int64_t d, in
     prof_end(PH_BWD_REDUCE, s);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
   }
-  auto& A = nccl::api();
   if (comm && comm->dp_x()) {  // C5: DP gradient allreduce
     prof_begin(PH_COMM, s);
-    if (A.AllReduce(dWf, dWf, static_cast<size_t>(V_local * d), nccl::ncclFloat32, nccl::ncclSum, comm->dp, s) != 0)
-      return AURORA_ERR_NCCL;
+    if ((st = coll_allreduce(comm, G_DP, dWf, dWf, static_cast<size_t>(V_local * d), DT_F32, s)) != AURORA_OK)
+      return st;
     prof_end(PH_COMM, s);
   }
   if (comm && comm->vp_x()) {  // C4: VP dH allreduce
     prof_begin(PH_COMM, s);
-    if (A.AllReduce(dH, dH, static_cast<size_t>(M * d), nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0)
-      return AURORA_ERR_NCCL;
+    if ((st = coll_allreduce(comm, G_VP, dH, dH, static_cast<size_t>(M * d), DT_F32, s)) != AURORA_OK)
+      return st;
     prof_end(PH_COMM, s);
   }
   return AURORA_OK;
@@ -707,15 +661,14 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   prof_end(PH_SCAN, s);
   if (comm && comm->vp_x()) {
     // C1: gather every VP rank's (value-ordered) top list and merge in global order.
-    auto& A = nccl::api();
     const size_t per = static_cast<size_t>(M) * k_max;
     const size_t need = 2 * per * comm->vp_size * sizeof(float);
     if (!ensure_scratch(comm, need)) return AURORA_ERR_CUDA;
     float* gv = static_cast<float*>(comm->scratch);
     int32_t* gi = reinterpret_cast<int32_t*>(gv + per * comm->vp_size);
     prof_begin(PH_COMM, s);
-    if (A.AllGather(w.top_val, gv, per, nccl::ncclFloat32, comm->vp, s) != 0) return AURORA_ERR_NCCL;
-    if (A.AllGather(w.top_idx, gi, per, nccl::ncclInt32, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+    if ((st = coll_allgather(comm, G_VP, w.top_val, gv, per, DT_F32, s)) != AURORA_OK) return st;
+    if ((st = coll_allgather(comm, G_VP, w.top_idx, gi, per, DT_I32, s)) != AURORA_OK) return st;
     prof_end(PH_COMM, s);
     // gathered layout [rank][M][k]: list l of row m at l*M*k + m*k (global ids already)
     if ((e = launch_topk_merge(p, gv, gi, comm->vp_size, k_max, static_cast<int64_t>(M) * k_max, s)) != cudaSuccess)
@@ -726,10 +679,9 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
     if (comm && comm->vp_x()) {  // VP: per-rank (max, sum, sum*t) triples -> allgather -> merge
       p.lse_part = w.lse_part;
       if ((e = launch_row_lse_t(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
-      auto& A = nccl::api();
       const size_t per = static_cast<size_t>(M) * 3;
       if (!ensure_scratch(comm, per * comm->vp_size * sizeof(float))) return AURORA_ERR_CUDA;
-      if (A.AllGather(w.lse_part, comm->scratch, per, nccl::ncclFloat32, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+      if ((st = coll_allgather(comm, G_VP, w.lse_part, comm->scratch, per, DT_F32, s)) != AURORA_OK) return st;
       p.lse_part = nullptr;
       if ((e = launch_row_lse_t_combine(p, static_cast<const float*>(comm->scratch), comm->vp_size, s)) !=
           cudaSuccess)
@@ -742,9 +694,8 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   prof_begin(PH_VERIFY, s);
   if ((e = launch_verify(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->dp_x()) {
-    auto& A = nccl::api();
-    if (A.AllReduce(out->counts, out->counts, 2, nccl::ncclInt32, nccl::ncclSum, comm->dp, s) != 0)
-      return AURORA_ERR_NCCL;
+    if ((st = coll_allreduce(comm, G_DP, out->counts, out->counts, 2, DT_I32, s)) != AURORA_OK)
+      return st;
   }
   if ((e = launch_finalize(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   prof_end(PH_VERIFY, s);
@@ -802,9 +753,8 @@ aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const au
   prof_begin(PH_VERIFY, s);
   if (launch_verify(p, s) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->dp_x()) {
-    auto& A = nccl::api();
-    if (A.AllReduce(out->counts, out->counts, 2, nccl::ncclInt32, nccl::ncclSum, comm->dp, s) != 0)
-      return AURORA_ERR_NCCL;
+    if ((st = coll_allreduce(comm, G_DP, out->counts, out->counts, 2, DT_I32, s)) != AURORA_OK)
+      return st;
   }
   if ((long_path ? launch_finalize_long(p, s) : launch_finalize(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   prof_end(PH_VERIFY, s);
@@ -815,6 +765,7 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
                                      int64_t vocab_offset, const aurora_labels_t* labels, float* row_lse,
                                      float* row_loss, float* loss, void* ws, size_t ws_bytes, aurora_comm_t comm,
                                      void* stream) {
+  aurora_status_t st = AURORA_OK;
   if (!gemm_shape_ok(H, W, M, d, V_local) || vocab_offset < 0) return AURORA_ERR_INVALID_ARG;
   if (!labels_ok(labels, false) || !row_lse || !loss) return AURORA_ERR_INVALID_ARG;
   aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
@@ -861,11 +812,9 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   const float* msu_all = w.msu;
   int P = 1;
   if (comm && comm->vp_x()) {
-    auto& A = nccl::api();
     const size_t need = static_cast<size_t>(M) * kMsu * comm->vp_size * sizeof(float);
     if (!ensure_scratch(comm, need)) return AURORA_ERR_CUDA;
-    if (A.AllGather(w.msu, comm->scratch, static_cast<size_t>(M) * kMsu, nccl::ncclFloat32, comm->vp, s) != 0)
-      return AURORA_ERR_NCCL;
+    if ((st = coll_allgather(comm, G_VP, w.msu, comm->scratch, static_cast<size_t>(M) * kMsu, DT_F32, s)) != AURORA_OK) return st;
     msu_all = static_cast<const float*>(comm->scratch);
     P = comm->vp_size;
   }
@@ -876,8 +825,8 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
     return AURORA_ERR_CUDA;
   if ((e = launch_loss_sum(w.bp, nb, loss, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->dp_x()) {
-    auto& A = nccl::api();
-    if (A.AllReduce(loss, loss, 1, nccl::ncclFloat32, nccl::ncclSum, comm->dp, s) != 0) return AURORA_ERR_NCCL;
+    if ((st = coll_allreduce(comm, G_DP, loss, loss, 1, DT_F32, s)) != AURORA_OK)
+      return st;
   }
   prof_end(PH_FWD_COMBINE, s);
   return AURORA_OK;
@@ -890,6 +839,7 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
                                         const float* row_lse, const float* dloss, float* dH, float* dWf,
                                         int accumulate_dW, void* ws, aurora_comm_t comm, cudaStream_t s,
                                         int32_t objective) {
+  aurora_status_t st = AURORA_OK;
   Carver c(ws);
   BwdWs w = carve_bwd(c, M, d, V_local);
 
@@ -981,11 +931,9 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
       prof_end(PH_BWD_DW, sW);
       if (e != cudaSuccess) return AURORA_ERR_CUDA;
       if (comm && comm->dp_x()) {  // C5: DP gradient allreduce of this dW chunk
-        auto& A = nccl::api();
         prof_begin(PH_COMM, sW);
-        if (A.AllReduce(dWf + c0 * d, dWf + c0 * d, static_cast<size_t>(vc * d), nccl::ncclFloat32, nccl::ncclSum,
-                        comm->dp, sW) != 0)
-          return AURORA_ERR_NCCL;
+        if ((st = coll_allreduce(comm, G_DP, dWf + c0 * d, dWf + c0 * d, static_cast<size_t>(vc * d), DT_F32, sW)) != AURORA_OK)
+      return st;
         prof_end(PH_COMM, sW);
       }
       if (S) cudaEventRecord(ev[2 + 3 * ch], sW);
@@ -1031,10 +979,9 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
     cudaStreamWaitEvent(s, ev[3 + 3 * (nchunks - 1)], 0);
   }
   if (comm && comm->vp_x()) {  // C4: VP dH allreduce
-    auto& A = nccl::api();
     prof_begin(PH_COMM, s);
-    if (A.AllReduce(dH, dH, static_cast<size_t>(M * d), nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0)
-      return AURORA_ERR_NCCL;
+    if ((st = coll_allreduce(comm, G_VP, dH, dH, static_cast<size_t>(M * d), DT_F32, s)) != AURORA_OK)
+      return st;
     prof_end(PH_COMM, s);
   }
   return AURORA_OK;
@@ -1060,54 +1007,6 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
                                        accumulate_dW, ws, comm, s);
   return bwd_classic_impl(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf, accumulate_dW, ws,
                           comm, s, objective);
-}
-
-aurora_status_t aurora_comm_get_unique_id(void* id_out) {
-  if (!id_out) return AURORA_ERR_INVALID_ARG;
-  auto& A = nccl::api();
-  if (!A.ok) return AURORA_ERR_NCCL;
-  nccl::UniqueId id;
-  if (A.GetUniqueId(&id) != 0) return AURORA_ERR_NCCL;
-  std::memcpy(id_out, &id, sizeof(id));
-  return AURORA_OK;
-}
-
-aurora_status_t aurora_comm_create(const void* id_in, int nranks, int rank, int vp_size, int dp_size,
-                                   aurora_comm_t* out) {
-  if (!id_in || !out || nranks < 1 || rank < 0 || rank >= nranks || vp_size < 1 || dp_size < 1 ||
-      vp_size * dp_size != nranks)
-    return AURORA_ERR_INVALID_ARG;
-  auto& A = nccl::api();
-  if (!A.ok) return AURORA_ERR_NCCL;
-  auto* c = new aurora_comm_s();
-  c->nranks = nranks;
-  c->rank = rank;
-  c->vp_size = vp_size;
-  c->dp_size = dp_size;
-  c->vp_rank = rank % vp_size;
-  c->dp_rank = rank / vp_size;
-  nccl::UniqueId id;
-  std::memcpy(&id, id_in, sizeof(id));
-  if (A.CommInitRank(&c->world, nranks, id, rank) != 0) { delete c; return AURORA_ERR_NCCL; }
-  if (A.CommSplit(c->world, c->dp_rank, c->vp_rank, &c->vp, nullptr) != 0 ||
-      A.CommSplit(c->world, c->vp_rank, c->dp_rank, &c->dp, nullptr) != 0) {
-    A.CommDestroy(c->world);
-    delete c;
-    return AURORA_ERR_NCCL;
-  }
-  *out = c;
-  return AURORA_OK;
-}
-
-aurora_status_t aurora_comm_destroy(aurora_comm_t c) {
-  if (!c) return AURORA_ERR_INVALID_ARG;
-  auto& A = nccl::api();
-  if (c->vp) A.CommDestroy(c->vp);
-  if (c->dp) A.CommDestroy(c->dp);
-  if (c->world) A.CommDestroy(c->world);
-  if (c->scratch) cudaFree(c->scratch);
-  delete c;
-  return AURORA_OK;
 }
 
 size_t aurora_adamw_workspace_size(int64_t n) {
@@ -1137,6 +1036,7 @@ static AdamwScalars adamw_scalars(const aurora_adamw_cfg_t* cfg, int64_t step) {
 aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float* v, const float* dW, int64_t n,
                                   int64_t step, const aurora_adamw_cfg_t* cfg, const float* extra_sq, float* grad_norm,
                                   void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream) {
+  aurora_status_t st = AURORA_OK;
   if (!W_master || !m || !v || !dW || !cfg || n < 4 || n % 4 || step < 1) return AURORA_ERR_INVALID_ARG;
   if (!al16(W_master) || !al16(m) || !al16(v) || !al16(dW) || (W_bf16 && (reinterpret_cast<uintptr_t>(W_bf16) & 7)))
     return AURORA_ERR_INVALID_ARG;
@@ -1150,8 +1050,8 @@ aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float
   prof_begin(PH_OPTIM, s);
   if (launch_sumsq(dW, n, extra_sq, partials, norm_sq, s) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->vp_x()) {  // disjoint vocab shards: the global norm^2 sums over the VP group
-    auto& A = nccl::api();
-    if (A.AllReduce(norm_sq, norm_sq, 1, nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+    if ((st = coll_allreduce(comm, G_VP, norm_sq, norm_sq, 1, DT_F32, s)) != AURORA_OK)
+      return st;
   }
   if (launch_adamw(W_master, W_bf16, m, v, dW, n, norm_sq, grad_norm, sc, s) != cudaSuccess) return AURORA_ERR_CUDA;
   prof_end(PH_OPTIM, s);
@@ -1211,8 +1111,8 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
   if (launch_sum_partials(partials, static_cast<int>(nparts), extra_sq, norm_sq, s) != cudaSuccess)
     return AURORA_ERR_CUDA;
   if (comm && comm->vp_x()) {
-    auto& A = nccl::api();
-    if (A.AllReduce(norm_sq, norm_sq, 1, nccl::ncclFloat32, nccl::ncclSum, comm->vp, s) != 0) return AURORA_ERR_NCCL;
+    if ((st = coll_allreduce(comm, G_VP, norm_sq, norm_sq, 1, DT_F32, s)) != AURORA_OK)
+      return st;
   }
   b.out = nullptr;
   b.opt_norm_sq = norm_sq;
