@@ -186,45 +186,66 @@ def run_ours(args):
     A.lib()
 
     cfg = tracegen.CONFIGS[args.config]
-    # Multi-GPU (N > 1): vocab-parallel weak scaling by default (the north star's box-level
-    # scheme): one global batch of N x R requests, rank p holds vocab slice p of the lm_head
-    # W and of the target logits T; per-GPU GEMM work M*N x V/N = M x V stays fixed, and
-    # only per-row scalars (C1, C3) and the dH partials (C4) cross NVLink.  --parallel dp:
-    # data-parallel (each rank its own batch, the full vocabulary, a dW allreduce of V*d fp32).
-    vp = ws > 1 and args.parallel == "vp"
-    if vp:
-        cfg = dataclasses.replace(cfg, R=cfg.R * ws)
-    seed = cfg.seed if vp else cfg.seed + 1000 * rank
-    if args.target_topk:
-        tr = tracegen.gen_trace_topk(cfg, K_t=args.target_topk, seed=seed)
+    # Multi-GPU (N > 1), weak scaling (per-GPU GEMM work = the 1-GPU config's M x V):
+    #   VP (default, the north star's box-level scheme): one global batch of N x R requests,
+    #     rank p holds vocab slice p of W and T; only per-row scalars (C1, C3) and the dH
+    #     partials (C4) cross NVLink;
+    #   DP (--parallel dp): each rank its own batch over the full vocabulary (C2 counts, C5
+    #     dW allreduce);
+    #   --vp A --dp B (A x B = N): the 2-D layout (the tree config's DP2 x VP4): B DP groups
+    #     of A x R requests, each split over A vocab slices.
+    if ws > 1:
+        if args.vp or args.dp:
+            n_vp, n_dp = (args.vp or ws // max(args.dp, 1)), (args.dp or ws // max(args.vp, 1))
+        else:
+            n_vp, n_dp = (ws, 1) if args.parallel == "vp" else (1, ws)
+        if n_vp * n_dp != ws:
+            raise SystemExit(f"--vp {n_vp} x --dp {n_dp} != WORLD_SIZE {ws}")
     else:
-        tr = tracegen.gen_trace(cfg, seed=seed)
-    R, N, d, V, M = cfg.R, cfg.N, cfg.d, cfg.V, cfg.M
-    v0, v1 = (rank * V // ws, (rank + 1) * V // ws) if vp else (0, V)
+        n_vp, n_dp = 1, 1
+    vp_rank, dp_rank = rank % n_vp, rank // n_vp
+    vp = n_vp > 1
+    cfg_g = dataclasses.replace(cfg, R=cfg.R * n_vp)   # this DP group's requests
+    R, N, d, V, M = cfg_g.R, cfg_g.N, cfg_g.d, cfg_g.V, cfg_g.M
+    v0, v1 = vp_rank * V // n_vp, (vp_rank + 1) * V // n_vp
     V_local = v1 - v0
-    if vp:  # this rank's vocab slice (the sparse payload stays replicated: no candidate exchange)
-        tr = dict(tr)
-        tr["W_bits"] = np.ascontiguousarray(tr["W_bits"][v0:v1])
-        if not args.target_topk:
-            tr["T_bits"] = np.ascontiguousarray(tr["T_bits"][:, v0:v1])
+    sparse = bool(args.target_topk)
+    if ws == 1:
+        tr = (tracegen.gen_trace_topk(cfg, K_t=args.target_topk) if sparse else tracegen.gen_trace(cfg))
+        W = _bf16(tr["W_bits"], torch, dev)
+        T = None if sparse else _bf16(tr["T_bits"], torch, dev)
+    else:
+        if sparse:
+            raise SystemExit("--target-topk is a single-GPU workload")
+        # the group's tokens / tree / H from tracegen (seed per DP group, shared by its VP
+        # ranks); this rank's W and T slices drawn on the device (same distributions: W ~
+        # N(0, (2/sqrt d)^2), T ~ N(0, 2^2) with the designated token planted as the strict
+        # row maximum) -- the full [M, V] T of a global batch does not fit host RAM at 8 GPUs
+        tr = tracegen.gen_trace(cfg_g, seed=cfg.seed + 1000 * dp_rank, gen_T=False, gen_W=False)
+        g = torch.Generator(device=dev).manual_seed(cfg.seed * 1000003 + 7919 * dp_rank + vp_rank)
+        W = (torch.randn(V_local, d, generator=g, device=dev) * (2.0 / math.sqrt(d))).to(torch.bfloat16)
+        T = torch.empty(M, V_local, dtype=torch.bfloat16, device=dev)
+        for m0 in range(0, M, 2048):
+            m1 = min(M, m0 + 2048)
+            T[m0:m1] = (torch.randn(m1 - m0, V_local, generator=g, device=dev) * 2.0).to(torch.bfloat16)
+        des = torch.from_numpy(tr["designated"].astype(np.int64)).to(dev)
+        own = torch.nonzero((des >= v0) & (des < v1)).flatten()
+        T[own, des[own] - v0] = 16.0           # > every N(0, 4) draw of the row: strict maximum
+        del des, own
 
     comm = None
     if ws > 1:
         uid = A.aurora_comm_get_unique_id() if rank == 0 else bytes(128)
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
-        comm = A.aurora_comm_create(obj[0], ws, rank, ws, 1) if vp else A.aurora_comm_create(obj[0], ws, rank, 1, ws)
+        comm = A.aurora_comm_create(obj[0], ws, rank, n_vp, n_dp)
     elif args.comm1:  # 1-rank communicator: every exchange runs (as an identity) on one GPU
         comm = A.aurora_comm_create(A.aurora_comm_get_unique_id(), 1, 0, 1, 1)
 
-    sparse = bool(args.target_topk)
     if sparse:
         Tk_idx = torch.from_numpy(tr["Tk_idx"]).to(dev)
         Tk_val = _bf16(tr["Tk_bits"], torch, dev)
-    else:
-        T = _bf16(tr["T_bits"], torch, dev)
     H = _bf16(tr["H_bits"], torch, dev)
-    W = _bf16(tr["W_bits"], torch, dev)
     draft = torch.from_numpy(tr["draft_tokens"]).to(dev)
     parents = None if tr["parents"] is None else torch.from_numpy(tr["parents"]).to(dev)
     num_nodes = None if tr["num_nodes"] is None else torch.from_numpy(tr["num_nodes"]).to(dev)
@@ -236,7 +257,12 @@ def run_ours(args):
     dH = torch.empty(M, d, dtype=torch.float32, device=dev)
     dW = torch.empty(V_local, d, dtype=torch.float32, device=dev)
     opt = None
-    if args.optimizer:  # F3: fp32 master lm_head + fused AdamW; the GEMMs read its bf16 copy
+    sharded = n_dp > 1 and args.optimizer is not None
+    if args.optimizer == "fused" and n_dp > 1:
+        raise SystemExit("--optimizer fused needs a DP group of 1 (DP: the sharded optimizer, --optimizer)")
+    if sharded:  # F3 DP half: reduce-scatter of dW + the optimizer state sharded over the DP group
+        opt = A.ShardedAdamW(W.float().reshape(-1), comm, dp_rank, n_dp, lr=1e-5, warmup_steps=400)
+    elif args.optimizer:  # F3: fp32 master lm_head + AdamW; the GEMMs read its bf16 copy
         opt = A.AdamW(W.float().reshape(-1), lr=1e-5, warmup_steps=400, comm=comm)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -252,11 +278,13 @@ def run_ours(args):
             return
         if sparse:
             st.verify_topk(draft, Tk_idx, Tk_val, parents, num_nodes)
-            st.forward(H, W)
-            st.backward(H, W, dH, dW)
         else:
-            st.step(draft, T, H, W, dH, dW, parents, num_nodes)
-        if opt is not None and args.optimizer == "unfused":
+            st.verify(draft, T, parents, num_nodes)
+        st.forward(H, W)
+        st.backward(H, W, dH, dW, dp_reduce=not sharded)
+        if sharded:
+            opt.step(dW.reshape(-1), W.reshape(-1))
+        elif opt is not None and args.optimizer == "unfused":
             opt.step(dW.reshape(-1), W_bf16=W.reshape(-1))
 
     for _ in range(args.warmup):
@@ -275,9 +303,9 @@ def run_ours(args):
     launch_mode = "eager"
     graph = None
     launches_per_step = None
-    # multi-rank runs stay eager: the DP exchanges are NCCL calls, and capturing them is
-    # untestable on the one-GPU development box
-    if not args.eager and ws == 1:
+    # multi-rank steps are captured too: the library's collectives are NCCL calls on the
+    # caller's stream, which NCCL supports inside CUDA-graph capture (eager on failure)
+    if not args.eager:
         try:
             A.aurora_profile_read()  # clear
             A.aurora_profile_enable(True)
@@ -334,11 +362,13 @@ def run_ours(args):
         dist.barrier()
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    tokens_per_s = (M if vp else M * ws) / (ms_step / 1e3)   # VP: one global batch of M rows
+    tokens_per_s = M * n_dp / (ms_step / 1e3)   # n_dp groups of M rows (each split over n_vp vocab slices)
 
     # ---------------- e2e: public API with pinned host inputs, result read back
+    if ws > 1 and not sparse:   # the e2e leg streams this rank's T slice from pinned host memory
+        tr = dict(tr, T_bits=T.view(torch.int16).cpu().numpy().view(np.uint16))
     e2e = None if opt is not None else _run_e2e(args, torch, dist, st, tr, W, dH, dW, dev, ws, flush, sparse,
-                                                 rows_total=M if vp else M * ws)
+                                                 rows_total=M * n_dp)
 
     if rank != 0:
         if comm is not None:
@@ -351,7 +381,7 @@ def run_ours(args):
     # traffic: only for the exact workload the committed ncu capture ran (default objective)
     plain = (not sparse and args.k_accept == 1 and args.k_discard == 10 and args.accept_loss == "fkl"
              and args.optimizer != "fused")
-    cfg_dev = dataclasses.replace(cfg, V=V_local)  # the work one GPU does (VP: its vocab slice)
+    cfg_dev = dataclasses.replace(cfg_g, V=V_local)  # the work one GPU does (its rows x its vocab slice)
     roof = _roofline(phases, cfg_dev, args.steps, peak_burst, peak_src, hbm,
                      workload=cfg.name if (plain and not vp and ws == 1) else None, optimizer=args.optimizer)
     out = {
@@ -368,14 +398,18 @@ def run_ours(args):
         "dtype": "bf16",
         "data": "synthetic (tracegen seeded traces; random-init lm_head)",
         "config": {"workload": cfg.name + (f"+topk{args.target_topk}" if sparse else ""), "R": R, "N": N,
-                   "M_rows_per_gpu": M, "d": d, "V": V,
+                   "M_rows_per_dp_group": M, "M_rows_total": M * n_dp, "d": d, "V": V,
                    "target": f"top-{args.target_topk} (id, logit) pairs per row (F1)" if sparse else "dense bf16 logits",
                    "k_accept": args.k_accept, "k_discard": args.k_discard, "accept_loss": args.accept_loss,
                    "ntp_beta": args.ntp_beta,
                    "optimizer": f"adamw ({args.optimizer}, F3)" if args.optimizer else None,
                    "tree": cfg.tree,
-                   "parallelism": (f"vp{ws} (vocab-parallel lm_head, global batch {R} requests)" if vp else
-                                   f"dp{ws}" if ws > 1 else ("single (1-rank comm)" if args.comm1 else "single")),
+                   "parallelism": (f"dp{n_dp}xvp{n_vp} ({n_dp} DP group(s) of {R} requests, lm_head vocab-"
+                                   f"parallel over {n_vp})" + (", sharded AdamW" if sharded else "") if ws > 1 else
+                                   ("single (1-rank comm)" if args.comm1 else "single")),
+                   "inputs": ("tracegen (seeded host draw)" if ws == 1 else
+                              "tracegen tokens/tree/H per DP group; W and T slices drawn on the device (seeded "
+                              "N(0,(2/sqrt d)^2) / N(0,4) with the designated token planted at 16.0)"),
                    "V_local": V_local,
                    "l2": "flushed between timed steps (256 MiB write outside the step events)",
                    "launch": launch_mode},
@@ -1088,6 +1122,8 @@ def main():
     ap.add_argument("--ntp-beta", type=float, default=0.0, help="NTP auxiliary weight with --accept-loss rkl (F2)")
     ap.add_argument("--parallel", default="vp", choices=["vp", "dp"],
                     help="N > 1: vocab-parallel weak scaling (default) or data-parallel")
+    ap.add_argument("--vp", type=int, default=0, help="N > 1: vocab-parallel group size (2-D layout with --dp)")
+    ap.add_argument("--dp", type=int, default=0, help="N > 1: data-parallel group count (2-D layout with --vp)")
     ap.add_argument("--comm1", action="store_true", help="N = 1: run every exchange through a 1-rank communicator")
     ap.add_argument("--eager", action="store_true", help="launch the timed steps directly instead of replaying "
                                                           "them as one captured CUDA graph")

@@ -201,7 +201,11 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
  * dloss (dev, nullable => g = 1) f32 [1] upstream gradient.
  * dH (dev) f32 [M,d] (overwritten; VP: summed over ranks).
  * dW (dev) [V_local,d]: f32 (dW_is_bf16 = 0) — bf16 output -> UNSUPPORTED in
- * this build; accumulate_dW = 1 adds into dW (micro-batch accumulation). */
+ * this build.  accumulate_dW: bit 0 (AURORA_BWD_ACCUMULATE) adds into dW (micro-batch
+ * accumulation); bit 1 (AURORA_BWD_NO_DP_REDUCE) skips the DP dW allreduce (C5)
+ * because the caller reduce-scatters it in aurora_adamw_step_sharded. */
+#define AURORA_BWD_ACCUMULATE 1
+#define AURORA_BWD_NO_DP_REDUCE 2
 aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, int64_t d,
                                      int64_t V_local, int64_t vocab_offset,
                                      const aurora_labels_t* labels, const float* row_lse,
@@ -263,11 +267,16 @@ int64_t aurora_get_option(const char* name);
  * FP32 before optimization": W_master, m, v, dW are fp32; the bf16 copy the
  * GEMMs read is rewritten from the updated master.
  *   W_master, m, v (dev) f32 [n], updated in place; W_bf16 (dev, nullable) bf16 [n] out;
- *   dW (dev) f32 [n]; step >= 1 (bias corrections 1 - beta^step);
+ *   dW (dev) f32 [n]; step >= 1: the step number (bias corrections 1 - beta^step, warm-up);
+ *   step = 0: the step counter kept on the device in `ws` (an int64 the call increments
+ *   before using it; a zero-filled workspace starts at step 1), so a CUDA graph that
+ *   captured the call advances the schedule on every replay;
  *   extra_sq (dev, nullable) f32 [1]: sum of squares of the gradients of parameters
- *   outside this call (they share the global norm); grad_norm (dev, nullable) f32 [1]
- *   out: the global norm before clipping.  comm: norm^2 is summed over the VP group
- *   (disjoint vocab shards); DP replicas hold the already-reduced dW (C5).
+ *   outside this call (they share the global norm; added once, AFTER the VP allreduce,
+ *   so it must hold the sum over every rank's other groups, e.g. replicated parameters
+ *   counted once); grad_norm (dev, nullable) f32 [1] out: the global norm before
+ *   clipping.  comm: norm^2 of dW is summed over the VP group (disjoint vocab shards); DP
+ *   replicas hold the already-reduced dW (C5) — or use aurora_adamw_step_sharded.
  *   n % 4 == 0 and 16-byte aligned pointers.  Deterministic (fixed reduction order). */
 typedef struct {
   float lr;              /* base learning rate (1e-5 finetune / 1e-4 scratch)  */
@@ -282,13 +291,32 @@ aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float
                                   int64_t step, const aurora_adamw_cfg_t* cfg, const float* extra_sq,
                                   float* grad_norm, void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream);
 
+/* F3 under data parallelism (ZeRO-style sharded optimizer state; P:487-489 optimizer,
+ * P:495 fp32 master and gradients).  dW (dev f32 [n]): this rank's UNREDUCED gradient of
+ * its (VP-local) lm_head, from aurora_spec_loss_bwd with AURORA_BWD_NO_DP_REDUCE.  It is
+ * reduce-scattered over the DP group (replacing the C5 allreduce: half the traffic); DP
+ * rank q owns elements [q n/P, (q+1) n/P) of the optimizer state: W_master_shard, m_shard,
+ * v_shard (dev f32 [n/P], updated in place).  The global norm sums the shards over the DP
+ * and VP groups (+ extra_sq once); after the update the bf16 shards are allgathered into
+ * W_bf16 (dev bf16 [n], every rank's full copy the GEMMs read).  comm required (a 1-rank
+ * or DP-1 comm degenerates to aurora_adamw_step); n % (4 P) == 0; 16-byte aligned
+ * pointers; step as in aurora_adamw_step (0 = device counter in ws).  ws:
+ * aurora_adamw_sharded_workspace_size(n, P) bytes. */
+size_t aurora_adamw_sharded_workspace_size(int64_t n, int dp_size);
+aurora_status_t aurora_adamw_step_sharded(float* W_master_shard, void* W_bf16, float* m_shard, float* v_shard,
+                                          const float* dW, int64_t n, int64_t step,
+                                          const aurora_adamw_cfg_t* cfg, const float* extra_sq,
+                                          float* grad_norm, void* ws, size_t ws_bytes,
+                                          aurora_comm_t comm, void* stream);
+
 /* NEXT F3, fused with the backward (SURVEY F3 "applied from the dW epilogue"): runs the
  * backward of aurora_spec_loss_bwd for dH, then the optimizer step of aurora_adamw_step on
  * the fp32 master lm_head WITHOUT materialising dW: the dW GEMM is recomputed from the
  * bf16 dZ^T the backward left in `ws`, once for the global gradient norm (sum of squares
- * in the epilogue) and once with the AdamW update in the epilogue.  W (bf16 [V_local, d])
+ * in the epilogue) and once with the AdamW update applied from the TMEM accumulators
+ * (m, v and the fp32 master streamed through shared memory by TMA; 26 B per element).  W (bf16 [V_local, d])
  * is rewritten from the updated master after dz and dH have read it.  Requires the whole
- * local vocabulary in one dZ^T chunk (option dz_chunk_bytes) and no DP group (the DP dW
+ * local vocabulary in one dZ^T chunk (option dz_chunk_bytes) and a DP group of size 1 (the DP dW
  * allreduce must precede the optimizer: use aurora_spec_loss_bwd + aurora_adamw_step);
  * otherwise UNSUPPORTED.  opt_ws: aurora_adamw_workspace_size(V_local * d) bytes. */
 aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, int64_t d, int64_t V_local,

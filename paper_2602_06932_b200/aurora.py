@@ -32,7 +32,8 @@ EXPORTS = ["aurora_workspace_size", "aurora_verify_labels", "aurora_spec_loss_fw
            "aurora_verify_labels_topk", "aurora_adamw_workspace_size", "aurora_adamw_step",
            "aurora_profile_peek", "aurora_spec_loss_bwd_adamw", "aurora_tree_attn_fwd",
            "aurora_tree_attn_workspace_size", "aurora_tree_attn_bwd", "aurora_tree_rope",
-           "aurora_draft_layer_workspace_size", "aurora_draft_layer_fwd", "aurora_draft_layer_bwd"]
+           "aurora_draft_layer_workspace_size", "aurora_draft_layer_fwd", "aurora_draft_layer_bwd",
+           "aurora_adamw_sharded_workspace_size", "aurora_adamw_step_sharded"]
 
 
 class AuroraError(RuntimeError):
@@ -156,6 +157,11 @@ def lib() -> C.CDLL:
     L.aurora_adamw_step.argtypes = [vp, vp, vp, vp, vp, i64, i64, C.POINTER(aurora_adamw_cfg_t), vp, vp, vp, sz, vp,
                                     vp]
     L.aurora_set_option.restype = C.c_int
+    L.aurora_adamw_sharded_workspace_size.argtypes = [i64, C.c_int]
+    L.aurora_adamw_sharded_workspace_size.restype = sz
+    L.aurora_adamw_step_sharded.argtypes = [vp, vp, vp, vp, vp, i64, i64, C.POINTER(aurora_adamw_cfg_t), vp, vp, vp,
+                                            sz, vp, vp]
+    L.aurora_adamw_step_sharded.restype = C.c_int
     L.aurora_tree_attn_fwd.argtypes = [C.POINTER(aurora_tree_attn_t), vp, vp, vp, vp, vp, vp, vp, vp]
     L.aurora_tree_attn_fwd.restype = C.c_int
     L.aurora_tree_attn_workspace_size.argtypes = [C.POINTER(aurora_tree_attn_t)]
@@ -243,7 +249,8 @@ def aurora_debug_gemm(a_mn: bool, b_mn: bool, A, B, D, M, N, K, lda, ldb, ldd, s
 
 def aurora_adamw_step(W_master, W_bf16, m, v, dW, step: int, cfg: aurora_adamw_cfg_t, ws, extra_sq=None,
                       grad_norm=None, comm=None, stream=None) -> None:
-    """NEXT F3: one fused AdamW step (global-norm clip, warm-up LR) on fp32 master weights."""
+    """NEXT F3: one fused AdamW step (global-norm clip, warm-up LR) on fp32 master weights.
+    step >= 1, or 0 = the device step counter kept in `ws` (graph-replay safe)."""
     for t, n in ((W_master, "W_master"), (m, "m"), (v, "v"), (dW, "dW")):
         _expect(t, "f32", n)
     _expect(W_bf16, "bf16", "W_bf16")
@@ -255,7 +262,9 @@ def aurora_adamw_step(W_master, W_bf16, m, v, dW, step: int, cfg: aurora_adamw_c
 class AdamW:
     """Owns the fp32 moments and workspace of a fused AdamW over one fp32 master tensor
     (defaults: P:487-489 / Table 3 — lr 1e-5, wd 0.0, clip 0.5, 400 warm-up steps;
-    betas / eps per SPEC's design decision)."""
+    betas / eps per SPEC's design decision).  The step counter lives on the device (in the
+    zero-initialised workspace), so a captured CUDA graph advances it on every replay;
+    `step_count` mirrors it on the host for eager use."""
 
     def __init__(self, W_master, lr: float = 1e-5, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
                  max_grad_norm: float = 0.5, warmup_steps: int = 400, comm=None):
@@ -265,15 +274,45 @@ class AdamW:
         self.v = torch.zeros_like(W_master)
         self.cfg = aurora_adamw_cfg_t(lr, betas[0], betas[1], eps, weight_decay, max_grad_norm, warmup_steps)
         n = int(lib().aurora_adamw_workspace_size(W_master.numel()))
-        self.ws = torch.empty(n, dtype=torch.uint8, device=W_master.device)
+        self.ws = torch.zeros(n, dtype=torch.uint8, device=W_master.device)
         self.grad_norm = torch.zeros(1, dtype=torch.float32, device=W_master.device)
         self.step_count = 0
         self.comm = comm
 
     def step(self, dW, W_bf16=None, extra_sq=None, stream=None):
         self.step_count += 1
-        aurora_adamw_step(self.W, W_bf16, self.m, self.v, dW, self.step_count, self.cfg, self.ws, extra_sq,
+        aurora_adamw_step(self.W, W_bf16, self.m, self.v, dW, 0, self.cfg, self.ws, extra_sq,
                           self.grad_norm, self.comm, stream)
+
+
+class ShardedAdamW:
+    """F3 under data parallelism (aurora_adamw_step_sharded): this DP rank owns shard
+    `dp_rank` of the fp32 master / moments of a flat lm_head of n elements; each step
+    reduce-scatters the (unreduced) dW over the DP group, updates the shard and allgathers
+    the bf16 weights every rank's GEMMs read."""
+
+    def __init__(self, W_master_full, comm, dp_rank: int, dp_size: int, lr: float = 1e-5, betas=(0.9, 0.999),
+                 eps: float = 1e-8, weight_decay: float = 0.0, max_grad_norm: float = 0.5, warmup_steps: int = 400):
+        import torch
+        n = W_master_full.numel()
+        if n % (4 * dp_size):
+            raise ValueError("n must be a multiple of 4 * dp_size")
+        sh = n // dp_size
+        self.n, self.comm = n, comm
+        self.W = W_master_full.reshape(-1)[dp_rank * sh:(dp_rank + 1) * sh].clone()
+        self.m = torch.zeros_like(self.W)
+        self.v = torch.zeros_like(self.W)
+        self.cfg = aurora_adamw_cfg_t(lr, betas[0], betas[1], eps, weight_decay, max_grad_norm, warmup_steps)
+        nb = int(lib().aurora_adamw_sharded_workspace_size(n, dp_size))
+        self.ws = torch.zeros(nb, dtype=torch.uint8, device=self.W.device)
+        self.grad_norm = torch.zeros(1, dtype=torch.float32, device=self.W.device)
+
+    def step(self, dW, W_bf16, extra_sq=None, stream=None):
+        _expect(dW, "f32", "dW")
+        _expect(W_bf16, "bf16", "W_bf16")
+        _check("aurora_adamw_step_sharded", lib().aurora_adamw_step_sharded(
+            _ptr(self.W), _ptr(W_bf16), _ptr(self.m), _ptr(self.v), _ptr(dW), self.n, 0, C.byref(self.cfg),
+            _ptr(extra_sq), _ptr(self.grad_norm), _ptr(self.ws), self.ws.numel(), self.comm, _stream(stream)))
 
 
 def aurora_set_option(name: str, value: int) -> None:
@@ -418,9 +457,11 @@ class SpecTrainStep:
                              self.row_loss, self.loss, self.ws.data_ptr(), self.ws_bytes, self.comm, stream)
         return self.loss
 
-    def backward(self, H, W, dH, dW, dloss=None, accumulate_dW=False, stream=None):
+    def backward(self, H, W, dH, dW, dloss=None, accumulate_dW=False, stream=None, dp_reduce=True):
+        """dp_reduce=False: leave dW unreduced over the DP group (ShardedAdamW reduce-scatters it)."""
+        flags = (1 if accumulate_dW else 0) | (0 if dp_reduce else 2)
         aurora_spec_loss_bwd(H, W, self.M, self.d, self.V_local, self.vocab_offset, self.labels, self.row_lse,
-                             dloss, dH, dW, False, accumulate_dW, self.ws.data_ptr(), self.ws_bytes, self.comm,
+                             dloss, dH, dW, False, flags, self.ws.data_ptr(), self.ws_bytes, self.comm,
                              stream)
 
     def backward_adamw(self, H, W, dH, opt: "AdamW", dloss=None, extra_sq=None, stream=None):
@@ -431,7 +472,7 @@ class SpecTrainStep:
         opt.step_count += 1
         _check("aurora_spec_loss_bwd_adamw", lib().aurora_spec_loss_bwd_adamw(
             _ptr(H), _ptr(W), self.M, self.d, self.V_local, self.vocab_offset, C.byref(self.labels), _ptr(self.row_lse),
-            _ptr(dloss), _ptr(dH), _ptr(opt.W), _ptr(opt.m), _ptr(opt.v), opt.step_count, C.byref(opt.cfg),
+            _ptr(dloss), _ptr(dH), _ptr(opt.W), _ptr(opt.m), _ptr(opt.v), 0, C.byref(opt.cfg),
             _ptr(extra_sq), _ptr(opt.grad_norm), _ptr(self.ws), self.ws_bytes, _ptr(opt.ws), opt.ws.numel(),
             self.comm, _stream(stream)))
     def step(self, draft_tokens, target_logits, H, W, dH, dW, parents=None, num_nodes=None, stream=None):
@@ -596,6 +637,13 @@ class SpeculatorParams:
         self.bf.copy_(self.master.to(torch.bfloat16))
 
     def adamw(self, **kw) -> "AdamW":
+        """One AdamW over every speculator parameter.  Single-rank only: under vocab
+        parallelism the flat buffer mixes the sharded lm_head with draft-layer parameters
+        replicated on every rank, whose squares a VP norm allreduce would count vp_size
+        times."""
+        if kw.get("comm") is not None:
+            raise ValueError("SpeculatorParams.adamw is single-rank (replicated draft-layer gradients would be "
+                             "counted once per VP rank in the global norm)")
         return AdamW(self.master, **kw)
 
     def optimizer_step(self, opt: "AdamW", stream=None):

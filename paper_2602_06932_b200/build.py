@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libaurora.so")
-SOURCES = ["api.cu", "comm.cu", "k_gemm.cu", "k_bwd.cu", "k_verify.cu", "k_rows.cu", "k_optim.cu", "k_dw.cu", "k_tree_attn.cu", "k_draft_layer.cu"]
+SOURCES = ["api.cu", "comm.cu", "k_gemm.cu", "k_bwd.cu", "k_verify.cu", "k_rows.cu", "k_optim.cu", "k_dw.cu", "k_dw_adamw.cu", "k_tree_attn.cu", "k_draft_layer.cu"]
 HEADERS = ["internal.h", "comm.h", "ptx.cuh", "gemm_dev.cuh", os.path.join("..", "..", "include", "aurora.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

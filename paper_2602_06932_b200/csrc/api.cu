@@ -372,7 +372,7 @@ aurora_status_t bwd_fused(const void* H, const void* W, int64_t M, int64_t d, in
   a.dzT[0] = w.dzT[0];
   a.dzT[1] = w.dzT[1];
   a.ld_dzT = w.m_pad;
-  a.accumulate_dW = accumulate_dW ? 1 : 0;
+  a.accumulate_dW = (accumulate_dW & 1) ? 1 : 0;
   a.dh_m_tiles = static_cast<int32_t>(cdiv(M, BM));
   a.dh_n_tiles = static_cast<int32_t>(cdiv(d, BN));
   a.tile_counter = w.counters;
@@ -436,7 +436,7 @@ aurora_status_t bwd_fused(const void* H, const void* W, int64_t M, int64_t d, in
     prof_end(PH_BWD_REDUCE, s);
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
   }
-  if (comm && comm->dp_x()) {  // C5: DP gradient allreduce
+  if (comm && comm->dp_x() && !(accumulate_dW & AURORA_BWD_NO_DP_REDUCE)) {  // C5: DP gradient allreduce
     prof_begin(PH_COMM, s);
     if ((st = coll_allreduce(comm, G_DP, dWf, dWf, static_cast<size_t>(V_local * d), DT_F32, s)) != AURORA_OK)
       return st;
@@ -918,7 +918,7 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
       b.N = d;
       b.out = dWf + c0 * d;
       b.ld_out = d;
-      b.accumulate = accumulate_dW ? 1 : 0;
+      b.accumulate = (accumulate_dW & 1) ? 1 : 0;
       b.tile_counter = w.counters + 3 * ch + 1;
       b.n_fastest = 1;  // A = dZ^T chunk (M x vc, may exceed L2) streams once; H (B) stays in L2
       CUtensorMap tmOW;
@@ -930,7 +930,7 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
         e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr, pw);
       prof_end(PH_BWD_DW, sW);
       if (e != cudaSuccess) return AURORA_ERR_CUDA;
-      if (comm && comm->dp_x()) {  // C5: DP gradient allreduce of this dW chunk
+      if (comm && comm->dp_x() && !(accumulate_dW & AURORA_BWD_NO_DP_REDUCE)) {  // C5: DP gradient allreduce of this dW chunk
         prof_begin(PH_COMM, sW);
         if ((st = coll_allreduce(comm, G_DP, dWf + c0 * d, dWf + c0 * d, static_cast<size_t>(vc * d), DT_F32, sW)) != AURORA_OK)
       return st;
@@ -1009,51 +1009,121 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
                           comm, s, objective);
 }
 
-size_t aurora_adamw_workspace_size(int64_t n) {
-  if (n < 1) return 0;
-  // norm-pass partials: the standalone pass (adamw_partials) or, fused into the dW GEMM,
-  // one per (tile, CTA, epilogue warp) <= n / 4096 + tails
-  const int64_t parts = std::max<int64_t>(adamw_partials(), n / 4096 + 4 * 1024);
-  return rup((parts + 64) * 4, 256) + 256;
+// ---- F3 optimizer workspace: [scalars: norm^2 at 0, k_adamw_prep's sc at 16.., the int64
+// device step counter at byte 128] [norm partials] [sharded mode: dW shard f32, bf16 shard]
+namespace {
+struct OptWs {
+  float* norm_sq;
+  float* sc;
+  int64_t* step_dev;
+  float* partials;
+  float* dw_shard;
+  uint16_t* wb_shard;
+};
+int64_t opt_parts(int64_t n) { return std::max<int64_t>(adamw_partials(), n / 4096 + 4 * 1024); }
+OptWs carve_opt(Carver& c, int64_t n, int64_t shard) {
+  OptWs w{};
+  float* scal = c.take<float>(64);
+  w.norm_sq = scal;
+  w.sc = scal ? scal + 16 : nullptr;
+  w.step_dev = scal ? reinterpret_cast<int64_t*>(scal + 32) : nullptr;
+  w.partials = c.take<float>(opt_parts(n));
+  if (shard > 0) {
+    w.dw_shard = c.take<float>(shard);
+    w.wb_shard = c.take<uint16_t>(shard);
+  }
+  return w;
 }
-
-static bool adamw_cfg_ok(const aurora_adamw_cfg_t* cfg) {
+bool adamw_cfg_ok(const aurora_adamw_cfg_t* cfg) {
   return cfg && cfg->lr >= 0.f && cfg->beta1 >= 0.f && cfg->beta1 < 1.f && cfg->beta2 >= 0.f && cfg->beta2 < 1.f &&
          cfg->eps > 0.f && cfg->weight_decay >= 0.f && std::isfinite(cfg->max_grad_norm) && cfg->warmup_steps >= 0;
 }
-// S:379 / P:489: lr(s) = lr * s / warmup for s < warmup, then constant; torch AdamW scalars
-static AdamwScalars adamw_scalars(const aurora_adamw_cfg_t* cfg, int64_t step) {
-  const double lr_t = (cfg->warmup_steps > 0 && step < cfg->warmup_steps)
-                          ? static_cast<double>(cfg->lr) * static_cast<double>(step) / cfg->warmup_steps
-                          : static_cast<double>(cfg->lr);
-  const double bc1 = 1.0 - std::pow(static_cast<double>(cfg->beta1), static_cast<double>(step));
-  const double bc2 = 1.0 - std::pow(static_cast<double>(cfg->beta2), static_cast<double>(step));
-  return AdamwScalars{cfg->beta1, cfg->beta2, cfg->eps, static_cast<float>(lr_t / bc1),
-                      static_cast<float>(1.0 / std::sqrt(bc2)), static_cast<float>(1.0 - lr_t * cfg->weight_decay),
-                      cfg->max_grad_norm};
+AdamwHyper hyper_of(const aurora_adamw_cfg_t* cfg) {
+  return AdamwHyper{cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, cfg->weight_decay, cfg->max_grad_norm,
+                    cfg->warmup_steps};
+}
+}  // namespace
+
+size_t aurora_adamw_workspace_size(int64_t n) {
+  if (n < 1) return 0;
+  Carver c(nullptr);
+  carve_opt(c, n, 0);
+  return rup(static_cast<int64_t>(c.off), 256) + 256;
+}
+
+size_t aurora_adamw_sharded_workspace_size(int64_t n, int dp_size) {
+  if (n < 1 || dp_size < 1) return 0;
+  Carver c(nullptr);
+  carve_opt(c, n, cdiv(n, dp_size));
+  return rup(static_cast<int64_t>(c.off), 256) + 256;
 }
 
 aurora_status_t aurora_adamw_step(float* W_master, void* W_bf16, float* m, float* v, const float* dW, int64_t n,
                                   int64_t step, const aurora_adamw_cfg_t* cfg, const float* extra_sq, float* grad_norm,
                                   void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream) {
   aurora_status_t st = AURORA_OK;
-  if (!W_master || !m || !v || !dW || !cfg || n < 4 || n % 4 || step < 1) return AURORA_ERR_INVALID_ARG;
+  if (!W_master || !m || !v || !dW || !cfg || n < 4 || n % 4 || step < 0) return AURORA_ERR_INVALID_ARG;
   if (!al16(W_master) || !al16(m) || !al16(v) || !al16(dW) || (W_bf16 && (reinterpret_cast<uintptr_t>(W_bf16) & 7)))
     return AURORA_ERR_INVALID_ARG;
   if (!adamw_cfg_ok(cfg)) return AURORA_ERR_INVALID_ARG;
   if (!ws || ws_bytes < aurora_adamw_workspace_size(n)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Carver c(ws);
-  float* norm_sq = c.take<float>(64);
-  float* partials = c.take<float>(adamw_partials());
-  const AdamwScalars sc = adamw_scalars(cfg, step);
+  OptWs w = carve_opt(c, n, 0);
   prof_begin(PH_OPTIM, s);
-  if (launch_sumsq(dW, n, extra_sq, partials, norm_sq, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (launch_sumsq(dW, n, w.partials, w.norm_sq, s) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->vp_x()) {  // disjoint vocab shards: the global norm^2 sums over the VP group
-    if ((st = coll_allreduce(comm, G_VP, norm_sq, norm_sq, 1, DT_F32, s)) != AURORA_OK)
-      return st;
+    if ((st = coll_allreduce(comm, G_VP, w.norm_sq, w.norm_sq, 1, DT_F32, s)) != AURORA_OK) return st;
   }
-  if (launch_adamw(W_master, W_bf16, m, v, dW, n, norm_sq, grad_norm, sc, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (launch_adamw_prep(w.norm_sq, extra_sq, hyper_of(cfg), step, w.step_dev, w.sc, grad_norm, s) != cudaSuccess)
+    return AURORA_ERR_CUDA;
+  if (launch_adamw(W_master, W_bf16, m, v, dW, n, w.sc, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  prof_end(PH_OPTIM, s);
+  return AURORA_OK;
+}
+
+aurora_status_t aurora_adamw_step_sharded(float* W_master_shard, void* W_bf16, float* m_shard, float* v_shard,
+                                          const float* dW, int64_t n, int64_t step, const aurora_adamw_cfg_t* cfg,
+                                          const float* extra_sq, float* grad_norm, void* ws, size_t ws_bytes,
+                                          aurora_comm_t comm, void* stream) {
+  aurora_status_t st = AURORA_OK;
+  if (!comm || !W_master_shard || !W_bf16 || !m_shard || !v_shard || !dW || !cfg || step < 0)
+    return AURORA_ERR_INVALID_ARG;
+  const int P = comm->dp_size, q = comm->dp_rank;
+  if (n < 4 * P || n % (4 * P)) return AURORA_ERR_INVALID_ARG;
+  if (!al16(W_master_shard) || !al16(m_shard) || !al16(v_shard) || !al16(dW) || !al16(W_bf16))
+    return AURORA_ERR_INVALID_ARG;
+  if (!adamw_cfg_ok(cfg)) return AURORA_ERR_INVALID_ARG;
+  if (!ws || ws_bytes < aurora_adamw_sharded_workspace_size(n, P)) return AURORA_ERR_WORKSPACE;
+  const int64_t sh = n / P;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  OptWs w = carve_opt(c, n, sh);
+  prof_begin(PH_OPTIM, s);
+  // C5': reduce-scatter of dW over the DP group (rank q receives the summed shard q)
+  if (comm->dp_x()) {
+    if ((st = coll_reduce_scatter(comm, G_DP, dW, w.dw_shard, static_cast<size_t>(sh), DT_F32, s)) != AURORA_OK)
+      return st;
+  } else if (cudaMemcpyAsync(w.dw_shard, dW, sh * sizeof(float), cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+    return AURORA_ERR_CUDA;
+  }
+  if (launch_sumsq(w.dw_shard, sh, w.partials, w.norm_sq, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  // the shards are disjoint over DP (reduce-scatter slots) and over VP (vocab slices)
+  if (comm->dp_x() && (st = coll_allreduce(comm, G_DP, w.norm_sq, w.norm_sq, 1, DT_F32, s)) != AURORA_OK) return st;
+  if (comm->vp_size > 1 && (st = coll_allreduce(comm, G_VP, w.norm_sq, w.norm_sq, 1, DT_F32, s)) != AURORA_OK)
+    return st;
+  if (launch_adamw_prep(w.norm_sq, extra_sq, hyper_of(cfg), step, w.step_dev, w.sc, grad_norm, s) != cudaSuccess)
+    return AURORA_ERR_CUDA;
+  if (launch_adamw(W_master_shard, w.wb_shard, m_shard, v_shard, w.dw_shard, sh, w.sc, s) != cudaSuccess)
+    return AURORA_ERR_CUDA;
+  // every rank needs the whole updated bf16 lm_head for the next step's GEMMs
+  if (comm->dp_x()) {
+    if ((st = coll_allgather(comm, G_DP, w.wb_shard, W_bf16, static_cast<size_t>(sh / 2), DT_I32, s)) != AURORA_OK)
+      return st;
+  } else if (cudaMemcpyAsync(static_cast<uint16_t*>(W_bf16) + q * sh, w.wb_shard, sh * 2, cudaMemcpyDeviceToDevice,
+                             s) != cudaSuccess) {
+    return AURORA_ERR_CUDA;
+  }
   prof_end(PH_OPTIM, s);
   return AURORA_OK;
 }
@@ -1064,9 +1134,10 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
                                            int64_t step, const aurora_adamw_cfg_t* cfg, const float* extra_sq,
                                            float* grad_norm, void* ws, size_t ws_bytes, void* opt_ws,
                                            size_t opt_ws_bytes, aurora_comm_t comm, void* stream) {
+  aurora_status_t st = AURORA_OK;
   if (!gemm_shape_ok(H, W, M, d, V_local) || vocab_offset < 0) return AURORA_ERR_INVALID_ARG;
   if (!labels_ok(labels, false) || !row_lse || !dH || !al16(dH)) return AURORA_ERR_INVALID_ARG;
-  if (!W_master || !m || !v || !al16(W_master) || !al16(m) || !al16(v) || step < 1 || !adamw_cfg_ok(cfg))
+  if (!W_master || !m || !v || !al16(W_master) || !al16(m) || !al16(v) || step < 0 || !adamw_cfg_ok(cfg))
     return AURORA_ERR_INVALID_ARG;
   aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
@@ -1075,15 +1146,16 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
   if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
                     labels->ld_target < V_local))
     return AURORA_ERR_INVALID_ARG;
-  if (comm && comm->dp_x()) return AURORA_ERR_UNSUPPORTED;        // DP: the dW allreduce must come first
+  if (comm && comm->dp_size > 1) return AURORA_ERR_UNSUPPORTED;   // DP: reduce-scatter + aurora_adamw_step_sharded
   if (chunk_cols(V_local, M) < V_local) return AURORA_ERR_UNSUPPORTED;  // dZ^T of the whole slice in ws
+  if (!dw_adamw_supported(V_local, d)) return AURORA_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // 1) dz (whole local vocabulary) and dH, no dW
-  aurora_status_t st = bwd_classic_impl(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, nullptr, 0,
-                                        ws, comm, s, objective);
+  st = bwd_classic_impl(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, nullptr, 0, ws, comm, s,
+                        objective);
   if (st != AURORA_OK) return st;
   // 2) dW tiles recomputed from the dZ^T left in ws: pass 1 their sum of squares (global
-  //    norm), pass 2 the AdamW update from the epilogue -- dW never reaches HBM
+  //    norm), pass 2 the AdamW update from the TMEM accumulators -- dW never reaches HBM
   Carver c(ws);
   BwdWs w = carve_bwd(c, M, d, V_local);
   CUtensorMap tmZ_k, tmH_mn;
@@ -1102,27 +1174,19 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
   b.n_fastest = 1;
   const int64_t nparts = static_cast<int64_t>(b.m_tiles) * b.n_tiles * pw * kEpiWarps;
   Carver oc(opt_ws);
-  float* norm_sq = oc.take<float>(64);
-  float* partials = oc.take<float>(nparts);
-  if (oc.off > opt_ws_bytes) return AURORA_ERR_WORKSPACE;
+  OptWs ow = carve_opt(oc, V_local * d, 0);
+  if (nparts > opt_parts(V_local * d)) return AURORA_ERR_WORKSPACE;
   prof_begin(PH_OPTIM, s);
-  b.out = partials;
+  b.out = ow.partials;
   if (launch_umma_gemm(EPI_SUMSQ, false, true, tmZ_k, tmH_mn, b, s, nullptr, pw) != cudaSuccess) return AURORA_ERR_CUDA;
-  if (launch_sum_partials(partials, static_cast<int>(nparts), extra_sq, norm_sq, s) != cudaSuccess)
-    return AURORA_ERR_CUDA;
+  if (launch_sum_partials(ow.partials, static_cast<int>(nparts), ow.norm_sq, s) != cudaSuccess) return AURORA_ERR_CUDA;
   if (comm && comm->vp_x()) {
-    if ((st = coll_allreduce(comm, G_VP, norm_sq, norm_sq, 1, DT_F32, s)) != AURORA_OK)
-      return st;
+    if ((st = coll_allreduce(comm, G_VP, ow.norm_sq, ow.norm_sq, 1, DT_F32, s)) != AURORA_OK) return st;
   }
-  b.out = nullptr;
-  b.opt_norm_sq = norm_sq;
-  b.opt_grad_norm = grad_norm;
-  b.opt_w = W_master;
-  b.opt_m = m;
-  b.opt_v = v;
-  b.opt_wb = static_cast<uint16_t*>(W);
-  b.opt = adamw_scalars(cfg, step);
-  if (launch_umma_gemm(EPI_ADAMW, false, true, tmZ_k, tmH_mn, b, s, nullptr, pw) != cudaSuccess) return AURORA_ERR_CUDA;
+  if (launch_adamw_prep(ow.norm_sq, extra_sq, hyper_of(cfg), step, ow.step_dev, ow.sc, grad_norm, s) != cudaSuccess)
+    return AURORA_ERR_CUDA;
+  if (launch_dw_adamw(w.dzT, w.m_pad, H, M, d, V_local, W_master, m, v, W, ow.sc, s) != cudaSuccess)
+    return AURORA_ERR_CUDA;
   prof_end(PH_OPTIM, s);
   return AURORA_OK;
 }

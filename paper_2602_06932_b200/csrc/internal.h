@@ -28,20 +28,28 @@ constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 1024 /*
 
 // *_T: the F2 objectives (reverse KL on ACCEPT rows, dense KL on DISCARD rows) — the
 // epilogue also reads the row's target logits T (bf16) for the tile's columns.
-// EPI_SUMSQ / EPI_ADAMW (F3 fused into the dW GEMM): sum of squares of the output tile per
-// (unit, CTA, epilogue warp) / the AdamW update applied straight from TMEM to the fp32
-// master weights, moments and bf16 copy (the output itself is never stored).
+// EPI_SUMSQ (F3 fused, norm pass): sum of squares of the output tile per (unit, CTA,
+// epilogue warp); the output itself is never stored.
 enum EpiKind : int {
   EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2, EPI_FWD_STATS_T = 3, EPI_BWD_DZ_T = 4,
-  EPI_SUMSQ = 5, EPI_ADAMW = 6
+  EPI_SUMSQ = 5
 };
 
-struct AdamwScalars {  // host-computed per step (torch.optim.AdamW formulation)
-  float beta1, beta2, eps;
-  float step_size;     // lr_t / (1 - beta1^t)
-  float inv_sqrt_bc2;  // 1 / sqrt(1 - beta2^t)
-  float decay;         // 1 - lr_t * weight_decay
-  float max_norm;      // <= 0: no clipping
+// F3 hyperparameters (aurora_adamw_cfg_t as fp32 scalars).  The per-step scalars (warm-up
+// LR, bias corrections, clip coefficient) are computed on the device by k_adamw_prep from
+// the step (host value, or the device counter in the optimizer workspace) and the global
+// norm, into a small float array `sc`: [0] clip, [1] step_size = lr_t / (1 - b1^t),
+// [2] 1 / sqrt(1 - b2^t), [3] decay = 1 - lr_t wd, [4] b1, [5] b2, [6] eps.
+struct AdamwHyper {
+  float lr, beta1, beta2, eps, weight_decay, max_norm;
+  int32_t warmup;
+};
+constexpr int kOptSc = 8;
+
+// k_dw_adamw (F3 fused into the dW GEMM)
+struct DwAdamwArgs {
+  int32_t m_tiles, n_tiles, kb_total;
+  const float* sc;
 };
 
 struct GemmArgs {
@@ -81,14 +89,7 @@ struct GemmArgs {
   const float* row_lse_t;    // [M] log-sum-exp of the T row
   const float* row_aux;      // [M] E_q[z - t] (bwd, RKL rows)
   float* p_r;                // [M, 2*n_tiles] partial sum e^{z-m} (z - t) (fwd, RKL rows)
-  // ---- F3 fused optimizer (EPI_SUMSQ: partials in `out`; EPI_ADAMW: the update)
-  const float* opt_norm_sq;  // device scalar: global sum of squares (clip coefficient)
-  float* opt_grad_norm;      // nullable out: sqrt(norm_sq)
-  float* opt_w;              // fp32 master [M, ld_out] (the dW GEMM's output layout)
-  float* opt_m;
-  float* opt_v;
-  uint16_t* opt_wb;          // nullable bf16 copy
-  AdamwScalars opt;
+  // ---- F3 fused optimizer, norm pass (EPI_SUMSQ): one partial per (unit, CTA, warp) in `out`
 };
 
 // Launch the tcgen05 GEMM engine.  a_mn / b_mn select MN-major operands.
@@ -209,11 +210,20 @@ cudaError_t launch_debug_dlogits(const __nv_bfloat16* H, const __nv_bfloat16* W,
 // ---------------------------------------------------------------- F3 optimizer
 int adamw_partials();
 // ordered sum of n partials (+ extra_sq) -> out[0] (one CTA)
-cudaError_t launch_sum_partials(const float* partials, int nparts, const float* extra_sq, float* out, cudaStream_t s);
-cudaError_t launch_sumsq(const float* g, int64_t n, const float* extra_sq, float* partials, float* norm_sq,
+cudaError_t launch_sum_partials(const float* partials, int nparts, float* out, cudaStream_t s);
+cudaError_t launch_sumsq(const float* g, int64_t n, float* partials, float* norm_sq, cudaStream_t s);
+// per-step scalars (see AdamwHyper): host_step >= 1, or 0 = increment and use *step_dev
+cudaError_t launch_adamw_prep(const float* norm_sq, const float* extra_sq, const AdamwHyper& h, int64_t host_step,
+                              int64_t* step_dev, float* sc, float* grad_norm, cudaStream_t s);
+cudaError_t launch_adamw(float* W, void* Wb, float* m, float* v, const float* g, int64_t n, const float* sc,
                          cudaStream_t s);
-cudaError_t launch_adamw(float* W, void* Wb, float* m, float* v, const float* g, int64_t n, const float* norm_sq,
-                         float* grad_norm, const AdamwScalars& c, cudaStream_t s);
+bool dw_adamw_supported(int64_t V, int64_t d);
+cudaError_t launch_dw_adamw(const void* dzT, int64_t ld_dzT, const void* H, int64_t M, int64_t d, int64_t V,
+                            float* W_master, float* m, float* v, void* W_bf16, const float* sc, cudaStream_t s);
+// generic 2-D map: dtype 0 bf16 / 1 fp32, dims {inner, outer}, row stride ld elements,
+// box {box_inner, box_outer}, swizzle 0 / 32 / 64 / 128 bytes
+bool make_tmap_2d(CUtensorMap* map, int dtype, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                  uint32_t box_inner, uint32_t box_outer, int swizzle);
 
 // ---------------------------------------------------------------- accounting
 extern std::atomic<uint64_t> g_launches;

@@ -1,0 +1,325 @@
+// k_dw_adamw.cu — NEXT F3 fused into A8: the lm_head's AdamW step applied straight from
+// the dW GEMM's TMEM accumulators (P:487-489 global-norm clip 0.5, warm-up LR; P:495 fp32
+// master weights and gradients).  dW = dZ^T H is recomputed on the tensor cores from the
+// bf16 dZ^T the backward left in the workspace (K = M is small, so the MMAs are ~8% of
+// the time) and never reaches HBM: per lm_head element the kernel moves m, v, W (fp32)
+// in and out and the bf16 copy out — 26 B, the optimizer's compulsory traffic.
+//
+// One 2-CTA cluster per 256 x 256 dW tile (tcgen05.mma.cta_group::2), 11 warps per CTA:
+//   warp 0      operand TMA (dZ^T K-major 128 x 64, H MN-major half 128 x 64), 2 stages
+//   warp 1      TMEM allocation + the pair MMA issuer (leader CTA)
+//   warps 2..9  epilogue: warp w owns TMEM lane quadrant w % 4 and column half (w-2)/4
+//   warp 10     optimizer-state loader: TMA loads of 128-row x 16-column blocks of m, v and
+//               the fp32 master W (SWIZZLE_64B, 24 KB per entry) into a 6-entry ring that
+//               runs ahead of the epilogue — the bytes in flight the update needs to run at
+//               HBM speed (the round-1 version issued these loads from the epilogue warps
+//               themselves and stalled at ~3.7 TB/s)
+// The epilogue updates each entry in place in shared memory (thread = row, conflict-free
+// 16 B accesses through the swizzle) and writes it back with TMA bulk stores (m, v, W,
+// and the bf16 copy from a per-warp 1 KB staging block); the entry is released to the
+// loader once the bulk engine has read it.
+#include <cfloat>
+
+#include "gemm_dev.cuh"
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace aur {
+namespace {
+
+constexpr int kFWarps = 11;
+constexpr int kFThreads = 32 * kFWarps;
+constexpr int kFSt = 2;                               // operand stages
+constexpr int kFSB = (BN / 2) * BK * 2;               // B half per CTA and stage
+constexpr int kFStage = kSmemA + kFSB;                // 32 KB
+constexpr int kECols = 16;                            // lm_head columns per state entry
+constexpr int kEArr = BM * kECols * 4;                // 8 KB: 128 rows x 16 fp32
+constexpr int kEBytes = 3 * kEArr;                    // m, v, W
+constexpr int kFR = 6;                                // state ring entries
+constexpr int kWbBytes = 32 * kECols * 2;             // 1 KB bf16 staging per epilogue warp
+constexpr int kEPerTile = BN / kECols;                // 16 entries per tile (8 per column half)
+constexpr int kRingOff = 0;
+constexpr int kStateOff = kFSt * kFStage;
+constexpr int kWbOff = kStateOff + kFR * kEBytes;
+constexpr int kBarOff = kWbOff + kEpiWarps * kWbBytes;
+constexpr int kFSmem = kBarOff + 1024 + 1024;         // barriers + base alignment
+static_assert(kFSmem <= 232448, "dynamic smem per CTA");
+
+struct Maps {
+  CUtensorMap A, B;           // dZ^T (K-major, box 64 x 128), H (MN-major, box 64 x 64)
+  CUtensorMap ml, vl, wl;     // fp32 [V, d] loads, box 16 x 128, SW64
+  CUtensorMap ms, vs, ws;     // fp32 stores, box 16 x 32, SW64
+  CUtensorMap wbs;            // bf16 store, box 16 x 32
+};
+
+// byte offset of (row r, 16 B chunk c) in a 64 B-row SWIZZLE_64B block
+__device__ __forceinline__ uint32_t sw64(int r, int c) {
+  return static_cast<uint32_t>(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+}
+
+__global__ void __launch_bounds__(kFThreads, 1)
+    k_dw_adamw(const __grid_constant__ Maps mp, const DwAdamwArgs args) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem + kRingOff;
+  uint8_t* sB = sA + kFSt * kSmemA;
+  uint8_t* sState = smem + kStateOff;
+  uint8_t* sWb = smem + kWbOff;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  uint64_t* empty_bar = full_bar + kFSt;
+  uint64_t* tfull_bar = empty_bar + kFSt;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* efull_bar = tempty_bar + 2;   // state entries loaded
+  uint64_t* eempty_bar = efull_bar + kFR;  // state entries written back (4 warps of a half)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(eempty_bar + kFR);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&mp.A);
+    tma_prefetch_desc(&mp.B);
+    tma_prefetch_desc(&mp.ml);
+    tma_prefetch_desc(&mp.vl);
+    tma_prefetch_desc(&mp.wl);
+    tma_prefetch_desc(&mp.ms);
+    tma_prefetch_desc(&mp.vs);
+    tma_prefetch_desc(&mp.ws);
+    tma_prefetch_desc(&mp.wbs);
+    for (int s = 0; s < kFSt; ++s) {
+      mbar_init(&full_bar[s], 2);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 2 * kEpiWarps);
+    }
+    for (int e = 0; e < kFR; ++e) {
+      mbar_init(&efull_bar[e], 1);
+      mbar_init(&eempty_bar[e], kEpiWarps / 2);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_holder);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  // static per-cluster schedule, n-fastest: the dZ^T rows of one vocab tile are read once
+  const int units = args.m_tiles * args.n_tiles;
+  const int ublk = static_cast<int>(blockIdx.x >> 1);
+  const int ugrid = static_cast<int>(gridDim.x >> 1);
+  auto decode = [&](int u, int& mt, int& nt) {
+    nt = u % args.n_tiles;
+    mt = u / args.n_tiles;
+  };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- operand TMA
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int u = ublk; u < units; u += ugrid) {
+        int mt, nt;
+        decode(u, mt, nt);
+        const int arow = (mt * 2 + static_cast<int>(rank)) * BM;
+        const int brow = nt * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < args.kb_total; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * kFStage);
+          else mbar_arrive_cluster(mapa_shared(smem_u32(&full_bar[stage]), 0));
+          uint8_t* a = sA + stage * kSmemA;
+          uint8_t* b = sB + stage * kFSB;
+          tma_load_2d_pair(&mp.A, &full_bar[stage], a, kb * BK, arow);
+#pragma unroll
+          for (int i = 0; i < BN / 2 / 64; ++i)
+            tma_load_2d_pair(&mp.B, &full_bar[stage], b + i * (BK * 128), brow + i * 64, kb * BK);
+          if (++stage == kFSt) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- pair MMA issuer
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN, false, true);
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int u = ublk; u < units; u += ugrid) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < args.kb_total; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * kSmemA);
+          const uint32_t b_base = smem_u32(sB + stage * kFSB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_pair(d_tmem, operand_desc<false>(a_base, k), operand_desc<true>(b_base, k), idesc,
+                           (kb > 0 || k > 0) ? 1u : 0u);
+          umma_commit_pair(&empty_bar[stage]);
+          if (++stage == kFSt) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&tfull_bar[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp == kFWarps - 1) {
+    // ---------------------------------------------------------------- state loader
+    if (lane == 0) {
+      uint32_t pos = 0;
+      for (int u = ublk; u < units; u += ugrid) {
+        int mt, nt;
+        decode(u, mt, nt);
+        const int row0 = (mt * 2 + static_cast<int>(rank)) * BM;
+        for (int e = 0; e < kEPerTile; ++e, ++pos) {
+          const int col = nt * BN + (e & 1) * (BN / 2) + (e >> 1) * kECols;
+          const uint32_t slot = pos % kFR, ph = (pos / kFR) & 1;
+          mbar_wait(&eempty_bar[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&efull_bar[slot], kEBytes);
+          uint8_t* dst = sState + slot * kEBytes;
+          tma_load_2d(&mp.ml, &efull_bar[slot], dst, col, row0);
+          tma_load_2d(&mp.vl, &efull_bar[slot], dst + kEArr, col, row0);
+          tma_load_2d(&mp.wl, &efull_bar[slot], dst + 2 * kEArr, col, row0);
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3;              // TMEM lane quadrant this warp may read
+    const int half = (warp - 2) >> 2;    // column half of the tile
+    const float clip = __ldg(args.sc + 0), step_size = __ldg(args.sc + 1), isb2 = __ldg(args.sc + 2);
+    const float decay = __ldg(args.sc + 3), b1 = __ldg(args.sc + 4), b2 = __ldg(args.sc + 5);
+    const float eps = __ldg(args.sc + 6);
+    uint8_t* wb_stage = sWb + (warp - 2) * kWbBytes;
+    const int r = q * 32 + lane;  // this thread's row within the CTA's 128-row block
+    uint32_t acc = 0, acc_phase = 0, tile = 0;
+    for (int u = ublk; u < units; u += ugrid, ++tile) {
+      int mt, nt;
+      decode(u, mt, nt);
+      const int row0q = (mt * 2 + static_cast<int>(rank)) * BM + q * 32;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      for (int k = 0; k < kEPerTile / 2; ++k) {
+        const int e = 2 * k + half;
+        const int cl = half * (BN / 2) + k * kECols;  // tile-local column
+        const uint32_t pos = tile * kEPerTile + e;
+        const uint32_t slot = pos % kFR, ph = (pos / kFR) & 1;
+        uint32_t g[16];
+        tmem_ld_32x32b_x16(taddr + cl, g);
+        mbar_wait(&efull_bar[slot], ph);
+        tmem_ld_wait();
+        const uint32_t base = smem_u32(sState + slot * kEBytes);
+        float wnew[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t o = sw64(r, c);
+          float4 m4 = lds128(base + o), v4 = lds128(base + kEArr + o), w4 = lds128(base + 2 * kEArr + o);
+          float* mm = &m4.x;
+          float* vv = &v4.x;
+          float* ww = &w4.x;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float gg = __uint_as_float(g[4 * c + j]) * clip;
+            mm[j] = fmaf(b1, mm[j], (1.f - b1) * gg);
+            vv[j] = fmaf(b2, vv[j], (1.f - b2) * gg * gg);
+            const float denom = sqrtf(vv[j]) * isb2 + eps;
+            ww[j] = ww[j] * decay - step_size * (mm[j] / denom);
+            wnew[4 * c + j] = ww[j];
+          }
+          sts128(base + o, m4.x, m4.y, m4.z, m4.w);
+          sts128(base + kEArr + o, v4.x, v4.y, v4.z, v4.w);
+          sts128(base + 2 * kEArr + o, w4.x, w4.y, w4.z, w4.w);
+        }
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const __nv_bfloat162 h2 = __floats2bfloat162_rn(wnew[2 * j], wnew[2 * j + 1]);
+          pk[j] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        const uint32_t wbo = smem_u32(wb_stage) + lane * 32;
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(wbo), "r"(pk[0]), "r"(pk[1]), "r"(pk[2]),
+                     "r"(pk[3]) : "memory");
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(wbo + 16), "r"(pk[4]), "r"(pk[5]),
+                     "r"(pk[6]), "r"(pk[7]) : "memory");
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int32_t col = nt * BN + cl;
+          uint8_t* blk = sState + slot * kEBytes + q * 32 * 64;  // this warp's 32 rows (2 KB-aligned)
+          tma_store_2d(&mp.ms, blk, col, row0q);
+          tma_store_2d(&mp.vs, blk + kEArr, col, row0q);
+          tma_store_2d(&mp.ws, blk + 2 * kEArr, col, row0q);
+          tma_store_2d(&mp.wbs, wb_stage, col, row0q);
+          bulk_commit();
+          bulk_wait_read<0>();  // entry and staging block read by the bulk engine
+          mbar_arrive(&eempty_bar[slot]);
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[acc]), 0));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem_base);
+  }
+}
+
+}  // namespace
+
+bool dw_adamw_supported(int64_t V, int64_t d) { return V >= 1 && d % 64 == 0 && d >= 64; }
+
+cudaError_t launch_dw_adamw(const void* dzT, int64_t ld_dzT, const void* H, int64_t M, int64_t d, int64_t V,
+                            float* W_master, float* m, float* v, void* W_bf16, const float* sc, cudaStream_t s) {
+  Maps mp;
+  bool ok = make_tmap_bf16(&mp.A, dzT, M, V, ld_dzT, 64, BM) && make_tmap_bf16(&mp.B, H, d, M, d, 64, 64);
+  ok = ok && make_tmap_2d(&mp.ml, 1, m, d, V, d, kECols, BM, 64) &&
+       make_tmap_2d(&mp.vl, 1, v, d, V, d, kECols, BM, 64) &&
+       make_tmap_2d(&mp.wl, 1, W_master, d, V, d, kECols, BM, 64) &&
+       make_tmap_2d(&mp.ms, 1, m, d, V, d, kECols, 32, 64) && make_tmap_2d(&mp.vs, 1, v, d, V, d, kECols, 32, 64) &&
+       make_tmap_2d(&mp.ws, 1, W_master, d, V, d, kECols, 32, 64) &&
+       make_tmap_2d(&mp.wbs, 0, W_bf16, d, V, d, kECols, 32, 0);
+  if (!ok) return cudaErrorInvalidValue;
+  DwAdamwArgs a{};
+  a.m_tiles = static_cast<int32_t>((V + 2 * BM - 1) / (2 * BM));
+  a.n_tiles = static_cast<int32_t>((d + BN - 1) / BN);
+  a.kb_total = static_cast<int32_t>((M + BK - 1) / BK);
+  a.sc = sc;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_dw_adamw, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int units = a.m_tiles * a.n_tiles;
+  const int pairs = units < kNumSMs / 2 ? units : kNumSMs / 2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kFThreads);
+  cfg.dynamicSmemBytes = kFSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_dw_adamw, mp, a);
+  count_launch();
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+}  // namespace aur

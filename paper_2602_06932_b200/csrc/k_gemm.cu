@@ -69,12 +69,10 @@ struct SmemPlan {
   static constexpr int kSB = (TBN / PAIR) * BK * 2;  // B bytes per stage in this CTA
   static constexpr int kStageBytes = kSmemA + kSB;
   static constexpr bool kStore = EPI == EPI_STORE_F32;
-  static constexpr bool kAdamw = EPI == EPI_ADAMW;  // 32x36 fp32 transpose slice per epilogue warp
-  static constexpr int kSt = PAIR == 2 ? (kAdamw ? 5 : 6) : (kAdamw ? 3 : kStages);
+  static constexpr int kSt = PAIR == 2 ? 6 : kStages;
   static constexpr int kRing = kSt * kStageBytes;
   static constexpr int kSlots = kStore ? 2 : 0;  // 2 KB bulk-store slots per warp
-  static constexpr int kAdamwLd = 36;            // staging row stride (floats): conflict-free 16 B access
-  static constexpr int kStaging = kAdamw ? kEpiWarps * 32 * kAdamwLd * 4 : kEpiWarps * kSlots * 2048;
+  static constexpr int kStaging = kEpiWarps * kSlots * 2048;
   static constexpr int kBytes = kRing + 1024 /*barriers*/ + 1024 /*base alignment*/ + kStaging;
   static_assert(kBytes <= 232448, "dynamic smem per CTA");
   static_assert(kSt * kStageBytes <= kStages * (kSmemA + kSmemB), "ring");
@@ -427,74 +425,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
         if (lane == 0) args.out[(static_cast<int64_t>(u) * PAIR + rank) * kEpiWarps + (warp - 2)] = acc2;
-      } else if constexpr (EPI == EPI_ADAMW) {
-        // F3 pass 2: the dW tile goes straight from TMEM into the AdamW update (torch.optim
-        // AdamW form, global-norm clip); dW itself never reaches HBM.  TMEM gives thread =
-        // row, so each 32x32 block is transposed through this warp's smem slice and the
-        // fp32 master / moments are then read and written 4 rows x 128 B per instruction.
-        const float nsq = __ldg(args.opt_norm_sq);
-        const float norm = sqrtf(nsq);
-        const AdamwScalars c = args.opt;
-        const float clip = (c.max_norm > 0.f) ? fminf(1.f, c.max_norm / (norm + 1e-6f)) : 1.f;
-        if (args.opt_grad_norm && blockIdx.x == 0 && warp == 2 && lane == 0) args.opt_grad_norm[0] = norm;
-        constexpr int LD = Plan::kAdamwLd;
-        const uint32_t stg = smem_u32(reinterpret_cast<uint8_t*>(stage_f32) + (warp - 2) * (32 * LD * 4));
-        const int64_t row0 = static_cast<int64_t>(mt) * BM + q * 32;
-        const int rl0 = lane >> 3, cc = (lane & 7) * 4;  // 4 rows x 8 lanes of 16 B per pass
-        for (int cb = cbeg; cb < cend; cb += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + cb, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            sts128(stg + (lane * LD + j) * 4, __uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                   __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-          __syncwarp();
-          // all 24 16-B loads of the block in flight before any arithmetic (memory-level
-          // parallelism: ~12 KB per warp); d % 64 == 0 => no column tails, rows predicated
-          float4 mm[8], vv[8], ww[8];
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int64_t grow = row0 + it * 4 + rl0;
-            const int64_t o = grow * args.ld_out + col0 + cb + cc;
-            if (grow < args.M) {
-              mm[it] = *reinterpret_cast<const float4*>(args.opt_m + o);
-              vv[it] = *reinterpret_cast<const float4*>(args.opt_v + o);
-              ww[it] = *reinterpret_cast<const float4*>(args.opt_w + o);
-            }
-          }
-#pragma unroll
-          for (int it = 0; it < 8; ++it) {
-            const int rl = it * 4 + rl0;
-            const int64_t grow = row0 + rl;
-            if (grow < args.M) {
-              const float4 gv = lds128(stg + (rl * LD + cc) * 4);
-              const int64_t o = grow * args.ld_out + col0 + cb + cc;
-              const float gs[4] = {gv.x, gv.y, gv.z, gv.w};
-              float* mp = &mm[it].x;
-              float* vp = &vv[it].x;
-              float* wp = &ww[it].x;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float g = gs[e] * clip;
-                mp[e] = fmaf(c.beta1, mp[e], (1.f - c.beta1) * g);
-                vp[e] = fmaf(c.beta2, vp[e], (1.f - c.beta2) * g * g);
-                const float denom = sqrtf(vp[e]) * c.inv_sqrt_bc2 + c.eps;
-                wp[e] = wp[e] * c.decay - c.step_size * (mp[e] / denom);
-              }
-              *reinterpret_cast<float4*>(args.opt_m + o) = mm[it];
-              *reinterpret_cast<float4*>(args.opt_v + o) = vv[it];
-              *reinterpret_cast<float4*>(args.opt_w + o) = ww[it];
-              if (args.opt_wb) {
-                const __nv_bfloat162 lo = __floats2bfloat162_rn(ww[it].x, ww[it].y);
-                const __nv_bfloat162 hi = __floats2bfloat162_rn(ww[it].z, ww[it].w);
-                *reinterpret_cast<uint2*>(args.opt_wb + o) =
-                    make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
-              }
-            }
-          }
-          __syncwarp();
-        }
       } else if (args.tma_store && !((args.dbg_epi & 4) && half == 1)) {  // EPI_STORE_F32, TMA bulk stores
         // thread = row; each 32x16 fp32 block goes to a 64B-swizzled smem slot (rows of
         // 64 B, 16 B chunk c of row r at chunk c ^ ((r >> 1) & 3): conflict-free 16 B
@@ -685,7 +615,6 @@ cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, cons
   if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_FWD_STATS_T && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS_T, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_SUMSQ && !a_mn && b_mn) return launch_impl<EPI_SUMSQ, false, true, PAIR>(tmA, tmB, C, g, s);
-  if (epi == EPI_ADAMW && !a_mn && b_mn) return launch_impl<EPI_ADAMW, false, true, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_BWD_DZ_T && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ_T, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_STORE_F32) {
     if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false, PAIR>(tmA, tmB, C, g, s);
@@ -764,6 +693,26 @@ bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool make_tmap_2d(CUtensorMap* map, int dtype, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                  uint32_t box_inner, uint32_t box_outer, int swizzle) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc || !base) return false;
+  const uint64_t esz = dtype == 1 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * esz) % 16) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * esz};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                 : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = enc(map, dtype == 1 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 

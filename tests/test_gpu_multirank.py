@@ -244,3 +244,49 @@ def test_adamw_norm_over_vp_shards():
     for W, gn in outs:
         assert abs(gn - norm) <= 2e-5 * norm
     np.testing.assert_allclose(np.concatenate([W for W, _ in outs]), Wr, rtol=2e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("dp,vp", [(2, 1), (4, 1), (2, 2)])
+def test_sharded_adamw_dp(dp, vp):
+    """F3 DP half: each DP rank's unreduced gradient of its VP slice is reduce-scattered,
+    the optimizer state is sharded over the DP group, the norm sums every shard over DP
+    and VP, and the updated bf16 lm_head is allgathered.  Against the oracle's AdamW on
+    the summed gradient of the whole lm_head, two steps."""
+    n_v = 4 * 8 * 1021                      # elements per VP slice (a multiple of 4 * dp)
+    n = n_v * vp
+    steps = 2
+    rng = np.random.default_rng(11)
+    W0 = (rng.standard_normal(n) * 0.03).astype(np.float32)
+    G = [[(rng.standard_normal(n) * 1e-2).astype(np.float32) for _ in range(dp)] for _ in range(steps)]
+    comms = A.aurora_comm_create_loopback(dp * vp, vp, dp)
+
+    def fn(rank, comm):
+        q, v = rank // vp, rank % vp
+        sl = slice(v * n_v, (v + 1) * n_v)
+        Wfull = torch.from_numpy(W0[sl].copy()).cuda()
+        Wb = Wfull.to(torch.bfloat16)
+        opt = A.ShardedAdamW(Wfull, comm, q, dp, lr=1e-3, warmup_steps=0)
+        for t in range(steps):
+            opt.step(torch.from_numpy(G[t][q][sl].copy()).cuda(), Wb)
+        torch.cuda.current_stream().synchronize()
+        return opt.W.cpu().numpy(), Wb.view(torch.int16).cpu().numpy().view(np.uint16), float(opt.grad_norm.item())
+
+    try:
+        outs = run_ranks(comms, fn)
+    finally:
+        for h in comms:
+            A.aurora_comm_destroy(h)
+    f32 = lambda x: float(np.float32(x))
+    Wr, mr, vr = W0.astype(np.float64), np.zeros(n), np.zeros(n)
+    for t in range(steps):
+        g = np.sum([G[t][q].astype(np.float64) for q in range(dp)], axis=0)
+        Wr, mr, vr, norm = oracle.adamw_step(Wr, mr, vr, g, t + 1, f32(1e-3), beta1=f32(0.9), beta2=f32(0.999),
+                                             eps=f32(1e-8), warmup_steps=0)
+    sh = n_v // dp
+    for rank, (Wsh, Wb, gn) in enumerate(outs):
+        q, v = rank // vp, rank % vp
+        assert abs(gn - norm) <= 2e-5 * norm
+        a = v * n_v + q * sh
+        np.testing.assert_allclose(Wsh, Wr[a:a + sh], rtol=2e-6, atol=1e-9)
+        # the allgathered bf16 copy is the RNE rounding of the whole updated VP slice
+        np.testing.assert_array_equal(Wb, tracegen.f32_to_bf16_bits(Wr[v * n_v:(v + 1) * n_v].astype(np.float32)))

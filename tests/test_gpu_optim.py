@@ -140,3 +140,52 @@ def test_fused_bwd_adamw_needs_one_chunk():
         assert ei.value.status == 5
     finally:
         A.aurora_set_option("dz_chunk_bytes", saved)
+
+
+def test_adamw_device_step_counter_graph_replay():
+    """The step counter lives on the device: three replays of ONE captured optimizer step
+    follow the oracle's steps 1, 2, 3 (warm-up LR and bias corrections advance)."""
+    n = 4 * 4099
+    inp = tracegen.gen_adamw_inputs(n, steps=1, grad_scale=1e-2)
+    W = torch.from_numpy(inp["W"].copy()).cuda()
+    g = torch.from_numpy(inp["G"][0]).cuda()
+    opt = A.AdamW(W, lr=1e-3, warmup_steps=5)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        opt.step(g)            # eager step 1 (also warms up the launch path)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        opt.step(g)
+    Wr, mr, vr = inp["W"].astype(np.float64), np.zeros(n), np.zeros(n)
+    Wr, mr, vr, _ = oracle.adamw_step(Wr, mr, vr, inp["G"][0], 1, _f32(1e-3), warmup_steps=5, **HP)
+    for step in (2, 3, 4):
+        graph.replay()
+        torch.cuda.synchronize()
+        Wr, mr, vr, _ = oracle.adamw_step(Wr, mr, vr, inp["G"][0], step, _f32(1e-3), warmup_steps=5, **HP)
+        np.testing.assert_allclose(W.cpu().numpy(), Wr, rtol=2e-6, atol=1e-9)
+
+
+def test_extra_sq_added_once_after_vp_allreduce():
+    """extra_sq (other parameter groups) enters the global norm once: with a 1-rank comm
+    (the VP allreduce runs as an identity) the result equals the comm-less call."""
+    n = 4096
+    inp = tracegen.gen_adamw_inputs(n, steps=1, grad_scale=1e-2)
+    extra = torch.tensor([2.0], device="cuda")
+    uid = A.aurora_comm_get_unique_id()
+    comm = A.aurora_comm_create(uid, 1, 0, 1, 1)
+    try:
+        outs = []
+        for c in (None, comm):
+            W = torch.from_numpy(inp["W"].copy()).cuda()
+            opt = A.AdamW(W, lr=1e-3, warmup_steps=0, comm=c)
+            opt.step(torch.from_numpy(inp["G"][0]).cuda(), extra_sq=extra)
+            torch.cuda.synchronize()
+            outs.append((W.cpu().numpy(), float(opt.grad_norm.item())))
+        assert outs[0][1] == outs[1][1]
+        assert np.array_equal(outs[0][0], outs[1][0])
+        _, _, _, norm = oracle.adamw_step(inp["W"], np.zeros(n), np.zeros(n), inp["G"][0], 1, _f32(1e-3),
+                                          warmup_steps=0, extra_sq=2.0, **HP)
+        assert abs(outs[0][1] - norm) <= 1e-5 * norm
+    finally:
+        A.aurora_comm_destroy(comm)

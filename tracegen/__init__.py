@@ -129,8 +129,10 @@ def _tree_parents(rng: np.random.Generator, R: int, depth: int, beam: int) -> np
 
 
 def gen_trace(cfg: TraceConfig | str, seed: Optional[int] = None, rows: Optional[np.ndarray] = None,
-              gen_T: bool = True) -> dict:
-    """Generate one trace batch. `rows` is unused (kept for API symmetry)."""
+              gen_T: bool = True, gen_W: bool = True) -> dict:
+    """Generate one trace batch. `rows` is unused (kept for API symmetry).  gen_W=False
+    skips the W draw (bench.py's multi-GPU legs draw W and T slices on the device); the
+    later draws then come from a different position of the stream."""
     if isinstance(cfg, str):
         cfg = CONFIGS[cfg]
     seed = cfg.seed if seed is None else seed
@@ -139,9 +141,9 @@ def gen_trace(cfg: TraceConfig | str, seed: Optional[int] = None, rows: Optional
     M = R * (N + 1)
 
     # --- W, H (bf16) -------------------------------------------------------
-    W_bits = np.empty((V, d), dtype=np.uint16)
+    W_bits = np.empty((V, d) if gen_W else (0, d), dtype=np.uint16)
     step = max(1, (1 << 24) // d)
-    for v0 in range(0, V, step):
+    for v0 in range(0, V if gen_W else 0, step):
         v1 = min(V, v0 + step)
         W_bits[v0:v1] = f32_to_bf16_bits(rng.standard_normal((v1 - v0, d), dtype=np.float32)
                                          * np.float32(2.0 / math.sqrt(d)))
