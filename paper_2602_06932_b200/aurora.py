@@ -338,7 +338,7 @@ def aurora_profile_enable(on: bool) -> None:
 def aurora_profile_read(peek: bool = False) -> dict:
     """Per-phase (total ms, launches) since the last read; peek=True keeps the events (a
     captured CUDA graph re-times them on every replay)."""
-    n = 16
+    n = 32
     names = (C.c_char_p * n)()
     ms = (C.c_float * n)()
     cnt = (C.c_int32 * n)()

@@ -32,7 +32,7 @@ cudaEvent_t ev_get() {
 const char* kPhaseNames[PH_COUNT] = {"target_scan", "verify", "fwd_gemm", "fwd_combine", "bwd_dz_gemm",
                                      "bwd_dw_gemm", "bwd_dh_gemm", "bwd_reduce", "comm", "bwd_fused", "adamw",
                                      "tree_attn_fwd", "tree_attn_bwd_dq", "tree_attn_bwd_dkdv",
-                                     "tree_attn_bwd_fused", "tree_attn_fwd_tc"};
+                                     "tree_attn_bwd_fused", "tree_attn_fwd_tc", "bwd_dz_rescale"};
 }  // namespace
 
 // Inside a CUDA-graph capture the phase events become external event-record nodes, so
@@ -96,7 +96,8 @@ struct Options {
   int bwd_concurrent = 0;  // classic mode: dW || dH on side streams (measured equal to serial; off
                            // by default so per-kernel event timings stay clean)
   int tile_n = 0;          // fwd / dz tile width: 0 auto, else 256 / 224 / 192
-  int64_t dz_chunk_bytes = int64_t(2) << 30;  // classic bwd: dZ^T chunk budget (bytes)
+  int64_t dz_chunk_bytes = int64_t(16) << 30;  // classic bwd: dZ^T chunk budget (bytes; 16 GiB of the
+                                                // 180 GB HBM: the tree config's 7.8 GB in one chunk)
   int scan_ctas = 2;                           // target-scan CTAs per SM (segments per row)
   int tree_fwd_tc = 0;                         // F4 fwd: 1 = tcgen05 kernel when G*(N+1) <= 128 (opt-in:
                                                // measured slower than the mma.sync kernel)
@@ -104,7 +105,10 @@ struct Options {
                                                // fused one applies (A/B and coverage of the general path)
   int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
                                                // slower at M = 384: 0.507 vs 0.470 ms; opt-in)
+  int fwd_stage = 1;                           // Eq. 3: the fwd stages exp(z - m_half) in dZ^T so the
+                                               // bwd needs no recompute GEMM (0: recompute, round-1 path)
   Options() {
+    if (const char* e = getenv("AURORA_FWD_STAGE")) fwd_stage = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_DW_RESIDENT")) dw_resident = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_CTAS")) scan_ctas = std::max(1, atoi(e));
     if (const char* e = getenv("AURORA_DZ_CHUNK_BYTES")) dz_chunk_bytes = atoll(e);
@@ -258,6 +262,57 @@ FusedWs carve_fused(Carver& c, int64_t M, int64_t d, int64_t V_local) {
   return w;
 }
 bool classic_bwd() { return opts().bwd_mode == 0; }
+
+// ---- staged layout (fwd_stage): [fwd partials][sup_z: fp32 M x k_max][bwd region], so the
+// numerators the fwd writes into the bwd's dZ^T buffer and the fwd's per-(row, tile half)
+// maxima both survive until the bwd.  The fwd region sits at offset 0 as in the compact
+// layout; a verify call on the same ws in between overwrites it and drops the record.
+struct StageLayout { size_t off_supz, off_bwd, total; };
+StageLayout stage_layout(int64_t M, int64_t d, int64_t V_local, int k_max) {
+  StageLayout L{};
+  Carver f(nullptr);
+  carve_fwd(f, M, V_local);
+  L.off_supz = rup(static_cast<int64_t>(f.off), 256);
+  L.off_bwd = L.off_supz + rup(M * k_max * 4, 256);
+  Carver b(nullptr);
+  carve_bwd(b, M, d, V_local);
+  L.total = L.off_bwd + b.off;
+  return L;
+}
+struct StageRec {
+  const void* H;
+  const void* W;
+  int64_t M, d, V_local, voff;
+  const int32_t* sup_idx;
+  int k_max, bn, n_tiles;
+};
+std::mutex g_stage_mu;
+std::vector<std::pair<const void*, StageRec>> g_stage;  // keyed by workspace pointer
+void stage_put(const void* ws, const StageRec* r) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  for (size_t i = 0; i < g_stage.size(); ++i)
+    if (g_stage[i].first == ws) {
+      if (r) g_stage[i].second = *r;
+      else g_stage.erase(g_stage.begin() + static_cast<long>(i));
+      return;
+    }
+  if (r) g_stage.emplace_back(ws, *r);
+}
+bool staged_matches(const StageRec& r, const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
+                    int64_t voff, const aurora_labels_t* l) {
+  return r.H == H && r.W == W && r.M == M && r.d == d && r.V_local == V_local && r.voff == voff &&
+         r.sup_idx == l->sup_idx && r.k_max == l->k_max && chunk_cols(V_local, M) >= V_local;
+}
+bool stage_take(const void* ws, StageRec* out) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  for (size_t i = 0; i < g_stage.size(); ++i)
+    if (g_stage[i].first == ws) {
+      *out = g_stage[i].second;
+      g_stage.erase(g_stage.begin() + static_cast<long>(i));
+      return true;
+    }
+  return false;
+}
 
 aurora_status_t check_cfg(const aurora_loss_cfg_t* cfg, int max_k = AURORA_MAX_K) {
   if (!cfg) return AURORA_ERR_INVALID_ARG;
@@ -504,6 +559,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
     o.scan_ctas = static_cast<int>(value);
     return AURORA_OK;
   }
+  if (std::strcmp(name, "fwd_stage") == 0 && (value == 0 || value == 1)) {
+    o.fwd_stage = static_cast<int>(value);
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "dz_chunk_bytes") == 0 && value >= 1) {
     o.dz_chunk_bytes = value;
     return AURORA_OK;
@@ -531,6 +590,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "dz_chunk_bytes") == 0) return o.dz_chunk_bytes;
   if (std::strcmp(name, "scan_ctas") == 0) return o.scan_ctas;
   if (std::strcmp(name, "dw_resident") == 0) return o.dw_resident;
+  if (std::strcmp(name, "fwd_stage") == 0) return o.fwd_stage;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
   return -1;
 }
@@ -600,6 +660,7 @@ size_t aurora_workspace_size(int op, int64_t M, int64_t d, int64_t V_local, cons
     carve_fused(f, M, d, V_local);
     best = std::max(best, f.off);
   }
+  if (op == AURORA_OP_ALL) best = std::max(best, stage_layout(M, d, V_local, k_max).total);  // fwd_stage
   return rup(static_cast<int64_t>(best), 256) + 256;
 }
 
@@ -624,6 +685,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   out->objective = objective;
   out->ntp_beta = cfg->ntp_beta;
+  stage_put(ws, nullptr);  // the verify scratch overlaps a staged forward's partials
 
   Carver c(ws);
   VerifyWs w = carve_verify(c, M, t->V_local, k_max);
@@ -724,6 +786,7 @@ aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const au
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   out->objective = 0;
   out->ntp_beta = 0.f;
+  stage_put(ws, nullptr);
   Carver c(ws);
   VerifyWs w = long_path ? carve_verify_long(c, M, kk) : carve_verify(c, M, t->K_t, k_max);
   VerifyLaunch p{};
@@ -802,11 +865,31 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
     set_f2_args(a, labels, 0);
     a.p_r = w.pr;
   }
+  // Eq. 3 with the whole local vocabulary in one dZ^T chunk and a workspace holding the
+  // staged layout: the epilogue also writes exp(z - m_half) into the bwd's dZ^T buffer and
+  // keeps the support logits, and the bwd skips the recompute GEMM.
+  const StageLayout L = stage_layout(M, d, V_local, labels->k_max);
+  const bool stage = opts().fwd_stage && !objective && classic_bwd() && chunk_cols(V_local, M) >= V_local &&
+                     ws_bytes >= L.total;
+  int epi = objective ? EPI_FWD_STATS_T : EPI_FWD_STATS;
+  if (stage) {
+    Carver cb(static_cast<char*>(ws) + L.off_bwd);
+    BwdWs bw = carve_bwd(cb, M, d, V_local);
+    a.dzT = bw.dzT;
+    a.ld_dzT = bw.m_pad;
+    a.sup_z = reinterpret_cast<float*>(static_cast<char*>(ws) + L.off_supz);
+    epi = EPI_FWD_STAGE;
+  }
   prof_begin(PH_FWD_GEMM, s);
-  cudaError_t e = launch_umma_gemm(objective ? EPI_FWD_STATS_T : EPI_FWD_STATS, false, false, tmH, tmW, a, s, nullptr,
-                                   pf, bn);
+  cudaError_t e = launch_umma_gemm(epi, false, false, tmH, tmW, a, s, nullptr, pf, bn);
   prof_end(PH_FWD_GEMM, s);
   if (e != cudaSuccess) return AURORA_ERR_CUDA;
+  if (stage) {
+    const StageRec rec{H, W, M, d, V_local, vocab_offset, labels->sup_idx, labels->k_max, bn, a.n_tiles};
+    stage_put(ws, &rec);
+  } else {
+    stage_put(ws, nullptr);
+  }
   prof_begin(PH_FWD_COMBINE, s);
   if ((e = launch_reduce_partials(w.pm, w.ps, w.pu, objective ? w.pr : nullptr, M, 2 * a.n_tiles, w.msu, s)) != cudaSuccess) return AURORA_ERR_CUDA;
   const float* msu_all = w.msu;
@@ -834,14 +917,19 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
 
 // The chunked backward (dz -> dW -> dH per dZ^T chunk).  dWf == nullptr skips dW and its
 // DP allreduce (the F3 fused optimizer recomputes dW tiles from the dZ^T left in ws).
+// staged: the forward left exp(z - m_half) in the dZ^T buffer of the staged layout (one
+// chunk): the recompute GEMM is replaced by the in-place rescale + the support fix-up.
 static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M, int64_t d, int64_t V_local,
                                         int64_t vocab_offset, const aurora_labels_t* labels,
                                         const float* row_lse, const float* dloss, float* dH, float* dWf,
                                         int accumulate_dW, void* ws, aurora_comm_t comm, cudaStream_t s,
-                                        int32_t objective) {
+                                        int32_t objective, const StageRec* staged = nullptr,
+                                        __nv_bfloat16** dzT_used = nullptr) {
   aurora_status_t st = AURORA_OK;
-  Carver c(ws);
+  const StageLayout SL = staged ? stage_layout(M, d, V_local, staged->k_max) : StageLayout{};
+  Carver c(static_cast<char*>(ws) + (staged ? SL.off_bwd : 0));
   BwdWs w = carve_bwd(c, M, d, V_local);
+  if (dzT_used) *dzT_used = w.dzT;
 
   CUtensorMap tmH_k, tmH_mn;
   if (!make_tmap_bf16(&tmH_k, H, d, M, d, 64, BM)) return AURORA_ERR_CUDA;
@@ -895,10 +983,23 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
     a.ld_dzT = w.m_pad;
     a.tile_counter = w.counters + 3 * ch;
     if (objective) set_f2_args(a, labels, c0);
-    prof_begin(PH_BWD_DZ, s);
-    cudaError_t e = launch_umma_gemm(objective ? EPI_BWD_DZ_T : EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s, nullptr,
-                                     pz, bz);
-    prof_end(PH_BWD_DZ, s);
+    cudaError_t e;
+    if (staged) {
+      Carver fc(ws);
+      const FwdWs fw = carve_fwd(fc, M, V_local);
+      prof_begin(PH_BWD_RESCALE, s);
+      e = launch_dz_rescale(dzT, w.m_pad, M, V_local, staged->bn, staged->n_tiles, fw.pm, row_lse, labels->row_w, dloss,
+                            s);
+      if (e == cudaSuccess)
+        e = launch_dz_support_fix(dzT, w.m_pad, M, V_local, vocab_offset, labels,
+                                  reinterpret_cast<const float*>(static_cast<char*>(ws) + SL.off_supz), row_lse, dloss,
+                                  s);
+      prof_end(PH_BWD_RESCALE, s);
+    } else {
+      prof_begin(PH_BWD_DZ, s);
+      e = launch_umma_gemm(objective ? EPI_BWD_DZ_T : EPI_BWD_DZ, false, false, tmH_k, tmW_k, a, s, nullptr, pz, bz);
+      prof_end(PH_BWD_DZ, s);
+    }
     if (e != cudaSuccess) return AURORA_ERR_CUDA;
     if (S) {
       cudaEventRecord(ev[1 + 3 * ch], s);
@@ -1002,11 +1103,14 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
   if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
                     labels->ld_target < V_local))
     return AURORA_ERR_INVALID_ARG;
+  StageRec rec;
+  const bool staged = stage_take(ws, &rec) && staged_matches(rec, H, W, M, d, V_local, vocab_offset, labels) &&
+                      !objective && classic_bwd() && ws_bytes >= stage_layout(M, d, V_local, rec.k_max).total;
   // the fused persistent bwd implements Eq. 3 only; the F2 objectives take the chunked path
   if (!classic_bwd() && !objective) return bwd_fused(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf,
                                        accumulate_dW, ws, comm, s);
   return bwd_classic_impl(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf, accumulate_dW, ws,
-                          comm, s, objective);
+                          comm, s, objective, staged ? &rec : nullptr);
 }
 
 // ---- F3 optimizer workspace: [scalars: norm^2 at 0, k_adamw_prep's sc at 16.., the int64
@@ -1151,13 +1255,18 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
   if (!dw_adamw_supported(V_local, d)) return AURORA_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // 1) dz (whole local vocabulary) and dH, no dW
+  StageRec rec;
+  const bool staged = stage_take(ws, &rec) && staged_matches(rec, H, W, M, d, V_local, vocab_offset, labels) &&
+                      !objective && ws_bytes >= stage_layout(M, d, V_local, rec.k_max).total;
+  __nv_bfloat16* dzT = nullptr;
   st = bwd_classic_impl(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, nullptr, 0, ws, comm, s,
-                        objective);
+                        objective, staged ? &rec : nullptr, &dzT);
   if (st != AURORA_OK) return st;
   // 2) dW tiles recomputed from the dZ^T left in ws: pass 1 their sum of squares (global
   //    norm), pass 2 the AdamW update from the TMEM accumulators -- dW never reaches HBM
-  Carver c(ws);
+  Carver c(nullptr);
   BwdWs w = carve_bwd(c, M, d, V_local);
+  w.dzT = dzT;
   CUtensorMap tmZ_k, tmH_mn;
   if (!make_tmap_bf16(&tmZ_k, w.dzT, M, V_local, w.m_pad, 64, BM)) return AURORA_ERR_CUDA;
   if (!make_tmap_bf16(&tmH_mn, H, d, M, d, 64, 64)) return AURORA_ERR_CUDA;

@@ -32,7 +32,7 @@ constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 1024 /*
 // epilogue warp); the output itself is never stored.
 enum EpiKind : int {
   EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2, EPI_FWD_STATS_T = 3, EPI_BWD_DZ_T = 4,
-  EPI_SUMSQ = 5
+  EPI_SUMSQ = 5, EPI_FWD_STAGE = 6
 };
 
 // F3 hyperparameters (aurora_adamw_cfg_t as fp32 scalars).  The per-step scalars (warm-up
@@ -89,6 +89,7 @@ struct GemmArgs {
   const float* row_lse_t;    // [M] log-sum-exp of the T row
   const float* row_aux;      // [M] E_q[z - t] (bwd, RKL rows)
   float* p_r;                // [M, 2*n_tiles] partial sum e^{z-m} (z - t) (fwd, RKL rows)
+  float* sup_z;              // EPI_FWD_STAGE: [M, k_max] fp32 logit of each support entry hit
   // ---- F3 fused optimizer, norm pass (EPI_SUMSQ): one partial per (unit, CTA, warp) in `out`
 };
 
@@ -202,6 +203,12 @@ cudaError_t launch_row_combine(const float* msu_all /*[P,M,kMsu]*/, int P, int64
 cudaError_t launch_loss_sum(const float* block_partials, int nblocks, float* loss, cudaStream_t s);
 cudaError_t launch_splitk_reduce(const float* partials, int splits, int64_t n_elems, float* out, int accumulate,
                                  cudaStream_t s);
+cudaError_t launch_dz_rescale(__nv_bfloat16* dzT, int64_t ld, int64_t M, int64_t V_local, int bn, int n_tiles,
+                              const float* pm, const float* row_lse, const float* row_w, const float* dloss,
+                              cudaStream_t s);
+cudaError_t launch_dz_support_fix(__nv_bfloat16* dzT, int64_t ld, int64_t M, int64_t V_local, int64_t vocab_offset,
+                                  const aurora_labels_t* lab, const float* sup_z, const float* row_lse,
+                                  const float* dloss, cudaStream_t s);
 cudaError_t launch_debug_dlogits(const __nv_bfloat16* H, const __nv_bfloat16* W, int64_t M, int64_t d,
                                  int64_t V_local, int64_t vocab_offset, const aurora_labels_t* lab,
                                  const float* row_lse, const float* dloss, const int32_t* rows, int n_rows,
@@ -233,7 +240,7 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 // Phase profiling (CUDA events on the caller's stream).
 enum Phase : int { PH_SCAN = 0, PH_VERIFY, PH_FWD_GEMM, PH_FWD_COMBINE, PH_BWD_DZ, PH_BWD_DW, PH_BWD_DH,
                    PH_BWD_REDUCE, PH_COMM, PH_BWD_FUSED, PH_OPTIM, PH_TREE_FWD, PH_TREE_BWD_DQ,
-                   PH_TREE_BWD_DKDV, PH_TREE_BWD_FUSED, PH_TREE_FWD_TC, PH_COUNT };
+                   PH_TREE_BWD_DKDV, PH_TREE_BWD_FUSED, PH_TREE_FWD_TC, PH_BWD_RESCALE, PH_COUNT };
 void prof_begin(int phase, cudaStream_t s);
 int opt_tree_bwd_split();  // aurora_set_option("tree_bwd_split")
 int opt_tree_fwd_tc();     // aurora_set_option("tree_fwd_tc")

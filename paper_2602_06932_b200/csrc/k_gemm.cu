@@ -17,6 +17,10 @@
 //                  rounded to bf16 and stored TRANSPOSED into the chunk workspace
 //                  dZ^T[v, m] (coalesced: a warp store covers 32 consecutive rows).
 //   EPI_STORE_F32  A8/A9: fp32 tile store (overwrite / accumulate / split-K slot).
+//   EPI_FWD_STAGE  A5 plus the staged half of A7 (default Eq. 3 path): the statistics of
+//                  EPI_FWD_STATS with an exact per-(row, tile half) max, and the softmax
+//                  numerators exp(z - m_half) stored as bf16 into the dZ^T workspace, so
+//                  the backward needs no recompute GEMM (k_dz_rescale finishes dz).
 #include <cfloat>
 #include <climits>
 
@@ -84,7 +88,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
   using Plan = SmemPlan<EPI, A_MN, PAIR, TBN>;
-  constexpr bool kFwd = EPI == EPI_FWD_STATS || EPI == EPI_FWD_STATS_T;
+  constexpr bool kStage = EPI == EPI_FWD_STAGE;
+  constexpr bool kFwd = EPI == EPI_FWD_STATS || EPI == EPI_FWD_STATS_T || kStage;
   constexpr bool kDz = EPI == EPI_BWD_DZ || EPI == EPI_BWD_DZ_T;
   constexpr bool kT = EPI == EPI_FWD_STATS_T || EPI == EPI_BWD_DZ_T;
   static_assert(TBN == BN || (PAIR == 1 && !B_MN), "narrow tiles: single-CTA, K-major B only");
@@ -314,6 +319,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (kDz && mode == 1) eqzt = __ldg(args.row_aux + row);
           }
         }
+        if constexpr (kStage) {
+          // A5 + the staged half of A7: pass 1 the exact max of this (row, tile half), pass 2
+          // e = exp(z - m_half) -> s, the support dot u (and each support logit z_j, fp32,
+          // for the backward's exact q_j - p~_j), and e rounded to bf16 into dZ^T[col][row]
+          // (the backward rescales it in place by g w exp(m_half - lse) once lse is known).
+          for (int cb = cbeg; cb < cend; cb += 32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + cb, r);
+            tmem_ld_wait();
+            const int nj = (cb + 32 <= ncols) ? 32 : ncols - cb;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mrun = (j < nj) ? fmaxf(mrun, __uint_as_float(r[j])) : mrun;
+          }
+          const float mb = mrun * kLog2e;
+          for (int cb = cbeg; cb < cend && mrun != -INFINITY; cb += 32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + cb, r);
+            tmem_ld_wait();
+            const int nj = (cb + 32 <= ncols) ? 32 : ncols - cb;
+            float z[32];
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(r[j]);
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float e0 = (j < nj) ? ex2_approx(fmaf(z[j], kLog2e, -mb)) : 0.f;
+              const float e1 = (j + 1 < nj) ? ex2_approx(fmaf(z[j + 1], kLog2e, -mb)) : 0.f;
+              s0 += e0;
+              s1 += e1;
+              if (row_ok) {
+                __nv_bfloat16* dst = args.dzT + (col0 + cb + j) * args.ld_dzT + row;
+                if (j < nj) dst[0] = __float2bfloat16_rn(e0);
+                if (j + 1 < nj) dst[args.ld_dzT] = __float2bfloat16_rn(e1);
+              }
+            }
+            srun += s0 + s1;
+            while (cur.nxt < col0 + cb + 32) {
+              const float zj = select32(z, static_cast<int>(cur.nxt - col0 - cb));
+              usum = fmaf(cur.nxt_p, zj, usum);
+              args.sup_z[row * args.k_max + cur.pos] = zj;
+              cur.advance();
+            }
+          }
+        } else
         for (int cb = cbeg; cb < cend; cb += 32) {  // warp-uniform bounds
           uint32_t r[32];
           tmem_ld_32x32b_x32(taddr + cb, r);
@@ -599,12 +648,14 @@ cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, cons
     if (bn != BN && (a_mn || b_mn || epi == EPI_STORE_F32)) return cudaErrorInvalidValue;
     if (bn == 224) {
       if (epi == EPI_FWD_STATS) return launch_impl<EPI_FWD_STATS, false, false, 1, 224>(tmA, tmB, C, g, s);
+      if (epi == EPI_FWD_STAGE) return launch_impl<EPI_FWD_STAGE, false, false, 1, 224>(tmA, tmB, C, g, s);
       if (epi == EPI_BWD_DZ) return launch_impl<EPI_BWD_DZ, false, false, 1, 224>(tmA, tmB, C, g, s);
       if (epi == EPI_FWD_STATS_T) return launch_impl<EPI_FWD_STATS_T, false, false, 1, 224>(tmA, tmB, C, g, s);
       return launch_impl<EPI_BWD_DZ_T, false, false, 1, 224>(tmA, tmB, C, g, s);
     }
     if (bn == 192) {
       if (epi == EPI_FWD_STATS) return launch_impl<EPI_FWD_STATS, false, false, 1, 192>(tmA, tmB, C, g, s);
+      if (epi == EPI_FWD_STAGE) return launch_impl<EPI_FWD_STAGE, false, false, 1, 192>(tmA, tmB, C, g, s);
       if (epi == EPI_BWD_DZ) return launch_impl<EPI_BWD_DZ, false, false, 1, 192>(tmA, tmB, C, g, s);
       if (epi == EPI_FWD_STATS_T) return launch_impl<EPI_FWD_STATS_T, false, false, 1, 192>(tmA, tmB, C, g, s);
       return launch_impl<EPI_BWD_DZ_T, false, false, 1, 192>(tmA, tmB, C, g, s);
@@ -612,6 +663,7 @@ cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, cons
   }
   if (bn != BN) return cudaErrorInvalidValue;
   if (epi == EPI_FWD_STATS && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS, false, false, PAIR>(tmA, tmB, C, g, s);
+  if (epi == EPI_FWD_STAGE && !a_mn && !b_mn) return launch_impl<EPI_FWD_STAGE, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_BWD_DZ && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_FWD_STATS_T && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS_T, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_SUMSQ && !a_mn && b_mn) return launch_impl<EPI_SUMSQ, false, true, PAIR>(tmA, tmB, C, g, s);

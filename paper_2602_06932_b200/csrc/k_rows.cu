@@ -11,6 +11,13 @@
 //                      plus beta (lse - z_y) (NTP) where u = beta z_y.
 //   k_loss_sum         one block: ordered sum of the block partials -> loss.
 //   k_splitk_reduce    dH = (acc ? dH : 0) + sum_s partial[s], ordered (deterministic).
+//   k_dz_rescale       A7 without the recompute GEMM: the forward staged e = exp(z - m_h)
+//                      (bf16) in dZ^T; once lse is known, dz = g w exp(m_h - lse) e in
+//                      place.  CTA per (vocab tile half h, 1024-row block): the factors
+//                      F_m = g w_m exp(m_h,m - lse_m) in shared memory, then 16 B vectors
+//                      of 8 rows along dZ^T's contiguous row axis (HBM-bound: 4 B per element).
+//   k_dz_support_fix   the support entries: dz_mj = g w_m (exp(z_mj - lse_m) - p~_mj) from
+//                      the fp32 logit the forward kept (no cancellation through bf16 e).
 #include <cfloat>
 #include <climits>
 
@@ -181,6 +188,83 @@ __global__ void k_debug_dlogits(const __nv_bfloat16* __restrict__ H, const __nv_
         dz -= coef * lab.sup_p[m * lab.k_max + j];
     out[r * V_local + v] = dz;
   }
+}
+
+constexpr int kRsRows = 1024;  // dZ^T columns (rows m) per rescale CTA
+__global__ void __launch_bounds__(256) k_dz_rescale(__nv_bfloat16* __restrict__ dzT, int64_t ld, int64_t M,
+                                                    int64_t V_local, int bn, const float* __restrict__ pm,
+                                                    int pm_stride, const float* __restrict__ row_lse,
+                                                    const float* __restrict__ row_w, const float* __restrict__ dloss) {
+  __shared__ float F[kRsRows];
+  const int h = blockIdx.x;  // tile half: tile h / 2, columns [0, 128) or [128, bn)
+  const int64_t c0 = static_cast<int64_t>(h >> 1) * bn + ((h & 1) ? BN / 2 : 0);
+  const int64_t c1 = min(static_cast<int64_t>(h >> 1) * bn + ((h & 1) ? bn : BN / 2), V_local);
+  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * kRsRows;
+  const int64_t m1 = min(m0 + kRsRows, ld);
+  const float g = dloss ? __ldg(dloss) : 1.f;
+  for (int i = threadIdx.x; i < kRsRows; i += blockDim.x) {
+    const int64_t m = m0 + i;
+    float f = 0.f;
+    if (m < M) {
+      const float w = __ldg(row_w + m);
+      const float mh = __ldg(pm + m * pm_stride + h);
+      if (w != 0.f && mh != -INFINITY) f = g * w * __expf(mh - __ldg(row_lse + m));
+    }
+    F[i] = f;
+  }
+  __syncthreads();
+  if (c0 >= c1) return;
+  const int nv = static_cast<int>((m1 - m0) >> 3);  // 8-row vectors per dZ^T row (ld % 8 == 0)
+  const int64_t total = (c1 - c0) * nv;
+  for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+    const int64_t c = c0 + i / nv;
+    const int vi = static_cast<int>(i % nv);
+    uint4* p = reinterpret_cast<uint4*>(dzT + c * ld + m0) + vi;
+    uint4 x = *p;
+    uint32_t* w = &x.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w[e]);
+      const float2 f = __bfloat1622float2(b);
+      b = __floats2bfloat162_rn(f.x * F[vi * 8 + 2 * e], f.y * F[vi * 8 + 2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&b);
+    }
+    *p = x;
+  }
+}
+
+__global__ void k_dz_support_fix(__nv_bfloat16* __restrict__ dzT, int64_t ld, int64_t M, int64_t V_local,
+                                 int64_t vocab_offset, const int32_t* __restrict__ sup_idx,
+                                 const float* __restrict__ sup_p, const float* __restrict__ sup_z, int k_max,
+                                 const float* __restrict__ row_lse, const float* __restrict__ row_w,
+                                 const float* __restrict__ dloss) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= M * k_max) return;
+  const int64_t m = i / k_max;
+  const int32_t gid = sup_idx[i];
+  if (gid == INT32_MAX) return;
+  const int64_t loc = static_cast<int64_t>(gid) - vocab_offset;
+  if (loc < 0 || loc >= V_local) return;
+  const float coef = (dloss ? __ldg(dloss) : 1.f) * row_w[m];
+  dzT[loc * ld + m] = __float2bfloat16_rn(coef * (__expf(sup_z[i] - row_lse[m]) - sup_p[i]));
+}
+
+cudaError_t launch_dz_rescale(__nv_bfloat16* dzT, int64_t ld, int64_t M, int64_t V_local, int bn, int n_tiles,
+                              const float* pm, const float* row_lse, const float* row_w, const float* dloss,
+                              cudaStream_t s) {
+  dim3 grid(static_cast<unsigned>(2 * n_tiles), static_cast<unsigned>((ld + kRsRows - 1) / kRsRows));
+  k_dz_rescale<<<grid, 256, 0, s>>>(dzT, ld, M, V_local, bn, pm, 2 * n_tiles, row_lse, row_w, dloss);
+  count_launch();
+  return cudaGetLastError();
+}
+cudaError_t launch_dz_support_fix(__nv_bfloat16* dzT, int64_t ld, int64_t M, int64_t V_local, int64_t vocab_offset,
+                                  const aurora_labels_t* lab, const float* sup_z, const float* row_lse,
+                                  const float* dloss, cudaStream_t s) {
+  const int64_t n = M * lab->k_max;
+  k_dz_support_fix<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      dzT, ld, M, V_local, vocab_offset, lab->sup_idx, lab->sup_p, sup_z, lab->k_max, row_lse, lab->row_w, dloss);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_reduce_partials(const float* pm, const float* ps, const float* pu, const float* pr, int64_t M,

@@ -279,7 +279,10 @@ def test_sharded_adamw_dp(dp, vp):
     f32 = lambda x: float(np.float32(x))
     Wr, mr, vr = W0.astype(np.float64), np.zeros(n), np.zeros(n)
     for t in range(steps):
-        g = np.sum([G[t][q].astype(np.float64) for q in range(dp)], axis=0)
+        g = G[t][0].copy()                  # the fp32 sum in rank order: the optimizer's input
+        for q in range(1, dp):
+            g = (g + G[t][q]).astype(np.float32)
+        g = g.astype(np.float64)
         Wr, mr, vr, norm = oracle.adamw_step(Wr, mr, vr, g, t + 1, f32(1e-3), beta1=f32(0.9), beta2=f32(0.999),
                                              eps=f32(1e-8), warmup_steps=0)
     sh = n_v // dp
