@@ -419,10 +419,15 @@ def run_ours(args):
         "e2e": e2e,
         "clocks": clk.summary(),
     }
-    # executed 8MVd (fwd, dz recompute, dW, dH) over the step, against the BURST bf16 peak
-    # (MEASURED_PEAKS.json bf16_tflops); the sustained figure is the power-capped 4 s loop
-    out["tensor_frac_step"] = round((8.0 * M * V_local * d / (ms_step / 1e3)) / (peak_burst * 1e12), 4)
-    out["tensor_frac_step_vs_sustained"] = round((8.0 * M * V_local * d / (ms_step / 1e3)) / (peak_sus * 1e12), 4)
+    # executed GEMM flops over the step against the BURST bf16 peak (MEASURED_PEAKS.json
+    # bf16_tflops; the sustained figure is the power-capped 4 s loop): 6MVd (fwd, dW, dH) on
+    # the staged path, 8MVd when the backward recomputes Z (dz GEMM)
+    gemms = 4 if "bwd_dz_gemm" in phases and phases["bwd_dz_gemm"][1] else 3
+    flops_step = 2.0 * gemms * M * V_local * d
+    out["executed_gemm_flops_per_step"] = flops_step
+    out["tensor_frac_step"] = round((flops_step / (ms_step / 1e3)) / (peak_burst * 1e12), 4)
+    out["tensor_frac_step_vs_sustained"] = round((flops_step / (ms_step / 1e3)) / (peak_sus * 1e12), 4)
+    out["algorithmic_tensor_frac_step"] = round((6.0 * M * V_local * d / (ms_step / 1e3)) / (peak_burst * 1e12), 4)
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = _cpu_baseline(cfg, args)
     print(json.dumps(out), flush=True)
@@ -548,14 +553,16 @@ def _roofline(phases, cfg, steps, peak, peak_src, hbm_peak_gbs=6551.0, workload=
             best = (k, tot_ms, rec)
     # G2 (target scan) and G6 (row combine) as achieved DRAM GB/s vs the HBM peak
     for k, byts in (("target_scan", 2.0 * cfg.M * cfg.V),
-                    ("fwd_combine", 16.0 * cfg.M * 2 * math.ceil(cfg.V / 256.0))):
+                    ("fwd_combine", 16.0 * cfg.M * 2 * math.ceil(cfg.V / 256.0)),
+                    ("bwd_dz_rescale", 4.0 * cfg.M * cfg.V)):
         if k in phases and phases[k][1]:
             tot_ms, n = phases[k]
             t = (tot_ms / steps) / 1e3
             per.append({"kernel": k, "ms_per_step": round(tot_ms / steps, 4), "achieved_gbs": round(byts / t / 1e9, 1),
                         "bound": "hbm", "frac": round(byts / t / 1e9 / hbm_peak_gbs, 4),
-                        "work": "M*V*2 B of T read once" if k == "target_scan" else
-                        "(m, s, u, r) partials, >= 16 B per (row, 128-column tile half)"})
+                        "work": {"target_scan": "M*V*2 B of T read once",
+                                 "fwd_combine": "(m, s, u, r) partials, >= 16 B per (row, 128-column tile half)",
+                                 "bwd_dz_rescale": "M*V bf16 staged numerators read + dz written (4 B per element)"}[k]})
     if best is None:
         return None
     k, _, rec = best

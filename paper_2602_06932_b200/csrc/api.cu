@@ -105,10 +105,12 @@ struct Options {
                                                // fused one applies (A/B and coverage of the general path)
   int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
                                                // slower at M = 384: 0.507 vs 0.470 ms; opt-in)
+  int scan_ring = 1;                           // A2: persistent TMA-ring scan (0: round-1 kernel)
   int fwd_stage = 1;                           // Eq. 3: the fwd stages exp(z - m_half) in dZ^T so the
                                                // bwd needs no recompute GEMM (0: recompute, round-1 path)
   Options() {
     if (const char* e = getenv("AURORA_FWD_STAGE")) fwd_stage = atoi(e) ? 1 : 0;
+    if (const char* e = getenv("AURORA_SCAN_RING")) scan_ring = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_DW_RESIDENT")) dw_resident = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_CTAS")) scan_ctas = std::max(1, atoi(e));
     if (const char* e = getenv("AURORA_DZ_CHUNK_BYTES")) dz_chunk_bytes = atoll(e);
@@ -189,8 +191,10 @@ int dh_splits(int64_t M, int64_t d, int64_t kb_total, int pair = 1) {
 }
 
 struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; float* ept; float* lse_part; };
+// TMA-ring scan: segments of ~24K columns (48 KB) -> M x nseg items over the 148 SMs
+int ring_nseg(int64_t V_local) { return static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(1, cdiv(V_local, 24576)))); }
 VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
-  const int nseg = scan_nseg(M, V_local);
+  const int nseg = std::max(scan_nseg(M, V_local), ring_nseg(V_local) * scan_ring_lists());
   VerifyWs w;
   w.ept = c.take<float>(M);
   w.lse_part = c.take<float>(M * 3);
@@ -559,6 +563,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
     o.scan_ctas = static_cast<int>(value);
     return AURORA_OK;
   }
+  if (std::strcmp(name, "scan_ring") == 0 && (value == 0 || value == 1)) {
+    o.scan_ring = static_cast<int>(value);
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "fwd_stage") == 0 && (value == 0 || value == 1)) {
     o.fwd_stage = static_cast<int>(value);
     return AURORA_OK;
@@ -591,6 +599,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "scan_ctas") == 0) return o.scan_ctas;
   if (std::strcmp(name, "dw_resident") == 0) return o.dw_resident;
   if (std::strcmp(name, "fwd_stage") == 0) return o.fwd_stage;
+  if (std::strcmp(name, "scan_ring") == 0) return o.scan_ring;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
   return -1;
 }
@@ -699,8 +708,14 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   p.R = t->R;
   p.N = t->N;
   p.k_max = k_max;
-  p.nseg = scan_nseg(M, t->V_local);
+  p.nseg = ring_nseg(t->V_local);
   p.seg_len = rup(cdiv(t->V_local, p.nseg), 8);
+  const bool ring = opts().scan_ring && scan_ring_ok(p);
+  if (!ring) {
+    p.nseg = scan_nseg(M, t->V_local);
+    p.seg_len = rup(cdiv(t->V_local, p.nseg), 8);
+  }
+  const int nlists = ring ? p.nseg * scan_ring_lists() : p.nseg;
   p.draft = t->draft_tokens;
   p.parents = t->parents;
   p.num_nodes = t->num_nodes;
@@ -716,8 +731,8 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   if ((e = cudaMemsetAsync(out->counts, 0, 2 * sizeof(int32_t), s)) != cudaSuccess) return AURORA_ERR_CUDA;
   if ((e = cudaMemsetAsync(out->status, 0, sizeof(uint32_t), s)) != cudaSuccess) return AURORA_ERR_CUDA;
   prof_begin(PH_SCAN, s);
-  if ((e = launch_target_scan(p, s)) != cudaSuccess) return AURORA_ERR_CUDA;
-  if ((e = launch_topk_merge(p, w.cand_val, w.cand_idx, p.nseg, static_cast<int64_t>(p.nseg) * k_max, k_max, s)) !=
+  if ((e = (ring ? launch_target_scan_ring(p, s) : launch_target_scan(p, s))) != cudaSuccess) return AURORA_ERR_CUDA;
+  if ((e = launch_topk_merge(p, w.cand_val, w.cand_idx, nlists, static_cast<int64_t>(nlists) * k_max, k_max, s)) !=
       cudaSuccess)
     return AURORA_ERR_CUDA;
   prof_end(PH_SCAN, s);

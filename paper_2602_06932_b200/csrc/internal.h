@@ -50,6 +50,9 @@ constexpr int kOptSc = 8;
 struct DwAdamwArgs {
   int32_t m_tiles, n_tiles, kb_total;
   const float* sc;
+  int64_t V, d;
+  float *m, *v, *w;    // fp32 [V, d] moments and master
+  __nv_bfloat16* wb;   // bf16 [V, d] copy
 };
 
 struct GemmArgs {
@@ -172,6 +175,10 @@ struct VerifyLaunch {
   aurora_loss_cfg_t cfg;
 };
 cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s);
+// persistent TMA-ring scan (16 B-aligned rows): writes scan_ring_lists() lists per (row, segment)
+bool scan_ring_ok(const VerifyLaunch& p);
+int scan_ring_lists();
+cudaError_t launch_target_scan_ring(const VerifyLaunch& p, cudaStream_t s);
 cudaError_t launch_topk_merge(const VerifyLaunch& p, const float* in_val, const int32_t* in_idx, int nlists,
                               int64_t row_stride, int64_t list_stride, cudaStream_t s);
 cudaError_t launch_target_scan_topk(const VerifyLaunch& p, const int32_t* tk_idx, const uint16_t* tk_val, int32_t K_t,

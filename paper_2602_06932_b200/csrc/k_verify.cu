@@ -278,6 +278,116 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
   }
 }
 
+// --------------------------------------------------------------------------- A2 scan (TMA ring)
+// Persistent variant for 16 B-aligned rows: one CTA per SM streams its (row, segment) work
+// items through a 6 x 16 KB shared-memory ring filled by 1-D bulk async copies
+// (cp.async.bulk, one producer thread), so the bytes in flight per SM (~96 KB) no longer
+// depend on registers or occupancy.  8 consumer warps read the ring with 16 B shared loads
+// (warp w: vectors w*32 + lane + i*256 of each stage) into per-warp lists; each warp writes
+// its list per item (k_topk_merge merges the nseg x 8 lists of a row), so items need no
+// CTA-wide synchronisation and can be small (good balance over the 148 SMs).
+constexpr int kRingStage = 16384;
+constexpr int kRingStages = 6;
+constexpr int kRingConsumers = 8;
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__global__ void __launch_bounds__(32 * (kRingConsumers + 1), 1) k_target_scan_ring(VerifyLaunch p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingStages * kRingStage);
+  uint64_t* empty = full + kRingStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = p.k_max;
+  const int items = p.M * p.nseg;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRingStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kRingConsumers);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == kRingConsumers) {
+    // ---- producer: one thread issues the bulk copies of every item of this CTA, in order
+    if (lane == 0) {
+      uint32_t slot = 0, ph = 0;
+      for (int u = blockIdx.x; u < items; u += gridDim.x) {
+        const int row = u / p.nseg, seg = u % p.nseg;
+        const int64_t c0 = static_cast<int64_t>(seg) * p.seg_len;
+        const int64_t c1 = min(p.V_local, c0 + p.seg_len);
+        const int64_t vbytes = c1 > c0 ? ((c1 - c0) >> 3) * 16 : 0;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.T + static_cast<int64_t>(row) * p.ldT + c0);
+        for (int64_t off = 0; off < vbytes; off += kRingStage) {
+          const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kRingStage), vbytes - off));
+          mbar_wait(&empty[slot], ph ^ 1);
+          mbar_arrive_expect_tx(&full[slot], bytes);
+          bulk_g2s(ring + slot * kRingStage, src + off, bytes, &full[slot]);
+          if (++slot == kRingStages) { slot = 0; ph ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  uint32_t slot = 0, ph = 0, bad = 0;
+  for (int u = blockIdx.x; u < items; u += gridDim.x) {
+    const int row = u / p.nseg, seg = u % p.nseg;
+    const int64_t c0 = static_cast<int64_t>(seg) * p.seg_len;
+    const int64_t c1 = min(p.V_local, c0 + p.seg_len);
+    const int64_t nvec = c1 > c0 ? (c1 - c0) >> 3 : 0;
+    WarpList L;
+    L.init(k);
+    for (int64_t v0 = 0; v0 < nvec; v0 += kRingStage / 16) {
+      const int nv = static_cast<int>(min(static_cast<int64_t>(kRingStage / 16), nvec - v0));
+      mbar_wait(&full[slot], ph);
+      const uint32_t sbase = smem_u32(ring + slot * kRingStage);
+      for (int b = warp * 32; b < nv; b += 32 * kRingConsumers) {  // warp-uniform trip count
+        const int vi = b + lane;
+        uint4 w = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+        if (vi < nv) {
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                       : "r"(sbase + vi * 16));
+          bad |= nonfinite8(w);
+        }
+        const bool h = vi < nv && max8(w) >= L.thr_v;
+        if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, w, c0 + (v0 + vi) * 8, -INFINITY);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (++slot == kRingStages) { slot = 0; ph ^= 1; }
+    }
+    // scalar tail of the segment (V_local % 8 columns of the row's last segment)
+    const uint16_t* T = p.T + static_cast<int64_t>(row) * p.ldT;
+    for (int64_t cb = c0 + nvec * 8 + static_cast<int64_t>(warp) * 32; cb < c1; cb += 32 * kRingConsumers) {
+      const int64_t col = cb + lane;
+      float v = -INFINITY;
+      if (col < c1) {
+        const uint32_t b16 = T[col];
+        bad |= static_cast<uint32_t>((b16 & 0x7FFFu) >= 0x7F80u);
+        v = __uint_as_float(b16 << 16);
+      }
+      uint32_t hit = __ballot_sync(0xffffffffu, col < c1 && L.admits(v, static_cast<int32_t>(col)));
+      while (hit) {
+        const int s2 = __ffs(hit) - 1;
+        hit &= hit - 1;
+        L.offer(v, static_cast<int32_t>(col), s2);
+      }
+    }
+    if (lane < k) {
+      const int64_t o = ((static_cast<int64_t>(row) * p.nseg + seg) * kRingConsumers + warp) * k;
+      p.cand_val[o + lane] = L.v;
+      p.cand_idx[o + lane] = (L.i == INT32_MAX) ? INT32_MAX : static_cast<int32_t>(L.i + p.vocab_offset);
+    }
+  }
+  bad = __reduce_or_sync(0xffffffffu, bad);
+  if (bad && lane == 0) atomicOr(p.lab.status, AURORA_STATUS_NONFINITE);
+}
+
 // --------------------------------------------------------------------------- A2 merge
 // warp per row: merge `nlists` (<= 32) sorted lists of length k -> top list + argmax.
 __global__ void __launch_bounds__(256) k_topk_merge(VerifyLaunch p, const float* in_val, const int32_t* in_idx,
@@ -717,6 +827,24 @@ __global__ void __launch_bounds__(256) k_row_lse_t_combine(VerifyLaunch p, const
 // --------------------------------------------------------------------------- launchers
 cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s) {
   k_target_scan<<<static_cast<unsigned>(p.M) * p.nseg, 256, 0, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+bool scan_ring_ok(const VerifyLaunch& p) {
+  return (reinterpret_cast<uintptr_t>(p.T) & 15) == 0 && (p.ldT & 7) == 0 && (p.seg_len & 7) == 0;
+}
+int scan_ring_lists() { return kRingConsumers; }
+cudaError_t launch_target_scan_ring(const VerifyLaunch& p, cudaStream_t s) {
+  constexpr int kSmem = kRingStages * kRingStage + 2 * kRingStages * 8 + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_target_scan_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t items = static_cast<int64_t>(p.M) * p.nseg;
+  const int grid = static_cast<int>(items < kNumSMs ? items : kNumSMs);
+  k_target_scan_ring<<<grid, 32 * (kRingConsumers + 1), kSmem, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }

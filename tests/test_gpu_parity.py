@@ -220,6 +220,7 @@ def test_accumulate_and_upstream_grad():
     dH2 = torch.empty_like(out["dH"])
     dW2 = out["dW"].clone()
     dl = torch.tensor([-2.0], device="cuda", dtype=torch.float32)
+    st.forward(g["H"], g["W"])   # re-stage the numerators (the first backward consumed them)
     st.backward(g["H"], g["W"], dH2, dW2, dloss=dl, accumulate_dW=True)
     torch.cuda.synchronize()
     # dW2 = dW + (-2) dW = -dW ; dH2 = -2 dH
