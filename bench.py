@@ -886,7 +886,8 @@ def run_draft_layer(args):
     W = dict(Wfc=rnd(d, 3 * d, k=(3 * d) ** -0.5), Wq=rnd(qd, 2 * d, k=(2 * d) ** -0.5),
              Wk=rnd(kd, 2 * d, k=(2 * d) ** -0.5), Wv=rnd(kd, 2 * d, k=(2 * d) ** -0.5), Wo=rnd(d, qd, k=qd ** -0.5),
              Wg=rnd(I, d, k=d ** -0.5), Wu=rnd(I, d, k=d ** -0.5), Wd=rnd(d, I, k=I ** -0.5),
-             we=torch.ones(d, device=dev), wh=torch.ones(d, device=dev), wpost=torch.ones(d, device=dev))
+             we=torch.ones(d, device=dev), wh=torch.ones(d, device=dev), wpost=torch.ones(d, device=dev),
+             wfinal=torch.ones(d, device=dev))
     h3, e = rnd(M, 3 * d), rnd(M, d)
     Kp, Vp = rnd(P, c.Hkv, c.dh), rnd(P, c.Hkv, c.dh)
     dH = torch.randn(M, d, generator=g, device=dev) * 0.1
@@ -974,7 +975,7 @@ def run_draft_layer(args):
         "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded device generator; tracegen structure)",
         "config": {"workload": c.name + "+draft_layer", "R": c.R, "N": c.N, "d": d, "I": I, "Hq": c.Hq, "Hkv": c.Hkv,
-                   "dh": c.dh, "prefix_tokens": P, "gemm": "cuBLAS bf16 (library GEMMs)",
+                   "dh": c.dh, "prefix_tokens": P, "gemm": "libaurora tcgen05 engine (bf16 / fp32 TMA-store epilogues)",
                    "l2": "flushed between timed steps (256 MiB write outside the step events)", "launch": launch_mode},
         "gpu_launches": int(n_launch),
         "phases_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in phases.items() if v[1]},
@@ -1024,7 +1025,7 @@ def run_full_step(args):
     fan = dict(Wfc=3 * d, Wq=2 * d, Wk=2 * d, Wv=2 * d, Wo=qd, Wg=d, Wu=d, Wd=I)
     for k_, f_ in fan.items():
         sp.M[k_].copy_(torch.randn(sp.M[k_].shape, generator=g, device=dev) * f_ ** -0.5)
-    for k_ in ("we", "wh", "wpost"):
+    for k_ in ("we", "wh", "wpost", "wfinal"):
         sp.M[k_].fill_(1.0)
     sp.M["W_lm"].copy_(_bf16(tr["W_bits"], torch, dev).float())
     sp.bf.copy_(sp.master.to(torch.bfloat16))

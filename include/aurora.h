@@ -388,15 +388,17 @@ aurora_status_t aurora_tree_rope(const aurora_tree_attn_t* ta, void* Q, int q_fp
 /* ---- NEXT F4: the EAGLE-3 draft layer around the tree attention (reading F4-R7) ----------
  *   g = h3 Wfc^T;  u = [rms(e) w_e ; rms(g) w_h];  q,k,v = u W{q,k,v}^T;  RoPE(q, k) at tree
  *   positions (aurora_tree_rope);  o = tree attention over [Kp; k], [Vp; v];  y = g + o Wo^T;
- *   z = rms(y) w_post;  H = y + (silu(z Wg^T) * (z Wu^T)) Wd^T,   rms(x) = x (mean x^2 + eps)^-1/2
+ *   z = rms(y) w_post;  h = y + (silu(z Wg^T) * (z Wu^T)) Wd^T;  H = rms(h) w_final (the final
+ *   norm before the lm_head),   rms(x) = x (mean x^2 + eps)^-1/2
  * Rows in the lm_head path's order, M = R (N+1).  Layouts (row-major, dense): h3 bf16 [M, 3d],
  * e bf16 [M, d] (token embeddings), H bf16 [M, d]; Wfc [d, 3d], Wq [Hq dh, 2d], Wk/Wv [Hkv dh, 2d],
- * Wo [d, Hq dh], Wg/Wu [I, d], Wd [d, I] bf16 (nn.Linear); w_e, w_h, w_post f32 [d].  The dense
- * projections are library GEMMs (cuBLAS, bf16 operands, fp32 accumulation).  aurora_draft_layer_fwd
+ * Wo [d, Hq dh], Wg/Wu [I, d], Wd [d, I] bf16 (nn.Linear); w_e, w_h, w_post, w_final f32 [d].  The
+ * dense projections run on the library's tcgen05 GEMM engine (bf16 operands, fp32 accumulation in
+ * TMEM, bf16 / fp32 TMA-store epilogues, residual adds as TMA reduce-add).  aurora_draft_layer_fwd
  * keeps the activations the backward needs in `ws` (aurora_draft_layer_workspace_size bytes); the
  * matching aurora_draft_layer_bwd must get the same ws.  Gradients: weights f32 (overwritten),
  * dh3 / de f32 [M, 3d] / [M, d], dKp / dVp bf16 like Kp / Vp.  Limits: dh == 128 (tree attention),
- * d and I multiples of 8, eps > 0; else UNSUPPORTED / INVALID_ARG with nothing enqueued. */
+ * d and I multiples of 64, eps > 0; else UNSUPPORTED / INVALID_ARG with nothing enqueued. */
 typedef struct {
   aurora_tree_attn_t ta;         /* batch structure, heads (Hq, Hkv, dh), prefix bounds, status */
   int32_t d, I;                  /* hidden size, MLP intermediate size                          */
@@ -404,10 +406,10 @@ typedef struct {
 } aurora_draft_layer_t;
 typedef struct {
   const void *Wfc, *Wq, *Wk, *Wv, *Wo, *Wg, *Wu, *Wd;   /* (dev) bf16 */
-  const float *we, *wh, *wpost;                          /* (dev) f32  */
+  const float *we, *wh, *wpost, *wfinal;                 /* (dev) f32  */
 } aurora_draft_weights_t;
 typedef struct {
-  float *Wfc, *Wq, *Wk, *Wv, *Wo, *Wg, *Wu, *Wd, *we, *wh, *wpost;  /* (dev) f32, overwritten */
+  float *Wfc, *Wq, *Wk, *Wv, *Wo, *Wg, *Wu, *Wd, *we, *wh, *wpost, *wfinal;  /* (dev) f32, overwritten */
 } aurora_draft_grads_t;
 size_t aurora_draft_layer_workspace_size(const aurora_draft_layer_t* L);
 aurora_status_t aurora_draft_layer_fwd(const aurora_draft_layer_t* L, const aurora_draft_weights_t* W, const void* h3,

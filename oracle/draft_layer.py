@@ -13,9 +13,9 @@ P:163-169 tree attention, P:376 D_RPC h_t) does not spell the layer out; reading
     o   = TreeAttention(q, [Kp; k], [Vp; v])           (oracle/tree_attention.py)
     y   = g + o Wo^T                                   residual on the fused hidden
     z   = rms(y) * w_post
-    H   = y + ((silu(z Wg^T) * (z Wu^T)) Wd^T)        SwiGLU MLP, residual
-with rms(x) = x / sqrt(mean(x^2) + eps).  H feeds the lm_head path (the final norm before the
-lm_head belongs to it).  Backward: the gradients of <dH, H> for every weight, for h3, e and the
+    h   = y + ((silu(z Wg^T) * (z Wu^T)) Wd^T)        SwiGLU MLP, residual
+    H   = rms(h) * w_final                             EAGLE-3's final norm before the lm_head
+with rms(x) = x / sqrt(mean(x^2) + eps).  H feeds the lm_head path.  Backward: the gradients of <dH, H> for every weight, for h3, e and the
 cached prefix K/V — written out step by step (chain rule per op, in reverse order).
 Pins: tests/test_draft_layer_oracle.py (torch f64 autograd of an independent torch module,
 central finite differences).  Everything float64.
@@ -47,7 +47,7 @@ def silu(x):
 
 def layer_fwd(P: dict, X: dict, cfg: dict):
     """P: weights (Wfc [d,3d], we [d], wh [d], Wq [Hq*dh, 2d], Wk, Wv [Hkv*dh, 2d], Wo [d, Hq*dh],
-    wpost [d], Wg, Wu [I, d], Wd [d, I]); X: h3 [R, N+1, 3d], e [R, N+1, d], Kp/Vp, prefix_off,
+    wpost [d], Wg, Wu [I, d], Wd [d, I], wfinal [d]); X: h3 [R, N+1, 3d], e [R, N+1, d], Kp/Vp, prefix_off,
     parents, num_nodes; cfg: Hq, Hkv, dh, theta, eps.  Returns H and the saved activations."""
     R, N1, _ = X["h3"].shape
     Hq, Hkv, dh = cfg["Hq"], cfg["Hkv"], cfg["dh"]
@@ -67,8 +67,9 @@ def layer_fwd(P: dict, X: dict, cfg: dict):
     z, rp = rms_fwd(y, P["wpost"], eps)
     a, b = z @ P["Wg"].T, z @ P["Wu"].T
     m = silu(a) * b
-    H = y + m @ P["Wd"].T
-    S = dict(g=g, re=re, rh=rh, u=u, pos=pos, qr=qr, kr=kr, v=v, of=of, y=y, z=z, rp=rp, a=a, b=b, m=m)
+    h = y + m @ P["Wd"].T
+    H, rf = rms_fwd(h, P["wfinal"], eps)
+    S = dict(g=g, re=re, rh=rh, u=u, pos=pos, qr=qr, kr=kr, v=v, of=of, y=y, z=z, rp=rp, a=a, b=b, m=m, h=h, rf=rf)
     return H, S
 
 
@@ -78,9 +79,11 @@ def layer_bwd(P: dict, X: dict, cfg: dict, S: dict, dH):
     Hq, Hkv, dh = cfg["Hq"], cfg["Hkv"], cfg["dh"]
     G = {}
     flat = lambda t: t.reshape(-1, t.shape[-1])
-    # H = y + m Wd^T
-    G["Wd"] = flat(dH).T @ flat(S["m"])
-    dm = dH @ P["Wd"]
+    # H = rms(h) w_final
+    dhid, G["wfinal"] = rms_bwd(S["h"], P["wfinal"], S["rf"], dH)
+    # h = y + m Wd^T
+    G["Wd"] = flat(dhid).T @ flat(S["m"])
+    dm = dhid @ P["Wd"]
     sa = 1.0 / (1.0 + np.exp(-S["a"]))
     da = dm * S["b"] * (sa * (1.0 + S["a"] * (1.0 - sa)))        # d silu(a)/da = s (1 + a (1 - s))
     db = dm * silu(S["a"])
@@ -88,7 +91,7 @@ def layer_bwd(P: dict, X: dict, cfg: dict, S: dict, dH):
     G["Wu"] = flat(db).T @ flat(S["z"])
     dz = da @ P["Wg"] + db @ P["Wu"]
     dy_mlp, G["wpost"] = rms_bwd(S["y"], P["wpost"], S["rp"], dz)
-    dy = dH + dy_mlp
+    dy = dhid + dy_mlp
     # y = g + of Wo^T
     G["Wo"] = flat(dy).T @ flat(S["of"])
     do = (dy @ P["Wo"]).reshape(R, N1, Hq, dh)

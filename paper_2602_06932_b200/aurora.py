@@ -85,7 +85,7 @@ class aurora_draft_layer_t(C.Structure):
                 ("eps", C.c_float)]
 
 
-_DL_W = ["Wfc", "Wq", "Wk", "Wv", "Wo", "Wg", "Wu", "Wd", "we", "wh", "wpost"]
+_DL_W = ["Wfc", "Wq", "Wk", "Wv", "Wo", "Wg", "Wu", "Wd", "we", "wh", "wpost", "wfinal"]
 
 
 class aurora_draft_weights_t(C.Structure):
@@ -556,7 +556,7 @@ class DraftLayer:
     def __init__(self, ta: "TreeAttention", d: int, I: int, W: dict, theta: float = 500000.0, eps: float = 1e-6):
         import torch
         for n in _DL_W:
-            _expect(W[n], "f32" if n in ("we", "wh", "wpost") else "bf16", n)
+            _expect(W[n], "f32" if n in ("we", "wh", "wpost", "wfinal") else "bf16", n)
         self.ta, self.W = ta, W
         self.cfg = aurora_draft_layer_t(ta.cfg, d, I, float(theta), float(eps))
         self.w = aurora_draft_weights_t(*[_ptr(W[n]) for n in _DL_W])
@@ -593,7 +593,16 @@ class SpeculatorStep:
 
     def step(self, draft_tokens, T, h3, e, Kp, Vp, W_lm, H, dH, dW_lm, G, dh3, de, dKp, dVp, parents=None,
              num_nodes=None, stream=None):
-        self.spec.verify(draft_tokens, T, parents, num_nodes, stream)
+        """The tree (parents, ragged node counts) is the layer's TreeAttention's: verification,
+        the tree-attention mask, tree RoPE and the prefix layout all follow the same batch.
+        `parents` / `num_nodes`, if given, must be those very tensors (a different tree would
+        silently mix two batches)."""
+        ta = self.layer.ta
+        for given, own, name in ((parents, ta.parents, "parents"), (num_nodes, ta.num_nodes, "num_nodes")):
+            if given is not None and (own is None or given.data_ptr() != own.data_ptr() or given.shape != own.shape):
+                raise ValueError(f"SpeculatorStep.step: {name} differs from the layer's TreeAttention {name}; "
+                                 "build a TreeAttention / DraftLayer for the new batch")
+        self.spec.verify(draft_tokens, T, ta.parents, ta.num_nodes, stream)
         self.layer.forward(h3, e, Kp, Vp, H, stream)
         self.spec.forward(H, W_lm, stream)
         self.spec.backward(H, W_lm, dH, dW_lm, stream=stream)
@@ -608,14 +617,14 @@ class SpeculatorParams:
     over the model).  `W` / `G` are views into the buffers (the norm weights' views are fp32 slices
     of the master: the kernels read them directly); `W_lm` / `dW_lm` are the lm_head's."""
 
-    NORMS = ("we", "wh", "wpost")
+    NORMS = ("we", "wh", "wpost", "wfinal")
 
     def __init__(self, d: int, I: int, Hq: int, Hkv: int, dh: int, V: int, device):
         import torch
         qd, kd = Hq * dh, Hkv * dh
         self.shapes = [("W_lm", (V, d)), ("Wfc", (d, 3 * d)), ("Wq", (qd, 2 * d)), ("Wk", (kd, 2 * d)),
                        ("Wv", (kd, 2 * d)), ("Wo", (d, qd)), ("Wg", (I, d)), ("Wu", (I, d)), ("Wd", (d, I)),
-                       ("we", (d,)), ("wh", (d,)), ("wpost", (d,))]
+                       ("we", (d,)), ("wh", (d,)), ("wpost", (d,)), ("wfinal", (d,))]
         sizes = [int(np.prod(s)) for _, s in self.shapes]
         total = int(sum(sizes))
         self.master = torch.zeros(total, dtype=torch.float32, device=device)

@@ -191,8 +191,9 @@ int dh_splits(int64_t M, int64_t d, int64_t kb_total, int pair = 1) {
 }
 
 struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; float* ept; float* lse_part; };
-// TMA-ring scan: segments of ~24K columns (48 KB) -> M x nseg items over the 148 SMs
-int ring_nseg(int64_t V_local) { return static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(1, cdiv(V_local, 24576)))); }
+// TMA-ring scan: segments of ~32K columns (64 KB; each of the 8 warps streams 8 KB of it after
+// a warm start of ~k offers) -> M x nseg items over the 148 SMs
+int ring_nseg(int64_t V_local) { return static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(1, cdiv(V_local, 32768)))); }
 VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
   const int nseg = std::max(scan_nseg(M, V_local), ring_nseg(V_local) * scan_ring_lists());
   VerifyWs w;

@@ -32,7 +32,7 @@ constexpr int kGemmSmem = kStages * (kSmemA + kSmemB) + 1024 /*align*/ + 1024 /*
 // epilogue warp); the output itself is never stored.
 enum EpiKind : int {
   EPI_FWD_STATS = 0, EPI_BWD_DZ = 1, EPI_STORE_F32 = 2, EPI_FWD_STATS_T = 3, EPI_BWD_DZ_T = 4,
-  EPI_SUMSQ = 5, EPI_FWD_STAGE = 6
+  EPI_SUMSQ = 5, EPI_FWD_STAGE = 6, EPI_STORE_BF16 = 7
 };
 
 // F3 hyperparameters (aurora_adamw_cfg_t as fp32 scalars).  The per-step scalars (warm-up
@@ -117,6 +117,7 @@ cudaError_t launch_dw_resident(const CUtensorMap& tmA, const CUtensorMap& tmB, c
 
 // 2D bf16 tensor map (SWIZZLE_128B) over a row-major [outer, inner] matrix with row
 // stride `ld` elements; box = {box_inner, box_outer}.
+bool make_tmap_bf16_out(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld);
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_inner, uint32_t box_outer);
 

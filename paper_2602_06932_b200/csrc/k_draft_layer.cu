@@ -3,14 +3,13 @@
 //   g = h3 Wfc^T;  u = [rms(e) w_e ; rms(g) w_h];  q,k,v = u W{q,k,v}^T;  RoPE(q, k) at tree
 //   positions;  o = TreeAttention(q, [Kp; k], [Vp; v]);  y = g + o Wo^T;  z = rms(y) w_post;
 //   H = y + (silu(z Wg^T) * (z Wu^T)) Wd^T
-// Dense projections are plain library GEMMs (cuBLAS, bf16 operands, fp32 accumulation: the
-// method-specific arithmetic is the tree attention + RoPE, in k_tree_attn.cu); the norms,
-// SwiGLU and their backward passes are the kernels below.  Activations the backward needs are
+//   H_out = rms(H) w_final   (EAGLE-3's final norm before the lm_head; the lm_head path's input)
+// Dense projections run on the library's own tcgen05 GEMM engine (k_gemm.cu: TMA-fed
+// tcgen05.mma, TMEM accumulators, bf16 / fp32 TMA-store epilogues, residual adds as TMA
+// reduce-add); the norms, SwiGLU and their backward passes are the kernels below.  Activations the backward needs are
 // kept in the caller's workspace between aurora_draft_layer_fwd and aurora_draft_layer_bwd.
 // Deterministic: row-wise reductions in fixed order, norm-weight gradients by a two-stage
 // fixed-order column reduction.
-#include <cublas_v2.h>
-
 #include <cmath>
 #include <algorithm>
 #include <mutex>
@@ -117,44 +116,76 @@ __global__ void k_f2bf(const float* __restrict__ x, bf16* __restrict__ y, int64_
 
 unsigned grid_for(int64_t count) { return (unsigned)std::min<int64_t>((count + 255) / 256, 148 * 16); }
 
-// ---- cuBLAS (column-major) wrappers for row-major tensors
-cublasHandle_t handle() {
-  static cublasHandle_t h = nullptr;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  if (!h && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) h = nullptr;
-  return h;
+// ---- dense projections on the library's tcgen05 engine (k_gemm.cu), row-major tensors:
+//   C[M, N] (+)= A B^T with A bf16 [M, K] (a_mn: stored as [K, M]) and B bf16 [N, K]
+//   (b_mn: stored as [K, N]); C bf16 (TMA bulk-store epilogue) or fp32 (TMA store, or TMA
+//   reduce-add when accumulating: the residual adds).  fp32 GEMMs whose tile count leaves
+//   SMs idle split K into ordered fp32 partials (split_ws) reduced by k_splitk_reduce.
+struct Eng {
+  cudaStream_t s;
+  float* split_ws;
+  int64_t split_elems;
+};
+bool eng_gemm(const Eng& E, const bf16* A, int64_t lda, bool a_mn, const bf16* B, int64_t ldb, bool b_mn, void* C,
+              int64_t ldc, bool out_bf16, bool accumulate, int64_t M, int64_t N, int64_t K) {
+  const int pr = (M % 256 == 0 || M >= 4096) ? 2 : 1;
+  CUtensorMap ta, tb, tc;
+  bool ok = a_mn ? make_tmap_bf16(&ta, A, M, K, lda, 64, 64) : make_tmap_bf16(&ta, A, K, M, lda, 64, BM);
+  ok = ok && (b_mn ? make_tmap_bf16(&tb, B, N, K, ldb, 64, 64) : make_tmap_bf16(&tb, B, K, N, ldb, 64, BN / pr));
+  if (!ok) return false;
+  GemmArgs g{};
+  g.m_tiles = static_cast<int32_t>((M + BM * pr - 1) / (BM * pr));
+  g.n_tiles = static_cast<int32_t>((N + BN - 1) / BN);
+  g.kb_total = static_cast<int32_t>((K + BK - 1) / BK);
+  g.M = M;
+  g.N = N;
+  int splits = 1;
+  if (!out_bf16) {  // fill idle SMs with K splits when the output has few tiles
+    const int64_t tiles = static_cast<int64_t>(g.m_tiles) * g.n_tiles, slots = kNumSMs / pr;
+    if (tiles < slots && ldc == N && (M * N) % 4 == 0) {
+      splits = static_cast<int>(std::min<int64_t>({8, slots / tiles, g.kb_total}));
+      while (splits > 1 && static_cast<int64_t>(splits) * M * N > E.split_elems) --splits;
+    }
+  }
+  g.kb_per_split = (g.kb_total + splits - 1) / splits;
+  g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
+  splits = g.splits;
+  if (out_bf16) {
+    if (accumulate || !make_tmap_bf16_out(&tc, C, N, M, ldc)) return false;
+    return launch_umma_gemm(EPI_STORE_BF16, a_mn, b_mn, ta, tb, g, E.s, &tc, pr) == cudaSuccess;
+  }
+  if (splits > 1) {
+    g.out = E.split_ws;
+    g.ld_out = N;
+    g.split_stride = M * N;
+    if (!make_tmap_f32_out(&tc, E.split_ws, N, M, N, splits, M * N)) return false;
+    if (launch_umma_gemm(EPI_STORE_F32, a_mn, b_mn, ta, tb, g, E.s, &tc, pr) != cudaSuccess) return false;
+    return launch_splitk_reduce(E.split_ws, splits, M * N, static_cast<float*>(C), accumulate ? 1 : 0, E.s) ==
+           cudaSuccess;
+  }
+  g.out = static_cast<float*>(C);
+  g.ld_out = ldc;
+  g.accumulate = accumulate ? 1 : 0;
+  const bool tmc = make_tmap_f32_out(&tc, C, N, M, ldc, 1, 0);
+  return launch_umma_gemm(EPI_STORE_F32, a_mn, b_mn, ta, tb, g, E.s, tmc ? &tc : nullptr, pr) == cudaSuccess;
 }
-// Y[M,N] (+)= X[M,K] W[N,K]^T        (Y f32 or bf16)
-bool gemm_xwt(cudaStream_t s, const bf16* X, const bf16* W, void* Y, bool y_f32, int M, int N, int K, float beta) {
-  cublasHandle_t h = handle();
-  if (!h || cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return false;
-  const float alpha = 1.f;
-  return cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, N, M, K, &alpha, W, CUDA_R_16BF, K, X, CUDA_R_16BF, K, &beta, Y,
-                      y_f32 ? CUDA_R_32F : CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) ==
-         CUBLAS_STATUS_SUCCESS;
+// Y[M,N] (+)= X[M,K] W[N,K]^T          (nn.Linear forward)
+bool gemm_xwt(const Eng& E, const bf16* X, const bf16* W, void* Y, bool y_f32, int M, int N, int K, bool acc) {
+  return eng_gemm(E, X, K, false, W, K, false, Y, N, !y_f32, acc, M, N, K);
 }
-// dX[M,K] (+)= dY[M,N] W[N,K]        (dX f32 or bf16)
-bool gemm_dyw(cudaStream_t s, const bf16* dY, const bf16* W, void* dX, bool f32, int M, int N, int K, float beta) {
-  cublasHandle_t h = handle();
-  if (!h || cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return false;
-  const float alpha = 1.f;
-  return cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_N, K, M, N, &alpha, W, CUDA_R_16BF, K, dY, CUDA_R_16BF, N, &beta, dX,
-                      f32 ? CUDA_R_32F : CUDA_R_16BF, K, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) ==
-         CUBLAS_STATUS_SUCCESS;
+// dX[M,K] (+)= dY[M,N] W[N,K]          (input gradient; W read as the MN-major B operand)
+bool gemm_dyw(const Eng& E, const bf16* dY, const bf16* W, void* dX, bool f32, int M, int N, int K, bool acc) {
+  return eng_gemm(E, dY, N, false, W, K, true, dX, K, !f32, acc, M, K, N);
 }
-// dW[N,K] = dY[M,N]^T X[M,K]          (f32)
-bool gemm_dw(cudaStream_t s, const bf16* dY, const bf16* X, float* dW, int M, int N, int K) {
-  cublasHandle_t h = handle();
-  if (!h || cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return false;
-  const float alpha = 1.f, beta = 0.f;
-  return cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, K, N, M, &alpha, X, CUDA_R_16BF, K, dY, CUDA_R_16BF, N, &beta, dW,
-                      CUDA_R_32F, K, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT) == CUBLAS_STATUS_SUCCESS;
+// dW[N,K] = dY[M,N]^T X[M,K]           (weight gradient, f32; both operands MN-major, K = M)
+bool gemm_dw(const Eng& E, const bf16* dY, const bf16* X, float* dW, int M, int N, int K) {
+  return eng_gemm(E, dY, N, true, X, K, true, dW, K, false, false, N, K, M);
 }
 
 // Workspace layout (bytes), shared by fwd (writes the saved activations) and bwd.
 struct DlWs {
-  float *g, *rs_e, *rs_h, *lse, *y, *rs_p, *f1, *f2, *part, *dq;
+  float *g, *rs_e, *rs_h, *lse, *y, *rs_p, *f1, *f2, *part, *dq, *hout, *rs_f, *split;
+  int64_t split_elems;
   bf16 *u, *q, *k, *v, *o, *z, *a, *b, *m, *b1, *b2, *b3, *dkt, *dvt;
   uint8_t* ta_ws;
   size_t ta_ws_bytes;
@@ -182,6 +213,10 @@ size_t carve(const aurora_draft_layer_t* L, uint8_t* base, DlWs* w) {
   t.f2 = take<float>(p, M * wide);
   t.part = take<float>(p, (int64_t)64 * wide);
   t.dq = take<float>(p, M * qd);
+  t.hout = take<float>(p, M * d);
+  t.rs_f = take<float>(p, M);
+  t.split_elems = std::min<int64_t>(M * wide * 4, int64_t(8) * 4096 * 4096);  // split-K partials
+  t.split = take<float>(p, t.split_elems);
   t.u = take<bf16>(p, M * 2 * d);
   t.q = take<bf16>(p, M * qd);
   t.k = take<bf16>(p, M * kd);
@@ -214,8 +249,10 @@ void rms_dw(cudaStream_t s, const TX* x, int64_t ldx, const float* rstd, const f
 aurora_status_t dl_check(const aurora_draft_layer_t* L, const aurora_draft_weights_t* W) {
   if (!L || !W || L->d < 1 || L->I < 1 || L->d % 8 || L->I % 8 || !(L->eps > 0.f)) return AURORA_ERR_INVALID_ARG;
   if (L->ta.dh != 128) return AURORA_ERR_UNSUPPORTED;
-  if (!W->Wfc || !W->Wq || !W->Wk || !W->Wv || !W->Wo || !W->Wg || !W->Wu || !W->Wd || !W->we || !W->wh || !W->wpost)
+  if (!W->Wfc || !W->Wq || !W->Wk || !W->Wv || !W->Wo || !W->Wg || !W->Wu || !W->Wd || !W->we || !W->wh || !W->wpost ||
+      !W->wfinal)
     return AURORA_ERR_INVALID_ARG;
+  if (L->d % 64 || L->I % 64) return AURORA_ERR_UNSUPPORTED;  // GEMM engine: K multiple of 64 (tails unsupported)
   return AURORA_OK;
 }
 
@@ -243,24 +280,25 @@ extern "C" aurora_status_t aurora_draft_layer_fwd(const aurora_draft_layer_t* L,
   const int qd = L->ta.Hq * L->ta.dh, kd = L->ta.Hkv * L->ta.dh;
   const bf16 *Wfc = (const bf16*)W->Wfc, *Wq = (const bf16*)W->Wq, *Wk = (const bf16*)W->Wk, *Wv = (const bf16*)W->Wv;
   const bf16 *Wo = (const bf16*)W->Wo, *Wg = (const bf16*)W->Wg, *Wu = (const bf16*)W->Wu, *Wd = (const bf16*)W->Wd;
-  bool ok = gemm_xwt(s, (const bf16*)h3, Wfc, w.g, true, M, d, 3 * d, 0.f);                    // g = h3 Wfc^T
+  const Eng E{s, w.split, w.split_elems};
+  bool ok = gemm_xwt(E, (const bf16*)h3, Wfc, w.g, true, M, d, 3 * d, false);                 // g = h3 Wfc^T
   k_rms_fwd<bf16><<<M, 256, 0, s>>>((const bf16*)e, d, W->we, L->eps, d, w.u, 2 * d, w.rs_e);  // u = [rms(e) we ;
   k_rms_fwd<float><<<M, 256, 0, s>>>(w.g, d, W->wh, L->eps, d, w.u + d, 2 * d, w.rs_h);        //      rms(g) wh]
-  ok = ok && gemm_xwt(s, w.u, Wq, w.q, false, M, qd, 2 * d, 0.f) && gemm_xwt(s, w.u, Wk, w.k, false, M, kd, 2 * d, 0.f) &&
-       gemm_xwt(s, w.u, Wv, w.v, false, M, kd, 2 * d, 0.f);
+  ok = ok && gemm_xwt(E, w.u, Wq, w.q, false, M, qd, 2 * d, false) &&
+       gemm_xwt(E, w.u, Wk, w.k, false, M, kd, 2 * d, false) && gemm_xwt(E, w.u, Wv, w.v, false, M, kd, 2 * d, false);
   if (!ok) return AURORA_ERR_CUDA;
   st = aurora_tree_rope(&L->ta, w.q, 0, w.k, 0, L->theta, 0, s);
   if (st == AURORA_OK) st = aurora_tree_attn_fwd(&L->ta, w.q, w.k, w.v, Kp, Vp, w.o, w.lse, s);
   if (st != AURORA_OK) return st;
   if (cudaMemcpyAsync(w.y, w.g, (size_t)M * d * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return AURORA_ERR_CUDA;
-  ok = gemm_xwt(s, w.o, Wo, w.y, true, M, d, qd, 1.f);                                        // y = g + o Wo^T
+  ok = gemm_xwt(E, w.o, Wo, w.y, true, M, d, qd, true);                                       // y = g + o Wo^T
   k_rms_fwd<float><<<M, 256, 0, s>>>(w.y, d, W->wpost, L->eps, d, w.z, d, w.rs_p);             // z = rms(y) wpost
-  ok = ok && gemm_xwt(s, w.z, Wg, w.a, false, M, I, d, 0.f) && gemm_xwt(s, w.z, Wu, w.b, false, M, I, d, 0.f);
+  ok = ok && gemm_xwt(E, w.z, Wg, w.a, false, M, I, d, false) && gemm_xwt(E, w.z, Wu, w.b, false, M, I, d, false);
   k_swiglu_fwd<<<grid_for((int64_t)M * I), 256, 0, s>>>(w.a, w.b, w.m, (int64_t)M * I);        // m = silu(a) b
-  if (cudaMemcpyAsync(w.f1, w.y, (size_t)M * d * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return AURORA_ERR_CUDA;
-  ok = ok && gemm_xwt(s, w.m, Wd, w.f1, true, M, d, I, 1.f);                                  // H = y + m Wd^T
-  k_f2bf<<<grid_for((int64_t)M * d), 256, 0, s>>>(w.f1, (bf16*)H, (int64_t)M * d);
-  count_launch(8);
+  if (cudaMemcpyAsync(w.hout, w.y, (size_t)M * d * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  ok = ok && gemm_xwt(E, w.m, Wd, w.hout, true, M, d, I, true);                               // h = y + m Wd^T
+  k_rms_fwd<float><<<M, 256, 0, s>>>(w.hout, d, W->wfinal, L->eps, d, (bf16*)H, d, w.rs_f);    // H = rms(h) wfinal
+  count_launch(5);
   if (!ok) return AURORA_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
 }
@@ -273,7 +311,7 @@ extern "C" aurora_status_t aurora_draft_layer_bwd(const aurora_draft_layer_t* L,
   aurora_status_t st = dl_check(L, W);
   if (st != AURORA_OK) return st;
   if (!h3 || !e || !dH || !G || !dh3 || !de || !G->Wfc || !G->Wq || !G->Wk || !G->Wv || !G->Wo || !G->Wg || !G->Wu ||
-      !G->Wd || !G->we || !G->wh || !G->wpost)
+      !G->Wd || !G->we || !G->wh || !G->wpost || !G->wfinal)
     return AURORA_ERR_INVALID_ARG;
   if (!ws || ws_bytes < aurora_draft_layer_workspace_size(L)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = (cudaStream_t)stream;
@@ -284,27 +322,32 @@ extern "C" aurora_status_t aurora_draft_layer_bwd(const aurora_draft_layer_t* L,
   const bf16 *Wfc = (const bf16*)W->Wfc, *Wq = (const bf16*)W->Wq, *Wk = (const bf16*)W->Wk, *Wv = (const bf16*)W->Wv;
   const bf16 *Wo = (const bf16*)W->Wo, *Wg = (const bf16*)W->Wg, *Wu = (const bf16*)W->Wu, *Wd = (const bf16*)W->Wd;
   const int64_t MI = (int64_t)M * I, Md = (int64_t)M * d;
-  // H = y + m Wd^T
-  k_f2bf<<<grid_for(Md), 256, 0, s>>>(dH, w.b1, Md);                                           // b1 = bf16(dH)
-  bool ok = gemm_dw(s, w.b1, w.m, G->Wd, M, d, I) && gemm_dyw(s, w.b1, Wd, w.f1, true, M, d, I, 0.f);  // f1 = dm
+  const Eng E{s, w.split, w.split_elems};
+  // H = rms(h) wfinal  (dh overwrites h in place: k_rms_bwd reads a row before writing it)
+  float* dh = w.hout;
+  rms_dw<float>(s, w.hout, d, w.rs_f, dH, d, M, d, w.part, G->wfinal);
+  k_rms_bwd<float><<<M, 256, 0, s>>>(w.hout, d, W->wfinal, w.rs_f, dH, d, nullptr, 0, dh, d, d);
+  // h = y + m Wd^T
+  k_f2bf<<<grid_for(Md), 256, 0, s>>>(dh, w.b1, Md);                                            // b1 = bf16(dh)
+  bool ok = gemm_dw(E, w.b1, w.m, G->Wd, M, d, I) && gemm_dyw(E, w.b1, Wd, w.f1, true, M, d, I, false);  // f1 = dm
   k_swiglu_bwd<<<grid_for(MI), 256, 0, s>>>(w.a, w.b, w.f1, w.b2, w.b3, MI);                    // b2 = da, b3 = db
-  ok = ok && gemm_dw(s, w.b2, w.z, G->Wg, M, I, d) && gemm_dw(s, w.b3, w.z, G->Wu, M, I, d) &&
-       gemm_dyw(s, w.b2, Wg, w.f2, true, M, I, d, 0.f) && gemm_dyw(s, w.b3, Wu, w.f2, true, M, I, d, 1.f);  // f2 = dz
-  // z = rms(y) wpost ; dy = dH + rms_bwd
+  ok = ok && gemm_dw(E, w.b2, w.z, G->Wg, M, I, d) && gemm_dw(E, w.b3, w.z, G->Wu, M, I, d) &&
+       gemm_dyw(E, w.b2, Wg, w.f2, true, M, I, d, false) && gemm_dyw(E, w.b3, Wu, w.f2, true, M, I, d, true);  // f2 = dz
+  // z = rms(y) wpost ; dy = dh + rms_bwd
   rms_dw<float>(s, w.y, d, w.rs_p, w.f2, d, M, d, w.part, G->wpost);
-  k_rms_bwd<float><<<M, 256, 0, s>>>(w.y, d, W->wpost, w.rs_p, w.f2, d, dH, d, w.f1, d, d);     // f1 = dy
+  k_rms_bwd<float><<<M, 256, 0, s>>>(w.y, d, W->wpost, w.rs_p, w.f2, d, dh, d, w.f1, d, d);     // f1 = dy
   // y = g + o Wo^T
   k_f2bf<<<grid_for(Md), 256, 0, s>>>(w.f1, w.b1, Md);                                          // b1 = bf16(dy)
-  ok = ok && gemm_dw(s, w.b1, w.o, G->Wo, M, d, qd) && gemm_dyw(s, w.b1, Wo, w.b2, false, M, d, qd, 0.f);  // b2 = do
+  ok = ok && gemm_dw(E, w.b1, w.o, G->Wo, M, d, qd) && gemm_dyw(E, w.b1, Wo, w.b2, false, M, d, qd, false);  // b2 = do
   if (!ok) return AURORA_ERR_CUDA;
   st = aurora_tree_attn_bwd(&L->ta, w.q, w.k, w.v, Kp, Vp, w.o, w.lse, w.b2, w.dq, w.dkt, w.dvt, dKp, dVp, w.ta_ws,
                             w.ta_ws_bytes, s);
   if (st == AURORA_OK) st = aurora_tree_rope(&L->ta, w.dq, 1, w.dkt, 0, L->theta, 1, s);
   if (st != AURORA_OK) return st;
   k_f2bf<<<grid_for((int64_t)M * qd), 256, 0, s>>>(w.dq, w.b3, (int64_t)M * qd);                // b3 = bf16(dq)
-  ok = gemm_dw(s, w.b3, w.u, G->Wq, M, qd, 2 * d) && gemm_dw(s, w.dkt, w.u, G->Wk, M, kd, 2 * d) &&
-       gemm_dw(s, w.dvt, w.u, G->Wv, M, kd, 2 * d) && gemm_dyw(s, w.b3, Wq, w.f2, true, M, qd, 2 * d, 0.f) &&
-       gemm_dyw(s, w.dkt, Wk, w.f2, true, M, kd, 2 * d, 1.f) && gemm_dyw(s, w.dvt, Wv, w.f2, true, M, kd, 2 * d, 1.f);
+  ok = gemm_dw(E, w.b3, w.u, G->Wq, M, qd, 2 * d) && gemm_dw(E, w.dkt, w.u, G->Wk, M, kd, 2 * d) &&
+       gemm_dw(E, w.dvt, w.u, G->Wv, M, kd, 2 * d) && gemm_dyw(E, w.b3, Wq, w.f2, true, M, qd, 2 * d, false) &&
+       gemm_dyw(E, w.dkt, Wk, w.f2, true, M, kd, 2 * d, true) && gemm_dyw(E, w.dvt, Wv, w.f2, true, M, kd, 2 * d, true);
   // u = [rms(e) we ; rms(g) wh]   (f2 = du [M, 2d])
   rms_dw<bf16>(s, (const bf16*)e, d, w.rs_e, w.f2, 2 * d, M, d, w.part, G->we);
   k_rms_bwd<bf16><<<M, 256, 0, s>>>((const bf16*)e, d, W->we, w.rs_e, w.f2, 2 * d, nullptr, 0, de, d, d);
@@ -312,9 +355,9 @@ extern "C" aurora_status_t aurora_draft_layer_bwd(const aurora_draft_layer_t* L,
   k_rms_bwd<float><<<M, 256, 0, s>>>(w.g, d, W->wh, w.rs_h, w.f2 + d, 2 * d, w.f1, d, w.f1, d, d);  // f1 = dg
   // g = h3 Wfc^T
   k_f2bf<<<grid_for(Md), 256, 0, s>>>(w.f1, w.b1, Md);
-  ok = ok && gemm_dw(s, w.b1, (const bf16*)h3, G->Wfc, M, d, 3 * d) &&
-       gemm_dyw(s, w.b1, Wfc, dh3, true, M, d, 3 * d, 0.f);
-  count_launch(16);
+  ok = ok && gemm_dw(E, w.b1, (const bf16*)h3, G->Wfc, M, d, 3 * d) &&
+       gemm_dyw(E, w.b1, Wfc, dh3, true, M, d, 3 * d, false);
+  count_launch(18);
   if (!ok) return AURORA_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
 }

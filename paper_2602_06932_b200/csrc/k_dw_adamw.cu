@@ -9,10 +9,12 @@
 //   warp 0      operand TMA (dZ^T K-major 128 x 64, H MN-major half 128 x 64), 2 stages
 //   warp 1      TMEM allocation + the pair MMA issuer (leader CTA)
 //   warps 2..9  epilogue: warp w owns TMEM lane quadrant w % 4 and column half (w-2)/4
-//   warp 10     optimizer-state loader: TMA loads of 128-row x 16-column blocks of m, v and
-//               the fp32 master W (SWIZZLE_64B, 24 KB per entry) into a 6-entry ring that
-//               runs ahead of the epilogue — the bytes in flight the update needs to run at
-//               HBM speed (the round-1 version issued these loads from the epilogue warps
+//   warp 10     optimizer-state loader: TMA loads of 128-row x 32-column blocks of m, v and
+//               the fp32 master W (full 128 B lines, SWIZZLE_128B, 48 KB per entry) into a
+//               3-entry ring that runs ahead of the epilogue; all 8 epilogue warps consume an
+//               entry together (warp = TMEM lane quadrant x 16-column half), so one entry is
+//               in use and two are in flight — the bytes the update needs to run at HBM speed
+//               (the round-1 version issued these loads from the epilogue warps
 //               themselves and stalled at ~3.7 TB/s)
 // The epilogue updates each entry in place in shared memory (thread = row, conflict-free
 // 16 B accesses through the swizzle), then reads it back transposed (4 lanes per 64 B row
@@ -34,12 +36,13 @@ constexpr int kFThreads = 32 * kFWarps;
 constexpr int kFSt = 2;                               // operand stages
 constexpr int kFSB = (BN / 2) * BK * 2;               // B half per CTA and stage
 constexpr int kFStage = kSmemA + kFSB;                // 32 KB
-constexpr int kECols = 16;                            // lm_head columns per state entry
-constexpr int kEArr = BM * kECols * 4;                // 8 KB: 128 rows x 16 fp32
+constexpr int kECols = 32;                            // lm_head columns per state entry (128 B rows)
+constexpr int kEArr = BM * kECols * 4;                // 16 KB: 128 rows x 32 fp32 (SW128)
 constexpr int kEBytes = 3 * kEArr;                    // m, v, W
-constexpr int kFR = 6;                                // state ring entries
-constexpr int kWbBytes = 32 * kECols * 2;             // 1 KB bf16 staging per epilogue warp
-constexpr int kEPerTile = BN / kECols;                // 16 entries per tile (8 per column half)
+constexpr int kFR = 3;                                // state ring entries
+constexpr int kWCols = kECols / 2;                    // columns per epilogue warp and entry
+constexpr int kWbBytes = 32 * kWCols * 2;             // 1 KB bf16 staging per epilogue warp
+constexpr int kEPerTile = BN / kECols;                // 8 entries per tile, each consumed by all 8 warps
 constexpr int kRingOff = 0;
 constexpr int kStateOff = kFSt * kFStage;
 constexpr int kWbOff = kStateOff + kFR * kEBytes;
@@ -49,16 +52,16 @@ static_assert(kFSmem <= 232448, "dynamic smem per CTA");
 
 struct Maps {
   CUtensorMap A, B;           // dZ^T (K-major, box 64 x 128), H (MN-major, box 64 x 64)
-  CUtensorMap ml, vl, wl;     // fp32 [V, d] loads, box 16 x 128, SW64
+  CUtensorMap ml, vl, wl;     // fp32 [V, d] loads, box 32 x 128, SW128
 };
 
 __device__ __forceinline__ void st_cs_v4(float* p, const float4& v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
-// byte offset of (row r, 16 B chunk c) in a 64 B-row SWIZZLE_64B block
-__device__ __forceinline__ uint32_t sw64(int r, int c) {
-  return static_cast<uint32_t>(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+// byte offset of (row r, 16 B chunk c) in a 128 B-row SWIZZLE_128B block
+__device__ __forceinline__ uint32_t sw128(int r, int c) {
+  return static_cast<uint32_t>(r * 128 + ((c ^ (r & 7)) << 4));
 }
 
 __global__ void __launch_bounds__(kFThreads, 1)
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
     }
     for (int e = 0; e < kFR; ++e) {
       mbar_init(&efull_bar[e], 1);
-      mbar_init(&eempty_bar[e], kEpiWarps / 2);
+      mbar_init(&eempty_bar[e], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -174,7 +177,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         decode(u, mt, nt);
         const int row0 = (mt * 2 + static_cast<int>(rank)) * BM;
         for (int e = 0; e < kEPerTile; ++e, ++pos) {
-          const int col = nt * BN + (e & 1) * (BN / 2) + (e >> 1) * kECols;
+          const int col = nt * BN + e * kECols;
           const uint32_t slot = pos % kFR, ph = (pos / kFR) & 1;
           mbar_wait(&eempty_bar[slot], ph ^ 1);
           mbar_arrive_expect_tx(&efull_bar[slot], kEBytes);
@@ -188,7 +191,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
   } else {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quadrant this warp may read
-    const int half = (warp - 2) >> 2;    // column half of the tile
+    const int half = (warp - 2) >> 2;    // 16-column half of every entry
     const float clip = __ldg(args.sc + 0), step_size = __ldg(args.sc + 1), isb2 = __ldg(args.sc + 2);
     const float decay = __ldg(args.sc + 3), b1 = __ldg(args.sc + 4), b2 = __ldg(args.sc + 5);
     const float eps = __ldg(args.sc + 6);
@@ -202,9 +205,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      for (int k = 0; k < kEPerTile / 2; ++k) {
-        const int e = 2 * k + half;
-        const int cl = half * (BN / 2) + k * kECols;  // tile-local column
+      for (int e = 0; e < kEPerTile; ++e) {
+        const int cl = e * kECols + half * kWCols;  // tile-local column of this warp's 16
         const uint32_t pos = tile * kEPerTile + e;
         const uint32_t slot = pos % kFR, ph = (pos / kFR) & 1;
         uint32_t g[16];
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         float wnew[16];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const uint32_t o = sw64(r, c);
+          const uint32_t o = sw128(r, half * 4 + c);
           float4 m4 = lds128(base + o), v4 = lds128(base + kEArr + o), w4 = lds128(base + 2 * kEArr + o);
           float* mm = &m4.x;
           float* vv = &v4.x;
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int rr = i * 8 + (lane >> 2), cc = lane & 3;
-          const uint32_t o = sw64(q * 32 + rr, cc);
+          const uint32_t o = sw128(q * 32 + rr, half * 4 + cc);
           const float4 m4 = lds128(base + o), v4 = lds128(base + kEArr + o), w4 = lds128(base + 2 * kEArr + o);
           const int64_t grow = row0q + rr;
           if (grow < args.V) {
@@ -296,9 +298,9 @@ cudaError_t launch_dw_adamw(const void* dzT, int64_t ld_dzT, const void* H, int6
                             float* W_master, float* m, float* v, void* W_bf16, const float* sc, cudaStream_t s) {
   Maps mp;
   bool ok = make_tmap_bf16(&mp.A, dzT, M, V, ld_dzT, 64, BM) && make_tmap_bf16(&mp.B, H, d, M, d, 64, 64);
-  ok = ok && make_tmap_2d(&mp.ml, 1, m, d, V, d, kECols, BM, 64) &&
-       make_tmap_2d(&mp.vl, 1, v, d, V, d, kECols, BM, 64) &&
-       make_tmap_2d(&mp.wl, 1, W_master, d, V, d, kECols, BM, 64);
+  ok = ok && make_tmap_2d(&mp.ml, 1, m, d, V, d, kECols, BM, 128) &&
+       make_tmap_2d(&mp.vl, 1, v, d, V, d, kECols, BM, 128) &&
+       make_tmap_2d(&mp.wl, 1, W_master, d, V, d, kECols, BM, 128);
   if (!ok) return cudaErrorInvalidValue;
   DwAdamwArgs a{};
   a.m_tiles = static_cast<int32_t>((V + 2 * BM - 1) / (2 * BM));

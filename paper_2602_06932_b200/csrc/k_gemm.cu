@@ -72,7 +72,7 @@ template <int EPI, bool A_MN, int PAIR, int TBN>
 struct SmemPlan {
   static constexpr int kSB = (TBN / PAIR) * BK * 2;  // B bytes per stage in this CTA
   static constexpr int kStageBytes = kSmemA + kSB;
-  static constexpr bool kStore = EPI == EPI_STORE_F32;
+  static constexpr bool kStore = EPI == EPI_STORE_F32 || EPI == EPI_STORE_BF16;
   static constexpr int kSt = PAIR == 2 ? 6 : kStages;
   static constexpr int kRing = kSt * kStageBytes;
   static constexpr int kSlots = kStore ? 2 : 0;  // 2 KB bulk-store slots per warp
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (EPI == EPI_STORE_F32 && args.tma_store) tma_prefetch_desc(&tmC);
+    if ((EPI == EPI_STORE_F32 && args.tma_store) || EPI == EPI_STORE_BF16) tma_prefetch_desc(&tmC);
     for (int s = 0; s < kSt; ++s) {
       mbar_init(&full_bar[s], PAIR);  // leader: own expect_tx arrive + peer's remote arrive
       mbar_init(&empty_bar[s], 1);
@@ -474,6 +474,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc2 += __shfl_xor_sync(0xffffffffu, acc2, o);
         if (lane == 0) args.out[(static_cast<int64_t>(u) * PAIR + rank) * kEpiWarps + (warp - 2)] = acc2;
+      } else if constexpr (EPI == EPI_STORE_BF16) {
+        // bf16 output (F4 draft-layer projections): thread = row; each 32x32 block is packed
+        // to bf16 (64 B per row) into a 64B-swizzled 2 KB slot and bulk-stored by TMA
+        // (rows / columns outside the output are clipped by the tensor map).
+        constexpr int kSlots = Plan::kSlots;
+        uint8_t* slots = reinterpret_cast<uint8_t*>(stage_f32) + (warp - 2) * (kSlots * 2048);
+        const int row0 = mt * BM + q * 32;
+        for (int cb = cbeg; cb < cend; cb += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + cb, r);
+          uint8_t* slot = slots + (epi_chunk % kSlots) * 2048;
+          if (lane == 0) bulk_wait_read<kSlots - 1>();
+          __syncwarp();
+          tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            pk[j] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          const uint32_t sbase = smem_u32(slot) + lane * 64;
+          const uint32_t sw = (lane >> 1) & 3;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + ((c ^ sw) << 4)), "r"(pk[4 * c]),
+                         "r"(pk[4 * c + 1]), "r"(pk[4 * c + 2]), "r"(pk[4 * c + 3])
+                         : "memory");
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmC, slot, static_cast<int32_t>(col0 + cb), row0, 0);
+            bulk_commit();
+          }
+          ++epi_chunk;
+        }
       } else if (args.tma_store && !((args.dbg_epi & 4) && half == 1)) {  // EPI_STORE_F32, TMA bulk stores
         // thread = row; each 32x16 fp32 block goes to a 64B-swizzled smem slot (rows of
         // 64 B, 16 B chunk c of row r at chunk c ^ ((r >> 1) & 3): conflict-free 16 B
@@ -563,7 +598,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (EPI == EPI_STORE_F32 && args.tma_store && lane == 0) bulk_wait<0>();
+    if (((EPI == EPI_STORE_F32 && args.tma_store) || EPI == EPI_STORE_BF16) && lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -668,6 +703,11 @@ cudaError_t dispatch(int epi, bool a_mn, bool b_mn, const CUtensorMap& tmA, cons
   if (epi == EPI_FWD_STATS_T && !a_mn && !b_mn) return launch_impl<EPI_FWD_STATS_T, false, false, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_SUMSQ && !a_mn && b_mn) return launch_impl<EPI_SUMSQ, false, true, PAIR>(tmA, tmB, C, g, s);
   if (epi == EPI_BWD_DZ_T && !a_mn && !b_mn) return launch_impl<EPI_BWD_DZ_T, false, false, PAIR>(tmA, tmB, C, g, s);
+  if (epi == EPI_STORE_BF16) {
+    if (!a_mn && !b_mn) return launch_impl<EPI_STORE_BF16, false, false, PAIR>(tmA, tmB, C, g, s);
+    if (!a_mn && b_mn) return launch_impl<EPI_STORE_BF16, false, true, PAIR>(tmA, tmB, C, g, s);
+    return cudaErrorInvalidValue;
+  }
   if (epi == EPI_STORE_F32) {
     if (!a_mn && !b_mn) return launch_impl<EPI_STORE_F32, false, false, PAIR>(tmA, tmB, C, g, s);
     if (!a_mn && b_mn) return launch_impl<EPI_STORE_F32, false, true, PAIR>(tmA, tmB, C, g, s);
@@ -687,7 +727,8 @@ cudaError_t launch_umma_gemm(int epi, bool a_mn, bool b_mn, const CUtensorMap& t
     const char* e = getenv("AURORA_DBG_LSU_STORE");
     return e && e[0] == '1';
   }();
-  g.tma_store = (epi == EPI_STORE_F32 && tmC && !no_tma_store) ? 1 : 0;
+  g.tma_store = ((epi == EPI_STORE_F32 && !no_tma_store) || epi == EPI_STORE_BF16) && tmC ? 1 : 0;
+  if (epi == EPI_STORE_BF16 && !tmC) return cudaErrorInvalidValue;
   static const int dbg_epi = [] {
     const char* e = getenv("AURORA_DBG_EPI");
     return e ? atoi(e) : 0;
@@ -744,6 +785,21 @@ bool make_tmap_bf16_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// 3D bf16 output map [1][outer][inner], box {32, 32, 1}, SWIZZLE_64B (EPI_STORE_BF16).
+bool make_tmap_bf16_out(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t ld) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (ld * 2) % 16) return false;
+  cuuint64_t dims[3] = {inner, outer, 1};
+  cuuint64_t strides[2] = {ld * 2, ld * outer * 2};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -54,6 +54,7 @@ struct TaParams {
   const int32_t *prefix_off, *parents, *num_nodes;
   uint32_t* status;
   int R, N, N1, Hq, Hkv, G, Gc, max_prefix;
+  int prefix_total;  // rows of Kp / Vp; offsets beyond it are malformed
   float scale, c2;  // c2 = scale * log2(e)
 };
 
@@ -97,13 +98,20 @@ __device__ __forceinline__ uint4 lds_u4(uint32_t a) {
   return v;
 }
 
-// Prefix extent of request r (clamped to max_prefix; a violation is flagged by the caller).
+// Prefix extent of request r: clamped to max_prefix; offsets outside [0, prefix_total] or
+// decreasing make the request's prefix empty (its K/V are never read or written).  Either
+// violation sets the RANGE bit when `flag`.
 __device__ __forceinline__ void prefix_of(const TaParams& p, int r, int& p0, int& Pr, bool flag) {
   p0 = p.prefix_off[r];
-  int len = p.prefix_off[r + 1] - p0;
-  if (len < 0 || len > p.max_prefix) {
+  const int p1 = p.prefix_off[r + 1];
+  int len = p1 - p0;
+  if (p0 < 0 || len < 0 || p1 > p.prefix_total) {
     if (flag && p.status) atomicOr(p.status, (uint32_t)AURORA_STATUS_RANGE);
-    len = len < 0 ? 0 : p.max_prefix;
+    p0 = 0;
+    len = 0;
+  } else if (len > p.max_prefix) {
+    if (flag && p.status) atomicOr(p.status, (uint32_t)AURORA_STATUS_RANGE);
+    len = p.max_prefix;
   }
   Pr = len;
 }
@@ -1220,7 +1228,8 @@ __global__ void __launch_bounds__(128) k_ta_rope(TaParams p, TQ* __restrict__ Q,
   __shared__ int s_pos;
   const int row = blockIdx.x, r = row / p.N1, s = row - r * p.N1;
   if (threadIdx.x == 0) {
-    const int Pr = p.prefix_off[r + 1] - p.prefix_off[r];
+    int p0, Pr;
+    prefix_of(p, r, p0, Pr, false);  // the same clamped extent the attention kernels use
     const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
     int pos = -1;
     if (nn >= 0 && nn <= p.N) {
@@ -1299,6 +1308,7 @@ TaParams ta_params(const aurora_tree_attn_t* ta, TaLaunch& L) {
   p.Hkv = ta->Hkv;
   p.G = ta->Hq / ta->Hkv;
   p.max_prefix = ta->max_prefix;
+  p.prefix_total = static_cast<int>(std::min<int64_t>(ta->prefix_total, INT32_MAX));
   p.scale = ta->scale > 0.f ? ta->scale : 1.f / sqrtf((float)D);
   p.c2 = p.scale * kLog2e;
   p.prefix_off = ta->prefix_off;

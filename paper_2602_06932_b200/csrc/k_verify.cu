@@ -341,6 +341,8 @@ __global__ void __launch_bounds__(32 * (kRingConsumers + 1), 1) k_target_scan_ri
     const int64_t nvec = c1 > c0 ? (c1 - c0) >> 3 : 0;
     WarpList L;
     L.init(k);
+    float floor = -INFINITY;
+    bool warm = true;
     for (int64_t v0 = 0; v0 < nvec; v0 += kRingStage / 16) {
       const int nv = static_cast<int>(min(static_cast<int64_t>(kRingStage / 16), nvec - v0));
       mbar_wait(&full[slot], ph);
@@ -354,8 +356,13 @@ __global__ void __launch_bounds__(32 * (kRingConsumers + 1), 1) k_target_scan_ri
                        : "r"(sbase + vi * 16));
           bad |= nonfinite8(w);
         }
-        const bool h = vi < nv && max8(w) >= L.thr_v;
-        if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, w, c0 + (v0 + vi) * 8, -INFINITY);
+        const float gm = vi < nv ? max8(w) : -INFINITY;
+        if (warm) {  // warm start: the k-th largest lane maximum (distinct elements) bounds the
+          warm = false;  // k-th best element from below, so the first batch offers ~k values
+          floor = warp_kth_largest(gm, k);
+        }
+        const bool h = vi < nv && gm >= fmaxf(floor, L.thr_v);
+        if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, w, c0 + (v0 + vi) * 8, floor);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(32 * (kRingConsumers + 1), 1) k_target_scan_ri
         bad |= static_cast<uint32_t>((b16 & 0x7FFFu) >= 0x7F80u);
         v = __uint_as_float(b16 << 16);
       }
-      uint32_t hit = __ballot_sync(0xffffffffu, col < c1 && L.admits(v, static_cast<int32_t>(col)));
+      uint32_t hit = __ballot_sync(0xffffffffu, col < c1 && v >= floor && L.admits(v, static_cast<int32_t>(col)));
       while (hit) {
         const int s2 = __ffs(hit) - 1;
         hit &= hit - 1;

@@ -147,7 +147,7 @@ def test_draft_layer_host_validation_without_gpu(L):
     """F4 draft layer: bad configurations and missing buffers return before any CUDA call."""
     ta = A.aurora_tree_attn_t(R=4, N=5, Hq=32, Hkv=8, dh=128, max_prefix=100, prefix_total=300, prefix_off=16)
     cfg = A.aurora_draft_layer_t(ta, 4096, 14336, 500000.0, 1e-6)
-    W = A.aurora_draft_weights_t(*([16] * 11))
+    W = A.aurora_draft_weights_t(*([16] * 12))
     need = L.aurora_draft_layer_workspace_size(C.byref(cfg))
     assert need > 24 * 4096 * 4
     f = lambda c, w=W, ws=need, h=16: L.aurora_draft_layer_fwd(C.byref(c), C.byref(w), h, 16, 16, 16, 16, 16, ws, None)
@@ -155,13 +155,13 @@ def test_draft_layer_host_validation_without_gpu(L):
     assert f(A.aurora_draft_layer_t(ta, 4096, 14336, 5e5, 0.0)) == 1                                    # eps
     assert f(A.aurora_draft_layer_t(A.aurora_tree_attn_t(R=4, N=5, Hq=32, Hkv=8, dh=64, prefix_off=16), 4096,
                                     14336, 5e5, 1e-6)) == 5                                             # dh
-    assert f(cfg, w=A.aurora_draft_weights_t(*([16] * 10 + [None]))) == 1                              # w_post
+    assert f(cfg, w=A.aurora_draft_weights_t(*([16] * 11 + [None]))) == 1                              # w_final
     assert f(cfg, h=None) == 1
     assert f(cfg, ws=need - 1) == 6
-    G = A.aurora_draft_grads_t(*([16] * 11))
+    G = A.aurora_draft_grads_t(*([16] * 12))
     b = lambda g: L.aurora_draft_layer_bwd(C.byref(cfg), C.byref(W), 16, 16, 16, 16, 16, C.byref(g), 16, 16, 16, 16,
                                            16, need, None)
-    assert b(A.aurora_draft_grads_t(*([16] * 10 + [None]))) == 1
+    assert b(A.aurora_draft_grads_t(*([16] * 11 + [None]))) == 1
 
 
 def test_speculator_params_layout():
@@ -180,7 +180,7 @@ def test_speculator_params_layout():
         assert st == pos
         pos += sizes[st]
     assert pos == total
-    for n in ("we", "wh", "wpost"):
+    for n in ("we", "wh", "wpost", "wfinal"):
         assert sp.W[n].dtype == torch.float32 and sp.W[n].data_ptr() == sp.M[n].data_ptr()
     for n in ("Wfc", "Wq", "Wd"):
         assert sp.W[n].dtype == torch.bfloat16 and sp.W[n].is_contiguous()

@@ -24,7 +24,7 @@ def _case(seed=0):
     n = lambda *s, sc=1.0: rng.standard_normal(s) * sc
     P = dict(Wfc=n(d, 3 * d, sc=0.2), we=1 + n(d, sc=0.1), wh=1 + n(d, sc=0.1), Wq=n(Hq * dh, 2 * d, sc=0.2),
              Wk=n(Hkv * dh, 2 * d, sc=0.2), Wv=n(Hkv * dh, 2 * d, sc=0.2), Wo=n(d, Hq * dh, sc=0.2),
-             wpost=1 + n(d, sc=0.1), Wg=n(I, d, sc=0.2), Wu=n(I, d, sc=0.2), Wd=n(d, I, sc=0.2))
+             wpost=1 + n(d, sc=0.1), wfinal=1 + n(d, sc=0.1), Wg=n(I, d, sc=0.2), Wu=n(I, d, sc=0.2), Wd=n(d, I, sc=0.2))
     X = dict(h3=n(R, N + 1, 3 * d), e=n(R, N + 1, d), Kp=n(sum(lens), Hkv, dh), Vp=n(sum(lens), Hkv, dh),
              prefix_off=off, parents=parents, num_nodes=num_nodes)
     cfg = dict(Hq=Hq, Hkv=Hkv, dh=dh, theta=10000.0, eps=1e-6)
@@ -89,8 +89,8 @@ def _torch_layer(P, X, cfg):
     of = torch.stack(outs)
     y = g + of @ T["Wo"].T
     z = rms(y, T["wpost"])
-    H = y + (F.silu(z @ T["Wg"].T) * (z @ T["Wu"].T)) @ T["Wd"].T
-    return H, T
+    h = y + (F.silu(z @ T["Wg"].T) * (z @ T["Wu"].T)) @ T["Wd"].T
+    return rms(h, T["wfinal"]), T
 
 
 def test_draft_layer_matches_torch_autograd():
@@ -110,7 +110,8 @@ def test_draft_layer_finite_differences():
     G = DL.layer_bwd(P, X, cfg, S, dH)
     rng = np.random.default_rng(9)
     eps = 1e-6
-    for name, src in [("Wfc", P), ("Wq", P), ("Wk", P), ("Wd", P), ("wh", P), ("wpost", P), ("h3", X), ("Kp", X)]:
+    for name, src in [("Wfc", P), ("Wq", P), ("Wk", P), ("Wd", P), ("wh", P), ("wpost", P), ("wfinal", P), ("h3", X),
+                      ("Kp", X)]:
         for _ in range(3):
             idx = tuple(int(rng.integers(0, s)) for s in src[name].shape)
             vals = []

@@ -35,9 +35,9 @@ def _case(seed=7, chain=False):
     P = dict(Wfc=_bf_round(n(d, 3 * d, k=sc(3 * d))), we=1 + n(d, k=0.1), wh=1 + n(d, k=0.1),
              Wq=_bf_round(n(Hq * dh, 2 * d, k=sc(2 * d))), Wk=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))),
              Wv=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))), Wo=_bf_round(n(d, Hq * dh, k=sc(Hq * dh))),
-             wpost=1 + n(d, k=0.1), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
+             wpost=1 + n(d, k=0.1), wfinal=1 + n(d, k=0.1), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
              Wd=_bf_round(n(d, I, k=sc(I))))
-    for k in ("we", "wh", "wpost"):
+    for k in ("we", "wh", "wpost", "wfinal"):
         P[k] = P[k].astype(np.float32).astype(np.float64)
     X = dict(h3=_bf_round(n(R, N + 1, 3 * d)), e=_bf_round(n(R, N + 1, d)), Kp=_bf_round(n(int(lens.sum()), Hkv, dh)),
              Vp=_bf_round(n(int(lens.sum()), Hkv, dh)), prefix_off=off, parents=parents, num_nodes=num_nodes)
@@ -55,7 +55,7 @@ def _run_layer(P, X, cfg, dH, reps=1):
     dev = "cuda"
     bf = lambda x: torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16).to(dev).contiguous()
     f32 = lambda x: torch.tensor(np.asarray(x, np.float32)).to(dev).contiguous()
-    W = {k: (f32(v) if k in ("we", "wh", "wpost") else bf(v)) for k, v in P.items()}
+    W = {k: (f32(v) if k in ("we", "wh", "wpost", "wfinal") else bf(v)) for k, v in P.items()}
     R, N, d, I = cfg["R"], cfg["N"], cfg["d"], cfg["I"]
     M = R * (N + 1)
     poff = torch.tensor(X["prefix_off"], dtype=torch.int32, device=dev)
@@ -125,7 +125,7 @@ def test_whole_speculator_step_parity():
     P = dict(Wfc=_bf_round(n(d, 3 * d, k=sc(3 * d))), we=np.ones(d), wh=np.ones(d),
              Wq=_bf_round(n(Hq * dh, 2 * d, k=sc(2 * d))), Wk=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))),
              Wv=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))), Wo=_bf_round(n(d, Hq * dh, k=sc(Hq * dh))),
-             wpost=np.ones(d), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
+             wpost=np.ones(d), wfinal=np.ones(d), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
              Wd=_bf_round(n(d, I, k=sc(I))))
     X = dict(h3=_bf_round(n(R, N + 1, 3 * d)), e=_bf_round(n(R, N + 1, d)), Kp=_bf_round(n(int(lens.sum()), Hkv, dh)),
              Vp=_bf_round(n(int(lens.sum()), Hkv, dh)), prefix_off=off, parents=tr["parents"], num_nodes=tr["num_nodes"])
@@ -144,7 +144,7 @@ def test_whole_speculator_step_parity():
     bf = lambda x: torch.tensor(np.asarray(x, np.float32)).to(torch.bfloat16).to(dev).contiguous()
     f32 = lambda x: torch.tensor(np.asarray(x, np.float32)).to(dev).contiguous()
     bits = lambda b: torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).view(torch.bfloat16).to(dev)
-    W = {k: (f32(v) if k in ("we", "wh", "wpost") else bf(v)) for k, v in P.items()}
+    W = {k: (f32(v) if k in ("we", "wh", "wpost", "wfinal") else bf(v)) for k, v in P.items()}
     par = torch.from_numpy(tr["parents"]).to(dev)
     ta = A.TreeAttention(R, N, Hq, Hkv, dh, torch.tensor(off, dtype=torch.int32, device=dev), int(lens.max()),
                          parents=par)
@@ -165,6 +165,13 @@ def test_whole_speculator_step_parity():
     torch.cuda.synchronize()
     assert int(spec.status.item()) == 0 and int(ta.status.item()) == 0
     assert np.array_equal(spec.accept_len.cpu().numpy(), lab["accept_len"])
+    # the layer's H (bf16) against the oracle's f64 H, then the loss at the 1e-3 bar against the
+    # oracle evaluated on the H the GPU layer produced (the lm_head stage's own inputs); the chain
+    # loss against the all-f64 oracle differs by the bf16 rounding of H
+    H_gpu = oracle.bf16_bits_to_f64(H.view(torch.int16).cpu().numpy().view(np.uint16))
+    assert _rel(H_gpu, Hr.reshape(M, d)) <= 2e-2
+    fw_h = oracle.loss_fwd(H_gpu, tr["W_bits"], tg)
+    assert abs(float(loss.item()) - fw_h["loss"]) <= 1e-3 * abs(fw_h["loss"])
     assert abs(float(loss.item()) - fw["loss"]) <= 5e-3 * abs(fw["loss"])
     assert _rel(dW_lm.cpu().numpy(), bw["dW"]) <= 2e-2
     assert _rel(dH.cpu().numpy(), bw["dH"]) <= 2e-2
@@ -179,10 +186,10 @@ def test_whole_speculator_step_parity():
 
 def test_whole_step_with_adamw_over_all_params():
     """F3 over the whole speculator: lm_head + draft-layer parameters in one flat master
-    (SpeculatorParams), one AdamW step with one global norm after SpeculatorStep.  Against the
-    oracle chain's gradients -> oracle.adamw_step: the global norm within 1e-2, and the first-step
-    update (= lr * sign(g) up to eps) agrees on >= 99 % of the elements outside the smallest
-    decile of |g| (tiny gradients may flip sign under bf16 rounding)."""
+    (SpeculatorParams), one AdamW step with one global norm after SpeculatorStep.  (1) The flat
+    gradient against the oracle chain's, per parameter within 2e-2 relative Frobenius error and the
+    global norm within 1e-2; (2) the optimizer arithmetic: the GPU update equals oracle.adamw_step
+    applied to the GPU's own gradient buffer (fp32 vs f64, rtol 2e-6)."""
     import oracle
     from paper_2602_06932_b200 import aurora as A
     tr = tracegen.gen_trace("small_tree")
@@ -198,7 +205,7 @@ def test_whole_step_with_adamw_over_all_params():
     P = dict(Wfc=_bf_round(n(d, 3 * d, k=sc(3 * d))), we=np.ones(d), wh=np.ones(d),
              Wq=_bf_round(n(Hq * dh, 2 * d, k=sc(2 * d))), Wk=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))),
              Wv=_bf_round(n(Hkv * dh, 2 * d, k=sc(2 * d))), Wo=_bf_round(n(d, Hq * dh, k=sc(Hq * dh))),
-             wpost=np.ones(d), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
+             wpost=np.ones(d), wfinal=np.ones(d), Wg=_bf_round(n(I, d, k=sc(d))), Wu=_bf_round(n(I, d, k=sc(d))),
              Wd=_bf_round(n(d, I, k=sc(I))))
     X = dict(h3=_bf_round(n(R, N + 1, 3 * d)), e=_bf_round(n(R, N + 1, d)), Kp=_bf_round(n(int(lens.sum()), Hkv, dh)),
              Vp=_bf_round(n(int(lens.sum()), Hkv, dh)), prefix_off=off, parents=tr["parents"], num_nodes=tr["num_nodes"])
@@ -213,7 +220,7 @@ def test_whole_step_with_adamw_over_all_params():
     fw = oracle.loss_fwd(Hr.reshape(M, d), tr["W_bits"], tg)
     bw = oracle.loss_bwd(Hr.reshape(M, d), tr["W_bits"], tg, fw["lse"])
     Gr = DL.layer_bwd(P, X, cfg, S, bw["dH"].reshape(R, N + 1, d))
-    order = ["Wfc", "Wq", "Wk", "Wv", "Wo", "Wg", "Wu", "Wd", "we", "wh", "wpost"]
+    order = ["Wfc", "Wq", "Wk", "Wv", "Wo", "Wg", "Wu", "Wd", "we", "wh", "wpost", "wfinal"]
     w0 = np.concatenate([W_lm64.ravel()] + [np.asarray(P[k], np.float32).astype(np.float64).ravel() for k in order])
     g64 = np.concatenate([bw["dW"].ravel()] + [Gr[k].ravel() for k in order])
     lr = 1e-3
@@ -237,14 +244,40 @@ def test_whole_step_with_adamw_over_all_params():
     dKp, dVp = torch.empty_like(Kp), torch.empty_like(Vp)
     step.step(torch.from_numpy(tr["draft_tokens"]).to(dev), bits(tr["T_bits"]), h3, e, Kp, Vp, sp.W_lm, H, dH,
               sp.dW_lm, sp.G, dh3, de, dKp, dVp, parents=par)
+    torch.cuda.synchronize()
+    g_gpu = sp.grad.cpu().numpy().astype(np.float64)
+    w_before = sp.master.cpu().numpy().astype(np.float64)
+    o = 0
+    for name, gref in [("W_lm", bw["dW"])] + [(k, Gr[k]) for k in order]:
+        nel = gref.size
+        assert _rel(g_gpu[o:o + nel], gref.ravel()) <= 2e-2, name
+        o += nel
     opt = sp.adamw(lr=lr, warmup_steps=0)
     sp.optimizer_step(opt)
     torch.cuda.synchronize()
     assert abs(float(opt.grad_norm.item()) - norm) <= 1e-2 * norm
-    dw_gpu = sp.master.cpu().numpy().astype(np.float64) - w0.astype(np.float32).astype(np.float64)
-    dw_ref = w1 - w0
-    big = np.abs(g64) > np.quantile(np.abs(g64), 0.1)
-    agree = np.mean(np.sign(dw_gpu[big]) == np.sign(dw_ref[big]))
-    assert agree >= 0.99, agree
+    f32 = lambda x: float(np.float32(x))
+    w_ref, _, _, norm_gpu = oracle.adamw_step(w_before, np.zeros_like(w0), np.zeros_like(w0), g_gpu, 1, f32(lr),
+                                              beta1=f32(0.9), beta2=f32(0.999), eps=f32(1e-8), warmup_steps=0)
+    assert abs(float(opt.grad_norm.item()) - norm_gpu) <= 2e-5 * norm_gpu
+    np.testing.assert_allclose(sp.master.cpu().numpy(), w_ref, rtol=2e-6, atol=1e-9)
     # the bf16 copy the GEMMs read was refreshed from the updated master
     np.testing.assert_allclose(sp.bf.float().cpu().numpy(), sp.master.cpu().numpy(), rtol=2 ** -8, atol=1e-30)
+
+
+def test_speculator_step_rejects_a_different_tree():
+    """verification must follow the tree the layer's TreeAttention was built with."""
+    from paper_2602_06932_b200 import aurora as A
+    dev = "cuda"
+    R, N, d, I, Hq, Hkv, dh, V = 2, 4, 256, 256, 2, 1, 128, 1000
+    par = torch.tensor([[-1, 0, 1, 2], [-1, 0, 0, 1]], dtype=torch.int32, device=dev)
+    off = torch.tensor([0, 5, 9], dtype=torch.int32, device=dev)
+    ta = A.TreeAttention(R, N, Hq, Hkv, dh, off, 5, parents=par)
+    bf = lambda *s: torch.zeros(*s, dtype=torch.bfloat16, device=dev)
+    W = dict(Wfc=bf(d, 3 * d), Wq=bf(Hq * dh, 2 * d), Wk=bf(Hkv * dh, 2 * d), Wv=bf(Hkv * dh, 2 * d), Wo=bf(d, Hq * dh),
+             Wg=bf(I, d), Wu=bf(I, d), Wd=bf(d, I), **{k: torch.ones(d, device=dev) for k in ("we", "wh", "wpost", "wfinal")})
+    step = A.SpeculatorStep(A.SpecTrainStep(R, N, d, V), A.DraftLayer(ta, d, I, W))
+    other = par.clone()
+    with pytest.raises(ValueError):
+        step.step(None, None, None, None, None, None, None, None, None, None, None, None, None, None, None,
+                  parents=other)

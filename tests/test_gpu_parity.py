@@ -630,7 +630,9 @@ def test_staged_and_recompute_backward_agree(option):
     a = _run_gpu(tr)
     option("fwd_stage", 0)
     b = _run_gpu(tr)
-    assert torch.equal(a["st"].loss, b["st"].loss)
+    # the staged fwd takes an exact per-(row, tile half) max before the exp sums, the
+    # recompute path an online one: same loss up to fp32 summation order
+    assert abs(float(a["st"].loss.item()) - float(b["st"].loss.item())) <= 1e-6 * abs(float(b["st"].loss.item()))
     assert _rfro(a["dW"].cpu().numpy(), b["dW"].cpu().numpy()) <= 5e-3
     assert _rfro(a["dH"].cpu().numpy(), b["dH"].cpu().numpy()) <= 5e-3
 

@@ -190,3 +190,43 @@ def test_tree_rope_parity(name, theta):
     torch.cuda.synchronize()
     np.testing.assert_allclose(Qf.cpu().numpy(), q64, rtol=1e-5, atol=2e-5)
     np.testing.assert_allclose(Ktf.cpu().numpy(), k64, rtol=1e-5, atol=2e-5)
+
+
+def test_malformed_prefix_offsets_flag_range_without_oob():
+    """prefix_off entries outside [0, prefix_total] (or decreasing) set the RANGE
+    bit and make that request's prefix empty — Kp/Vp are never read or written out of bounds
+    (the guard bands around them stay untouched) and every output stays finite."""
+    from paper_2602_06932_b200 import aurora as A
+    inp = tracegen.gen_tree_attn("ta_small")
+    c = inp["cfg"]
+    R, N1 = len(inp["requests"]), c.N + 1
+    off = inp["prefix_off"].astype(np.int32).copy()
+    total = int(off[-1])
+    bad = off.copy()
+    bad[2] = total + 500                      # request 1 ends beyond Kp, request 2 starts there
+    dev = "cuda"
+    t = {k: _bf(inp[k + "_bits"]) for k in ["Q", "Kt", "Vt", "dO"]}
+    guard = 4096
+    Kp_all = torch.zeros(total + 2 * guard, c.Hkv, c.dh, dtype=torch.bfloat16, device=dev)
+    Vp_all = torch.zeros_like(Kp_all)
+    Kp_all[guard:guard + total] = _bf(inp["Kp_bits"])
+    Vp_all[guard:guard + total] = _bf(inp["Vp_bits"])
+    Kp, Vp = Kp_all[guard:guard + total], Vp_all[guard:guard + total]
+    dKp_all = torch.full_like(Kp_all, 7.0)
+    dVp_all = torch.full_like(Kp_all, 7.0)
+    par = None if inp["parents"] is None else torch.from_numpy(inp["parents"].astype(np.int32)).to(dev)
+    nn = None if inp["num_nodes"] is None else torch.from_numpy(inp["num_nodes"].astype(np.int32)).to(dev)
+    ta = A.TreeAttention(R, c.N, c.Hq, c.Hkv, c.dh, torch.from_numpy(bad).to(dev), int(np.max(np.diff(off))),
+                         parents=par, num_nodes=nn, prefix_total=total)
+    O = torch.empty_like(t["Q"])
+    lse = torch.empty(R, N1, c.Hq, dtype=torch.float32, device=dev)
+    dQ = torch.empty(t["Q"].shape, dtype=torch.float32, device=dev)
+    dKt, dVt = torch.empty_like(t["Kt"]), torch.empty_like(t["Vt"])
+    ta.forward(t["Q"], t["Kt"], t["Vt"], Kp, Vp, O, lse)
+    ta.backward(t["Q"], t["Kt"], t["Vt"], Kp, Vp, O, lse, t["dO"], dQ, dKt, dVt, dKp_all[guard:guard + total],
+                dVp_all[guard:guard + total])
+    torch.cuda.synchronize()
+    assert int(ta.status.item()) & A.STATUS_RANGE
+    assert torch.isfinite(O.float()).all() and torch.isfinite(dQ).all()
+    for g in (dKp_all, dVp_all):
+        assert bool((g[:guard].float() == 7.0).all()) and bool((g[guard + total:].float() == 7.0).all())
