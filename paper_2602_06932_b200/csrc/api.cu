@@ -118,7 +118,7 @@ struct Options {
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
     if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
-    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = atoi(e) ? 1 : 0;
+    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = std::min(2, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_TREE_BWD_SPLIT")) tree_bwd_split = atoi(e) ? 1 : 0;
   }
 };
@@ -191,11 +191,15 @@ int dh_splits(int64_t M, int64_t d, int64_t kb_total, int pair = 1) {
 }
 
 struct VerifyWs { float* cand_val; int32_t* cand_idx; float* top_val; int32_t* top_idx; float* ept; float* lse_part; };
-// TMA-ring scan: segments of ~32K columns (64 KB; each of the 8 warps streams 8 KB of it after
-// a warm start of ~k offers) -> M x nseg items over the 148 SMs
-int ring_nseg(int64_t V_local) { return static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(1, cdiv(V_local, 32768)))); }
+// TMA-ring scan: one warp per (row, segment) item; enough items for 2 per warp slot of the grid
+// (148 x 8 warps), segments >= 16K columns (one top-k list per segment), <= 32 per row
+int ring_nseg(int64_t M, int64_t V_local) {
+  int64_t nseg = cdiv(2 * kNumSMs * 8, std::max<int64_t>(M, 1));
+  nseg = std::min<int64_t>(nseg, std::max<int64_t>(1, V_local / 16384));
+  return static_cast<int>(std::min<int64_t>(std::max<int64_t>(nseg, 1), 32));
+}
 VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
-  const int nseg = std::max(scan_nseg(M, V_local), ring_nseg(V_local) * scan_ring_lists());
+  const int nseg = std::max(scan_nseg(M, V_local), ring_nseg(M, V_local) * scan_ring_lists());
   VerifyWs w;
   w.ept = c.take<float>(M);
   w.lse_part = c.take<float>(M * 3);
@@ -548,7 +552,7 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
-  if (std::strcmp(name, "tree_fwd_tc") == 0 && (value == 0 || value == 1)) {
+  if (std::strcmp(name, "tree_fwd_tc") == 0 && value >= 0 && value <= 2) {
     o.tree_fwd_tc = static_cast<int>(value);
     return AURORA_OK;
   }
@@ -709,7 +713,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   p.R = t->R;
   p.N = t->N;
   p.k_max = k_max;
-  p.nseg = ring_nseg(t->V_local);
+  p.nseg = ring_nseg(M, t->V_local);
   p.seg_len = rup(cdiv(t->V_local, p.nseg), 8);
   const bool ring = opts().scan_ring && scan_ring_ok(p);
   if (!ring) {

@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const uint32_t o = sw128(q * 32 + rr, half * 4 + cc);
           const float4 m4 = lds128(base + o), v4 = lds128(base + kEArr + o), w4 = lds128(base + 2 * kEArr + o);
           const int64_t grow = row0q + rr;
-          if (grow < args.V) {
+          if (grow < args.V && col < args.d) {  // d % 64 == 0: an entry is wholly in or out
             const int64_t g = grow * args.d + col + cc * 4;
             st_cs_v4(args.m + g, m4);
             st_cs_v4(args.v + g, v4);
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
           const int rr = i * 16 + (lane >> 1), hh = lane & 1;
           const float4 b4 = lds128(smem_u32(wb_stage) + rr * 32 + hh * 16);
           const int64_t grow = row0q + rr;
-          if (grow < args.V) st_cs_v4(reinterpret_cast<float*>(args.wb + grow * args.d + col + hh * 8), b4);
+          if (grow < args.V && col < args.d) st_cs_v4(reinterpret_cast<float*>(args.wb + grow * args.d + col + hh * 8), b4);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&eempty_bar[slot]);

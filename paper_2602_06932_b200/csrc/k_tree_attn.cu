@@ -1216,6 +1216,313 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_ta_fwd_tc(const __grid_consta
 }
 
 
+// ------------------------------------------------------------------------------ tcgen05 forward, one pass
+// k_ta_fwd_tc2: one pass over the key tiles with an online softmax and lazy O rescaling, two
+// work items in flight per SM.  The CTA holds two independent groups of 6 warps (group g = warps
+// 6g .. 6g+5): a TMA producer (Q, then K and V tiles of 64 keys through two 2-stage rings), an MMA
+// issuer (S = Q K^T into one of two 64-column TMEM buffers, O += P V into a 128-column TMEM
+// accumulator) and 4 softmax warps (thread = query row = TMEM lane).  Per tile the softmax thread
+// takes the row max; only when it exceeds the running max by more than 2^8 (log2 domain) does it
+// rescale O in TMEM (wait for the previous P V, tcgen05.ld / scale / tcgen05.st) — otherwise P is
+// computed against the stale max (values <= 256, exact in fp32, fine in bf16).  P goes to shared
+// memory as the K-major A operand.  While one group runs its softmax, the tensor core works on the
+// other group's S / P V, so the MMA <-> softmax round trips of the single-item kernel (k_ta_fwd_tc,
+// two passes) overlap.  Work item = (request, KV head) with its G (N+1) <= 128 query rows.
+constexpr int kT2NK = 64;
+constexpr int kT2Threads = 384;
+constexpr int kT2Slot = kT2NK * 128 * 2;            // 16 KB: K tile (2 K-major atoms) or V tile (2 MN slices)
+constexpr int kT2OffK = 32768;                      // after Q (2 atoms of 128 rows x 128 B)
+constexpr int kT2OffV = kT2OffK + 2 * kT2Slot;
+constexpr int kT2OffP = kT2OffV + 2 * kT2Slot;
+constexpr int kT2Grp = kT2OffP + 128 * kT2NK * 2;   // 112 KB per group
+constexpr int kT2OffBar = 2 * kT2Grp;
+constexpr size_t kSmemT2 = kT2OffBar + 1024 + 1024;
+
+__global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_constant__ TaTcMaps maps, TaParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / 6, role = warp - grp * 6;
+  uint8_t* gs = smem + grp * kT2Grp;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kT2OffBar);
+  uint64_t* gb = bars + grp * 24;
+  uint64_t* q_full = gb + 0;
+  uint64_t* q_free = gb + 1;
+  uint64_t* k_full = gb + 2;   // [2]
+  uint64_t* k_empty = gb + 4;  // [2]
+  uint64_t* v_full = gb + 6;   // [2]
+  uint64_t* v_empty = gb + 8;  // [2]
+  uint64_t* s_full = gb + 10;  // [2]
+  uint64_t* s_free = gb + 12;  // [2]
+  uint64_t* p_full = gb + 14;
+  uint64_t* p_free = gb + 15;
+  uint64_t* o_ready = gb + 16;
+  uint64_t* o_done = gb + 17;
+  uint64_t* o_free = gb + 18;
+  uint64_t* anc = bars + 48 + grp * 40;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 128);
+  const int G = p.G, N1 = p.N1;
+  const int nwork = p.R * p.Hkv;
+
+  if (threadIdx.x == 0) {
+    for (int g2 = 0; g2 < 2; ++g2) {
+      uint64_t* b = bars + g2 * 24;
+      for (int k = 0; k < 10; ++k) mbar_init(&b[k], 1);   // q_full..v_empty
+      for (int k = 10; k < 12; ++k) mbar_init(&b[k], 1);  // s_full
+      for (int k = 12; k < 14; ++k) mbar_init(&b[k], 128);  // s_free
+      mbar_init(&b[14], 128);  // p_full
+      mbar_init(&b[15], 1);    // p_free
+      mbar_init(&b[16], 1);    // o_ready
+      mbar_init(&b[17], 1);    // o_done
+      mbar_init(&b[18], 128);  // o_free
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder + grp * 256;  // S0 +0, S1 +64, O +128
+  const int wstep = 2 * gridDim.x;
+
+  if (role == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      if (grp == 0) {
+        tma_prefetch_desc(&maps.Q);
+        tma_prefetch_desc(&maps.Kp);
+        tma_prefetch_desc(&maps.Vp);
+        tma_prefetch_desc(&maps.Kt);
+        tma_prefetch_desc(&maps.Vt);
+      }
+      uint32_t kc = 0, vc = 0;
+      int wi = 0;
+      for (int w = 2 * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
+        const int r = w / p.Hkv, hk = w - r * p.Hkv;
+        int p0, Pr;
+        prefix_of(p, r, p0, Pr, hk == 0);
+        const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
+        if (wi > 0) mbar_wait_sleep(q_free, (wi - 1) & 1);
+        mbar_arrive_expect_tx(q_full, 2u * 128u * G * N1);
+        tma_load_3d(&maps.Q, q_full, gs, 0, hk * G, r * N1);
+        tma_load_3d(&maps.Q, q_full, gs + 16384, 64, hk * G, r * N1);
+        for (int j = 0; j < nt; ++j) {
+          const CUtensorMap* mk = j < npt ? &maps.Kp : &maps.Kt;
+          const CUtensorMap* mv = j < npt ? &maps.Vp : &maps.Vt;
+          const int z = j < npt ? p0 + j * kT2NK : r * N1;
+          const uint32_t ks = kc & 1, vs = vc & 1;
+          if (kc >= 2) mbar_wait_sleep(&k_empty[ks], ((kc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[ks], kT2Slot);
+          uint8_t* kd = gs + kT2OffK + ks * kT2Slot;
+          tma_load_3d(mk, &k_full[ks], kd, 0, hk, z);
+          tma_load_3d(mk, &k_full[ks], kd + kT2NK * 128, 64, hk, z);
+          ++kc;
+          if (vc >= 2) mbar_wait_sleep(&v_empty[vs], ((vc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&v_full[vs], kT2Slot);
+          uint8_t* vd = gs + kT2OffV + vs * kT2Slot;
+          tma_load_3d(mv, &v_full[vs], vd, 0, hk, z);
+          tma_load_3d(mv, &v_full[vs], vd + kT2NK * 128, 64, hk, z);
+          ++vc;
+        }
+      }
+    }
+  } else if (role == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, kT2NK, false, false);
+      constexpr uint32_t idPV = umma_idesc_bf16(128, 128, false, true);
+      const uint32_t aQ = smem_u32(gs), aP = smem_u32(gs + kT2OffP);
+      uint32_t kc = 0, vc = 0, sc = 0, pc = 0;
+      int wi = 0;
+      auto pv_issue = [&](int jj) {
+        const uint32_t vs = vc & 1;
+        mbar_wait(&v_full[vs], (vc >> 1) & 1);
+        mbar_wait(p_full, pc & 1);
+        if (jj == 0 && wi > 0) mbar_wait(o_free, (wi - 1) & 1);  // the epilogue read the previous O
+        tc_fence_after();
+        const uint32_t vb = smem_u32(gs + kT2OffV + vs * kT2Slot);
+#pragma unroll
+        for (int kk = 0; kk < kT2NK / 16; ++kk)
+          umma_bf16(tmem + 128, kmaj_desc(aP, kk, 128), mnmaj_desc(vb, kk, kT2NK), idPV, (jj > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(p_free);
+        umma_commit(&v_empty[vs]);
+        umma_commit(o_ready);
+        ++vc;
+        ++pc;
+      };
+      for (int w = 2 * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
+        const int r = w / p.Hkv;
+        int p0, Pr;
+        prefix_of(p, r, p0, Pr, false);
+        const int nt = (Pr + kT2NK - 1) / kT2NK + 1;
+        mbar_wait(q_full, wi & 1);
+        for (int j = 0; j < nt; ++j) {
+          const uint32_t ks = kc & 1, sb = sc & 1;
+          mbar_wait(&k_full[ks], (kc >> 1) & 1);
+          if (sc >= 2) mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t kb = smem_u32(gs + kT2OffK + ks * kT2Slot);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + sb * kT2NK, kmaj_desc(aQ, kk, 128), kmaj_desc(kb, kk, kT2NK), idS, kk > 0);
+          umma_commit(&s_full[sb]);
+          umma_commit(&k_empty[ks]);
+          ++kc;
+          ++sc;
+          if (j == nt - 1) umma_commit(q_free);
+          if (j >= 1) pv_issue(j - 1);
+        }
+        pv_issue(nt - 1);
+        umma_commit(o_done);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax (4 warps, thread = row)
+    const int q4 = warp & 3;
+    const int i = q4 * 32 + lane;
+    const int rows = G * N1;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
+    const uint32_t aProw = smem_u32(gs + kT2OffP) + i * 128;
+    const float c2 = p.c2;
+    const int st_id = (role - 2) * 32 + lane;  // 0..127
+    uint32_t sc = 0, pvc = 0;
+    int wi = 0;
+    for (int w = 2 * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
+      const int r = w / p.Hkv, hk = w - r * p.Hkv;
+      int p0, Pr;
+      prefix_of(p, r, p0, Pr, false);
+      const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
+      if (st_id < N1) {  // ancestor masks of this request (bit t = tree key t visible)
+        const int s = st_id;
+        const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
+        bool bad = nn < 0 || nn > p.N;
+        uint64_t m = 0;
+        if (!bad) {
+          if (s == 0) {
+            m = 1ull;
+          } else if (s - 1 < nn) {
+            int cur = s - 1;
+            m = 1ull | (1ull << s);
+            for (int k = 0; k <= p.N; ++k) {
+              const int par = p.parents ? p.parents[(size_t)r * p.N + cur] : cur - 1;
+              if (par < -1 || par >= cur) { bad = true; break; }
+              if (par < 0) break;
+              m |= 1ull << (par + 1);
+              cur = par;
+            }
+          }
+        }
+        if (bad && p.status && hk == 0) atomicOr(p.status, (uint32_t)AURORA_STATUS_STRUCTURE);
+        anc[s] = bad ? 0ull : m;
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+      const int s_row = i / G, g = i - s_row * G;
+      const uint64_t a = i < rows ? anc[s_row] : 0ull;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nt; ++j, ++sc) {
+        const uint32_t sb = sc & 1;
+        const bool tree = j == npt;
+        const int lim = tree ? 0 : Pr - j * kT2NK;
+        mbar_wait(&s_full[sb], (sc >> 1) & 1);
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        tmem_ld_32x32b_x32(trow + sb * kT2NK, v0);
+        tmem_ld_32x32b_x32(trow + sb * kT2NK + 32, v1);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&s_free[sb]);
+        float x[64];
+        const bool full = a != 0ull && !tree && lim >= kT2NK;
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          bool ok;
+          if (full) ok = true;
+          else if (tree) ok = (a >> e) & 1ull;
+          else ok = a != 0ull && e < lim;
+          x[e] = ok ? __uint_as_float(e < 32 ? v0[e] : v1[e - 32]) : -INFINITY;
+        }
+        float mt = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 64; ++e) mt = fmaxf(mt, x[e]);
+        mt *= c2;
+        if (mt > m + 8.f) {  // lazy rescale: only when the max grew by more than 2^8
+          if (m != -INFINITY) {
+            const float f = ex2_approx(m - mt);
+            l *= f;
+            mbar_wait(o_ready, (pvc - 1) & 1);  // the previous P V (the last one) has landed
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t o[32];
+              tmem_ld_32x32b_x32(trow + 128 + c * 32, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+              tmem_st_32x32b_x32(trow + 128 + c * 32, o);
+            }
+            tmem_st_wait();
+          }
+          m = mt;
+        }
+        uint32_t w32[32];
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+        for (int h = 0; h < 32; ++h) {
+          const float e0 = ex2_approx(fmaf(x[2 * h], c2, -m)), e1 = ex2_approx(fmaf(x[2 * h + 1], c2, -m));
+          s0 += e0;
+          s1 += e1;
+          w32[h] = pk_bf16(e0, e1);
+        }
+        l += s0 + s1;
+        if (pvc >= 1) mbar_wait(p_free, (pvc - 1) & 1);  // the previous P V has read P
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t ch = static_cast<uint32_t>(c ^ (i & 7));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aProw + ch * 16), "r"(w32[4 * c]),
+                       "r"(w32[4 * c + 1]), "r"(w32[4 * c + 2]), "r"(w32[4 * c + 3])
+                       : "memory");
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(p_full);
+        ++pvc;
+      }
+      // epilogue: O / l -> bf16 global, lse
+      mbar_wait(o_done, wi & 1);
+      tc_fence_after();
+      uint32_t o[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(trow + 128 + c * 32, o[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(o_free);
+      if (i < rows) {
+        const bool live = a != 0ull && l > 0.f;
+        const float inv = live ? 1.f / l : 0.f;
+        uint16_t* orow = p.Oout + (((size_t)r * N1 + s_row) * p.Hq + hk * G + g) * D;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 o4;
+            o4.x = pk_bf16(__uint_as_float(o[c][8 * q + 0]) * inv, __uint_as_float(o[c][8 * q + 1]) * inv);
+            o4.y = pk_bf16(__uint_as_float(o[c][8 * q + 2]) * inv, __uint_as_float(o[c][8 * q + 3]) * inv);
+            o4.z = pk_bf16(__uint_as_float(o[c][8 * q + 4]) * inv, __uint_as_float(o[c][8 * q + 5]) * inv);
+            o4.w = pk_bf16(__uint_as_float(o[c][8 * q + 6]) * inv, __uint_as_float(o[c][8 * q + 7]) * inv);
+            *reinterpret_cast<uint4*>(orow + c * 32 + q * 8) = o4;
+          }
+        p.lse_out[((size_t)r * N1 + s_row) * p.Hq + hk * G + g] = live ? (m + __log2f(l)) * kLn2 : -INFINITY;
+      }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");  // anc is rewritten by the next item
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(*tmem_holder);
+  }
+}
+
 // ------------------------------------------------------------------------------ tree RoPE
 // Block per tree row (request r, row s): position P_r + depth(s) (F4-R6; siblings share it),
 // cos/sin of pos * theta^(-2i/dh) for the dh/2 frequencies computed once in double into shared
@@ -1350,7 +1657,8 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
   p.Oout = (uint16_t*)O;
   p.lse_out = lse;
   cudaStream_t s = (cudaStream_t)stream;
-  if (opt_tree_fwd_tc() && p.G * p.N1 <= 128) {
+  const int tcmode = opt_tree_fwd_tc();
+  if (tcmode && p.G * p.N1 <= 128) {
     TaTcMaps maps;
     const uint64_t rows_t = (uint64_t)p.R * p.N1;
     const uint64_t ptot = ta->prefix_total > 0 ? (uint64_t)ta->prefix_total : 1;
@@ -1365,11 +1673,15 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
     static bool tattr = false;
     if (!tattr) {
       cudaFuncSetAttribute(k_ta_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTc);
+      cudaFuncSetAttribute(k_ta_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemT2);
       tattr = true;
     }
     const int work = p.R * p.Hkv;
     prof_begin(PH_TREE_FWD_TC, s);
-    k_ta_fwd_tc<<<std::min(work, kNumSMs), kTcThreads, kSmemTc, s>>>(maps, p);
+    if (tcmode == 1)
+      k_ta_fwd_tc<<<std::min(work, kNumSMs), kTcThreads, kSmemTc, s>>>(maps, p);
+    else
+      k_ta_fwd_tc2<<<std::min((work + 1) / 2, kNumSMs), kT2Threads, kSmemT2, s>>>(maps, p);
     count_launch();
     prof_end(PH_TREE_FWD_TC, s);
     return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;

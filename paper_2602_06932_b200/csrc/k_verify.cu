@@ -278,76 +278,63 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
   }
 }
 
-// --------------------------------------------------------------------------- A2 scan (TMA ring)
-// Persistent variant for 16 B-aligned rows: one CTA per SM streams its (row, segment) work
-// items through a 6 x 16 KB shared-memory ring filled by 1-D bulk async copies
-// (cp.async.bulk, one producer thread), so the bytes in flight per SM (~96 KB) no longer
-// depend on registers or occupancy.  8 consumer warps read the ring with 16 B shared loads
-// (warp w: vectors w*32 + lane + i*256 of each stage) into per-warp lists; each warp writes
-// its list per item (k_topk_merge merges the nseg x 8 lists of a row), so items need no
-// CTA-wide synchronisation and can be small (good balance over the 148 SMs).
-constexpr int kRingStage = 16384;
-constexpr int kRingStages = 6;
-constexpr int kRingConsumers = 8;
+// --------------------------------------------------------------------------- A2 scan (TMA rings)
+// Persistent variant for 16 B-aligned rows.  Every warp owns a private 3-slot ring of 8 KB in
+// shared memory and streams its own (row, segment) work items through it: lane 0 issues the 1-D
+// bulk async copy (cp.async.bulk) of chunk c + 2 before the warp scans chunk c, so each warp keeps
+// 16 KB in flight (128 KB per SM) independently of registers and occupancy, and each item has
+// ONE list (the cost of keeping a top-k list is ~k ln(n / k) offers per list: one list per
+// 16K+ columns keeps it well below the streaming work).  Warm start per item: the k-th largest
+// lane maximum of the first batch bounds the k-th best element from below.
+constexpr int kRingChunk = 8192;   // bytes per slot (4096 columns)
+constexpr int kRingSlots = 3;
+constexpr int kRingWarps = 8;
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__global__ void __launch_bounds__(32 * (kRingConsumers + 1), 1) k_target_scan_ring(VerifyLaunch p) {
+__global__ void __launch_bounds__(32 * kRingWarps, 1) k_target_scan_ring(VerifyLaunch p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kRingStages * kRingStage);
-  uint64_t* empty = full + kRingStages;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = base + warp * (kRingSlots * kRingChunk);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + kRingWarps * kRingSlots * kRingChunk) + warp * kRingSlots;
   const int k = p.k_max;
   const int items = p.M * p.nseg;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kRingStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kRingConsumers);
-    }
+  if (lane == 0) {
+    for (int i = 0; i < kRingSlots; ++i) mbar_init(&full[i], 1);
     fence_barrier_init();
   }
-  __syncthreads();
-  if (warp == kRingConsumers) {
-    // ---- producer: one thread issues the bulk copies of every item of this CTA, in order
-    if (lane == 0) {
-      uint32_t slot = 0, ph = 0;
-      for (int u = blockIdx.x; u < items; u += gridDim.x) {
-        const int row = u / p.nseg, seg = u % p.nseg;
-        const int64_t c0 = static_cast<int64_t>(seg) * p.seg_len;
-        const int64_t c1 = min(p.V_local, c0 + p.seg_len);
-        const int64_t vbytes = c1 > c0 ? ((c1 - c0) >> 3) * 16 : 0;
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(p.T + static_cast<int64_t>(row) * p.ldT + c0);
-        for (int64_t off = 0; off < vbytes; off += kRingStage) {
-          const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kRingStage), vbytes - off));
-          mbar_wait(&empty[slot], ph ^ 1);
-          mbar_arrive_expect_tx(&full[slot], bytes);
-          bulk_g2s(ring + slot * kRingStage, src + off, bytes, &full[slot]);
-          if (++slot == kRingStages) { slot = 0; ph ^= 1; }
-        }
-      }
-    }
-    return;
-  }
-  // ---- consumers
-  uint32_t slot = 0, ph = 0, bad = 0;
-  for (int u = blockIdx.x; u < items; u += gridDim.x) {
+  __syncwarp();
+  uint32_t bad = 0, used = 0;  // chunks consumed by this warp (slot = used % 3, parity = (used / 3) & 1)
+  for (int u = blockIdx.x * kRingWarps + warp; u < items; u += gridDim.x * kRingWarps) {
     const int row = u / p.nseg, seg = u % p.nseg;
     const int64_t c0 = static_cast<int64_t>(seg) * p.seg_len;
     const int64_t c1 = min(p.V_local, c0 + p.seg_len);
     const int64_t nvec = c1 > c0 ? (c1 - c0) >> 3 : 0;
+    const int64_t vbytes = nvec * 16;
+    const int nch = static_cast<int>((vbytes + kRingChunk - 1) / kRingChunk);
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(p.T + static_cast<int64_t>(row) * p.ldT + c0);
+    auto issue = [&](int c) {  // lane 0: chunk c of this item into slot (used + c) % 3
+      const uint32_t slot = (used + c) % kRingSlots;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kRingChunk), vbytes - static_cast<int64_t>(c) * kRingChunk));
+      mbar_arrive_expect_tx(&full[slot], bytes);
+      bulk_g2s(ring + slot * kRingChunk, src + static_cast<int64_t>(c) * kRingChunk, bytes, &full[slot]);
+    };
+    if (lane == 0)
+      for (int c = 0; c < 2 && c < nch; ++c) issue(c);
     WarpList L;
     L.init(k);
     float floor = -INFINITY;
-    bool warm = true;
-    for (int64_t v0 = 0; v0 < nvec; v0 += kRingStage / 16) {
-      const int nv = static_cast<int>(min(static_cast<int64_t>(kRingStage / 16), nvec - v0));
+    for (int c = 0; c < nch; ++c) {
+      const uint32_t slot = (used + c) % kRingSlots, ph = ((used + c) / kRingSlots) & 1;
+      if (lane == 0 && c + 2 < nch) issue(c + 2);  // slot (c + 2) % 3 was released by the __syncwarp below
       mbar_wait(&full[slot], ph);
-      const uint32_t sbase = smem_u32(ring + slot * kRingStage);
-      for (int b = warp * 32; b < nv; b += 32 * kRingConsumers) {  // warp-uniform trip count
+      const int nv = static_cast<int>(min(static_cast<int64_t>(kRingChunk / 16), nvec - static_cast<int64_t>(c) * (kRingChunk / 16)));
+      const uint32_t sbase = smem_u32(ring + slot * kRingChunk);
+      for (int b = 0; b < nv; b += 32) {  // warp-uniform trip count
         const int vi = b + lane;
         uint4 w = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
         if (vi < nv) {
@@ -357,20 +344,17 @@ __global__ void __launch_bounds__(32 * (kRingConsumers + 1), 1) k_target_scan_ri
           bad |= nonfinite8(w);
         }
         const float gm = vi < nv ? max8(w) : -INFINITY;
-        if (warm) {  // warm start: the k-th largest lane maximum (distinct elements) bounds the
-          warm = false;  // k-th best element from below, so the first batch offers ~k values
-          floor = warp_kth_largest(gm, k);
-        }
+        if (c == 0 && b == 0) floor = warp_kth_largest(gm, k);
         const bool h = vi < nv && gm >= fmaxf(floor, L.thr_v);
-        if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, w, c0 + (v0 + vi) * 8, floor);
+        if (__any_sync(0xffffffffu, h))
+          offer_vectors(L, h, w, c0 + (static_cast<int64_t>(c) * (kRingChunk / 16) + vi) * 8, floor);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-      if (++slot == kRingStages) { slot = 0; ph ^= 1; }
+      __syncwarp();  // every lane is done with this slot before lane 0 refills it
     }
-    // scalar tail of the segment (V_local % 8 columns of the row's last segment)
+    used += nch;
+    // scalar tail of the segment (the V_local % 8 columns of the row's last segment)
     const uint16_t* T = p.T + static_cast<int64_t>(row) * p.ldT;
-    for (int64_t cb = c0 + nvec * 8 + static_cast<int64_t>(warp) * 32; cb < c1; cb += 32 * kRingConsumers) {
+    for (int64_t cb = c0 + nvec * 8; cb < c1; cb += 32) {
       const int64_t col = cb + lane;
       float v = -INFINITY;
       if (col < c1) {
@@ -386,7 +370,7 @@ __global__ void __launch_bounds__(32 * (kRingConsumers + 1), 1) k_target_scan_ri
       }
     }
     if (lane < k) {
-      const int64_t o = ((static_cast<int64_t>(row) * p.nseg + seg) * kRingConsumers + warp) * k;
+      const int64_t o = (static_cast<int64_t>(row) * p.nseg + seg) * k;
       p.cand_val[o + lane] = L.v;
       p.cand_idx[o + lane] = (L.i == INT32_MAX) ? INT32_MAX : static_cast<int32_t>(L.i + p.vocab_offset);
     }
@@ -840,9 +824,9 @@ cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s) {
 bool scan_ring_ok(const VerifyLaunch& p) {
   return (reinterpret_cast<uintptr_t>(p.T) & 15) == 0 && (p.ldT & 7) == 0 && (p.seg_len & 7) == 0;
 }
-int scan_ring_lists() { return kRingConsumers; }
+int scan_ring_lists() { return 1; }
 cudaError_t launch_target_scan_ring(const VerifyLaunch& p, cudaStream_t s) {
-  constexpr int kSmem = kRingStages * kRingStage + 2 * kRingStages * 8 + 128;
+  constexpr int kSmem = kRingWarps * kRingSlots * kRingChunk + kRingWarps * kRingSlots * 8 + 128;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_target_scan_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
@@ -850,8 +834,9 @@ cudaError_t launch_target_scan_ring(const VerifyLaunch& p, cudaStream_t s) {
     attr = true;
   }
   const int64_t items = static_cast<int64_t>(p.M) * p.nseg;
-  const int grid = static_cast<int>(items < kNumSMs ? items : kNumSMs);
-  k_target_scan_ring<<<grid, 32 * (kRingConsumers + 1), kSmem, s>>>(p);
+  const int64_t ctas = (items + kRingWarps - 1) / kRingWarps;
+  const int grid = static_cast<int>(ctas < kNumSMs ? ctas : kNumSMs);
+  k_target_scan_ring<<<grid, 32 * kRingWarps, kSmem, s>>>(p);
   count_launch();
   return cudaGetLastError();
 }

@@ -81,22 +81,23 @@ def _compare(got, ref, reqs_got, off_got, reqs_ref_off=None):
             assert _rel(a, ref[name]) <= 2e-2, (name, _rel(a, ref[name]))
 
 
-@pytest.mark.parametrize("tc,split", [(1, 0), (0, 1), (0, 0)], ids=["tc_fwd+fused_bwd", "sync_fwd+split_bwd",
-                                                                      "sync_fwd+fused_bwd"])
+@pytest.mark.parametrize("tc,split", [(2, 0), (1, 0), (0, 1), (0, 0)],
+                         ids=["tc2_fwd+fused_bwd", "tc_fwd+fused_bwd", "sync_fwd+split_bwd", "sync_fwd+fused_bwd"])
 @pytest.mark.parametrize("name", ["ta_small", "ta_chain", "ta_gqa8"])
 def test_tree_attention_parity(name, tc, split):
-    """tc=1: the tcgen05 forward (TMEM accumulators, TMA K/V; opt-in, option tree_fwd_tc),
-    tc=0: the mma.sync forward (default); split=0: the one-kernel backward (all rows of
+    """tc=2: the one-pass tcgen05 forward (online softmax, lazy O rescale in TMEM, two items
+    per SM), tc=1: the two-pass tcgen05 forward, tc=0: the mma.sync forward; split=0: the one-kernel backward (all rows of
     a kv head in one CTA); split=1: the general dQ + dK/dV kernels (used when G*(N+1) > 128)."""
     from paper_2602_06932_b200 import aurora as A
     inp = tracegen.gen_tree_attn(name)
+    saved = A.aurora_get_option("tree_fwd_tc")
     A.aurora_set_option("tree_bwd_split", split)
     A.aurora_set_option("tree_fwd_tc", tc)
     try:
         got = _run(inp)
     finally:
         A.aurora_set_option("tree_bwd_split", 0)
-        A.aurora_set_option("tree_fwd_tc", 0)
+        A.aurora_set_option("tree_fwd_tc", saved)
     ref = TA.fwd_bwd(inp)
     R = len(inp["requests"])
     _compare(got, ref, np.arange(R), inp["prefix_off"])
@@ -117,12 +118,19 @@ def test_tree_attention_deterministic():
         assert torch.equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("tc", [0, 2])
 @pytest.mark.parametrize("name,sample", [("ta_llama", [0, 37, 63]), ("ta_tree", [0, 511, 1023])])
-def test_tree_attention_full_size_sampled(name, sample):
-    """Full BASELINE sizes in the bench's launch configuration; the oracle recomputes a
-    sample of requests (each request is independent, so the sample is exact)."""
+def test_tree_attention_full_size_sampled(name, sample, tc):
+    """Full BASELINE sizes in the bench's launch configuration (both forwards); the oracle
+    recomputes a sample of requests (each request is independent, so the sample is exact)."""
+    from paper_2602_06932_b200 import aurora as A
     inp = tracegen.gen_tree_attn(name)
-    got = _run(inp)
+    saved = A.aurora_get_option("tree_fwd_tc")
+    A.aurora_set_option("tree_fwd_tc", tc)
+    try:
+        got = _run(inp)
+    finally:
+        A.aurora_set_option("tree_fwd_tc", saved)
     ref = TA.fwd_bwd(tracegen.gen_tree_attn(name, requests=sample))
     _compare(got, ref, np.asarray(sample), inp["prefix_off"])
     # every prefix gradient row of the whole batch was written (no NaN sentinel left)
