@@ -105,7 +105,8 @@ struct Options {
                                                // fused one applies (A/B and coverage of the general path)
   int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
                                                // slower at M = 384: 0.507 vs 0.470 ms; opt-in)
-  int scan_ring = 1;                           // A2: persistent TMA-ring scan (0: round-1 kernel)
+  int debug_gemm_group = 0;                    // aurora_debug_gemm only: grouped raster (< 0: groups of n-tiles)
+  int scan_ring = 0;                           // A2: 1 = persistent TMA-ring scan (measured slower: opt-in)
   int fwd_stage = 1;                           // Eq. 3: the fwd stages exp(z - m_half) in dZ^T so the
                                                // bwd needs no recompute GEMM (0: recompute, round-1 path)
   Options() {
@@ -568,6 +569,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
     o.scan_ctas = static_cast<int>(value);
     return AURORA_OK;
   }
+  if (std::strcmp(name, "debug_gemm_group") == 0 && value >= -64 && value <= 64) {
+    o.debug_gemm_group = static_cast<int>(value);
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "scan_ring") == 0 && (value == 0 || value == 1)) {
     o.scan_ring = static_cast<int>(value);
     return AURORA_OK;
@@ -605,6 +610,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "dw_resident") == 0) return o.dw_resident;
   if (std::strcmp(name, "fwd_stage") == 0) return o.fwd_stage;
   if (std::strcmp(name, "scan_ring") == 0) return o.scan_ring;
+  if (std::strcmp(name, "debug_gemm_group") == 0) return o.debug_gemm_group;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
   return -1;
 }
@@ -1336,6 +1342,10 @@ aurora_status_t aurora_debug_gemm(int a_mn, int b_mn, const void* A, const void*
     return (e && e[0] == '1') ? 1 : 0;
   }();
   g.n_fastest = dbg_nfast;
+  if (opts().debug_gemm_group) {  // test hook: the grouped raster of the F4 projections
+    g.group = std::abs(opts().debug_gemm_group);
+    g.group_on_n = opts().debug_gemm_group < 0 ? 1 : 0;
+  }
   g.m_tiles = static_cast<int32_t>(cdiv(M, BM * pr));
   g.n_tiles = static_cast<int32_t>(cdiv(N, BN));
   g.splits = 1;

@@ -33,6 +33,23 @@ __device__ __forceinline__ float select32(const float (&z)[32], int j) {
 // Tile raster: m-fastest (default: consecutive units share the B tile, so the large B
 // operand streams once) or n-fastest (the large operand is A, e.g. dZ^T in the dW GEMM).
 __device__ __forceinline__ void decode_unit(const GemmArgs& a, int u, int& mt, int& nt, int& sp) {
+  if (a.group > 0) {
+    // grouped raster (large operands on both sides, F4 projections): units sweep the other
+    // dimension inside groups of `group` tiles, so the group's blocks stay in L2 while the
+    // other operand's block is reused `group` times
+    const int per = a.m_tiles * a.n_tiles;
+    sp = u / per;
+    const int v = u - sp * per;
+    const int outer = a.group_on_n ? a.n_tiles : a.m_tiles, inner_n = a.group_on_n ? a.m_tiles : a.n_tiles;
+    const int g = v / (a.group * inner_n);
+    const int first = g * a.group;
+    const int gs = min(a.group, outer - first);
+    const int w = v - g * a.group * inner_n;
+    const int in_grp = first + w % gs, other = w / gs;
+    if (a.group_on_n) { nt = in_grp; mt = other; }
+    else { mt = in_grp; nt = other; }
+    return;
+  }
   if (a.n_fastest) {
     nt = u % a.n_tiles;
     const int rest = u / a.n_tiles;

@@ -79,6 +79,8 @@ struct GemmArgs {
   int64_t ld_dzT;
   int32_t* tile_counter;  // nullable: dynamic tile scheduler counter (zero before first use)
   int32_t n_fastest;      // tile raster: 0 = m-fastest (B streams once), 1 = n-fastest (A streams once)
+  int32_t group;          // > 0: grouped raster, `group` m-tiles (group_on_n: n-tiles) per L2-resident group
+  int32_t group_on_n;
   int32_t tma_store;      // set by launch_umma_gemm when an output tensor map is given
   int32_t dbg_epi;        // diagnostics only (AURORA_DBG_EPI): 1 skip tcgen05.ld, 2 skip fence + bulk store
   // ---- F2 objectives (EPI_*_T)

@@ -147,6 +147,20 @@ bool eng_gemm(const Eng& E, const bf16* A, int64_t lda, bool a_mn, const bf16* B
       while (splits > 1 && static_cast<int64_t>(splits) * M * N > E.split_elems) --splits;
     }
   }
+  // grouped raster when both operands are large: keep a group of one side's blocks in L2 (~48 MB)
+  // while the other side sweeps; pick the side with less HBM re-reading
+  {
+    const double l2 = 48.0 * (1 << 20), ablk = 2.0 * BM * pr * K, bblk = 2.0 * BN * K;
+    const double atot = 2.0 * M * K, btot = 2.0 * N * K;
+    if (atot + btot > l2) {
+      const int gm = static_cast<int>(std::max(1.0, std::min<double>(g.m_tiles, (l2 - bblk) / ablk)));
+      const int gn = static_cast<int>(std::max(1.0, std::min<double>(g.n_tiles, (l2 - ablk) / bblk)));
+      const double cm = atot + btot * std::ceil(static_cast<double>(g.m_tiles) / gm);
+      const double cn = btot + atot * std::ceil(static_cast<double>(g.n_tiles) / gn);
+      g.group = cm <= cn ? gm : gn;
+      g.group_on_n = cm <= cn ? 0 : 1;
+    }
+  }
   g.kb_per_split = (g.kb_total + splits - 1) / splits;
   g.splits = (g.kb_total + g.kb_per_split - 1) / g.kb_per_split;
   splits = g.splits;

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         const int arow = (mt * 2 + static_cast<int>(rank)) * BM;
         const int brow = nt * BN + static_cast<int>(rank) * (BN / 2);
         for (int kb = 0; kb < args.kb_total; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
+          mbar_wait_sleep(&empty_bar[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * kFStage);
           else mbar_arrive_cluster(mapa_shared(smem_u32(&full_bar[stage]), 0));
           uint8_t* a = sA + stage * kSmemA;
@@ -148,11 +148,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
       constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN, false, true);
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       for (int u = ublk; u < units; u += ugrid) {
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        mbar_wait_sleep(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < args.kb_total; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+          mbar_wait_sleep(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * kSmemA);
           const uint32_t b_base = smem_u32(sB + stage * kFSB);
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int e = 0; e < kEPerTile; ++e, ++pos) {
           const int col = nt * BN + e * kECols;
           const uint32_t slot = pos % kFR, ph = (pos / kFR) & 1;
-          mbar_wait(&eempty_bar[slot], ph ^ 1);
+          mbar_wait_sleep(&eempty_bar[slot], ph ^ 1);
           mbar_arrive_expect_tx(&efull_bar[slot], kEBytes);
           uint8_t* dst = sState + slot * kEBytes;
           tma_load_2d(&mp.ml, &efull_bar[slot], dst, col, row0);

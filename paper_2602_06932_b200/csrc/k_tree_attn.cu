@@ -1236,7 +1236,7 @@ constexpr int kT2OffV = kT2OffK + 2 * kT2Slot;
 constexpr int kT2OffP = kT2OffV + 2 * kT2Slot;
 constexpr int kT2Grp = kT2OffP + 128 * kT2NK * 2;   // 112 KB per group
 constexpr int kT2OffBar = 2 * kT2Grp;
-constexpr size_t kSmemT2 = kT2OffBar + 1024 + 1024;
+constexpr size_t kSmemT2 = kT2OffBar + 1024 + 64 + 1024;  // barriers + anc, TMEM holder, alignment
 
 __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_constant__ TaTcMaps maps, TaParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -1445,25 +1445,28 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_const
 #pragma unroll
         for (int e = 0; e < 64; ++e) mt = fmaxf(mt, x[e]);
         mt *= c2;
-        if (mt > m + 8.f) {  // lazy rescale: only when the max grew by more than 2^8
-          if (m != -INFINITY) {
-            const float f = ex2_approx(m - mt);
-            l *= f;
-            mbar_wait(o_ready, (pvc - 1) & 1);  // the previous P V (the last one) has landed
-            tc_fence_after();
+        // lazy rescale: only when a row's max grew by more than 2^8 (log2 domain); the TMEM
+        // load / store are warp-collective, so the warp rescales together (factor 1 on the
+        // rows that keep their max)
+        const bool grow = mt > m + 8.f;
+        const bool resc = grow && m != -INFINITY;
+        const float f = resc ? ex2_approx(m - mt) : 1.f;
+        if (resc) l *= f;
+        if (__any_sync(0xffffffffu, resc)) {
+          mbar_wait(o_ready, (pvc - 1) & 1);  // the previous P V (the last one) has landed
+          tc_fence_after();
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t o[32];
-              tmem_ld_32x32b_x32(trow + 128 + c * 32, o);
-              tmem_ld_wait();
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(trow + 128 + c * 32, o);
+            tmem_ld_wait();
 #pragma unroll
-              for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
-              tmem_st_32x32b_x32(trow + 128 + c * 32, o);
-            }
-            tmem_st_wait();
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * f);
+            tmem_st_32x32b_x32(trow + 128 + c * 32, o);
           }
-          m = mt;
+          tmem_st_wait();
         }
+        if (grow) m = mt;
         uint32_t w32[32];
         float s0 = 0.f, s1 = 0.f;
 #pragma unroll

@@ -173,10 +173,21 @@ def _adversarial_rows(V, seed):
     return np.stack(rows)
 
 
+@pytest.mark.parametrize("ring", [0, 1])
 @pytest.mark.parametrize("R,N", [(1, 1), (8, 7), (64, 6)])
-def test_scan_adversarial_rows_full_vocab(R, N):
+def test_scan_adversarial_rows_full_vocab(R, N, ring):
     """Bit-exact argmax and top-10 set (k_accept = k_discard = 10 exposes the whole list)
-    at V = 151,936 for three row counts (32, 5 and 3 scan segments per row)."""
+    at V = 151,936 for three row counts (several segment counts per row), for the default
+    scan and the TMA-ring scan (option scan_ring)."""
+    saved = A.aurora_get_option("scan_ring")
+    A.aurora_set_option("scan_ring", ring)
+    try:
+        _scan_adversarial(R, N)
+    finally:
+        A.aurora_set_option("scan_ring", saved)
+
+
+def _scan_adversarial(R, N):
     V = 151936
     M = R * (N + 1)
     rows = _adversarial_rows(V, seed=M)

@@ -679,3 +679,13 @@ def test_staged_dloss_scaling():
         outs.append((dH, dW))
     assert _rfro(outs[1][1].cpu().numpy(), -2.5 * outs[0][1].cpu().numpy()) < 1e-2
     assert _rfro(outs[1][0].cpu().numpy(), -2.5 * outs[0][0].cpu().numpy()) < 1e-2
+
+
+@pytest.mark.parametrize("group", [3, -2])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(1000, 1300, 192), (256 * 5, 256 * 7, 128)])
+def test_gemm_engine_grouped_raster(option, a_mn, b_mn, M, N, K, group):
+    """The grouped tile raster of the F4 projections (groups of m-tiles, or of n-tiles when
+    negative; ragged last group) covers every tile exactly once: vs PyTorch fp32."""
+    option("debug_gemm_group", group)
+    test_gemm_engine_vs_torch_fp32(a_mn, b_mn, M, N, K)
