@@ -105,6 +105,7 @@ struct Options {
                                                // fused one applies (A/B and coverage of the general path)
   int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
                                                // slower at M = 384: 0.507 vs 0.470 ms; opt-in)
+  int gram_norm = 1;                           // F3 fused: Gram-form global norm when M is small
   int debug_gemm_group = 0;                    // aurora_debug_gemm only: grouped raster (< 0: groups of n-tiles)
   int scan_ring = 0;                           // A2: 1 = persistent TMA-ring scan (measured slower: opt-in)
   int fwd_stage = 1;                           // Eq. 3: the fwd stages exp(z - m_half) in dZ^T so the
@@ -569,6 +570,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
     o.scan_ctas = static_cast<int>(value);
     return AURORA_OK;
   }
+  if (std::strcmp(name, "gram_norm") == 0 && (value == 0 || value == 1)) {
+    o.gram_norm = static_cast<int>(value);
+    return AURORA_OK;
+  }
   if (std::strcmp(name, "debug_gemm_group") == 0 && value >= -64 && value <= 64) {
     o.debug_gemm_group = static_cast<int>(value);
     return AURORA_OK;
@@ -611,6 +616,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "fwd_stage") == 0) return o.fwd_stage;
   if (std::strcmp(name, "scan_ring") == 0) return o.scan_ring;
   if (std::strcmp(name, "debug_gemm_group") == 0) return o.debug_gemm_group;
+  if (std::strcmp(name, "gram_norm") == 0) return o.gram_norm;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;
   return -1;
 }
@@ -1312,9 +1318,70 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
   OptWs ow = carve_opt(oc, V_local * d, 0);
   if (nparts > opt_parts(V_local * d)) return AURORA_ERR_WORKSPACE;
   prof_begin(PH_OPTIM, s);
-  b.out = ow.partials;
-  if (launch_umma_gemm(EPI_SUMSQ, false, true, tmZ_k, tmH_mn, b, s, nullptr, pw) != cudaSuccess) return AURORA_ERR_CUDA;
-  if (launch_sum_partials(ow.partials, static_cast<int>(nparts), ow.norm_sq, s) != cudaSuccess) return AURORA_ERR_CUDA;
+  // Global norm.  Small M: the Gram form ||dZ^T H||_F^2 = sum_{m,m'} (dZ dZ^T)_{mm'} (H H^T)_{mm'}
+  // (two M x M GEMMs, 2 M^2 (V + d) flops instead of the 2 M V d of recomputing every dW tile),
+  // in scratch that is free at this point (the staged forward's partials, or the space after the
+  // recompute layout's bwd region); otherwise the dW recompute with a sum-of-squares epilogue.
+  const int64_t MM = M * M;
+  char* gbase = nullptr;
+  size_t gbytes = 0;
+  if (staged) {
+    gbase = static_cast<char*>(ws);
+    gbytes = stage_layout(M, d, V_local, rec.k_max).off_supz;
+  } else {
+    Carver bc(nullptr);
+    carve_bwd(bc, M, d, V_local);
+    const size_t used = static_cast<size_t>(rup(static_cast<int64_t>(bc.off), 256));
+    gbase = static_cast<char*>(ws) + used;
+    gbytes = ws_bytes > used ? ws_bytes - used : 0;
+  }
+  int gs = 0;  // split-K factor of dZ dZ^T (K = V_local)
+  if (M <= 2048 && MM % 4 == 0 && opts().gram_norm)
+    for (int sp = 8; sp >= 1; --sp)
+      if (static_cast<size_t>(2 + sp) * MM * 4 + 4096 <= gbytes) { gs = sp; break; }
+  if (gs > 0) {
+    float* Gz = reinterpret_cast<float*>(gbase);
+    float* Gh = Gz + MM;
+    float* gpart = Gh + MM;
+    CUtensorMap tzA, tzB, tzC, thA, thB, thC;
+    bool ok = make_tmap_bf16(&tzA, dzT, M, V_local, w.m_pad, 64, 64) && make_tmap_bf16(&tzB, dzT, M, V_local, w.m_pad, 64, 64);
+    ok = ok && make_tmap_bf16(&thA, H, d, M, d, 64, BM) && make_tmap_bf16(&thB, H, d, M, d, 64, BN);
+    GemmArgs gz{};
+    gz.m_tiles = static_cast<int32_t>(cdiv(M, BM));
+    gz.n_tiles = static_cast<int32_t>(cdiv(M, BN));
+    gz.kb_total = static_cast<int32_t>(cdiv(V_local, BK));
+    gz.kb_per_split = static_cast<int32_t>(cdiv(gz.kb_total, gs));
+    gz.splits = static_cast<int32_t>(cdiv(gz.kb_total, gz.kb_per_split));
+    gz.M = M;
+    gz.N = M;
+    gz.out = gpart;
+    gz.ld_out = M;
+    gz.split_stride = MM;
+    ok = ok && make_tmap_f32_out(&tzC, gpart, M, M, M, gz.splits, MM);
+    GemmArgs gh{};
+    gh.m_tiles = gz.m_tiles;
+    gh.n_tiles = gz.n_tiles;
+    gh.kb_total = static_cast<int32_t>(d / BK);
+    gh.kb_per_split = gh.kb_total;
+    gh.splits = 1;
+    gh.M = M;
+    gh.N = M;
+    gh.out = Gh;
+    gh.ld_out = M;
+    ok = ok && make_tmap_f32_out(&thC, Gh, M, M, M, 1, 0);
+    if (!ok) return AURORA_ERR_CUDA;
+    if (launch_umma_gemm(EPI_STORE_F32, true, true, tzA, tzB, gz, s, &tzC, 1) != cudaSuccess ||
+        launch_splitk_reduce(gpart, gz.splits, MM, Gz, 0, s) != cudaSuccess ||
+        launch_umma_gemm(EPI_STORE_F32, false, false, thA, thB, gh, s, &thC, 1) != cudaSuccess ||
+        launch_dot(Gz, Gh, MM, ow.partials, ow.norm_sq, s) != cudaSuccess)
+      return AURORA_ERR_CUDA;
+  } else {
+    b.out = ow.partials;
+    if (launch_umma_gemm(EPI_SUMSQ, false, true, tmZ_k, tmH_mn, b, s, nullptr, pw) != cudaSuccess)
+      return AURORA_ERR_CUDA;
+    if (launch_sum_partials(ow.partials, static_cast<int>(nparts), ow.norm_sq, s) != cudaSuccess)
+      return AURORA_ERR_CUDA;
+  }
   if (comm && comm->vp_x()) {
     if ((st = coll_allreduce(comm, G_VP, ow.norm_sq, ow.norm_sq, 1, DT_F32, s)) != AURORA_OK) return st;
   }

@@ -229,6 +229,7 @@ int adamw_partials();
 // ordered sum of n partials (+ extra_sq) -> out[0] (one CTA)
 cudaError_t launch_sum_partials(const float* partials, int nparts, float* out, cudaStream_t s);
 cudaError_t launch_sumsq(const float* g, int64_t n, float* partials, float* norm_sq, cudaStream_t s);
+cudaError_t launch_dot(const float* a, const float* b, int64_t n, float* partials, float* out, cudaStream_t s);
 // per-step scalars (see AdamwHyper): host_step >= 1, or 0 = increment and use *step_dev
 cudaError_t launch_adamw_prep(const float* norm_sq, const float* extra_sq, const AdamwHyper& h, int64_t host_step,
                               int64_t* step_dev, float* sc, float* grad_norm, cudaStream_t s);

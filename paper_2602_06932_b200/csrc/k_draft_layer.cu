@@ -36,6 +36,14 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
+// 4 consecutive elements (n % 4 == 0, rows 16 B / 8 B aligned)
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 ld4(const bf16* p) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                     __uint_as_float(u.y & 0xFFFF0000u));
+}
+
 // y[row, :n] = x * rstd * w (bf16), rstd[row] = (mean(x^2) + eps)^-1/2
 template <typename TX>
 __global__ void __launch_bounds__(256) k_rms_fwd(const TX* __restrict__ x, int64_t ldx, const float* __restrict__ w,
@@ -45,31 +53,46 @@ __global__ void __launch_bounds__(256) k_rms_fwd(const TX* __restrict__ x, int64
   const int64_t row = blockIdx.x;
   const TX* xr = x + row * ldx;
   float ss = 0.f;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    const float v = to_f(xr[j]);
-    ss += v * v;
+  for (int j = threadIdx.x * 4; j < n; j += blockDim.x * 4) {
+    const float4 v = ld4(xr + j);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   const float r = rsqrtf(block_sum(ss, red) / n + eps);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) y[row * ldy + j] = __float2bfloat16(to_f(xr[j]) * r * w[j]);
+  for (int j = threadIdx.x * 4; j < n; j += blockDim.x * 4) {
+    const float4 v = ld4(xr + j), g = ld4(w + j);
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x * r * g.x, v.y * r * g.y);
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(v.z * r * g.z, v.w * r * g.w);
+    *reinterpret_cast<uint2*>(y + row * ldy + j) =
+        make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+  }
   if (threadIdx.x == 0) rstd[row] = r;
 }
 
-// dx = add + r (w dy) - x r^3 mean(x w dy)    (add may be null)
+// dx = add + r (w dy) - x r^3 mean(x w dy)    (add may be null; dx may alias x: each row is
+// read completely before it is written)
 template <typename TX>
-__global__ void __launch_bounds__(256) k_rms_bwd(const TX* __restrict__ x, int64_t ldx, const float* __restrict__ w,
+__global__ void __launch_bounds__(256) k_rms_bwd(const TX* x, int64_t ldx, const float* __restrict__ w,
                                                  const float* __restrict__ rstd, const float* __restrict__ dy,
-                                                 int64_t ldy, const float* __restrict__ add, int64_t lda,
-                                                 float* __restrict__ dx, int64_t lddx, int n) {
+                                                 int64_t ldy, const float* add, int64_t lda,
+                                                 float* dx, int64_t lddx, int n) {
   __shared__ float red[8];
   const int64_t row = blockIdx.x;
   const float r = rstd[row];
   float dot = 0.f;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) dot += to_f(x[row * ldx + j]) * w[j] * dy[row * ldy + j];
+  for (int j = threadIdx.x * 4; j < n; j += blockDim.x * 4) {
+    const float4 xv = ld4(x + row * ldx + j), g = ld4(w + j), d4 = ld4(dy + row * ldy + j);
+    dot += xv.x * g.x * d4.x + xv.y * g.y * d4.y + xv.z * g.z * d4.z + xv.w * g.w * d4.w;
+  }
   const float c = block_sum(dot, red) / n * r * r * r;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    float v = r * w[j] * dy[row * ldy + j] - to_f(x[row * ldx + j]) * c;
-    if (add) v += add[row * lda + j];
-    dx[row * lddx + j] = v;
+  for (int j = threadIdx.x * 4; j < n; j += blockDim.x * 4) {
+    const float4 xv = ld4(x + row * ldx + j), g = ld4(w + j), d4 = ld4(dy + row * ldy + j);
+    float4 v = make_float4(r * g.x * d4.x - xv.x * c, r * g.y * d4.y - xv.y * c, r * g.z * d4.z - xv.z * c,
+                           r * g.w * d4.w - xv.w * c);
+    if (add) {
+      const float4 a4 = ld4(add + row * lda + j);
+      v.x += a4.x; v.y += a4.y; v.z += a4.z; v.w += a4.w;
+    }
+    *reinterpret_cast<float4*>(dx + row * lddx + j) = v;
   }
 }
 
@@ -95,26 +118,67 @@ __global__ void k_col_reduce(const float* __restrict__ part, int chunks, int n, 
 
 __device__ __forceinline__ float silu_f(float a) { return a / (1.f + __expf(-a)); }
 
+// Elementwise passes, 8 elements (16 B of bf16) per thread and iteration; counts are multiples
+// of 8 and rows 16 B aligned (d, I multiples of 64).
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float* f) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    w[i] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 __global__ void k_swiglu_fwd(const bf16* __restrict__ a, const bf16* __restrict__ b, bf16* __restrict__ m, int64_t count) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-    m[i] = __float2bfloat16(silu_f(__bfloat162float(a[i])) * __bfloat162float(b[i]));
+  const int64_t n8 = count >> 3;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float fa[8], fb[8], fm[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(a) + i), fa);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(b) + i), fb);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) fm[e] = silu_f(fa[e]) * fb[e];
+    reinterpret_cast<uint4*>(m)[i] = pack8(fm);
+  }
 }
 // da = dm * b * s (1 + a (1 - s)),  db = dm * silu(a)   (bf16: the next GEMMs' operands)
 __global__ void k_swiglu_bwd(const bf16* __restrict__ a, const bf16* __restrict__ b, const float* __restrict__ dm,
                              bf16* __restrict__ da, bf16* __restrict__ db, int64_t count) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
-    const float av = __bfloat162float(a[i]), bv = __bfloat162float(b[i]);
-    const float s = 1.f / (1.f + __expf(-av));
-    da[i] = __float2bfloat16(dm[i] * bv * s * (1.f + av * (1.f - s)));
-    db[i] = __float2bfloat16(dm[i] * av * s);
+  const int64_t n8 = count >> 3;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float fa[8], fb[8], g[8], oa[8], ob[8];
+    unpack8(__ldg(reinterpret_cast<const uint4*>(a) + i), fa);
+    unpack8(__ldg(reinterpret_cast<const uint4*>(b) + i), fb);
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(dm) + 2 * i), g1 = __ldg(reinterpret_cast<const float4*>(dm) + 2 * i + 1);
+    g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float s = 1.f / (1.f + __expf(-fa[e]));
+      oa[e] = g[e] * fb[e] * s * (1.f + fa[e] * (1.f - s));
+      ob[e] = g[e] * fa[e] * s;
+    }
+    reinterpret_cast<uint4*>(da)[i] = pack8(oa);
+    reinterpret_cast<uint4*>(db)[i] = pack8(ob);
   }
 }
 __global__ void k_f2bf(const float* __restrict__ x, bf16* __restrict__ y, int64_t count) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = __float2bfloat16(x[i]);
+  const int64_t n8 = count >> 3;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 u = __ldg(reinterpret_cast<const float4*>(x) + 2 * i), v = __ldg(reinterpret_cast<const float4*>(x) + 2 * i + 1);
+    const float f[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
+    reinterpret_cast<uint4*>(y)[i] = pack8(f);
+  }
 }
 
-unsigned grid_for(int64_t count) { return (unsigned)std::min<int64_t>((count + 255) / 256, 148 * 16); }
+unsigned grid_for(int64_t count) { return (unsigned)std::min<int64_t>((count / 8 + 255) / 256, 148 * 16); }
 
 // ---- dense projections on the library's tcgen05 engine (k_gemm.cu), row-major tensors:
 //   C[M, N] (+)= A B^T with A bf16 [M, K] (a_mn: stored as [K, M]) and B bf16 [N, K]

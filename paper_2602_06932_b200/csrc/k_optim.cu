@@ -116,6 +116,40 @@ __global__ void __launch_bounds__(kOptThreads) k_adamw(float4* __restrict__ W, u
   }
 }
 
+// <a, b> over n floats (n % 4 == 0): per-CTA partials in fixed order (the Gram-form norm of
+// the fused optimizer: ||dZ^T H||_F^2 = sum (dZ dZ^T) .* (H H^T))
+__global__ void __launch_bounds__(kOptThreads) k_dot_partial(const float4* __restrict__ a, const float4* __restrict__ b,
+                                                             int64_t n4, float* __restrict__ partial) {
+  float acc = 0.f;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kOptThreads + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * kOptThreads) {
+    const float4 x = __ldg(a + i), y = __ldg(b + i);
+    acc = fmaf(x.x, y.x, acc);
+    acc = fmaf(x.y, y.y, acc);
+    acc = fmaf(x.z, y.z, acc);
+    acc = fmaf(x.w, y.w, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ float red[kOptThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < kOptThreads / 32; ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+cudaError_t launch_dot(const float* a, const float* b, int64_t n, float* partials, float* out, cudaStream_t s) {
+  k_dot_partial<<<kOptBlocks, kOptThreads, 0, s>>>(reinterpret_cast<const float4*>(a),
+                                                   reinterpret_cast<const float4*>(b), n / 4, partials);
+  count_launch();
+  k_sumsq_final<<<1, kOptThreads, 0, s>>>(partials, kOptBlocks, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
 int adamw_partials() { return kOptBlocks; }
 
 cudaError_t launch_sum_partials(const float* partials, int nparts, float* out, cudaStream_t s) {

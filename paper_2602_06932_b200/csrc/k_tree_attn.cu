@@ -1469,9 +1469,10 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_const
         if (grow) m = mt;
         uint32_t w32[32];
         float s0 = 0.f, s1 = 0.f;
+        const float mref = m == -INFINITY ? 0.f : m;  // rows with no visible key yet: e = 0, not NaN
 #pragma unroll
         for (int h = 0; h < 32; ++h) {
-          const float e0 = ex2_approx(fmaf(x[2 * h], c2, -m)), e1 = ex2_approx(fmaf(x[2 * h + 1], c2, -m));
+          const float e0 = ex2_approx(fmaf(x[2 * h], c2, -mref)), e1 = ex2_approx(fmaf(x[2 * h + 1], c2, -mref));
           s0 += e0;
           s1 += e1;
           w32[h] = pk_bf16(e0, e1);
