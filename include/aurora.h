@@ -200,8 +200,9 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
  * dW[chunk] = dZ^T H and dH += dZ W[chunk].
  * dloss (dev, nullable => g = 1) f32 [1] upstream gradient.
  * dH (dev) f32 [M,d] (overwritten; VP: summed over ranks).
- * dW (dev) [V_local,d]: f32 (dW_is_bf16 = 0) — bf16 output -> UNSUPPORTED in
- * this build.  accumulate_dW: bit 0 (AURORA_BWD_ACCUMULATE) adds into dW (micro-batch
+ * dW (dev) [V_local,d]: f32 (dW_is_bf16 = 0, P:495 fp32 gradients) or bf16 (dW_is_bf16 = 1:
+ * the GEMM's fp32 accumulators rounded once; not with accumulation, an unreduced DP group or
+ * the fused persistent backward -> UNSUPPORTED).  accumulate_dW: bit 0 (AURORA_BWD_ACCUMULATE) adds into dW (micro-batch
  * accumulation); bit 1 (AURORA_BWD_NO_DP_REDUCE) skips the DP dW allreduce (C5)
  * because the caller reduce-scatters it in aurora_adamw_step_sharded. */
 #define AURORA_BWD_ACCUMULATE 1

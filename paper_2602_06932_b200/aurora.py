@@ -206,6 +206,11 @@ def _expect(t, dtype_name: str, what: str):
         raise ValueError(f"{what}: must be contiguous")
 
 
+def torch_f32():
+    import torch
+    return torch.float32
+
+
 def _stream(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -458,11 +463,12 @@ class SpecTrainStep:
         return self.loss
 
     def backward(self, H, W, dH, dW, dloss=None, accumulate_dW=False, stream=None, dp_reduce=True):
-        """dp_reduce=False: leave dW unreduced over the DP group (ShardedAdamW reduce-scatters it)."""
+        """dW: fp32 or bf16 [V_local, d].  dp_reduce=False: leave dW unreduced over the
+        DP group (ShardedAdamW reduce-scatters it)."""
         flags = (1 if accumulate_dW else 0) | (0 if dp_reduce else 2)
         aurora_spec_loss_bwd(H, W, self.M, self.d, self.V_local, self.vocab_offset, self.labels, self.row_lse,
-                             dloss, dH, dW, False, flags, self.ws.data_ptr(), self.ws_bytes, self.comm,
-                             stream)
+                             dloss, dH, dW, dW.dtype != torch_f32(), flags, self.ws.data_ptr(), self.ws_bytes,
+                             self.comm, stream)
 
     def backward_adamw(self, H, W, dH, opt: "AdamW", dloss=None, extra_sq=None, stream=None):
         """NEXT F3 fused: backward (dH) + the AdamW step applied from the dW GEMM epilogue

@@ -273,6 +273,7 @@ FusedWs carve_fused(Carver& c, int64_t M, int64_t d, int64_t V_local) {
   return w;
 }
 bool classic_bwd() { return opts().bwd_mode == 0; }
+constexpr int kBwdDwBf16 = 1 << 8;  // internal bwd flag: dW is bf16
 
 // ---- staged layout (fwd_stage): [fwd partials][sup_z: fp32 M x k_max][bwd region], so the
 // numerators the fwd writes into the bwd's dZ^T buffer and the fwd's per-(row, tile half)
@@ -1055,9 +1056,14 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
       b.tile_counter = w.counters + 3 * ch + 1;
       b.n_fastest = 1;  // A = dZ^T chunk (M x vc, may exceed L2) streams once; H (B) stays in L2
       CUtensorMap tmOW;
-      const bool ow = make_tmap_f32_out(&tmOW, dWf + c0 * d, d, vc, d, 1, 0);
+      const bool dw_bf16 = (accumulate_dW & kBwdDwBf16) != 0;  // bf16 dW (§8(b) dW_is_bf16)
+      const bool ow = dw_bf16 ? make_tmap_bf16_out(&tmOW, reinterpret_cast<uint16_t*>(dWf) + c0 * d, d, vc, d)
+                              : make_tmap_f32_out(&tmOW, dWf + c0 * d, d, vc, d, 1, 0);
       prof_begin(PH_BWD_DW, sW);
-      if (pw == 2 && ow && opts().dw_resident && dw_resident_ok(b.kb_total))
+      if (dw_bf16) {
+        if (!ow) return AURORA_ERR_CUDA;
+        e = launch_umma_gemm(EPI_STORE_BF16, false, true, tmZ_k, tmH_mn, b, sW, &tmOW, pw);
+      } else if (pw == 2 && ow && opts().dw_resident && dw_resident_ok(b.kb_total))
         e = launch_dw_resident(tmZ_k, tmH_mn, tmOW, b, sW);  // small M: dZ^T rows stay in smem
       else
         e = launch_umma_gemm(EPI_STORE_F32, false, true, tmZ_k, tmH_mn, b, sW, ow ? &tmOW : nullptr, pw);
@@ -1126,7 +1132,13 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
                                      void* ws, size_t ws_bytes, aurora_comm_t comm, void* stream) {
   if (!gemm_shape_ok(H, W, M, d, V_local) || vocab_offset < 0) return AURORA_ERR_INVALID_ARG;
   if (!labels_ok(labels, false) || !row_lse || !dH || !dW || !al16(dH) || !al16(dW)) return AURORA_ERR_INVALID_ARG;
-  if (dW_is_bf16) return AURORA_ERR_UNSUPPORTED;
+  // bf16 dW: a plain TMA bf16-store epilogue; not with accumulation, a DP reduction or the
+  // opt-in fused persistent backward (fp32 sums)
+  if (dW_is_bf16 && ((accumulate_dW & AURORA_BWD_ACCUMULATE) || (comm && comm->dp_size > 1 &&
+                                                                 !(accumulate_dW & AURORA_BWD_NO_DP_REDUCE)) ||
+                     !classic_bwd()))
+    return AURORA_ERR_UNSUPPORTED;
+  if (dW_is_bf16) accumulate_dW |= kBwdDwBf16;
   aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -111,7 +111,9 @@ def test_fused_bwd_adamw_matches_unfused(name):
     torch.cuda.synchronize()
     assert torch.equal(dH1, dH2)
     n1, n2 = float(opt1.grad_norm.item()), float(opt2.grad_norm.item())
-    assert abs(n1 - n2) <= 1e-5 * n1
+    # the fused path takes the Gram form of the norm for small M (sum over M^2 products of fp32
+    # Gram entries instead of V*d squares): equal up to fp32 summation order, ~1e-5 relative
+    assert abs(n1 - n2) <= 1e-4 * n1
     np.testing.assert_allclose(opt2.W.cpu().numpy(), opt1.W.cpu().numpy(), rtol=1e-6, atol=1e-9)
     np.testing.assert_allclose(opt2.m.cpu().numpy(), opt1.m.cpu().numpy(), rtol=1e-4,
                                atol=1e-6 * float(opt1.m.abs().max()))
@@ -120,8 +122,29 @@ def test_fused_bwd_adamw_matches_unfused(name):
     Wr, mr, vr, norm = oracle.adamw_step(W0.reshape(-1).cpu().numpy(), np.zeros(W0.numel()), np.zeros(W0.numel()),
                                          dW1.reshape(-1).cpu().numpy(), 1, f32(1e-4), warmup_steps=0,
                                          beta1=f32(0.9), beta2=f32(0.999), eps=f32(1e-8))
-    assert abs(n2 - norm) <= 2e-5 * norm
+    assert abs(n2 - norm) <= 1e-4 * norm
     np.testing.assert_allclose(opt2.W.cpu().numpy(), Wr, rtol=2e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["small", "mid"])
+def test_fused_gram_norm_equals_sum_of_squares(name):
+    """The Gram-form norm (||dZ^T H||_F^2 = sum (dZ dZ^T) .* (H H^T)) against the dW-recompute
+    sum-of-squares path of the same fused call (option gram_norm)."""
+    tr = tracegen.gen_trace(name)
+    norms = []
+    saved = A.aurora_get_option("gram_norm")
+    try:
+        for gram in (1, 0):
+            A.aurora_set_option("gram_norm", gram)
+            c, H, W, st = _prepare(tr)
+            st.forward(H, W)
+            opt = A.AdamW(W.float().reshape(-1).clone(), lr=1e-4, warmup_steps=0)
+            st.backward_adamw(H, W, torch.empty(c.M, c.d, device="cuda"), opt)
+            torch.cuda.synchronize()
+            norms.append(float(opt.grad_norm.item()))
+    finally:
+        A.aurora_set_option("gram_norm", saved)
+    assert abs(norms[0] - norms[1]) <= 1e-4 * norms[1]
 
 
 def test_fused_bwd_adamw_needs_one_chunk():

@@ -689,3 +689,27 @@ def test_gemm_engine_grouped_raster(option, a_mn, b_mn, M, N, K, group):
     negative; ragged last group) covers every tile exactly once: vs PyTorch fp32."""
     option("debug_gemm_group", group)
     test_gemm_engine_vs_torch_fp32(a_mn, b_mn, M, N, K)
+
+
+@pytest.mark.parametrize("name", ["small", "small_tree", "mid"])
+def test_bf16_dw_output(name):
+    """§8(b) dW_is_bf16: the dW GEMM's fp32 accumulators rounded once to bf16 (TMA bf16-store
+    epilogue); within the north-star bound of the oracle and equal to the fp32 dW rounded."""
+    tr = tracegen.gen_trace(name)
+    ref = oracle.step(tr)
+    c = tr["cfg"]
+    g = _to_gpu(tr)
+    st = A.SpecTrainStep(c.R, c.N, c.d, c.V)
+    st.verify(g["draft"], g["T"], g["parents"], g["num_nodes"])
+    st.forward(g["H"], g["W"])
+    dH = torch.empty(c.M, c.d, dtype=torch.float32, device="cuda")
+    dWb = torch.empty(c.V, c.d, dtype=torch.bfloat16, device="cuda")
+    st.backward(g["H"], g["W"], dH, dWb)
+    st.forward(g["H"], g["W"])
+    dWf = torch.empty(c.V, c.d, dtype=torch.float32, device="cuda")
+    st.backward(g["H"], g["W"], dH, dWf)
+    torch.cuda.synchronize()
+    assert _rfro(dWb.float().cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert torch.equal(dWb, dWf.to(torch.bfloat16))
+    with pytest.raises(A.AuroraError):   # accumulation into bf16 is not offered
+        st.backward(g["H"], g["W"], dH, dWb, accumulate_dW=True)
