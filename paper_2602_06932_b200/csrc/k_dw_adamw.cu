@@ -6,22 +6,22 @@
 // in and out and the bf16 copy out — 26 B, the optimizer's compulsory traffic.
 //
 // One 2-CTA cluster per 256 x 256 dW tile (tcgen05.mma.cta_group::2), 11 warps per CTA:
-//   warp 0      operand TMA (dZ^T K-major 128 x 64, H MN-major half 128 x 64), 2 stages
+//   warp 0      operand TMA (dZ^T K-major 128 x 64, H MN-major half 128 x 64), one stage (K = M
+//               is 6-8 k-blocks per tile; the two TMEM accumulators hide the serial loads)
 //   warp 1      TMEM allocation + the pair MMA issuer (leader CTA)
-//   warps 2..9  epilogue: warp w owns TMEM lane quadrant w % 4 and column half (w-2)/4
+//   warps 2..9  epilogue: warp w owns TMEM lane quadrant w % 4 and a 16-column half of every entry
 //   warp 10     optimizer-state loader: TMA loads of 128-row x 32-column blocks of m, v and
 //               the fp32 master W (full 128 B lines, SWIZZLE_128B, 48 KB per entry) into a
-//               3-entry ring that runs ahead of the epilogue; all 8 epilogue warps consume an
-//               entry together (warp = TMEM lane quadrant x 16-column half), so one entry is
-//               in use and two are in flight — the bytes the update needs to run at HBM speed
-//               (the round-1 version issued these loads from the epilogue warps
-//               themselves and stalled at ~3.7 TB/s)
+//               4-entry ring that runs ahead of the epilogue; all 8 epilogue warps consume an
+//               entry together, so one entry is in use and three (144 KB) are in flight — the
+//               bytes the update needs to run at HBM speed
 // The epilogue updates each entry in place in shared memory (thread = row, conflict-free
 // 16 B accesses through the swizzle), then reads it back transposed (4 lanes per 64 B row
-// segment) and writes m, v, W and the bf16 copy with streaming 16 B stores, releasing the
-// entry to the loader as soon as the values are in registers.  (Measured: TMA bulk stores
-// from the entry made every warp wait on cp.async.bulk.wait_group.read before the release —
-// 15.6 % of the stall samples on the release — and held the kernel at 5.06 TB/s.)
+// segment) and writes m, v, W (16 B) and the bf16 copy (8 B) with streaming stores, releasing
+// the entry to the loader as soon as the values are in registers.  Measured and replaced: TMA
+// bulk stores from the entry (every warp waited on cp.async.bulk.wait_group.read before the
+// release: 5.06 TB/s), 16-column entries / a 3-entry ring (≈ 4.7 TB/s, latency-bound: bytes
+// in flight per SM too few), spinning producer / MMA / loader waits (issue slots).
 #include <cfloat>
 
 #include "gemm_dev.cuh"
@@ -33,20 +33,19 @@ namespace {
 
 constexpr int kFWarps = 11;
 constexpr int kFThreads = 32 * kFWarps;
-constexpr int kFSt = 2;                               // operand stages
+constexpr int kFSt = 1;                               // operand stages (K = M: 6-8 k-blocks per tile;
+                                                      // the TMEM double buffer hides the serial loads)
 constexpr int kFSB = (BN / 2) * BK * 2;               // B half per CTA and stage
 constexpr int kFStage = kSmemA + kFSB;                // 32 KB
 constexpr int kECols = 32;                            // lm_head columns per state entry (128 B rows)
 constexpr int kEArr = BM * kECols * 4;                // 16 KB: 128 rows x 32 fp32 (SW128)
 constexpr int kEBytes = 3 * kEArr;                    // m, v, W
-constexpr int kFR = 3;                                // state ring entries
+constexpr int kFR = 4;                                // state ring entries (3 in flight, 144 KB)
 constexpr int kWCols = kECols / 2;                    // columns per epilogue warp and entry
-constexpr int kWbBytes = 32 * kWCols * 2;             // 1 KB bf16 staging per epilogue warp
 constexpr int kEPerTile = BN / kECols;                // 8 entries per tile, each consumed by all 8 warps
 constexpr int kRingOff = 0;
 constexpr int kStateOff = kFSt * kFStage;
-constexpr int kWbOff = kStateOff + kFR * kEBytes;
-constexpr int kBarOff = kWbOff + kEpiWarps * kWbBytes;
+constexpr int kBarOff = kStateOff + kFR * kEBytes;
 constexpr int kFSmem = kBarOff + 1024 + 1024;         // barriers + base alignment
 static_assert(kFSmem <= 232448, "dynamic smem per CTA");
 
@@ -71,7 +70,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
   uint8_t* sA = smem + kRingOff;
   uint8_t* sB = sA + kFSt * kSmemA;
   uint8_t* sState = smem + kStateOff;
-  uint8_t* sWb = smem + kWbOff;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kBarOff);
   uint64_t* empty_bar = full_bar + kFSt;
   uint64_t* tfull_bar = empty_bar + kFSt;
@@ -195,7 +193,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
     const float clip = __ldg(args.sc + 0), step_size = __ldg(args.sc + 1), isb2 = __ldg(args.sc + 2);
     const float decay = __ldg(args.sc + 3), b1 = __ldg(args.sc + 4), b2 = __ldg(args.sc + 5);
     const float eps = __ldg(args.sc + 6);
-    uint8_t* wb_stage = sWb + (warp - 2) * kWbBytes;
     const int r = q * 32 + lane;  // this thread's row within the CTA's 128-row block
     uint32_t acc = 0, acc_phase = 0, tile = 0;
     for (int u = ublk; u < units; u += ugrid, ++tile) {
@@ -214,7 +211,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
         mbar_wait(&efull_bar[slot], ph);
         tmem_ld_wait();
         const uint32_t base = smem_u32(sState + slot * kEBytes);
-        float wnew[16];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const uint32_t o = sw128(r, half * 4 + c);
@@ -229,23 +225,11 @@ __global__ void __launch_bounds__(kFThreads, 1)
             vv[j] = fmaf(b2, vv[j], (1.f - b2) * gg * gg);
             const float denom = sqrtf(vv[j]) * isb2 + eps;
             ww[j] = ww[j] * decay - step_size * (mm[j] / denom);
-            wnew[4 * c + j] = ww[j];
           }
           sts128(base + o, m4.x, m4.y, m4.z, m4.w);
           sts128(base + kEArr + o, v4.x, v4.y, v4.z, v4.w);
           sts128(base + 2 * kEArr + o, w4.x, w4.y, w4.z, w4.w);
         }
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const __nv_bfloat162 h2 = __floats2bfloat162_rn(wnew[2 * j], wnew[2 * j + 1]);
-          pk[j] = *reinterpret_cast<const uint32_t*>(&h2);
-        }
-        const uint32_t wbo = smem_u32(wb_stage) + lane * 32;
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(wbo), "r"(pk[0]), "r"(pk[1]), "r"(pk[2]),
-                     "r"(pk[3]) : "memory");
-        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(wbo + 16), "r"(pk[4]), "r"(pk[5]),
-                     "r"(pk[6]), "r"(pk[7]) : "memory");
         __syncwarp();
         // transposed write-back with the LSU: lane l -> (row 8 i + l / 4, 16 B chunk l % 4), so
         // each store instruction writes eight full 64 B row segments; the entry is released
@@ -262,14 +246,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
             st_cs_v4(args.m + g, m4);
             st_cs_v4(args.v + g, v4);
             st_cs_v4(args.w + g, w4);
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(w4.x, w4.y), hi = __floats2bfloat162_rn(w4.z, w4.w);
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(&lo), b1 = *reinterpret_cast<const uint32_t*>(&hi);
+            asm volatile("st.global.cs.v2.b32 [%0], {%1, %2};" ::"l"(args.wb + g), "r"(b0), "r"(b1) : "memory");
           }
-        }
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int rr = i * 16 + (lane >> 1), hh = lane & 1;
-          const float4 b4 = lds128(smem_u32(wb_stage) + rr * 32 + hh * 16);
-          const int64_t grow = row0q + rr;
-          if (grow < args.V && col < args.d) st_cs_v4(reinterpret_cast<float*>(args.wb + grow * args.d + col + hh * 8), b4);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&eempty_bar[slot]);
