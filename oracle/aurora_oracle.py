@@ -25,7 +25,8 @@ step by step in the paper's order (PAPER.md = P, SPEC.md = S, line numbers):
                    (Eq. 3; full-vocab log-softmax per north_star).
   O5 loss_bwd      dL/dz = w (q - p~) (gradient of KL(p~||q) wrt logits, S:321);
                    dW = dZ^T H, dH = dZ W (fp32 gradients; here fp64).
-  O6 step_variants (NEXT F2, the objectives of §5.1): accepted rows with
+  O6 step_variants (NEXT F2, the objectives of §5.1, and SPEC's restricted-softmax
+                   discard loss S:328-331): accepted rows with
                    reverse KL(q || p_target) (gradient q*((ln q - ln p) - KL))
                    plus beta * NTP cross-entropy on the verified token,
                    discard rows with the unfiltered dense KL(p_target || q) ("top-k =
@@ -369,7 +370,7 @@ def _log_softmax(x: np.ndarray) -> np.ndarray:
 
 def step_variants(trace: dict, accept_loss: str = "fkl", ntp_beta: float = 0.0, k_accept: int = 1,
                   k_discard: int = 10, lambda_discard: float = 1.0, normalize: int = 0, discard_scope: int = 0,
-                  g: float = 1.0, want_grads: bool = True, rows=None):
+                  g: float = 1.0, want_grads: bool = True, rows=None, discard_loss: str = "full"):
     """O6 (NEXT F2): the §5.1 objectives on a dense trace, row by row.
 
     ACCEPT rows: accept_loss "fkl" = KL(p~ || q) on the target top-k_accept support
@@ -381,7 +382,10 @@ def step_variants(trace: dict, accept_loss: str = "fkl", ntp_beta: float = 0.0, 
     S:330 "topk=0 disables filtering"; gradient q - p).  Row weights as O3 (per-term
     means over the global counts, reading Q7); the NTP term shares the accepted rows'
     weight.  rows: subset of rows to evaluate (weights still use the full counts);
-    gradients then cover only those rows' contributions.
+    gradients then cover only those rows' contributions.  discard_loss "restricted" (SPEC
+    S:328-331, discard_loss_grad): on DISCARD rows with k_discard >= 1 both distributions are
+    renormalised over the support, KL(p~ || q~) with q~ = softmax of the restricted logits z_S;
+    the gradient is q~ - p~ on S and zero outside it.
     """
     T = bf16_bits_to_f64(trace["T_bits"])
     H64 = bf16_bits_to_f64(trace["H_bits"])
@@ -423,6 +427,13 @@ def step_variants(trace: dict, accept_loss: str = "fkl", ntp_beta: float = 0.0, 
         elif c == DISCARD and k_discard == 0:
             loss = float(np.sum(p * (logp - logq)))
             grad = q - p
+        elif c == DISCARD and discard_loss == "restricted":
+            S = np.asarray(topk[m][:k_discard], dtype=np.int64)
+            pt = np.exp(_log_softmax(T[m][S]))
+            logqt = _log_softmax(z[S])
+            loss = float(np.sum(pt * (np.log(pt) - logqt)))
+            grad = np.zeros_like(q)
+            grad[S] = np.exp(logqt) - pt
         else:
             k = k_accept if c == ACCEPT else k_discard
             S = np.asarray(topk[m][:k], dtype=np.int64)

@@ -667,3 +667,97 @@ def test_loss_bwd_sampled_matches_torch_autograd():
     np.testing.assert_allclose(s["dH"], Ht.grad.numpy()[rows], rtol=1e-9, atol=1e-14)
     for v0, v1 in ranges:
         np.testing.assert_allclose(s["dW"][(v0, v1)], Wt.grad.numpy()[v0:v1], rtol=1e-9, atol=1e-14)
+
+
+# ------------------------------------------------------- O6' restricted-softmax discard (F2)
+def test_restricted_discard_matches_torch_kl_on_the_support():
+    """SPEC S:328-331 discard_loss_grad: KL(p~ || q~) with q~ = softmax of the support logits,
+    gradient zero outside the support — against torch f64 kl_div on the restricted softmax and
+    its autograd (library route, row by row), on a tree trace with rejections."""
+    cfg = tracegen.TraceConfig("rvar", d=24, V=97, R=5, N=6, seed=321, tree=True, beam=2, alpha=(0.6,))
+    tr = tracegen.gen_trace(cfg)
+    out = oracle.step_variants(tr, k_discard=7, discard_loss="restricted")
+    assert out["counts"][1] > 0
+    T = torch.from_numpy(oracle.bf16_bits_to_f64(tr["T_bits"]))
+    H = torch.from_numpy(oracle.bf16_bits_to_f64(tr["H_bits"])).requires_grad_(True)
+    W = torch.from_numpy(oracle.bf16_bits_to_f64(tr["W_bits"])).requires_grad_(True)
+    Z = H @ W.T
+    total = 0.0
+    for m in range(Z.shape[0]):
+        c = int(out["row_class"][m])
+        if c == oracle.PAD:
+            continue
+        k = 1 if c == ACCEPT else 7
+        S = torch.from_numpy(np.asarray(out["topk"][m][:k], dtype=np.int64))
+        pt = F.softmax(T[m, S], 0)
+        logq = F.log_softmax(Z[m, S], 0) if c == DISCARD else F.log_softmax(Z[m], 0)[S]
+        row = F.kl_div(logq, pt, reduction="sum")
+        assert abs(float(row) - out["row_loss"][m]) <= 1e-10 * max(1.0, abs(float(row)))
+        total = total + out["w"][m] * row
+    total.backward()
+    assert abs(float(total) - out["loss"]) <= 1e-10 * abs(out["loss"])
+    np.testing.assert_allclose(out["dW"], W.grad.numpy(), rtol=1e-9, atol=1e-14)
+    np.testing.assert_allclose(out["dH"], H.grad.numpy(), rtol=1e-9, atol=1e-14)
+
+
+def test_restricted_discard_spec_examples():
+    """S:333 'topk = V -> identical to the FKL accepted loss' (the restricted softmax over the
+    whole vocabulary is the softmax); S:334 'target one-hot, topk = 1 -> loss 0'; and a
+    discard row's gradient vanishes outside its support."""
+    tr = tracegen.gen_trace("tiny")
+    V = tr["V"]
+    full = oracle.step_variants(tr, k_discard=V)
+    restr = oracle.step_variants(tr, k_discard=V, discard_loss="restricted")
+    np.testing.assert_allclose(restr["row_loss"], full["row_loss"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(restr["dW"], full["dW"], rtol=1e-9, atol=1e-14)
+    one = oracle.step_variants(tr, k_discard=1, discard_loss="restricted")
+    dis = one["row_class"] == DISCARD
+    assert dis.any() and np.all(np.abs(one["row_loss"][dis]) <= 1e-12)
+    # gradient support: a discard row's dz (recovered from dH = dz W on a single row) is zero
+    # off the support — checked through the column sums of dW restricted to off-support ids
+    out = oracle.step_variants(tr, k_discard=3, discard_loss="restricted", rows=[int(np.flatnonzero(
+        oracle.step_variants(tr)["row_class"] == DISCARD)[0])])
+    m = int(np.flatnonzero(out["row_class"] == DISCARD)[0])
+    S = set(int(j) for j in out["topk"][m][:3])
+    off = [j for j in range(V) if j not in S]
+    assert np.abs(out["dW"][off]).max() == 0.0
+
+
+def test_restricted_discard_finite_differences():
+    tr = _dense_problem(77, d=5, V=23, R=3, N=3)
+    H64 = oracle.bf16_bits_to_f64(tr["H_bits"])
+    W64 = oracle.bf16_bits_to_f64(tr["W_bits"])
+    out = oracle.step_variants(tr, k_discard=4, discard_loss="restricted")
+    assert out["counts"][1] > 0
+    rng = np.random.default_rng(5)
+    h = 1e-6
+    for _ in range(6):
+        i, j = int(rng.integers(0, W64.shape[0])), int(rng.integers(0, W64.shape[1]))
+        Wp, Wm = W64.copy(), W64.copy()
+        Wp[i, j] += h
+        Wm[i, j] -= h
+        fd = (_restricted_loss_f64(tr, Wp, H64) - _restricted_loss_f64(tr, Wm, H64)) / (2 * h)
+        assert abs(fd - out["dW"][i, j]) <= 1e-6 * max(1e-3, abs(out["dW"][i, j])) + 1e-9
+
+
+def _restricted_loss_f64(tr, W64, H64):
+    """The restricted-discard loss with f64 weights (labels from the bf16 trace, which do not
+    depend on H, W) — the step_variants definition evaluated on perturbed weights."""
+    out = oracle.step_variants(tr, k_discard=4, discard_loss="restricted", want_grads=False)
+    T = oracle.bf16_bits_to_f64(tr["T_bits"])
+    Z = H64 @ W64.T
+    tot = 0.0
+    for m in range(Z.shape[0]):
+        c = int(out["row_class"][m])
+        if c == oracle.PAD:
+            continue
+        k = 1 if c == ACCEPT else 4
+        S = np.asarray(out["topk"][m][:k], dtype=np.int64)
+        t = T[m][S]
+        pt = np.exp(t - t.max())
+        pt /= pt.sum()
+        zz = Z[m][S] if c == DISCARD else Z[m]
+        lz = zz - (zz.max() + np.log(np.exp(zz - zz.max()).sum()))
+        lq = lz if c == DISCARD else lz[S]
+        tot += out["w"][m] * float(np.sum(pt * (np.log(pt) - lq)))
+    return tot
