@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define AURORA_ABI_VERSION 2
+#define AURORA_ABI_VERSION 3
 #define AURORA_MAX_NODES 32   /* N <= 32: one warp lane per draft node      */
 #define AURORA_MAX_K 16       /* k_accept, k_discard <= 16 on the dense path */
 #define AURORA_MAX_K_SPARSE 1024  /* k <= 1024 with the sparse top-K ingest (F1) */
@@ -109,6 +109,14 @@ typedef struct {
   float ntp_beta;         /* >= 0: auxiliary NTP cross-entropy -ln q_y on ACCEPT rows,
                              y = verified token, weight beta x the row weight ("RKL +
                              NTP"); requires accept_loss = 1           */
+  int32_t discard_restricted; /* 0 (default): DISCARD rows use the full-vocabulary log-softmax
+                             (reading Q6); 1: SPEC's restricted softmax: both
+                             distributions renormalised over the top-k_discard support,
+                             KL(p~ || q~) with q~ = softmax of the support logits, gradient
+                             q~ - p~ on the support and zero elsewhere (NEXT F2).  Requires
+                             accept_loss = 0, k_discard >= 1, the staged forward (ws of
+                             AURORA_OP_ALL, one dZ^T chunk) and no VP group; the row's support
+                             log-sum-exp is written to labels->row_aux                       */
 } aurora_loss_cfg_t;
 
 /* Caller-allocated outputs of verify; inputs of fwd/bwd.  All (dev). */
@@ -135,7 +143,8 @@ typedef struct {
                                 must stay valid until the bwd call has run                 */
   int64_t ld_target;         /* row stride of target_logits in elements                     */
   int32_t objective;         /* written by verify: bit 0 RKL ACCEPT rows, bit 1 dense-KL
-                                DISCARD rows (0 = Eq. 3 everywhere); read by fwd / bwd      */
+                                DISCARD rows, bit 2 restricted-softmax DISCARD rows (0 = Eq. 3
+                                everywhere); read by fwd / bwd                              */
   float ntp_beta;            /* written by verify: cfg->ntp_beta                             */
 } aurora_labels_t;
 

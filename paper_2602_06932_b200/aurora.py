@@ -57,7 +57,7 @@ class aurora_trace_topk_t(C.Structure):
 class aurora_loss_cfg_t(C.Structure):
     _fields_ = [("k_accept", C.c_int32), ("k_discard", C.c_int32), ("lambda_discard", C.c_float),
                 ("normalize", C.c_int32), ("discard_scope", C.c_int32), ("accept_loss", C.c_int32),
-                ("ntp_beta", C.c_float)]
+                ("ntp_beta", C.c_float), ("discard_restricted", C.c_int32)]
 
 
 class aurora_labels_t(C.Structure):
@@ -388,7 +388,8 @@ class SpecTrainStep:
 
     def __init__(self, R: int, N: int, d: int, V: int, V_local: Optional[int] = None, vocab_offset: int = 0,
                  k_accept: int = 1, k_discard: int = 10, lambda_discard: float = 1.0, normalize: int = 0,
-                 discard_scope: int = 0, device="cuda", comm=None, accept_loss: str = "fkl", ntp_beta: float = 0.0):
+                 discard_scope: int = 0, device="cuda", comm=None, accept_loss: str = "fkl", ntp_beta: float = 0.0,
+                 discard_loss: str = "full"):
         import torch
         self.R, self.N, self.d, self.V = R, N, d, V
         self.V_local = V if V_local is None else V_local
@@ -397,8 +398,11 @@ class SpecTrainStep:
         self.comm = comm
         if accept_loss not in ("fkl", "rkl"):
             raise ValueError("accept_loss must be 'fkl' or 'rkl'")
+        if discard_loss not in ("full", "restricted"):
+            raise ValueError("discard_loss must be 'full' or 'restricted'")
         self.cfg = aurora_loss_cfg_t(k_accept, k_discard, lambda_discard, normalize, discard_scope,
-                                     1 if accept_loss == "rkl" else 0, ntp_beta)
+                                     1 if accept_loss == "rkl" else 0, ntp_beta,
+                                     1 if discard_loss == "restricted" else 0)
         self.k_max = max(k_accept, k_discard, 1)
         dev = torch.device(device)
         M, km = self.M, self.k_max

@@ -336,11 +336,13 @@ aurora_status_t check_cfg(const aurora_loss_cfg_t* cfg, int max_k = AURORA_MAX_K
   if (cfg->accept_loss != 0 && cfg->accept_loss != 1) return AURORA_ERR_INVALID_ARG;
   if (!(cfg->ntp_beta >= 0.f) || !std::isfinite(cfg->ntp_beta)) return AURORA_ERR_INVALID_ARG;
   if (cfg->ntp_beta > 0.f && cfg->accept_loss != 1) return AURORA_ERR_INVALID_ARG;  // NTP pairs with RKL
+  if (cfg->discard_restricted != 0 && cfg->discard_restricted != 1) return AURORA_ERR_INVALID_ARG;
+  if (cfg->discard_restricted && (cfg->accept_loss != 0 || cfg->k_discard < 1)) return AURORA_ERR_INVALID_ARG;
   return AURORA_OK;
 }
 // F2 objectives that read the dense target row again (bit 0 RKL, bit 1 dense discard KL)
 int32_t objective_of(const aurora_loss_cfg_t* cfg) {
-  return (cfg->accept_loss == 1 ? 1 : 0) | (cfg->k_discard == 0 ? 2 : 0);
+  return (cfg->accept_loss == 1 ? 1 : 0) | (cfg->k_discard == 0 ? 2 : 0) | (cfg->discard_restricted ? 4 : 0);
 }
 // GEMM arguments of the F2 epilogues; c0 = first T column of the GEMM's column 0.
 void set_f2_args(GemmArgs& a, const aurora_labels_t* l, int64_t c0) {
@@ -708,7 +710,8 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->V_local, cfg)) return AURORA_ERR_WORKSPACE;
   if (comm && comm->vp_size > 1 && t->V_local == t->V) return AURORA_ERR_INVALID_ARG;  // VP needs shards
   const int32_t objective = objective_of(cfg);
-  if (objective && (!out->row_lse_t || !out->row_aux)) return AURORA_ERR_INVALID_ARG;  // F2 row statistics
+  if ((objective & 3) && (!out->row_lse_t || !out->row_aux)) return AURORA_ERR_INVALID_ARG;  // F2 row statistics
+  if ((objective & 4) && (!out->row_aux || (comm && comm->vp_size > 1))) return AURORA_ERR_UNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   out->objective = objective;
   out->ntp_beta = cfg->ntp_beta;
@@ -769,7 +772,7 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
     if ((e = launch_topk_merge(p, gv, gi, comm->vp_size, k_max, static_cast<int64_t>(M) * k_max, s)) != cudaSuccess)
       return AURORA_ERR_CUDA;
   }
-  if (objective) {  // F2: row statistics of T (a second read of T, so it counts as scan time)
+  if (objective & 3) {  // F2: row statistics of T (a second read of T, so it counts as scan time)
     prof_begin(PH_SCAN, s);
     if (comm && comm->vp_x()) {  // VP: per-rank (max, sum, sum*t) triples -> allgather -> merge
       p.lse_part = w.lse_part;
@@ -814,10 +817,11 @@ aurora_status_t aurora_verify_labels_topk(const aurora_trace_topk_t* t, const au
   if (long_path && t->K_t > AURORA_MAX_KT_SPARSE) return AURORA_ERR_UNSUPPORTED;
   if (!long_path && k_max > AURORA_MAX_K) return AURORA_ERR_INVALID_ARG;  // warp lists hold <= 16
   const int64_t M = static_cast<int64_t>(t->R) * (t->N + 1);
-  if (objective_of(cfg)) return AURORA_ERR_UNSUPPORTED;  // F2 needs the dense target row
+  if (objective_of(cfg) & 3) return AURORA_ERR_UNSUPPORTED;  // F2 RKL / dense KL need the dense target row
+  if (cfg->discard_restricted && (!out->row_aux || (comm && comm->vp_size > 1))) return AURORA_ERR_UNSUPPORTED;
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_VERIFY, M, 64, t->K_t, cfg)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  out->objective = 0;
+  out->objective = objective_of(cfg) & 4;
   out->ntp_beta = 0.f;
   stage_put(ws, nullptr);
   Carver c(ws);
@@ -866,7 +870,9 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   if (!labels_ok(labels, false) || !row_lse || !loss) return AURORA_ERR_INVALID_ARG;
   aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_FWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
-  const int32_t objective = labels->objective;
+  const int32_t objective = labels->objective & 3;  // the T-reading F2 objectives
+  const bool restricted = (labels->objective & 4) != 0;
+  if (restricted && (!labels->row_aux || (comm && comm->vp_size > 1))) return AURORA_ERR_UNSUPPORTED;
   if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
                     labels->ld_target < V_local))
     return AURORA_ERR_INVALID_ARG;
@@ -904,6 +910,7 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
   const StageLayout L = stage_layout(M, d, V_local, labels->k_max);
   const bool stage = opts().fwd_stage && !objective && classic_bwd() && chunk_cols(V_local, M) >= V_local &&
                      ws_bytes >= L.total;
+  if (restricted && !stage) return AURORA_ERR_UNSUPPORTED;  // needs the support logits of the staged fwd
   int epi = objective ? EPI_FWD_STATS_T : EPI_FWD_STATS;
   if (stage) {
     Carver cb(static_cast<char*>(ws) + L.off_bwd);
@@ -935,7 +942,9 @@ aurora_status_t aurora_spec_loss_fwd(const void* H, const void* W, int64_t M, in
     P = comm->vp_size;
   }
   int nb = 0;
-  RowF2 f2{(objective & 1) ? 1 : 0, labels->ntp_beta, labels->row_lse_t, labels->row_aux};
+  RowF2 f2{(objective & 1) ? 1 : 0, labels->ntp_beta, labels->row_lse_t, labels->row_aux, restricted ? 1 : 0,
+           restricted ? reinterpret_cast<const float*>(static_cast<char*>(ws) + L.off_supz) : nullptr,
+           labels->sup_idx, labels->k_max};
   if ((e = launch_row_combine(msu_all, P, M, labels->row_H, labels->row_w, labels->row_class, row_lse, row_loss,
                               w.bp, &nb, f2, s)) != cudaSuccess)
     return AURORA_ERR_CUDA;
@@ -1021,12 +1030,13 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
       Carver fc(ws);
       const FwdWs fw = carve_fwd(fc, M, V_local);
       prof_begin(PH_BWD_RESCALE, s);
+      const int restricted = (labels->objective & 4) ? 1 : 0;  // F2 restricted-softmax DISCARD rows
       e = launch_dz_rescale(dzT, w.m_pad, M, V_local, staged->bn, staged->n_tiles, fw.pm, row_lse, labels->row_w, dloss,
-                            s);
+                            labels->row_class, restricted, s);
       if (e == cudaSuccess)
         e = launch_dz_support_fix(dzT, w.m_pad, M, V_local, vocab_offset, labels,
                                   reinterpret_cast<const float*>(static_cast<char*>(ws) + SL.off_supz), row_lse, dloss,
-                                  s);
+                                  restricted, s);
       prof_end(PH_BWD_RESCALE, s);
     } else {
       prof_begin(PH_BWD_DZ, s);
@@ -1143,13 +1153,15 @@ aurora_status_t aurora_spec_loss_bwd(const void* H, const void* W, int64_t M, in
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   float* dWf = static_cast<float*>(dW);
-  const int32_t objective = labels->objective;
+  const int32_t objective = labels->objective & 3;  // the T-reading F2 objectives
+  const bool restricted = (labels->objective & 4) != 0;
   if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
                     labels->ld_target < V_local))
     return AURORA_ERR_INVALID_ARG;
   StageRec rec;
   const bool staged = stage_take(ws, &rec) && staged_matches(rec, H, W, M, d, V_local, vocab_offset, labels) &&
                       !objective && classic_bwd() && ws_bytes >= stage_layout(M, d, V_local, rec.k_max).total;
+  if (restricted && !staged) return AURORA_ERR_UNSUPPORTED;  // the support logits live in the staged ws
   // the fused persistent bwd implements Eq. 3 only; the F2 objectives take the chunked path
   if (!classic_bwd() && !objective) return bwd_fused(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, dWf,
                                        accumulate_dW, ws, comm, s);
@@ -1290,7 +1302,8 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
   aurora_loss_cfg_t dummy{1, 1, 1.f, 0, 0};
   if (!ws || ws_bytes < aurora_workspace_size(AURORA_OP_BWD, M, d, V_local, &dummy)) return AURORA_ERR_WORKSPACE;
   if (!opt_ws || opt_ws_bytes < aurora_adamw_workspace_size(V_local * d)) return AURORA_ERR_WORKSPACE;
-  const int32_t objective = labels->objective;
+  const int32_t objective = labels->objective & 3;
+  const bool restricted = (labels->objective & 4) != 0;
   if (objective && (!labels->target_logits || !labels->row_lse_t || !labels->row_aux ||
                     labels->ld_target < V_local))
     return AURORA_ERR_INVALID_ARG;
@@ -1302,6 +1315,7 @@ aurora_status_t aurora_spec_loss_bwd_adamw(const void* H, void* W, int64_t M, in
   StageRec rec;
   const bool staged = stage_take(ws, &rec) && staged_matches(rec, H, W, M, d, V_local, vocab_offset, labels) &&
                       !objective && ws_bytes >= stage_layout(M, d, V_local, rec.k_max).total;
+  if (restricted && !staged) return AURORA_ERR_UNSUPPORTED;
   __nv_bfloat16* dzT = nullptr;
   st = bwd_classic_impl(H, W, M, d, V_local, vocab_offset, labels, row_lse, dloss, dH, nullptr, 0, ws, comm, s,
                         objective, staged ? &rec : nullptr, &dzT);

@@ -205,7 +205,11 @@ struct RowF2 {  // F2 objectives in the row combine (all zero / null: Eq. 3 FKL 
   int32_t rkl;
   float beta;
   const float* row_lse_t;
-  float* row_aux;  // out: E_q[z - t] on RKL rows
+  float* row_aux;  // out: E_q[z - t] on RKL rows; the support log-sum-exp on restricted rows
+  int32_t restricted;        // DISCARD rows: SPEC's restricted softmax over the support
+  const float* sup_z;        // [M, k_max] support logits (staged forward)
+  const int32_t* sup_idx;    // [M, k_max] (INT32_MAX = padding)
+  int32_t k_max;
 };
 cudaError_t launch_row_combine(const float* msu_all /*[P,M,kMsu]*/, int P, int64_t M, const float* row_H,
                                const float* row_w, const uint8_t* row_class, float* row_lse, float* row_loss,
@@ -215,10 +219,10 @@ cudaError_t launch_splitk_reduce(const float* partials, int splits, int64_t n_el
                                  cudaStream_t s);
 cudaError_t launch_dz_rescale(__nv_bfloat16* dzT, int64_t ld, int64_t M, int64_t V_local, int bn, int n_tiles,
                               const float* pm, const float* row_lse, const float* row_w, const float* dloss,
-                              cudaStream_t s);
+                              const uint8_t* row_class, int restricted, cudaStream_t s);
 cudaError_t launch_dz_support_fix(__nv_bfloat16* dzT, int64_t ld, int64_t M, int64_t V_local, int64_t vocab_offset,
                                   const aurora_labels_t* lab, const float* sup_z, const float* row_lse,
-                                  const float* dloss, cudaStream_t s);
+                                  const float* dloss, int restricted, cudaStream_t s);
 cudaError_t launch_debug_dlogits(const __nv_bfloat16* H, const __nv_bfloat16* W, int64_t M, int64_t d,
                                  int64_t V_local, int64_t vocab_offset, const aurora_labels_t* lab,
                                  const float* row_lse, const float* dloss, const int32_t* rows, int n_rows,

@@ -123,6 +123,20 @@ __global__ void __launch_bounds__(256) k_row_combine(const float* __restrict__ m
       const float eqzt = r / s;  // E_q[z - t]
       l = eqzt - lse + f2.row_lse_t[row] + f2.beta * lse - u;
       f2.row_aux[row] = eqzt;
+    } else if (cls == AURORA_ROW_DISCARD && f2.restricted) {
+      // SPEC's restricted softmax: l = KL(p~ || q~) = H~ - u + lse_S with lse_S the
+      // log-sum-exp of the support logits the staged forward kept
+      const float* zr = f2.sup_z + row * f2.k_max;
+      const int32_t* ir = f2.sup_idx + row * f2.k_max;
+      float zm = -INFINITY;
+      for (int j = 0; j < f2.k_max; ++j)
+        if (ir[j] != INT32_MAX) zm = fmaxf(zm, zr[j]);
+      float se = 0.f;
+      for (int j = 0; j < f2.k_max; ++j)
+        if (ir[j] != INT32_MAX) se += __expf(zr[j] - zm);
+      const float lse_s = zm + logf(se);
+      f2.row_aux[row] = lse_s;
+      l = lse_s - u + row_H[row];
     } else if (cls != AURORA_ROW_PAD) {
       l = lse - u + row_H[row];
     }
@@ -194,7 +208,8 @@ constexpr int kRsRows = 1024;  // dZ^T columns (rows m) per rescale CTA
 __global__ void __launch_bounds__(256) k_dz_rescale(__nv_bfloat16* __restrict__ dzT, int64_t ld, int64_t M,
                                                     int64_t V_local, int bn, const float* __restrict__ pm,
                                                     int pm_stride, const float* __restrict__ row_lse,
-                                                    const float* __restrict__ row_w, const float* __restrict__ dloss) {
+                                                    const float* __restrict__ row_w, const float* __restrict__ dloss,
+                                                    const uint8_t* __restrict__ row_class, int restricted) {
   __shared__ float F[kRsRows];
   const int h = blockIdx.x;  // tile half: tile h / 2, columns [0, 128) or [128, bn)
   const int64_t c0 = static_cast<int64_t>(h >> 1) * bn + ((h & 1) ? BN / 2 : 0);
@@ -208,7 +223,9 @@ __global__ void __launch_bounds__(256) k_dz_rescale(__nv_bfloat16* __restrict__ 
     if (m < M) {
       const float w = __ldg(row_w + m);
       const float mh = __ldg(pm + m * pm_stride + h);
-      if (w != 0.f && mh != -INFINITY) f = g * w * __expf(mh - __ldg(row_lse + m));
+      // restricted-softmax DISCARD rows: no full-vocabulary term (dz lives on the support only)
+      const bool off = restricted && row_class[m] == AURORA_ROW_DISCARD;
+      if (w != 0.f && mh != -INFINITY && !off) f = g * w * __expf(mh - __ldg(row_lse + m));
     }
     F[i] = f;
   }
@@ -237,7 +254,8 @@ __global__ void k_dz_support_fix(__nv_bfloat16* __restrict__ dzT, int64_t ld, in
                                  int64_t vocab_offset, const int32_t* __restrict__ sup_idx,
                                  const float* __restrict__ sup_p, const float* __restrict__ sup_z, int k_max,
                                  const float* __restrict__ row_lse, const float* __restrict__ row_w,
-                                 const float* __restrict__ dloss) {
+                                 const float* __restrict__ dloss, const uint8_t* __restrict__ row_class,
+                                 const float* __restrict__ row_aux, int restricted) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= M * k_max) return;
   const int64_t m = i / k_max;
@@ -246,23 +264,27 @@ __global__ void k_dz_support_fix(__nv_bfloat16* __restrict__ dzT, int64_t ld, in
   const int64_t loc = static_cast<int64_t>(gid) - vocab_offset;
   if (loc < 0 || loc >= V_local) return;
   const float coef = (dloss ? __ldg(dloss) : 1.f) * row_w[m];
-  dzT[loc * ld + m] = __float2bfloat16_rn(coef * (__expf(sup_z[i] - row_lse[m]) - sup_p[i]));
+  // restricted DISCARD rows: q~_j = exp(z_j - lse_S) over the support (lse_S from the combine)
+  const float lse = (restricted && row_class[m] == AURORA_ROW_DISCARD) ? row_aux[m] : row_lse[m];
+  dzT[loc * ld + m] = __float2bfloat16_rn(coef * (__expf(sup_z[i] - lse) - sup_p[i]));
 }
 
 cudaError_t launch_dz_rescale(__nv_bfloat16* dzT, int64_t ld, int64_t M, int64_t V_local, int bn, int n_tiles,
                               const float* pm, const float* row_lse, const float* row_w, const float* dloss,
-                              cudaStream_t s) {
+                              const uint8_t* row_class, int restricted, cudaStream_t s) {
   dim3 grid(static_cast<unsigned>(2 * n_tiles), static_cast<unsigned>((ld + kRsRows - 1) / kRsRows));
-  k_dz_rescale<<<grid, 256, 0, s>>>(dzT, ld, M, V_local, bn, pm, 2 * n_tiles, row_lse, row_w, dloss);
+  k_dz_rescale<<<grid, 256, 0, s>>>(dzT, ld, M, V_local, bn, pm, 2 * n_tiles, row_lse, row_w, dloss, row_class,
+                                    restricted);
   count_launch();
   return cudaGetLastError();
 }
 cudaError_t launch_dz_support_fix(__nv_bfloat16* dzT, int64_t ld, int64_t M, int64_t V_local, int64_t vocab_offset,
                                   const aurora_labels_t* lab, const float* sup_z, const float* row_lse,
-                                  const float* dloss, cudaStream_t s) {
+                                  const float* dloss, int restricted, cudaStream_t s) {
   const int64_t n = M * lab->k_max;
   k_dz_support_fix<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
-      dzT, ld, M, V_local, vocab_offset, lab->sup_idx, lab->sup_p, sup_z, lab->k_max, row_lse, lab->row_w, dloss);
+      dzT, ld, M, V_local, vocab_offset, lab->sup_idx, lab->sup_p, sup_z, lab->k_max, row_lse, lab->row_w, dloss,
+      lab->row_class, lab->row_aux, restricted);
   count_launch();
   return cudaGetLastError();
 }

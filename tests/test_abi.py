@@ -75,9 +75,9 @@ def test_host_validation_without_gpu(L):
     assert L.aurora_verify_labels(C.byref(t2), C.byref(cfg), C.byref(lab), None, 0, None, None) == 1
     # fwd with d not a multiple of 64
     assert L.aurora_spec_loss_fwd(16, 16, 20, 100, 1000, 0, C.byref(lab), 16, None, 16, None, 0, None, None) == 1
-    # bf16 dW output is declared but unsupported in this build
+    # bf16 dW output: supported, but not with accumulation (host-detectable, nothing enqueued)
     lab2 = A.aurora_labels_t(10, 16, 16, 16, 16, 16, 16, 16, 16, 16, 16, 16)
-    assert L.aurora_spec_loss_bwd(16, 16, 20, 64, 1000, 0, C.byref(lab2), 16, None, 16, 16, 1, 0, 16, 1 << 30,
+    assert L.aurora_spec_loss_bwd(16, 16, 20, 64, 1000, 0, C.byref(lab2), 16, None, 16, 16, 1, 1, 16, 1 << 30,
                                   None, None) == 5
     # missing workspace
     assert L.aurora_spec_loss_fwd(16, 16, 20, 64, 1000, 0, C.byref(lab2), 16, None, 16, None, 0, None, None) == 6

@@ -713,3 +713,31 @@ def test_bf16_dw_output(name):
     assert torch.equal(dWb, dWf.to(torch.bfloat16))
     with pytest.raises(A.AuroraError):   # accumulation into bf16 is not offered
         st.backward(g["H"], g["W"], dH, dWb, accumulate_dW=True)
+
+
+@pytest.mark.parametrize("kd", [3, 10])
+@pytest.mark.parametrize("name", ["tiny", "small", "small_tree", "mid"])
+def test_restricted_discard_parity(name, kd):
+    """F2, SPEC's restricted-softmax discard loss: DISCARD rows use KL(p~ || q~)
+    with q~ the softmax of the support logits (the staged forward's fp32 support logits give
+    the support log-sum-exp; the backward keeps dz only on the support), vs oracle O6'."""
+    tr = tracegen.gen_trace(name)
+    ref = oracle.step_variants(tr, k_discard=kd, discard_loss="restricted")
+    out = _run_gpu(tr, k_discard=kd, discard_loss="restricted")
+    st = out["st"]
+    assert int(st.status.item()) == 0
+    np.testing.assert_array_equal(st.row_class.cpu().numpy(), ref["row_class"])
+    valid = ref["row_class"] != oracle.PAD
+    np.testing.assert_allclose(st.row_loss.cpu().numpy()[valid], ref["row_loss"][valid], rtol=1e-3, atol=2e-4)
+    loss = float(st.loss.item())
+    assert abs(loss - ref["loss"]) <= LOSS_RTOL * abs(ref["loss"]), (loss, ref["loss"])
+    assert _rfro(out["dW"].cpu().numpy(), ref["dW"]) <= GRAD_RFRO
+    assert _rfro(out["dH"].cpu().numpy(), ref["dH"]) <= GRAD_RFRO
+
+
+def test_restricted_discard_needs_the_staged_forward(option):
+    option("fwd_stage", 0)
+    tr = tracegen.gen_trace("small")
+    with pytest.raises(A.AuroraError) as ei:
+        _run_gpu(tr, discard_loss="restricted")
+    assert ei.value.status == 5
