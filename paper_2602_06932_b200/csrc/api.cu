@@ -120,7 +120,7 @@ struct Options {
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
     if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
-    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = std::min(2, std::max(0, atoi(e)));
+    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = std::min(3, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_TREE_BWD_SPLIT")) tree_bwd_split = atoi(e) ? 1 : 0;
   }
 };
@@ -557,7 +557,7 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
-  if (std::strcmp(name, "tree_fwd_tc") == 0 && value >= 0 && value <= 2) {
+  if (std::strcmp(name, "tree_fwd_tc") == 0 && value >= 0 && value <= 3) {
     o.tree_fwd_tc = static_cast<int>(value);
     return AURORA_OK;
   }

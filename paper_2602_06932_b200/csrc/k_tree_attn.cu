@@ -1229,61 +1229,73 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_ta_fwd_tc(const __grid_consta
 // other group's S / P V, so the MMA <-> softmax round trips of the single-item kernel (k_ta_fwd_tc,
 // two passes) overlap.  Work item = (request, KV head) with its G (N+1) <= 128 query rows.
 constexpr int kT2NK = 64;
-constexpr int kT2Threads = 384;
 constexpr int kT2Slot = kT2NK * 128 * 2;            // 16 KB: K tile (2 K-major atoms) or V tile (2 MN slices)
-constexpr int kT2OffK = 32768;                      // after Q (2 atoms of 128 rows x 128 B)
-constexpr int kT2OffV = kT2OffK + 2 * kT2Slot;
-constexpr int kT2OffP = kT2OffV + 2 * kT2Slot;
-constexpr int kT2Grp = kT2OffP + 128 * kT2NK * 2;   // 112 KB per group
-constexpr int kT2OffBar = 2 * kT2Grp;
-constexpr size_t kSmemT2 = kT2OffBar + 1024 + 64 + 1024;  // barriers + anc, TMEM holder, alignment
+// GRP work items per CTA (independent groups of 6 warps), KST / VST K / V ring stages, PB P
+// buffers per group.  <2, 2, 2, 1>: two items in flight, 112 KB each; <1, 4, 4, 2>: one item
+// with deep rings (192 KB: ~4 tiles of K and V in flight per SM)
+template <int GRP, int KST, int VST, int PB>
+struct TcPlan {
+  static constexpr int kThreads = GRP * 192;
+  static constexpr int kOffK = 32768;               // after Q (2 atoms of 128 rows x 128 B)
+  static constexpr int kOffV = kOffK + KST * kT2Slot;
+  static constexpr int kOffP = kOffV + VST * kT2Slot;
+  static constexpr int kGrp = kOffP + PB * 128 * kT2NK * 2;
+  static constexpr int kOffBar = GRP * kGrp;
+  static constexpr size_t kSmem = kOffBar + 1536 + 1024;  // barriers + anc + TMEM holder, alignment
+  static_assert(kSmem <= 232448, "smem");
+  static_assert(2 + 2 * KST + 2 * VST + 4 + 2 * PB + 3 <= 32, "barriers per group");
+};
 
-__global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_constant__ TaTcMaps maps, TaParams p) {
+template <int GRP, int KST, int VST, int PB>
+__global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_constant__ TaTcMaps maps, TaParams p) {
+  using Plan = TcPlan<GRP, KST, VST, PB>;
+  constexpr int kT2OffK = Plan::kOffK, kT2OffV = Plan::kOffV, kT2OffP = Plan::kOffP, kT2Grp = Plan::kGrp;
+  constexpr int kT2OffBar = Plan::kOffBar;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = warp / 6, role = warp - grp * 6;
   uint8_t* gs = smem + grp * kT2Grp;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kT2OffBar);
-  uint64_t* gb = bars + grp * 24;
+  uint64_t* gb = bars + grp * 32;
   uint64_t* q_full = gb + 0;
   uint64_t* q_free = gb + 1;
-  uint64_t* k_full = gb + 2;   // [2]
-  uint64_t* k_empty = gb + 4;  // [2]
-  uint64_t* v_full = gb + 6;   // [2]
-  uint64_t* v_empty = gb + 8;  // [2]
-  uint64_t* s_full = gb + 10;  // [2]
-  uint64_t* s_free = gb + 12;  // [2]
-  uint64_t* p_full = gb + 14;
-  uint64_t* p_free = gb + 15;
-  uint64_t* o_ready = gb + 16;
-  uint64_t* o_done = gb + 17;
-  uint64_t* o_free = gb + 18;
-  uint64_t* anc = bars + 48 + grp * 40;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 128);
+  uint64_t* k_full = gb + 2;                 // [KST]
+  uint64_t* k_empty = k_full + KST;          // [KST]
+  uint64_t* v_full = k_empty + KST;          // [VST]
+  uint64_t* v_empty = v_full + VST;          // [VST]
+  uint64_t* s_full = v_empty + VST;          // [2]
+  uint64_t* s_free = s_full + 2;             // [2]
+  uint64_t* p_full = s_free + 2;             // [PB]
+  uint64_t* p_free = p_full + PB;            // [PB]
+  uint64_t* o_ready = p_free + PB;
+  uint64_t* o_done = o_ready + 1;
+  uint64_t* o_free = o_done + 1;
+  uint64_t* anc = bars + 64 + grp * 40;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 160);
   const int G = p.G, N1 = p.N1;
   const int nwork = p.R * p.Hkv;
 
   if (threadIdx.x == 0) {
-    for (int g2 = 0; g2 < 2; ++g2) {
-      uint64_t* b = bars + g2 * 24;
-      for (int k = 0; k < 10; ++k) mbar_init(&b[k], 1);   // q_full..v_empty
-      for (int k = 10; k < 12; ++k) mbar_init(&b[k], 1);  // s_full
-      for (int k = 12; k < 14; ++k) mbar_init(&b[k], 128);  // s_free
-      mbar_init(&b[14], 128);  // p_full
-      mbar_init(&b[15], 1);    // p_free
-      mbar_init(&b[16], 1);    // o_ready
-      mbar_init(&b[17], 1);    // o_done
-      mbar_init(&b[18], 128);  // o_free
+    for (int g2 = 0; g2 < GRP; ++g2) {
+      uint64_t* b = bars + g2 * 32;
+      int o = 0;
+      for (int k = 0; k < 2 + 2 * KST + 2 * VST + 2; ++k) mbar_init(&b[o++], 1);  // q, k, v rings, s_full
+      for (int k = 0; k < 2; ++k) mbar_init(&b[o++], 128);                          // s_free
+      for (int k = 0; k < PB; ++k) mbar_init(&b[o++], 128);                         // p_full
+      for (int k = 0; k < PB; ++k) mbar_init(&b[o++], 1);                           // p_free
+      mbar_init(&b[o++], 1);    // o_ready
+      mbar_init(&b[o++], 1);    // o_done
+      mbar_init(&b[o++], 128);  // o_free
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  if (warp == 1) tmem_alloc<GRP * 256>(tmem_holder);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder + grp * 256;  // S0 +0, S1 +64, O +128
-  const int wstep = 2 * gridDim.x;
+  const int wstep = GRP * gridDim.x;
 
   if (role == 0) {
     // ---------------------------------------------------------------- TMA producer
@@ -1297,7 +1309,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_const
       }
       uint32_t kc = 0, vc = 0;
       int wi = 0;
-      for (int w = 2 * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
+      for (int w = GRP * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
         const int r = w / p.Hkv, hk = w - r * p.Hkv;
         int p0, Pr;
         prefix_of(p, r, p0, Pr, hk == 0);
@@ -1310,14 +1322,14 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_const
           const CUtensorMap* mk = j < npt ? &maps.Kp : &maps.Kt;
           const CUtensorMap* mv = j < npt ? &maps.Vp : &maps.Vt;
           const int z = j < npt ? p0 + j * kT2NK : r * N1;
-          const uint32_t ks = kc & 1, vs = vc & 1;
-          if (kc >= 2) mbar_wait_sleep(&k_empty[ks], ((kc >> 1) & 1) ^ 1);
+          const uint32_t ks = kc % KST, vs = vc % VST;
+          if (kc >= KST) mbar_wait_sleep(&k_empty[ks], ((kc / KST) & 1) ^ 1);
           mbar_arrive_expect_tx(&k_full[ks], kT2Slot);
           uint8_t* kd = gs + kT2OffK + ks * kT2Slot;
           tma_load_3d(mk, &k_full[ks], kd, 0, hk, z);
           tma_load_3d(mk, &k_full[ks], kd + kT2NK * 128, 64, hk, z);
           ++kc;
-          if (vc >= 2) mbar_wait_sleep(&v_empty[vs], ((vc >> 1) & 1) ^ 1);
+          if (vc >= VST) mbar_wait_sleep(&v_empty[vs], ((vc / VST) & 1) ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], kT2Slot);
           uint8_t* vd = gs + kT2OffV + vs * kT2Slot;
           tma_load_3d(mv, &v_full[vs], vd, 0, hk, z);
@@ -1335,30 +1347,31 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_const
       uint32_t kc = 0, vc = 0, sc = 0, pc = 0;
       int wi = 0;
       auto pv_issue = [&](int jj) {
-        const uint32_t vs = vc & 1;
-        mbar_wait(&v_full[vs], (vc >> 1) & 1);
-        mbar_wait(p_full, pc & 1);
+        const uint32_t vs = vc % VST, pbuf = pc % PB;
+        mbar_wait(&v_full[vs], (vc / VST) & 1);
+        mbar_wait(&p_full[pbuf], (pc / PB) & 1);
         if (jj == 0 && wi > 0) mbar_wait(o_free, (wi - 1) & 1);  // the epilogue read the previous O
         tc_fence_after();
         const uint32_t vb = smem_u32(gs + kT2OffV + vs * kT2Slot);
 #pragma unroll
         for (int kk = 0; kk < kT2NK / 16; ++kk)
-          umma_bf16(tmem + 128, kmaj_desc(aP, kk, 128), mnmaj_desc(vb, kk, kT2NK), idPV, (jj > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(p_free);
+          umma_bf16(tmem + 128, kmaj_desc(aP + pbuf * (128 * kT2NK * 2), kk, 128), mnmaj_desc(vb, kk, kT2NK), idPV,
+                    (jj > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&p_free[pbuf]);
         umma_commit(&v_empty[vs]);
         umma_commit(o_ready);
         ++vc;
         ++pc;
       };
-      for (int w = 2 * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
+      for (int w = GRP * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
         const int r = w / p.Hkv;
         int p0, Pr;
         prefix_of(p, r, p0, Pr, false);
         const int nt = (Pr + kT2NK - 1) / kT2NK + 1;
         mbar_wait(q_full, wi & 1);
         for (int j = 0; j < nt; ++j) {
-          const uint32_t ks = kc & 1, sb = sc & 1;
-          mbar_wait(&k_full[ks], (kc >> 1) & 1);
+          const uint32_t ks = kc % KST, sb = sc & 1;
+          mbar_wait(&k_full[ks], (kc / KST) & 1);
           if (sc >= 2) mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t kb = smem_u32(gs + kT2OffK + ks * kT2Slot);
@@ -1387,7 +1400,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_const
     const int st_id = (role - 2) * 32 + lane;  // 0..127
     uint32_t sc = 0, pvc = 0;
     int wi = 0;
-    for (int w = 2 * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
+    for (int w = GRP * blockIdx.x + grp; w < nwork; w += wstep, ++wi) {
       const int r = w / p.Hkv, hk = w - r * p.Hkv;
       int p0, Pr;
       prefix_of(p, r, p0, Pr, false);
@@ -1478,17 +1491,19 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_const
           w32[h] = pk_bf16(e0, e1);
         }
         l += s0 + s1;
-        if (pvc >= 1) mbar_wait(p_free, (pvc - 1) & 1);  // the previous P V has read P
+        const uint32_t pbuf = pvc % PB;
+        if (pvc >= PB) mbar_wait(&p_free[pbuf], ((pvc / PB) & 1) ^ 1);  // the P V that last read this buffer
+        const uint32_t prow = aProw + pbuf * (128 * kT2NK * 2);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const uint32_t ch = static_cast<uint32_t>(c ^ (i & 7));
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(aProw + ch * 16), "r"(w32[4 * c]),
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(w32[4 * c]),
                        "r"(w32[4 * c + 1]), "r"(w32[4 * c + 2]), "r"(w32[4 * c + 3])
                        : "memory");
         }
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(p_full);
+        mbar_arrive(&p_full[pbuf]);
         ++pvc;
       }
       // epilogue: O / l -> bf16 global, lse
@@ -1523,7 +1538,7 @@ __global__ void __launch_bounds__(kT2Threads, 1) k_ta_fwd_tc2(const __grid_const
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<512>(*tmem_holder);
+    tmem_dealloc<GRP * 256>(*tmem_holder);
   }
 }
 
@@ -1677,15 +1692,22 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
     static bool tattr = false;
     if (!tattr) {
       cudaFuncSetAttribute(k_ta_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTc);
-      cudaFuncSetAttribute(k_ta_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemT2);
+      cudaFuncSetAttribute(k_ta_fwd_tc2<2, 2, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcPlan<2, 2, 2, 1>::kSmem);
+      cudaFuncSetAttribute(k_ta_fwd_tc2<1, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcPlan<1, 4, 4, 2>::kSmem);
       tattr = true;
     }
     const int work = p.R * p.Hkv;
     prof_begin(PH_TREE_FWD_TC, s);
     if (tcmode == 1)
       k_ta_fwd_tc<<<std::min(work, kNumSMs), kTcThreads, kSmemTc, s>>>(maps, p);
+    else if (tcmode == 2)
+      k_ta_fwd_tc2<2, 2, 2, 1><<<std::min((work + 1) / 2, kNumSMs), TcPlan<2, 2, 2, 1>::kThreads,
+                                  TcPlan<2, 2, 2, 1>::kSmem, s>>>(maps, p);
     else
-      k_ta_fwd_tc2<<<std::min((work + 1) / 2, kNumSMs), kT2Threads, kSmemT2, s>>>(maps, p);
+      k_ta_fwd_tc2<1, 4, 4, 2><<<std::min(work, kNumSMs), TcPlan<1, 4, 4, 2>::kThreads,
+                                  TcPlan<1, 4, 4, 2>::kSmem, s>>>(maps, p);
     count_launch();
     prof_end(PH_TREE_FWD_TC, s);
     return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
