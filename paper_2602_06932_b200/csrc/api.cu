@@ -101,6 +101,7 @@ struct Options {
   int scan_ctas = 2;                           // target-scan CTAs per SM (segments per row)
   int tree_fwd_tc = 0;                         // F4 fwd: 1 = tcgen05 kernel when G*(N+1) <= 128 (opt-in:
                                                // measured slower than the mma.sync kernel)
+  int tree_bwd_tc = 0;                         // F4 bwd: 1 = tcgen05 kernel when G*(N+1) <= 128
   int tree_bwd_split = 0;                      // F4 bwd: 1 = separate dQ / dK-dV kernels even when the
                                                // fused one applies (A/B and coverage of the general path)
   int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
@@ -122,6 +123,7 @@ struct Options {
     if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
     if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = std::min(3, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_TREE_BWD_SPLIT")) tree_bwd_split = atoi(e) ? 1 : 0;
+    if (const char* e = getenv("AURORA_TREE_BWD_TC")) tree_bwd_tc = atoi(e) ? 1 : 0;
   }
 };
 Options& opts() {
@@ -523,6 +525,7 @@ aurora_status_t bwd_fused(const void* H, const void* W, int64_t M, int64_t d, in
 }  // namespace
 int opt_tree_bwd_split() { return opts().tree_bwd_split; }
 int opt_tree_fwd_tc() { return opts().tree_fwd_tc; }
+int opt_tree_bwd_tc() { return opts().tree_bwd_tc; }
 }  // namespace aur
 
 using namespace aur;
@@ -559,6 +562,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "tree_fwd_tc") == 0 && value >= 0 && value <= 3) {
     o.tree_fwd_tc = static_cast<int>(value);
+    return AURORA_OK;
+  }
+  if (std::strcmp(name, "tree_bwd_tc") == 0 && (value == 0 || value == 1)) {
+    o.tree_bwd_tc = static_cast<int>(value);
     return AURORA_OK;
   }
   if (std::strcmp(name, "tree_bwd_split") == 0 && (value == 0 || value == 1)) {
@@ -611,6 +618,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "bwd_mode") == 0) return o.bwd_mode;
   if (std::strcmp(name, "tree_bwd_split") == 0) return o.tree_bwd_split;
   if (std::strcmp(name, "tree_fwd_tc") == 0) return o.tree_fwd_tc;
+  if (std::strcmp(name, "tree_bwd_tc") == 0) return o.tree_bwd_tc;
   if (std::strcmp(name, "bwd_concurrent") == 0) return o.bwd_concurrent;
   if (std::strcmp(name, "tile_n") == 0) return o.tile_n;
   if (std::strcmp(name, "dz_chunk_bytes") == 0) return o.dz_chunk_bytes;

@@ -259,6 +259,7 @@ enum Phase : int { PH_SCAN = 0, PH_VERIFY, PH_FWD_GEMM, PH_FWD_COMBINE, PH_BWD_D
 void prof_begin(int phase, cudaStream_t s);
 int opt_tree_bwd_split();  // aurora_set_option("tree_bwd_split")
 int opt_tree_fwd_tc();     // aurora_set_option("tree_fwd_tc")
+int opt_tree_bwd_tc();     // aurora_set_option("tree_bwd_tc")
 void prof_end(int phase, cudaStream_t s);
 
 }  // namespace aur

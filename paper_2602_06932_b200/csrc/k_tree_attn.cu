@@ -1542,6 +1542,343 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
   }
 }
 
+// ------------------------------------------------------------------------------ tcgen05 backward
+// k_ta_bwd_tc: the one-kernel backward on the tensor cores.  Work item = (request, KV head) with
+// all its G (N+1) <= 128 query rows (so every key's dK / dV is complete after one tile step: no
+// atomics), one item per CTA and SM, key tiles of 64.  Per tile j the MMA warp issues
+//   S = Q K^T and dP = dO V^T                       (M 128 rows, N 64 keys, K 128 dh)  -> TMEM
+// and, once the compute warps wrote P and dS = scale P (dP - D) (bf16, shared memory):
+//   dV^T = dO^T P, dK^T = Q^T dS                    (M 128 dh, N 64 keys, K 128 rows)  -> TMEM
+//   dQ += dS K                                      (M 128 rows, N 128 dh, K 64 keys)  -> TMEM
+// every operand read straight from the swizzled tiles TMA loaded: Q / dO serve as K-major A
+// (rows x dh) and as MN-major A (dh x rows); the K tile as K-major B (keys x dh) and MN-major B
+// (dh x keys); P / dS as K-major A and MN-major B.  The 4 compute warps (thread = row for the
+// softmax, = dh lane for the dK / dV epilogue) overlap the next tile's softmax with the
+// gradient MMAs of the previous one (S, dP and P / dS double-buffered).
+// TMEM columns: S[2] 0 / 64, dP[2] 128 / 192, dQ 256..383, dV^T 384..447, dK^T 448..511.
+struct TaBwdMaps {
+  CUtensorMap Q, dO, Kp, Vp, Kt, Vt;
+};
+constexpr int kTbOffQ = 0, kTbOffDO = 32768, kTbOffK = 65536;
+constexpr int kTbOffV = kTbOffK + 2 * kT2Slot;
+constexpr int kTbOffP = kTbOffV + 2 * kT2Slot;     // 2 x [128 rows x 64 keys] bf16
+constexpr int kTbOffDS = kTbOffP + 2 * 16384;
+constexpr int kTbOffBar = kTbOffDS + 2 * 16384;    // 192 KB
+constexpr size_t kSmemTb = kTbOffBar + 1024 + 1024;
+
+__global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ TaBwdMaps maps, TaParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTbOffBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_free = bars + 1;
+  uint64_t* k_full = bars + 2;    // [2]
+  uint64_t* k_empty = bars + 4;   // [2]
+  uint64_t* v_full = bars + 6;    // [2]
+  uint64_t* v_empty = bars + 8;   // [2]
+  uint64_t* s_full = bars + 10;   // [2] S and dP of a tile in TMEM
+  uint64_t* s_free = bars + 12;   // [2]
+  uint64_t* pd_full = bars + 14;  // [2] P and dS of a tile in smem
+  uint64_t* pd_free = bars + 16;  // [2]
+  uint64_t* kv_full = bars + 18;  // dV^T, dK^T of a tile in TMEM
+  uint64_t* kv_free = bars + 19;
+  uint64_t* dq_done = bars + 20;
+  uint64_t* dq_free = bars + 21;
+  uint64_t* anc = bars + 32;      // [40]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 80);
+  const int G = p.G, N1 = p.N1;
+  const int nwork = p.R * p.Hkv;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 12; ++k) mbar_init(&bars[k], 1);
+    for (int k = 12; k < 14; ++k) mbar_init(&bars[k], 128);  // s_free
+    for (int k = 14; k < 16; ++k) mbar_init(&bars[k], 128);  // pd_full
+    for (int k = 16; k < 18; ++k) mbar_init(&bars[k], 1);    // pd_free
+    mbar_init(kv_full, 1);
+    mbar_init(kv_free, 128);
+    mbar_init(dq_done, 1);
+    mbar_init(dq_free, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_holder);
+  {  // rows >= G (N+1) of the Q / dO tiles are never loaded but feed the dV^T / dK^T sums over
+     // rows (times P = dS = 0): zero them once so stale shared memory cannot inject NaN
+    const int rows = G * N1;
+    for (int idx = threadIdx.x; idx < (128 - rows) * 4 * 8; idx += blockDim.x) {
+      const int row = rows + idx / 32, part = (idx / 8) & 3, c = idx & 7;
+      const int off = (part >> 1) * kTbOffDO + (part & 1) * 16384 + row * 128 + c * 16;
+      *reinterpret_cast<uint4*>(smem + off) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      tma_prefetch_desc(&maps.Q);
+      tma_prefetch_desc(&maps.dO);
+      tma_prefetch_desc(&maps.Kp);
+      tma_prefetch_desc(&maps.Vp);
+      tma_prefetch_desc(&maps.Kt);
+      tma_prefetch_desc(&maps.Vt);
+      uint32_t kc = 0, vc = 0;
+      int wi = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++wi) {
+        const int r = w / p.Hkv, hk = w - r * p.Hkv;
+        int p0, Pr;
+        prefix_of(p, r, p0, Pr, false);
+        const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
+        if (wi > 0) mbar_wait_sleep(q_free, (wi - 1) & 1);
+        mbar_arrive_expect_tx(q_full, 4u * 128u * G * N1);
+        tma_load_3d(&maps.Q, q_full, smem + kTbOffQ, 0, hk * G, r * N1);
+        tma_load_3d(&maps.Q, q_full, smem + kTbOffQ + 16384, 64, hk * G, r * N1);
+        tma_load_3d(&maps.dO, q_full, smem + kTbOffDO, 0, hk * G, r * N1);
+        tma_load_3d(&maps.dO, q_full, smem + kTbOffDO + 16384, 64, hk * G, r * N1);
+        for (int j = 0; j < nt; ++j) {
+          const CUtensorMap* mk = j < npt ? &maps.Kp : &maps.Kt;
+          const CUtensorMap* mv = j < npt ? &maps.Vp : &maps.Vt;
+          const int z = j < npt ? p0 + j * kT2NK : r * N1;
+          const uint32_t ks = kc & 1, vs = vc & 1;
+          if (kc >= 2) mbar_wait_sleep(&k_empty[ks], ((kc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[ks], kT2Slot);
+          uint8_t* kd = smem + kTbOffK + ks * kT2Slot;
+          tma_load_3d(mk, &k_full[ks], kd, 0, hk, z);
+          tma_load_3d(mk, &k_full[ks], kd + kT2NK * 128, 64, hk, z);
+          ++kc;
+          if (vc >= 2) mbar_wait_sleep(&v_empty[vs], ((vc >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&v_full[vs], kT2Slot);
+          uint8_t* vd = smem + kTbOffV + vs * kT2Slot;
+          tma_load_3d(mv, &v_full[vs], vd, 0, hk, z);
+          tma_load_3d(mv, &v_full[vs], vd + kT2NK * 128, 64, hk, z);
+          ++vc;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, kT2NK, false, false);     // S, dP
+      constexpr uint32_t idT = umma_idesc_bf16(128, kT2NK, true, true);       // dV^T, dK^T
+      constexpr uint32_t idQ = umma_idesc_bf16(128, 128, false, true);        // dQ
+      const uint32_t aQ = smem_u32(smem + kTbOffQ), aDO = smem_u32(smem + kTbOffDO);
+      uint32_t kc = 0, vc = 0, sc = 0, gc = 0;  // K / V loads consumed, S tiles issued, gradient steps issued
+      int wi = 0;
+      for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++wi) {
+        const int r = w / p.Hkv;
+        int p0, Pr;
+        prefix_of(p, r, p0, Pr, false);
+        const int nt = (Pr + kT2NK - 1) / kT2NK + 1;
+        mbar_wait(q_full, wi & 1);
+        uint32_t kslot_prev = 0;
+        auto grad = [&](int jj, uint32_t kslot) {  // gradient MMAs of tile jj (P / dS written)
+          const uint32_t pb = gc & 1;
+          mbar_wait(&pd_full[pb], (gc >> 1) & 1);
+          if (gc >= 1) mbar_wait(kv_free, (gc - 1) & 1);            // the epilogue read dV^T / dK^T
+          if (jj == 0 && wi > 0) mbar_wait(dq_free, (wi - 1) & 1);  // the epilogue read the last dQ
+          tc_fence_after();
+          const uint32_t aP = smem_u32(smem + kTbOffP + pb * 16384), aS = smem_u32(smem + kTbOffDS + pb * 16384);
+          const uint32_t kb = smem_u32(smem + kTbOffK + kslot * kT2Slot);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // K = 128 rows
+            umma_bf16(tmem + 384, mnmaj_desc(aDO, kk, 128), mnmaj_desc(aP, kk, 128), idT, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + 448, mnmaj_desc(aQ, kk, 128), mnmaj_desc(aS, kk, 128), idT, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < kT2NK / 16; ++kk)  // K = 64 keys
+            umma_bf16(tmem + 256, kmaj_desc(aS, kk, 128), mnmaj_desc(kb, kk, kT2NK), idQ, (jj > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(kv_full);
+          umma_commit(&pd_free[pb]);
+          umma_commit(&k_empty[kslot]);  // K: S and dQ done
+          ++gc;
+        };
+        for (int j = 0; j < nt; ++j) {
+          const uint32_t ks = kc & 1, vs = vc & 1, sb = sc & 1;
+          mbar_wait(&k_full[ks], (kc >> 1) & 1);
+          mbar_wait(&v_full[vs], (vc >> 1) & 1);
+          if (sc >= 2) mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t kb = smem_u32(smem + kTbOffK + ks * kT2Slot), vb = smem_u32(smem + kTbOffV + vs * kT2Slot);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + sb * kT2NK, kmaj_desc(aQ, kk, 128), kmaj_desc(kb, kk, kT2NK), idS, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_bf16(tmem + 128 + sb * kT2NK, kmaj_desc(aDO, kk, 128), kmaj_desc(vb, kk, kT2NK), idS, kk > 0);
+          umma_commit(&s_full[sb]);
+          umma_commit(&v_empty[vs]);  // V: dP done
+          ++vc;
+          ++sc;
+          if (j >= 1) grad(j - 1, kslot_prev);
+          kslot_prev = ks;
+          ++kc;
+        }
+        grad(nt - 1, kslot_prev);
+        umma_commit(dq_done);
+        umma_commit(q_free);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- compute (4 warps)
+    const int q4 = warp & 3;
+    const int i = q4 * 32 + lane;  // row (softmax) or dh lane (dK / dV epilogue)
+    const int rows = G * N1;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
+    const float c2 = p.c2, scale = p.scale;
+    const int st_id = (warp - 2) * 32 + lane;
+    uint32_t sc = 0, gc = 0;
+    int wi = 0;
+    for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++wi) {
+      const int r = w / p.Hkv, hk = w - r * p.Hkv;
+      int p0, Pr;
+      prefix_of(p, r, p0, Pr, false);
+      const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
+      if (st_id < N1) {
+        const int s = st_id;
+        const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
+        bool bad = nn < 0 || nn > p.N;
+        uint64_t m = 0;
+        if (!bad) {
+          if (s == 0) {
+            m = 1ull;
+          } else if (s - 1 < nn) {
+            int cur = s - 1;
+            m = 1ull | (1ull << s);
+            for (int k = 0; k <= p.N; ++k) {
+              const int par = p.parents ? p.parents[(size_t)r * p.N + cur] : cur - 1;
+              if (par < -1 || par >= cur) { bad = true; break; }
+              if (par < 0) break;
+              m |= 1ull << (par + 1);
+              cur = par;
+            }
+          }
+        }
+        anc[s] = bad ? 0ull : m;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int s_row = i / G, g = i - s_row * G;
+      const uint64_t a = i < rows ? anc[s_row] : 0ull;
+      const size_t rix = ((size_t)r * N1 + s_row) * p.Hq + hk * G + g;
+      const float lse2 = (a != 0ull) ? p.lse[rix] * kLog2e : 0.f;
+      const float Di = (a != 0ull) ? p.Dsum[rix] : 0.f;
+      const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
+      auto epilogue = [&](int jj) {  // dV^T / dK^T of tile jj -> global (thread = dh lane i)
+        mbar_wait(kv_full, gc & 1);
+        tc_fence_after();
+        uint32_t dv[2][32], dk[2][32];
+        tmem_ld_32x32b_x32(trow + 384, dv[0]);
+        tmem_ld_32x32b_x32(trow + 384 + 32, dv[1]);
+        tmem_ld_32x32b_x32(trow + 448, dk[0]);
+        tmem_ld_32x32b_x32(trow + 448 + 32, dk[1]);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(kv_free);
+        ++gc;
+        const bool tree = jj == npt;
+        const int nkeys = tree ? N1 : min(kT2NK, Pr - jj * kT2NK);
+        uint16_t* gdv = tree ? p.dVt : p.dVp;
+        uint16_t* gdk = tree ? p.dKt : p.dKp;
+        const int64_t key0 = tree ? (int64_t)r * N1 : (int64_t)p0 + jj * kT2NK;
+#pragma unroll
+        for (int t = 0; t < kT2NK; ++t) {  // unrolled: register-indexed dv / dk
+          if (t < nkeys) {
+            const int64_t o = ((key0 + t) * p.Hkv + hk) * D + i;
+            gdv[o] = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dv[t >> 5][t & 31])));
+            gdk[o] = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dk[t >> 5][t & 31])));
+          }
+        }
+      };
+      (void)nn;
+      for (int j = 0; j < nt; ++j, ++sc) {
+        const uint32_t sb = sc & 1;
+        const bool tree = j == npt;
+        const int lim = tree ? 0 : Pr - j * kT2NK;
+        mbar_wait(&s_full[sb], (sc >> 1) & 1);
+        tc_fence_after();
+        uint32_t sv[2][32], dp[2][32];
+        tmem_ld_32x32b_x32(trow + sb * kT2NK, sv[0]);
+        tmem_ld_32x32b_x32(trow + sb * kT2NK + 32, sv[1]);
+        tmem_ld_32x32b_x32(trow + 128 + sb * kT2NK, dp[0]);
+        tmem_ld_32x32b_x32(trow + 128 + sb * kT2NK + 32, dp[1]);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&s_free[sb]);
+        const bool full = a != 0ull && !tree && lim >= kT2NK;
+        uint32_t pw[32], dw[32];
+#pragma unroll
+        for (int h = 0; h < 32; ++h) {
+          float pv[2], dv2[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int e = 2 * h + u;
+            bool ok;
+            if (full) ok = true;
+            else if (tree) ok = (a >> e) & 1ull;
+            else ok = a != 0ull && e < lim;
+            const float x = __uint_as_float(e < 32 ? sv[0][e] : sv[1][e - 32]);
+            const float dpe = __uint_as_float(e < 32 ? dp[0][e] : dp[1][e - 32]);
+            const float pe = ok ? ex2_approx(fmaf(x, c2, -lse2)) : 0.f;
+            pv[u] = pe;
+            dv2[u] = ok ? scale * pe * (dpe - Di) : 0.f;  // never 0 * (NaN) from unused rows
+          }
+          pw[h] = pk_bf16(pv[0], pv[1]);
+          dw[h] = pk_bf16(dv2[0], dv2[1]);
+        }
+        const uint32_t pb = (sc) & 1;
+        if (sc >= 2) mbar_wait(&pd_free[pb], ((sc >> 1) & 1) ^ 1);
+        const uint32_t prow = smem_u32(smem + kTbOffP + pb * 16384) + i * 128;
+        const uint32_t drow = smem_u32(smem + kTbOffDS + pb * 16384) + i * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t ch = static_cast<uint32_t>(c ^ (i & 7));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(pw[4 * c]),
+                       "r"(pw[4 * c + 1]), "r"(pw[4 * c + 2]), "r"(pw[4 * c + 3])
+                       : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(drow + ch * 16), "r"(dw[4 * c]),
+                       "r"(dw[4 * c + 1]), "r"(dw[4 * c + 2]), "r"(dw[4 * c + 3])
+                       : "memory");
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&pd_full[pb]);
+        if (j >= 1) epilogue(j - 1);
+      }
+      epilogue(nt - 1);
+      // dQ (thread = row): fp32 [row][dh]
+      mbar_wait(dq_done, wi & 1);
+      tc_fence_after();
+      uint32_t dq[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(trow + 256 + c * 32, dq[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(dq_free);
+      if (i < rows) {
+        float* out = p.dQ + rix * D;
+        const bool live = a != 0ull;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<float4*>(out + c * 32 + q * 4) =
+                live ? make_float4(__uint_as_float(dq[c][4 * q]), __uint_as_float(dq[c][4 * q + 1]),
+                                   __uint_as_float(dq[c][4 * q + 2]), __uint_as_float(dq[c][4 * q + 3]))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // anc is rewritten by the next item
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 // ------------------------------------------------------------------------------ tree RoPE
 // Block per tree row (request r, row s): position P_r + depth(s) (F4-R6; siblings share it),
 // cos/sin of pos * theta^(-2i/dh) for the dh/2 frequencies computed once in double into shared
@@ -1769,6 +2106,32 @@ extern "C" aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, co
     attr = true;
   }
   const int64_t n_rows = (int64_t)p.R * p.N1 * p.Hq;
+  if (p.G * p.N1 <= 128 && opt_tree_bwd_tc() && !opt_tree_bwd_split()) {
+    TaBwdMaps maps;
+    const uint64_t rows_t = (uint64_t)p.R * p.N1;
+    const uint64_t ptot = ta->prefix_total > 0 ? (uint64_t)ta->prefix_total : 1;
+    const void* kp = ta->prefix_total > 0 ? Kp : Kt;
+    const void* vp = ta->prefix_total > 0 ? Vp : Vt;
+    bool ok = make_tmap_bf16_3d(&maps.Q, Q, D, p.Hq, rows_t, D, (uint64_t)p.Hq * D, 64, p.G, p.N1) &&
+              make_tmap_bf16_3d(&maps.dO, dO, D, p.Hq, rows_t, D, (uint64_t)p.Hq * D, 64, p.G, p.N1) &&
+              make_tmap_bf16_3d(&maps.Kp, kp, D, p.Hkv, ptot, D, (uint64_t)p.Hkv * D, 64, 1, kT2NK) &&
+              make_tmap_bf16_3d(&maps.Vp, vp, D, p.Hkv, ptot, D, (uint64_t)p.Hkv * D, 64, 1, kT2NK) &&
+              make_tmap_bf16_3d(&maps.Kt, Kt, D, p.Hkv, rows_t, D, (uint64_t)p.Hkv * D, 64, 1, kT2NK) &&
+              make_tmap_bf16_3d(&maps.Vt, Vt, D, p.Hkv, rows_t, D, (uint64_t)p.Hkv * D, 64, 1, kT2NK);
+    if (!ok) return AURORA_ERR_CUDA;
+    static bool tattr = false;
+    if (!tattr) {
+      cudaFuncSetAttribute(k_ta_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemTb);
+      tattr = true;
+    }
+    const int work = p.R * p.Hkv;
+    prof_begin(PH_TREE_BWD_FUSED, s);
+    k_ta_dsum<<<(unsigned)((n_rows + 7) / 8), 256, 0, s>>>(p.O, p.dO, (float*)ws, n_rows);
+    k_ta_bwd_tc<<<std::min(work, kNumSMs), 192, kSmemTb, s>>>(maps, p);
+    prof_end(PH_TREE_BWD_FUSED, s);
+    count_launch(2);
+    return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
+  }
   if (p.G * p.N1 <= 128 && !opt_tree_bwd_split()) {
     static bool fattr = false;
     if (!fattr) {

@@ -239,3 +239,39 @@ def test_malformed_prefix_offsets_flag_range_without_oob():
     assert torch.isfinite(O.float()).all() and torch.isfinite(dQ).all()
     for g in (dKp_all, dVp_all):
         assert bool((g[:guard].float() == 7.0).all()) and bool((g[guard + total:].float() == 7.0).all())
+
+
+@pytest.mark.parametrize("fwd_tc", [0, 3])
+@pytest.mark.parametrize("name", ["ta_small", "ta_chain", "ta_gqa8"])
+def test_tree_attention_tcgen05_backward(name, fwd_tc):
+    """The tcgen05 backward (option tree_bwd_tc: S / dP / dV^T / dK^T / dQ on the tensor cores,
+    TMEM accumulators, TMA-fed tiles) after either forward, against the f64 oracle."""
+    from paper_2602_06932_b200 import aurora as A
+    inp = tracegen.gen_tree_attn(name)
+    saved = (A.aurora_get_option("tree_fwd_tc"), A.aurora_get_option("tree_bwd_tc"))
+    A.aurora_set_option("tree_fwd_tc", fwd_tc)
+    A.aurora_set_option("tree_bwd_tc", 1)
+    try:
+        got = _run(inp)
+    finally:
+        A.aurora_set_option("tree_fwd_tc", saved[0])
+        A.aurora_set_option("tree_bwd_tc", saved[1])
+    ref = TA.fwd_bwd(inp)
+    _compare(got, ref, np.arange(len(inp["requests"])), inp["prefix_off"])
+
+
+@pytest.mark.parametrize("name,sample", [("ta_llama", [0, 37, 63]), ("ta_tree", [0, 511, 1023])])
+def test_tree_attention_tcgen05_full_size_sampled(name, sample):
+    from paper_2602_06932_b200 import aurora as A
+    inp = tracegen.gen_tree_attn(name)
+    saved = (A.aurora_get_option("tree_fwd_tc"), A.aurora_get_option("tree_bwd_tc"))
+    A.aurora_set_option("tree_fwd_tc", 3)
+    A.aurora_set_option("tree_bwd_tc", 1)
+    try:
+        got = _run(inp)
+    finally:
+        A.aurora_set_option("tree_fwd_tc", saved[0])
+        A.aurora_set_option("tree_bwd_tc", saved[1])
+    ref = TA.fwd_bwd(tracegen.gen_tree_attn(name, requests=sample))
+    _compare(got, ref, np.asarray(sample), inp["prefix_off"])
+    assert not torch.isnan(got["dKp"]).any() and not torch.isnan(got["dVp"]).any()
