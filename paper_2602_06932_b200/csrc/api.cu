@@ -107,6 +107,7 @@ struct Options {
   int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
                                                // slower at M = 384: 0.507 vs 0.470 ms; opt-in)
   int gram_norm = 1;                           // F3 fused: Gram-form global norm when M is small
+  int dw_adamw_qe = 1;                         // F3 fused state entries: 0 = 128 x 32, 1 = 32 x 128, 2 = 32 x 64
   int debug_gemm_group = 0;                    // aurora_debug_gemm only: grouped raster (< 0: groups of n-tiles)
   int scan_ring = 0;                           // A2: 1 = persistent TMA-ring scan (measured slower: opt-in)
   int fwd_stage = 1;                           // Eq. 3: the fwd stages exp(z - m_half) in dZ^T so the
@@ -114,6 +115,7 @@ struct Options {
   Options() {
     if (const char* e = getenv("AURORA_FWD_STAGE")) fwd_stage = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_RING")) scan_ring = atoi(e) ? 1 : 0;
+    if (const char* e = getenv("AURORA_DW_ADAMW_QE")) dw_adamw_qe = std::min(2, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_DW_RESIDENT")) dw_resident = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_CTAS")) scan_ctas = std::max(1, atoi(e));
     if (const char* e = getenv("AURORA_DZ_CHUNK_BYTES")) dz_chunk_bytes = atoll(e);
@@ -121,7 +123,7 @@ struct Options {
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
     if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
-    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = std::min(3, std::max(0, atoi(e)));
+    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = std::min(5, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_TREE_BWD_SPLIT")) tree_bwd_split = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_TREE_BWD_TC")) tree_bwd_tc = atoi(e) ? 1 : 0;
   }
@@ -526,6 +528,7 @@ aurora_status_t bwd_fused(const void* H, const void* W, int64_t M, int64_t d, in
 int opt_tree_bwd_split() { return opts().tree_bwd_split; }
 int opt_tree_fwd_tc() { return opts().tree_fwd_tc; }
 int opt_tree_bwd_tc() { return opts().tree_bwd_tc; }
+int opt_dw_adamw_qe() { return opts().dw_adamw_qe; }
 }  // namespace aur
 
 using namespace aur;
@@ -560,7 +563,7 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
-  if (std::strcmp(name, "tree_fwd_tc") == 0 && value >= 0 && value <= 3) {
+  if (std::strcmp(name, "tree_fwd_tc") == 0 && value >= 0 && value <= 5) {
     o.tree_fwd_tc = static_cast<int>(value);
     return AURORA_OK;
   }
@@ -590,6 +593,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   }
   if (std::strcmp(name, "scan_ring") == 0 && (value == 0 || value == 1)) {
     o.scan_ring = static_cast<int>(value);
+    return AURORA_OK;
+  }
+  if (std::strcmp(name, "dw_adamw_qe") == 0 && value >= 0 && value <= 2) {
+    o.dw_adamw_qe = static_cast<int>(value);
     return AURORA_OK;
   }
   if (std::strcmp(name, "fwd_stage") == 0 && (value == 0 || value == 1)) {
@@ -626,6 +633,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "dw_resident") == 0) return o.dw_resident;
   if (std::strcmp(name, "fwd_stage") == 0) return o.fwd_stage;
   if (std::strcmp(name, "scan_ring") == 0) return o.scan_ring;
+  if (std::strcmp(name, "dw_adamw_qe") == 0) return o.dw_adamw_qe;
   if (std::strcmp(name, "debug_gemm_group") == 0) return o.debug_gemm_group;
   if (std::strcmp(name, "gram_norm") == 0) return o.gram_norm;
   if (std::strcmp(name, "pair_max_active_clusters") == 0) return g_pair_max_clusters;

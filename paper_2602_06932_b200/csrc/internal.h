@@ -260,6 +260,7 @@ void prof_begin(int phase, cudaStream_t s);
 int opt_tree_bwd_split();  // aurora_set_option("tree_bwd_split")
 int opt_tree_fwd_tc();     // aurora_set_option("tree_fwd_tc")
 int opt_tree_bwd_tc();     // aurora_set_option("tree_bwd_tc")
+int opt_dw_adamw_qe();     // aurora_set_option("dw_adamw_qe")
 void prof_end(int phase, cudaStream_t s);
 
 }  // namespace aur

@@ -1233,22 +1233,24 @@ constexpr int kT2Slot = kT2NK * 128 * 2;            // 16 KB: K tile (2 K-major 
 // GRP work items per CTA (independent groups of 6 warps), KST / VST K / V ring stages, PB P
 // buffers per group.  <2, 2, 2, 1>: two items in flight, 112 KB each; <1, 4, 4, 2>: one item
 // with deep rings (192 KB: ~4 tiles of K and V in flight per SM)
-template <int GRP, int KST, int VST, int PB>
+// PT: P stays in TMEM (bf16 pairs written over its own S buffer, the P V MMA reads A from TMEM):
+// no shared-memory P buffer, no proxy fence, no wait for the previous P V before writing P.
+template <int GRP, int KST, int VST, int PB, bool PT = false>
 struct TcPlan {
   static constexpr int kThreads = GRP * 192;
   static constexpr int kOffK = 32768;               // after Q (2 atoms of 128 rows x 128 B)
   static constexpr int kOffV = kOffK + KST * kT2Slot;
   static constexpr int kOffP = kOffV + VST * kT2Slot;
-  static constexpr int kGrp = kOffP + PB * 128 * kT2NK * 2;
+  static constexpr int kGrp = kOffP + (PT ? 0 : PB * 128 * kT2NK * 2);
   static constexpr int kOffBar = GRP * kGrp;
   static constexpr size_t kSmem = kOffBar + 1536 + 1024;  // barriers + anc + TMEM holder, alignment
   static_assert(kSmem <= 232448, "smem");
   static_assert(2 + 2 * KST + 2 * VST + 4 + 2 * PB + 3 <= 32, "barriers per group");
 };
 
-template <int GRP, int KST, int VST, int PB>
+template <int GRP, int KST, int VST, int PB, bool PT = false>
 __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_constant__ TaTcMaps maps, TaParams p) {
-  using Plan = TcPlan<GRP, KST, VST, PB>;
+  using Plan = TcPlan<GRP, KST, VST, PB, PT>;
   constexpr int kT2OffK = Plan::kOffK, kT2OffV = Plan::kOffV, kT2OffP = Plan::kOffP, kT2Grp = Plan::kGrp;
   constexpr int kT2OffBar = Plan::kOffBar;
   extern __shared__ uint8_t smem_raw[];
@@ -1353,11 +1355,19 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
         if (jj == 0 && wi > 0) mbar_wait(o_free, (wi - 1) & 1);  // the epilogue read the previous O
         tc_fence_after();
         const uint32_t vb = smem_u32(gs + kT2OffV + vs * kT2Slot);
+        if constexpr (PT) {
+          // P of tile jj sits in S buffer jj & 1 (pc counts tiles like sc): 8 columns per K = 16
+          const uint32_t aT = tmem + (pc & 1) * kT2NK;
 #pragma unroll
-        for (int kk = 0; kk < kT2NK / 16; ++kk)
-          umma_bf16(tmem + 128, kmaj_desc(aP + pbuf * (128 * kT2NK * 2), kk, 128), mnmaj_desc(vb, kk, kT2NK), idPV,
-                    (jj > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&p_free[pbuf]);
+          for (int kk = 0; kk < kT2NK / 16; ++kk)
+            umma_bf16_ts(tmem + 128, aT + kk * 8, mnmaj_desc(vb, kk, kT2NK), idPV, (jj > 0 || kk > 0) ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < kT2NK / 16; ++kk)
+            umma_bf16(tmem + 128, kmaj_desc(aP + pbuf * (128 * kT2NK * 2), kk, 128), mnmaj_desc(vb, kk, kT2NK), idPV,
+                      (jj > 0 || kk > 0) ? 1u : 0u);
+          umma_commit(&p_free[pbuf]);
+        }
         umma_commit(&v_empty[vs]);
         umma_commit(o_ready);
         ++vc;
@@ -1372,7 +1382,9 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
         for (int j = 0; j < nt; ++j) {
           const uint32_t ks = kc % KST, sb = sc & 1;
           mbar_wait(&k_full[ks], (kc / KST) & 1);
-          if (sc >= 2) mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
+          // PT: the buffer's previous P was read by the P V issued before this S (the tensor pipe
+          // runs one thread's MMAs in order), and that P V waited for the softmax's P
+          if (!PT && sc >= 2) mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t kb = smem_u32(gs + kT2OffK + ks * kT2Slot);
 #pragma unroll
@@ -1442,8 +1454,10 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
         tmem_ld_32x32b_x32(trow + sb * kT2NK, v0);
         tmem_ld_32x32b_x32(trow + sb * kT2NK + 32, v1);
         tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&s_free[sb]);
+        if constexpr (!PT) {
+          tc_fence_before();
+          mbar_arrive(&s_free[sb]);
+        }
         float x[64];
         const bool full = a != 0ull && !tree && lim >= kT2NK;
 #pragma unroll
@@ -1492,16 +1506,21 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
         }
         l += s0 + s1;
         const uint32_t pbuf = pvc % PB;
-        if (pvc >= PB) mbar_wait(&p_free[pbuf], ((pvc / PB) & 1) ^ 1);  // the P V that last read this buffer
-        const uint32_t prow = aProw + pbuf * (128 * kT2NK * 2);
+        if constexpr (PT) {
+          tmem_st_32x32b_x32(trow + sb * kT2NK, w32);  // over this tile's own S columns
+          tmem_st_wait();
+        } else {
+          if (pvc >= PB) mbar_wait(&p_free[pbuf], ((pvc / PB) & 1) ^ 1);  // the P V that last read this buffer
+          const uint32_t prow = aProw + pbuf * (128 * kT2NK * 2);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t ch = static_cast<uint32_t>(c ^ (i & 7));
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(w32[4 * c]),
-                       "r"(w32[4 * c + 1]), "r"(w32[4 * c + 2]), "r"(w32[4 * c + 3])
-                       : "memory");
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t ch = static_cast<uint32_t>(c ^ (i & 7));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(w32[4 * c]),
+                         "r"(w32[4 * c + 1]), "r"(w32[4 * c + 2]), "r"(w32[4 * c + 3])
+                         : "memory");
+          }
+          fence_proxy_async_smem();
         }
-        fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[pbuf]);
         ++pvc;
@@ -2033,6 +2052,10 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
                            (int)TcPlan<2, 2, 2, 1>::kSmem);
       cudaFuncSetAttribute(k_ta_fwd_tc2<1, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TcPlan<1, 4, 4, 2>::kSmem);
+      cudaFuncSetAttribute(k_ta_fwd_tc2<2, 3, 2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcPlan<2, 3, 2, 1, true>::kSmem);
+      cudaFuncSetAttribute(k_ta_fwd_tc2<2, 2, 2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcPlan<2, 2, 2, 1, true>::kSmem);
       tattr = true;
     }
     const int work = p.R * p.Hkv;
@@ -2042,9 +2065,15 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
     else if (tcmode == 2)
       k_ta_fwd_tc2<2, 2, 2, 1><<<std::min((work + 1) / 2, kNumSMs), TcPlan<2, 2, 2, 1>::kThreads,
                                   TcPlan<2, 2, 2, 1>::kSmem, s>>>(maps, p);
-    else
+    else if (tcmode == 3)
       k_ta_fwd_tc2<1, 4, 4, 2><<<std::min(work, kNumSMs), TcPlan<1, 4, 4, 2>::kThreads,
                                   TcPlan<1, 4, 4, 2>::kSmem, s>>>(maps, p);
+    else if (tcmode == 4)
+      k_ta_fwd_tc2<2, 3, 2, 1, true><<<std::min((work + 1) / 2, kNumSMs), TcPlan<2, 3, 2, 1, true>::kThreads,
+                                        TcPlan<2, 3, 2, 1, true>::kSmem, s>>>(maps, p);
+    else
+      k_ta_fwd_tc2<2, 2, 2, 1, true><<<std::min((work + 1) / 2, kNumSMs), TcPlan<2, 2, 2, 1, true>::kThreads,
+                                        TcPlan<2, 2, 2, 1, true>::kSmem, s>>>(maps, p);
     count_launch();
     prof_end(PH_TREE_FWD_TC, s);
     return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;

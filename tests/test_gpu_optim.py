@@ -89,11 +89,23 @@ def _prepare(tr):
     return c, H, W, st
 
 
+@pytest.mark.parametrize("qe", [0, 1, 2])
 @pytest.mark.parametrize("name", ["small", "small_tree", "mid"])
-def test_fused_bwd_adamw_matches_unfused(name):
+def test_fused_bwd_adamw_matches_unfused(name, qe):
     """F3 fused into the dW epilogue (dW never stored) vs bwd + aurora_adamw_step: same dH
     bits, the same update up to the norm's summation order; and the oracle's AdamW applied
-    to the unfused dW pins the arithmetic."""
+    to the unfused dW pins the arithmetic.  Both state-entry shapes of the fused kernel
+    (128 x 32 entries shared by all epilogue warps; qe 1 / 2: 32 x 128 / 32 x 64 entries per lane
+    quadrant)."""
+    saved = A.aurora_get_option("dw_adamw_qe")
+    A.aurora_set_option("dw_adamw_qe", qe)
+    try:
+        _fused_vs_unfused(name)
+    finally:
+        A.aurora_set_option("dw_adamw_qe", saved)
+
+
+def _fused_vs_unfused(name):
     tr = tracegen.gen_trace(name)
     c, H, W1, st1 = _prepare(tr)
     st1.forward(H, W1)

@@ -81,13 +81,14 @@ def _compare(got, ref, reqs_got, off_got, reqs_ref_off=None):
             assert _rel(a, ref[name]) <= 2e-2, (name, _rel(a, ref[name]))
 
 
-@pytest.mark.parametrize("tc,split", [(3, 0), (2, 0), (1, 0), (0, 1), (0, 0)],
-                         ids=["tc3_fwd+fused_bwd", "tc2_fwd+fused_bwd", "tc_fwd+fused_bwd", "sync_fwd+split_bwd",
-                              "sync_fwd+fused_bwd"])
+@pytest.mark.parametrize("tc,split", [(5, 0), (4, 0), (3, 0), (2, 0), (1, 0), (0, 1), (0, 0)],
+                         ids=["tc5_fwd+fused_bwd", "tc4_fwd+fused_bwd", "tc3_fwd+fused_bwd", "tc2_fwd+fused_bwd",
+                              "tc_fwd+fused_bwd", "sync_fwd+split_bwd", "sync_fwd+fused_bwd"])
 @pytest.mark.parametrize("name", ["ta_small", "ta_chain", "ta_gqa8"])
 def test_tree_attention_parity(name, tc, split):
     """tc=3 / tc=2: the one-pass tcgen05 forward (online softmax, lazy O rescale in TMEM) with
-    deep K/V rings (one item per SM) / two items per SM, tc=1: the two-pass tcgen05 forward, tc=0: the mma.sync forward; split=0: the one-kernel backward (all rows of
+    deep K/V rings (one item per SM) / two items per SM; tc=4 / 5: two items per SM with P kept
+    in TMEM (the P V MMA reads A from TMEM; K ring 3 / 2 deep), tc=1: the two-pass tcgen05 forward, tc=0: the mma.sync forward; split=0: the one-kernel backward (all rows of
     a kv head in one CTA); split=1: the general dQ + dK/dV kernels (used when G*(N+1) > 128)."""
     from paper_2602_06932_b200 import aurora as A
     inp = tracegen.gen_tree_attn(name)
@@ -119,7 +120,7 @@ def test_tree_attention_deterministic():
         assert torch.equal(a[k], b[k]), k
 
 
-@pytest.mark.parametrize("tc", [0, 3])
+@pytest.mark.parametrize("tc", [0, 3, 4])
 @pytest.mark.parametrize("name,sample", [("ta_llama", [0, 37, 63]), ("ta_tree", [0, 511, 1023])])
 def test_tree_attention_full_size_sampled(name, sample, tc):
     """Full BASELINE sizes in the bench's launch configuration (both forwards); the oracle
