@@ -9,7 +9,7 @@
  *   aurora_spec_loss_fwd  lm_head GEMM + vocab-wide log-softmax + Eq. 3 loss
  *   aurora_spec_loss_bwd  dLogits (tiles only) -> dW_lmhead, dHidden
  * The [M x V] logits are never stored; dLogits exist only as a bf16 per-vocab-chunk
- * workspace bounded by the "dz_chunk_bytes" option (default 2 GiB; see aurora_set_option).
+ * workspace bounded by the "dz_chunk_bytes" option (default 16 GiB; see aurora_set_option).
  *
  * Conventions (all entry points):
  *  - Pointers marked (dev) are CUDA device pointers, (host) are host pointers.  The
@@ -260,8 +260,11 @@ uint64_t aurora_launch_count(void);
  *   "bwd_concurrent" 0 (default): serial; 1: dW || dH of a chunk on library side streams
  *   "dw_resident"    0 (default): streamed pair tiles for dW; 1: with K = M <= 512 each CTA
  *                    pair keeps its dZ^T rows in shared memory across all column tiles
- *   "scan_ctas"      target-scan CTAs per SM (row segments), default 2
- *   "dz_chunk_bytes" budget of the bwd's bf16 dZ^T chunk (default 2 GiB: the whole local
+ *   "scan_ctas"      target-scan CTAs per SM (row segments) of the (row, segment) scan, default 2
+ *   "scan_flat"      1 (default): load-balanced scan, the batch's 16 B vectors cut into equal
+ *                    contiguous ranges per warp (rows 16 B aligned, V_local % 8 == 0; else
+ *                    the (row, segment) scan); 0: the (row, segment) scan
+ *   "dz_chunk_bytes" budget of the bwd's bf16 dZ^T chunk (default 16 GiB: the whole local
  *                    vocabulary at the bench shapes; smaller -> more chunks).  Options that
  *                    change workspace sizes must be set before aurora_workspace_size.
  *   "tile_n"         fwd / dz vocab tile width with single-CTA tiles: 0 auto (default:

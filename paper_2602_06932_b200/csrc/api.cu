@@ -99,8 +99,9 @@ struct Options {
   int64_t dz_chunk_bytes = int64_t(16) << 30;  // classic bwd: dZ^T chunk budget (bytes; 16 GiB of the
                                                 // 180 GB HBM: the tree config's 7.8 GB in one chunk)
   int scan_ctas = 2;                           // target-scan CTAs per SM (segments per row)
-  int tree_fwd_tc = 0;                         // F4 fwd: 1 = tcgen05 kernel when G*(N+1) <= 128 (opt-in:
-                                               // measured slower than the mma.sync kernel)
+  int tree_fwd_tc = 2;                         // F4 fwd when G*(N+1) <= 128: 2 (default) = one-pass tcgen05
+                                               // kernel, two work items per SM; 3 = one item, deep rings;
+                                               // 1 = two-pass tcgen05; 0 = mma.sync
   int tree_bwd_tc = 0;                         // F4 bwd: 1 = tcgen05 kernel when G*(N+1) <= 128
   int tree_bwd_split = 0;                      // F4 bwd: 1 = separate dQ / dK-dV kernels even when the
                                                // fused one applies (A/B and coverage of the general path)
@@ -109,12 +110,14 @@ struct Options {
   int gram_norm = 1;                           // F3 fused: Gram-form global norm when M is small
   int dw_adamw_qe = 1;                         // F3 fused state entries: 0 = 128 x 32, 1 = 32 x 128, 2 = 32 x 64
   int debug_gemm_group = 0;                    // aurora_debug_gemm only: grouped raster (< 0: groups of n-tiles)
+  int scan_flat = 1;                           // A2: 1 = load-balanced flat scan (equal vector ranges per warp)
   int scan_ring = 0;                           // A2: 1 = persistent TMA-ring scan (measured slower: opt-in)
   int fwd_stage = 1;                           // Eq. 3: the fwd stages exp(z - m_half) in dZ^T so the
                                                // bwd needs no recompute GEMM (0: recompute, round-1 path)
   Options() {
     if (const char* e = getenv("AURORA_FWD_STAGE")) fwd_stage = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_RING")) scan_ring = atoi(e) ? 1 : 0;
+    if (const char* e = getenv("AURORA_SCAN_FLAT")) scan_flat = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_DW_ADAMW_QE")) dw_adamw_qe = std::min(2, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_DW_RESIDENT")) dw_resident = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_CTAS")) scan_ctas = std::max(1, atoi(e));
@@ -123,7 +126,7 @@ struct Options {
     if (const char* e = getenv("AURORA_PAIR")) gemm_pair = atoi(e);
     if (const char* e = getenv("AURORA_BWD")) bwd_mode = std::strcmp(e, "fused") == 0 ? 1 : 0;
     if (const char* e = getenv("AURORA_SERIAL_BWD")) bwd_concurrent = (e[0] == '0') ? 1 : 0;
-    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = std::min(5, std::max(0, atoi(e)));
+    if (const char* e = getenv("AURORA_TREE_FWD_TC")) tree_fwd_tc = std::min(3, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_TREE_BWD_SPLIT")) tree_bwd_split = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_TREE_BWD_TC")) tree_bwd_tc = atoi(e) ? 1 : 0;
   }
@@ -205,7 +208,8 @@ int ring_nseg(int64_t M, int64_t V_local) {
   return static_cast<int>(std::min<int64_t>(std::max<int64_t>(nseg, 1), 32));
 }
 VerifyWs carve_verify(Carver& c, int64_t M, int64_t V_local, int k_max) {
-  const int nseg = std::max(scan_nseg(M, V_local), ring_nseg(M, V_local) * scan_ring_lists());
+  const int nseg = std::max({scan_nseg(M, V_local), ring_nseg(M, V_local) * scan_ring_lists(),
+                             scan_flat_slots(M, V_local)});
   VerifyWs w;
   w.ept = c.take<float>(M);
   w.lse_part = c.take<float>(M * 3);
@@ -563,7 +567,7 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   Options& o = opts();
   if (std::strcmp(name, "gemm_pair") == 0 && value >= 0 && value <= 2) { o.gemm_pair = static_cast<int>(value); return AURORA_OK; }
   if (std::strcmp(name, "bwd_mode") == 0 && value >= 0 && value <= 1) { o.bwd_mode = static_cast<int>(value); return AURORA_OK; }
-  if (std::strcmp(name, "tree_fwd_tc") == 0 && value >= 0 && value <= 5) {
+  if (std::strcmp(name, "tree_fwd_tc") == 0 && value >= 0 && value <= 3) {
     o.tree_fwd_tc = static_cast<int>(value);
     return AURORA_OK;
   }
@@ -589,6 +593,10 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
   }
   if (std::strcmp(name, "debug_gemm_group") == 0 && value >= -64 && value <= 64) {
     o.debug_gemm_group = static_cast<int>(value);
+    return AURORA_OK;
+  }
+  if (std::strcmp(name, "scan_flat") == 0 && (value == 0 || value == 1)) {
+    o.scan_flat = static_cast<int>(value);
     return AURORA_OK;
   }
   if (std::strcmp(name, "scan_ring") == 0 && (value == 0 || value == 1)) {
@@ -633,6 +641,7 @@ int64_t aurora_get_option(const char* name) {
   if (std::strcmp(name, "dw_resident") == 0) return o.dw_resident;
   if (std::strcmp(name, "fwd_stage") == 0) return o.fwd_stage;
   if (std::strcmp(name, "scan_ring") == 0) return o.scan_ring;
+  if (std::strcmp(name, "scan_flat") == 0) return o.scan_flat;
   if (std::strcmp(name, "dw_adamw_qe") == 0) return o.dw_adamw_qe;
   if (std::strcmp(name, "debug_gemm_group") == 0) return o.debug_gemm_group;
   if (std::strcmp(name, "gram_norm") == 0) return o.gram_norm;
@@ -752,7 +761,8 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
     p.nseg = scan_nseg(M, t->V_local);
     p.seg_len = rup(cdiv(t->V_local, p.nseg), 8);
   }
-  const int nlists = ring ? p.nseg * scan_ring_lists() : p.nseg;
+  const bool flat = !ring && opts().scan_flat && scan_flat_ok(p);
+  int nlists = ring ? p.nseg * scan_ring_lists() : p.nseg;
   p.draft = t->draft_tokens;
   p.parents = t->parents;
   p.num_nodes = t->num_nodes;
@@ -768,7 +778,10 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
   if ((e = cudaMemsetAsync(out->counts, 0, 2 * sizeof(int32_t), s)) != cudaSuccess) return AURORA_ERR_CUDA;
   if ((e = cudaMemsetAsync(out->status, 0, sizeof(uint32_t), s)) != cudaSuccess) return AURORA_ERR_CUDA;
   prof_begin(PH_SCAN, s);
-  if ((e = (ring ? launch_target_scan_ring(p, s) : launch_target_scan(p, s))) != cudaSuccess) return AURORA_ERR_CUDA;
+  if ((e = (ring   ? launch_target_scan_ring(p, s)
+             : flat ? launch_target_scan_flat(p, &nlists, s)
+                    : launch_target_scan(p, s))) != cudaSuccess)
+    return AURORA_ERR_CUDA;
   if ((e = launch_topk_merge(p, w.cand_val, w.cand_idx, nlists, static_cast<int64_t>(nlists) * k_max, k_max, s)) !=
       cudaSuccess)
     return AURORA_ERR_CUDA;

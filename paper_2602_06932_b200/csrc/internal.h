@@ -182,6 +182,12 @@ cudaError_t launch_target_scan(const VerifyLaunch& p, cudaStream_t s);
 bool scan_ring_ok(const VerifyLaunch& p);
 int scan_ring_lists();
 cudaError_t launch_target_scan_ring(const VerifyLaunch& p, cudaStream_t s);
+// load-balanced flat scan (scan_flat_ok): equal contiguous vector ranges per warp, `*nlists`
+// (= scan_flat_slots) lists per row in cand_val / cand_idx
+constexpr int kScanFlatCtas = 3;
+bool scan_flat_ok(const VerifyLaunch& p);
+int scan_flat_slots(int64_t M, int64_t V_local);
+cudaError_t launch_target_scan_flat(const VerifyLaunch& p, int* nlists, cudaStream_t s);
 cudaError_t launch_topk_merge(const VerifyLaunch& p, const float* in_val, const int32_t* in_idx, int nlists,
                               int64_t row_stride, int64_t list_stride, cudaStream_t s);
 cudaError_t launch_target_scan_topk(const VerifyLaunch& p, const int32_t* tk_idx, const uint16_t* tk_val, int32_t K_t,

@@ -1233,24 +1233,22 @@ constexpr int kT2Slot = kT2NK * 128 * 2;            // 16 KB: K tile (2 K-major 
 // GRP work items per CTA (independent groups of 6 warps), KST / VST K / V ring stages, PB P
 // buffers per group.  <2, 2, 2, 1>: two items in flight, 112 KB each; <1, 4, 4, 2>: one item
 // with deep rings (192 KB: ~4 tiles of K and V in flight per SM)
-// PT: P stays in TMEM (bf16 pairs written over its own S buffer, the P V MMA reads A from TMEM):
-// no shared-memory P buffer, no proxy fence, no wait for the previous P V before writing P.
-template <int GRP, int KST, int VST, int PB, bool PT = false>
+template <int GRP, int KST, int VST, int PB>
 struct TcPlan {
   static constexpr int kThreads = GRP * 192;
   static constexpr int kOffK = 32768;               // after Q (2 atoms of 128 rows x 128 B)
   static constexpr int kOffV = kOffK + KST * kT2Slot;
   static constexpr int kOffP = kOffV + VST * kT2Slot;
-  static constexpr int kGrp = kOffP + (PT ? 0 : PB * 128 * kT2NK * 2);
+  static constexpr int kGrp = kOffP + PB * 128 * kT2NK * 2;
   static constexpr int kOffBar = GRP * kGrp;
-  static constexpr size_t kSmem = kOffBar + 1536 + 1024;  // barriers + anc + TMEM holder, alignment
+  static constexpr size_t kSmem = kOffBar + 2048 + 1024;  // barriers + anc + TMEM holder + parents, alignment
   static_assert(kSmem <= 232448, "smem");
   static_assert(2 + 2 * KST + 2 * VST + 4 + 2 * PB + 3 <= 32, "barriers per group");
 };
 
-template <int GRP, int KST, int VST, int PB, bool PT = false>
+template <int GRP, int KST, int VST, int PB>
 __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_constant__ TaTcMaps maps, TaParams p) {
-  using Plan = TcPlan<GRP, KST, VST, PB, PT>;
+  using Plan = TcPlan<GRP, KST, VST, PB>;
   constexpr int kT2OffK = Plan::kOffK, kT2OffV = Plan::kOffV, kT2OffP = Plan::kOffP, kT2Grp = Plan::kGrp;
   constexpr int kT2OffBar = Plan::kOffBar;
   extern __shared__ uint8_t smem_raw[];
@@ -1275,8 +1273,18 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
   uint64_t* o_free = o_done + 1;
   uint64_t* anc = bars + 64 + grp * 40;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 160);
+  int32_t* par_s = reinterpret_cast<int32_t*>(bars + 168 + grp * 16);  // the request's parents (N <= 32)
   const int G = p.G, N1 = p.N1;
   const int nwork = p.R * p.Hkv;
+  {  // Q rows >= G (N+1) are never loaded: zero them once so their scores are 0 (unmasked, finite)
+    const int rows = G * N1;
+    for (int idx = threadIdx.x; idx < GRP * 2 * (128 - rows) * 8; idx += blockDim.x) {
+      const int c = idx & 7, row = rows + (idx >> 3) % (128 - rows), part = (idx >> 3) / (128 - rows);
+      *reinterpret_cast<uint4*>(smem + (part >> 1) * kT2Grp + (part & 1) * 16384 + row * 128 + c * 16) =
+          make_uint4(0u, 0u, 0u, 0u);
+    }
+    fence_proxy_async_smem();
+  }
 
   if (threadIdx.x == 0) {
     for (int g2 = 0; g2 < GRP; ++g2) {
@@ -1355,19 +1363,11 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
         if (jj == 0 && wi > 0) mbar_wait(o_free, (wi - 1) & 1);  // the epilogue read the previous O
         tc_fence_after();
         const uint32_t vb = smem_u32(gs + kT2OffV + vs * kT2Slot);
-        if constexpr (PT) {
-          // P of tile jj sits in S buffer jj & 1 (pc counts tiles like sc): 8 columns per K = 16
-          const uint32_t aT = tmem + (pc & 1) * kT2NK;
 #pragma unroll
-          for (int kk = 0; kk < kT2NK / 16; ++kk)
-            umma_bf16_ts(tmem + 128, aT + kk * 8, mnmaj_desc(vb, kk, kT2NK), idPV, (jj > 0 || kk > 0) ? 1u : 0u);
-        } else {
-#pragma unroll
-          for (int kk = 0; kk < kT2NK / 16; ++kk)
-            umma_bf16(tmem + 128, kmaj_desc(aP + pbuf * (128 * kT2NK * 2), kk, 128), mnmaj_desc(vb, kk, kT2NK), idPV,
-                      (jj > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&p_free[pbuf]);
-        }
+        for (int kk = 0; kk < kT2NK / 16; ++kk)
+          umma_bf16(tmem + 128, kmaj_desc(aP + pbuf * (128 * kT2NK * 2), kk, 128), mnmaj_desc(vb, kk, kT2NK), idPV,
+                    (jj > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&p_free[pbuf]);
         umma_commit(&v_empty[vs]);
         umma_commit(o_ready);
         ++vc;
@@ -1382,9 +1382,7 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
         for (int j = 0; j < nt; ++j) {
           const uint32_t ks = kc % KST, sb = sc & 1;
           mbar_wait(&k_full[ks], (kc / KST) & 1);
-          // PT: the buffer's previous P was read by the P V issued before this S (the tensor pipe
-          // runs one thread's MMAs in order), and that P V waited for the softmax's P
-          if (!PT && sc >= 2) mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
+          if (sc >= 2) mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t kb = smem_u32(gs + kT2OffK + ks * kT2Slot);
 #pragma unroll
@@ -1417,60 +1415,75 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
       int p0, Pr;
       prefix_of(p, r, p0, Pr, false);
       const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
-      if (st_id < N1) {  // ancestor masks of this request (bit t = tree key t visible)
-        const int s = st_id;
+      {  // ancestor masks of this request (bit t = tree key t visible): the parents are loaded in
+         // parallel into shared memory, then each row walks its ancestor chain there
         const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
-        bool bad = nn < 0 || nn > p.N;
-        uint64_t m = 0;
-        if (!bad) {
-          if (s == 0) {
-            m = 1ull;
-          } else if (s - 1 < nn) {
-            int cur = s - 1;
-            m = 1ull | (1ull << s);
-            for (int k = 0; k <= p.N; ++k) {
-              const int par = p.parents ? p.parents[(size_t)r * p.N + cur] : cur - 1;
-              if (par < -1 || par >= cur) { bad = true; break; }
-              if (par < 0) break;
-              m |= 1ull << (par + 1);
-              cur = par;
+        if (st_id < p.N) par_s[st_id] = p.parents ? p.parents[(size_t)r * p.N + st_id] : st_id - 1;
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+        if (st_id < N1) {
+          const int s = st_id;
+          bool bad = nn < 0 || nn > p.N;
+          uint64_t m = 0;
+          if (!bad) {
+            if (s == 0) {
+              m = 1ull;
+            } else if (s - 1 < nn) {
+              int cur = s - 1;
+              m = 1ull | (1ull << s);
+              for (int k = 0; k <= p.N; ++k) {
+                const int par = par_s[cur];
+                if (par < -1 || par >= cur) { bad = true; break; }
+                if (par < 0) break;
+                m |= 1ull << (par + 1);
+                cur = par;
+              }
             }
           }
+          if (bad && p.status && hk == 0) atomicOr(p.status, (uint32_t)AURORA_STATUS_STRUCTURE);
+          anc[s] = bad ? 0ull : m;
         }
-        if (bad && p.status && hk == 0) atomicOr(p.status, (uint32_t)AURORA_STATUS_STRUCTURE);
-        anc[s] = bad ? 0ull : m;
       }
       asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
       const int s_row = i / G, g = i - s_row * G;
       const uint64_t a = i < rows ? anc[s_row] : 0ull;
+      // Rows that are not output (a = 0: padding rows, whose Q rows are zero in shared memory, and
+      // invalid tree rows, written as O = 0, lse = -inf) need no mask: their scores are finite.
+      // So a prefix tile with every key inside the prefix is unmasked for the whole warp (the
+      // common case); the request's last prefix tile and its tree tile take the masked path.
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nt; ++j, ++sc) {
         const uint32_t sb = sc & 1;
         const bool tree = j == npt;
         const int lim = tree ? 0 : Pr - j * kT2NK;
+        uint64_t vis = tree ? a : (lim >= kT2NK ? ~0ull : ((1ull << max(lim, 0)) - 1ull));
+        if (a == 0ull) vis = ~0ull;
+        const bool wfull = __all_sync(0xffffffffu, vis == ~0ull);
         mbar_wait(&s_full[sb], (sc >> 1) & 1);
         tc_fence_after();
-        uint32_t v0[32], v1[32];
-        tmem_ld_32x32b_x32(trow + sb * kT2NK, v0);
-        tmem_ld_32x32b_x32(trow + sb * kT2NK + 32, v1);
-        tmem_ld_wait();
-        if constexpr (!PT) {
-          tc_fence_before();
-          mbar_arrive(&s_free[sb]);
-        }
         float x[64];
-        const bool full = a != 0ull && !tree && lim >= kT2NK;
+        tmem_ld_32x32b_x32(trow + sb * kT2NK, reinterpret_cast<uint32_t(&)[32]>(x[0]));
+        tmem_ld_32x32b_x32(trow + sb * kT2NK + 32, reinterpret_cast<uint32_t(&)[32]>(x[32]));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&s_free[sb]);
+        if (!wfull) {
+          const uint32_t vlo = static_cast<uint32_t>(vis), vhi = static_cast<uint32_t>(vis >> 32);
 #pragma unroll
-        for (int e = 0; e < 64; ++e) {
-          bool ok;
-          if (full) ok = true;
-          else if (tree) ok = (a >> e) & 1ull;
-          else ok = a != 0ull && e < lim;
-          x[e] = ok ? __uint_as_float(e < 32 ? v0[e] : v1[e - 32]) : -INFINITY;
+          for (int e = 0; e < 32; ++e) {
+            x[e] = ((vlo >> e) & 1u) ? x[e] : -INFINITY;
+            x[e + 32] = ((vhi >> e) & 1u) ? x[e + 32] : -INFINITY;
+          }
         }
-        float mt = -INFINITY;
+        // row max: a tree of independent max3 (no 64-long dependency chain)
+        float t21[22];
 #pragma unroll
-        for (int e = 0; e < 64; ++e) mt = fmaxf(mt, x[e]);
+        for (int q = 0; q < 21; ++q) t21[q] = fmaxf(fmaxf(x[3 * q], x[3 * q + 1]), x[3 * q + 2]);
+        t21[21] = x[63];
+        float t7[8];
+#pragma unroll
+        for (int q = 0; q < 7; ++q) t7[q] = fmaxf(fmaxf(t21[3 * q], t21[3 * q + 1]), t21[3 * q + 2]);
+        t7[7] = t21[21];
+        float mt = fmaxf(fmaxf(fmaxf(t7[0], t7[1]), fmaxf(t7[2], t7[3])), fmaxf(fmaxf(t7[4], t7[5]), fmaxf(t7[6], t7[7])));
         mt *= c2;
         // lazy rescale: only when a row's max grew by more than 2^8 (log2 domain); the TMEM
         // load / store are warp-collective, so the warp rescales together (factor 1 on the
@@ -1495,32 +1508,27 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
         }
         if (grow) m = mt;
         uint32_t w32[32];
-        float s0 = 0.f, s1 = 0.f;
-        const float mref = m == -INFINITY ? 0.f : m;  // rows with no visible key yet: e = 0, not NaN
+        float sacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const float nm = m == -INFINITY ? 0.f : -m;  // rows with no visible key yet: e = 0, not NaN
 #pragma unroll
         for (int h = 0; h < 32; ++h) {
-          const float e0 = ex2_approx(fmaf(x[2 * h], c2, -mref)), e1 = ex2_approx(fmaf(x[2 * h + 1], c2, -mref));
-          s0 += e0;
-          s1 += e1;
+          const float e0 = ex2_approx(fmaf(x[2 * h], c2, nm)), e1 = ex2_approx(fmaf(x[2 * h + 1], c2, nm));
+          sacc[(2 * h) & 7] += e0;
+          sacc[(2 * h + 1) & 7] += e1;
           w32[h] = pk_bf16(e0, e1);
         }
-        l += s0 + s1;
+        l += ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3])) + ((sacc[4] + sacc[5]) + (sacc[6] + sacc[7]));
         const uint32_t pbuf = pvc % PB;
-        if constexpr (PT) {
-          tmem_st_32x32b_x32(trow + sb * kT2NK, w32);  // over this tile's own S columns
-          tmem_st_wait();
-        } else {
-          if (pvc >= PB) mbar_wait(&p_free[pbuf], ((pvc / PB) & 1) ^ 1);  // the P V that last read this buffer
-          const uint32_t prow = aProw + pbuf * (128 * kT2NK * 2);
+        if (pvc >= PB) mbar_wait(&p_free[pbuf], ((pvc / PB) & 1) ^ 1);  // the P V that last read this buffer
+        const uint32_t prow = aProw + pbuf * (128 * kT2NK * 2);
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint32_t ch = static_cast<uint32_t>(c ^ (i & 7));
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(w32[4 * c]),
-                         "r"(w32[4 * c + 1]), "r"(w32[4 * c + 2]), "r"(w32[4 * c + 3])
-                         : "memory");
-          }
-          fence_proxy_async_smem();
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t ch = static_cast<uint32_t>(c ^ (i & 7));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(w32[4 * c]),
+                       "r"(w32[4 * c + 1]), "r"(w32[4 * c + 2]), "r"(w32[4 * c + 3])
+                       : "memory");
         }
+        fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[pbuf]);
         ++pvc;
@@ -1606,6 +1614,7 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
   uint64_t* dq_free = bars + 21;
   uint64_t* anc = bars + 32;      // [40]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 80);
+  int32_t* par_s = reinterpret_cast<int32_t*>(bars + 88);  // the request's parents (N <= 32)
   const int G = p.G, N1 = p.N1;
   const int nwork = p.R * p.Hkv;
   if (threadIdx.x == 0) {
@@ -1756,27 +1765,31 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
       int p0, Pr;
       prefix_of(p, r, p0, Pr, false);
       const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
-      if (st_id < N1) {
-        const int s = st_id;
-        const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
-        bool bad = nn < 0 || nn > p.N;
-        uint64_t m = 0;
-        if (!bad) {
-          if (s == 0) {
-            m = 1ull;
-          } else if (s - 1 < nn) {
-            int cur = s - 1;
-            m = 1ull | (1ull << s);
-            for (int k = 0; k <= p.N; ++k) {
-              const int par = p.parents ? p.parents[(size_t)r * p.N + cur] : cur - 1;
-              if (par < -1 || par >= cur) { bad = true; break; }
-              if (par < 0) break;
-              m |= 1ull << (par + 1);
-              cur = par;
+      {  // ancestor masks: parents loaded in parallel into shared memory, walked there
+        if (st_id < p.N) par_s[st_id] = p.parents ? p.parents[(size_t)r * p.N + st_id] : st_id - 1;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (st_id < N1) {
+          const int s = st_id;
+          const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
+          bool bad = nn < 0 || nn > p.N;
+          uint64_t m = 0;
+          if (!bad) {
+            if (s == 0) {
+              m = 1ull;
+            } else if (s - 1 < nn) {
+              int cur = s - 1;
+              m = 1ull | (1ull << s);
+              for (int k = 0; k <= p.N; ++k) {
+                const int par = par_s[cur];
+                if (par < -1 || par >= cur) { bad = true; break; }
+                if (par < 0) break;
+                m |= 1ull << (par + 1);
+                cur = par;
+              }
             }
           }
+          anc[s] = bad ? 0ull : m;
         }
-        anc[s] = bad ? 0ull : m;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const int s_row = i / G, g = i - s_row * G;
@@ -1826,26 +1839,37 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&s_free[sb]);
-        const bool full = a != 0ull && !tree && lim >= kT2NK;
+        // visibility of this tile's keys; rows >= G (N+1) have zero Q / dO rows in shared memory
+        // (P = 1, dP = 0, D = 0: they add nothing), so only real rows are masked, and a prefix tile
+        // wholly inside the prefix needs no mask at all (warp-uniform fast path)
+        uint64_t vis = tree ? a : (a == 0ull ? 0ull : (lim >= kT2NK ? ~0ull : ((1ull << max(lim, 0)) - 1ull)));
+        if (i >= rows) vis = ~0ull;
+        const bool wfull = __all_sync(0xffffffffu, vis == ~0ull);
+        float* x = reinterpret_cast<float*>(sv);
+        float* dpv = reinterpret_cast<float*>(dp);
         uint32_t pw[32], dw[32];
+        const float nl = -lse2;
+        if (wfull) {
 #pragma unroll
-        for (int h = 0; h < 32; ++h) {
-          float pv[2], dv2[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int e = 2 * h + u;
-            bool ok;
-            if (full) ok = true;
-            else if (tree) ok = (a >> e) & 1ull;
-            else ok = a != 0ull && e < lim;
-            const float x = __uint_as_float(e < 32 ? sv[0][e] : sv[1][e - 32]);
-            const float dpe = __uint_as_float(e < 32 ? dp[0][e] : dp[1][e - 32]);
-            const float pe = ok ? ex2_approx(fmaf(x, c2, -lse2)) : 0.f;
-            pv[u] = pe;
-            dv2[u] = ok ? scale * pe * (dpe - Di) : 0.f;  // never 0 * (NaN) from unused rows
+          for (int h = 0; h < 32; ++h) {
+            const float p0 = ex2_approx(fmaf(x[2 * h], c2, nl)), p1 = ex2_approx(fmaf(x[2 * h + 1], c2, nl));
+            pw[h] = pk_bf16(p0, p1);
+            dw[h] = pk_bf16(scale * p0 * (dpv[2 * h] - Di), scale * p1 * (dpv[2 * h + 1] - Di));
           }
-          pw[h] = pk_bf16(pv[0], pv[1]);
-          dw[h] = pk_bf16(dv2[0], dv2[1]);
+        } else {
+          const uint32_t vlo = static_cast<uint32_t>(vis), vhi = static_cast<uint32_t>(vis >> 32);
+#pragma unroll
+          for (int h = 0; h < 32; ++h) {
+            const uint32_t vv = h < 16 ? vlo : vhi;
+            const bool ok0 = (vv >> ((2 * h) & 31)) & 1u, ok1 = (vv >> ((2 * h + 1) & 31)) & 1u;
+            const float p0 = ok0 ? ex2_approx(fmaf(x[2 * h], c2, nl)) : 0.f;
+            const float p1 = ok1 ? ex2_approx(fmaf(x[2 * h + 1], c2, nl)) : 0.f;
+            // never 0 * NaN from masked keys
+            const float d0 = ok0 ? scale * p0 * (dpv[2 * h] - Di) : 0.f;
+            const float d1 = ok1 ? scale * p1 * (dpv[2 * h + 1] - Di) : 0.f;
+            pw[h] = pk_bf16(p0, p1);
+            dw[h] = pk_bf16(d0, d1);
+          }
         }
         const uint32_t pb = (sc) & 1;
         if (sc >= 2) mbar_wait(&pd_free[pb], ((sc >> 1) & 1) ^ 1);
@@ -2052,10 +2076,6 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
                            (int)TcPlan<2, 2, 2, 1>::kSmem);
       cudaFuncSetAttribute(k_ta_fwd_tc2<1, 4, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TcPlan<1, 4, 4, 2>::kSmem);
-      cudaFuncSetAttribute(k_ta_fwd_tc2<2, 3, 2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TcPlan<2, 3, 2, 1, true>::kSmem);
-      cudaFuncSetAttribute(k_ta_fwd_tc2<2, 2, 2, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TcPlan<2, 2, 2, 1, true>::kSmem);
       tattr = true;
     }
     const int work = p.R * p.Hkv;
@@ -2065,15 +2085,9 @@ extern "C" aurora_status_t aurora_tree_attn_fwd(const aurora_tree_attn_t* ta, co
     else if (tcmode == 2)
       k_ta_fwd_tc2<2, 2, 2, 1><<<std::min((work + 1) / 2, kNumSMs), TcPlan<2, 2, 2, 1>::kThreads,
                                   TcPlan<2, 2, 2, 1>::kSmem, s>>>(maps, p);
-    else if (tcmode == 3)
+    else
       k_ta_fwd_tc2<1, 4, 4, 2><<<std::min(work, kNumSMs), TcPlan<1, 4, 4, 2>::kThreads,
                                   TcPlan<1, 4, 4, 2>::kSmem, s>>>(maps, p);
-    else if (tcmode == 4)
-      k_ta_fwd_tc2<2, 3, 2, 1, true><<<std::min((work + 1) / 2, kNumSMs), TcPlan<2, 3, 2, 1, true>::kThreads,
-                                        TcPlan<2, 3, 2, 1, true>::kSmem, s>>>(maps, p);
-    else
-      k_ta_fwd_tc2<2, 2, 2, 1, true><<<std::min((work + 1) / 2, kNumSMs), TcPlan<2, 2, 2, 1, true>::kThreads,
-                                        TcPlan<2, 2, 2, 1, true>::kSmem, s>>>(maps, p);
     count_launch();
     prof_end(PH_TREE_FWD_TC, s);
     return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;

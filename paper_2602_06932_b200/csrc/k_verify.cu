@@ -278,6 +278,148 @@ __global__ void __launch_bounds__(256) k_target_scan(VerifyLaunch p) {
   }
 }
 
+// --------------------------------------------------------------------------- A2 scan (flat split)
+// Persistent, load-balanced variant (rows 16 B aligned, V_local % 8 == 0): the M x V_local/8
+// 16-byte vectors of the batch, flattened row-major, are cut into W equal contiguous ranges, one
+// per warp of a grid of `ctas_per_sm` x 148 CTAs, so every warp streams the same number of bytes
+// and no wave tail is left (the (row, segment) grid leaves one: M = 1792 rows over 444 resident
+// CTAs is 4.04 waves).  A range covers pieces of one or more rows; each piece gets its own list
+// (warm start: the k-th largest lane maximum of its first batch) written to slot
+// (warp - first warp of the row) of the row's S list slots; the warp that ends a row fills the
+// row's remaining slots with empty lists, so the merge reads exactly S lists per row.
+struct FlatSplit {
+  int64_t V8, NV;  // vectors per row, vectors in the batch
+  int32_t W, S;    // warps with a range (each >= 64 vectors), list slots per row
+  __device__ __host__ __forceinline__ int64_t start(int64_t g) const { return g * NV / W; }
+  // the warp whose range contains vector v: largest g with start(g) <= v
+  __device__ __forceinline__ int64_t warp_of(int64_t v) const {
+    int64_t g = ((v + 1) * W + NV - 1) / NV - 1;
+    while (g + 1 < W && start(g + 1) <= v) ++g;
+    while (g > 0 && start(g) > v) --g;
+    return g;
+  }
+};
+
+// Scan vectors [v0, v1) of one row (rowv: the row's first vector) into the warp list L.
+// `slot` (shared memory, may be null) is the row's CTA-wide admission floor: every warp of the CTA
+// scanning a piece of the same row publishes its k-th value there and admits only elements >= the
+// maximum published (a lower bound for the row's k-th best), so the warps' lists stay short.
+// Returns this lane's running maximum of |bits| (non-finite test at the end).
+__device__ __forceinline__ uint32_t scan_piece(WarpList& L, const uint4* __restrict__ rowv, int64_t v0, int64_t v1,
+                                               int* slot, uint4* stash) {
+  constexpr int U = 8;  // 16 B loads in flight per lane
+  const int lane = threadIdx.x & 31;
+  uint32_t amax = 0;
+  auto absmax = [&](const uint4& w) {
+    amax = __vmaxu2(amax, __vmaxu2(__vmaxu2(w.x & 0x7FFF7FFFu, w.y & 0x7FFF7FFFu),
+                                   __vmaxu2(w.z & 0x7FFF7FFFu, w.w & 0x7FFF7FFFu)));
+  };
+  float floor;
+  {
+    // warm start without offers: the k-th largest of the 32 lane maxima of the first batch
+    // (distinct elements) bounds the piece's k-th best element from below; the batch itself is
+    // scanned again (from L2) by the main loop
+    float lm = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t vi = v0 + u * 32 + lane;
+      if (vi < v1) lm = fmaxf(lm, max8(ld_nc_v4(rowv + vi)));
+    }
+    floor = warp_kth_largest(lm, L.k);
+    if (slot) {
+      if (lane == 0) atomicMax(slot, f2ord(floor));
+      floor = fmaxf(floor, ord2f(*reinterpret_cast<volatile int*>(slot)));
+    }
+  }
+  int64_t base = v0;
+  for (; base + U * 32 <= v1; base += U * 32) {
+    uint4 w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = ld_nc_v4(rowv + base + u * 32 + lane);
+    bool any = false;
+    const float f = fmaxf(floor, L.thr_v);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      absmax(w[u]);
+      any |= max8(w[u]) >= f;
+    }
+    if (__any_sync(0xffffffffu, any)) {
+      // rare path, kept rolled (one copy of the offer code): the batch goes through this warp's
+      // shared-memory stash so the vectors can be indexed at run time
+#pragma unroll
+      for (int u = 0; u < U; ++u) stash[u * 32 + lane] = w[u];
+      __syncwarp();
+#pragma unroll 1
+      for (int u = 0; u < U; ++u) {
+        const uint4 wu = stash[u * 32 + lane];
+        const bool h = max8(wu) >= fmaxf(floor, L.thr_v);
+        if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, wu, (base + u * 32 + lane) * 8, floor);
+      }
+      __syncwarp();
+      if (slot) {
+        if (lane == 0 && L.thr_v > floor) atomicMax(slot, f2ord(L.thr_v));
+        floor = fmaxf(floor, ord2f(*reinterpret_cast<volatile int*>(slot)));
+      }
+    } else if (slot) {
+      floor = fmaxf(floor, ord2f(*reinterpret_cast<volatile int*>(slot)));
+    }
+  }
+  for (; base < v1; base += 32) {
+    const int64_t vi = base + lane;
+    uint4 w = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+    if (vi < v1) {
+      w = ld_nc_v4(rowv + vi);
+      absmax(w);
+    }
+    const bool h = vi < v1 && max8(w) >= fmaxf(floor, L.thr_v);
+    if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, w, vi * 8, floor);
+  }
+  return amax;
+}
+
+template <int kCtas>
+__global__ void __launch_bounds__(256, kCtas) k_target_scan_flat(VerifyLaunch p, FlatSplit fs) {
+  constexpr int kSlots = 16;  // rows of the CTA's vector span with a shared admission floor
+  __shared__ int s_floor[kSlots];
+  __shared__ uint4 s_stash[8][8 * 32];  // per warp: one batch (8 vectors per lane)
+  const int lane = threadIdx.x & 31;
+  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * 8;
+  const int64_t row0 = fs.start(g0 < fs.W ? g0 : fs.W - 1) / fs.V8;
+  if (threadIdx.x < kSlots) s_floor[threadIdx.x] = f2ord(-INFINITY);
+  __syncthreads();
+  const int64_t g = g0 + (threadIdx.x >> 5);
+  if (g >= fs.W) return;
+  const int k = p.k_max;
+  int64_t a = fs.start(g);
+  const int64_t b = fs.start(g + 1);
+  uint32_t amax = 0;
+  while (a < b) {
+    const int64_t row = a / fs.V8;
+    const int64_t rs = row * fs.V8;
+    const int64_t re = min(b, rs + fs.V8);
+    WarpList L;
+    L.init(k);
+    const uint4* rowv = reinterpret_cast<const uint4*>(p.T + row * p.ldT);
+    int* slot = row - row0 < kSlots ? &s_floor[row - row0] : nullptr;
+    amax = __vmaxu2(amax, scan_piece(L, rowv, a - rs, re - rs, slot, s_stash[threadIdx.x >> 5]));
+    const int64_t sl0 = g - fs.warp_of(rs);
+    float* cv = p.cand_val + row * fs.S * k;
+    int32_t* ci = p.cand_idx + row * fs.S * k;
+    if (lane < k) {
+      cv[sl0 * k + lane] = L.v;
+      ci[sl0 * k + lane] = (L.i == INT32_MAX) ? INT32_MAX : static_cast<int32_t>(L.i + p.vocab_offset);
+    }
+    if (re == rs + fs.V8) {  // this warp ends the row: empty lists in the row's unused slots
+      for (int64_t sl = sl0 + 1; sl < fs.S; ++sl)
+        if (lane < k) { cv[sl * k + lane] = -INFINITY; ci[sl * k + lane] = INT32_MAX; }
+    }
+    a = re;
+  }
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  if (lane == 0 && ((amax & 0xFFFFu) >= 0x7F80u || (amax >> 16) >= 0x7F80u))
+    atomicOr(p.lab.status, AURORA_STATUS_NONFINITE);
+}
+
 // --------------------------------------------------------------------------- A2 scan (TMA rings)
 // Persistent variant for 16 B-aligned rows.  Every warp owns a private 3-slot ring of 8 KB in
 // shared memory and streams its own (row, segment) work items through it: lane 0 issues the 1-D
@@ -837,6 +979,37 @@ cudaError_t launch_target_scan_ring(const VerifyLaunch& p, cudaStream_t s) {
   const int64_t ctas = (items + kRingWarps - 1) / kRingWarps;
   const int grid = static_cast<int>(ctas < kNumSMs ? ctas : kNumSMs);
   k_target_scan_ring<<<grid, 32 * kRingWarps, kSmem, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+bool scan_flat_ok(const VerifyLaunch& p) {
+  return (p.V_local % 8) == 0 && (p.ldT % 8) == 0 && (reinterpret_cast<uintptr_t>(p.T) & 15) == 0;
+}
+int scan_flat_ctas() {
+  static int c = [] {
+    const char* e = getenv("AURORA_SCAN_FLAT_CTAS");
+    return (e && atoi(e) == 2) ? 2 : kScanFlatCtas;
+  }();
+  return c;
+}
+FlatSplit flat_split(int64_t M, int64_t V_local) {
+  FlatSplit f;
+  f.V8 = V_local / 8;
+  f.NV = M * f.V8;
+  const int64_t warps = static_cast<int64_t>(scan_flat_ctas()) * kNumSMs * 8;
+  f.W = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(warps, f.NV / 64)));
+  const int64_t minlen = std::max<int64_t>(1, f.NV / f.W);
+  f.S = static_cast<int32_t>(std::min<int64_t>(f.W, (f.V8 + minlen - 1) / minlen + 1));
+  return f;
+}
+int scan_flat_slots(int64_t M, int64_t V_local) { return flat_split(M, V_local).S; }
+cudaError_t launch_target_scan_flat(const VerifyLaunch& p, int* nlists, cudaStream_t s) {
+  const FlatSplit f = flat_split(p.M, p.V_local);
+  *nlists = f.S;
+  if (scan_flat_ctas() == 2)
+    k_target_scan_flat<2><<<(f.W + 7) / 8, 256, 0, s>>>(p, f);
+  else
+    k_target_scan_flat<kScanFlatCtas><<<(f.W + 7) / 8, 256, 0, s>>>(p, f);
   count_launch();
   return cudaGetLastError();
 }

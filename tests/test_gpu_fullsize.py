@@ -173,18 +173,68 @@ def _adversarial_rows(V, seed):
     return np.stack(rows)
 
 
-@pytest.mark.parametrize("ring", [0, 1])
+SCAN_MODES = {"flat": (1, 0), "seg": (0, 0), "ring": (0, 1)}   # (scan_flat, scan_ring)
+
+
+def _with_scan_mode(mode, fn, *a):
+    saved = [A.aurora_get_option("scan_flat"), A.aurora_get_option("scan_ring")]
+    A.aurora_set_option("scan_flat", SCAN_MODES[mode][0])
+    A.aurora_set_option("scan_ring", SCAN_MODES[mode][1])
+    try:
+        fn(*a)
+    finally:
+        A.aurora_set_option("scan_flat", saved[0])
+        A.aurora_set_option("scan_ring", saved[1])
+
+
+@pytest.mark.parametrize("mode", list(SCAN_MODES))
 @pytest.mark.parametrize("R,N", [(1, 1), (8, 7), (64, 6)])
-def test_scan_adversarial_rows_full_vocab(R, N, ring):
+def test_scan_adversarial_rows_full_vocab(R, N, mode):
     """Bit-exact argmax and top-10 set (k_accept = k_discard = 10 exposes the whole list)
     at V = 151,936 for three row counts (several segment counts per row), for the default
-    scan and the TMA-ring scan (option scan_ring)."""
-    saved = A.aurora_get_option("scan_ring")
-    A.aurora_set_option("scan_ring", ring)
-    try:
-        _scan_adversarial(R, N)
-    finally:
-        A.aurora_set_option("scan_ring", saved)
+    load-balanced scan (scan_flat), the (row, segment) scan and the TMA-ring scan."""
+    _with_scan_mode(mode, _scan_adversarial, R, N)
+
+
+def _flat_piece_bounds(M, V):
+    """Columns where the flat scan's warp ranges start inside each row (the split the library
+    documents for option scan_flat: W = min(3 * 148 * 8, NV / 64) equal ranges of the NV =
+    M * V / 8 row-major vectors, range g starting at vector g * NV // W)."""
+    V8 = V // 8
+    NV = M * V8
+    W = max(1, min(3 * 148 * 8, NV // 64))
+    out = [[] for _ in range(M)]
+    for g in range(1, W):
+        s = g * NV // W
+        r, c = divmod(s, V8)
+        if c:
+            out[r].append(8 * c)
+    return out
+
+
+@pytest.mark.parametrize("R,N", [(8, 7), (64, 6), (128, 6)])
+def test_scan_flat_range_boundaries(R, N):
+    """The load-balanced scan cuts rows at warp-range boundaries: exact maxima and 10th-place
+    ties straddling those cuts, maxima as the first / last column of a piece, bit-exact against
+    the oracle."""
+    V = 151936
+    M = R * (N + 1)
+    rng = np.random.default_rng(M + 1)
+    T32 = rng.normal(-5.0, 1.0, size=(M, V)).astype(np.float32)
+    cuts = _flat_piece_bounds(M, V)
+    for m in range(M):
+        for j, b in enumerate(cuts[m]):
+            kind = (m + j) % 4
+            if kind == 0:
+                T32[m, b - 1] = T32[m, b] = 3.0                  # tied maximum across the cut
+            elif kind == 1:
+                T32[m, rng.choice(V, 9, replace=False)] = 6.0    # 10th place tied across the cut
+                T32[m, max(0, b - 6):b + 6] = 2.5
+            elif kind == 2:
+                T32[m, b] = 4.0                                  # max = first column of a piece
+            else:
+                T32[m, b - 1] = 4.0                              # max = last column of a piece
+    _with_scan_mode("flat", _scan_check, R, N, T32)
 
 
 def _scan_adversarial(R, N):
@@ -192,7 +242,11 @@ def _scan_adversarial(R, N):
     M = R * (N + 1)
     rows = _adversarial_rows(V, seed=M)
     reps = (M + len(rows) - 1) // len(rows)
-    T32 = np.concatenate([rows] * reps)[:M]
+    _scan_check(R, N, np.concatenate([rows] * reps)[:M])
+
+
+def _scan_check(R, N, T32):
+    M, V = T32.shape
     Tb = _bits(T32)
     T64 = oracle.bf16_bits_to_f64(Tb)
     am, topk, nf = oracle.target_scan(T64, 10)
