@@ -261,9 +261,11 @@ uint64_t aurora_launch_count(void);
  *   "dw_resident"    0 (default): streamed pair tiles for dW; 1: with K = M <= 512 each CTA
  *                    pair keeps its dZ^T rows in shared memory across all column tiles
  *   "scan_ctas"      target-scan CTAs per SM (row segments) of the (row, segment) scan, default 2
- *   "scan_flat"      1 (default): load-balanced scan, the batch's 16 B vectors cut into equal
- *                    contiguous ranges per warp (rows 16 B aligned, V_local % 8 == 0; else
- *                    the (row, segment) scan); 0: the (row, segment) scan
+ *   "scan_flat"      1 (default): load-balanced scan (the batch's 16 B vectors cut into equal
+ *                    contiguous ranges per warp; rows 16 B aligned, V_local % 8 == 0) where the
+ *                    (row, segment) grid would leave a wave tail (>= 2 waves, last one under
+ *                    half full), else the (row, segment) scan; 2: always the load-balanced
+ *                    scan (when aligned); 0: always the (row, segment) scan
  *   "dz_chunk_bytes" budget of the bwd's bf16 dZ^T chunk (default 16 GiB: the whole local
  *                    vocabulary at the bench shapes; smaller -> more chunks).  Options that
  *                    change workspace sizes must be set before aurora_workspace_size.

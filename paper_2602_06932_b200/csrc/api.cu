@@ -102,7 +102,8 @@ struct Options {
   int tree_fwd_tc = 2;                         // F4 fwd when G*(N+1) <= 128: 2 (default) = one-pass tcgen05
                                                // kernel, two work items per SM; 3 = one item, deep rings;
                                                // 1 = two-pass tcgen05; 0 = mma.sync
-  int tree_bwd_tc = 0;                         // F4 bwd: 1 = tcgen05 kernel when G*(N+1) <= 128
+  int tree_bwd_tc = 1;                         // F4 bwd when G*(N+1) <= 128: 1 (default) = tcgen05 kernel,
+                                               // 0 = mma.sync fused kernel
   int tree_bwd_split = 0;                      // F4 bwd: 1 = separate dQ / dK-dV kernels even when the
                                                // fused one applies (A/B and coverage of the general path)
   int dw_resident = 0;                         // dW with K = M <= 512: A-resident pair sweep (measured
@@ -117,7 +118,7 @@ struct Options {
   Options() {
     if (const char* e = getenv("AURORA_FWD_STAGE")) fwd_stage = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_RING")) scan_ring = atoi(e) ? 1 : 0;
-    if (const char* e = getenv("AURORA_SCAN_FLAT")) scan_flat = atoi(e) ? 1 : 0;
+    if (const char* e = getenv("AURORA_SCAN_FLAT")) scan_flat = std::min(2, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_DW_ADAMW_QE")) dw_adamw_qe = std::min(2, std::max(0, atoi(e)));
     if (const char* e = getenv("AURORA_DW_RESIDENT")) dw_resident = atoi(e) ? 1 : 0;
     if (const char* e = getenv("AURORA_SCAN_CTAS")) scan_ctas = std::max(1, atoi(e));
@@ -595,7 +596,7 @@ aurora_status_t aurora_set_option(const char* name, int64_t value) {
     o.debug_gemm_group = static_cast<int>(value);
     return AURORA_OK;
   }
-  if (std::strcmp(name, "scan_flat") == 0 && (value == 0 || value == 1)) {
+  if (std::strcmp(name, "scan_flat") == 0 && value >= 0 && value <= 2) {
     o.scan_flat = static_cast<int>(value);
     return AURORA_OK;
   }
@@ -761,7 +762,13 @@ aurora_status_t aurora_verify_labels(const aurora_trace_t* t, const aurora_loss_
     p.nseg = scan_nseg(M, t->V_local);
     p.seg_len = rup(cdiv(t->V_local, p.nseg), 8);
   }
-  const bool flat = !ring && opts().scan_flat && scan_flat_ok(p);
+  // The flat scan removes the (row, segment) grid's wave tail; where that grid is a single partial
+  // wave or its last wave is mostly full, the per-row CTAs (one shared floor and warm start per
+  // row) are faster (measured: qwen3 M = 1792, 4.04 waves: flat 0.147 vs 0.166 ms; llama M = 384,
+  // 0.86 waves: 0.057 vs 0.043 ms).  scan_flat = 2 forces the flat scan.
+  const double seg_waves = static_cast<double>(M) * p.nseg / (3.0 * kNumSMs);
+  const bool flat_pays = opts().scan_flat == 2 || (seg_waves >= 2.0 && seg_waves - std::floor(seg_waves) < 0.5);
+  const bool flat = !ring && opts().scan_flat && flat_pays && scan_flat_ok(p);
   int nlists = ring ? p.nseg * scan_ring_lists() : p.nseg;
   p.draft = t->draft_tokens;
   p.parents = t->parents;

@@ -1815,14 +1815,32 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
         uint16_t* gdv = tree ? p.dVt : p.dVp;
         uint16_t* gdk = tree ? p.dKt : p.dKp;
         const int64_t key0 = tree ? (int64_t)r * N1 : (int64_t)p0 + jj * kT2NK;
+        // transpose through the P / dS buffer of tile jj (free: kv_full covers every MMA that read
+        // it): [key][dh] bf16 rows of 256 B, then 16 B coalesced stores of whole key rows
+        const int b = static_cast<int>((sc - 1) & 1);
+        uint8_t* sdv = smem + kTbOffP + b * 16384;
+        uint8_t* sdk = smem + kTbOffDS + b * 16384;
+        const uint32_t adv = smem_u32(sdv) + i * 2, adk = smem_u32(sdk) + i * 2;
 #pragma unroll
         for (int t = 0; t < kT2NK; ++t) {  // unrolled: register-indexed dv / dk
+          const uint16_t hv = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dv[t >> 5][t & 31])));
+          const uint16_t hk2 = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dk[t >> 5][t & 31])));
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(adv + t * 256), "h"(hv) : "memory");
+          asm volatile("st.shared.b16 [%0], %1;" ::"r"(adk + t * 256), "h"(hk2) : "memory");
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const int tid = (warp - 2) * 32 + lane;
+        const int part = tid & 15;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = (tid >> 4) + 8 * u;
           if (t < nkeys) {
-            const int64_t o = ((key0 + t) * p.Hkv + hk) * D + i;
-            gdv[o] = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dv[t >> 5][t & 31])));
-            gdk[o] = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dk[t >> 5][t & 31])));
+            const int64_t o = ((key0 + t) * p.Hkv + hk) * D + part * 8;
+            *reinterpret_cast<uint4*>(gdv + o) = *reinterpret_cast<const uint4*>(sdv + t * 256 + part * 16);
+            *reinterpret_cast<uint4*>(gdk + o) = *reinterpret_cast<const uint4*>(sdk + t * 256 + part * 16);
           }
         }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the buffer takes the next P / dS
       };
       (void)nn;
       for (int j = 0; j < nt; ++j, ++sc) {

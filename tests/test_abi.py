@@ -102,7 +102,7 @@ def test_options_validate_host_side(L):
     for name, good, bad in [("gemm_pair", (0, 1, 2), (3, -1)), ("bwd_mode", (0, 1), (2,)),
                             ("bwd_concurrent", (0, 1), (2,)), ("tile_n", (0, 256, 224, 192), (128, 200, 512)),
                             ("dz_chunk_bytes", (1 << 20, 1 << 31), (0, -5)), ("scan_ctas", (1, 2, 16), (0, 17)),
-                            ("dw_resident", (0, 1), (2,)), ("scan_flat", (0, 1), (2,))]:
+                            ("dw_resident", (0, 1), (2,)), ("scan_flat", (0, 1, 2), (3,))]:
         saved = A.aurora_get_option(name)
         try:
             for v in good:

@@ -173,7 +173,7 @@ def _adversarial_rows(V, seed):
     return np.stack(rows)
 
 
-SCAN_MODES = {"flat": (1, 0), "seg": (0, 0), "ring": (0, 1)}   # (scan_flat, scan_ring)
+SCAN_MODES = {"flat": (2, 0), "seg": (0, 0), "ring": (0, 1)}   # (scan_flat, scan_ring)
 
 
 def _with_scan_mode(mode, fn, *a):

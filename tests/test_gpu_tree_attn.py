@@ -81,25 +81,40 @@ def _compare(got, ref, reqs_got, off_got, reqs_ref_off=None):
             assert _rel(a, ref[name]) <= 2e-2, (name, _rel(a, ref[name]))
 
 
-@pytest.mark.parametrize("tc,split", [(3, 0), (2, 0), (1, 0), (0, 1), (0, 0)],
-                         ids=["tc3_fwd+fused_bwd", "tc2_fwd+fused_bwd",
-                              "tc_fwd+fused_bwd", "sync_fwd+split_bwd", "sync_fwd+fused_bwd"])
+# (forward kernel, backward kernel): tree_fwd_tc 2 = one-pass tcgen05, two items per SM (default),
+# 3 = one item per SM with deep rings, 1 = two-pass tcgen05, 0 = mma.sync; backward "tc" = tcgen05
+# (default), "fused" = mma.sync one-kernel, "split" = the general dQ + dK/dV kernels (used when
+# G*(N+1) > 128)
+KERNELS = {"tc2_fwd+tc_bwd": (2, "tc"), "tc3_fwd+tc_bwd": (3, "tc"), "tc_fwd+fused_bwd": (1, "fused"),
+           "sync_fwd+split_bwd": (0, "split"), "sync_fwd+fused_bwd": (0, "fused"), "sync_fwd+tc_bwd": (0, "tc")}
+
+
+class _kernels:
+    """Context: select the forward / backward kernels through the library options."""
+
+    def __init__(self, fwd_tc, bwd):
+        self.fwd_tc, self.bwd = fwd_tc, bwd
+
+    def __enter__(self):
+        from paper_2602_06932_b200 import aurora as A
+        self.A = A
+        self.saved = [A.aurora_get_option(k) for k in ("tree_fwd_tc", "tree_bwd_tc", "tree_bwd_split")]
+        A.aurora_set_option("tree_fwd_tc", self.fwd_tc)
+        A.aurora_set_option("tree_bwd_tc", 1 if self.bwd == "tc" else 0)
+        A.aurora_set_option("tree_bwd_split", 1 if self.bwd == "split" else 0)
+
+    def __exit__(self, *exc):
+        for k, v in zip(("tree_fwd_tc", "tree_bwd_tc", "tree_bwd_split"), self.saved):
+            self.A.aurora_set_option(k, v)
+
+
+@pytest.mark.parametrize("kern", list(KERNELS))
 @pytest.mark.parametrize("name", ["ta_small", "ta_chain", "ta_gqa8"])
-def test_tree_attention_parity(name, tc, split):
-    """tc=3 / tc=2: the one-pass tcgen05 forward (online softmax, lazy O rescale in TMEM) with
-    deep K/V rings (one item per SM) / two items per SM; tc=4 / 5: two items per SM with P kept
-    in TMEM (the P V MMA reads A from TMEM; K ring 3 / 2 deep), tc=1: the two-pass tcgen05 forward, tc=0: the mma.sync forward; split=0: the one-kernel backward (all rows of
-    a kv head in one CTA); split=1: the general dQ + dK/dV kernels (used when G*(N+1) > 128)."""
-    from paper_2602_06932_b200 import aurora as A
+def test_tree_attention_parity(name, kern):
+    """Every forward x backward kernel pair against the f64 oracle (O, lse, dQ, dK, dV)."""
     inp = tracegen.gen_tree_attn(name)
-    saved = A.aurora_get_option("tree_fwd_tc")
-    A.aurora_set_option("tree_bwd_split", split)
-    A.aurora_set_option("tree_fwd_tc", tc)
-    try:
+    with _kernels(*KERNELS[kern]):
         got = _run(inp)
-    finally:
-        A.aurora_set_option("tree_bwd_split", 0)
-        A.aurora_set_option("tree_fwd_tc", saved)
     ref = TA.fwd_bwd(inp)
     R = len(inp["requests"])
     _compare(got, ref, np.arange(R), inp["prefix_off"])
@@ -120,19 +135,14 @@ def test_tree_attention_deterministic():
         assert torch.equal(a[k], b[k]), k
 
 
-@pytest.mark.parametrize("tc", [0, 2, 3])
+@pytest.mark.parametrize("kern", ["tc2_fwd+tc_bwd", "tc3_fwd+tc_bwd", "sync_fwd+fused_bwd"])
 @pytest.mark.parametrize("name,sample", [("ta_llama", [0, 37, 63]), ("ta_tree", [0, 511, 1023])])
-def test_tree_attention_full_size_sampled(name, sample, tc):
-    """Full BASELINE sizes in the bench's launch configuration (both forwards); the oracle
-    recomputes a sample of requests (each request is independent, so the sample is exact)."""
-    from paper_2602_06932_b200 import aurora as A
+def test_tree_attention_full_size_sampled(name, sample, kern):
+    """Full BASELINE sizes in the bench's launch configuration; the oracle recomputes a sample of
+    requests (each request is independent, so the sample is exact)."""
     inp = tracegen.gen_tree_attn(name)
-    saved = A.aurora_get_option("tree_fwd_tc")
-    A.aurora_set_option("tree_fwd_tc", tc)
-    try:
+    with _kernels(*KERNELS[kern]):
         got = _run(inp)
-    finally:
-        A.aurora_set_option("tree_fwd_tc", saved)
     ref = TA.fwd_bwd(tracegen.gen_tree_attn(name, requests=sample))
     _compare(got, ref, np.asarray(sample), inp["prefix_off"])
     # every prefix gradient row of the whole batch was written (no NaN sentinel left)
@@ -240,39 +250,3 @@ def test_malformed_prefix_offsets_flag_range_without_oob():
     assert torch.isfinite(O.float()).all() and torch.isfinite(dQ).all()
     for g in (dKp_all, dVp_all):
         assert bool((g[:guard].float() == 7.0).all()) and bool((g[guard + total:].float() == 7.0).all())
-
-
-@pytest.mark.parametrize("fwd_tc", [0, 3])
-@pytest.mark.parametrize("name", ["ta_small", "ta_chain", "ta_gqa8"])
-def test_tree_attention_tcgen05_backward(name, fwd_tc):
-    """The tcgen05 backward (option tree_bwd_tc: S / dP / dV^T / dK^T / dQ on the tensor cores,
-    TMEM accumulators, TMA-fed tiles) after either forward, against the f64 oracle."""
-    from paper_2602_06932_b200 import aurora as A
-    inp = tracegen.gen_tree_attn(name)
-    saved = (A.aurora_get_option("tree_fwd_tc"), A.aurora_get_option("tree_bwd_tc"))
-    A.aurora_set_option("tree_fwd_tc", fwd_tc)
-    A.aurora_set_option("tree_bwd_tc", 1)
-    try:
-        got = _run(inp)
-    finally:
-        A.aurora_set_option("tree_fwd_tc", saved[0])
-        A.aurora_set_option("tree_bwd_tc", saved[1])
-    ref = TA.fwd_bwd(inp)
-    _compare(got, ref, np.arange(len(inp["requests"])), inp["prefix_off"])
-
-
-@pytest.mark.parametrize("name,sample", [("ta_llama", [0, 37, 63]), ("ta_tree", [0, 511, 1023])])
-def test_tree_attention_tcgen05_full_size_sampled(name, sample):
-    from paper_2602_06932_b200 import aurora as A
-    inp = tracegen.gen_tree_attn(name)
-    saved = (A.aurora_get_option("tree_fwd_tc"), A.aurora_get_option("tree_bwd_tc"))
-    A.aurora_set_option("tree_fwd_tc", 3)
-    A.aurora_set_option("tree_bwd_tc", 1)
-    try:
-        got = _run(inp)
-    finally:
-        A.aurora_set_option("tree_fwd_tc", saved[0])
-        A.aurora_set_option("tree_bwd_tc", saved[1])
-    ref = TA.fwd_bwd(tracegen.gen_tree_attn(name, requests=sample))
-    _compare(got, ref, np.asarray(sample), inp["prefix_off"])
-    assert not torch.isnan(got["dKp"]).any() and not torch.isnan(got["dVp"]).any()
