@@ -1586,46 +1586,49 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
 struct TaBwdMaps {
   CUtensorMap Q, dO, Kp, Vp, Kt, Vt;
 };
+constexpr int kTbKST = 3, kTbVST = 3;              // K / V ring depths
 constexpr int kTbOffQ = 0, kTbOffDO = 32768, kTbOffK = 65536;
-constexpr int kTbOffV = kTbOffK + 2 * kT2Slot;
-constexpr int kTbOffP = kTbOffV + 2 * kT2Slot;     // 2 x [128 rows x 64 keys] bf16
+constexpr int kTbOffV = kTbOffK + kTbKST * kT2Slot;
+constexpr int kTbOffP = kTbOffV + kTbVST * kT2Slot;  // 2 x [128 rows x 64 keys] bf16
 constexpr int kTbOffDS = kTbOffP + 2 * 16384;
-constexpr int kTbOffBar = kTbOffDS + 2 * 16384;    // 192 KB
+constexpr int kTbOffBar = kTbOffDS + 2 * 16384;    // 224 KB
 constexpr size_t kSmemTb = kTbOffBar + 1024 + 1024;
 
-__global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ TaBwdMaps maps, TaParams p) {
+constexpr int kTbCompute = 256;                    // compute threads (8 warps)
+__global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_constant__ TaBwdMaps maps, TaParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTbOffBar);
   uint64_t* q_full = bars + 0;
   uint64_t* q_free = bars + 1;
-  uint64_t* k_full = bars + 2;    // [2]
-  uint64_t* k_empty = bars + 4;   // [2]
-  uint64_t* v_full = bars + 6;    // [2]
-  uint64_t* v_empty = bars + 8;   // [2]
-  uint64_t* s_full = bars + 10;   // [2] S and dP of a tile in TMEM
-  uint64_t* s_free = bars + 12;   // [2]
-  uint64_t* pd_full = bars + 14;  // [2] P and dS of a tile in smem
-  uint64_t* pd_free = bars + 16;  // [2]
-  uint64_t* kv_full = bars + 18;  // dV^T, dK^T of a tile in TMEM
-  uint64_t* kv_free = bars + 19;
-  uint64_t* dq_done = bars + 20;
-  uint64_t* dq_free = bars + 21;
+  uint64_t* k_full = bars + 2;    // [3]
+  uint64_t* k_empty = bars + 5;   // [3]
+  uint64_t* v_full = bars + 8;    // [3]
+  uint64_t* v_empty = bars + 11;  // [3]
+  uint64_t* s_full = bars + 14;   // [2] S and dP of a tile in TMEM
+  uint64_t* s_free = bars + 16;   // [2]
+  uint64_t* pd_full = bars + 18;  // [2] P and dS of a tile in smem
+  uint64_t* pd_free = bars + 20;  // [2]
+  uint64_t* kv_full = bars + 22;  // dV^T, dK^T of a tile in TMEM
+  uint64_t* kv_free = bars + 23;
+  uint64_t* dq_done = bars + 24;
+  uint64_t* dq_free = bars + 25;
+  static_assert(kTbKST == 3 && kTbVST == 3, "barrier layout");
   uint64_t* anc = bars + 32;      // [40]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 80);
   int32_t* par_s = reinterpret_cast<int32_t*>(bars + 88);  // the request's parents (N <= 32)
   const int G = p.G, N1 = p.N1;
   const int nwork = p.R * p.Hkv;
   if (threadIdx.x == 0) {
-    for (int k = 0; k < 12; ++k) mbar_init(&bars[k], 1);
-    for (int k = 12; k < 14; ++k) mbar_init(&bars[k], 128);  // s_free
-    for (int k = 14; k < 16; ++k) mbar_init(&bars[k], 128);  // pd_full
-    for (int k = 16; k < 18; ++k) mbar_init(&bars[k], 1);    // pd_free
+    for (int k = 0; k < 16; ++k) mbar_init(&bars[k], 1);            // q, k / v rings, s_full
+    for (int k = 16; k < 18; ++k) mbar_init(&bars[k], kTbCompute);  // s_free
+    for (int k = 18; k < 20; ++k) mbar_init(&bars[k], kTbCompute);  // pd_full
+    for (int k = 20; k < 22; ++k) mbar_init(&bars[k], 1);           // pd_free
     mbar_init(kv_full, 1);
-    mbar_init(kv_free, 128);
+    mbar_init(kv_free, kTbCompute);
     mbar_init(dq_done, 1);
-    mbar_init(dq_free, 128);
+    mbar_init(dq_free, kTbCompute);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_holder);
@@ -1670,14 +1673,14 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
           const CUtensorMap* mk = j < npt ? &maps.Kp : &maps.Kt;
           const CUtensorMap* mv = j < npt ? &maps.Vp : &maps.Vt;
           const int z = j < npt ? p0 + j * kT2NK : r * N1;
-          const uint32_t ks = kc & 1, vs = vc & 1;
-          if (kc >= 2) mbar_wait_sleep(&k_empty[ks], ((kc >> 1) & 1) ^ 1);
+          const uint32_t ks = kc % kTbKST, vs = vc % kTbVST;
+          if (kc >= kTbKST) mbar_wait_sleep(&k_empty[ks], ((kc / kTbKST) & 1) ^ 1);
           mbar_arrive_expect_tx(&k_full[ks], kT2Slot);
           uint8_t* kd = smem + kTbOffK + ks * kT2Slot;
           tma_load_3d(mk, &k_full[ks], kd, 0, hk, z);
           tma_load_3d(mk, &k_full[ks], kd + kT2NK * 128, 64, hk, z);
           ++kc;
-          if (vc >= 2) mbar_wait_sleep(&v_empty[vs], ((vc >> 1) & 1) ^ 1);
+          if (vc >= kTbVST) mbar_wait_sleep(&v_empty[vs], ((vc / kTbVST) & 1) ^ 1);
           mbar_arrive_expect_tx(&v_full[vs], kT2Slot);
           uint8_t* vd = smem + kTbOffV + vs * kT2Slot;
           tma_load_3d(mv, &v_full[vs], vd, 0, hk, z);
@@ -1725,9 +1728,9 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
           ++gc;
         };
         for (int j = 0; j < nt; ++j) {
-          const uint32_t ks = kc & 1, vs = vc & 1, sb = sc & 1;
-          mbar_wait(&k_full[ks], (kc >> 1) & 1);
-          mbar_wait(&v_full[vs], (vc >> 1) & 1);
+          const uint32_t ks = kc % kTbKST, vs = vc % kTbVST, sb = sc & 1;
+          mbar_wait(&k_full[ks], (kc / kTbKST) & 1);
+          mbar_wait(&v_full[vs], (vc / kTbVST) & 1);
           if (sc >= 2) mbar_wait(&s_free[sb], ((sc >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t kb = smem_u32(smem + kTbOffK + ks * kT2Slot), vb = smem_u32(smem + kTbOffV + vs * kT2Slot);
@@ -1751,13 +1754,16 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
       }
     }
   } else {
-    // ---------------------------------------------------------------- compute (4 warps)
+    // ---------------------------------------------------------------- compute (8 warps)
+    // two warps per TMEM lane quadrant: warp half hf owns key columns [32 hf, 32 hf + 32) of S / dP
+    // and of dV^T / dK^T, and dQ columns [64 hf, 64 hf + 64)
     const int q4 = warp & 3;
+    const int hf = (warp - 2) >> 2;
     const int i = q4 * 32 + lane;  // row (softmax) or dh lane (dK / dV epilogue)
     const int rows = G * N1;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
     const float c2 = p.c2, scale = p.scale;
-    const int st_id = (warp - 2) * 32 + lane;
+    const int st_id = (warp - 2) * 32 + lane;  // 0 .. 255
     uint32_t sc = 0, gc = 0;
     int wi = 0;
     for (int w = blockIdx.x; w < nwork; w += gridDim.x, ++wi) {
@@ -1767,7 +1773,7 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
       const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
       {  // ancestor masks: parents loaded in parallel into shared memory, walked there
         if (st_id < p.N) par_s[st_id] = p.parents ? p.parents[(size_t)r * p.N + st_id] : st_id - 1;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");
         if (st_id < N1) {
           const int s = st_id;
           const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
@@ -1791,21 +1797,18 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
           anc[s] = bad ? 0ull : m;
         }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");
       const int s_row = i / G, g = i - s_row * G;
       const uint64_t a = i < rows ? anc[s_row] : 0ull;
       const size_t rix = ((size_t)r * N1 + s_row) * p.Hq + hk * G + g;
       const float lse2 = (a != 0ull) ? p.lse[rix] * kLog2e : 0.f;
       const float Di = (a != 0ull) ? p.Dsum[rix] : 0.f;
-      const int nn = p.num_nodes ? p.num_nodes[r] : p.N;
       auto epilogue = [&](int jj) {  // dV^T / dK^T of tile jj -> global (thread = dh lane i)
         mbar_wait(kv_full, gc & 1);
         tc_fence_after();
-        uint32_t dv[2][32], dk[2][32];
-        tmem_ld_32x32b_x32(trow + 384, dv[0]);
-        tmem_ld_32x32b_x32(trow + 384 + 32, dv[1]);
-        tmem_ld_32x32b_x32(trow + 448, dk[0]);
-        tmem_ld_32x32b_x32(trow + 448 + 32, dk[1]);
+        uint32_t dv[32], dk[32];
+        tmem_ld_32x32b_x32(trow + 384 + hf * 32, dv);
+        tmem_ld_32x32b_x32(trow + 448 + hf * 32, dk);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(kv_free);
@@ -1817,43 +1820,45 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
         const int64_t key0 = tree ? (int64_t)r * N1 : (int64_t)p0 + jj * kT2NK;
         // transpose through the P / dS buffer of tile jj (free: kv_full covers every MMA that read
         // it): [key][dh] bf16 rows of 256 B, then 16 B coalesced stores of whole key rows
-        const int b = static_cast<int>((sc - 1) & 1);
-        uint8_t* sdv = smem + kTbOffP + b * 16384;
-        uint8_t* sdk = smem + kTbOffDS + b * 16384;
-        const uint32_t adv = smem_u32(sdv) + i * 2, adk = smem_u32(sdk) + i * 2;
+        const uint32_t b = (sc - 1) & 1;
+        const uint32_t sdv = smem_u32(smem + kTbOffP) + b * 16384, sdk = smem_u32(smem + kTbOffDS) + b * 16384;
+        const uint32_t adv = sdv + (hf * 32) * 256 + i * 2, adk = sdk + (hf * 32) * 256 + i * 2;
 #pragma unroll
-        for (int t = 0; t < kT2NK; ++t) {  // unrolled: register-indexed dv / dk
-          const uint16_t hv = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dv[t >> 5][t & 31])));
-          const uint16_t hk2 = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dk[t >> 5][t & 31])));
+        for (int t = 0; t < 32; ++t) {  // unrolled: register-indexed dv / dk
+          const uint16_t hv = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dv[t])));
+          const uint16_t hk2 = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dk[t])));
           asm volatile("st.shared.b16 [%0], %1;" ::"r"(adv + t * 256), "h"(hv) : "memory");
           asm volatile("st.shared.b16 [%0], %1;" ::"r"(adk + t * 256), "h"(hk2) : "memory");
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const int tid = (warp - 2) * 32 + lane;
-        const int part = tid & 15;
+        asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");
+        const int part = st_id & 15;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int t = (tid >> 4) + 8 * u;
+        for (int u = 0; u < kT2NK * 16 / kTbCompute; ++u) {
+          const int t = (st_id >> 4) + (kTbCompute / 16) * u;
           if (t < nkeys) {
             const int64_t o = ((key0 + t) * p.Hkv + hk) * D + part * 8;
-            *reinterpret_cast<uint4*>(gdv + o) = *reinterpret_cast<const uint4*>(sdv + t * 256 + part * 16);
-            *reinterpret_cast<uint4*>(gdk + o) = *reinterpret_cast<const uint4*>(sdk + t * 256 + part * 16);
+            uint4 v4, k4;
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v4.x), "=r"(v4.y), "=r"(v4.z), "=r"(v4.w)
+                         : "r"(sdv + t * 256 + part * 16));
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(k4.x), "=r"(k4.y), "=r"(k4.z), "=r"(k4.w)
+                         : "r"(sdk + t * 256 + part * 16));
+            *reinterpret_cast<uint4*>(gdv + o) = v4;
+            *reinterpret_cast<uint4*>(gdk + o) = k4;
           }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the buffer takes the next P / dS
+        asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");  // the buffer takes the next P / dS
       };
-      (void)nn;
       for (int j = 0; j < nt; ++j, ++sc) {
         const uint32_t sb = sc & 1;
         const bool tree = j == npt;
         const int lim = tree ? 0 : Pr - j * kT2NK;
         mbar_wait(&s_full[sb], (sc >> 1) & 1);
         tc_fence_after();
-        uint32_t sv[2][32], dp[2][32];
-        tmem_ld_32x32b_x32(trow + sb * kT2NK, sv[0]);
-        tmem_ld_32x32b_x32(trow + sb * kT2NK + 32, sv[1]);
-        tmem_ld_32x32b_x32(trow + 128 + sb * kT2NK, dp[0]);
-        tmem_ld_32x32b_x32(trow + 128 + sb * kT2NK + 32, dp[1]);
+        float x[32], dpv[32];
+        tmem_ld_32x32b_x32(trow + sb * kT2NK + hf * 32, reinterpret_cast<uint32_t(&)[32]>(x));
+        tmem_ld_32x32b_x32(trow + 128 + sb * kT2NK + hf * 32, reinterpret_cast<uint32_t(&)[32]>(dpv));
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&s_free[sb]);
@@ -1862,30 +1867,27 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
         // wholly inside the prefix needs no mask at all (warp-uniform fast path)
         uint64_t vis = tree ? a : (a == 0ull ? 0ull : (lim >= kT2NK ? ~0ull : ((1ull << max(lim, 0)) - 1ull)));
         if (i >= rows) vis = ~0ull;
-        const bool wfull = __all_sync(0xffffffffu, vis == ~0ull);
-        float* x = reinterpret_cast<float*>(sv);
-        float* dpv = reinterpret_cast<float*>(dp);
-        uint32_t pw[32], dw[32];
+        const uint32_t vv = hf ? static_cast<uint32_t>(vis >> 32) : static_cast<uint32_t>(vis);
+        const bool wfull = __all_sync(0xffffffffu, vv == 0xFFFFFFFFu);
+        uint32_t pw[16], dw[16];
         const float nl = -lse2;
         if (wfull) {
 #pragma unroll
-          for (int h = 0; h < 32; ++h) {
-            const float p0 = ex2_approx(fmaf(x[2 * h], c2, nl)), p1 = ex2_approx(fmaf(x[2 * h + 1], c2, nl));
-            pw[h] = pk_bf16(p0, p1);
-            dw[h] = pk_bf16(scale * p0 * (dpv[2 * h] - Di), scale * p1 * (dpv[2 * h + 1] - Di));
+          for (int h = 0; h < 16; ++h) {
+            const float e0 = ex2_approx(fmaf(x[2 * h], c2, nl)), e1 = ex2_approx(fmaf(x[2 * h + 1], c2, nl));
+            pw[h] = pk_bf16(e0, e1);
+            dw[h] = pk_bf16(scale * e0 * (dpv[2 * h] - Di), scale * e1 * (dpv[2 * h + 1] - Di));
           }
         } else {
-          const uint32_t vlo = static_cast<uint32_t>(vis), vhi = static_cast<uint32_t>(vis >> 32);
 #pragma unroll
-          for (int h = 0; h < 32; ++h) {
-            const uint32_t vv = h < 16 ? vlo : vhi;
-            const bool ok0 = (vv >> ((2 * h) & 31)) & 1u, ok1 = (vv >> ((2 * h + 1) & 31)) & 1u;
-            const float p0 = ok0 ? ex2_approx(fmaf(x[2 * h], c2, nl)) : 0.f;
-            const float p1 = ok1 ? ex2_approx(fmaf(x[2 * h + 1], c2, nl)) : 0.f;
+          for (int h = 0; h < 16; ++h) {
+            const bool ok0 = (vv >> (2 * h)) & 1u, ok1 = (vv >> (2 * h + 1)) & 1u;
+            const float e0 = ok0 ? ex2_approx(fmaf(x[2 * h], c2, nl)) : 0.f;
+            const float e1 = ok1 ? ex2_approx(fmaf(x[2 * h + 1], c2, nl)) : 0.f;
             // never 0 * NaN from masked keys
-            const float d0 = ok0 ? scale * p0 * (dpv[2 * h] - Di) : 0.f;
-            const float d1 = ok1 ? scale * p1 * (dpv[2 * h + 1] - Di) : 0.f;
-            pw[h] = pk_bf16(p0, p1);
+            const float d0 = ok0 ? scale * e0 * (dpv[2 * h] - Di) : 0.f;
+            const float d1 = ok1 ? scale * e1 * (dpv[2 * h + 1] - Di) : 0.f;
+            pw[h] = pk_bf16(e0, e1);
             dw[h] = pk_bf16(d0, d1);
           }
         }
@@ -1894,13 +1896,13 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
         const uint32_t prow = smem_u32(smem + kTbOffP + pb * 16384) + i * 128;
         const uint32_t drow = smem_u32(smem + kTbOffDS + pb * 16384) + i * 128;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t ch = static_cast<uint32_t>(c ^ (i & 7));
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(pw[4 * c]),
-                       "r"(pw[4 * c + 1]), "r"(pw[4 * c + 2]), "r"(pw[4 * c + 3])
+        for (int cc = 0; cc < 4; ++cc) {
+          const uint32_t ch = static_cast<uint32_t>((hf * 4 + cc) ^ (i & 7));
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(pw[4 * cc]),
+                       "r"(pw[4 * cc + 1]), "r"(pw[4 * cc + 2]), "r"(pw[4 * cc + 3])
                        : "memory");
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(drow + ch * 16), "r"(dw[4 * c]),
-                       "r"(dw[4 * c + 1]), "r"(dw[4 * c + 2]), "r"(dw[4 * c + 3])
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(drow + ch * 16), "r"(dw[4 * cc]),
+                       "r"(dw[4 * cc + 1]), "r"(dw[4 * cc + 2]), "r"(dw[4 * cc + 3])
                        : "memory");
         }
         fence_proxy_async_smem();
@@ -1909,20 +1911,20 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
         if (j >= 1) epilogue(j - 1);
       }
       epilogue(nt - 1);
-      // dQ (thread = row): fp32 [row][dh]
+      // dQ (thread = row, this warp's 64 of the 128 columns): fp32 [row][dh]
       mbar_wait(dq_done, wi & 1);
       tc_fence_after();
-      uint32_t dq[4][32];
+      uint32_t dq[2][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(trow + 256 + c * 32, dq[c]);
+      for (int c = 0; c < 2; ++c) tmem_ld_32x32b_x32(trow + 256 + hf * 64 + c * 32, dq[c]);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_free);
       if (i < rows) {
-        float* out = p.dQ + rix * D;
+        float* out = p.dQ + rix * D + hf * 64;
         const bool live = a != 0ull;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 2; ++c)
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(out + c * 32 + q * 4) =
@@ -1930,7 +1932,7 @@ __global__ void __launch_bounds__(192, 1) k_ta_bwd_tc(const __grid_constant__ Ta
                                    __uint_as_float(dq[c][4 * q + 2]), __uint_as_float(dq[c][4 * q + 3]))
                      : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // anc is rewritten by the next item
+      asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");  // anc is rewritten by the next item
     }
   }
   __syncthreads();
@@ -2188,7 +2190,7 @@ extern "C" aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, co
     const int work = p.R * p.Hkv;
     prof_begin(PH_TREE_BWD_FUSED, s);
     k_ta_dsum<<<(unsigned)((n_rows + 7) / 8), 256, 0, s>>>(p.O, p.dO, (float*)ws, n_rows);
-    k_ta_bwd_tc<<<std::min(work, kNumSMs), 192, kSmemTb, s>>>(maps, p);
+    k_ta_bwd_tc<<<std::min(work, kNumSMs), 64 + kTbCompute, kSmemTb, s>>>(maps, p);
     prof_end(PH_TREE_BWD_FUSED, s);
     count_launch(2);
     return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
