@@ -306,7 +306,7 @@ struct FlatSplit {
 // maximum published (a lower bound for the row's k-th best), so the warps' lists stay short.
 // Returns this lane's running maximum of |bits| (non-finite test at the end).
 __device__ __forceinline__ uint32_t scan_piece(WarpList& L, const uint4* __restrict__ rowv, int64_t v0, int64_t v1,
-                                               int* slot, uint4* stash) {
+                                               int* slot, uint4* stash, float f0, bool own_warm) {
   constexpr int U = 8;  // 16 B loads in flight per lane
   const int lane = threadIdx.x & 31;
   uint32_t amax = 0;
@@ -314,18 +314,20 @@ __device__ __forceinline__ uint32_t scan_piece(WarpList& L, const uint4* __restr
     amax = __vmaxu2(amax, __vmaxu2(__vmaxu2(w.x & 0x7FFF7FFFu, w.y & 0x7FFF7FFFu),
                                    __vmaxu2(w.z & 0x7FFF7FFFu, w.w & 0x7FFF7FFFu)));
   };
-  float floor;
+  float floor = f0;
   {
-    // warm start without offers: the k-th largest of the 32 lane maxima of the first batch
-    // (distinct elements) bounds the piece's k-th best element from below; the batch itself is
-    // scanned again (from L2) by the main loop
-    float lm = -INFINITY;
+    // warm start without offers (unless the caller has a floor): the k-th largest of the 32 lane
+    // maxima of the first batch (distinct elements) bounds the piece's k-th best element from
+    // below; the batch itself is scanned again (from L2) by the main loop
+    if (own_warm) {
+      float lm = -INFINITY;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t vi = v0 + u * 32 + lane;
-      if (vi < v1) lm = fmaxf(lm, max8(ld_nc_v4(rowv + vi)));
+      for (int u = 0; u < U; ++u) {
+        const int64_t vi = v0 + u * 32 + lane;
+        if (vi < v1) lm = fmaxf(lm, max8(ld_nc_v4(rowv + vi)));
+      }
+      floor = fmaxf(floor, warp_kth_largest(lm, L.k));
     }
-    floor = warp_kth_largest(lm, L.k);
     if (slot) {
       if (lane == 0) atomicMax(slot, f2ord(floor));
       floor = fmaxf(floor, ord2f(*reinterpret_cast<volatile int*>(slot)));
@@ -336,21 +338,23 @@ __device__ __forceinline__ uint32_t scan_piece(WarpList& L, const uint4* __restr
     uint4 w[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) w[u] = ld_nc_v4(rowv + base + u * 32 + lane);
-    bool any = false;
+    uint32_t hm = 0;  // this lane's vectors whose max reaches the admission threshold
     const float f = fmaxf(floor, L.thr_v);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       absmax(w[u]);
-      any |= max8(w[u]) >= f;
+      hm |= (max8(w[u]) >= f ? 1u : 0u) << u;
     }
-    if (__any_sync(0xffffffffu, any)) {
+    const uint32_t wm = __reduce_or_sync(0xffffffffu, hm);
+    if (wm) {
       // rare path, kept rolled (one copy of the offer code): the batch goes through this warp's
-      // shared-memory stash so the vectors can be indexed at run time
+      // shared-memory stash so the hit vectors can be indexed at run time
 #pragma unroll
       for (int u = 0; u < U; ++u) stash[u * 32 + lane] = w[u];
       __syncwarp();
 #pragma unroll 1
-      for (int u = 0; u < U; ++u) {
+      for (uint32_t mm = wm; mm; mm &= mm - 1) {
+        const int u = __ffs(mm) - 1;
         const uint4 wu = stash[u * 32 + lane];
         const bool h = max8(wu) >= fmaxf(floor, L.thr_v);
         if (__any_sync(0xffffffffu, h)) offer_vectors(L, h, wu, (base + u * 32 + lane) * 8, floor);
@@ -385,14 +389,63 @@ __global__ void __launch_bounds__(256, kCtas) k_target_scan_flat(VerifyLaunch p,
   const int lane = threadIdx.x & 31;
   const int64_t g0 = static_cast<int64_t>(blockIdx.x) * 8;
   const int64_t row0 = fs.start(g0 < fs.W ? g0 : fs.W - 1) / fs.V8;
+  __shared__ float s_lm[8][32];
+  __shared__ int64_t s_row[8];
   if (threadIdx.x < kSlots) s_floor[threadIdx.x] = f2ord(-INFINITY);
-  __syncthreads();
-  const int64_t g = g0 + (threadIdx.x >> 5);
-  if (g >= fs.W) return;
+  const int warp = threadIdx.x >> 5;
+  const int64_t g = g0 + warp;
   const int k = p.k_max;
-  int64_t a = fs.start(g);
-  const int64_t b = fs.start(g + 1);
+  int64_t a = g < fs.W ? fs.start(g) : 0;
+  const int64_t b = g < fs.W ? fs.start(g + 1) : 0;
+  // CTA-wide warm start of every warp's first piece: the 32 lane maxima of each warp's first batch
+  // go to shared memory; each warp takes the k-th largest of those of the warps on its row (256
+  // distinct elements of the row at most): a much tighter first floor than one warp's 32
+  float f0 = -INFINITY;
+  {
+    constexpr int U = 8;
+    float lm = -INFINITY;
+    int64_t row = -1;
+    if (a < b) {
+      row = a / fs.V8;
+      const int64_t rs = row * fs.V8, re = min(b, rs + fs.V8);
+      const uint4* rowv = reinterpret_cast<const uint4*>(p.T + row * p.ldT);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t vi = a - rs + u * 32 + lane;
+        if (vi < re - rs) lm = fmaxf(lm, max8(ld_nc_v4(rowv + vi)));
+      }
+    }
+    s_lm[warp][lane] = lm;
+    if (lane == 0) s_row[warp] = row;
+    __syncthreads();
+    if (row >= 0) {
+      float v8[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v8[j] = s_row[j] == row ? s_lm[j][lane] : -INFINITY;
+      for (int r = 0; r < k; ++r) {
+        float m = v8[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) m = fmaxf(m, v8[j]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        if (r == k - 1) f0 = m;
+        const uint32_t has = __ballot_sync(0xffffffffu, v8[0] == m || v8[1] == m || v8[2] == m || v8[3] == m ||
+                                                            v8[4] == m || v8[5] == m || v8[6] == m || v8[7] == m);
+        if (lane == __ffs(has) - 1) {
+          bool done = false;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const bool hit = !done && v8[j] == m;
+            v8[j] = hit ? -INFINITY : v8[j];
+            done = done || hit;
+          }
+        }
+      }
+    }
+  }
+  if (g >= fs.W) return;
   uint32_t amax = 0;
+  bool first = true;
   while (a < b) {
     const int64_t row = a / fs.V8;
     const int64_t rs = row * fs.V8;
@@ -401,7 +454,8 @@ __global__ void __launch_bounds__(256, kCtas) k_target_scan_flat(VerifyLaunch p,
     L.init(k);
     const uint4* rowv = reinterpret_cast<const uint4*>(p.T + row * p.ldT);
     int* slot = row - row0 < kSlots ? &s_floor[row - row0] : nullptr;
-    amax = __vmaxu2(amax, scan_piece(L, rowv, a - rs, re - rs, slot, s_stash[threadIdx.x >> 5]));
+    amax = __vmaxu2(amax, scan_piece(L, rowv, a - rs, re - rs, slot, s_stash[warp], first ? f0 : -INFINITY, !first));
+    first = false;
     const int64_t sl0 = g - fs.warp_of(rs);
     float* cv = p.cand_val + row * fs.S * k;
     int32_t* ci = p.cand_idx + row * fs.S * k;
@@ -522,13 +576,48 @@ __global__ void __launch_bounds__(32 * kRingWarps, 1) k_target_scan_ring(VerifyL
 }
 
 // --------------------------------------------------------------------------- A2 merge
-// warp per row: merge `nlists` (<= 32) sorted lists of length k -> top list + argmax.
+// warp per row: merge `nlists` sorted lists of length k -> top list + argmax.  Up to 32 lists: a
+// k-way merge, lane l holding the head of list l; each of the k steps picks the best head by
+// (value desc, index asc) with a warp reduction and advances that list (k steps of ~20
+// instructions instead of nlists * k list insertions).  The lists hold distinct indices.
 __global__ void __launch_bounds__(256) k_topk_merge(VerifyLaunch p, const float* in_val, const int32_t* in_idx,
                                                     int nlists, int64_t row_stride, int64_t list_stride) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= p.M) return;
   const int k = p.k_max;
+  if (nlists <= 32) {
+    const int64_t base = static_cast<int64_t>(row) * row_stride + lane * list_stride;
+    int pos = 0;
+    float hv = -INFINITY;
+    int32_t hi = INT32_MAX;
+    if (lane < nlists) { hv = in_val[base]; hi = in_idx[base]; }
+    float ov = -INFINITY;
+    int32_t oi = INT32_MAX;
+    for (int r = 0; r < k; ++r) {
+      float bv = hv;
+      int32_t bi = hi;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int32_t i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (better(v2, i2, bv, bi)) { bv = v2; bi = i2; }
+      }
+      if (lane == r) { ov = bv; oi = bi; }
+      if (hv == bv && hi == bi && lane < nlists) {  // this lane's list supplied the winner: advance
+        ++pos;
+        if (pos < k) { hv = in_val[base + pos]; hi = in_idx[base + pos]; }
+        else { hv = -INFINITY; hi = INT32_MAX; }
+      }
+    }
+    if (lane < k) {
+      p.top_val[static_cast<int64_t>(row) * k + lane] = ov;
+      p.top_idx[static_cast<int64_t>(row) * k + lane] = oi;
+    }
+    const int32_t am = __shfl_sync(0xffffffffu, oi, 0);
+    if (lane == 0) p.lab.target_argmax[row] = am;
+    return;
+  }
   WarpList F;
   F.init(k);
   for (int l = 0; l < nlists; ++l) {
