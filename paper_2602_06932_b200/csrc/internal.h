@@ -184,7 +184,7 @@ int scan_ring_lists();
 cudaError_t launch_target_scan_ring(const VerifyLaunch& p, cudaStream_t s);
 // load-balanced flat scan (scan_flat_ok): equal contiguous vector ranges per warp, `*nlists`
 // (= scan_flat_slots) lists per row in cand_val / cand_idx
-constexpr int kScanFlatCtas = 3;
+constexpr int kScanFlatCtas = 2;
 bool scan_flat_ok(const VerifyLaunch& p);
 int scan_flat_slots(int64_t M, int64_t V_local);
 cudaError_t launch_target_scan_flat(const VerifyLaunch& p, int* nlists, cudaStream_t s);

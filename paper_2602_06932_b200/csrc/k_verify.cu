@@ -307,7 +307,7 @@ struct FlatSplit {
 // Returns this lane's running maximum of |bits| (non-finite test at the end).
 __device__ __forceinline__ uint32_t scan_piece(WarpList& L, const uint4* __restrict__ rowv, int64_t v0, int64_t v1,
                                                int* slot, uint4* stash, float f0, bool own_warm) {
-  constexpr int U = 8;  // 16 B loads in flight per lane
+  constexpr int U = 8;  // 16 B loads per lane per batch (two batches in flight)
   const int lane = threadIdx.x & 31;
   uint32_t amax = 0;
   auto absmax = [&](const uint4& w) {
@@ -334,10 +334,19 @@ __device__ __forceinline__ uint32_t scan_piece(WarpList& L, const uint4* __restr
     }
   }
   int64_t base = v0;
-  for (; base + U * 32 <= v1; base += U * 32) {
-    uint4 w[U];
+  // full batches, software-pipelined: the next batch's loads are issued before this one is
+  // scanned (two batches in flight per warp while it works), the registers handed over at the end
+  uint4 w[U], nx[U];
+  if (base + U * 32 <= v1) {
 #pragma unroll
     for (int u = 0; u < U; ++u) w[u] = ld_nc_v4(rowv + base + u * 32 + lane);
+  }
+  for (; base + U * 32 <= v1; base += U * 32) {
+    const bool more = base + 2 * U * 32 <= v1;
+    if (more) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) nx[u] = ld_nc_v4(rowv + base + U * 32 + u * 32 + lane);
+    }
     uint32_t hm = 0;  // this lane's vectors whose max reaches the admission threshold
     const float f = fmaxf(floor, L.thr_v);
 #pragma unroll
@@ -366,6 +375,10 @@ __device__ __forceinline__ uint32_t scan_piece(WarpList& L, const uint4* __restr
       }
     } else if (slot) {
       floor = fmaxf(floor, ord2f(*reinterpret_cast<volatile int*>(slot)));
+    }
+    if (more) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = nx[u];
     }
   }
   for (; base < v1; base += 32) {
@@ -1077,7 +1090,7 @@ bool scan_flat_ok(const VerifyLaunch& p) {
 int scan_flat_ctas() {
   static int c = [] {
     const char* e = getenv("AURORA_SCAN_FLAT_CTAS");
-    return (e && atoi(e) == 2) ? 2 : kScanFlatCtas;
+    return (e && atoi(e) == 3) ? 3 : kScanFlatCtas;
   }();
   return c;
 }
@@ -1095,8 +1108,8 @@ int scan_flat_slots(int64_t M, int64_t V_local) { return flat_split(M, V_local).
 cudaError_t launch_target_scan_flat(const VerifyLaunch& p, int* nlists, cudaStream_t s) {
   const FlatSplit f = flat_split(p.M, p.V_local);
   *nlists = f.S;
-  if (scan_flat_ctas() == 2)
-    k_target_scan_flat<2><<<(f.W + 7) / 8, 256, 0, s>>>(p, f);
+  if (scan_flat_ctas() == 3)
+    k_target_scan_flat<3><<<(f.W + 7) / 8, 256, 0, s>>>(p, f);
   else
     k_target_scan_flat<kScanFlatCtas><<<(f.W + 7) / 8, 256, 0, s>>>(p, f);
   count_launch();

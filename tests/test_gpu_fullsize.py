@@ -198,11 +198,11 @@ def test_scan_adversarial_rows_full_vocab(R, N, mode):
 
 def _flat_piece_bounds(M, V):
     """Columns where the flat scan's warp ranges start inside each row (the split the library
-    documents for option scan_flat: W = min(3 * 148 * 8, NV / 64) equal ranges of the NV =
+    documents for option scan_flat: W = min(2 * 148 * 8, NV / 64) equal ranges of the NV =
     M * V / 8 row-major vectors, range g starting at vector g * NV // W)."""
     V8 = V // 8
     NV = M * V8
-    W = max(1, min(3 * 148 * 8, NV // 64))
+    W = max(1, min(2 * 148 * 8, NV // 64))
     out = [[] for _ in range(M)]
     for g in range(1, W):
         s = g * NV // W
