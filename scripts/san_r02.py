@@ -94,15 +94,27 @@ def part_attn():
     nn = torch.from_numpy(inp["num_nodes"].astype(np.int32)).cuda()
     ta = A.TreeAttention(R, c.N, c.Hq, c.Hkv, c.dh, off, int(np.max(np.diff(inp["prefix_off"]))), parents=par,
                          num_nodes=nn)
-    A.aurora_set_option("tree_fwd_tc", 2)
+    A.aurora_set_option("tree_fwd_tc", 2)   # the defaults: one-pass tcgen05 fwd, tcgen05 bwd
+    A.aurora_set_option("tree_bwd_tc", 1)
     O = torch.empty_like(t["Q"])
     lse = torch.empty(R, N1, c.Hq, device="cuda")
     ta.forward(t["Q"], t["Kt"], t["Vt"], t["Kp"], t["Vp"], O, lse)
+    dQ = torch.empty(t["Q"].shape, dtype=torch.float32, device="cuda")
+    dKt, dVt, dKp, dVp = (torch.empty_like(t[k]) for k in ("Kt", "Vt", "Kp", "Vp"))
+    ta.backward(t["Q"], t["Kt"], t["Vt"], t["Kp"], t["Vp"], O, lse, t["dO"], dQ, dKt, dVt, dKp, dVp)
     torch.cuda.synchronize()
     assert int(ta.status.item()) == 0
 
 
-PARTS = dict(main=part_main, multirank=part_multirank, attn=part_attn)
+def part_scan():
+    """A2 load-balanced flat scan (forced) and the k-way merge."""
+    tr = tracegen.gen_trace("tiny")
+    A.aurora_set_option("scan_flat", 2)
+    spec(tr)
+    A.aurora_set_option("scan_flat", 1)
+
+
+PARTS = dict(main=part_main, multirank=part_multirank, attn=part_attn, scan=part_scan)
 if __name__ == "__main__":
     A.lib()
     for name in (sys.argv[1:] or list(PARTS)):

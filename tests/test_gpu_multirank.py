@@ -190,7 +190,8 @@ def test_f2_objectives_multirank(vp, dp):
     check_against_oracle(tr, run_spec_step(tr, vp, dp, **kw), vp, dp, ref)
 
 
-@pytest.mark.parametrize("opt", [dict(gemm_pair=1, tile_n=224), dict(dz_chunk_bytes=64 << 10)])
+@pytest.mark.parametrize("opt", [dict(gemm_pair=1, tile_n=224), dict(dz_chunk_bytes=64 << 10), dict(scan_flat=2),
+                                 dict(scan_flat=0)])
 def test_vocab_parallel_other_launch_configs(opt):
     saved = {k: A.aurora_get_option(k) for k in opt}
     try:
