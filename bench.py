@@ -811,6 +811,7 @@ def run_tree_attn(args):
     _, _, hbm, peak_src = _peaks()
     per = []
     for k, byts, flops in (("tree_attn_fwd", w["fwd_bytes"], w["fwd_flops"]),
+                           ("tree_attn_fwd_tc", w["fwd_bytes"], w["fwd_flops"]),
                            ("tree_attn_bwd_dq", w["dq_bytes"], 0.4 * w["bwd_flops"]),
                            ("tree_attn_bwd_dkdv", w["dkdv_bytes"], 0.6 * w["bwd_flops"]),
                            ("tree_attn_bwd_fused", w["fused_bytes"], w["bwd_flops"])):
