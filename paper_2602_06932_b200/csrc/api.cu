@@ -399,6 +399,16 @@ SideStreams* side_streams() {
   return &S;
 }
 bool serial_bwd() { return opts().bwd_concurrent == 0; }
+// the communicator's side stream and fork / join events, created on first use
+bool comm_side_ready(aurora_comm_t c) {
+  if (c->side) return true;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return false;
+  for (auto& e : c->side_ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return false;
+  c->side = st;
+  return true;
+}
 
 // The comm owns a device scratch for gathered per-row data; it grows on first use
 // (one cudaMalloc per size increase, never in steady state).
@@ -1019,6 +1029,12 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
   SideStreams* S = serial_bwd() ? nullptr : side_streams();
   cudaStream_t sW = S ? S->s[0] : s, sH = S ? S->s[1] : s;
   cudaEvent_t* ev = S ? S->ev : nullptr;  // [0] start, [1+3c] dz(c), [2+3c] dW(c), [3+3c] dH(c)
+  // Serial backward under VP: dH before dW in every chunk, and the C4 allreduce of dH on the
+  // comm's own side stream while the last chunk's dW GEMM runs (dW needs no communication)
+  // (not when a DP allreduce of dW follows on the main stream: two collectives of different
+  // communicators in flight at once could be ordered differently on different GPUs)
+  const bool dp_c5 = comm && comm->dp_x() && dWf && !(accumulate_dW & AURORA_BWD_NO_DP_REDUCE);
+  const bool c4_side = !S && comm && comm->vp_x() && !dp_c5 && dWf && comm_side_ready(comm);
   if (cudaMemsetAsync(w.counters, 0, kCounters * sizeof(int32_t), s) != cudaSuccess) return AURORA_ERR_CUDA;
   if (S) {
     if (cudaEventRecord(ev[0], s) != cudaSuccess) return AURORA_ERR_CUDA;
@@ -1086,6 +1102,50 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
       cudaStreamWaitEvent(sH, ev[1 + 3 * ch], 0);
     }
 
+    // A9: dH += dZ W[chunk]   (A = dZ^T as MN-major, B = W MN-major, K = vc)
+    GemmArgs h{};
+    const int ph = pair_for(M);
+    h.m_tiles = static_cast<int32_t>(cdiv(M, BM * ph));
+    h.n_tiles = static_cast<int32_t>(cdiv(d, BN));
+    h.kb_total = static_cast<int32_t>(cdiv(vc, BK));
+    h.splits = std::min<int>(dh_splits(M, d, h.kb_total, ph), w.splits);
+    h.kb_per_split = static_cast<int32_t>(cdiv(h.kb_total, h.splits));
+    h.splits = static_cast<int32_t>(cdiv(h.kb_total, h.kb_per_split));
+    h.M = M;
+    h.N = d;
+    h.ld_out = d;
+    h.tile_counter = w.counters + 3 * ch + 2;
+    if (h.splits > 1) {
+      h.out = w.dh_part;
+      h.split_stride = M * d;
+      h.accumulate = 0;
+    } else {
+      h.out = dH;
+      h.accumulate = ch > 0 ? 1 : 0;
+    }
+    CUtensorMap tmOH;
+    const bool oh = h.splits > 1 ? make_tmap_f32_out(&tmOH, w.dh_part, d, M, d, h.splits, M * d)
+                                 : make_tmap_f32_out(&tmOH, dH, d, M, d, 1, 0);
+    prof_begin(PH_BWD_DH, sH);
+    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, sH, oh ? &tmOH : nullptr, ph);
+    prof_end(PH_BWD_DH, sH);
+    if (e != cudaSuccess) return AURORA_ERR_CUDA;
+    if (h.splits > 1) {
+      prof_begin(PH_BWD_REDUCE, sH);
+      e = launch_splitk_reduce(w.dh_part, h.splits, M * d, dH, ch > 0 ? 1 : 0, sH);
+      prof_end(PH_BWD_REDUCE, sH);
+      if (e != cudaSuccess) return AURORA_ERR_CUDA;
+    }
+    if (S) cudaEventRecord(ev[3 + 3 * ch], sH);
+    if (c4_side && ch == nchunks - 1) {  // C4 on the comm's side stream, overlapped with the last dW
+      cudaEventRecord(comm->side_ev[0], s);
+      cudaStreamWaitEvent(comm->side, comm->side_ev[0], 0);
+      prof_begin(PH_COMM, comm->side);
+      if ((st = coll_allreduce(comm, G_VP, dH, dH, static_cast<size_t>(M * d), DT_F32, comm->side)) != AURORA_OK)
+        return st;
+      prof_end(PH_COMM, comm->side);
+      cudaEventRecord(comm->side_ev[1], comm->side);
+    }
     if (dWf) {
       // A8: dW[chunk] = dZ^T H   (A = dZ^T K-major, B = H MN-major, K = M)
       GemmArgs b{};
@@ -1123,47 +1183,14 @@ static aurora_status_t bwd_classic_impl(const void* H, const void* W, int64_t M,
       }
       if (S) cudaEventRecord(ev[2 + 3 * ch], sW);
     }
-    // A9: dH += dZ W[chunk]   (A = dZ^T as MN-major, B = W MN-major, K = vc)
-    GemmArgs h{};
-    const int ph = pair_for(M);
-    h.m_tiles = static_cast<int32_t>(cdiv(M, BM * ph));
-    h.n_tiles = static_cast<int32_t>(cdiv(d, BN));
-    h.kb_total = static_cast<int32_t>(cdiv(vc, BK));
-    h.splits = std::min<int>(dh_splits(M, d, h.kb_total, ph), w.splits);
-    h.kb_per_split = static_cast<int32_t>(cdiv(h.kb_total, h.splits));
-    h.splits = static_cast<int32_t>(cdiv(h.kb_total, h.kb_per_split));
-    h.M = M;
-    h.N = d;
-    h.ld_out = d;
-    h.tile_counter = w.counters + 3 * ch + 2;
-    if (h.splits > 1) {
-      h.out = w.dh_part;
-      h.split_stride = M * d;
-      h.accumulate = 0;
-    } else {
-      h.out = dH;
-      h.accumulate = ch > 0 ? 1 : 0;
-    }
-    CUtensorMap tmOH;
-    const bool oh = h.splits > 1 ? make_tmap_f32_out(&tmOH, w.dh_part, d, M, d, h.splits, M * d)
-                                 : make_tmap_f32_out(&tmOH, dH, d, M, d, 1, 0);
-    prof_begin(PH_BWD_DH, sH);
-    e = launch_umma_gemm(EPI_STORE_F32, true, true, tmZ_mn, tmW_mn, h, sH, oh ? &tmOH : nullptr, ph);
-    prof_end(PH_BWD_DH, sH);
-    if (e != cudaSuccess) return AURORA_ERR_CUDA;
-    if (h.splits > 1) {
-      prof_begin(PH_BWD_REDUCE, sH);
-      e = launch_splitk_reduce(w.dh_part, h.splits, M * d, dH, ch > 0 ? 1 : 0, sH);
-      prof_end(PH_BWD_REDUCE, sH);
-      if (e != cudaSuccess) return AURORA_ERR_CUDA;
-    }
-    if (S) cudaEventRecord(ev[3 + 3 * ch], sH);
   }
   if (S) {  // join
     cudaStreamWaitEvent(s, ev[2 + 3 * (nchunks - 1)], 0);
     cudaStreamWaitEvent(s, ev[3 + 3 * (nchunks - 1)], 0);
   }
-  if (comm && comm->vp_x()) {  // C4: VP dH allreduce
+  if (c4_side) {
+    cudaStreamWaitEvent(s, comm->side_ev[1], 0);
+  } else if (comm && comm->vp_x()) {  // C4: VP dH allreduce
     prof_begin(PH_COMM, s);
     if ((st = coll_allreduce(comm, G_VP, dH, dH, static_cast<size_t>(M * d), DT_F32, s)) != AURORA_OK)
       return st;

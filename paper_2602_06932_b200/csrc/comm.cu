@@ -284,6 +284,9 @@ aurora_status_t aurora_comm_destroy(aurora_comm_t c) {
     loop_group_release(c->ldp);
   }
   if (c->scratch) cudaFree(c->scratch);
+  for (auto& e : c->side_ev)
+    if (e) cudaEventDestroy(e);
+  if (c->side) cudaStreamDestroy(c->side);
   delete c;
   return AURORA_OK;
 }

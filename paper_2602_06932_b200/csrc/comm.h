@@ -52,6 +52,10 @@ struct aurora_comm_s {
   aur::LoopGroup* ldp = nullptr;  // loopback groups
   void* scratch = nullptr;        // comm-owned device scratch for gathered candidates / stats
   size_t scratch_bytes = 0;
+  // comm-owned side stream + fork / join events (created on first use on the calling device):
+  // the C4 dH allreduce runs there, overlapped with the last dW GEMM
+  cudaStream_t side = nullptr;
+  cudaEvent_t side_ev[2] = {nullptr, nullptr};
 };
 
 namespace aur {
