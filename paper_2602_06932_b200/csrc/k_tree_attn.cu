@@ -1586,7 +1586,8 @@ __global__ void __launch_bounds__(GRP * 192, 1) k_ta_fwd_tc2(const __grid_consta
 struct TaBwdMaps {
   CUtensorMap Q, dO, Kp, Vp, Kt, Vt;
 };
-constexpr int kTbKST = 3, kTbVST = 3;              // K / V ring depths
+constexpr int kTbKST = 4, kTbVST = 2;              // K / V ring depths (a K slot is held until the
+                                                   // tile's dQ MMA, a V slot only until its dP MMA)
 constexpr int kTbOffQ = 0, kTbOffDO = 32768, kTbOffK = 65536;
 constexpr int kTbOffV = kTbOffK + kTbKST * kT2Slot;
 constexpr int kTbOffP = kTbOffV + kTbVST * kT2Slot;  // 2 x [128 rows x 64 keys] bf16
@@ -1602,10 +1603,10 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTbOffBar);
   uint64_t* q_full = bars + 0;
   uint64_t* q_free = bars + 1;
-  uint64_t* k_full = bars + 2;    // [3]
-  uint64_t* k_empty = bars + 5;   // [3]
-  uint64_t* v_full = bars + 8;    // [3]
-  uint64_t* v_empty = bars + 11;  // [3]
+  uint64_t* k_full = bars + 2;               // [kTbKST]
+  uint64_t* k_empty = k_full + kTbKST;       // [kTbKST]
+  uint64_t* v_full = k_empty + kTbKST;       // [kTbVST]
+  uint64_t* v_empty = v_full + kTbVST;       // [kTbVST]
   uint64_t* s_full = bars + 14;   // [2] S and dP of a tile in TMEM
   uint64_t* s_free = bars + 16;   // [2]
   uint64_t* pd_full = bars + 18;  // [2] P and dS of a tile in smem
@@ -1614,7 +1615,7 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
   uint64_t* kv_free = bars + 23;
   uint64_t* dq_done = bars + 24;
   uint64_t* dq_free = bars + 25;
-  static_assert(kTbKST == 3 && kTbVST == 3, "barrier layout");
+  static_assert(2 * kTbKST + 2 * kTbVST == 12, "barrier layout: s_full starts at 14");
   uint64_t* anc = bars + 32;      // [40]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 80);
   int32_t* par_s = reinterpret_cast<int32_t*>(bars + 88);  // the request's parents (N <= 32)
