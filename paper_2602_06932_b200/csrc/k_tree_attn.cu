@@ -1595,7 +1595,23 @@ constexpr int kTbOffDS = kTbOffP + 2 * 16384;
 constexpr int kTbOffBar = kTbOffDS + 2 * 16384;    // 224 KB
 constexpr size_t kSmemTb = kTbOffBar + 1024 + 1024;
 
-constexpr int kTbCompute = 256;                    // compute threads (8 warps)
+#ifndef TA_BWD_KV_KSTEPS
+#define TA_BWD_KV_KSTEPS 8  // (experiments only: fewer K steps in the dV^T / dK^T MMAs)
+#endif
+#ifndef TA_BWD_CW
+#define TA_BWD_CW 16
+#endif
+constexpr int kTbCW = TA_BWD_CW;                    // compute warps (8 or 16: 2 or 4 per TMEM lane quadrant)
+constexpr int kTbCompute = 32 * kTbCW;             // compute threads
+constexpr int kTbSplit = kTbCW / 4;                // warps per lane quadrant
+constexpr int kTbCols = 64 / kTbSplit;             // key columns of S / dP / dV^T / dK^T per warp
+constexpr int kTbQCols = 128 / kTbSplit;           // dQ columns per warp
+static_assert(kTbCW == 8 || kTbCW == 16, "compute warps");
+template <int N>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[N]) {
+  if constexpr (N == 32) tmem_ld_32x32b_x32(taddr, r);
+  else tmem_ld_32x32b_x16(taddr, r);
+}
 __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_constant__ TaBwdMaps maps, TaParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1715,10 +1731,10 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
           const uint32_t aP = smem_u32(smem + kTbOffP + pb * 16384), aS = smem_u32(smem + kTbOffDS + pb * 16384);
           const uint32_t kb = smem_u32(smem + kTbOffK + kslot * kT2Slot);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)  // K = 128 rows
+          for (int kk = 0; kk < TA_BWD_KV_KSTEPS; ++kk)  // K = 128 rows
             umma_bf16(tmem + 384, mnmaj_desc(aDO, kk, 128), mnmaj_desc(aP, kk, 128), idT, kk > 0);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
+          for (int kk = 0; kk < TA_BWD_KV_KSTEPS; ++kk)
             umma_bf16(tmem + 448, mnmaj_desc(aQ, kk, 128), mnmaj_desc(aS, kk, 128), idT, kk > 0);
 #pragma unroll
           for (int kk = 0; kk < kT2NK / 16; ++kk)  // K = 64 keys
@@ -1755,9 +1771,9 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
       }
     }
   } else {
-    // ---------------------------------------------------------------- compute (8 warps)
-    // two warps per TMEM lane quadrant: warp half hf owns key columns [32 hf, 32 hf + 32) of S / dP
-    // and of dV^T / dK^T, and dQ columns [64 hf, 64 hf + 64)
+    // ---------------------------------------------------------------- compute (kTbCW warps)
+    // kTbSplit warps per TMEM lane quadrant: warp slice hf owns key columns [kTbCols hf, +kTbCols)
+    // of S / dP and of dV^T / dK^T, and dQ columns [kTbQCols hf, +kTbQCols)
     const int q4 = warp & 3;
     const int hf = (warp - 2) >> 2;
     const int i = q4 * 32 + lane;  // row (softmax) or dh lane (dK / dV epilogue)
@@ -1807,9 +1823,9 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
       auto epilogue = [&](int jj) {  // dV^T / dK^T of tile jj -> global (thread = dh lane i)
         mbar_wait(kv_full, gc & 1);
         tc_fence_after();
-        uint32_t dv[32], dk[32];
-        tmem_ld_32x32b_x32(trow + 384 + hf * 32, dv);
-        tmem_ld_32x32b_x32(trow + 448 + hf * 32, dk);
+        uint32_t dv[kTbCols], dk[kTbCols];
+        tmem_ld_cols(trow + 384 + hf * kTbCols, dv);
+        tmem_ld_cols(trow + 448 + hf * kTbCols, dk);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(kv_free);
@@ -1823,9 +1839,9 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
         // it): [key][dh] bf16 rows of 256 B, then 16 B coalesced stores of whole key rows
         const uint32_t b = (sc - 1) & 1;
         const uint32_t sdv = smem_u32(smem + kTbOffP) + b * 16384, sdk = smem_u32(smem + kTbOffDS) + b * 16384;
-        const uint32_t adv = sdv + (hf * 32) * 256 + i * 2, adk = sdk + (hf * 32) * 256 + i * 2;
+        const uint32_t adv = sdv + (hf * kTbCols) * 256 + i * 2, adk = sdk + (hf * kTbCols) * 256 + i * 2;
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {  // unrolled: register-indexed dv / dk
+        for (int t = 0; t < kTbCols; ++t) {  // unrolled: register-indexed dv / dk
           const uint16_t hv = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dv[t])));
           const uint16_t hk2 = __bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(dk[t])));
           asm volatile("st.shared.b16 [%0], %1;" ::"r"(adv + t * 256), "h"(hv) : "memory");
@@ -1845,8 +1861,12 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
             asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(k4.x), "=r"(k4.y), "=r"(k4.z), "=r"(k4.w)
                          : "r"(sdk + t * 256 + part * 16));
+#ifndef TA_BWD_NO_KV_STORE
             *reinterpret_cast<uint4*>(gdv + o) = v4;
             *reinterpret_cast<uint4*>(gdk + o) = k4;
+#else
+            if ((v4.x ^ k4.y) == 0x12345678u) gdv[o] = 0;  // experiments only: keep the loads alive
+#endif
           }
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");  // the buffer takes the next P / dS
@@ -1857,9 +1877,9 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
         const int lim = tree ? 0 : Pr - j * kT2NK;
         mbar_wait(&s_full[sb], (sc >> 1) & 1);
         tc_fence_after();
-        float x[32], dpv[32];
-        tmem_ld_32x32b_x32(trow + sb * kT2NK + hf * 32, reinterpret_cast<uint32_t(&)[32]>(x));
-        tmem_ld_32x32b_x32(trow + 128 + sb * kT2NK + hf * 32, reinterpret_cast<uint32_t(&)[32]>(dpv));
+        float x[kTbCols], dpv[kTbCols];
+        tmem_ld_cols(trow + sb * kT2NK + hf * kTbCols, reinterpret_cast<uint32_t(&)[kTbCols]>(x));
+        tmem_ld_cols(trow + 128 + sb * kT2NK + hf * kTbCols, reinterpret_cast<uint32_t(&)[kTbCols]>(dpv));
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&s_free[sb]);
@@ -1868,20 +1888,22 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
         // wholly inside the prefix needs no mask at all (warp-uniform fast path)
         uint64_t vis = tree ? a : (a == 0ull ? 0ull : (lim >= kT2NK ? ~0ull : ((1ull << max(lim, 0)) - 1ull)));
         if (i >= rows) vis = ~0ull;
-        const uint32_t vv = hf ? static_cast<uint32_t>(vis >> 32) : static_cast<uint32_t>(vis);
-        const bool wfull = __all_sync(0xffffffffu, vv == 0xFFFFFFFFu);
-        uint32_t pw[16], dw[16];
+        constexpr uint32_t kFullMask = kTbCols == 32 ? 0xFFFFFFFFu : ((1u << kTbCols) - 1u);
+        const uint32_t vv = static_cast<uint32_t>(vis >> (hf * kTbCols)) & kFullMask;
+        const bool wfull = __all_sync(0xffffffffu, vv == kFullMask);
+        uint32_t pw[kTbCols / 2], dw[kTbCols / 2];
         const float nl = -lse2;
+        const float sDi = -scale * Di;  // dS = P (scale dP - scale D)
         if (wfull) {
 #pragma unroll
-          for (int h = 0; h < 16; ++h) {
+          for (int h = 0; h < kTbCols / 2; ++h) {
             const float e0 = ex2_approx(fmaf(x[2 * h], c2, nl)), e1 = ex2_approx(fmaf(x[2 * h + 1], c2, nl));
             pw[h] = pk_bf16(e0, e1);
-            dw[h] = pk_bf16(scale * e0 * (dpv[2 * h] - Di), scale * e1 * (dpv[2 * h + 1] - Di));
+            dw[h] = pk_bf16(e0 * fmaf(dpv[2 * h], scale, sDi), e1 * fmaf(dpv[2 * h + 1], scale, sDi));
           }
         } else {
 #pragma unroll
-          for (int h = 0; h < 16; ++h) {
+          for (int h = 0; h < kTbCols / 2; ++h) {
             const bool ok0 = (vv >> (2 * h)) & 1u, ok1 = (vv >> (2 * h + 1)) & 1u;
             const float e0 = ok0 ? ex2_approx(fmaf(x[2 * h], c2, nl)) : 0.f;
             const float e1 = ok1 ? ex2_approx(fmaf(x[2 * h + 1], c2, nl)) : 0.f;
@@ -1897,8 +1919,8 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
         const uint32_t prow = smem_u32(smem + kTbOffP + pb * 16384) + i * 128;
         const uint32_t drow = smem_u32(smem + kTbOffDS + pb * 16384) + i * 128;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const uint32_t ch = static_cast<uint32_t>((hf * 4 + cc) ^ (i & 7));
+        for (int cc = 0; cc < kTbCols / 8; ++cc) {
+          const uint32_t ch = static_cast<uint32_t>((hf * (kTbCols / 8) + cc) ^ (i & 7));
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(prow + ch * 16), "r"(pw[4 * cc]),
                        "r"(pw[4 * cc + 1]), "r"(pw[4 * cc + 2]), "r"(pw[4 * cc + 3])
                        : "memory");
@@ -1915,17 +1937,17 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
       // dQ (thread = row, this warp's 64 of the 128 columns): fp32 [row][dh]
       mbar_wait(dq_done, wi & 1);
       tc_fence_after();
-      uint32_t dq[2][32];
+      uint32_t dq[kTbQCols / 32][32];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) tmem_ld_32x32b_x32(trow + 256 + hf * 64 + c * 32, dq[c]);
+      for (int c = 0; c < kTbQCols / 32; ++c) tmem_ld_32x32b_x32(trow + 256 + hf * kTbQCols + c * 32, dq[c]);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_free);
       if (i < rows) {
-        float* out = p.dQ + rix * D + hf * 64;
+        float* out = p.dQ + rix * D + hf * kTbQCols;
         const bool live = a != 0ull;
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < kTbQCols / 32; ++c)
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<float4*>(out + c * 32 + q * 4) =
