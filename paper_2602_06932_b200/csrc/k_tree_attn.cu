@@ -1598,6 +1598,9 @@ constexpr size_t kSmemTb = kTbOffBar + 1024 + 1024;
 #ifndef TA_BWD_KV_KSTEPS
 #define TA_BWD_KV_KSTEPS 8  // (experiments only: fewer K steps in the dV^T / dK^T MMAs)
 #endif
+#ifndef TA_BWD_DP_KSTEPS
+#define TA_BWD_DP_KSTEPS 8  // (experiments only: fewer K steps in the dP MMAs)
+#endif
 #ifndef TA_BWD_CW
 #define TA_BWD_CW 16
 #endif
@@ -1755,7 +1758,7 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
           for (int kk = 0; kk < 8; ++kk)
             umma_bf16(tmem + sb * kT2NK, kmaj_desc(aQ, kk, 128), kmaj_desc(kb, kk, kT2NK), idS, kk > 0);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
+          for (int kk = 0; kk < TA_BWD_DP_KSTEPS; ++kk)
             umma_bf16(tmem + 128 + sb * kT2NK, kmaj_desc(aDO, kk, 128), kmaj_desc(vb, kk, kT2NK), idS, kk > 0);
           umma_commit(&s_full[sb]);
           umma_commit(&v_empty[vs]);  // V: dP done
