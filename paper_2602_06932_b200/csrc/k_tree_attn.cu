@@ -1791,6 +1791,11 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
       int p0, Pr;
       prefix_of(p, r, p0, Pr, false);
       const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
+      const int s_row = i / G, g = i - s_row * G;
+      const size_t rix = ((size_t)r * N1 + s_row) * p.Hq + hk * G + g;
+      // this row's lse and D, loaded before the ancestor walk so their latency overlaps it
+      const float lse_raw = i < rows ? p.lse[rix] : 0.f;
+      const float D_raw = i < rows ? p.Dsum[rix] : 0.f;
       {  // ancestor masks: parents loaded in parallel into shared memory, walked there
         if (st_id < p.N) par_s[st_id] = p.parents ? p.parents[(size_t)r * p.N + st_id] : st_id - 1;
         asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");
@@ -1818,11 +1823,9 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
         }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");
-      const int s_row = i / G, g = i - s_row * G;
       const uint64_t a = i < rows ? anc[s_row] : 0ull;
-      const size_t rix = ((size_t)r * N1 + s_row) * p.Hq + hk * G + g;
-      const float lse2 = (a != 0ull) ? p.lse[rix] * kLog2e : 0.f;
-      const float Di = (a != 0ull) ? p.Dsum[rix] : 0.f;
+      const float lse2 = (a != 0ull) ? lse_raw * kLog2e : 0.f;
+      const float Di = (a != 0ull) ? D_raw : 0.f;
       auto epilogue = [&](int jj) {  // dV^T / dK^T of tile jj -> global (thread = dh lane i)
         mbar_wait(kv_full, gc & 1);
         tc_fence_after();
