@@ -5,7 +5,17 @@
 // Row s of request r (s = 0 root, s = n+1 draft node n) attends the P_r cached prefix
 // positions of its request and the tree rows of its ancestor closure (F4-R1..R5).
 //
-// Work decomposition (one launch per phase, no atomics, deterministic):
+// Default kernels when G (N+1) <= 128 (options tree_fwd_tc = 2, tree_bwd_tc = 1), tcgen05 / TMEM /
+// TMA, persistent, work item = (request, kv head) with all its query rows as one M = 128 tile:
+//   k_ta_fwd_tc2  two items in flight per SM (independent groups of TMA / MMA / 4 softmax warps),
+//                 one-pass online softmax with lazy O rescaling in TMEM, P through shared memory.
+//   k_ta_bwd_tc   one item per SM: S, dP, dV^T, dK^T, dQ MMAs from the TMA-loaded tiles into
+//                 TMEM, P / dS in shared memory, dK / dV transposed through shared memory into
+//                 whole 256 B key rows; 16 compute warps.
+// Both take a warp-uniform unmasked path for prefix tiles wholly inside the request's prefix.
+// The mma.sync kernels below are kept as options (and the split backward for G (N+1) > 128).
+//
+// mma.sync work decomposition (one launch per phase, no atomics, deterministic):
 //   k_ta_fwd    CTA = (request, kv head, query-head chunk): the G query heads of a kv head
 //               share every K/V tile they read (GQA), so a tile of 64 keys is loaded once for
 //               up to 128 query rows = (heads x tree rows); warp = 16 query rows; online
@@ -18,9 +28,7 @@
 //               row of the request that can see the tile (all G heads x N+1 rows, streamed in
 //               32-row chunks) is in the CTA, so dK/dV of a key are complete in one CTA and
 //               are written once as bf16 — the G-head GQA sum happens in registers.
-// Tensor cores: mma.sync m16n8k16 bf16 (fp32 accumulate) with ldmatrix from 128-B-XOR
-// swizzled shared tiles (conflict-free).  The tcgen05 (TMEM) version is the next step
-// (DESIGN.md §6): at these shapes the phase is close to HBM-bound on the prefix K/V.
+// mma.sync m16n8k16 bf16 (fp32 accumulate) with ldmatrix from 128-B-XOR swizzled shared tiles.
 #include <cmath>
 #include <initializer_list>
 #include <type_traits>
