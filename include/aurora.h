@@ -271,7 +271,15 @@ uint64_t aurora_launch_count(void);
  *                    change workspace sizes must be set before aurora_workspace_size.
  *   "tile_n"         fwd / dz vocab tile width with single-CTA tiles: 0 auto (default:
  *                    the width among 256/224/192 with the least per-SM work for the
- *                    tile count), or force 256, 224 or 192.  Other values: INVALID_ARG. */
+ *                    tile count), or force 256, 224 or 192.
+ *   "tree_fwd_tc"    tree-attention forward when (Hq/Hkv)*(N+1) <= 128: 2 (default) one-pass
+ *                    tcgen05 kernel, two work items per SM; 3 the same with one item and deeper
+ *                    K/V rings; 1 two-pass tcgen05 kernel; 0 the mma.sync kernel
+ *   "tree_bwd_tc"    tree-attention backward when (Hq/Hkv)*(N+1) <= 128: 1 (default) tcgen05
+ *                    one-kernel backward; 0 the mma.sync one-kernel backward
+ *   "tree_bwd_split" 1: the general dQ + dK/dV mma.sync kernels even where the one-kernel
+ *                    backward applies (always used when (Hq/Hkv)*(N+1) > 128)
+ *   Other values: INVALID_ARG. */
 aurora_status_t aurora_set_option(const char* name, int64_t value);
 int64_t aurora_get_option(const char* name);
 
