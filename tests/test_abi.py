@@ -102,7 +102,9 @@ def test_options_validate_host_side(L):
     for name, good, bad in [("gemm_pair", (0, 1, 2), (3, -1)), ("bwd_mode", (0, 1), (2,)),
                             ("bwd_concurrent", (0, 1), (2,)), ("tile_n", (0, 256, 224, 192), (128, 200, 512)),
                             ("dz_chunk_bytes", (1 << 20, 1 << 31), (0, -5)), ("scan_ctas", (1, 2, 16), (0, 17)),
-                            ("dw_resident", (0, 1), (2,)), ("scan_flat", (0, 1, 2), (3,))]:
+                            ("dw_resident", (0, 1), (2,)), ("scan_flat", (0, 1, 2), (3,)),
+                            ("tree_fwd_tc", (0, 1, 3, 2), (4, 5, -1)), ("tree_bwd_tc", (0, 1), (2,)),
+                            ("tree_bwd_split", (1, 0), (2,))]:
         saved = A.aurora_get_option(name)
         try:
             for v in good:
@@ -115,6 +117,22 @@ def test_options_validate_host_side(L):
         finally:
             A.aurora_set_option(name, saved)
     assert A.aurora_get_option("no_such_option") == -1
+
+
+def test_documented_option_defaults(L):
+    """The defaults aurora.h documents (read in a fresh process: options are process-wide and the
+    environment can override them): tcgen05 tree attention, load-balanced scan where it pays,
+    serial per-chunk backward, auto CTA pairs / tile width, 16 GiB dZ^T chunk budget."""
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if not k.startswith("AURORA_")}
+    code = ("from paper_2602_06932_b200 import aurora as A; A.lib(); print([A.aurora_get_option(n) for n in "
+            "('tree_fwd_tc', 'tree_bwd_tc', 'tree_bwd_split', 'scan_flat', 'bwd_mode', 'bwd_concurrent', "
+            "'gemm_pair', 'tile_n', 'dz_chunk_bytes', 'dw_resident')])")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == str([2, 1, 0, 1, 0, 0, 0, 0, 16 << 30, 0])
 
 
 def test_tree_attn_host_validation_without_gpu(L):
