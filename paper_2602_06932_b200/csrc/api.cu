@@ -175,7 +175,7 @@ int scan_nseg(int64_t M, int64_t V_local) {
 }
 // dLogits chunk width.  The bf16 dZ^T of the whole local vocabulary is M x V_local x 2 B
 // (Llama: 98 MB of the 180 GB HBM): keep it whole when it fits the chunk budget (option
-// "dz_chunk_bytes", default 2 GiB) so the bwd is one dz, one dW and one dH launch with no
+// "dz_chunk_bytes", default 16 GiB) so the bwd is one dz, one dW and one dH launch with no
 // per-chunk wave tails; otherwise the fewest equal chunks that fit (<= 20), rounded to 256.
 int64_t chunk_cols(int64_t V_local, int64_t M) {
   const int64_t per_col = rup(M, 8) * 2;
