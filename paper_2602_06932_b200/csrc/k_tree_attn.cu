@@ -67,6 +67,8 @@ struct TaParams {
 };
 
 __device__ __forceinline__ uint32_t swz(int row, int ch) { return row * ROWB + ((ch ^ (row & 7)) << 4); }
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 __device__ __forceinline__ void cp16(uint32_t s, const void* g, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(g), "r"(bytes) : "memory");
@@ -1801,9 +1803,15 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
       const int npt = (Pr + kT2NK - 1) / kT2NK, nt = npt + 1;
       const int s_row = i / G, g = i - s_row * G;
       const size_t rix = ((size_t)r * N1 + s_row) * p.Hq + hk * G + g;
-      // this row's lse and D, loaded before the ancestor walk so their latency overlaps it
+      // this row's lse and its slice of O, loaded before the ancestor walk so their latency
+      // overlaps it; D = rowsum(dO * O) is formed here from the dO tile the TMA brought in (no
+      // separate pass over O and dO)
       const float lse_raw = i < rows ? p.lse[rix] : 0.f;
-      const float D_raw = i < rows ? p.Dsum[rix] : 0.f;
+      uint4 o_sl[kTbQCols / 8];
+#pragma unroll
+      for (int c = 0; c < kTbQCols / 8; ++c)
+        o_sl[c] = i < rows ? *reinterpret_cast<const uint4*>(p.O + rix * D + hf * kTbQCols + c * 8)
+                           : make_uint4(0u, 0u, 0u, 0u);
       {  // ancestor masks: parents loaded in parallel into shared memory, walked there
         if (st_id < p.N) par_s[st_id] = p.parents ? p.parents[(size_t)r * p.N + st_id] : st_id - 1;
         asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");
@@ -1830,10 +1838,33 @@ __global__ void __launch_bounds__(64 + kTbCompute, 1) k_ta_bwd_tc(const __grid_c
           anc[s] = bad ? 0ull : m;
         }
       }
+      // D: this warp's kTbQCols columns of dO (row i of the swizzled K-major tile) times O, the
+      // kTbSplit partials summed in slice order through the free P buffer (deterministic)
+      mbar_wait(q_full, wi & 1);
+      {
+        float part = 0.f;
+        const uint32_t arow = smem_u32(smem + kTbOffDO) + (hf * kTbQCols / 64) * 16384 + i * 128;
+#pragma unroll
+        for (int c = 0; c < kTbQCols / 8; ++c) {
+          const uint32_t ch = static_cast<uint32_t>(((hf * kTbQCols % 64) / 8 + c) ^ (i & 7));
+          const float4 dv4 = lds128(arow + ch * 16);
+          const uint32_t dw4[4] = {__float_as_uint(dv4.x), __float_as_uint(dv4.y), __float_as_uint(dv4.z),
+                                   __float_as_uint(dv4.w)};
+          const uint32_t ow4[4] = {o_sl[c].x, o_sl[c].y, o_sl[c].z, o_sl[c].w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            part = fmaf(bf16_hi(dw4[q]), bf16_hi(ow4[q]), fmaf(bf16_lo(dw4[q]), bf16_lo(ow4[q]), part));
+        }
+        reinterpret_cast<float*>(smem + kTbOffP + (sc & 1) * 16384)[hf * 128 + i] = part;
+      }
       asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");
+      float D_row = 0.f;
+#pragma unroll
+      for (int h2 = 0; h2 < kTbSplit; ++h2) D_row += reinterpret_cast<const float*>(smem + kTbOffP + (sc & 1) * 16384)[h2 * 128 + i];
+      asm volatile("bar.sync 1, %0;" ::"n"(kTbCompute) : "memory");  // the buffer takes P / dS next
       const uint64_t a = i < rows ? anc[s_row] : 0ull;
       const float lse2 = (a != 0ull) ? lse_raw * kLog2e : 0.f;
-      const float Di = (a != 0ull) ? D_raw : 0.f;
+      const float Di = (a != 0ull) ? D_row : 0.f;
       auto epilogue = [&](int jj) {  // dV^T / dK^T of tile jj -> global (thread = dh lane i)
         mbar_wait(kv_full, gc & 1);
         tc_fence_after();
@@ -2226,10 +2257,9 @@ extern "C" aurora_status_t aurora_tree_attn_bwd(const aurora_tree_attn_t* ta, co
     }
     const int work = p.R * p.Hkv;
     prof_begin(PH_TREE_BWD_FUSED, s);
-    k_ta_dsum<<<(unsigned)((n_rows + 7) / 8), 256, 0, s>>>(p.O, p.dO, (float*)ws, n_rows);
-    k_ta_bwd_tc<<<std::min(work, kNumSMs), 64 + kTbCompute, kSmemTb, s>>>(maps, p);
+    k_ta_bwd_tc<<<std::min(work, kNumSMs), 64 + kTbCompute, kSmemTb, s>>>(maps, p);  // D formed in-kernel
     prof_end(PH_TREE_BWD_FUSED, s);
-    count_launch(2);
+    count_launch(1);
     return cudaGetLastError() == cudaSuccess ? AURORA_OK : AURORA_ERR_CUDA;
   }
   if (p.G * p.N1 <= 128 && !opt_tree_bwd_split()) {
