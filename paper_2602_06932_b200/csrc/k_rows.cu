@@ -231,22 +231,44 @@ __global__ void __launch_bounds__(256) k_dz_rescale(__nv_bfloat16* __restrict__ 
   }
   __syncthreads();
   if (c0 >= c1) return;
-  const int nv = static_cast<int>((m1 - m0) >> 3);  // 8-row vectors per dZ^T row (ld % 8 == 0)
-  const int64_t total = (c1 - c0) * nv;
-  for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
-    const int64_t c = c0 + i / nv;
-    const int vi = static_cast<int>(i % nv);
-    uint4* p = reinterpret_cast<uint4*>(dzT + c * ld + m0) + vi;
-    uint4 x = *p;
+  const int nv = static_cast<int>((m1 - m0) >> 3);  // 8-row vectors per dZ^T row (ld % 8 == 0), <= 128
+  // thread = one 8-row vector slot vi (its 8 factors in registers) of every cstep-th dZ^T row of
+  // the half tile (cstep = blockDim / nv); 4 rows per step in flight (no per-element index
+  // arithmetic)
+  if (nv <= 0) return;
+  const int vi = threadIdx.x % nv;
+  const int cs = threadIdx.x / nv, cstep = blockDim.x / nv;
+  if (cs >= cstep) return;
+  float fv[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) fv[e] = F[vi * 8 + e];
+  auto scale8 = [&](uint4& x) {
     uint32_t* w = &x.x;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&w[e]);
       const float2 f = __bfloat1622float2(b);
-      b = __floats2bfloat162_rn(f.x * F[vi * 8 + 2 * e], f.y * F[vi * 8 + 2 * e + 1]);
+      b = __floats2bfloat162_rn(f.x * fv[2 * e], f.y * fv[2 * e + 1]);
       w[e] = *reinterpret_cast<uint32_t*>(&b);
     }
-    *p = x;
+  };
+  uint4* base = reinterpret_cast<uint4*>(dzT + m0) + vi;
+  const int64_t ldv = ld / 8;  // uint4 per dZ^T row
+  int64_t c = c0 + cs;
+  for (; c + 3 * cstep < c1; c += 4 * cstep) {
+    uint4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = base[(c + u * cstep) * ldv];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      scale8(x[u]);
+      base[(c + u * cstep) * ldv] = x[u];
+    }
+  }
+  for (; c < c1; c += cstep) {
+    uint4 x = base[c * ldv];
+    scale8(x);
+    base[c * ldv] = x;
   }
 }
 
