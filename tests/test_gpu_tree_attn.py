@@ -250,3 +250,18 @@ def test_malformed_prefix_offsets_flag_range_without_oob():
     assert torch.isfinite(O.float()).all() and torch.isfinite(dQ).all()
     for g in (dKp_all, dVp_all):
         assert bool((g[:guard].float() == 7.0).all()) and bool((g[guard + total:].float() == 7.0).all())
+
+
+@pytest.mark.parametrize("kern", ["tc2_fwd+tc_bwd", "tc3_fwd+tc_bwd", "sync_fwd+fused_bwd"])
+@pytest.mark.parametrize("p_len", [0, 64, 128])
+def test_tree_attention_prefix_edge_lengths(kern, p_len):
+    """Every request's prefix empty (no Kp / Vp at all: the tensor maps fall back to the tree
+    keys) or exactly one / two full 64-key tiles (no partial prefix tile), against the oracle."""
+    cfg = tracegen.TreeAttnConfig(f"ta_edge{p_len}", R=5, N=9, Hq=16, Hkv=4, dh=128, p_min=p_len, p_max=p_len,
+                                  seed=3100 + p_len, tree=True, beam=3)
+    inp = tracegen.gen_tree_attn(cfg)
+    assert int(inp["prefix_off"][-1]) == 5 * p_len
+    with _kernels(*KERNELS[kern]):
+        got = _run(inp)
+    ref = TA.fwd_bwd(inp)
+    _compare(got, ref, np.arange(5), inp["prefix_off"])
