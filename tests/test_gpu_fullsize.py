@@ -245,18 +245,31 @@ def _scan_adversarial(R, N):
     _scan_check(R, N, np.concatenate([rows] * reps)[:M])
 
 
-def _scan_check(R, N, T32):
+def _scan_check(R, N, T32, k=10):
     M, V = T32.shape
     Tb = _bits(T32)
     T64 = oracle.bf16_bits_to_f64(Tb)
-    am, topk, nf = oracle.target_scan(T64, 10)
+    am, topk, nf = oracle.target_scan(T64, k)
     assert not nf
     draft = torch.zeros(R, N, dtype=torch.int32, device="cuda")
-    st = A.SpecTrainStep(R, N, 64, V, k_accept=10, k_discard=10)
+    st = A.SpecTrainStep(R, N, 64, V, k_accept=k, k_discard=k)
     st.verify(draft, _bf16(Tb))
     torch.cuda.synchronize()
     assert int(st.status.item()) == 0
     np.testing.assert_array_equal(st.target_argmax.cpu().numpy(), am)
     sup = st.sup_idx.cpu().numpy()
     for m in range(M):
-        np.testing.assert_array_equal(sup[m, :10], np.sort(topk[m]), err_msg=f"row {m}")
+        np.testing.assert_array_equal(sup[m, :k], np.sort(topk[m]), err_msg=f"row {m}")
+
+
+@pytest.mark.parametrize("mode", ["flat", "seg"])
+def test_scan_top16_full_vocab(mode):
+    """The largest dense list (k_accept = k_discard = 16 = AURORA_MAX_K): every row's top-16 set
+    and argmax bit-exact at V = 151,936, bf16-quantised N(0, 4) rows with a 40-way tie across the
+    16th place in some rows."""
+    R, N, V = 16, 6, 151936
+    rng = np.random.default_rng(32)
+    T32 = (rng.standard_normal((R * (N + 1), V)) * 2.0).astype(np.float32)
+    for m in range(0, R * (N + 1), 3):
+        T32[m, rng.choice(V, 40, replace=False)] = 9.0
+    _with_scan_mode(mode, _scan_check, R, N, T32, 16)
